@@ -1,0 +1,171 @@
+"""ctypes binding of ``lib/libadrom_b200.so`` (C-ABI: ``include/adrom_b200.h``).
+
+The product path has no CPU fallback: if the shared library is missing or
+no CUDA device is visible, every entry point raises ``RuntimeError``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from pathlib import Path
+
+import numpy as np
+
+from .errors import DenseError, RomStepError
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "lib" / "libadrom_b200.so"
+
+OK, ERR_NONFINITE, ERR_SINGULAR, ERR_ROMSTEP, ERR_ARG, ERR_CUDA, ERR_NOCONV, ERR_DENSE = range(8)
+BURGERS, SOD = 1, 2
+
+_p = C.c_void_p
+_i32, _i64, _f64 = C.c_int32, C.c_int64, C.c_double
+
+
+class Model(C.Structure):
+    """``adrom_model`` (include/adrom_b200.h)."""
+
+    _fields_ = [("kind", _i32), ("n_var", _i32), ("n_elem", _i64),
+                ("dx", _f64), ("nu", _f64), ("gamma", _f64)]
+
+
+class NewtonInfo(C.Structure):
+    _fields_ = [("converged", _i32), ("iterations", _i32), ("residual_norm", _f64)]
+
+
+class IsvdInfo(C.Structure):
+    _fields_ = [("qnorm", _f64), ("ynorm", _f64), ("proj_resid", _f64),
+                ("degenerate", _i32), ("reorthogonalised", _i32), ("sweeps", _i32), ("pad", _i32)]
+
+
+# name -> (restype, argtypes)
+SIGNATURES = {
+    "adrom_abi_version": (_i32, []),
+    "adrom_ctx_create": (_i32, [C.POINTER(_p), _p]),
+    "adrom_ctx_set_stream": (_i32, [_p, _p]),
+    "adrom_ctx_destroy": (None, [_p]),
+    "adrom_ctx_last_error": (C.c_char_p, [_p]),
+    "adrom_ctx_synchronize": (_i32, [_p]),
+    "adrom_rhs": (_i32, [_p, C.POINTER(Model), _p, _p]),
+    "adrom_rhs_at_cells": (_i32, [_p, C.POINTER(Model), _p, _i64, _p]),
+    "adrom_plan_evaluate": (_i32, [_p, C.POINTER(Model), _p, _i64, _p, _p, _i64, _p, _p, _p,
+                                   _i64, _i32, _p]),
+    "adrom_fd_jacobian_blocks": (_i32, [_p, C.POINTER(Model), _p, _p]),
+    "adrom_implicit_step": (_i32, [_p, C.POINTER(Model), _p, _f64, _f64, _i32, _p,
+                                   C.POINTER(NewtonInfo)]),
+    "adrom_project": (_i32, [_p, _p, _p, _i64, _i32, _p]),
+    "adrom_encode": (_i32, [_p, _p, _p, _p, _p, _i64, _i32, _p]),
+    "adrom_decode": (_i32, [_p, _p, _p, _p, _p, _i64, _i32, _p]),
+    "adrom_isvd_update": (_i32, [_p, _p, _p, _p, _i64, _i32, _i32, _f64, _p, _p,
+                                 C.POINTER(IsvdInfo)]),
+    "adrom_small_svd": (_i32, [_p, _p, _i32, _i32, _p, _p, _p]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load(path: str | os.PathLike | None = None) -> C.CDLL:
+    """Load the C-ABI library (fail loudly if it is absent)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        p = Path(path) if path else LIB_PATH
+        if not p.exists():
+            raise RuntimeError(
+                f"{p} is missing: build it with `python -m paper_2605_28684_b200._build` "
+                "(there is no CPU fallback)")
+        lib = C.CDLL(str(p))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name, None)
+            if fn is None:
+                continue
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def exported_symbols(path=None) -> set[str]:
+    """Names from SIGNATURES that the library exports (no GPU needed)."""
+    lib = C.CDLL(str(Path(path) if path else LIB_PATH))
+    return {n for n in SIGNATURES if hasattr(lib, n)}
+
+
+class Context:
+    """One ``adrom_ctx`` per (device, thread); rebinds to torch's current stream."""
+
+    _tls = threading.local()
+
+    def __init__(self):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2605_28684_b200 needs a CUDA device (no CPU fallback)")
+        self.lib = load()
+        handle = _p()
+        st = self.lib.adrom_ctx_create(C.byref(handle), _p(torch.cuda.current_stream().cuda_stream))
+        if st != OK:
+            raise RuntimeError(f"adrom_ctx_create failed with status {st}")
+        self.handle = handle
+        self._stream = None
+
+    @classmethod
+    def get(cls) -> "Context":
+        import torch
+        dev = torch.cuda.current_device()
+        table = getattr(cls._tls, "table", None)
+        if table is None:
+            table = cls._tls.table = {}
+        ctx = table.get(dev)
+        if ctx is None:
+            ctx = table[dev] = cls()
+        ctx.bind()
+        return ctx
+
+    def bind(self):
+        import torch
+        s = torch.cuda.current_stream().cuda_stream
+        if s != self._stream:
+            self.lib.adrom_ctx_set_stream(self.handle, _p(s))
+            self._stream = s
+
+    def error(self) -> str:
+        msg = self.lib.adrom_ctx_last_error(self.handle)
+        return msg.decode() if msg else ""
+
+    def check(self, status: int, what: str = ""):
+        if status == OK:
+            return
+        msg = self.error() or what
+        if status in (ERR_NONFINITE, ERR_SINGULAR, ERR_NOCONV, ERR_DENSE):
+            raise DenseError(msg)
+        if status == ERR_ROMSTEP:
+            raise RomStepError(msg)
+        if status == ERR_ARG:
+            raise ValueError(msg)
+        raise RuntimeError(f"CUDA failure in {what}: {msg}")
+
+    def call(self, name: str, *args):
+        self.check(getattr(self.lib, name)(self.handle, *args), name)
+
+    def sync(self):
+        self.call("adrom_ctx_synchronize")
+
+
+def ptr(t) -> _p:
+    """Device pointer of a torch tensor (None -> NULL)."""
+    if t is None:
+        return _p(0)
+    return _p(t.data_ptr())
+
+
+def model_struct(kind: int, n_var: int, n_elem: int, dx: float, nu: float, gamma: float) -> Model:
+    return Model(kind, n_var, n_elem, dx, nu, gamma)
+
+
+__all__ = ["Context", "load", "ptr", "Model", "NewtonInfo", "IsvdInfo", "SIGNATURES",
+           "exported_symbols", "np"]

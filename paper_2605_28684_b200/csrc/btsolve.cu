@@ -1,0 +1,482 @@
+// Partitioned block-tridiagonal solver for the backward-Euler Newton systems.
+//
+// The reference factors the dense N x N matrix I - dt J with LAPACK getrf
+// (dense.py:162).  That matrix is block tridiagonal (cyclic for the
+// periodic Burgers grid, open chain for Sod's clamped ghosts), so here it is
+// solved in O(N) with a recursive partition method:
+//
+//   level l: rows are cut into partitions of M rows.  Inside partition p
+//   the M-1 interior rows are eliminated (block Thomas, partial pivoting
+//   inside the nv x nv diagonal blocks) as affine functions of the two
+//   "interface" unknowns that bound them — X_{p-1} (last row of the left
+//   partition) and X_p (own last row):  x_i = y_i + V_i X_{p-1} + W_i X_p.
+//   Substituting into the interface rows gives a block-tridiagonal system
+//   of P = ceil(n/M) rows with the same cyclic structure; recurse until a
+//   single partition remains, then back-substitute level by level.
+//
+// Rounding differs from LU with row pivoting at the 1e-16 level; the Newton
+// iterate and iteration count are compared with the reference in
+// tests/test_gpu_fom.py.
+#include "btsolve.cuh"
+
+namespace adrom {
+
+constexpr int BT_M = 32;  // rows per partition
+
+template <int NV>
+struct Blk {
+  double a[NV][NV];
+};
+
+template <int NV>
+__device__ __forceinline__ void load_blk(const double* p, Blk<NV>& b) {
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+#pragma unroll
+    for (int j = 0; j < NV; ++j) b.a[i][j] = p[i * NV + j];
+}
+template <int NV>
+__device__ __forceinline__ void store_blk(double* p, const Blk<NV>& b) {
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+#pragma unroll
+    for (int j = 0; j < NV; ++j) p[i * NV + j] = b.a[i][j];
+}
+template <int NV>
+__device__ __forceinline__ void zero_blk(Blk<NV>& b) {
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+#pragma unroll
+    for (int j = 0; j < NV; ++j) b.a[i][j] = 0.0;
+}
+// c = a * b
+template <int NV>
+__device__ __forceinline__ void mm(const Blk<NV>& a, const Blk<NV>& b, Blk<NV>& c) {
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) s += a.a[i][k] * b.a[k][j];
+      c.a[i][j] = s;
+    }
+}
+// y = a * x
+template <int NV>
+__device__ __forceinline__ void mv(const Blk<NV>& a, const double* x, double* y) {
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) s += a.a[i][k] * x[k];
+    y[i] = s;
+  }
+}
+
+// in-place LU with partial pivoting of a small block; false on zero pivot
+template <int NV>
+__device__ __forceinline__ bool lu(Blk<NV>& A, int* piv) {
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    int p = k;
+    double best = fabs(A.a[k][k]);
+#pragma unroll
+    for (int i = k + 1; i < NV; ++i)
+      if (fabs(A.a[i][k]) > best) {
+        best = fabs(A.a[i][k]);
+        p = i;
+      }
+    piv[k] = p;
+    if (p != k) {
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        const double t = A.a[k][j];
+        A.a[k][j] = A.a[p][j];
+        A.a[p][j] = t;
+      }
+    }
+    const double d = A.a[k][k];
+    if (d == 0.0 || !isfinite(d)) ok = false;
+    const double inv = 1.0 / d;
+#pragma unroll
+    for (int i = k + 1; i < NV; ++i) {
+      A.a[i][k] *= inv;
+#pragma unroll
+      for (int j = k + 1; j < NV; ++j) A.a[i][j] -= A.a[i][k] * A.a[k][j];
+    }
+  }
+  return ok;
+}
+template <int NV>
+__device__ __forceinline__ void lu_solve(const Blk<NV>& A, const int* piv, double* x) {
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+    if (piv[k] != k) {
+      const double t = x[k];
+      x[k] = x[piv[k]];
+      x[piv[k]] = t;
+    }
+#pragma unroll
+  for (int i = 1; i < NV; ++i)
+#pragma unroll
+    for (int k = 0; k < i; ++k) x[i] -= A.a[i][k] * x[k];
+#pragma unroll
+  for (int i = NV - 1; i >= 0; --i) {
+#pragma unroll
+    for (int k = i + 1; k < NV; ++k) x[i] -= A.a[i][k] * x[k];
+    x[i] /= A.a[i][i];
+  }
+}
+// B <- A^{-1} B  (column by column)
+template <int NV>
+__device__ __forceinline__ void lu_solve_blk(const Blk<NV>& A, const int* piv, Blk<NV>& B) {
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    double c[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) c[i] = B.a[i][j];
+    lu_solve<NV>(A, piv, c);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) B.a[i][j] = c[i];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// per-partition elimination of the interior rows
+// ---------------------------------------------------------------------------
+template <int NV>
+__global__ void part_solve_kernel(const double* __restrict__ sys, const double* __restrict__ rhs,
+                                  double sign, int64_t n, double* __restrict__ Y,
+                                  double* __restrict__ V, double* __restrict__ W,
+                                  double* __restrict__ G, int* __restrict__ flag) {
+  constexpr int NV2 = NV * NV;
+  const int64_t P = (n + BT_M - 1) / BT_M;
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  const int64_t s = p * BT_M;
+  const int64_t e = ((s + BT_M < n) ? s + BT_M : n) - 1;
+  if (e == s) return;
+  double cb[NV];
+  Blk<NV> cV, Gp, cW;
+  bool ok = true;
+  zero_blk<NV>(Gp);
+  zero_blk<NV>(cW);
+  for (int64_t i = s; i < e; ++i) {
+    Blk<NV> L, D, U;
+    load_blk<NV>(sys + (i * 3 + 0) * NV2, L);
+    load_blk<NV>(sys + (i * 3 + 1) * NV2, D);
+    load_blk<NV>(sys + (i * 3 + 2) * NV2, U);
+    double b[NV];
+#pragma unroll
+    for (int a = 0; a < NV; ++a) b[a] = sign * rhs[i * NV + a];
+    Blk<NV> fV;
+    if (i > s) {
+      Blk<NV> LG;
+      mm<NV>(L, Gp, LG);
+#pragma unroll
+      for (int a = 0; a < NV; ++a)
+#pragma unroll
+        for (int c = 0; c < NV; ++c) D.a[a][c] -= LG.a[a][c];
+      double Lc[NV];
+      mv<NV>(L, cb, Lc);
+#pragma unroll
+      for (int a = 0; a < NV; ++a) b[a] -= Lc[a];
+      Blk<NV> LV;
+      mm<NV>(L, cV, LV);
+#pragma unroll
+      for (int a = 0; a < NV; ++a)
+#pragma unroll
+        for (int c = 0; c < NV; ++c) fV.a[a][c] = -LV.a[a][c];
+    } else {
+#pragma unroll
+      for (int a = 0; a < NV; ++a)
+#pragma unroll
+        for (int c = 0; c < NV; ++c) fV.a[a][c] = -L.a[a][c];
+    }
+    int piv[NV];
+    ok &= lu<NV>(D, piv);
+    lu_solve<NV>(D, piv, b);
+    lu_solve_blk<NV>(D, piv, fV);
+#pragma unroll
+    for (int a = 0; a < NV; ++a) cb[a] = b[a];
+    cV = fV;
+    if (i < e - 1) {
+      lu_solve_blk<NV>(D, piv, U);
+      Gp = U;
+    } else {
+#pragma unroll
+      for (int a = 0; a < NV; ++a)
+#pragma unroll
+        for (int c = 0; c < NV; ++c) cW.a[a][c] = -U.a[a][c];
+      lu_solve_blk<NV>(D, piv, cW);
+      zero_blk<NV>(Gp);
+    }
+#pragma unroll
+    for (int a = 0; a < NV; ++a) Y[i * NV + a] = cb[a];
+    store_blk<NV>(V + i * NV2, cV);
+    store_blk<NV>(G + i * NV2, Gp);
+  }
+  // backward sweep: z_i = c_i - G_i z_{i+1};  W has no forward part
+  double yn[NV];
+  Blk<NV> Vn, Wn;
+#pragma unroll
+  for (int a = 0; a < NV; ++a) yn[a] = cb[a];
+  Vn = cV;
+  Wn = cW;
+  store_blk<NV>(W + (e - 1) * NV2, Wn);
+  for (int64_t i = e - 2; i >= s; --i) {
+    Blk<NV> Gi, Vi;
+    load_blk<NV>(G + i * NV2, Gi);
+    load_blk<NV>(V + i * NV2, Vi);
+    double yi[NV], t[NV];
+#pragma unroll
+    for (int a = 0; a < NV; ++a) yi[a] = Y[i * NV + a];
+    mv<NV>(Gi, yn, t);
+#pragma unroll
+    for (int a = 0; a < NV; ++a) yn[a] = yi[a] - t[a];
+    Blk<NV> GV, GW;
+    mm<NV>(Gi, Vn, GV);
+    mm<NV>(Gi, Wn, GW);
+#pragma unroll
+    for (int a = 0; a < NV; ++a)
+#pragma unroll
+      for (int c = 0; c < NV; ++c) {
+        Vn.a[a][c] = Vi.a[a][c] - GV.a[a][c];
+        Wn.a[a][c] = -GW.a[a][c];
+      }
+#pragma unroll
+    for (int a = 0; a < NV; ++a) Y[i * NV + a] = yn[a];
+    store_blk<NV>(V + i * NV2, Vn);
+    store_blk<NV>(W + i * NV2, Wn);
+  }
+  if (!ok) atomicOr(flag, 2);
+}
+
+// ---------------------------------------------------------------------------
+// interface rows -> reduced system (or, with one partition, its solution)
+// ---------------------------------------------------------------------------
+template <int NV>
+__global__ void assemble_kernel(const double* __restrict__ sys, const double* __restrict__ rhs,
+                                double sign, int64_t n, bool cyclic,
+                                const double* __restrict__ Y, const double* __restrict__ V,
+                                const double* __restrict__ W, double* __restrict__ nsys,
+                                double* __restrict__ nrhs, double* __restrict__ xsol,
+                                int* __restrict__ flag) {
+  constexpr int NV2 = NV * NV;
+  const int64_t P = (n + BT_M - 1) / BT_M;
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  const int64_t s = p * BT_M;
+  const int64_t e = ((s + BT_M < n) ? s + BT_M : n) - 1;
+  Blk<NV> L, D, U;
+  load_blk<NV>(sys + (e * 3 + 0) * NV2, L);
+  load_blk<NV>(sys + (e * 3 + 1) * NV2, D);
+  load_blk<NV>(sys + (e * 3 + 2) * NV2, U);
+  double bt[NV];
+#pragma unroll
+  for (int a = 0; a < NV; ++a) bt[a] = sign * rhs[e * NV + a];
+  Blk<NV> Lt, Ut, T;
+  zero_blk<NV>(Lt);
+  zero_blk<NV>(Ut);
+  const bool has_left = (p > 0) || cyclic;
+  const bool has_right = (p < P - 1) || cyclic;
+  // left side: x_{e-1}
+  if (e > s) {
+    Blk<NV> Vb, Wb;
+    load_blk<NV>(V + (e - 1) * NV2, Vb);
+    load_blk<NV>(W + (e - 1) * NV2, Wb);
+    mm<NV>(L, Vb, Lt);
+    mm<NV>(L, Wb, T);
+#pragma unroll
+    for (int a = 0; a < NV; ++a)
+#pragma unroll
+      for (int c = 0; c < NV; ++c) D.a[a][c] += T.a[a][c];
+    double t[NV];
+    mv<NV>(L, Y + (e - 1) * NV, t);
+#pragma unroll
+    for (int a = 0; a < NV; ++a) bt[a] -= t[a];
+  } else if (has_left) {
+    Lt = L;
+  }
+  // right side: x_{e+1} = first row of the next partition
+  if (has_right) {
+    const int64_t pr = (p + 1 < P) ? p + 1 : 0;
+    const int64_t s2 = pr * BT_M;
+    const int64_t e2 = ((s2 + BT_M < n) ? s2 + BT_M : n) - 1;
+    if (e2 > s2) {
+      Blk<NV> Vb, Wb;
+      load_blk<NV>(V + s2 * NV2, Vb);
+      load_blk<NV>(W + s2 * NV2, Wb);
+      mm<NV>(U, Vb, T);
+#pragma unroll
+      for (int a = 0; a < NV; ++a)
+#pragma unroll
+        for (int c = 0; c < NV; ++c) D.a[a][c] += T.a[a][c];
+      mm<NV>(U, Wb, Ut);
+      double t[NV];
+      mv<NV>(U, Y + s2 * NV, t);
+#pragma unroll
+      for (int a = 0; a < NV; ++a) bt[a] -= t[a];
+    } else {
+      Ut = U;
+    }
+  }
+  if (P == 1) {
+    // every neighbour is this partition's own interface unknown
+#pragma unroll
+    for (int a = 0; a < NV; ++a)
+#pragma unroll
+      for (int c = 0; c < NV; ++c) D.a[a][c] += Lt.a[a][c] + Ut.a[a][c];
+    int piv[NV];
+    if (!lu<NV>(D, piv)) atomicOr(flag, 2);
+    lu_solve<NV>(D, piv, bt);
+#pragma unroll
+    for (int a = 0; a < NV; ++a) xsol[a] = bt[a];
+    return;
+  }
+  store_blk<NV>(nsys + (p * 3 + 0) * NV2, Lt);
+  store_blk<NV>(nsys + (p * 3 + 1) * NV2, D);
+  store_blk<NV>(nsys + (p * 3 + 2) * NV2, Ut);
+#pragma unroll
+  for (int a = 0; a < NV; ++a) nrhs[p * NV + a] = bt[a];
+}
+
+// ---------------------------------------------------------------------------
+// back-substitution, one thread per row (coalesced)
+// ---------------------------------------------------------------------------
+template <int NV>
+__global__ void backsub_kernel(int64_t n, bool cyclic, const double* __restrict__ Y,
+                               const double* __restrict__ V, const double* __restrict__ W,
+                               const double* __restrict__ X, double* __restrict__ out) {
+  constexpr int NV2 = NV * NV;
+  const int64_t P = (n + BT_M - 1) / BT_M;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = i / BT_M;
+    const int64_t s = p * BT_M;
+    const int64_t e = ((s + BT_M < n) ? s + BT_M : n) - 1;
+    double xo[NV];
+    if (i == e) {
+#pragma unroll
+      for (int a = 0; a < NV; ++a) xo[a] = X[p * NV + a];
+    } else {
+      Blk<NV> Vb, Wb;
+      load_blk<NV>(V + i * NV2, Vb);
+      load_blk<NV>(W + i * NV2, Wb);
+      double t[NV];
+#pragma unroll
+      for (int a = 0; a < NV; ++a) xo[a] = Y[i * NV + a];
+      mv<NV>(Wb, X + p * NV, t);
+#pragma unroll
+      for (int a = 0; a < NV; ++a) xo[a] += t[a];
+      if (p > 0 || cyclic) {
+        const int64_t pl = (p > 0) ? p - 1 : P - 1;
+        mv<NV>(Vb, X + pl * NV, t);
+#pragma unroll
+        for (int a = 0; a < NV; ++a) xo[a] += t[a];
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < NV; ++a) out[i * NV + a] = xo[a];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host driver
+// ---------------------------------------------------------------------------
+struct LevelBufs {
+  int64_t n;
+  const double* sys;
+  const double* rhs;
+  double sign;
+  double *Y, *V, *W, *G;
+  double* sol;  // solution of this level (n rows)
+};
+
+static size_t level_bytes(int64_t n, int nv) {
+  return 4 * align_up(sizeof(double) * n * nv * nv) + align_up(sizeof(double) * n * nv);
+}
+
+size_t bt_workspace_bytes(int64_t n, int nv) {
+  size_t b = 0;
+  int64_t cur = n;
+  while (true) {
+    b += level_bytes(cur, nv);  // Y, V, W, G
+    const int64_t P = (cur + BT_M - 1) / BT_M;
+    // next level: sys + rhs + sol
+    b += align_up(sizeof(double) * P * 3 * nv * nv) + 2 * align_up(sizeof(double) * P * nv);
+    if (P == 1) break;
+    cur = P;
+  }
+  return b;
+}
+
+template <int NV>
+static int bt_solve_t(adrom_ctx* ctx, const double* sys, const double* rhs, double sign,
+                      int64_t n, bool cyclic, double* out, void* ws, int* flag) {
+  constexpr int NV2 = NV * NV;
+  LevelBufs lv[16];
+  int nl = 0;
+  char* w = (char*)ws;
+  auto take = [&](size_t bytes) {
+    double* p = (double*)w;
+    w += align_up(bytes);
+    return p;
+  };
+  lv[0].n = n;
+  lv[0].sys = sys;
+  lv[0].rhs = rhs;
+  lv[0].sign = sign;
+  lv[0].sol = out;
+  // forward: eliminate interiors level by level
+  while (true) {
+    LevelBufs& L = lv[nl];
+    L.Y = take(sizeof(double) * L.n * NV);
+    L.V = take(sizeof(double) * L.n * NV2);
+    L.W = take(sizeof(double) * L.n * NV2);
+    L.G = take(sizeof(double) * L.n * NV2);
+    take(0);
+    const int64_t P = (L.n + BT_M - 1) / BT_M;
+    double* nsys = take(sizeof(double) * P * 3 * NV2);
+    double* nrhs = take(sizeof(double) * P * NV);
+    double* nsol = take(sizeof(double) * P * NV);
+    const int nt = 128;
+    const int gb = (int)((P + nt - 1) / nt);
+    part_solve_kernel<NV><<<gb, nt, 0, ctx->stream>>>(L.sys, L.rhs, L.sign, L.n, L.Y, L.V, L.W,
+                                                      L.G, flag);
+    ADROM_LAUNCH_CK(ctx);
+    assemble_kernel<NV><<<gb, nt, 0, ctx->stream>>>(L.sys, L.rhs, L.sign, L.n, cyclic, L.Y, L.V,
+                                                    L.W, nsys, nrhs, nsol, flag);
+    ADROM_LAUNCH_CK(ctx);
+    if (nl + 1 >= 16) return set_error(ctx, ADROM_ERR_ARG, "bt_solve: too many levels");
+    LevelBufs& N = lv[nl + 1];
+    N.n = P;
+    N.sys = nsys;
+    N.rhs = nrhs;
+    N.sign = 1.0;
+    N.sol = nsol;
+    ++nl;
+    if (P == 1) break;
+  }
+  // backward: level nl holds the 1-row solution; substitute upwards
+  for (int l = nl - 1; l >= 0; --l) {
+    const LevelBufs& L = lv[l];
+    int64_t gb = (L.n + 255) / 256;
+    if (gb > (int64_t)ctx->num_sms * 16) gb = (int64_t)ctx->num_sms * 16;
+    backsub_kernel<NV><<<(int)gb, 256, 0, ctx->stream>>>(L.n, cyclic, L.Y, L.V, L.W,
+                                                         lv[l + 1].sol, L.sol);
+    ADROM_LAUNCH_CK(ctx);
+  }
+  return ADROM_OK;
+}
+
+int bt_solve(adrom_ctx* ctx, const double* sys, const double* rhs, double rhs_sign, int64_t n,
+             int nv, bool cyclic, double* out, void* ws, int* flag) {
+  if (nv == 1) return bt_solve_t<1>(ctx, sys, rhs, rhs_sign, n, cyclic, out, ws, flag);
+  if (nv == 3) return bt_solve_t<3>(ctx, sys, rhs, rhs_sign, n, cyclic, out, ws, flag);
+  return set_error(ctx, ADROM_ERR_ARG, "bt_solve: unsupported block size %d", nv);
+}
+
+}  // namespace adrom

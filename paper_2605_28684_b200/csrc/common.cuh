@@ -1,0 +1,112 @@
+// Shared helpers for the adrom B200 kernels (sm_100a, fp64).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+
+#include "../../include/adrom_b200.h"
+
+#define ADROM_WARP 32
+
+namespace adrom {
+
+// numpy.maximum semantics: NaN in either operand propagates; otherwise max.
+// (fmax() returns the non-NaN operand, which numpy does not.)
+__device__ __forceinline__ double np_max(double a, double b) {
+  if (a != a) return a;
+  if (b != b) return b;
+  return a >= b ? a : b;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Deterministic block sum (fixed reduction tree); result valid in all threads.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* sh /* >= NT/32 */) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x < 32) {
+    t = (lane < NT / 32) ? sh[lane] : 0.0;
+    t = warp_sum(t);
+    if (lane == 0) sh[0] = t;
+  }
+  __syncthreads();
+  t = sh[0];
+  __syncthreads();
+  return t;
+}
+
+// Runtime-sized variant (blockDim.x multiple of 32).
+__device__ __forceinline__ double block_sum_dyn(double v, double* sh) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x < 32) {
+    t = (lane < nw) ? sh[lane] : 0.0;
+    t = warp_sum(t);
+    if (lane == 0) sh[0] = t;
+  }
+  __syncthreads();
+  t = sh[0];
+  __syncthreads();
+  return t;
+}
+
+}  // namespace adrom
+
+// ---------------------------------------------------------------------------
+// host-side context
+// ---------------------------------------------------------------------------
+struct adrom_ctx {
+  cudaStream_t stream = nullptr;
+  int device = 0;
+  int num_sms = 148;
+  // growable device scratch
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  // device status words: [0] error code, [1] aux int, ...
+  int* dflags = nullptr;
+  // pinned host staging for small results
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+  char err[512] = {0};
+};
+
+namespace adrom {
+
+int set_error(adrom_ctx* ctx, int code, const char* fmt, ...);
+int check_cuda(adrom_ctx* ctx, cudaError_t e, const char* where);
+// scratch sub-allocation: returns a 256-byte aligned device pointer into the
+// context scratch area (grown if needed; growing synchronises the stream).
+void* scratch(adrom_ctx* ctx, size_t bytes, size_t offset_bytes = 0);
+int ensure_scratch(adrom_ctx* ctx, size_t bytes);
+int ensure_pinned(adrom_ctx* ctx, size_t bytes);
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+}  // namespace adrom
+
+#define ADROM_CK(ctx, call)                                          \
+  do {                                                               \
+    cudaError_t _e = (call);                                         \
+    if (_e != cudaSuccess) return adrom::check_cuda(ctx, _e, #call); \
+  } while (0)
+
+#define ADROM_LAUNCH_CK(ctx) ADROM_CK(ctx, cudaGetLastError())

@@ -1,0 +1,116 @@
+// Context management: stream, device scratch, pinned staging, error text.
+#include "common.cuh"
+
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+namespace adrom {
+
+int set_error(adrom_ctx* ctx, int code, const char* fmt, ...) {
+  if (ctx) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(ctx->err, sizeof(ctx->err), fmt, ap);
+    va_end(ap);
+  }
+  return code;
+}
+
+int check_cuda(adrom_ctx* ctx, cudaError_t e, const char* where) {
+  return set_error(ctx, ADROM_ERR_CUDA, "CUDA error %s (%s) at %s", cudaGetErrorName(e),
+                   cudaGetErrorString(e), where);
+}
+
+int ensure_scratch(adrom_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->scratch_bytes && ctx->scratch) return ADROM_OK;
+  size_t want = bytes < 1 << 20 ? (1 << 20) : bytes;
+  want = want + want / 4;
+  if (ctx->scratch) {
+    ADROM_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    ADROM_CK(ctx, cudaFree(ctx->scratch));
+    ctx->scratch = nullptr;
+    ctx->scratch_bytes = 0;
+  }
+  ADROM_CK(ctx, cudaMalloc(&ctx->scratch, want));
+  ctx->scratch_bytes = want;
+  return ADROM_OK;
+}
+
+void* scratch(adrom_ctx* ctx, size_t bytes, size_t offset_bytes) {
+  (void)bytes;
+  return (char*)ctx->scratch + offset_bytes;
+}
+
+int ensure_pinned(adrom_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->pinned_bytes && ctx->pinned) return ADROM_OK;
+  if (ctx->pinned) {
+    ADROM_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    ADROM_CK(ctx, cudaFreeHost(ctx->pinned));
+    ctx->pinned = nullptr;
+  }
+  size_t want = bytes < 4096 ? 4096 : bytes;
+  ADROM_CK(ctx, cudaMallocHost(&ctx->pinned, want));
+  ctx->pinned_bytes = want;
+  return ADROM_OK;
+}
+
+}  // namespace adrom
+
+extern "C" {
+
+int adrom_abi_version(void) { return ADROM_ABI_VERSION; }
+
+int adrom_ctx_create(adrom_ctx** out, void* stream) {
+  if (!out) return ADROM_ERR_ARG;
+  adrom_ctx* ctx = new adrom_ctx();
+  ctx->stream = (cudaStream_t)stream;
+  cudaError_t e = cudaGetDevice(&ctx->device);
+  if (e != cudaSuccess) {
+    delete ctx;
+    *out = nullptr;
+    return ADROM_ERR_CUDA;
+  }
+  cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  e = cudaMalloc(&ctx->dflags, 64 * sizeof(int));
+  if (e != cudaSuccess) {
+    delete ctx;
+    *out = nullptr;
+    return ADROM_ERR_CUDA;
+  }
+  cudaMemset(ctx->dflags, 0, 64 * sizeof(int));
+  int st = adrom::ensure_pinned(ctx, 1 << 16);
+  if (st) {
+    cudaFree(ctx->dflags);
+    delete ctx;
+    *out = nullptr;
+    return st;
+  }
+  *out = ctx;
+  return ADROM_OK;
+}
+
+int adrom_ctx_set_stream(adrom_ctx* ctx, void* stream) {
+  if (!ctx) return ADROM_ERR_ARG;
+  ctx->stream = (cudaStream_t)stream;
+  return ADROM_OK;
+}
+
+void adrom_ctx_destroy(adrom_ctx* ctx) {
+  if (!ctx) return;
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->scratch) cudaFree(ctx->scratch);
+  if (ctx->dflags) cudaFree(ctx->dflags);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  delete ctx;
+}
+
+const char* adrom_ctx_last_error(const adrom_ctx* ctx) { return ctx ? ctx->err : "null context"; }
+
+int adrom_ctx_synchronize(adrom_ctx* ctx) {
+  if (!ctx) return ADROM_ERR_ARG;
+  ADROM_CK(ctx, cudaStreamSynchronize(ctx->stream));
+  return ADROM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,249 @@
+"""GPU-backed full-order models with the reference ``FomProblem`` surface.
+
+Mirrors ``/root/reference/pkg/src/adrom/fom.py``: ``BurgersProblem``
+(fom.py:161-201), ``SodProblem`` (fom.py:249-282), ``TimeStepper``
+(fom.py:42-53), ``implicit_step`` / ``coarse_step`` (fom.py:331-356),
+``fd_jacobian`` (fom.py:301-328).  Every residual, Jacobian and Newton
+solve runs in the CUDA library (``adrom_rhs``, ``adrom_fd_jacobian_blocks``,
+``adrom_implicit_step``); topology helpers (neighbour indices, cell
+centres) stay on the host like the reference's.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _dev
+from ._lib import BURGERS, SOD, Context, Model, NewtonInfo, ptr
+from .errors import DenseError
+
+__all__ = ["TimeStepper", "FomProblem", "BurgersProblem", "SodProblem", "NewtonResult",
+           "fd_jacobian", "fd_jacobian_blocks", "implicit_step", "coarse_step",
+           "sod_initial_state", "PRIM_FLOOR", "FD_EPS"]
+
+PRIM_FLOOR = 1e-10   # fom.py:36
+FD_EPS = 1e-7        # fom.py:39
+
+
+@dataclass(frozen=True)
+class TimeStepper:
+    """fom.py:42-53 — backward-Euler settings."""
+
+    dt: float
+    newton_tol: float = 1e-8
+    newton_max_iter: int = 10
+
+    def __post_init__(self):
+        if self.dt <= 0:
+            raise ValueError("dt must be positive")
+
+
+@dataclass
+class NewtonResult:
+    """dense.py:129-137."""
+
+    x: object
+    converged: bool
+    iterations: int
+    residual_norm: float
+
+
+class FomProblem:
+    """fom.py:56-116 — common surface of the device-backed models."""
+
+    n_var: int = 1
+    boundary: str = "periodic"
+    stencil_radius: int = 1
+    var_names: tuple[str, ...] = ()
+    kind: int = 0
+
+    def __init__(self, n_elem: int, length: float = 1.0):
+        if n_elem < 4:
+            raise ValueError("n_elem must be at least 4")
+        self.n_elem = int(n_elem)
+        self.length = float(length)
+        self.dx = self.length / self.n_elem
+
+    @property
+    def n_dof(self) -> int:
+        return self.n_var * self.n_elem
+
+    @property
+    def cell_centers(self) -> np.ndarray:
+        return (np.arange(self.n_elem) + 0.5) * self.dx
+
+    def abi(self) -> Model:
+        return Model(self.kind, self.n_var, self.n_elem, self.dx,
+                     getattr(self, "nu", 0.0), getattr(self, "gamma", 1.4))
+
+    def neighbor_cells(self, cells):
+        """fom.py:92-97."""
+        cells = np.asarray(cells, dtype=int)
+        if self.boundary == "periodic":
+            return (cells - 1) % self.n_elem, (cells + 1) % self.n_elem
+        return np.maximum(cells - 1, 0), np.minimum(cells + 1, self.n_elem - 1)
+
+    # -- residual (kernel 1) ------------------------------------------------
+    def rhs(self, q):
+        """f(q) on the device (bitwise equal to the reference's numpy)."""
+        qd = _dev.dev(q)
+        if qd.numel() != self.n_dof:
+            raise ValueError(f"state length {qd.numel()} != n_dof {self.n_dof}")
+        out = _dev.empty(self.n_dof)
+        m = self.abi()
+        Context.get().call("adrom_rhs", C.byref(m), ptr(qd), ptr(out))
+        return _dev.like(out, q)
+
+    def rhs_at_cells(self, gathered):
+        """fom.py:104-110 — (k, 3, n_var) stencils -> (k, n_var)."""
+        g = _dev.dev(gathered)
+        if g.dim() != 3 or g.shape[1] != 3 or g.shape[2] != self.n_var:
+            raise ValueError(f"gathered must have shape (k, 3, {self.n_var})")
+        k = g.shape[0]
+        out = _dev.empty(k, self.n_var)
+        m = self.abi()
+        Context.get().call("adrom_rhs_at_cells", C.byref(m), ptr(g), C.c_int64(k), ptr(out))
+        return _dev.like(out, gathered)
+
+    def sampling_plan(self, sampling):
+        from .sampling import SamplingPlan
+        return SamplingPlan(self, sampling)
+
+    def primitive_fields(self, q):
+        raise NotImplementedError
+
+    def initial_state(self):
+        raise NotImplementedError
+
+
+class BurgersProblem(FomProblem):
+    """fom.py:161-201 — viscous Burgers, periodic, upwind convection."""
+
+    n_var = 1
+    boundary = "periodic"
+    var_names = ("u",)
+    kind = BURGERS
+
+    def __init__(self, n_elem: int, nu: float = 0.01, length: float = 1.0, ic_width: float = 0.1):
+        super().__init__(n_elem, length)
+        if nu <= 0:
+            raise ValueError("viscosity must be positive")
+        self.nu = float(nu)
+        self.ic_width = float(ic_width)
+
+    def initial_state(self) -> np.ndarray:
+        """fom.py:176-178 (host-generated input data)."""
+        x = self.cell_centers
+        return np.exp(-0.5 * ((x - 0.5 * self.length) / self.ic_width) ** 2)
+
+    def primitive_fields(self, q):
+        return {"u": q}
+
+
+def sod_initial_state(n_elem: int, gamma: float = 1.4) -> np.ndarray:
+    """fom.py:239-246 (host-generated input data)."""
+    x = (np.arange(n_elem) + 0.5) / n_elem
+    rho = np.where(x < 0.5, 1.0, 0.125)
+    p = np.where(x < 0.5, 1.0, 0.1)
+    u = np.zeros(n_elem)
+    return np.stack([rho, rho * u, p / (gamma - 1.0) + 0.5 * rho * u ** 2], axis=1).ravel()
+
+
+class SodProblem(FomProblem):
+    """fom.py:249-282 — 1D Euler, Rusanov flux, zero-gradient ghosts."""
+
+    n_var = 3
+    boundary = "zero-gradient"
+    var_names = ("rho", "v", "p")
+    kind = SOD
+
+    def __init__(self, n_elem: int, gamma: float = 1.4, length: float = 1.0):
+        super().__init__(n_elem, length)
+        if gamma <= 1.0:
+            raise ValueError("gamma must exceed 1")
+        self.gamma = float(gamma)
+
+    def initial_state(self) -> np.ndarray:
+        return sod_initial_state(self.n_elem, self.gamma)
+
+    def primitive_fields(self, q):
+        """fom.py:279-282 (diagnostics; evaluated where q lives)."""
+        if _dev.is_device(q):
+            t = _dev.torch()
+            u = q.reshape(self.n_elem, 3)
+            rho = t.clamp_min(u[:, 0], PRIM_FLOOR)
+            vel = u[:, 1] / rho
+            p = t.clamp_min((self.gamma - 1.0) * (u[:, 2] - 0.5 * rho * vel ** 2), PRIM_FLOOR)
+            return {"rho": rho, "v": vel, "p": p}
+        u = np.asarray(q, dtype=float).reshape(self.n_elem, 3)
+        rho = np.maximum(u[:, 0], PRIM_FLOOR)
+        vel = u[:, 1] / rho
+        p = np.maximum((self.gamma - 1.0) * (u[:, 2] - 0.5 * rho * vel ** 2), PRIM_FLOOR)
+        return {"rho": rho, "v": vel, "p": p}
+
+
+def _check_model(model):
+    if not isinstance(model, (BurgersProblem, SodProblem)):
+        raise TypeError(
+            f"{type(model).__name__} has no device implementation; the B200 path "
+            "supports BurgersProblem and SodProblem (subclasses may override "
+            "initial_state only)")
+
+
+def fd_jacobian_blocks(model: FomProblem, q):
+    """Nonzero blocks of ``fd_jacobian`` (fom.py:301-328), shape
+    (n_elem, 3, n_var, n_var): d rhs_i / d q_{left(i)}, d q_i, d q_{right(i)}."""
+    _check_model(model)
+    qd = _dev.dev(q)
+    nv = model.n_var
+    out = _dev.empty(model.n_elem, 3, nv, nv)
+    m = model.abi()
+    Context.get().call("adrom_fd_jacobian_blocks", C.byref(m), ptr(qd), ptr(out))
+    return _dev.like(out, q)
+
+
+def fd_jacobian(model: FomProblem, q, rhs0=None):
+    """Dense FD Jacobian (fom.py:301-328) assembled from the device blocks.
+    O(N^2) memory like the reference — for small grids / tests only."""
+    blocks = _dev.host(fd_jacobian_blocks(model, q))
+    nv, n = model.n_var, model.n_elem
+    dense = np.zeros((n * nv, n * nv))
+    cells = np.arange(n)
+    left, right = model.neighbor_cells(cells)
+    for i in range(n):
+        rows = slice(i * nv, (i + 1) * nv)
+        if left[i] != i:
+            dense[rows, left[i] * nv:(left[i] + 1) * nv] = blocks[i, 0]
+        dense[rows, i * nv:(i + 1) * nv] = blocks[i, 1]
+        if right[i] != i:
+            dense[rows, right[i] * nv:(right[i] + 1) * nv] = blocks[i, 2]
+    return dense
+
+
+def implicit_step(model: FomProblem, q, dt: float, stepper: TimeStepper | None = None) -> NewtonResult:
+    """fom.py:331-347 — backward Euler by Newton; non-convergence flagged."""
+    _check_model(model)
+    if stepper is None:
+        stepper = TimeStepper(dt=dt)
+    if stepper.newton_tol <= 0:
+        raise DenseError("newton_solve requires tol > 0")
+    qd = _dev.dev(q)
+    x = _dev.empty(model.n_dof)
+    info = NewtonInfo()
+    m = model.abi()
+    Context.get().call("adrom_implicit_step", C.byref(m), ptr(qd), C.c_double(dt),
+                       C.c_double(stepper.newton_tol), C.c_int32(stepper.newton_max_iter),
+                       ptr(x), C.byref(info))
+    return NewtonResult(x=_dev.like(x, q), converged=bool(info.converged),
+                        iterations=int(info.iterations), residual_norm=float(info.residual_norm))
+
+
+def coarse_step(model: FomProblem, y, z: int, dt: float,
+                stepper: TimeStepper | None = None) -> NewtonResult:
+    """fom.py:350-356 — implicit step of size z*dt."""
+    if z < 1:
+        raise ValueError("z must be at least 1")
+    return implicit_step(model, y, z * dt, stepper)

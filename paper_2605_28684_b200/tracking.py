@@ -1,0 +1,116 @@
+"""Device-resident basis tracking: ``ReducedBasis`` and the iSVD update.
+
+Mirrors ``/root/reference/pkg/src/adrom/tracking.py``: ``ReducedBasis``
+(51-64), ``UpdateRule`` (96-138), ``isvd_update`` (141-178).  The other
+five rules of the reference (wsvd/direct/onestep/oja/grouse) are outside
+the north-star path and are not provided.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _dev
+from ._lib import Context, IsvdInfo, ptr
+
+__all__ = ["ReducedBasis", "UpdateRule", "isvd_update", "DEGENERATE_TOL", "last_isvd_info"]
+
+DEGENERATE_TOL = 1e-12  # tracking.py:46
+
+
+@dataclass(frozen=True)
+class ReducedBasis:
+    """tracking.py:51-64 — orthonormal basis (N x r) + singular values."""
+
+    phi: object
+    sigma: object
+
+    @property
+    def rank(self) -> int:
+        return int(self.phi.shape[1])
+
+    def orthonormality_defect(self) -> float:
+        if _dev.is_device(self.phi):
+            t = _dev.torch()
+            g = self.phi.T @ self.phi
+            return float(t.linalg.norm(g - t.eye(self.rank, dtype=g.dtype, device=g.device)))
+        r = self.rank
+        return float(np.linalg.norm(self.phi.T @ self.phi - np.eye(r)))
+
+
+@dataclass(frozen=True)
+class UpdateRule:
+    """tracking.py:96-138 (only ``isvd`` is implemented on the device)."""
+
+    kind: str
+    lam: float = 1.0
+    window: int = 8
+    eta: float = 0.01
+
+    HISTORY_AWARE = ("isvd", "wsvd", "direct")
+    INSTANTANEOUS = ("onestep", "oja", "grouse")
+
+    def __post_init__(self):
+        if self.kind not in self.HISTORY_AWARE + self.INSTANTANEOUS:
+            raise ValueError(f"unknown update rule {self.kind!r}")
+        if not 0.0 <= self.lam <= 1.0:
+            raise ValueError("forgetting factor must lie in [0, 1]")
+        if self.eta <= 0.0:
+            raise ValueError("learning rate must be positive")
+        if self.window < 1:
+            raise ValueError("window size must be at least 1")
+
+    @property
+    def history_aware(self) -> bool:
+        return self.kind in self.HISTORY_AWARE
+
+    @property
+    def uses_window(self) -> bool:
+        return self.kind in ("wsvd", "direct")
+
+    def label(self) -> str:
+        if self.kind == "isvd":
+            return f"isvd(lambda={self.lam:g})"
+        if self.kind in ("wsvd", "direct"):
+            return f"{self.kind}(w={self.window})"
+        if self.kind == "onestep":
+            return "onestep"
+        return f"{self.kind}(eta={self.eta:g})"
+
+
+_last_info = {}
+
+
+def last_isvd_info() -> dict:
+    """Diagnostics of the most recent ``isvd_update`` call (qnorm, ynorm,
+    proj_resid, degenerate, reorthogonalised, sweeps)."""
+    return dict(_last_info)
+
+
+def isvd_update(basis: ReducedBasis, y_hat, lam: float, r: int) -> ReducedBasis:
+    """tracking.py:141-178 — rank-r incremental SVD with forgetting ``lam``.
+
+    Runs three device passes (projection, optional re-orthogonalisation,
+    fused rotation) around a one-block Jacobi SVD of the (r+1)^2 core
+    matrix.  Returns a new basis (inputs are not modified), on the device
+    if the inputs were device tensors, else as numpy arrays.
+    """
+    phi = _dev.dev(basis.phi)
+    n, r_cur = phi.shape
+    y = _dev.dev(y_hat)
+    if y.dim() != 1 or y.shape[0] != n:
+        raise ValueError(f"snapshot length {tuple(y.shape)} does not match basis rows {n}")
+    sigma = _dev.dev(basis.sigma)
+    phi_out = _dev.empty(n, r)
+    sigma_out = _dev.empty(r)
+    info = IsvdInfo()
+    Context.get().call("adrom_isvd_update", ptr(phi), ptr(sigma), ptr(y), C.c_int64(n),
+                       C.c_int32(r_cur), C.c_int32(r), C.c_double(lam), ptr(phi_out),
+                       ptr(sigma_out), C.byref(info))
+    _last_info.update(qnorm=info.qnorm, ynorm=info.ynorm, proj_resid=info.proj_resid,
+                      degenerate=bool(info.degenerate),
+                      reorthogonalised=bool(info.reorthogonalised), sweeps=info.sweeps)
+    return ReducedBasis(phi=_dev.like(phi_out, basis.phi), sigma=_dev.like(sigma_out, basis.sigma))
