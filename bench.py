@@ -1,0 +1,587 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 adaptive-ROM hot path (driver contract, one JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config cfg3|cfg2|cfg1|cfg0]
+
+Workloads (BASELINE.json configs; seeded synthetic inputs, no datasets):
+  cfg3  Burgers N=2^24 adaptive ROM, iSVD every step (r=n_s=64)   [default]
+        step = one online step of driver._run_rom (LSPG step + decode +
+        coarse Newton + iSVD + QDEIM + operator rebuild + encode)
+  cfg2  iSVD stream N=2^22, r=64: step = one rank-1 update (tracking.py:141)
+  cfg1  Sod N=4096 adaptive ROM (LSPG + FGS, z=5)
+  cfg0  Burgers N=1024 adaptive ROM (LSPG + QDEIM, z=10)
+
+Multi-GPU: the path does not shard (replicas only); with N ranks
+every rank runs an independent replica, `value` sums the replicas and the
+time is the max over ranks (CUDA events, barrier + synchronize around the
+timed region).
+
+--impl reference times the CPU implementation of the same path (the oracle
+port of the reference, oracle/; the reference itself is Python and does not
+travel to the GPU box) on rank 0 with all host threads.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS = {}
+try:
+    PEAKS = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+except Exception:  # noqa: BLE001
+    PEAKS = {}
+HBM_PEAK = float(PEAKS.get("hbm_gbs", 6650.0))
+HBM_PEAK_SRC = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in PEAKS else \
+    "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+# --------------------------------------------------------------------------- utils
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sms.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+def dist_setup():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    import torch
+    if torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:  # noqa: BLE001
+        return os.cpu_count() or 1
+
+
+def roofline(bytes_per_launch: float, ms_per_launch: float, traffic=None) -> dict:
+    achieved = bytes_per_launch / (ms_per_launch * 1e-3) / 1e9
+    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": HBM_PEAK, "unit": "GB/s",
+            "frac": round(achieved / HBM_PEAK, 4), "traffic": traffic, "peak_source": HBM_PEAK_SRC}
+
+
+# --------------------------------------------------------------------------- cfg2
+
+def cfg2_inputs(case, n_snap: int, seed: int = 0):
+    """Device-generated rank-K stream (torch CUDA RNG; the parity tests use
+    the numpy recipe of configs.StreamCase at smaller N)."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    q = torch.linalg.qr(torch.randn(case.n, case.k, dtype=torch.float64, device="cuda",
+                                    generator=g))[0]
+    s = torch.arange(1, case.k + 1, dtype=torch.float64, device="cuda") ** -1.5
+    coef = torch.randn(case.k, n_snap, dtype=torch.float64, device="cuda", generator=g) * s[:, None]
+    snaps = q @ coef + case.noise * torch.randn(case.n, n_snap, dtype=torch.float64,
+                                                device="cuda", generator=g)
+    del q
+    return snaps.T.contiguous()  # (n_snap, N): row k = snapshot k
+
+
+def bench_cfg2(args, rank, world):
+    import ctypes as C
+    import torch
+    from paper_2605_28684_b200 import _lib
+    from paper_2605_28684_b200.configs import cfg2
+    case = cfg2()
+    if args.n:
+        case = type(case)(n=args.n)
+    n, r = case.n, case.r
+    K, W = args.steps, args.warmup
+    snaps = cfg2_inputs(case, r + W + K)
+    # setup (untimed): thin_svd of the first r snapshots via QR + small SVD
+    qf, rf = torch.linalg.qr(snaps[:r].T)
+    ur, s, _ = torch.linalg.svd(rf)
+    phi = (qf @ ur).contiguous()
+    sig = s.contiguous()
+    del qf
+    ctx = _lib.Context.get()
+    P = _lib.ptr
+    gram = torch.empty((r, r), dtype=torch.float64, device="cuda")
+    ctx.call("adrom_gram", P(phi), C.c_int64(n), C.c_int32(r), P(gram))  # tracked from here
+
+    def update(k):
+        y = snaps[r + k]
+        ctx.call("adrom_isvd_update", P(phi), P(sig), P(y), C.c_int64(n), C.c_int32(r),
+                 C.c_int32(r), C.c_double(case.lam), P(phi), P(sig), P(gram), None)
+
+    for k in range(W):
+        update(k)
+    torch.cuda.synchronize()
+    barrier(world)
+    ctx.prof_enable(True)
+    l0 = ctx.launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        torch.cuda.synchronize()
+        ev0.record()
+        for k in range(W, W + K):
+            update(k)
+        ev1.record()
+        torch.cuda.synchronize()
+    launches = ctx.launches() - l0
+    probes = ctx.prof_read()
+    ctx.prof_enable(False)
+    ms = ev0.elapsed_time(ev1)
+    ms = max_over_ranks(ms, world)
+    barrier(world)
+    ms_step = ms / K
+    value = world * K / (ms * 1e-3)
+    rot_ms, rot_n = probes.get("isvd_rotate", (0.0, 0))
+    rot_bytes = 8.0 * (2 * n * r + n)
+    canon = 8.0 * (3 * n * r + 2 * n)
+    extra = {
+        "isvd_update_ms": round(ms_step, 4),
+        "isvd_update_hbm_frac": round(canon / (ms_step * 1e-3) / 1e9 / HBM_PEAK, 4),
+        "isvd_update_canonical_bytes": canon,
+        "probes_ms": {k: round(v[0] / max(v[1], 1), 4) for k, v in probes.items()},
+        "reorth_passes": probes.get("isvd_resid", (0, 0))[1],
+    }
+    line = {
+        "metric": "iSVD rank-1 updates/s (N=2^22, r=64); iSVD % of HBM roofline",
+        "value": round(value, 3), "unit": "updates/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded rank-96 stream, device RNG)",
+        "config": {"workload": "cfg2-isvd-stream", "n": n, "r": r, "lam": case.lam,
+                   "l2": "inputs larger than L2 (basis 2 GiB)", "parallelism": f"replicas{world}"},
+        "roofline": roofline(rot_bytes, rot_ms / max(rot_n, 1)) if rot_n else None,
+        "gpu_launches": launches,
+    }
+    line["roofline_kernel"] = "isvd_rotate (rot_tiled_kernel<64>): 8(2Nr+N) bytes/launch"
+    line.update(extra)
+    line["clocks"] = clk.summary()
+    if rank == 0 and not args.no_e2e:
+        line["e2e"] = e2e_cfg2(args, case, snaps, phi, sig)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_cfg2(case)
+    return line
+
+
+def e2e_cfg2(args, case, snaps, phi, sig):
+    """Same update through the C-ABI with HOST buffers: every step copies the
+    basis, sigma and snapshot from pinned host memory and the result back."""
+    import ctypes as C
+    import torch
+    from paper_2605_28684_b200 import _lib
+    n, r = case.n, case.r
+    steps = min(args.steps, 5)
+    h_phi = torch.empty((n, r), dtype=torch.float64, pin_memory=True)
+    h_phi.copy_(phi)
+    h_sig = torch.empty(r, dtype=torch.float64, pin_memory=True)
+    h_sig.copy_(sig)
+    h_y = torch.empty((steps, n), dtype=torch.float64, pin_memory=True)
+    h_y.copy_(snaps[-steps:])
+    d_phi = torch.empty_like(phi)
+    d_sig = torch.empty_like(sig)
+    d_gram = torch.empty((r, r), dtype=torch.float64, device="cuda")
+    d_y = torch.empty(n, dtype=torch.float64, device="cuda")
+    ctx = _lib.Context.get()
+    P = _lib.ptr
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for k in range(steps):
+        d_phi.copy_(h_phi, non_blocking=True)
+        d_sig.copy_(h_sig, non_blocking=True)
+        d_y.copy_(h_y[k], non_blocking=True)
+        ctx.call("adrom_isvd_update", P(d_phi), P(d_sig), P(d_y), C.c_int64(n), C.c_int32(r),
+                 C.c_int32(r), C.c_double(case.lam), P(d_phi), P(d_sig), None, None)
+        h_phi.copy_(d_phi, non_blocking=True)
+        h_sig.copy_(d_sig, non_blocking=True)
+    ev1.record()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / steps
+    return {"value": round(1e3 / ms, 3), "unit": "updates/s", "ms_per_step": round(ms, 3),
+            "h2d_bytes_per_step": 8 * (n * r + r + n), "d2h_bytes_per_step": 8 * (n * r + r),
+            "steps": steps}
+
+
+def cpu_baseline_cfg2(case, n_sample=1 << 20, reps=2):
+    """Oracle port of tracking.isvd_update (gelsd least squares, as the
+    reference) on the host; timed at n_sample rows and scaled linearly to N."""
+    from oracle import subspace
+    rng = np.random.default_rng(0)
+    r = case.r
+    phi = np.linalg.qr(rng.standard_normal((n_sample, r)))[0]
+    sig = np.linspace(10, 1, r)
+    ys = [rng.standard_normal(n_sample) for _ in range(reps)]
+    t0 = time.perf_counter()
+    for y in ys:
+        phi, sig, _ = subspace.isvd_update(phi, sig, y, case.lam, r)
+    dt = (time.perf_counter() - t0) / reps
+    scale = n_sample / case.n
+    return {"value": round(scale / dt, 6), "unit": "updates/s", "cores": cpu_cores(),
+            "kind": "port", "sample": f"{reps} oracle isvd_update (numpy/LAPACK gelsd) at "
+            f"N={n_sample}, r={r}; {dt:.2f} s/update scaled x{case.n // n_sample} to N={case.n}"}
+
+
+def reference_cfg2(args, rank, world):
+    if rank != 0:
+        return None
+    from paper_2605_28684_b200.configs import cfg2
+    case = cfg2()
+    if args.n:
+        case = type(case)(n=args.n)
+    n_sample = min(case.n, 1 << 18)
+    from oracle import subspace
+    rng = np.random.default_rng(1)
+    r = case.r
+    phi = np.linalg.qr(rng.standard_normal((n_sample, r)))[0]
+    sig = np.linspace(10, 1, r)
+    for _ in range(args.warmup):
+        phi, sig, _ = subspace.isvd_update(phi, sig, rng.standard_normal(n_sample), case.lam, r)
+    ys = [rng.standard_normal(n_sample) for _ in range(args.steps)]
+    t0 = time.perf_counter()
+    for y in ys:
+        phi, sig, _ = subspace.isvd_update(phi, sig, y, case.lam, r)
+    dt = (time.perf_counter() - t0) / args.steps
+    value = (n_sample / case.n) / dt
+    return {
+        "metric": "iSVD rank-1 updates/s (N=2^22, r=64); iSVD % of HBM roofline",
+        "impl": "reference", "value": round(value, 6), "unit": "updates/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 / value, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": "cfg2-isvd-stream", "n": case.n, "r": r},
+        "cpu_baseline": {"value": round(value, 6), "unit": "updates/s", "cores": cpu_cores(),
+                         "kind": "port",
+                         "sample": f"oracle isvd_update (gelsd) at N={n_sample}, scaled to "
+                                   f"N={case.n}"},
+        "e2e": {"value": round(value, 6), "unit": "updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+# --------------------------------------------------------------------------- ROM loops
+
+def rom_case(name: str, n_override: int = 0):
+    from paper_2605_28684_b200 import configs
+    case = {"cfg0": configs.cfg0, "cfg1": configs.cfg1, "cfg3": configs.cfg3}[name]()
+    if n_override:
+        case = case.scaled(n_elem=n_override)
+    return case
+
+
+def rom_experiment(case):
+    import paper_2605_28684_b200 as P
+    cfg = P.ExperimentConfig(
+        model=case.model, n_elem=case.n_elem, nu=case.nu, gamma=case.gamma, dt=case.dt,
+        n_t=case.n_t, w_init=case.w_init, r=case.r, n_s=case.n_s, z=case.z,
+        rule=P.UpdateRule("isvd", lam=case.lam), projection=case.projection,
+        sampling=case.sampling, feature=case.feature, n_extra=case.n_extra)
+    ic = case.initial_state()
+    base = P.BurgersProblem if case.model == "burgers" else P.SodProblem
+
+    class Problem(base):  # the seeded IC of the case (driver.make_problem + custom IC)
+        def initial_state(self):
+            return ic.copy()
+
+    model = Problem(case.n_elem, nu=case.nu) if case.model == "burgers" else Problem(case.n_elem)
+    return cfg, model
+
+
+ROM_METRIC = "adaptive-ROM online steps/s; FOM residual Gcell/s and iSVD % of HBM roofline"
+
+
+def bench_rom(args, rank, world):
+    import torch
+    from paper_2605_28684_b200 import _lib
+    from paper_2605_28684_b200.driver import Session, offline_stage
+    case = rom_case(args.config, args.n)
+    cfg, model = rom_experiment(case)
+    K, W = args.steps, args.warmup
+    N, r = model.n_dof, case.r
+    if W + K > case.n_t - case.w_init:
+        raise SystemExit("steps + warmup exceed the online horizon")
+    t_off = time.perf_counter()
+    training, scaling, basis0 = offline_stage(cfg, model)
+    q_last = training[cfg.w_init].clone()
+    del training
+    torch.cuda.synchronize()
+    t_off = time.perf_counter() - t_off
+    ctx = _lib.Context.get()
+    sess = Session(cfg, model, adaptive=True)
+    sess.load(scaling, basis0, q_last)
+    t0 = time.perf_counter()
+    sess.start()  # driver.py:321-331 (first lookahead + sampling without pivot guesses)
+    torch.cuda.synchronize()
+    t_start = time.perf_counter() - t0
+    sess.advance(W)
+    torch.cuda.synchronize()
+    barrier(world)
+    ctx.prof_enable(True)
+    l0 = ctx.launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        torch.cuda.synchronize()
+        ev0.record()
+        sess.advance(K)
+        ev1.record()
+        torch.cuda.synchronize()
+    launches = ctx.launches() - l0
+    probes = ctx.prof_read()
+    ctx.prof_enable(False)
+    log, events, *_ = sess.read(W + K, W + K)
+    sess.close()
+    ms = max_over_ranks(ev0.elapsed_time(ev1), world)
+    barrier(world)
+    ms_step = ms / K
+    value = world * K / (ms * 1e-3)
+    per = {k: (v[0] / max(v[1], 1), v[1]) for k, v in probes.items()}
+    share = {k: round(v[0] / ms, 4) for k, v in probes.items()}
+    # dominant kernel by share of the step
+    dom = max(probes, key=lambda k: probes[k][0]) if probes else None
+    bytes_per = {
+        "isvd_rotate": 8.0 * (2 * N * r + N), "isvd_project": 8.0 * (N * r + N),
+        "isvd_resid": 8.0 * (N * r + N), "qdeim_scan": 8.0 * N * r, "decode": 8.0 * (N * r + 3 * N),
+        "encode": 8.0 * (N * r + 3 * N), "fom_residual": 8.0 * 3 * N,
+    }
+    roof = None
+    if dom in bytes_per:
+        roof = roofline(bytes_per[dom], per[dom][0])
+        roof["kernel"] = dom
+    isvd_keys = ("isvd_project", "isvd_resid", "isvd_core", "isvd_rotate")
+    isvd_ms = sum(probes.get(k, (0, 0))[0] for k in isvd_keys) / max(probes.get("isvd_rotate", (0, 1))[1], 1)
+    canon = 8.0 * (3 * N * r + 2 * N)
+    fres = per.get("fom_residual")
+    line = {
+        "metric": ROM_METRIC, "value": round(value, 3), "unit": "online steps/s", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded Burgers bump IC, configs.py)" if case.model == "burgers"
+                else "synthetic (Sod Riemann data)",
+        "config": {"workload": case.name, "n_elem": case.n_elem, "r": r, "n_s": case.n_s,
+                   "z": case.z, "lam": case.lam, "dt": case.dt, "projection": case.projection,
+                   "sampling": case.sampling,
+                   "l2": "inputs larger than L2 (basis %.1f GB)" % (8 * N * r / 1e9)
+                         if 8 * N * r > 126e6 else "working set L2-resident (latency-bound)",
+                   "parallelism": f"replicas{world}"},
+        "roofline": roof,
+        "gpu_launches": launches,
+        "fom_residual_gcells": round(model.n_elem / (fres[0] * 1e-3) / 1e9, 2) if fres else None,
+        "isvd_update_ms": round(isvd_ms, 4),
+        "isvd_update_hbm_frac": round(canon / (isvd_ms * 1e-3) / 1e9 / HBM_PEAK, 4) if isvd_ms else None,
+        "probes_ms_per_launch": {k: round(v[0], 4) for k, v in per.items()},
+        "probes_launches": {k: v[1] for k, v in per.items()},
+        "share_of_step": share,
+        "setup_s": {"offline": round(t_off, 3), "start": round(t_start, 3)},
+        "rom_iterations_mean": float(np.mean(log[:, 1])) if len(log) else None,
+        "event_errors": sum(1 for e in events if e.error),
+    }
+    line["clocks"] = clk.summary()
+    if rank == 0 and not args.no_e2e:
+        line["e2e"] = e2e_rom(args, case)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_rom(case, steps=3)
+    return line
+
+
+def e2e_rom(args, case):
+    """Online loop through the C-ABI session with HOST buffers: the offline
+    results (basis, scaling, last training state) are copied in from pinned
+    host memory inside the timed region and every step's decoded state is
+    copied back to pinned host memory (the reference keeps its trajectory on
+    the host, driver.py:306/344)."""
+    import torch
+    from paper_2605_28684_b200.driver import Session, offline_stage
+    cfg, model = rom_experiment(case)
+    K = min(args.steps, 10)
+    N, r = model.n_dof, case.r
+    training, scaling, basis0 = offline_stage(cfg, model)
+    pin = lambda x: x.detach().to("cpu").pin_memory()  # noqa: E731
+    h = dict(q_ref=pin(scaling.q_ref), d=pin(scaling.row_scale), phi=pin(basis0.phi),
+             sig=pin(basis0.sigma), q_last=pin(training[cfg.w_init]))
+    phi_norm = scaling.phi_norm
+    del training, scaling, basis0
+    out = torch.empty((K, N), dtype=torch.float64, pin_memory=True)
+    sess = Session(cfg, model, adaptive=True)
+    from paper_2605_28684_b200.snapshots import ScalingTransform
+    from paper_2605_28684_b200.tracking import ReducedBasis
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    d = {k: v.to("cuda", non_blocking=True) for k, v in h.items()}
+    sess.load(ScalingTransform(q_ref=d["q_ref"], phi_norm=phi_norm), ReducedBasis(d["phi"], d["sig"]),
+              d["q_last"])
+    sess.start()
+    sess.advance(K, 1, None, out)
+    sess.finish()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    sess.close()
+    h2d = sum(v.numel() * 8 for v in h.values())
+    return {"value": round(K / wall, 3), "unit": "online steps/s", "steps": K,
+            "h2d_bytes_per_step": int(h2d / K), "d2h_bytes_per_step": 8 * N,
+            "note": "timed region = reference's (driver.py:319-389) incl. start, "
+                    "plus H2D of the offline results; wall clock"}
+
+
+def cpu_baseline_rom(case, steps=3, n_sample=None, timed_steps=None):
+    """Oracle port of driver._run_rom on the host at a reduced grid (bounded
+    sample), scaled linearly in N to the case's grid (all per-step work of
+    the loop is O(N r) or O(N r^2))."""
+    from oracle import online, physics
+    n_sample = n_sample or min(case.n_elem, 1 << 14 if case.model == "sod" else 1 << 16)
+    small = case.scaled(n_elem=n_sample)
+    m = physics.Model(small.model, small.n_elem, nu=small.nu, gamma=small.gamma)
+    w_init = min(small.w_init, 64)
+    ocfg = online.LoopConfig(model=m, dt=small.dt, n_t=w_init + steps + 1, w_init=w_init, r=small.r,
+                             n_s=small.n_s, z=small.z, lam=small.lam, projection=small.projection,
+                             sampling=small.sampling, feature=small.feature, n_extra=small.n_extra)
+    training = online.training_states(ocfg, small.initial_state())
+    q_ref, d, phi0, sigma0 = online.offline(ocfg, training)
+    t0 = time.perf_counter()
+    online.run_online(ocfg, training, q_ref, d, phi0, sigma0, keep_stride=10 ** 9, n_steps=steps)
+    dt = time.perf_counter() - t0
+    per_step = dt / steps * (case.n_elem / n_sample)
+    return {"value": round(1.0 / per_step, 6), "unit": "online steps/s", "cores": cpu_cores(),
+            "kind": "port",
+            "sample": f"oracle online loop (numpy/scipy: gelsd iSVD, geqp3 QDEIM, sparse-LU "
+                      f"Newton) for {steps} steps at N={n_sample} (incl. start, w_init={w_init}); "
+                      f"{dt / steps:.3f} s/step scaled x{case.n_elem / n_sample:g} to N={case.n_elem}"}
+
+
+def reference_rom(args, rank, world):
+    if rank != 0:
+        return None
+    case = rom_case(args.config, args.n)
+    for _ in range(1):  # warm-up run (imports, BLAS threads)
+        cpu_baseline_rom(case, steps=1)
+    base = cpu_baseline_rom(case, steps=max(1, min(args.steps, 10)))
+    value = base["value"]
+    return {
+        "metric": ROM_METRIC, "impl": "reference", "value": value, "unit": "online steps/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 / value, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": case.name, "n_elem": case.n_elem, "r": case.r, "n_s": case.n_s,
+                   "z": case.z},
+        "cpu_baseline": base,
+        "e2e": {"value": value, "unit": "online steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+# --------------------------------------------------------------------------- main
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg3", choices=["cfg0", "cfg1", "cfg2", "cfg3"])
+    ap.add_argument("--n", type=int, default=0, help="override grid size (testing)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: the contract asks for >= 3 warm-up steps", file=sys.stderr)
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        fn = {"cfg2": reference_cfg2, "cfg0": reference_rom, "cfg1": reference_rom,
+              "cfg3": reference_rom}.get(args.config)
+        line = fn(args, rank, world) if fn else None
+        if rank == 0:
+            print(json.dumps(line if line else {"impl": "reference",
+                                                "unavailable": f"{args.config} not wired yet"}))
+        return 0
+    rank, world, _ = dist_setup()
+    fn = {"cfg2": bench_cfg2, "cfg0": bench_rom, "cfg1": bench_rom, "cfg3": bench_rom}[args.config]
+    line = fn(args, rank, world)
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -71,6 +71,22 @@ int adrom_ctx_set_stream(adrom_ctx* ctx, void* stream);
 void adrom_ctx_destroy(adrom_ctx* ctx);
 const char* adrom_ctx_last_error(const adrom_ctx* ctx);
 int adrom_ctx_synchronize(adrom_ctx* ctx);
+/* number of kernels this context has launched (bench.py's gpu_launches) */
+int64_t adrom_ctx_launch_count(const adrom_ctx* ctx);
+
+/* ---- timing probes ----------------------------------------------------- */
+/* CUDA-event probes around the library's kernels on the context stream
+ * (used by bench.py to time the dominant kernel inside the timed region). */
+enum adrom_probe {
+  ADROM_PROBE_ISVD_ROTATE = 0, ADROM_PROBE_ISVD_PROJECT = 1, ADROM_PROBE_ISVD_RESID = 2,
+  ADROM_PROBE_ISVD_CORE = 3, ADROM_PROBE_FOM_RESIDUAL = 4, ADROM_PROBE_FOM_JACOBIAN = 5,
+  ADROM_PROBE_FOM_SOLVE = 6, ADROM_PROBE_QDEIM_SCAN = 7, ADROM_PROBE_ROM_STEP = 8,
+  ADROM_PROBE_DECODE = 9, ADROM_PROBE_OPERATOR = 10, ADROM_PROBE_ENCODE = 11,
+  ADROM_PROBE_COUNT = 16
+};
+int adrom_prof_enable(adrom_ctx* ctx, int enable);
+/* host_ms[ADROM_PROBE_COUNT], host_count[ADROM_PROBE_COUNT]; resets probes */
+int adrom_prof_read(adrom_ctx* ctx, double* host_ms, int32_t* host_count);
 
 /* ---- full-order residual (kernel 1) ------------------------------------ */
 /* f = model.rhs(q)  — BurgersProblem.rhs fom.py:180-188, SodProblem.rhs
@@ -140,17 +156,138 @@ typedef struct adrom_isvd_info {
 } adrom_isvd_info;
 
 /* isvd_update (tracking.py:141-178):
+ *   p = Phi^+ y (gelsd least squares), q = y - Phi p,
  *   phi_out = [phi, q/||q||] U_core[:, :r],  sigma_out = s_core[:r]
- * phi: n x r_cur, phi_out: n x r (may alias phi when r <= r_cur).
+ * phi: n x r_cur, phi_out: n x r (may alias phi when r == r_cur).
+ * gram: optional device r_cur x r_cur matrix holding phi^T phi on entry and
+ * phi_out^T phi_out on exit (tracked across a stream of updates; NULL =
+ * computed afresh, one extra N r^2 pass).  The least-squares coefficients
+ * use it exactly like gelsd uses the basis' actual (not assumed) Gram.
  * host_info may be NULL (then the call does not synchronise). */
 int adrom_isvd_update(adrom_ctx* ctx, const double* phi, const double* sigma,
                       const double* y_hat, int64_t n, int32_t r_cur, int32_t r, double lam,
-                      double* phi_out, double* sigma_out, adrom_isvd_info* host_info);
+                      double* phi_out, double* sigma_out, double* gram,
+                      adrom_isvd_info* host_info);
+/* gram = phi^T phi (device r x r) */
+int adrom_gram(adrom_ctx* ctx, const double* phi, int64_t n, int32_t r, double* gram);
 
 /* thin_svd of a small dense matrix (dense.py:59-72), m x n row-major with
  * m, n <= 256, one thread block: u (m x k), s (k), v (n x k), k = min(m,n). */
 int adrom_small_svd(adrom_ctx* ctx, const double* a, int32_t m, int32_t n, double* u,
                     double* s, double* v);
+
+/* ---- hyper-reduction sampling + reduced operator ----------------------- */
+/* qdeim_sample (sampling.py:107-114): first n_s pivots of the restarted
+ * column-pivoted QR of phi^T (exact greedy, ties to the lowest row).
+ * idx: device int64[n_s]. Blocking. */
+int adrom_qdeim(adrom_ctx* ctx, const double* phi, int64_t n, int32_t r, int32_t n_s,
+                int64_t* idx);
+
+/* fgs_sample (sampling.py:117-159): QDEIM rows for n_s - n_extra, then the
+ * cells with the largest |grad feature(y_corr)| (feature 0 = pressure-,
+ * 1 = velocity-gradient), all variables, skipping duplicates. Blocking. */
+int adrom_fgs(adrom_ctx* ctx, const adrom_model* m, const double* phi, int32_t r,
+              const double* y_corr, int32_t n_s, int32_t n_extra, int32_t feature,
+              int64_t* idx);
+
+/* build_deim_operator (sampling.py:162-175): pinv = (phi[idx, :])^+, r x n_s
+ * row-major; rank deficiency (s_min <= 1e-12 s_max) -> ADROM_ERR_SINGULAR. */
+int adrom_deim_operator(adrom_ctx* ctx, const double* phi, int64_t n, int32_t r, const int64_t* idx,
+                        int32_t n_s, double* pinv);
+
+/* Device-resident reduced operator (projection.py:57-87 RomOperator +
+ * fom.py:119-158 SamplingPlan).  All pointers are device buffers allocated
+ * by the caller with the listed capacities; sizes[] is written by the build:
+ * sizes[0] = n_s, sizes[1] = closure length, sizes[2] = sampled cells. */
+typedef struct adrom_rom_op {
+  int32_t r, n_var;
+  int32_t ns_cap;     /* >= n_s                                  */
+  int32_t nc_cap;     /* >= 3 * n_s * n_var  (closure rows)       */
+  int32_t ncell_cap;  /* >= n_s                                  */
+  int32_t pad;
+  int64_t* idx;        /* [ns_cap] sampled rows, sampling order      */
+  int64_t* closure;    /* [nc_cap] sorted closure rows               */
+  int64_t* gather;     /* [ncell_cap * 3 * n_var] closure positions  */
+  int64_t* out_cell;   /* [ns_cap]                                  */
+  int64_t* out_var;    /* [ns_cap]                                  */
+  int64_t* sample_pos; /* [ns_cap]                                  */
+  int32_t* sizes;      /* [4]                                       */
+  double* pinv;        /* [r * ns_cap] (P^T Phi)^+, row-major r x n_s */
+  double* d_s;         /* [ns_cap]                                  */
+  double* q_ref_c;     /* [nc_cap]                                  */
+  double* dinv_phi_c;  /* [nc_cap * r]                              */
+  double* phi_s;       /* [ns_cap * r]                              */
+} adrom_rom_op;
+
+/* stencil_closure (sampling.py:178-189) + build_rom_operator
+ * (projection.py:61-80, build_deim_operator sampling.py:162-175) for the
+ * rows op->idx[0..n_s) (copied from `idx` if non-NULL).  Blocking. */
+int adrom_rom_operator_build(adrom_ctx* ctx, const adrom_model* m, const double* phi, int64_t n,
+                             const double* q_ref, const double* d, const int64_t* idx,
+                             int32_t n_s, adrom_rom_op* op);
+
+typedef struct adrom_rom_step_info {
+  int32_t converged;   /* RomStepResult.converged (projection.py:50-54) */
+  int32_t iterations;
+  double residual_norm;
+} adrom_rom_step_info;
+
+/* rom_step (projection.py:217-221): kind 0 = lspg_step (158-204),
+ * 1 = galerkin_step (111-147).  a_out may alias a_prev.  Blocking. */
+int adrom_rom_step(adrom_ctx* ctx, const adrom_model* m, const adrom_rom_op* op, int32_t kind,
+                   const double* a_prev, double dt, double tol, int32_t max_iter, double* a_out,
+                   adrom_rom_step_info* host_info);
+
+/* ---- device-resident online loop (driver.py:291-410) ------------------- */
+/* The fields of ExperimentConfig (driver.py:63-91) the online loop reads. */
+typedef struct adrom_session_config {
+  adrom_model model;
+  int32_t r, n_s, n_extra, z;
+  int32_t projection;       /* 0 = lspg, 1 = galerkin                      */
+  int32_t sampling;         /* 0 = qdeim, 1 = fgs                          */
+  int32_t feature;          /* 0 = pressure-gradient, 1 = velocity-gradient */
+  int32_t adaptive;         /* 1 = run_adaptive_rom (iSVD), 0 = static     */
+  int32_t newton_max_iter;  /* also the reduced steps' max_iter            */
+  int32_t pad;
+  int64_t w_init, n_t;
+  double dt, lam, newton_tol;
+} adrom_session_config;
+
+/* one adaptation event (driver.py:351-387 event dict) */
+typedef struct adrom_event_record {
+  int64_t step;              /* event["step"]                                  */
+  int32_t coarse_converged;  /* event["coarse_converged"]                      */
+  int32_t coarse_iterations; /* event["coarse_iterations"]                     */
+  double residual_norm;      /* event["residual_norm"]                         */
+  int32_t error;             /* 0, or the adrom_status of event["update_error"] */
+  int32_t pad;
+} adrom_event_record;
+
+typedef struct adrom_session adrom_session;
+
+int adrom_session_create(adrom_ctx* ctx, const adrom_session_config* cfg, adrom_session** out);
+void adrom_session_destroy(adrom_session* s);
+/* offline results (device): q_ref, row scale d, POD basis phi0 (N x r),
+ * sigma0 (r) and q_last = training[w_init] (driver.py:296-300). */
+int adrom_session_load(adrom_session* s, const double* q_ref, const double* d, const double* phi0,
+                       const double* sigma0, const double* q_last);
+/* driver.py:321-331 (start of the timed region): lookahead, sampling,
+ * operator, encode. */
+int adrom_session_start(adrom_session* s);
+/* driver.py:337-387 for n_steps fine steps; every save_every-th decoded
+ * state is copied to dev_out and/or host_out (pinned).  A reduced-step
+ * failure returns ADROM_ERR_ROMSTEP like the reference. */
+int adrom_session_advance(adrom_session* s, int64_t n_steps, int64_t save_every, double* dev_out,
+                          double* host_out, int64_t* n_saved);
+int adrom_session_finish(adrom_session* s);
+/* logs and current state; host_step_log is n_steps x [converged,
+ * iterations, residual_norm]; dev_* may be NULL. */
+int adrom_session_read(adrom_session* s, double* host_step_log, int64_t max_steps,
+                       adrom_event_record* host_events, int64_t max_events, int64_t* n_steps,
+                       int64_t* n_events, double* dev_a, double* dev_phi, double* dev_sigma,
+                       double* dev_q_tilde);
+/* current sampled rows (device int64[n_s]) */
+int adrom_session_sampling(adrom_session* s, int64_t* dev_idx);
 
 #ifdef __cplusplus
 }

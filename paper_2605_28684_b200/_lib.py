@@ -41,6 +41,34 @@ class IsvdInfo(C.Structure):
                 ("degenerate", _i32), ("reorthogonalised", _i32), ("sweeps", _i32), ("pad", _i32)]
 
 
+class RomOp(C.Structure):
+    """``adrom_rom_op`` — device buffers of a reduced operator."""
+
+    _fields_ = [("r", _i32), ("n_var", _i32), ("ns_cap", _i32), ("nc_cap", _i32),
+                ("ncell_cap", _i32), ("pad", _i32),
+                ("idx", _p), ("closure", _p), ("gather", _p), ("out_cell", _p),
+                ("out_var", _p), ("sample_pos", _p), ("sizes", _p),
+                ("pinv", _p), ("d_s", _p), ("q_ref_c", _p), ("dinv_phi_c", _p), ("phi_s", _p)]
+
+
+class RomStepInfo(C.Structure):
+    _fields_ = [("converged", _i32), ("iterations", _i32), ("residual_norm", _f64)]
+
+
+class SessionConfig(C.Structure):
+    """``adrom_session_config``."""
+
+    _fields_ = [("model", Model), ("r", _i32), ("n_s", _i32), ("n_extra", _i32), ("z", _i32),
+                ("projection", _i32), ("sampling", _i32), ("feature", _i32), ("adaptive", _i32),
+                ("newton_max_iter", _i32), ("pad", _i32), ("w_init", _i64), ("n_t", _i64),
+                ("dt", _f64), ("lam", _f64), ("newton_tol", _f64)]
+
+
+class EventRecord(C.Structure):
+    _fields_ = [("step", _i64), ("coarse_converged", _i32), ("coarse_iterations", _i32),
+                ("residual_norm", _f64), ("error", _i32), ("pad", _i32)]
+
+
 # name -> (restype, argtypes)
 SIGNATURES = {
     "adrom_abi_version": (_i32, []),
@@ -49,6 +77,9 @@ SIGNATURES = {
     "adrom_ctx_destroy": (None, [_p]),
     "adrom_ctx_last_error": (C.c_char_p, [_p]),
     "adrom_ctx_synchronize": (_i32, [_p]),
+    "adrom_ctx_launch_count": (_i64, [_p]),
+    "adrom_prof_enable": (_i32, [_p, _i32]),
+    "adrom_prof_read": (_i32, [_p, C.POINTER(_f64), C.POINTER(_i32)]),
     "adrom_rhs": (_i32, [_p, C.POINTER(Model), _p, _p]),
     "adrom_rhs_at_cells": (_i32, [_p, C.POINTER(Model), _p, _i64, _p]),
     "adrom_plan_evaluate": (_i32, [_p, C.POINTER(Model), _p, _i64, _p, _p, _i64, _p, _p, _p,
@@ -59,10 +90,30 @@ SIGNATURES = {
     "adrom_project": (_i32, [_p, _p, _p, _i64, _i32, _p]),
     "adrom_encode": (_i32, [_p, _p, _p, _p, _p, _i64, _i32, _p]),
     "adrom_decode": (_i32, [_p, _p, _p, _p, _p, _i64, _i32, _p]),
-    "adrom_isvd_update": (_i32, [_p, _p, _p, _p, _i64, _i32, _i32, _f64, _p, _p,
+    "adrom_isvd_update": (_i32, [_p, _p, _p, _p, _i64, _i32, _i32, _f64, _p, _p, _p,
                                  C.POINTER(IsvdInfo)]),
+    "adrom_gram": (_i32, [_p, _p, _i64, _i32, _p]),
     "adrom_small_svd": (_i32, [_p, _p, _i32, _i32, _p, _p, _p]),
+    "adrom_qdeim": (_i32, [_p, _p, _i64, _i32, _i32, _p]),
+    "adrom_fgs": (_i32, [_p, C.POINTER(Model), _p, _i32, _p, _i32, _i32, _i32, _p]),
+    "adrom_deim_operator": (_i32, [_p, _p, _i64, _i32, _p, _i32, _p]),
+    "adrom_rom_operator_build": (_i32, [_p, C.POINTER(Model), _p, _i64, _p, _p, _p, _i32,
+                                        C.POINTER(RomOp)]),
+    "adrom_rom_step": (_i32, [_p, C.POINTER(Model), C.POINTER(RomOp), _i32, _p, _f64, _f64,
+                              _i32, _p, C.POINTER(RomStepInfo)]),
+    "adrom_session_create": (_i32, [_p, C.POINTER(SessionConfig), C.POINTER(_p)]),
+    "adrom_session_destroy": (None, [_p]),
+    "adrom_session_load": (_i32, [_p, _p, _p, _p, _p, _p]),
+    "adrom_session_start": (_i32, [_p]),
+    "adrom_session_advance": (_i32, [_p, _i64, _i64, _p, _p, C.POINTER(_i64)]),
+    "adrom_session_finish": (_i32, [_p]),
+    "adrom_session_read": (_i32, [_p, _p, _i64, _p, _i64, C.POINTER(_i64), C.POINTER(_i64),
+                                  _p, _p, _p, _p]),
+    "adrom_session_sampling": (_i32, [_p, _p]),
 }
+
+PROBES = ["isvd_rotate", "isvd_project", "isvd_resid", "isvd_core", "fom_residual",
+          "fom_jacobian", "fom_solve", "qdeim_scan", "rom_step", "decode", "operator", "encode"]
 
 _lib = None
 _lock = threading.Lock()
@@ -152,8 +203,24 @@ class Context:
     def call(self, name: str, *args):
         self.check(getattr(self.lib, name)(self.handle, *args), name)
 
+    def scall(self, name: str, session, *args):
+        """Call a session entry point (first argument is the session handle)."""
+        self.check(getattr(self.lib, name)(session, *args), name)
+
     def sync(self):
         self.call("adrom_ctx_synchronize")
+
+    def launches(self) -> int:
+        return int(self.lib.adrom_ctx_launch_count(self.handle))
+
+    def prof_enable(self, on: bool = True):
+        self.call("adrom_prof_enable", _i32(1 if on else 0))
+
+    def prof_read(self) -> dict:
+        ms = (_f64 * 16)()
+        cnt = (_i32 * 16)()
+        self.call("adrom_prof_read", ms, cnt)
+        return {PROBES[i]: (ms[i], cnt[i]) for i in range(len(PROBES)) if cnt[i]}
 
 
 def ptr(t) -> _p:

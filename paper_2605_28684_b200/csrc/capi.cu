@@ -62,13 +62,13 @@ int adrom_implicit_step(adrom_ctx* ctx, const adrom_model* m, const double* q, d
 int adrom_project(adrom_ctx* ctx, const double* phi, const double* x, int64_t n, int32_t r,
                   double* out) {
   if (!ctx) return ADROM_ERR_ARG;
-  const size_t need = align_up(sizeof(double) * (size_t)ctx->num_sms * 3 * (r + 1)) +
+  const size_t need = align_up(sizeof(double) * (size_t)adrom::partial_rows(ctx) * (r + 1)) +
                       align_up(sizeof(double) * (r + 1));
   int st = ensure_scratch(ctx, need);
   if (st) return st;
   double* partial = (double*)ctx->scratch;
   double* tmp = (double*)((char*)ctx->scratch +
-                          align_up(sizeof(double) * (size_t)ctx->num_sms * 3 * (r + 1)));
+                          align_up(sizeof(double) * (size_t)adrom::partial_rows(ctx) * (r + 1)));
   st = ts_project(ctx, phi, n, r, 1, x, nullptr, nullptr, tmp, partial, nullptr);
   if (st) return st;
   ADROM_CK(ctx, cudaMemcpyAsync(out, tmp, sizeof(double) * r, cudaMemcpyDeviceToDevice,
@@ -79,7 +79,7 @@ int adrom_project(adrom_ctx* ctx, const double* phi, const double* x, int64_t n,
 int adrom_encode(adrom_ctx* ctx, const double* phi, const double* q_ref, const double* d,
                  const double* q, int64_t n, int32_t r, double* a) {
   if (!ctx) return ADROM_ERR_ARG;
-  const size_t pb = align_up(sizeof(double) * (size_t)ctx->num_sms * 3 * (r + 1));
+  const size_t pb = align_up(sizeof(double) * (size_t)adrom::partial_rows(ctx) * (r + 1));
   int st = ensure_scratch(ctx, pb + align_up(sizeof(double) * (r + 1)));
   if (st) return st;
   double* partial = (double*)ctx->scratch;
@@ -97,18 +97,26 @@ int adrom_decode(adrom_ctx* ctx, const double* phi, const double* q_ref, const d
   return ts_decode(ctx, phi, n, r, a, q_ref, d, q);
 }
 
+int adrom_gram(adrom_ctx* ctx, const double* phi, int64_t n, int32_t r, double* gram) {
+  if (!ctx) return ADROM_ERR_ARG;
+  int st = ensure_scratch(ctx, sizeof(double) * 2 * (size_t)partial_rows(ctx) * (r + 1) + 4096);
+  if (st) return st;
+  return ts_gram(ctx, phi, n, r, gram, (double*)ctx->scratch);
+}
+
 int adrom_isvd_update(adrom_ctx* ctx, const double* phi, const double* sigma,
                       const double* y_hat, int64_t n, int32_t r_cur, int32_t r, double lam,
-                      double* phi_out, double* sigma_out, adrom_isvd_info* host_info) {
+                      double* phi_out, double* sigma_out, double* gram,
+                      adrom_isvd_info* host_info) {
   if (!ctx) return ADROM_ERR_ARG;
   int st = ensure_scratch(ctx, isvd_workspace_bytes(ctx, n, r_cur, r) + 4096);
   if (st) return st;
   st = reset_flags(ctx);
   if (st) return st;
   double* stats = (double*)((char*)ctx->scratch + isvd_workspace_bytes(ctx, n, r_cur, r));
-  st = isvd_update_async(ctx, phi, sigma, y_hat, n, r_cur, r, lam, phi_out, sigma_out,
-                         ctx->scratch, ctx->dflags, ISVD_REORTH_RATIO, stats, nullptr, nullptr,
-                         nullptr, nullptr);
+  st = isvd_update_async(ctx, phi, sigma, y_hat, n, r_cur, r, lam, phi_out, sigma_out, gram,
+                         gram, ctx->scratch, ctx->dflags, ISVD_REORTH_RATIO, stats, nullptr,
+                         nullptr, nullptr, nullptr);
   if (st) return st;
   int flags[16];
   ADROM_CK(ctx, cudaMemcpyAsync((char*)ctx->pinned + 256, stats, sizeof(double) * 8,

@@ -88,7 +88,16 @@ struct adrom_ctx {
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
   char err[512] = {0};
+  // kernel timing probes (CUDA events on ctx->stream), see adrom_prof_*
+  bool prof = false;
+  int prof_used = 0;
+  cudaEvent_t* prof_ev = nullptr;  // 2 * ADROM_PROF_SLOTS events
+  int* prof_id = nullptr;          // probe id per slot
+  long long launches = 0;          // kernels launched through this context
 };
+
+#define ADROM_PROF_SLOTS 8192
+#define ADROM_PROF_IDS 16
 
 namespace adrom {
 
@@ -100,6 +109,27 @@ void* scratch(adrom_ctx* ctx, size_t bytes, size_t offset_bytes = 0);
 int ensure_scratch(adrom_ctx* ctx, size_t bytes);
 int ensure_pinned(adrom_ctx* ctx, size_t bytes);
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+// upper bound on the blocks of any reduction kernel (rows of a partials buffer)
+inline int partial_rows(const adrom_ctx* ctx) { return ctx->num_sms * 4; }
+
+// probe ids (adrom_prof_read)
+enum ProbeId {
+  PROBE_ISVD_ROTATE = 0,
+  PROBE_ISVD_PROJECT = 1,
+  PROBE_ISVD_RESID = 2,
+  PROBE_ISVD_CORE = 3,
+  PROBE_FOM_RESIDUAL = 4,
+  PROBE_FOM_JACOBIAN = 5,
+  PROBE_FOM_SOLVE = 6,
+  PROBE_QDEIM_SCAN = 7,
+  PROBE_ROM_STEP = 8,
+  PROBE_DECODE = 9,
+  PROBE_OPERATOR = 10,
+  PROBE_ENCODE = 11,
+};
+// record a begin / end event for probe `id` (no-op unless profiling)
+int prof_begin(adrom_ctx* ctx, int id);
+void prof_end(adrom_ctx* ctx, int slot);
 
 }  // namespace adrom
 
@@ -109,4 +139,8 @@ inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
     if (_e != cudaSuccess) return adrom::check_cuda(ctx, _e, #call); \
   } while (0)
 
-#define ADROM_LAUNCH_CK(ctx) ADROM_CK(ctx, cudaGetLastError())
+#define ADROM_LAUNCH_CK(ctx)               \
+  do {                                     \
+    ++(ctx)->launches;                     \
+    ADROM_CK(ctx, cudaGetLastError());     \
+  } while (0)

@@ -55,11 +55,61 @@ int ensure_pinned(adrom_ctx* ctx, size_t bytes) {
   return ADROM_OK;
 }
 
+int prof_begin(adrom_ctx* ctx, int id) {
+  if (!ctx->prof || ctx->prof_used >= ADROM_PROF_SLOTS) return -1;
+  const int slot = ctx->prof_used++;
+  ctx->prof_id[slot] = id;
+  cudaEventRecord(ctx->prof_ev[2 * slot], ctx->stream);
+  return slot;
+}
+
+void prof_end(adrom_ctx* ctx, int slot) {
+  if (slot < 0) return;
+  cudaEventRecord(ctx->prof_ev[2 * slot + 1], ctx->stream);
+}
+
 }  // namespace adrom
 
 extern "C" {
 
+int adrom_prof_enable(adrom_ctx* ctx, int enable) {
+  if (!ctx) return ADROM_ERR_ARG;
+  if (enable && !ctx->prof_ev) {
+    ctx->prof_ev = new cudaEvent_t[2 * ADROM_PROF_SLOTS];
+    ctx->prof_id = new int[ADROM_PROF_SLOTS];
+    for (int i = 0; i < 2 * ADROM_PROF_SLOTS; ++i)
+      ADROM_CK(ctx, cudaEventCreate(&ctx->prof_ev[i]));
+  }
+  ctx->prof = enable != 0;
+  ctx->prof_used = 0;
+  return ADROM_OK;
+}
+
+int adrom_prof_read(adrom_ctx* ctx, double* host_ms, int32_t* host_count) {
+  if (!ctx) return ADROM_ERR_ARG;
+  for (int i = 0; i < ADROM_PROF_IDS; ++i) {
+    host_ms[i] = 0.0;
+    host_count[i] = 0;
+  }
+  if (!ctx->prof_ev) return ADROM_OK;
+  ADROM_CK(ctx, cudaStreamSynchronize(ctx->stream));
+  for (int s = 0; s < ctx->prof_used; ++s) {
+    float ms = 0.f;
+    ADROM_CK(ctx, cudaEventElapsedTime(&ms, ctx->prof_ev[2 * s], ctx->prof_ev[2 * s + 1]));
+    const int id = ctx->prof_id[s];
+    if (id >= 0 && id < ADROM_PROF_IDS) {
+      host_ms[id] += ms;
+      host_count[id] += 1;
+    }
+  }
+  ctx->prof_used = 0;
+  return ADROM_OK;
+}
+
+
 int adrom_abi_version(void) { return ADROM_ABI_VERSION; }
+
+int64_t adrom_ctx_launch_count(const adrom_ctx* ctx) { return ctx ? (int64_t)ctx->launches : 0; }
 
 int adrom_ctx_create(adrom_ctx** out, void* stream) {
   if (!out) return ADROM_ERR_ARG;
@@ -102,6 +152,11 @@ void adrom_ctx_destroy(adrom_ctx* ctx) {
   if (ctx->scratch) cudaFree(ctx->scratch);
   if (ctx->dflags) cudaFree(ctx->dflags);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->prof_ev) {
+    for (int i = 0; i < 2 * ADROM_PROF_SLOTS; ++i) cudaEventDestroy(ctx->prof_ev[i]);
+    delete[] ctx->prof_ev;
+    delete[] ctx->prof_id;
+  }
   delete ctx;
 }
 

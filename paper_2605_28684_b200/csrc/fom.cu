@@ -394,7 +394,10 @@ static int launch_residual(adrom_ctx* ctx, const adrom_model& m, const double* x
 int fom_rhs(adrom_ctx* ctx, const adrom_model& m, const double* q, double* f) {
   int st = check_model(ctx, m);
   if (st) return st;
-  return launch_residual(ctx, m, q, f, false, nullptr, 0.0, nullptr, nullptr, nullptr);
+  const int pr = prof_begin(ctx, PROBE_FOM_RESIDUAL);
+  st = launch_residual(ctx, m, q, f, false, nullptr, 0.0, nullptr, nullptr, nullptr);
+  prof_end(ctx, pr);
+  return st;
 }
 
 int fom_rhs_at_cells(adrom_ctx* ctx, const adrom_model& m, const double* gathered, int64_t k,
@@ -494,7 +497,9 @@ int fom_implicit_step(adrom_ctx* ctx, const adrom_model& m, const double* q, dou
 
   auto residual_norm = [&](double* rn) -> int {
     int nb = 0;
+    const int pr = prof_begin(ctx, PROBE_FOM_RESIDUAL);
     int s2 = launch_residual(ctx, m, x, r, true, q, dt, partial, flag, &nb);
+    prof_end(ctx, pr);
     if (s2) return s2;
     sum_partials_kernel<<<1, 256, 0, ctx->stream>>>(partial, nb, sums);
     ADROM_LAUNCH_CK(ctx);
@@ -514,10 +519,14 @@ int fom_implicit_step(adrom_ctx* ctx, const adrom_model& m, const double* q, dou
       if (info) *info = adrom_newton_info{1, it, rn};
       return ADROM_OK;
     }
+    int pr = prof_begin(ctx, PROBE_FOM_JACOBIAN);
     st = launch_jacobian(ctx, m, x, A, true, dt, flag);
+    prof_end(ctx, pr);
     if (st) return st;
     // solve (I - dt J) delta = -r, then x += delta
+    pr = prof_begin(ctx, PROBE_FOM_SOLVE);
     st = bt_solve(ctx, A, r, -1.0, m.n_elem, m.n_var, m.kind == ADROM_BURGERS, delta, btws, flag);
+    prof_end(ctx, pr);
     if (st) return st;
     axpy1_kernel<<<grid_for(ctx, N, 256), 256, 0, ctx->stream>>>(x, delta, N);
     ADROM_LAUNCH_CK(ctx);

@@ -21,9 +21,17 @@ struct JacobiResult {
 };
 
 // All threads of the block must call.  blockDim.x must be a multiple of 32.
+// Each column pair of a round is handled by one half-warp (16 lanes), so up
+// to blockDim/16 pairs rotate concurrently and a round costs one barrier.
+__device__ __forceinline__ double hw_sum(double v) {
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, 16);
+  return v;
+}
+
 __device__ inline JacobiResult block_jacobi(double* A, int lda, int m, int n, double* V, int ldv,
                                             int max_sweeps, double tol, int* sh_flag) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int tid = threadIdx.x, hl = tid & 15, hw = tid >> 4, nhw = blockDim.x >> 4;
   for (int e = tid; e < n * n; e += blockDim.x) {
     const int c = e / n, rr = e - c * n;
     V[c * ldv + rr] = (c == rr) ? 1.0 : 0.0;
@@ -39,8 +47,11 @@ __device__ inline JacobiResult block_jacobi(double* A, int lda, int m, int n, do
     if (tid == 0) *sh_flag = 0;
     __syncthreads();
     for (int round = 0; round < ne - 1; ++round) {
-      for (int pr = warp; pr < ne / 2; pr += nw) {
-        int a, b;
+      // pb is warp-uniform so both half-warps run the same iterations (the
+      // 16-wide shuffles below are issued with the full warp mask)
+      for (int pb = (hw & ~1); pb < ne / 2; pb += nhw) {
+        const int pr = pb + (hw & 1);
+        int a = 0, b = 0;
         if (pr == 0) {
           a = round;
           b = ne - 1;
@@ -48,43 +59,45 @@ __device__ inline JacobiResult block_jacobi(double* A, int lda, int m, int n, do
           a = (round + pr) % (ne - 1);
           b = (round - pr + ne - 1) % (ne - 1);
         }
-        if (a >= n || b >= n) continue;
+        const bool live = (pr < ne / 2) && (a < n && b < n);
         if (a > b) {
           const int t = a;
           a = b;
           b = t;
         }
+        double al = 0.0, be = 0.0, ga = 0.0;
         double* ca = A + (size_t)a * lda;
         double* cb = A + (size_t)b * lda;
-        double al = 0.0, be = 0.0, ga = 0.0;
-        for (int i = lane; i < m; i += 32) {
-          const double x = ca[i], y = cb[i];
-          al += x * x;
-          be += y * y;
-          ga += x * y;
+        if (live) {
+          for (int i = hl; i < m; i += 16) {
+            const double x = ca[i], y = cb[i];
+            al += x * x;
+            be += y * y;
+            ga += x * y;
+          }
         }
-        al = warp_sum(al);
-        be = warp_sum(be);
-        ga = warp_sum(ga);
-        if (al == 0.0 || be == 0.0) continue;
-        if (!(fabs(ga) > tol * sqrt(al) * sqrt(be))) continue;
+        al = hw_sum(al);
+        be = hw_sum(be);
+        ga = hw_sum(ga);
+        if (!live || al == 0.0 || be == 0.0) continue;
+        if (!(fabs(ga) > tol * sqrt(al * be))) continue;
         const double zeta = (be - al) / (2.0 * ga);
         const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
         const double c = 1.0 / sqrt(1.0 + t * t);
         const double s = c * t;
-        for (int i = lane; i < m; i += 32) {
+        for (int i = hl; i < m; i += 16) {
           const double x = ca[i], y = cb[i];
           ca[i] = c * x - s * y;
           cb[i] = s * x + c * y;
         }
         double* va = V + (size_t)a * ldv;
         double* vb = V + (size_t)b * ldv;
-        for (int i = lane; i < n; i += 32) {
+        for (int i = hl; i < n; i += 16) {
           const double x = va[i], y = vb[i];
           va[i] = c * x - s * y;
           vb[i] = s * x + c * y;
         }
-        if (lane == 0) *sh_flag = 1;
+        if (hl == 0) *sh_flag = 1;
       }
       __syncthreads();
     }
@@ -111,11 +124,12 @@ __device__ inline void column_norms_sorted(const double* A, int lda, int m, int 
     if (lane == 0) s[j] = sqrt(a);
   }
   __syncthreads();
+  // total order (NaN sorts last) so `order` is always a permutation
   for (int j = threadIdx.x; j < n; j += blockDim.x) {
     int rank = 0;
-    const double sj = s[j];
+    const double sj = isnan(s[j]) ? -1.0 : s[j];
     for (int k = 0; k < n; ++k) {
-      const double sk = s[k];
+      const double sk = isnan(s[k]) ? -1.0 : s[k];
       if (sk > sj || (sk == sj && k < j)) ++rank;
     }
     order[rank] = j;

@@ -39,6 +39,7 @@ struct TileArgs {
   const double* d;      // row scale
   double* out_q;        // decode output
   double* partial;      // gridDim.x x (r+1)
+  double* out_w;        // if non-null: out_w[i] = w_i (the iSVD residual q)
   int* flag;            // bit 0: non-finite basis / input
   const int* skip;      // if non-null and *skip == 0 the kernel is a no-op
 };
@@ -94,6 +95,7 @@ __global__ void __launch_bounds__(TS_NT) tile_kernel(TileArgs a) {
         bad |= !isfinite(w);
         sacc += w * w;
         ww[tid] = w;
+        if (a.out_w) a.out_w[i] = w;
       }
     }
     if (WKIND != W_NONE) {
@@ -133,6 +135,142 @@ __global__ void reduce_partials_kernel(const double* __restrict__ partial, int n
   for (int b = threadIdx.x; b < nb; b += blockDim.x) s += partial[(size_t)b * w + j];
   s = block_sum<256>(s, red);
   if (threadIdx.x == 0) out[j] = s;
+}
+
+
+// ---------------------------------------------------------------------------
+// streaming variant for r in {16, 32, 64, 128}: one row per LPR lanes,
+// 16-byte loads straight from global (no smem staging), U rows in flight per
+// lane.  Same semantics as tile_kernel.
+// ---------------------------------------------------------------------------
+template <int R, bool ROWDOT, bool DECODE, int WKIND>
+__global__ void __launch_bounds__(256) stream_kernel(TileArgs a) {
+  constexpr int LPR = (R >= 64) ? 32 : R / 2;  // lanes per row
+  constexpr int VPL = R / LPR;                 // doubles per lane (2 or 4)
+  constexpr int RPW = 32 / LPR;                // rows per warp per sub-iteration
+  constexpr int U = 4;                         // sub-iterations in flight
+  __shared__ double red[8 * R];
+  __shared__ double sred[32];
+  if (a.skip && *a.skip == 0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int seg = lane / LPR, sl = lane - seg * LPR;
+  // lane columns: 2sl, 2sl+1 and (VPL == 4) 2sl+2LPR, 2sl+2LPR+1
+  double vv[VPL];
+  if (ROWDOT) {
+#pragma unroll
+    for (int h = 0; h < VPL / 2; ++h) {
+      vv[2 * h] = a.v[2 * sl + 2 * LPR * h];
+      vv[2 * h + 1] = a.v[2 * sl + 2 * LPR * h + 1];
+    }
+  }
+  double acc[VPL];
+#pragma unroll
+  for (int c = 0; c < VPL; ++c) acc[c] = 0.0;
+  double sacc = 0.0;
+  bool bad = false;
+  const int64_t total_warps = (int64_t)gridDim.x * 8;
+  const int64_t rows_per_iter = (int64_t)RPW * U;
+  for (int64_t g = (int64_t)blockIdx.x * 8 + warp; g * rows_per_iter < a.n; g += total_warps) {
+    const int64_t base = g * rows_per_iter;
+    double2 val[U][VPL / 2];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + u * RPW + seg;
+      if (i < a.n) {
+        const double2* rowp = reinterpret_cast<const double2*>(a.phi + i * R);
+#pragma unroll
+        for (int h = 0; h < VPL / 2; ++h) val[u][h] = rowp[sl + LPR * h];
+      } else {
+#pragma unroll
+        for (int h = 0; h < VPL / 2; ++h) val[u][h] = make_double2(0.0, 0.0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + u * RPW + seg;
+      const bool live = i < a.n;
+      double rd = 0.0;
+#pragma unroll
+      for (int h = 0; h < VPL / 2; ++h) {
+        bad |= !(isfinite(val[u][h].x) && isfinite(val[u][h].y));
+        if (ROWDOT) rd += val[u][h].x * vv[2 * h] + val[u][h].y * vv[2 * h + 1];
+      }
+      if (ROWDOT) {
+#pragma unroll
+        for (int o = LPR / 2; o > 0; o >>= 1) rd += __shfl_xor_sync(0xffffffffu, rd, o);
+      }
+      if (DECODE && live && sl == 0) a.out_q[i] = a.q_ref[i] + rd / a.d[i];
+      if (WKIND != W_NONE && live) {
+        double w;
+        if (WKIND == W_X) w = a.x[i];
+        else if (WKIND == W_ENCODE) w = a.d[i] * (a.x[i] - a.q_ref[i]);
+        else w = a.x[i] - rd;
+        bad |= !isfinite(w);
+        if (sl == 0) {
+          sacc += w * w;
+          if (a.out_w) a.out_w[i] = w;
+        }
+#pragma unroll
+        for (int h = 0; h < VPL / 2; ++h) {
+          acc[2 * h] += val[u][h].x * w;
+          acc[2 * h + 1] += val[u][h].y * w;
+        }
+      }
+    }
+  }
+  if (WKIND == W_NONE) {
+    if (bad && a.flag) atomicOr(a.flag, 1);
+    return;
+  }
+  // fold segments sharing columns, then warps
+#pragma unroll
+  for (int o = LPR; o < 32; o <<= 1)
+#pragma unroll
+    for (int c = 0; c < VPL; ++c) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+  if (seg == 0) {
+#pragma unroll
+    for (int h = 0; h < VPL / 2; ++h) {
+      red[warp * R + 2 * sl + 2 * LPR * h] = acc[2 * h];
+      red[warp * R + 2 * sl + 2 * LPR * h + 1] = acc[2 * h + 1];
+    }
+  }
+  __syncthreads();
+  double* out = a.partial + (size_t)blockIdx.x * (R + 1);
+  for (int c = threadIdx.x; c < R; c += 256) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s += red[w * R + c];
+    out[c] = s;
+  }
+  const double tot = block_sum<256>(sacc, sred);
+  if (threadIdx.x == 0) out[R] = tot;
+  if (bad && a.flag) atomicOr(a.flag, 1);
+}
+
+template <int R, bool ROWDOT, bool DECODE, int WKIND>
+static int launch_stream_t(adrom_ctx* ctx, const TileArgs& a, int grid) {
+  stream_kernel<R, ROWDOT, DECODE, WKIND><<<grid, 256, 0, ctx->stream>>>(a);
+  ADROM_LAUNCH_CK(ctx);
+  return ADROM_OK;
+}
+
+static bool stream_ok(int r) { return r == 16 || r == 32 || r == 64 || r == 128; }
+
+static int stream_grid(adrom_ctx* ctx, int64_t n) {
+  int64_t g = (int64_t)ctx->num_sms * 4;
+  const int64_t need = (n + 31) / 32;
+  if (g > need) g = need;
+  return (int)(g < 1 ? 1 : g);
+}
+
+template <bool ROWDOT, bool DECODE, int WKIND>
+static int launch_stream(adrom_ctx* ctx, const TileArgs& a, int grid) {
+  switch (a.r) {
+    case 16: return launch_stream_t<16, ROWDOT, DECODE, WKIND>(ctx, a, grid);
+    case 32: return launch_stream_t<32, ROWDOT, DECODE, WKIND>(ctx, a, grid);
+    case 64: return launch_stream_t<64, ROWDOT, DECODE, WKIND>(ctx, a, grid);
+    default: return launch_stream_t<128, ROWDOT, DECODE, WKIND>(ctx, a, grid);
+  }
 }
 
 static size_t tile_smem(int r) {
@@ -180,8 +318,12 @@ int ts_project(adrom_ctx* ctx, const double* phi, int64_t n, int r, int wkind, c
   a.d = d;
   a.partial = partial;
   a.flag = flag;
-  const int grid = tile_grid(ctx, n, r);
-  if (wkind == W_X)
+  const bool fast = stream_ok(r);
+  const int grid = fast ? stream_grid(ctx, n) : tile_grid(ctx, n, r);
+  if (fast)
+    st = (wkind == W_X) ? launch_stream<false, false, W_X>(ctx, a, grid)
+                        : launch_stream<false, false, W_ENCODE>(ctx, a, grid);
+  else if (wkind == W_X)
     st = launch_tile<false, false, W_X>(ctx, a, grid);
   else
     st = launch_tile<false, false, W_ENCODE>(ctx, a, grid);
@@ -203,6 +345,7 @@ int ts_decode(adrom_ctx* ctx, const double* phi, int64_t n, int r, const double*
   a.q_ref = q_ref;
   a.d = d;
   a.out_q = q_out;
+  if (stream_ok(r)) return launch_stream<true, true, W_NONE>(ctx, a, stream_grid(ctx, n));
   return launch_tile<true, true, W_NONE>(ctx, a, tile_grid(ctx, n, r));
 }
 
@@ -223,18 +366,21 @@ int ts_decode_project(adrom_ctx* ctx, const double* phi, int64_t n, int r, const
   a.x = y;
   a.partial = partial;
   a.flag = flag;
-  const int grid = tile_grid(ctx, n, r);
+  const bool fast = stream_ok(r);
+  const int grid = fast ? stream_grid(ctx, n) : tile_grid(ctx, n, r);
   // ROWDOT with the decode vector, weights = y (W_X); DECODE writes q_out
-  st = launch_tile<true, true, W_X>(ctx, a, grid);
+  st = fast ? launch_stream<true, true, W_X>(ctx, a, grid) : launch_tile<true, true, W_X>(ctx, a, grid);
   if (st) return st;
   reduce_partials_kernel<<<r + 1, 256, 0, ctx->stream>>>(partial, grid, r + 1, out, nullptr);
   ADROM_LAUNCH_CK(ctx);
   return ADROM_OK;
 }
 
-// residual pass: q = y - phi p ; out = [phi^T q, ||q||^2]; no-op if *skip == 0
+// residual pass: q = y - phi p (stored to qbuf if non-null);
+// out = [phi^T q, ||q||^2]; no-op if *skip == 0
 int ts_residual(adrom_ctx* ctx, const double* phi, int64_t n, int r, const double* p,
-                const double* y, double* out, double* partial, int* flag, const int* skip) {
+                const double* y, double* out, double* partial, int* flag, const int* skip,
+                double* qbuf) {
   TileArgs a{};
   a.phi = phi;
   a.n = n;
@@ -244,8 +390,11 @@ int ts_residual(adrom_ctx* ctx, const double* phi, int64_t n, int r, const doubl
   a.partial = partial;
   a.flag = flag;
   a.skip = skip;
-  const int grid = tile_grid(ctx, n, r);
-  int st = launch_tile<true, false, W_RESID>(ctx, a, grid);
+  a.out_w = qbuf;
+  const bool fast = stream_ok(r);
+  const int grid = fast ? stream_grid(ctx, n) : tile_grid(ctx, n, r);
+  int st = fast ? launch_stream<true, false, W_RESID>(ctx, a, grid)
+                : launch_tile<true, false, W_RESID>(ctx, a, grid);
   if (st) return st;
   reduce_partials_kernel<<<r + 1, 256, 0, ctx->stream>>>(partial, grid, r + 1, out, skip);
   ADROM_LAUNCH_CK(ctx);
@@ -253,10 +402,25 @@ int ts_residual(adrom_ctx* ctx, const double* phi, int64_t n, int r, const doubl
 }
 
 // ---------------------------------------------------------------------------
-// rotation  out = [phi | y] [M ; b^T]   (tracking.py:176-177 with q_hat
-// formed on the fly: [phi, q/||q||] U = phi (U_top - p u_bot^T/||q||) +
-// y u_bot^T/||q||).  out may alias phi (each block stages its rows first).
+// rotation  out = [phi | q_hat] [U_top ; u_bot^T]     (tracking.py:176-177)
+// q_hat_i = q_i / ||q|| with q_i read from the residual pass (qbuf) or formed
+// here as y_i - phi_i . p from the staged tile; the same q feeds the Gram
+// update, so the tracked Phi^T Phi stays consistent with the rotated basis.
+// out may alias phi (each block stages its rows before writing them).
 // ---------------------------------------------------------------------------
+struct RotArgs {
+  const double* phi;
+  const double* y;
+  const double* qbuf;   // may be null
+  const int* need;      // q is read from qbuf iff *need (null: iff qbuf)
+  const double* p;      // r_in (used when q is formed here)
+  const double* qinv;   // device scalar 1/||q|| (0 when degenerate)
+  const double* B;      // (r_in + 1) x r_out row-major: [U_top ; u_bot]
+  int64_t n;
+  int r_in, r_out;
+  double* out;
+};
+
 template <int R>
 struct RotCfg {
   static constexpr int TM = (R <= 64) ? 128 : 64;  // rows per tile
@@ -266,25 +430,25 @@ struct RotCfg {
 };
 
 template <int R>
-__global__ void __launch_bounds__(256) rot_tiled_kernel(const double* __restrict__ phi,
-                                                        const double* __restrict__ y,
-                                                        const double* __restrict__ M,
-                                                        const double* __restrict__ b, int64_t n,
-                                                        double* out) {
+__global__ void __launch_bounds__(256) rot_tiled_kernel(RotArgs a) {
   using C = RotCfg<R>;
   extern __shared__ double sm[];
-  double* As = sm;                    // TM x SA  (col R = y)
+  double* As = sm;                    // TM x SA  (col R = q_hat)
   double* Bs = As + C::TM * C::SA;    // (R+1) x R
+  double* ps = Bs + (R + 1) * R;      // R
   const int tid = threadIdx.x;
-  for (int e = tid; e < R * R; e += 256) Bs[e] = M[e];
-  for (int e = tid; e < R; e += 256) Bs[R * R + e] = b[e];
+  const bool use_q = a.qbuf && (a.need == nullptr || *a.need != 0);
+  for (int e = tid; e < (R + 1) * R; e += 256) Bs[e] = a.B[e];
+  for (int e = tid; e < R; e += 256) ps[e] = use_q ? 0.0 : a.p[e];
+  const double qinv = *a.qinv;
   const int rg = tid >> 4, cg = tid & 15;
+  const int64_t n = a.n;
   const int64_t ntiles = (n + C::TM - 1) / C::TM;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int64_t row0 = t * C::TM;
     const int rows = (int)((n - row0 < C::TM) ? (n - row0) : C::TM);
     __syncthreads();
-    const double2* src = reinterpret_cast<const double2*>(phi + row0 * R);
+    const double2* src = reinterpret_cast<const double2*>(a.phi + row0 * R);
     const int cnt2 = rows * R / 2;
     for (int e = tid; e < cnt2; e += 256) {
       const double2 v = src[e];
@@ -292,7 +456,22 @@ __global__ void __launch_bounds__(256) rot_tiled_kernel(const double* __restrict
       As[rr * C::SA + cc] = v.x;
       As[rr * C::SA + cc + 1] = v.y;
     }
-    for (int e = tid; e < C::TM; e += 256) As[e * C::SA + R] = (e < rows) ? y[row0 + e] : 0.0;
+    __syncthreads();
+    for (int e = tid; e < C::TM; e += 256) {
+      double qh = 0.0;
+      if (e < rows) {
+        double qv;
+        if (use_q) {
+          qv = a.qbuf[row0 + e];
+        } else {
+          double s = 0.0;
+          for (int k = 0; k < R; ++k) s = fma(As[e * C::SA + k], ps[k], s);
+          qv = a.y[row0 + e] - s;
+        }
+        qh = qv * qinv;
+      }
+      As[e * C::SA + R] = qh;
+    }
     __syncthreads();
     double acc[C::RM][C::RN];
 #pragma unroll
@@ -305,7 +484,7 @@ __global__ void __launch_bounds__(256) rot_tiled_kernel(const double* __restrict
 #pragma unroll
       for (int m = 0; m < C::RM; ++m) av[m] = As[(rg * C::RM + m) * C::SA + k];
 #pragma unroll
-      for (int q = 0; q < C::RN; ++q) bv[q] = Bs[k * R + cg * C::RN + q];
+      for (int q = 0; q < C::RN; ++q) bv[q] = Bs[k * R + cg + 16 * q];  // conflict-free
 #pragma unroll
       for (int m = 0; m < C::RM; ++m)
 #pragma unroll
@@ -317,39 +496,49 @@ __global__ void __launch_bounds__(256) rot_tiled_kernel(const double* __restrict
     for (int m = 0; m < C::RM; ++m) {
       const int rr = rg * C::RM + m;
       if (rr < rows) {
-        double* dst = out + (row0 + rr) * R + cg * C::RN;
+        double* dst = a.out + (row0 + rr) * R + cg;
 #pragma unroll
-        for (int q = 0; q < C::RN; ++q) dst[q] = acc[m][q];
+        for (int q = 0; q < C::RN; ++q) dst[16 * q] = acc[m][q];
       }
     }
   }
 }
 
-// generic sizes: out (n x r_out) = phi (n x r_in) M (r_in x r_out) + y b^T
-__global__ void __launch_bounds__(256) rot_generic_kernel(const double* __restrict__ phi,
-                                                          const double* __restrict__ y,
-                                                          const double* __restrict__ M,
-                                                          const double* __restrict__ b,
-                                                          int64_t n, int r_in, int r_out,
-                                                          double* out) {
+// generic sizes: out (n x r_out) = [phi | q_hat] B
+__global__ void __launch_bounds__(256) rot_generic_kernel(RotArgs a) {
   extern __shared__ double sm[];
   const int T = 32;
+  const int r_in = a.r_in, r_out = a.r_out;
   const int S = r_in + 1;
-  double* As = sm;           // T x S
-  double* Bs = As + T * S;   // (r_in+1) x r_out
+  double* As = sm;                   // T x S
+  double* Bs = As + T * S;           // (r_in+1) x r_out
+  double* ps = Bs + (r_in + 1) * r_out;
   const int tid = threadIdx.x;
-  for (int e = tid; e < r_in * r_out; e += 256) Bs[e] = M[e];
-  for (int e = tid; e < r_out; e += 256) Bs[r_in * r_out + e] = b[e];
-  const int64_t ntiles = (n + T - 1) / T;
+  const bool use_q = a.qbuf && (a.need == nullptr || *a.need != 0);
+  for (int e = tid; e < (r_in + 1) * r_out; e += 256) Bs[e] = a.B[e];
+  for (int e = tid; e < r_in; e += 256) ps[e] = use_q ? 0.0 : a.p[e];
+  const double qinv = *a.qinv;
+  const int64_t ntiles = (a.n + T - 1) / T;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int64_t row0 = t * T;
-    const int rows = (int)((n - row0 < T) ? (n - row0) : T);
+    const int rows = (int)((a.n - row0 < T) ? (a.n - row0) : T);
     __syncthreads();
     for (int e = tid; e < rows * r_in; e += 256) {
       const int rr = e / r_in, cc = e - rr * r_in;
-      As[rr * S + cc] = phi[row0 * r_in + e];
+      As[rr * S + cc] = a.phi[row0 * r_in + e];
     }
-    for (int e = tid; e < rows; e += 256) As[e * S + r_in] = y[row0 + e];
+    __syncthreads();
+    for (int e = tid; e < rows; e += 256) {
+      double qv;
+      if (use_q) {
+        qv = a.qbuf[row0 + e];
+      } else {
+        double s = 0.0;
+        for (int k = 0; k < r_in; ++k) s = fma(As[e * S + k], ps[k], s);
+        qv = a.y[row0 + e] - s;
+      }
+      As[e * S + r_in] = qv * qinv;
+    }
     __syncthreads();
     double res[32];
     int cntv = 0;
@@ -361,20 +550,21 @@ __global__ void __launch_bounds__(256) rot_generic_kernel(const double* __restri
     }
     __syncthreads();
     cntv = 0;
-    for (int e = tid; e < rows * r_out; e += 256) out[row0 * r_out + e] = res[cntv++];
+    for (int e = tid; e < rows * r_out; e += 256) a.out[row0 * r_out + e] = res[cntv++];
   }
 }
 
-int ts_rotate(adrom_ctx* ctx, const double* phi, const double* y, const double* M,
-              const double* b, int64_t n, int r_in, int r_out, double* out) {
+int ts_rotate(adrom_ctx* ctx, const RotArgs& a) {
+  const int64_t n = a.n;
+  const int r_in = a.r_in, r_out = a.r_out;
   if (r_in == r_out && (r_in == 16 || r_in == 32 || r_in == 64 || r_in == 128)) {
     int64_t g = (int64_t)ctx->num_sms * 2;
     auto launch = [&](auto kern, int TM, int R) -> int {
-      const size_t sm = sizeof(double) * ((size_t)TM * (R + 1) + (size_t)(R + 1) * R);
+      const size_t sm = sizeof(double) * ((size_t)TM * (R + 1) + (size_t)(R + 1) * R + R);
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       const int64_t nt = (n + TM - 1) / TM;
       const int64_t gg = g < nt ? g : nt;
-      kern<<<(int)(gg < 1 ? 1 : gg), 256, sm, ctx->stream>>>(phi, y, M, b, n, out);
+      kern<<<(int)(gg < 1 ? 1 : gg), 256, sm, ctx->stream>>>(a);
       ADROM_LAUNCH_CK(ctx);
       return ADROM_OK;
     };
@@ -385,12 +575,68 @@ int ts_rotate(adrom_ctx* ctx, const double* phi, const double* y, const double* 
   }
   if (r_in > 256 || r_out > 256)
     return set_error(ctx, ADROM_ERR_ARG, "rotation size %d x %d unsupported", r_in, r_out);
-  const size_t sm = sizeof(double) * ((size_t)32 * (r_in + 1) + (size_t)(r_in + 1) * r_out);
+  const size_t sm = sizeof(double) * ((size_t)32 * (r_in + 1) + (size_t)(r_in + 1) * r_out + r_in);
   cudaFuncSetAttribute(rot_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   int64_t g = (int64_t)ctx->num_sms * 4, nt = (n + 31) / 32;
   if (g > nt) g = nt;
-  rot_generic_kernel<<<(int)(g < 1 ? 1 : g), 256, sm, ctx->stream>>>(phi, y, M, b, n, r_in,
-                                                                     r_out, out);
+  rot_generic_kernel<<<(int)(g < 1 ? 1 : g), 256, sm, ctx->stream>>>(a);
+  ADROM_LAUNCH_CK(ctx);
+  return ADROM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Gram matrix G = Phi^T Phi (tracked across updates; computed afresh once)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ phi, int64_t n,
+                                                   int r, double* __restrict__ partial) {
+  extern __shared__ double sm[];
+  const int T = 64;
+  const int S = r | 1;
+  double* tile = sm;  // T x S
+  const int tid = threadIdx.x;
+  const int rr2 = r * r;
+  double acc[64];
+  const int mine = (rr2 + 255) / 256;
+  for (int k = 0; k < mine && k < 64; ++k) acc[k] = 0.0;
+  const int64_t ntiles = (n + T - 1) / T;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t row0 = t * T;
+    const int rows = (int)((n - row0 < T) ? (n - row0) : T);
+    __syncthreads();
+    for (int e = tid; e < rows * r; e += 256) {
+      const int a = e / r, c = e - a * r;
+      tile[a * S + c] = phi[row0 * r + e];
+    }
+    __syncthreads();
+    for (int k = 0; k < mine && k < 64; ++k) {
+      const int e = tid + 256 * k;
+      if (e >= rr2) break;
+      const int i = e / r, j = e - i * r;
+      double s = acc[k];
+      for (int a = 0; a < rows; ++a) s = fma(tile[a * S + i], tile[a * S + j], s);
+      acc[k] = s;
+    }
+  }
+  for (int k = 0; k < mine && k < 64; ++k) {
+    const int e = tid + 256 * k;
+    if (e < rr2) partial[(size_t)blockIdx.x * rr2 + e] = acc[k];
+  }
+}
+
+int ts_gram(adrom_ctx* ctx, const double* phi, int64_t n, int r, double* gram, double* partial) {
+  if (r > 128) return set_error(ctx, ADROM_ERR_ARG, "gram: rank %d unsupported", r);
+  int64_t g = (n + 63) / 64;
+  // partials hold 2 * partial_rows * (r + 1) doubles (isvd_workspace_bytes)
+  const int64_t cap = 2 * (int64_t)partial_rows(ctx) * (r + 1) / ((int64_t)r * r);
+  int64_t lim = (int64_t)ctx->num_sms * 2;
+  if (lim > cap) lim = cap;
+  if (g > lim) g = lim;
+  if (g < 1) g = 1;
+  const size_t sm = sizeof(double) * 64 * (r | 1);
+  cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  gram_kernel<<<(int)g, 256, sm, ctx->stream>>>(phi, n, r, partial);
+  ADROM_LAUNCH_CK(ctx);
+  reduce_partials_kernel<<<r * r, 256, 0, ctx->stream>>>(partial, (int)g, r * r, gram, nullptr);
   ADROM_LAUNCH_CK(ctx);
   return ADROM_OK;
 }
@@ -400,21 +646,84 @@ int ts_rotate(adrom_ctx* ctx, const double* phi, const double* y, const double* 
 // ---------------------------------------------------------------------------
 // stats layout (doubles): [0] qnorm [1] ynorm [2] proj_resid [3] degenerate
 //                         [4] reorth [5] sweeps [6] converged [7] nonfinite
-__global__ void isvd_decide_kernel(const double* __restrict__ red1, int r, double ratio,
-                                   int* __restrict__ need) {
-  // red1 = [p (r), ||y||^2]
-  double pp = 0.0;
-  for (int j = 0; j < r; ++j) pp += red1[j] * red1[j];
-  const double yy = red1[r];
-  const double est = yy - pp;
-  *need = (est > ratio * yy) ? 0 : 1;
+// Least-squares coefficients p = (Phi^T Phi)^{-1} Phi^T y (tracking.py:161,
+// gelsd) from the tracked Gram matrix G: Neumann series in E = G - I (the
+// tracked basis is orthonormal to << 1), Gaussian elimination otherwise.
+// Decides whether the explicit residual pass is needed:
+//   ||q||^2 = ||y||^2 - p . p1 cancels when ||q||^2 / ||y||^2 < ratio.
+// red1 = [p1 = Phi^T y (r), ||y||^2]; writes p (r) and *need.
+__global__ void __launch_bounds__(128) isvd_solve_kernel(const double* __restrict__ red1,
+                                                         const double* __restrict__ G, int r,
+                                                         double ratio, double* __restrict__ p,
+                                                         int* __restrict__ need) {
+  __shared__ double sp[128], st[128], sn[128];
+  __shared__ int sh_done;
+  const int tid = threadIdx.x;
+  for (int j = tid; j < r; j += blockDim.x) {
+    sp[j] = red1[j];
+    st[j] = red1[j];
+  }
+  __syncthreads();
+  bool conv = false;
+  for (int it = 0; it < 40 && !conv; ++it) {
+    // term <- -(G - I) term
+    for (int i = tid; i < r; i += blockDim.x) {
+      double s = 0.0;
+      for (int k = 0; k < r; ++k) s = fma(G[i * r + k] - (i == k ? 1.0 : 0.0), st[k], s);
+      sn[i] = -s;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double tn = 0.0, pn = 0.0;
+      for (int j = 0; j < r; ++j) {
+        sp[j] += sn[j];
+        st[j] = sn[j];
+        tn += sn[j] * sn[j];
+        pn += sp[j] * sp[j];
+      }
+      sh_done = (tn <= 1e-34 * pn) ? 1 : (!(tn <= 1e300) ? 2 : 0);
+    }
+    __syncthreads();
+    conv = sh_done != 0;
+  }
+  if (tid == 0) {
+    if (sh_done != 1) {
+      // fallback for a far-from-orthonormal basis: Gauss-Seidel on the SPD
+      // system G p = p1 (always convergent for SPD G; rare, slow, one thread)
+      for (int j = 0; j < r; ++j) sp[j] = red1[j];
+      for (int sweep = 0; sweep < 200; ++sweep) {
+        for (int i = 0; i < r; ++i) {
+          double s = red1[i];
+          for (int k = 0; k < r; ++k)
+            if (k != i) s -= G[i * r + k] * sp[k];
+          sp[i] = s / G[i * r + i];
+        }
+      }
+    }
+    double pdot = 0.0;
+    for (int j = 0; j < r; ++j) pdot += sp[j] * red1[j];
+    const double yy = red1[r];
+    const double est = yy - pdot;
+    *need = (est > ratio * yy) ? 0 : 1;
+  }
+  __syncthreads();
+  for (int j = tid; j < r; j += blockDim.x) p[j] = sp[j];
 }
 
+// iSVD core (tracking.py:163-177) for p = lstsq coefficients (isvd_solve_kernel):
+//   ||q||^2: explicit pass (red2[r]) or ||y||^2 - p.p1 when that does not cancel
+//   K = [[lam Sigma, p], [0, ||q||]] (last row 0 if degenerate), K = U S V^T
+//   B = [U_top ; u_bot][:, :r] sorted by S (rotation factors), qinv = 1/||q||
+//   G' = B^T [[G, c_hat], [c_hat^T, 1]] B with c_hat = Phi^T q / ||q||
+//   proj_resid = ||y - Phi Phi^T y|| = sqrt(||q||^2 + d^T G d), d = p - p1
+//                                                       (driver.py:366-367)
 __global__ void __launch_bounds__(1024) isvd_core_kernel(
     const double* __restrict__ sigma, const double* __restrict__ red1,
-    const double* __restrict__ red2, const int* __restrict__ need, int r_cur, int r, double lam,
-    double* __restrict__ Mout, double* __restrict__ bout, double* __restrict__ sigma_out,
-    double* __restrict__ stats, int* __restrict__ flag) {
+    const double* __restrict__ pls, const double* __restrict__ red2,
+    const int* __restrict__ need, const double* __restrict__ G, int r_cur, int r, double lam,
+    double* __restrict__ Bout, double* __restrict__ qinv_out, double* __restrict__ Tws,
+    double* __restrict__ Gout, double* __restrict__ sigma_out, double* __restrict__ stats,
+    int* __restrict__ flag) {
   extern __shared__ double sm[];
   const int n = r_cur + 1;
   const int ld = n + ((n & 1) ? 0 : 1);  // odd leading dimension
@@ -422,29 +731,41 @@ __global__ void __launch_bounds__(1024) isvd_core_kernel(
   double* V = A + n * ld;    // n x ld
   double* p = V + n * ld;    // r_cur
   double* s = p + r_cur;     // n
-  int* order = (int*)(s + n);
+  double* chat = s + n;      // r_cur
+  double* dv = chat + r_cur; // r_cur (p - p1)
+  double* red = dv + r_cur;  // 32
+  int* order = (int*)(red + 32);
   __shared__ int sh_flag;
   __shared__ double sh_q[4];
   const int tid = threadIdx.x;
   const bool reorth = need[0] != 0;
+  for (int j = tid; j < r_cur; j += blockDim.x) {
+    p[j] = pls[j];
+    dv[j] = pls[j] - red1[j];
+  }
+  __syncthreads();
+  // d^T G d for the driver's residual diagnostic
+  double dgd = 0.0;
+  for (int e = tid; e < r_cur * r_cur; e += blockDim.x) {
+    const int i = e / r_cur, k = e - i * r_cur;
+    dgd += dv[i] * G[e] * dv[k];
+  }
+  dgd = block_sum_dyn(dgd, red);
   if (tid == 0) {
-    double yy = red1[r_cur], pp = 0.0;
-    double qq, proj;
+    const double yy = red1[r_cur];
+    double qq;
     if (reorth) {
-      double p2 = 0.0;
-      for (int j = 0; j < r_cur; ++j) p2 += red2[j] * red2[j];
-      proj = red2[r_cur];    // ||y - Phi Phi^T y||^2
-      qq = proj - p2;        // ||q||^2 after one re-orthogonalisation
+      qq = red2[r_cur];
     } else {
-      for (int j = 0; j < r_cur; ++j) pp += red1[j] * red1[j];
-      proj = yy - pp;
-      qq = proj;
+      double pdot = 0.0;
+      for (int j = 0; j < r_cur; ++j) pdot += p[j] * red1[j];
+      qq = yy - pdot;
     }
     sh_q[0] = sqrt(qq > 0.0 ? qq : 0.0);
     sh_q[1] = sqrt(yy);
+    const double proj = (qq > 0.0 ? qq : 0.0) + dgd;
     sh_q[2] = sqrt(proj > 0.0 ? proj : 0.0);
   }
-  for (int j = tid; j < r_cur; j += blockDim.x) p[j] = red1[j] + (reorth ? red2[j] : 0.0);
   __syncthreads();
   const double qnorm = sh_q[0], ynorm = sh_q[1];
   // tracking.py:169 — degenerate residual keeps the subspace
@@ -462,21 +783,61 @@ __global__ void __launch_bounds__(1024) isvd_core_kernel(
     A[r_cur * ld + r_cur] = degenerate ? 0.0 : qnorm;  // tracking.py:172
     bad |= !isfinite(qnorm) || !isfinite(ynorm);
   }
-  if (bad) atomicOr(flag, 1);
+  __shared__ int sh_bad;
+  if (tid == 0) sh_bad = 0;
   __syncthreads();
+  if (bad) {
+    atomicOr(flag, 1);
+    sh_bad = 1;
+  }
+  __syncthreads();
+  if (sh_bad) {  // thin_svd rejects non-finite input (dense.py:61): no SVD, no rotation
+    for (int e = tid; e < n * r; e += blockDim.x) Bout[e] = 0.0;
+    if (tid == 0) *qinv_out = 0.0;
+    return;
+  }
   const JacobiResult jr = block_jacobi(A, ld, n, n, V, ld, 60, 1e-15, &sh_flag);
   column_norms_sorted(A, ld, n, n, s, order);
-  // M[k][c] = U_top[k][order[c]] - p_k u_bot[order[c]] / qnorm ; b[c] = u_bot/qnorm
+  // rotation factors B[k][c] = U[k][order[c]] (k = r_cur is u_bot), left
+  // singular vectors of K = accumulated rotations of the one-sided Jacobi on K^T
   const double inv = degenerate ? 0.0 : 1.0 / qnorm;
-  for (int e = tid; e < r_cur * r; e += blockDim.x) {
+  for (int e = tid; e < n * r; e += blockDim.x) {
     const int k = e / r, c = e - k * r;
-    const int jc = order[c];
-    const double ub = V[jc * ld + r_cur];
-    Mout[e] = V[jc * ld + k] - (degenerate ? 0.0 : p[k] * ub * inv);
+    Bout[e] = V[order[c] * ld + k];
   }
-  for (int c = tid; c < r; c += blockDim.x) {
-    const int jc = order[c];
-    bout[c] = degenerate ? 0.0 : V[jc * ld + r_cur] * inv;
+  if (tid == 0) *qinv_out = inv;
+  // c_hat = Phi^T q / ||q||: explicit (pass 2) or p1 - G p (normal equations)
+  for (int k = tid; k < r_cur; k += blockDim.x) {
+    double c;
+    if (reorth) {
+      c = red2[k];
+    } else {
+      double gp = 0.0;
+      for (int j = 0; j < r_cur; ++j) gp += G[k * r_cur + j] * p[j];
+      c = red1[k] - gp;
+    }
+    chat[k] = c * inv;
+  }
+  __syncthreads();
+  // T = Ghat B  ((r_cur+1) x r), then G' = B^T T  (r x r)
+  for (int e = tid; e < n * r; e += blockDim.x) {
+    const int k = e / r, c = e - k * r;
+    double acc = 0.0;
+    if (k < r_cur) {
+      for (int l = 0; l < r_cur; ++l) acc += G[k * r_cur + l] * V[order[c] * ld + l];
+      acc += chat[k] * V[order[c] * ld + r_cur];
+    } else {
+      for (int l = 0; l < r_cur; ++l) acc += chat[l] * V[order[c] * ld + l];
+      acc += (degenerate ? 0.0 : 1.0) * V[order[c] * ld + r_cur];
+    }
+    Tws[e] = acc;
+  }
+  __syncthreads();
+  for (int e = tid; e < r * r; e += blockDim.x) {
+    const int a = e / r, b = e - a * r;
+    double acc = 0.0;
+    for (int k = 0; k < n; ++k) acc += V[order[a] * ld + k] * Tws[k * r + b];
+    Gout[e] = acc;
   }
   __syncthreads();
   for (int c = tid; c < r; c += blockDim.x) sigma_out[c] = s[order[c]];
@@ -495,64 +856,95 @@ __global__ void __launch_bounds__(1024) isvd_core_kernel(
 static size_t core_smem(int r_cur) {
   const int n = r_cur + 1;
   const int ld = n + ((n & 1) ? 0 : 1);
-  return sizeof(double) * (2 * (size_t)n * ld + r_cur + n) + sizeof(int) * n + 64;
+  return sizeof(double) * (2 * (size_t)n * ld + 3 * (size_t)r_cur + n + 32) + sizeof(int) * n + 64;
 }
 
 size_t isvd_workspace_bytes(adrom_ctx* ctx, int64_t n, int r_cur, int r) {
-  const int64_t grid = (int64_t)ctx->num_sms * 3;
+  const int64_t grid = (int64_t)partial_rows(ctx);
   size_t b = 0;
-  b += align_up(sizeof(double) * grid * (r_cur + 1));  // partials
+  const int w = (r_cur * r_cur > r_cur + 1) ? r_cur * r_cur : r_cur + 1;
+  b += align_up(sizeof(double) * grid * (w > r_cur + 1 ? (r_cur + 1) : w));  // partials
+  b += align_up(sizeof(double) * (size_t)partial_rows(ctx) * (r_cur + 1));     // (gram partials fit)
   b += 2 * align_up(sizeof(double) * (r_cur + 1));     // red1, red2
-  b += align_up(sizeof(double) * r_cur * r);           // M
-  b += align_up(sizeof(double) * r);                   // b
-  b += align_up(sizeof(double) * 16);                  // stats
+  b += align_up(sizeof(double) * r_cur);               // p (least squares)
+  b += align_up(sizeof(double) * (r_cur + 1) * r);     // B
+  b += align_up(sizeof(double) * (r_cur + 1) * r);     // T
+  b += align_up(sizeof(double) * r_cur * r_cur);       // Gram (when not supplied)
+  b += align_up(sizeof(double) * 16);                  // stats + qinv
   b += align_up(sizeof(int) * 4);                      // need
-  (void)n;
+  b += align_up(sizeof(double) * (size_t)n);           // residual q
   return b;
 }
 
 int isvd_update_async(adrom_ctx* ctx, const double* phi, const double* sigma, const double* y,
                       int64_t n, int r_cur, int r, double lam, double* phi_out,
-                      double* sigma_out, void* ws, int* flag, double reorth_ratio,
-                      double* stats_out, const double* dec_a, const double* q_ref,
-                      const double* d, double* dec_out) {
+                      double* sigma_out, const double* gram_in, double* gram_out, void* ws,
+                      int* flag, double reorth_ratio, double* stats_out, const double* dec_a,
+                      const double* q_ref, const double* d, double* dec_out) {
   if (r_cur < 1 || r_cur > 110 || r < 1 || r > r_cur + 1)
     return set_error(ctx, ADROM_ERR_ARG, "isvd_update: bad ranks r_cur=%d r=%d", r_cur, r);
   if (phi_out == phi && r != r_cur)
     return set_error(ctx, ADROM_ERR_ARG, "isvd_update: in-place update needs r == r_cur");
+  if (gram_out && r != r_cur)
+    return set_error(ctx, ADROM_ERR_ARG, "isvd_update: a tracked Gram needs r == r_cur");
   char* w = (char*)ws;
-  const int64_t grid = (int64_t)ctx->num_sms * 3;
-  double* partial = (double*)w;
-  w += align_up(sizeof(double) * grid * (r_cur + 1));
-  double* red1 = (double*)w;
-  w += align_up(sizeof(double) * (r_cur + 1));
-  double* red2 = (double*)w;
-  w += align_up(sizeof(double) * (r_cur + 1));
-  double* M = (double*)w;
-  w += align_up(sizeof(double) * r_cur * r);
-  double* bv = (double*)w;
-  w += align_up(sizeof(double) * r);
-  double* stats = stats_out ? stats_out : (double*)w;
-  w += align_up(sizeof(double) * 16);
-  int* need = (int*)w;
+  auto take = [&](size_t bytes) {
+    void* q = w;
+    w += align_up(bytes);
+    return q;
+  };
+  const int64_t grid = (int64_t)partial_rows(ctx);
+  double* partial = (double*)take(sizeof(double) * grid * (r_cur + 1));
+  take(sizeof(double) * (size_t)partial_rows(ctx) * (r_cur + 1));
+  double* red1 = (double*)take(sizeof(double) * (r_cur + 1));
+  double* red2 = (double*)take(sizeof(double) * (r_cur + 1));
+  double* pls = (double*)take(sizeof(double) * r_cur);
+  double* B = (double*)take(sizeof(double) * (r_cur + 1) * r);
+  double* T = (double*)take(sizeof(double) * (r_cur + 1) * r);
+  double* Gloc = (double*)take(sizeof(double) * r_cur * r_cur);
+  double* sbuf = (double*)take(sizeof(double) * 16);
+  int* need = (int*)take(sizeof(int) * 4);
+  double* qbuf = (double*)take(sizeof(double) * (size_t)n);
+  double* stats = stats_out ? stats_out : sbuf;
+  double* qinv = sbuf + 12;
   int st;
-  // pass 1: p = Phi^T y, ||y||^2 (+ fused decode of the ROM state if asked)
+  const double* G = gram_in;
+  if (!G) {  // Gram afresh (one extra N r^2 pass; the session tracks it instead)
+    st = ts_gram(ctx, phi, n, r_cur, Gloc, partial);
+    if (st) return st;
+    G = Gloc;
+  }
+  // pass 1: p1 = Phi^T y, ||y||^2 (+ fused decode of the ROM state if asked)
+  int pr = prof_begin(ctx, PROBE_ISVD_PROJECT);
   if (dec_a)
     st = ts_decode_project(ctx, phi, n, r_cur, dec_a, q_ref, d, dec_out, y, red1, partial, flag);
   else
     st = ts_project(ctx, phi, n, r_cur, W_X, y, nullptr, nullptr, red1, partial, flag);
+  prof_end(ctx, pr);
   if (st) return st;
-  isvd_decide_kernel<<<1, 1, 0, ctx->stream>>>(red1, r_cur, reorth_ratio, need);
+  // least squares p = G^{-1} p1 (gelsd semantics for a full-rank basis)
+  isvd_solve_kernel<<<1, 128, 0, ctx->stream>>>(red1, G, r_cur, reorth_ratio, pls, need);
   ADROM_LAUNCH_CK(ctx);
-  // pass 2 (only if cancellation threatens ||q||): q = y - Phi p, Phi^T q, ||q||^2
-  st = ts_residual(ctx, phi, n, r_cur, red1, y, red2, partial, flag, need);
+  // pass 2 (only if ||y||^2 - p.p1 would cancel): q = y - Phi p, Phi^T q, ||q||^2
+  pr = prof_begin(ctx, PROBE_ISVD_RESID);
+  st = ts_residual(ctx, phi, n, r_cur, pls, y, red2, partial, flag, need, qbuf);
+  prof_end(ctx, pr);
   if (st) return st;
   const size_t csm = core_smem(r_cur);
   cudaFuncSetAttribute(isvd_core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
-  isvd_core_kernel<<<1, 1024, csm, ctx->stream>>>(sigma, red1, red2, need, r_cur, r, lam, M, bv,
-                                                  sigma_out, stats, flag);
+  pr = prof_begin(ctx, PROBE_ISVD_CORE);
+  // Gout may alias G: the kernel reads G completely before its final barrier
+  double* Gout = gram_out ? gram_out : Gloc;
+  isvd_core_kernel<<<1, 1024, csm, ctx->stream>>>(sigma, red1, pls, red2, need, G, r_cur, r, lam,
+                                                  B, qinv, T, Gout, sigma_out, stats, flag);
+  prof_end(ctx, pr);
   ADROM_LAUNCH_CK(ctx);
-  return ts_rotate(ctx, phi, y, M, bv, n, r_cur, r, phi_out);
+  // the rotation reads q from pass 2 when it ran, else forms it from y and p
+  RotArgs ra{phi, y, qbuf, need, pls, qinv, B, n, r_cur, r, phi_out};
+  pr = prof_begin(ctx, PROBE_ISVD_ROTATE);
+  st = ts_rotate(ctx, ra);
+  prof_end(ctx, pr);
+  return st;
 }
 
 // ---------------------------------------------------------------------------

@@ -1,0 +1,432 @@
+// Reduced time steppers on the device (kernel 5): the hyper-reduced LSPG
+// Gauss-Newton step (projection.py:158-204) and the hyper-reduced Galerkin
+// Newton step (projection.py:111-147).  One thread block runs the whole
+// nonlinear iteration (no host round-trip per iteration).
+//
+// Compiled with --fmad=false: the sampled residual and the FD perturbations
+// `qc + h_j * dinv_phi_closure[:, j]` reproduce numpy's unfused arithmetic.
+#include "physics.cuh"
+#include "jacobi.cuh"
+#include "rom_internal.cuh"
+
+namespace adrom {
+
+struct PlanView {
+  int kind, nv;
+  BurgersParams bp;
+  double gamma;
+  const int64_t* gather;
+  const int64_t* out_cell;
+  const int64_t* out_var;
+};
+
+// rhs at sampled row j from closure values (+ optional direction h * dir[:, k])
+__device__ __forceinline__ double eval_row(const PlanView& p, int j, const double* qc,
+                                           const double* dir, int ldd, int k, double h) {
+  const int64_t cell = p.out_cell[j];
+  if (p.kind == ADROM_BURGERS) {
+    const int64_t* g = p.gather + 3 * cell;
+    double v[3];
+#pragma unroll
+    for (int s = 0; s < 3; ++s)
+      v[s] = dir ? qc[g[s]] + h * dir[g[s] * ldd + k] : qc[g[s]];
+    return burgers_cell(v[0], v[1], v[2], p.bp);
+  }
+  const int64_t* g = p.gather + 9 * cell;
+  double v[9];
+#pragma unroll
+  for (int s = 0; s < 9; ++s) v[s] = dir ? qc[g[s]] + h * dir[g[s] * ldd + k] : qc[g[s]];
+  const Cons l{v[0], v[1], v[2]}, c{v[3], v[4], v[5]}, r{v[6], v[7], v[8]};
+  return cons_get(sod_cell(l, c, r, p.gamma, p.bp.dx), (int)p.out_var[j]);
+}
+
+// ---------------------------------------------------------------------------
+// Square least squares with a certified condition bound.
+// jac (r x r, column-major jA[l*ld + k]) = QR by Householder; if
+// ||R||_F ||R^{-1}||_F <= CERT (so cond_2(jac) <= CERT < 1e12), the reference's
+// SVD-based lstsq with rcond 1e-12 truncates nothing and its conditioning
+// test (sv[-1] <= 1e-14 sv[0], projection.py:194) cannot fire: the QR solve
+// gives the same least-squares solution.  Otherwise the caller falls back
+// to the SVD.  Overwrites jA (R in the upper triangle) and rhs.
+// Returns true when certified; delta = jac^{-1} rhs in `out`.
+// ---------------------------------------------------------------------------
+constexpr double LS_CERT = 1e10;
+
+__device__ bool block_qr_certified_solve(double* jA, int ld, int r, double* rhs, double* out,
+                                         double* vbuf, double* red) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  __shared__ double sh_beta, sh_alpha;
+  for (int k = 0; k < r; ++k) {
+    double* col = jA + (size_t)k * ld;
+    // norm of col[k:]
+    double a = 0.0;
+    for (int i = k + tid; i < r; i += blockDim.x) a += col[i] * col[i];
+    a = block_sum_dyn(a, red);
+    if (tid == 0) {
+      const double x0 = col[k];
+      const double nrm = sqrt(a);
+      const double alpha = (x0 >= 0.0) ? -nrm : nrm;
+      sh_alpha = alpha;
+      // v = x - alpha e1, beta = 1 / (v^T v / 2) = 1 / (nrm^2 - x0 alpha)
+      const double vtv_half = a - x0 * alpha;
+      sh_beta = (vtv_half > 0.0) ? 1.0 / vtv_half : 0.0;
+      vbuf[k] = x0 - alpha;
+    }
+    __syncthreads();
+    for (int i = k + 1 + tid; i < r; i += blockDim.x) vbuf[i] = col[i];
+    __syncthreads();
+    const double beta = sh_beta;
+    // apply H = I - beta v v^T to trailing columns and the rhs (warp per column)
+    for (int j = k + 1 + warp; j <= r; j += nw) {
+      double* cj = (j < r) ? jA + (size_t)j * ld : rhs;
+      double s = 0.0;
+      for (int i = k + lane; i < r; i += 32) s += vbuf[i] * cj[i];
+      s = warp_sum(s) * beta;
+      for (int i = k + lane; i < r; i += 32) cj[i] -= s * vbuf[i];
+    }
+    __syncthreads();
+    if (tid == 0) col[k] = sh_alpha;
+    __syncthreads();
+  }
+  // ||R||_F and ||R^{-1}||_F (column c of R^{-1} by back substitution)
+  double rf = 0.0;
+  for (int e = tid; e < r * r; e += blockDim.x) {
+    const int l = e / r, k = e - l * r;
+    if (k <= l) rf += jA[(size_t)l * ld + k] * jA[(size_t)l * ld + k];
+  }
+  rf = block_sum_dyn(rf, red);
+  double inv2 = 0.0;
+  bool bad = false;
+  for (int c = tid; c < r; c += blockDim.x) {
+    // solve R x = e_c (x_i = 0 for i > c)
+    double xs[128];
+    for (int i = c; i >= 0; --i) {
+      double s = (i == c) ? 1.0 : 0.0;
+      for (int l = i + 1; l <= c; ++l) s -= jA[(size_t)l * ld + i] * xs[l];
+      const double d = jA[(size_t)i * ld + i];
+      if (d == 0.0) {
+        bad = true;
+        xs[i] = 0.0;
+      } else {
+        xs[i] = s / d;
+      }
+      inv2 += xs[i] * xs[i];
+    }
+  }
+  inv2 = block_sum_dyn(inv2, red);
+  __shared__ int sh_bad;
+  if (tid == 0) sh_bad = 0;
+  __syncthreads();
+  if (bad) sh_bad = 1;
+  __syncthreads();
+  const bool cert = !sh_bad && isfinite(inv2) && isfinite(rf) && sqrt(rf) * sqrt(inv2) <= LS_CERT;
+  if (cert && tid == 0) {
+    for (int i = r - 1; i >= 0; --i) {
+      double s = rhs[i];
+      for (int l = i + 1; l < r; ++l) s -= jA[(size_t)l * ld + i] * out[l];
+      out[i] = s / jA[(size_t)i * ld + i];
+    }
+  }
+  __syncthreads();
+  return cert;
+}
+
+// ---------------------------------------------------------------------------
+// LSPG (projection.py:158-204)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(512) lspg_kernel(RomStepArgs A) {
+  extern __shared__ double sm[];
+  const int r = A.op.r;
+  const int n_s = A.op.sizes[0], n_c = A.op.sizes[1];
+  const int ld = r | 1;
+  double* a = sm;                   // r
+  double* rho = a + r;              // r
+  double* h = rho + r;              // r
+  double* grad = h + r;             // r
+  double* jA = grad + r;            // r x ld  (column-major: jA[l*ld + k] = jac[k][l])
+  double* V = jA + (size_t)r * ld;  // r x ld
+  double* sv = V + (size_t)r * ld;  // r
+  double* red = sv + r;             // 32
+  double* qrhs = red + 32;          // r
+  double* qout = qrhs + r;          // r
+  double* qv = qout + r;            // r
+  int* order = (int*)(qv + r);
+  __shared__ int sh_flag, sh_stop;
+  __shared__ double sh_gn;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  PlanView pv{A.kind, A.op.n_var, A.bp, A.gamma, A.op.gather, A.op.out_cell, A.op.out_var};
+  double* qc = A.work;                    // n_c
+  double* fs = qc + A.op.nc_cap;          // n_s
+  double* prev = fs + A.op.ns_cap;        // n_s
+  double* res = prev + A.op.ns_cap;       // n_s
+  double* test = res + A.op.ns_cap;       // n_s x r
+  const double* Dc = A.op.dinv_phi_c;
+  for (int k = tid; k < r; k += blockDim.x) a[k] = A.a_prev[k];
+  __syncthreads();
+  // prev_sampled = decode_closure(a_prev)[sample_pos]   (projection.py:170)
+  for (int j = tid; j < n_s; j += blockDim.x) {
+    const int64_t p = A.op.sample_pos[j];
+    double s = 0.0;
+    for (int k = 0; k < r; ++k) s += Dc[p * r + k] * a[k];
+    prev[j] = A.op.q_ref_c[p] + s;
+  }
+  int it = 0;
+  double gnorm = INFINITY;
+  int status = 0;
+  while (it < A.max_iter) {
+    // qc = decode_closure(a)
+    for (int i = tid; i < n_c; i += blockDim.x) {
+      double s = 0.0;
+      for (int k = 0; k < r; ++k) s += Dc[(int64_t)i * r + k] * a[k];
+      qc[i] = A.op.q_ref_c[i] + s;
+    }
+    __syncthreads();
+    for (int j = tid; j < n_s; j += blockDim.x) {
+      const double f = eval_row(pv, j, qc, nullptr, 0, 0, 0.0);
+      fs[j] = f;
+      res[j] = A.op.d_s[j] * ((qc[A.op.sample_pos[j]] - prev[j]) - A.dt * f);
+    }
+    for (int k = tid; k < r; k += blockDim.x) h[k] = FD_EPS * np_max(1.0, fabs(a[k]));
+    __syncthreads();
+    // rho = pinv @ res
+    for (int k = warp; k < r; k += nw) {
+      double s = 0.0;
+      for (int j = lane; j < n_s; j += 32) s += A.op.pinv[(int64_t)k * n_s + j] * res[j];
+      s = warp_sum(s);
+      if (lane == 0) rho[k] = s;
+    }
+    // test_sampled = phi_s - dt * (d_s * dfs)   (projection.py:183-186)
+    for (int e = tid; e < n_s * r; e += blockDim.x) {
+      const int j = e / r, k = e - j * r;
+      const double df = (eval_row(pv, j, qc, Dc, r, k, h[k]) - fs[j]) / h[k];
+      test[e] = A.op.phi_s[e] - A.dt * (A.op.d_s[j] * df);
+    }
+    __syncthreads();
+    // jac = pinv @ test  -> stored column-major in jA
+    for (int o = warp; o < r * r; o += nw) {
+      const int k = o / r, l = o - k * r;
+      double s = 0.0;
+      for (int j = lane; j < n_s; j += 32) s += A.op.pinv[(int64_t)k * n_s + j] * test[j * r + l];
+      s = warp_sum(s);
+      if (lane == 0) jA[l * ld + k] = s;
+    }
+    __syncthreads();
+    // grad = jac^T rho
+    double g2 = 0.0;
+    for (int l = tid; l < r; l += blockDim.x) {
+      double s = 0.0;
+      for (int k = 0; k < r; ++k) s += jA[l * ld + k] * rho[k];
+      grad[l] = s;
+      g2 += s * s;
+    }
+    g2 = block_sum_dyn(g2, red);
+    gnorm = sqrt(g2);
+    if (gnorm <= A.tol) break;
+    // fast path: Householder QR on a copy with a certified condition bound
+    for (int e = tid; e < r * ld; e += blockDim.x) V[e] = jA[e];
+    for (int k = tid; k < r; k += blockDim.x) qrhs[k] = -rho[k];
+    __syncthreads();
+    if (block_qr_certified_solve(V, ld, r, qrhs, qout, qv, red)) {
+      for (int k = tid; k < r; k += blockDim.x) a[k] = a[k] + qout[k];
+      __syncthreads();
+      ++it;
+      continue;
+    }
+    // conditioning check + least squares via the SVD of jac (projection.py:193-199)
+    const JacobiResult jr = block_jacobi(jA, ld, r, r, V, ld, 60, 1e-15, &sh_flag);
+    column_norms_sorted(jA, ld, r, r, sv, order);
+    const double smax = sv[order[0]], smin = sv[order[r - 1]];
+    if (tid == 0) sh_stop = (!(smin > 1e-14 * smax) || !jr.converged) ? 1 : 0;
+    __syncthreads();
+    if (sh_stop) {
+      status = 1;
+      if (tid == 0) A.info[3] = smax / fmax(smin, 1e-300);
+      break;
+    }
+    // delta = -V S^+ U^T rho with U = W / s, cut at 1e-12 s_max (rcond)
+    for (int c = warp; c < r; c += nw) {
+      double s = 0.0;
+      for (int k = lane; k < r; k += 32) s += jA[c * ld + k] * rho[k];
+      s = warp_sum(s);
+      if (lane == 0) {
+        const double sc = sv[c];
+        grad[c] = (sc > 1e-12 * smax) ? s / (sc * sc) : 0.0;  // reuse grad as coefficients
+      }
+    }
+    __syncthreads();
+    for (int k = tid; k < r; k += blockDim.x) {
+      double s = 0.0;
+      for (int c = 0; c < r; ++c) s += V[c * ld + k] * grad[c];
+      a[k] = a[k] + (-s);
+    }
+    __syncthreads();
+    ++it;
+  }
+  __syncthreads();
+  for (int k = tid; k < r; k += blockDim.x) A.a_out[k] = a[k];
+  if (tid == 0) {
+    A.info[0] = (gnorm <= A.tol) ? 1.0 : 0.0;
+    A.info[1] = it;
+    A.info[2] = gnorm;
+    A.info[4] = status;
+  }
+  (void)sh_gn;
+}
+
+// ---------------------------------------------------------------------------
+// Galerkin (projection.py:111-147)
+// ---------------------------------------------------------------------------
+// out = pinv @ (d_s * evaluate(q_ref_c + Dc @ av)), block-wide
+__device__ void reduced_rhs(const RomStepArgs& A, const PlanView& pv, const double* av,
+                            double* qc, double* fsd, double* out) {
+  const int r = A.op.r, n_s = A.op.sizes[0], n_c = A.op.sizes[1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const double* Dc = A.op.dinv_phi_c;
+  for (int i = tid; i < n_c; i += blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < r; ++k) s += Dc[(int64_t)i * r + k] * av[k];
+    qc[i] = A.op.q_ref_c[i] + s;
+  }
+  __syncthreads();
+  for (int j = tid; j < n_s; j += blockDim.x) fsd[j] = A.op.d_s[j] * eval_row(pv, j, qc, nullptr, 0, 0, 0.0);
+  __syncthreads();
+  for (int k = warp; k < r; k += nw) {
+    double s = 0.0;
+    for (int j = lane; j < n_s; j += 32) s += A.op.pinv[(int64_t)k * n_s + j] * fsd[j];
+    s = warp_sum(s);
+    if (lane == 0) out[k] = s;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(512) galerkin_kernel(RomStepArgs A) {
+  extern __shared__ double sm[];
+  const int r = A.op.r;
+  double* a0 = sm;            // r
+  double* a = a0 + r;         // r
+  double* ap = a + r;         // r
+  double* g = ap + r;         // r
+  double* fa = g + r;         // r
+  double* fp = fa + r;        // r
+  double* h = fp + r;         // r
+  double* J = h + r;          // r x r row-major
+  double* red = J + r * r;    // 32
+  __shared__ int sh_sing;
+  const int tid = threadIdx.x;
+  PlanView pv{A.kind, A.op.n_var, A.bp, A.gamma, A.op.gather, A.op.out_cell, A.op.out_var};
+  double* qc = A.work;
+  double* fsd = qc + A.op.nc_cap;
+  for (int k = tid; k < r; k += blockDim.x) {
+    a0[k] = A.a_prev[k];
+    a[k] = A.a_prev[k];
+  }
+  __syncthreads();
+  auto residual = [&]() -> double {
+    reduced_rhs(A, pv, a, qc, fsd, fp);
+    double s2 = 0.0;
+    for (int k = tid; k < r; k += blockDim.x) {
+      const double gk = (a[k] - a0[k]) - A.dt * fp[k];
+      g[k] = gk;
+      s2 += gk * gk;
+    }
+    s2 = block_sum_dyn(s2, red);
+    return sqrt(s2);
+  };
+  double gnorm = residual();
+  int it = 0, status = 0;
+  while (gnorm > A.tol && it < A.max_iter) {
+    for (int k = tid; k < r; k += blockDim.x) h[k] = FD_EPS * np_max(1.0, fabs(a[k]));
+    reduced_rhs(A, pv, a, qc, fsd, fa);
+    for (int j = 0; j < r; ++j) {
+      for (int k = tid; k < r; k += blockDim.x) ap[k] = (k == j) ? a[k] + h[k] : a[k];
+      __syncthreads();
+      reduced_rhs(A, pv, ap, qc, fsd, fp);
+      for (int k = tid; k < r; k += blockDim.x)
+        J[k * r + j] = ((k == j) ? 1.0 : 0.0) - (A.dt * (fp[k] - fa[k])) / h[j];
+      __syncthreads();
+    }
+    // solve J delta = -g by LU with partial pivoting (one thread; r <= 128)
+    if (tid == 0) {
+      sh_sing = 0;
+      double* b = fp;
+      for (int k = 0; k < r; ++k) b[k] = -g[k];
+      for (int k = 0; k < r; ++k) {
+        int p = k;
+        double best = fabs(J[k * r + k]);
+        for (int i = k + 1; i < r; ++i)
+          if (fabs(J[i * r + k]) > best) {
+            best = fabs(J[i * r + k]);
+            p = i;
+          }
+        if (best == 0.0) {
+          sh_sing = 1;
+          break;
+        }
+        if (p != k) {
+          for (int c = 0; c < r; ++c) {
+            const double t = J[k * r + c];
+            J[k * r + c] = J[p * r + c];
+            J[p * r + c] = t;
+          }
+          const double t = b[k];
+          b[k] = b[p];
+          b[p] = t;
+        }
+        for (int i = k + 1; i < r; ++i) {
+          const double l = J[i * r + k] / J[k * r + k];
+          for (int c = k + 1; c < r; ++c) J[i * r + c] -= l * J[k * r + c];
+          b[i] -= l * b[k];
+        }
+      }
+      if (!sh_sing)
+        for (int i = r - 1; i >= 0; --i) {
+          double s = b[i];
+          for (int c = i + 1; c < r; ++c) s -= J[i * r + c] * b[c];
+          b[i] = s / J[i * r + i];
+        }
+    }
+    __syncthreads();
+    if (sh_sing) {
+      status = 1;
+      break;
+    }
+    for (int k = tid; k < r; k += blockDim.x) a[k] = a[k] + fp[k];
+    __syncthreads();
+    gnorm = residual();
+    ++it;
+  }
+  __syncthreads();
+  for (int k = tid; k < r; k += blockDim.x) A.a_out[k] = a[k];
+  if (tid == 0) {
+    A.info[0] = (gnorm <= A.tol) ? 1.0 : 0.0;
+    A.info[1] = it;
+    A.info[2] = gnorm;
+    A.info[4] = status;
+  }
+}
+
+size_t rom_step_work_doubles(const DevOp& op) {
+  return (size_t)op.nc_cap + 3 * (size_t)op.ns_cap + (size_t)op.ns_cap * op.r + 64;
+}
+
+int rom_step_async(adrom_ctx* ctx, const RomStepArgs& args, bool lspg) {
+  const int r = args.op.r;
+  if (r < 1 || r > 128) return set_error(ctx, ADROM_ERR_ARG, "rom_step: rank %d unsupported", r);
+  const int pr = prof_begin(ctx, PROBE_ROM_STEP);
+  if (lspg) {
+    const int ld = r | 1;
+    const size_t sm = sizeof(double) * (7 * (size_t)r + 2 * (size_t)r * ld + r + 32) +
+                      sizeof(int) * r + 64;
+    cudaFuncSetAttribute(lspg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    lspg_kernel<<<1, 512, sm, ctx->stream>>>(args);
+  } else {
+    const size_t sm = sizeof(double) * (7 * (size_t)r + (size_t)r * r + 32) + 64;
+    cudaFuncSetAttribute(galerkin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    galerkin_kernel<<<1, 512, sm, ctx->stream>>>(args);
+  }
+  prof_end(ctx, pr);
+  ADROM_LAUNCH_CK(ctx);
+  return ADROM_OK;
+}
+
+}  // namespace adrom

@@ -1,0 +1,42 @@
+// Host-side internal API: QDEIM / FGS sampling, stencil closure + gather plan,
+// reduced operator assembly.
+#pragma once
+
+#include "common.cuh"
+
+namespace adrom {
+
+// Persistent pivot guesses (one chunk of <= r pivots per QDEIM restart).
+struct QdeimGuess {
+  int64_t* rows = nullptr;  // device, max_chunks * r
+  int g[64] = {0};          // confirmed/guessed length per chunk (host mirror)
+  int max_chunks = 0;
+  int r = 0;
+};
+
+size_t qdeim_workspace_bytes(adrom_ctx* ctx, int r, int count);
+// First `count` pivots of the restarted column-pivoted QR of phi^T
+// (sampling.py:77-104), exact greedy, ties to the lowest row.  Blocking
+// (synchronises once per verification pass).  `guess` may be null.
+int qdeim_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int count, int64_t* out_idx,
+                 QdeimGuess* guess, void* ws, int* iterations_out);
+
+// FGS (sampling.py:117-159): idx[0..n_base) must already hold the QDEIM
+// rows; appends n_extra rows ranked by |grad feature(y_corr)|.
+int fgs_extend(adrom_ctx* ctx, const adrom_model& m, const double* y_corr, int feature_kind,
+               int64_t* idx, int n_base, int n_extra, void* ws);
+size_t fgs_workspace_bytes(const adrom_model& m);
+
+// Device layout of a reduced operator (projection.py:57-87) with capacities.
+using DevOp = adrom_rom_op;
+
+// plan + closure from idx (device, n_s rows) — fom.py:127-152, sampling.py:178-189
+int plan_build(adrom_ctx* ctx, const adrom_model& m, DevOp& op, int n_s, int* flag);
+// gathers + DEIM pseudo-inverse (sampling.py:162-175, projection.py:69-80)
+int operator_fill(adrom_ctx* ctx, DevOp& op, const double* phi, const double* q_ref,
+                  const double* d, int n_s, int* flag);
+
+int deim_pinv_only(adrom_ctx* ctx, const double* phi, const int64_t* idx, int n_s, int r,
+                   double* phi_s, double* pinv, int* flag);
+
+}  // namespace adrom

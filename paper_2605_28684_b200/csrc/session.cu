@@ -1,0 +1,606 @@
+// Device-resident online loop of the adaptive ROM (driver.py:291-410) and the
+// C-ABI entry points for sampling, reduced operators and reduced steps.
+//
+// One fine step = rom_step (one block, whole Gauss-Newton loop) + decode; no
+// host round-trip.  Every z steps an adaptation event runs on the device:
+// coarse backward-Euler Newton of the lookahead trajectory, preprocess,
+// iSVD update, QDEIM / FGS sampling, operator rebuild, state transfer.  An
+// event that fails keeps the previous basis and operator (driver.py:384-385):
+// the new basis / operator are built into second buffers and swapped in only
+// when every stage succeeded.
+#include "common.cuh"
+#include "fom_internal.cuh"
+#include "linalg_internal.cuh"
+#include "rom_internal.cuh"
+#include "sampling_internal.cuh"
+
+#include <string.h>
+
+#include <vector>
+
+using namespace adrom;
+
+namespace {
+
+int read_flags(adrom_ctx* ctx, int* host_flags) {
+  ADROM_CK(ctx, cudaMemcpyAsync(ctx->pinned, ctx->dflags, sizeof(int) * 16,
+                                cudaMemcpyDeviceToHost, ctx->stream));
+  ADROM_CK(ctx, cudaStreamSynchronize(ctx->stream));
+  memcpy(host_flags, ctx->pinned, sizeof(int) * 16);
+  return ADROM_OK;
+}
+
+int reset_flags(adrom_ctx* ctx) {
+  ADROM_CK(ctx, cudaMemsetAsync(ctx->dflags, 0, sizeof(int) * 16, ctx->stream));
+  return ADROM_OK;
+}
+
+// map device flag bits of the sampling / operator stages to reference errors
+int sampling_flag_error(adrom_ctx* ctx, int f) {
+  if (f & 16) return set_error(ctx, ADROM_ERR_DENSE, "not enough distinct rows to satisfy the sampling budget");
+  if (f & 32) return set_error(ctx, ADROM_ERR_ARG, "sampling indices must be distinct");
+  if (f & 64) return set_error(ctx, ADROM_ERR_SINGULAR, "sampled basis is rank deficient");
+  if (f & 8) return set_error(ctx, ADROM_ERR_NOCONV, "SVD did not converge");
+  if (f & 1) return set_error(ctx, ADROM_ERR_NONFINITE, "thin_svd input contains non-finite entries");
+  return ADROM_OK;
+}
+
+__global__ void preprocess_kernel(const double* __restrict__ y, const double* __restrict__ q_ref,
+                                  const double* __restrict__ d, int64_t n,
+                                  double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = d[i] * (y[i] - q_ref[i]);  // snapshots.py:47-48
+}
+
+__global__ void copy_i64_kernel(const int64_t* __restrict__ a, int64_t* __restrict__ b, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) b[i] = a[i];
+}
+
+// rom-step log: per step [converged, iterations, residual]; status -> first failing step
+__global__ void log_step_kernel(const double* __restrict__ info, double* __restrict__ log,
+                                int64_t step, int* __restrict__ fail_step) {
+  log[0] = info[0];
+  log[1] = info[1];
+  log[2] = info[2];
+  if (info[4] != 0.0) atomicCAS(fail_step, -1, (int)step);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// session
+// ---------------------------------------------------------------------------
+struct adrom_session {
+  adrom_ctx* ctx = nullptr;
+  adrom_session_config cfg{};
+  int64_t N = 0;
+  int r = 0;
+  // state (device)
+  double *phi[2] = {nullptr, nullptr}, *sigma[2] = {nullptr, nullptr};
+  double* gram[2] = {nullptr, nullptr};  // tracked Phi^T Phi of each basis buffer
+  int cur = 0;
+  double *q_ref = nullptr, *d = nullptr;
+  double *y_corr = nullptr, *y_next = nullptr, *y_hat = nullptr, *q_tilde = nullptr;
+  double *a = nullptr;
+  adrom_rom_op op[2]{};
+  int opcur = 0;
+  QdeimGuess guess;
+  double* rom_work = nullptr;
+  double* rom_info = nullptr;
+  double* isvd_stats = nullptr;
+  void* isvd_ws = nullptr;
+  void* qd_ws = nullptr;
+  double* step_log = nullptr;    // n_t_online x 3
+  int* fail_step = nullptr;
+  int64_t n_online = 0;          // steps done
+  int64_t cap_steps = 0;
+  std::vector<adrom_event_record> events;
+  std::vector<void*> allocs;
+
+  double* alloc_d(size_t n) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, sizeof(double) * (n ? n : 1)) != cudaSuccess) return nullptr;
+    allocs.push_back(p);
+    return (double*)p;
+  }
+  template <typename T>
+  T* alloc_t(size_t n) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, sizeof(T) * (n ? n : 1)) != cudaSuccess) return nullptr;
+    allocs.push_back(p);
+    return (T*)p;
+  }
+};
+
+namespace {
+
+adrom_model model_of(const adrom_session* s) { return s->cfg.model; }
+
+int alloc_op(adrom_session* s, adrom_rom_op& op) {
+  const int ns = s->cfg.n_s, nv = s->cfg.model.n_var, r = s->r;
+  op.r = r;
+  op.n_var = nv;
+  op.ns_cap = ns;
+  op.nc_cap = 3 * ns * nv;
+  op.ncell_cap = ns;
+  op.idx = s->alloc_t<int64_t>(ns);
+  op.closure = s->alloc_t<int64_t>(op.nc_cap);
+  op.gather = s->alloc_t<int64_t>((size_t)ns * 3 * nv);
+  op.out_cell = s->alloc_t<int64_t>(ns);
+  op.out_var = s->alloc_t<int64_t>(ns);
+  op.sample_pos = s->alloc_t<int64_t>(ns);
+  op.sizes = s->alloc_t<int32_t>(4);
+  op.pinv = s->alloc_d((size_t)r * ns);
+  op.d_s = s->alloc_d(ns);
+  op.q_ref_c = s->alloc_d(op.nc_cap);
+  op.dinv_phi_c = s->alloc_d((size_t)op.nc_cap * r);
+  op.phi_s = s->alloc_d((size_t)ns * r);
+  if (!op.phi_s) return set_error(s->ctx, ADROM_ERR_CUDA, "session: device allocation failed");
+  return ADROM_OK;
+}
+
+// sampling (driver.py:264-273) + closure + operator for basis `phi` into op
+int build_sampling_operator(adrom_session* s, const double* phi, adrom_rom_op& op,
+                            const double* y_corr) {
+  adrom_ctx* ctx = s->ctx;
+  const adrom_model m = model_of(s);
+  const int n_s = s->cfg.n_s;
+  int st;
+  int it = 0;
+  if (s->cfg.sampling == 1) {
+    const int n_base = n_s - s->cfg.n_extra;
+    if (n_base > 0) {
+      st = qdeim_select(ctx, phi, s->N, s->r, n_base, op.idx, &s->guess, s->qd_ws, &it);
+      if (st) return st;
+    }
+    st = reset_flags(ctx);
+    if (st) return st;
+    st = fgs_extend(ctx, m, y_corr, s->cfg.feature, op.idx, n_base, s->cfg.n_extra, nullptr);
+    if (st) return st;
+  } else {
+    st = qdeim_select(ctx, phi, s->N, s->r, n_s, op.idx, &s->guess, s->qd_ws, &it);
+    if (st) return st;
+    st = reset_flags(ctx);
+    if (st) return st;
+  }
+  const int pr = prof_begin(ctx, PROBE_OPERATOR);
+  st = plan_build(ctx, m, op, n_s, ctx->dflags);
+  if (st) return st;
+  st = operator_fill(ctx, op, phi, s->q_ref, s->d, n_s, ctx->dflags);
+  prof_end(ctx, pr);
+  if (st) return st;
+  int flags[16];
+  st = read_flags(ctx, flags);
+  if (st) return st;
+  return sampling_flag_error(ctx, flags[0]);
+}
+
+int encode_into(adrom_session* s, const double* phi, const double* q, double* a) {
+  adrom_ctx* ctx = s->ctx;
+  double* partial = (double*)s->isvd_ws;  // first region of the iSVD workspace
+  double* out = s->rom_info + 16;         // r+1 doubles after the info block
+  const int pr = prof_begin(ctx, PROBE_ENCODE);
+  int st = ts_project(ctx, phi, s->N, s->r, 2, q, s->q_ref, s->d, out, partial, nullptr);
+  prof_end(ctx, pr);
+  if (st) return st;
+  ADROM_CK(ctx, cudaMemcpyAsync(a, out, sizeof(double) * s->r, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+  return ADROM_OK;
+}
+
+int rom_step(adrom_session* s) {
+  RomStepArgs A{};
+  A.op = s->op[s->opcur];
+  A.kind = s->cfg.model.kind;
+  A.bp = make_bp(s->cfg.model);
+  A.gamma = s->cfg.model.gamma;
+  A.a_prev = s->a;
+  A.a_out = s->a;
+  A.dt = s->cfg.dt;
+  A.tol = s->cfg.newton_tol;
+  A.max_iter = s->cfg.newton_max_iter;
+  A.work = s->rom_work;
+  A.info = s->rom_info;
+  int st = rom_step_async(s->ctx, A, s->cfg.projection == 0);
+  if (st) return st;
+  if (s->n_online < s->cap_steps) {
+    log_step_kernel<<<1, 1, 0, s->ctx->stream>>>(s->rom_info, s->step_log + 3 * s->n_online,
+                                                 s->n_online, s->fail_step);
+    ADROM_LAUNCH_CK(s->ctx);
+  }
+  return ADROM_OK;
+}
+
+// one adaptation event (driver.py:351-387, history-aware branch)
+int run_event(adrom_session* s, adrom_event_record& ev) {
+  adrom_ctx* ctx = s->ctx;
+  const adrom_model m = model_of(s);
+  ev.error = 0;
+  ev.residual_norm = 0.0;
+  // advance_signal: coarse backward-Euler step of size z*dt (driver.py:354-358)
+  adrom_newton_info ni{};
+  int st = fom_implicit_step(ctx, m, s->y_corr, s->cfg.z * s->cfg.dt, s->cfg.newton_tol,
+                             s->cfg.newton_max_iter, s->y_next, &ni);
+  if (st == ADROM_ERR_CUDA) return st;
+  if (st) {
+    ev.error = st;
+    return ADROM_OK;
+  }
+  std::swap(s->y_corr, s->y_next);
+  ev.coarse_converged = ni.converged;
+  ev.coarse_iterations = ni.iterations;
+  ev.pad = 1;  // coarse advance done (event dict carries coarse_* keys)
+  // y_hat = D (y - q_ref)
+  preprocess_kernel<<<(int)((s->N + 255) / 256 < ctx->num_sms * 8 ? (s->N + 255) / 256
+                                                                   : ctx->num_sms * 8),
+                      256, 0, ctx->stream>>>(s->y_corr, s->q_ref, s->d, s->N, s->y_hat);
+  ADROM_LAUNCH_CK(ctx);
+  // iSVD into the spare buffers
+  const int nxt = 1 - s->cur;
+  st = reset_flags(ctx);
+  if (st) return st;
+  st = isvd_update_async(ctx, s->phi[s->cur], s->sigma[s->cur], s->y_hat, s->N, s->r, s->r,
+                         s->cfg.lam, s->phi[nxt], s->sigma[nxt], s->gram[s->cur], s->gram[nxt],
+                         s->isvd_ws, ctx->dflags, ISVD_REORTH_RATIO, s->isvd_stats, nullptr,
+                         nullptr, nullptr, nullptr);
+  if (st) return st;
+  int flags[16];
+  ADROM_CK(ctx, cudaMemcpyAsync((char*)ctx->pinned + 512, s->isvd_stats, sizeof(double) * 8,
+                                cudaMemcpyDeviceToHost, ctx->stream));
+  st = read_flags(ctx, flags);
+  if (st) return st;
+  const double* hs = (const double*)((char*)ctx->pinned + 512);
+  if (flags[0] & 1) {
+    ev.error = ADROM_ERR_NONFINITE;
+    return ADROM_OK;
+  }
+  if (flags[0] & 8) {
+    ev.error = ADROM_ERR_NOCONV;
+    return ADROM_OK;
+  }
+  ev.residual_norm = hs[2];  // ||y - Phi Phi^T y|| with the old basis (driver.py:366-367)
+  // sampling + operator for the new basis (driver.py:369-374)
+  const int onx = 1 - s->opcur;
+  st = build_sampling_operator(s, s->phi[nxt], s->op[onx], s->y_corr);
+  if (st == ADROM_ERR_CUDA) return st;
+  if (st) {
+    ev.error = st;
+    return ADROM_OK;
+  }
+  // state transfer a = Phi'^T D (q~ - q_ref)  (driver.py:376)
+  st = encode_into(s, s->phi[nxt], s->q_tilde, s->a);
+  if (st) return st;
+  s->cur = nxt;
+  s->opcur = onx;
+  return ADROM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int adrom_session_create(adrom_ctx* ctx, const adrom_session_config* cfg, adrom_session** out) {
+  if (!ctx || !cfg || !out) return ADROM_ERR_ARG;
+  adrom_session* s = new adrom_session();
+  s->ctx = ctx;
+  s->cfg = *cfg;
+  s->N = cfg->model.n_elem * cfg->model.n_var;
+  s->r = cfg->r;
+  if (cfg->r < 1 || cfg->r > 110 || cfg->n_s < cfg->r || cfg->z < 1) {
+    delete s;
+    return set_error(ctx, ADROM_ERR_ARG, "session: bad r/n_s/z");
+  }
+  const int64_t N = s->N;
+  const int r = s->r;
+  for (int b = 0; b < 2; ++b) {
+    s->phi[b] = s->alloc_d((size_t)N * r);
+    s->sigma[b] = s->alloc_d(r);
+    s->gram[b] = s->alloc_d((size_t)r * r);
+  }
+  s->q_ref = s->alloc_d(N);
+  s->d = s->alloc_d(N);
+  s->y_corr = s->alloc_d(N);
+  s->y_next = s->alloc_d(N);
+  s->y_hat = s->alloc_d(N);
+  s->q_tilde = s->alloc_d(N);
+  s->a = s->alloc_d(r);
+  int st = alloc_op(s, s->op[0]);
+  if (!st) st = alloc_op(s, s->op[1]);
+  s->rom_work = s->alloc_d(rom_step_work_doubles(s->op[0]));
+  s->rom_info = s->alloc_d(16 + r + 1 + 16);
+  s->isvd_stats = s->alloc_d(16);
+  const size_t iws = isvd_workspace_bytes(ctx, N, r, r);
+  cudaMalloc(&s->isvd_ws, iws);
+  s->allocs.push_back(s->isvd_ws);
+  cudaMalloc(&s->qd_ws, qdeim_workspace_bytes(ctx, r, cfg->n_s));
+  s->allocs.push_back(s->qd_ws);
+  s->guess.r = r;
+  s->guess.max_chunks = (cfg->n_s + r - 1) / r;
+  if (s->guess.max_chunks > 64) s->guess.max_chunks = 64;
+  s->guess.rows = s->alloc_t<int64_t>((size_t)s->guess.max_chunks * r);
+  s->cap_steps = cfg->n_t > cfg->w_init ? cfg->n_t - cfg->w_init : 1;
+  s->step_log = s->alloc_d((size_t)s->cap_steps * 3);
+  s->fail_step = s->alloc_t<int>(1);
+  if (st || !s->phi[1] || !s->step_log || !s->fail_step || !s->qd_ws || !s->isvd_ws) {
+    for (void* p : s->allocs) cudaFree(p);
+    delete s;
+    return set_error(ctx, ADROM_ERR_CUDA, "session: device allocation failed (N=%lld r=%d)",
+                     (long long)N, r);
+  }
+  cudaMemsetAsync(s->fail_step, 0xff, sizeof(int), ctx->stream);  // -1
+  size_t need = fom_newton_workspace(cfg->model) + 4096;
+  st = ensure_scratch(ctx, need);
+  if (st) {
+    for (void* p : s->allocs) cudaFree(p);
+    delete s;
+    return st;
+  }
+  *out = s;
+  return ADROM_OK;
+}
+
+void adrom_session_destroy(adrom_session* s) {
+  if (!s) return;
+  cudaStreamSynchronize(s->ctx->stream);
+  for (void* p : s->allocs) cudaFree(p);
+  delete s;
+}
+
+// offline results (device pointers): q_ref, row scale d, basis phi0 (N x r),
+// sigma0 (r), q_last (= training[w_init]).  Copied into the session.
+int adrom_session_load(adrom_session* s, const double* q_ref, const double* d, const double* phi0,
+                       const double* sigma0, const double* q_last) {
+  if (!s) return ADROM_ERR_ARG;
+  adrom_ctx* ctx = s->ctx;
+  const size_t N = s->N;
+  ADROM_CK(ctx, cudaMemcpyAsync(s->q_ref, q_ref, 8 * N, cudaMemcpyDeviceToDevice, ctx->stream));
+  ADROM_CK(ctx, cudaMemcpyAsync(s->d, d, 8 * N, cudaMemcpyDeviceToDevice, ctx->stream));
+  ADROM_CK(ctx, cudaMemcpyAsync(s->phi[0], phi0, 8 * N * s->r, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+  ADROM_CK(ctx, cudaMemcpyAsync(s->sigma[0], sigma0, 8 * s->r, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+  int st = ts_gram(ctx, s->phi[0], s->N, s->r, s->gram[0], (double*)s->isvd_ws);
+  if (st) return st;
+  ADROM_CK(ctx, cudaMemcpyAsync(s->q_tilde, q_last, 8 * N, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+  ADROM_CK(ctx, cudaMemcpyAsync(s->y_corr, q_last, 8 * N, cudaMemcpyDeviceToDevice, ctx->stream));
+  s->cur = 0;
+  s->opcur = 0;
+  s->n_online = 0;
+  s->events.clear();
+  memset(s->guess.g, 0, sizeof(s->guess.g));
+  ADROM_CK(ctx, cudaMemsetAsync(s->fail_step, 0xff, sizeof(int), ctx->stream));
+  return ADROM_OK;
+}
+
+// driver.py:321-331: initial lookahead (adaptive or FGS), sampling, operator,
+// encode(q_last).  Errors here propagate (they are outside the event try).
+int adrom_session_start(adrom_session* s) {
+  if (!s) return ADROM_ERR_ARG;
+  adrom_ctx* ctx = s->ctx;
+  const adrom_model m = model_of(s);
+  const bool needs_signal = s->cfg.adaptive || s->cfg.sampling == 1;
+  if (needs_signal) {
+    adrom_newton_info ni{};
+    int st = fom_implicit_step(ctx, m, s->y_corr, s->cfg.z * s->cfg.dt, s->cfg.newton_tol,
+                               s->cfg.newton_max_iter, s->y_next, &ni);
+    if (st) return st;
+    std::swap(s->y_corr, s->y_next);
+  }
+  int st = build_sampling_operator(s, s->phi[s->cur], s->op[s->opcur], s->y_corr);
+  if (st) return st;
+  return encode_into(s, s->phi[s->cur], s->q_tilde, s->a);
+}
+
+// Advance n_steps online steps (driver.py:337-387).  For saved steps (every
+// `save_every`-th, counted from the first online step) the decoded state is
+// copied to dev_out (device, row-major) and/or host_out (pinned host).
+int adrom_session_advance(adrom_session* s, int64_t n_steps, int64_t save_every, double* dev_out,
+                          double* host_out, int64_t* n_saved) {
+  if (!s) return ADROM_ERR_ARG;
+  adrom_ctx* ctx = s->ctx;
+  int64_t saved = 0;
+  const int64_t N = s->N;
+  for (int64_t k = 0; k < n_steps; ++k) {
+    const int64_t n = s->cfg.w_init + s->n_online;  // driver loop index
+    int st = rom_step(s);
+    if (st) return st;
+    const int pr = prof_begin(ctx, PROBE_DECODE);
+    st = ts_decode(ctx, s->phi[s->cur], N, s->r, s->a, s->q_ref, s->d, s->q_tilde);
+    prof_end(ctx, pr);
+    if (st) return st;
+    ++s->n_online;
+    if (save_every > 0 && (s->n_online % save_every == 0 || k == n_steps - 1)) {
+      if (dev_out)
+        ADROM_CK(ctx, cudaMemcpyAsync(dev_out + saved * N, s->q_tilde, 8 * N,
+                                      cudaMemcpyDeviceToDevice, ctx->stream));
+      if (host_out)
+        ADROM_CK(ctx, cudaMemcpyAsync(host_out + saved * N, s->q_tilde, 8 * N,
+                                      cudaMemcpyDeviceToHost, ctx->stream));
+      ++saved;
+    }
+    const bool at_event = s->cfg.adaptive && ((n + 1 - s->cfg.w_init) % s->cfg.z == 0);
+    if (at_event) {
+      adrom_event_record ev{};
+      ev.step = n + 1;
+      st = run_event(s, ev);
+      if (st) return st;
+      s->events.push_back(ev);
+      // a failed reduced step aborts the run like the reference (driver.py:338)
+      int fs = -1;
+      ADROM_CK(ctx, cudaMemcpyAsync(ctx->pinned, s->fail_step, sizeof(int),
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+      ADROM_CK(ctx, cudaStreamSynchronize(ctx->stream));
+      memcpy(&fs, ctx->pinned, sizeof(int));
+      if (fs >= 0)
+        return set_error(ctx, ADROM_ERR_ROMSTEP, "rank-deficient sampled Jacobian at online step %d",
+                         fs + (int)s->cfg.w_init + 1);
+    }
+  }
+  if (n_saved) *n_saved = saved;
+  return ADROM_OK;
+}
+
+int adrom_session_finish(adrom_session* s) {
+  if (!s) return ADROM_ERR_ARG;
+  adrom_ctx* ctx = s->ctx;
+  int fs = -1;
+  ADROM_CK(ctx, cudaMemcpyAsync(ctx->pinned, s->fail_step, sizeof(int), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+  ADROM_CK(ctx, cudaStreamSynchronize(ctx->stream));
+  memcpy(&fs, ctx->pinned, sizeof(int));
+  if (fs >= 0)
+    return set_error(ctx, ADROM_ERR_ROMSTEP, "rank-deficient sampled Jacobian at online step %d",
+                     fs + (int)s->cfg.w_init + 1);
+  return ADROM_OK;
+}
+
+int adrom_session_read(adrom_session* s, double* host_step_log, int64_t max_steps,
+                       adrom_event_record* host_events, int64_t max_events, int64_t* n_steps,
+                       int64_t* n_events, double* dev_a, double* dev_phi, double* dev_sigma,
+                       double* dev_q_tilde) {
+  if (!s) return ADROM_ERR_ARG;
+  adrom_ctx* ctx = s->ctx;
+  const int64_t ns = s->n_online < max_steps ? s->n_online : max_steps;
+  if (host_step_log && ns > 0)
+    ADROM_CK(ctx, cudaMemcpyAsync(host_step_log, s->step_log, sizeof(double) * 3 * ns,
+                                  cudaMemcpyDeviceToHost, ctx->stream));
+  if (dev_a)
+    ADROM_CK(ctx, cudaMemcpyAsync(dev_a, s->a, 8 * s->r, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (dev_phi)
+    ADROM_CK(ctx, cudaMemcpyAsync(dev_phi, s->phi[s->cur], 8 * (size_t)s->N * s->r,
+                                  cudaMemcpyDeviceToDevice, ctx->stream));
+  if (dev_sigma)
+    ADROM_CK(ctx, cudaMemcpyAsync(dev_sigma, s->sigma[s->cur], 8 * s->r, cudaMemcpyDeviceToDevice,
+                                  ctx->stream));
+  if (dev_q_tilde)
+    ADROM_CK(ctx, cudaMemcpyAsync(dev_q_tilde, s->q_tilde, 8 * (size_t)s->N,
+                                  cudaMemcpyDeviceToDevice, ctx->stream));
+  ADROM_CK(ctx, cudaStreamSynchronize(ctx->stream));
+  const int64_t ne = (int64_t)s->events.size() < max_events ? (int64_t)s->events.size() : max_events;
+  if (host_events)
+    for (int64_t i = 0; i < ne; ++i) host_events[i] = s->events[i];
+  if (n_steps) *n_steps = s->n_online;
+  if (n_events) *n_events = (int64_t)s->events.size();
+  return ADROM_OK;
+}
+
+int adrom_session_sampling(adrom_session* s, int64_t* dev_idx) {
+  if (!s) return ADROM_ERR_ARG;
+  ADROM_CK(s->ctx, cudaMemcpyAsync(dev_idx, s->op[s->opcur].idx, sizeof(int64_t) * s->cfg.n_s,
+                                   cudaMemcpyDeviceToDevice, s->ctx->stream));
+  return ADROM_OK;
+}
+
+// ---- stateless entry points ---------------------------------------------
+int adrom_qdeim(adrom_ctx* ctx, const double* phi, int64_t n, int32_t r, int32_t n_s,
+                int64_t* idx) {
+  if (!ctx) return ADROM_ERR_ARG;
+  int st = ensure_scratch(ctx, qdeim_workspace_bytes(ctx, r, n_s) + 4096);
+  if (st) return st;
+  return qdeim_select(ctx, phi, n, r, n_s, idx, nullptr, ctx->scratch, nullptr);
+}
+
+int adrom_fgs(adrom_ctx* ctx, const adrom_model* m, const double* phi, int32_t r,
+              const double* y_corr, int32_t n_s, int32_t n_extra, int32_t feature, int64_t* idx) {
+  if (!ctx || !m) return ADROM_ERR_ARG;
+  if (n_extra > n_s) return set_error(ctx, ADROM_ERR_ARG, "n_extra cannot exceed the total number of sampling points");
+  const int64_t N = m->n_elem * m->n_var;
+  const int n_base = n_s - n_extra;
+  int st = ensure_scratch(ctx, qdeim_workspace_bytes(ctx, r, n_s) + 4096);
+  if (st) return st;
+  if (n_base > 0) {
+    st = qdeim_select(ctx, phi, N, r, n_base, idx, nullptr, ctx->scratch, nullptr);
+    if (st) return st;
+  }
+  st = reset_flags(ctx);
+  if (st) return st;
+  st = fgs_extend(ctx, *m, y_corr, feature, idx, n_base, n_extra, nullptr);
+  if (st) return st;
+  int flags[16];
+  st = read_flags(ctx, flags);
+  if (st) return st;
+  return sampling_flag_error(ctx, flags[0]);
+}
+
+int adrom_deim_operator(adrom_ctx* ctx, const double* phi, int64_t n, int32_t r, const int64_t* idx,
+                        int32_t n_s, double* pinv) {
+  if (!ctx) return ADROM_ERR_ARG;
+  (void)n;
+  int st = ensure_scratch(ctx, sizeof(double) * (size_t)n_s * r + 4096);
+  if (st) return st;
+  st = reset_flags(ctx);
+  if (st) return st;
+  st = deim_pinv_only(ctx, phi, idx, n_s, r, (double*)ctx->scratch, pinv, ctx->dflags);
+  if (st) return st;
+  int flags[16];
+  st = read_flags(ctx, flags);
+  if (st) return st;
+  return sampling_flag_error(ctx, flags[0]);
+}
+
+int adrom_rom_operator_build(adrom_ctx* ctx, const adrom_model* m, const double* phi, int64_t n,
+                             const double* q_ref, const double* d, const int64_t* idx,
+                             int32_t n_s, adrom_rom_op* op) {
+  if (!ctx || !m || !op) return ADROM_ERR_ARG;
+  (void)n;
+  if (n_s < 1 || n_s > op->ns_cap || op->nc_cap < 3 * n_s * m->n_var)
+    return set_error(ctx, ADROM_ERR_ARG, "rom_operator_build: capacities too small");
+  int st = reset_flags(ctx);
+  if (st) return st;
+  if (idx && idx != op->idx) {
+    copy_i64_kernel<<<1, 256, 0, ctx->stream>>>(idx, op->idx, n_s);
+    ADROM_LAUNCH_CK(ctx);
+  }
+  st = plan_build(ctx, *m, *op, n_s, ctx->dflags);
+  if (st) return st;
+  st = operator_fill(ctx, *op, phi, q_ref, d, n_s, ctx->dflags);
+  if (st) return st;
+  int flags[16];
+  st = read_flags(ctx, flags);
+  if (st) return st;
+  return sampling_flag_error(ctx, flags[0]);
+}
+
+int adrom_rom_step(adrom_ctx* ctx, const adrom_model* m, const adrom_rom_op* op, int32_t kind,
+                   const double* a_prev, double dt, double tol, int32_t max_iter, double* a_out,
+                   adrom_rom_step_info* host_info) {
+  if (!ctx || !m || !op) return ADROM_ERR_ARG;
+  const size_t wd = rom_step_work_doubles(*op);
+  int st = ensure_scratch(ctx, sizeof(double) * (wd + 64));
+  if (st) return st;
+  RomStepArgs A{};
+  A.op = *op;
+  A.kind = m->kind;
+  A.bp = make_bp(*m);
+  A.gamma = m->gamma;
+  A.a_prev = a_prev;
+  A.a_out = a_out;
+  A.dt = dt;
+  A.tol = tol;
+  A.max_iter = max_iter;
+  A.work = (double*)ctx->scratch;
+  A.info = A.work + wd;
+  st = rom_step_async(ctx, A, kind == 0);
+  if (st) return st;
+  ADROM_CK(ctx, cudaMemcpyAsync(ctx->pinned, A.info, sizeof(double) * 8, cudaMemcpyDeviceToHost,
+                                ctx->stream));
+  ADROM_CK(ctx, cudaStreamSynchronize(ctx->stream));
+  const double* hi = (const double*)ctx->pinned;
+  if (hi[4] != 0.0) {
+    if (kind == 0)
+      return set_error(ctx, ADROM_ERR_ROMSTEP,
+                       "rank-deficient sampled Jacobian at iteration %d (condition number %.3e)",
+                       (int)hi[1], hi[3]);
+    return set_error(ctx, ADROM_ERR_ROMSTEP, "singular reduced Jacobian at iteration %d", (int)hi[1]);
+  }
+  if (host_info) {
+    host_info->converged = (int)hi[0];
+    host_info->iterations = (int)hi[1];
+    host_info->residual_norm = hi[2];
+  }
+  return ADROM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,369 @@
+"""Experiment driver with the reference API (``adrom/driver.py``), running the
+online loop as a device-resident session (``adrom_session_*``).
+
+``run_adaptive_rom`` / ``run_static_rom`` keep the reference contract
+(``ExperimentConfig`` -> ``RunResult``; driver.py:63-165, 291-423).  The
+offline stage (training window, scaling, POD) runs on the GPU before the
+timed region exactly where the reference computes it; the timed region is
+the reference's (driver.py:319-389): initial lookahead, sampling, operator,
+encode, and every online step with its adaptation events.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _dev
+from ._lib import Context, EventRecord, SessionConfig, _p, ptr
+from .errors import DenseError, RomStepError
+from .fom import BurgersProblem, FomProblem, SodProblem, TimeStepper, implicit_step
+from .snapshots import ScalingTransform, fit_scaling, pod
+from .tracking import UpdateRule
+
+__all__ = ["ExperimentConfig", "RunResult", "make_problem", "run_fom", "run_static_rom",
+           "run_adaptive_rom", "relative_error", "acceleration", "Session"]
+
+CONSUME_LOOKAHEAD = True  # driver.py:60 (history-aware rules consume the new snapshot)
+
+_ERR_NAMES = {1: "DenseError", 2: "DenseError", 3: "RomStepError", 4: "ValueError",
+              6: "DenseError", 7: "DenseError"}
+
+
+@dataclass(frozen=True)
+class ExperimentConfig:
+    """driver.py:63-120."""
+
+    model: str = "burgers"
+    n_elem: int = 1000
+    nu: float = 0.01
+    gamma: float = 1.4
+    dt: float = 1e-3
+    n_t: int = 500
+    mode: str = "adaptive"
+    projection: str = "lspg"
+    sampling: str = "qdeim"
+    feature: str = "pressure-gradient"
+    n_extra: int = 0
+    r: int = 4
+    n_s: int = 4
+    w_init: int = 4
+    z: int = 10
+    rule: UpdateRule = field(default_factory=lambda: UpdateRule("isvd", lam=0.1))
+    cadence: str = "every-event"
+    seed: int = 0
+    save_stride: int = 10
+    save_times: tuple = ()
+    timing_repeats: int = 1
+    newton_tol: float = 1e-8
+    newton_max_iter: int = 10
+    label: str = ""
+
+    def __post_init__(self):
+        if self.model not in ("burgers", "sod"):
+            raise ValueError(f"unknown model {self.model!r}")
+        if self.mode not in ("fom", "static", "adaptive"):
+            raise ValueError(f"unknown mode {self.mode!r}")
+        if self.projection not in ("galerkin", "lspg"):
+            raise ValueError(f"unknown projection {self.projection!r}")
+        if self.sampling not in ("qdeim", "fgs"):
+            raise ValueError(f"unknown sampling {self.sampling!r}")
+        if self.cadence not in ("every-event", "every-step"):
+            raise ValueError(f"unknown cadence {self.cadence!r}")
+        if self.w_init < self.r:
+            raise ValueError("w_init must be at least r")
+        if self.n_s < self.r:
+            raise ValueError("n_s must be at least r")
+        if self.z < 1:
+            raise ValueError("z must be at least 1")
+        if self.n_t < self.w_init:
+            raise ValueError("horizon must cover the offline window")
+        if self.n_extra > self.n_s:
+            raise ValueError("n_extra cannot exceed n_s")
+
+    @property
+    def n_events(self) -> int:
+        return (self.n_t - self.w_init) // self.z
+
+    def stepper(self) -> TimeStepper:
+        return TimeStepper(dt=self.dt, newton_tol=self.newton_tol,
+                           newton_max_iter=self.newton_max_iter)
+
+
+def make_problem(config: ExperimentConfig) -> FomProblem:
+    """driver.py:123-126."""
+    if config.model == "burgers":
+        return BurgersProblem(config.n_elem, nu=config.nu)
+    return SodProblem(config.n_elem, gamma=config.gamma)
+
+
+@dataclass
+class RunResult:
+    """driver.py:129-165.  ``trajectory`` holds every ``keep_every``-th state
+    (all of them by default, like the reference); ``trajectory_steps`` names
+    the rows."""
+
+    config: ExperimentConfig
+    kind: str
+    trajectory: np.ndarray
+    wall_seconds: float
+    var_names: tuple
+    newton_failures: list = field(default_factory=list)
+    error_steps: np.ndarray | None = None
+    errors: np.ndarray | None = None
+    event_log: list = field(default_factory=list)
+    signal_steps: np.ndarray | None = None
+    signal_errors: np.ndarray | None = None
+    acceleration: float | None = None
+    trajectory_steps: np.ndarray | None = None
+    step_iterations: np.ndarray | None = None
+
+    def time_averaged_error(self, var=0) -> float:
+        if self.errors is None or self.errors.size == 0:
+            raise ValueError("run carries no error history")
+        j = self.var_names.index(var) if isinstance(var, str) else var
+        return float(self.errors[:, j].mean())
+
+    def saved_steps(self) -> np.ndarray:
+        stride = max(1, self.config.save_stride)
+        steps = np.arange(0, self.trajectory.shape[0], stride)
+        if steps[-1] != self.trajectory.shape[0] - 1:
+            steps = np.append(steps, self.trajectory.shape[0] - 1)
+        return steps
+
+
+def relative_error(pred, truth) -> float:
+    """driver.py:168-175."""
+    tn = float(np.linalg.norm(truth))
+    dn = float(np.linalg.norm(np.asarray(pred) - np.asarray(truth)))
+    return dn if tn == 0.0 else dn / tn
+
+
+def acceleration(t_fom: float, t_rom: float) -> float:
+    """driver.py:178-182."""
+    if t_rom <= 0:
+        raise ValueError("ROM wall-clock time must be positive")
+    return t_fom / t_rom
+
+
+def _per_variable_errors(model, pred, truth) -> np.ndarray:
+    pf = model.primitive_fields(pred)
+    tf = model.primitive_fields(truth)
+    return np.array([relative_error(pf[v], tf[v]) for v in model.var_names])
+
+
+def run_fom(config: ExperimentConfig, keep_every: int = 1, problem: FomProblem | None = None) -> RunResult:
+    """driver.py:202-229 — fine-step backward Euler on the device."""
+    model = problem or make_problem(config)
+    stepper = config.stepper()
+    walls = []
+    for _ in range(max(1, config.timing_repeats)):
+        q = _dev.dev(model.initial_state())
+        rows = [q.clone()]
+        failures = []
+        _dev.torch().cuda.synchronize()
+        t0 = time.perf_counter()
+        for n in range(config.n_t):
+            res = implicit_step(model, q, config.dt, stepper)
+            if not res.converged:
+                failures.append(n + 1)
+            q = res.x
+            if (n + 1) % keep_every == 0 or n + 1 == config.n_t:
+                rows.append(q.clone())
+        _dev.torch().cuda.synchronize()
+        walls.append(time.perf_counter() - t0)
+    traj = _dev.host(_dev.torch().stack(rows))
+    return RunResult(config=config, kind="fom", trajectory=traj, wall_seconds=float(np.mean(walls)),
+                     var_names=model.var_names, newton_failures=failures)
+
+
+def _training_states(config, model, truth):
+    """driver.py:250-261 (device)."""
+    t = _dev.torch()
+    if truth is not None:
+        return _dev.dev(np.asarray(truth[: config.w_init + 1]) if not _dev.is_device(truth)
+                        else truth[: config.w_init + 1])
+    stepper = config.stepper()
+    states = [_dev.dev(model.initial_state())]
+    for _ in range(config.w_init):
+        states.append(implicit_step(model, states[-1], config.dt, stepper).x)
+    return t.stack(states)
+
+
+def offline_stage(config, model, truth=None):
+    """driver.py:296-300: training window, scaling, POD (device, untimed)."""
+    t = _dev.torch()
+    training = _training_states(config, model, truth)
+    if model.n_var == 1:  # driver.py:232-247
+        scaling = ScalingTransform(q_ref=training[0].clone(), phi_norm=t.ones(1, dtype=t.float64, device="cuda"))
+    else:
+        scaling = fit_scaling(list(training), model.n_var)
+    d = scaling.row_scale
+    y_train = (d[None, :] * (training - scaling.q_ref[None, :])).T.contiguous()
+    basis0 = pod(y_train, config.r)
+    return training, scaling, basis0
+
+
+class Session:
+    """Python handle of an ``adrom_session`` (device-resident online loop)."""
+
+    def __init__(self, config: ExperimentConfig, model: FomProblem, adaptive: bool):
+        if adaptive and config.rule.kind != "isvd":
+            raise NotImplementedError(
+                f"update rule {config.rule.kind!r} is outside the B200 hot path (only isvd)")
+        if config.cadence != "every-event":
+            raise NotImplementedError("only the every-event cadence is on the B200 path")
+        self.ctx = Context.get()
+        self.config = config
+        self.model = model
+        cfg = SessionConfig()
+        cfg.model = model.abi()
+        cfg.r, cfg.n_s, cfg.n_extra, cfg.z = config.r, config.n_s, config.n_extra, config.z
+        cfg.projection = 0 if config.projection == "lspg" else 1
+        cfg.sampling = 0 if config.sampling == "qdeim" else 1
+        cfg.feature = 0 if config.feature == "pressure-gradient" else 1
+        cfg.adaptive = 1 if adaptive else 0
+        cfg.newton_max_iter = config.newton_max_iter
+        cfg.w_init, cfg.n_t = config.w_init, config.n_t
+        cfg.dt, cfg.lam, cfg.newton_tol = config.dt, config.rule.lam, config.newton_tol
+        if config.sampling == "fgs" and config.feature not in ("pressure-gradient", "velocity-gradient"):
+            raise ValueError(f"unknown feature map {config.feature!r}")
+        self.cfg = cfg
+        h = _p()
+        self.ctx.check(self.ctx.lib.adrom_session_create(self.ctx.handle, C.byref(cfg), C.byref(h)),
+                       "adrom_session_create")
+        self.handle = h
+        self.n_dof = model.n_dof
+
+    def close(self):
+        if self.handle:
+            self.ctx.lib.adrom_session_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    def load(self, scaling, basis0, q_last):
+        self._keep = [_dev.dev(scaling.q_ref), _dev.dev(scaling.row_scale), _dev.dev(basis0.phi),
+                      _dev.dev(basis0.sigma), _dev.dev(q_last)]
+        self.ctx.scall("adrom_session_load", self.handle, *(ptr(x) for x in self._keep))
+
+    def start(self):
+        self.ctx.scall("adrom_session_start", self.handle)
+
+    def advance(self, n_steps, save_every=0, dev_out=None, host_out=None) -> int:
+        n_saved = C.c_int64(0)
+        self.ctx.scall("adrom_session_advance", self.handle, C.c_int64(n_steps),
+                       C.c_int64(save_every), ptr(dev_out), ptr(host_out), C.byref(n_saved))
+        return int(n_saved.value)
+
+    def finish(self):
+        self.ctx.scall("adrom_session_finish", self.handle)
+
+    def read(self, max_steps, max_events):
+        t = _dev.torch()
+        log = np.zeros((max(max_steps, 1), 3))
+        evs = (EventRecord * max(max_events, 1))()
+        ns, ne = C.c_int64(0), C.c_int64(0)
+        r = self.config.r
+        a = t.empty(r, dtype=t.float64, device="cuda")
+        sig = t.empty(r, dtype=t.float64, device="cuda")
+        q = t.empty(self.n_dof, dtype=t.float64, device="cuda")
+        self.ctx.scall("adrom_session_read", self.handle, log.ctypes.data_as(_p), C.c_int64(max_steps),
+                       evs, C.c_int64(max_events), C.byref(ns), C.byref(ne), ptr(a), None, ptr(sig),
+                       ptr(q))
+        return log[: ns.value], list(evs)[: ne.value], a, sig, q
+
+    def basis(self):
+        t = _dev.torch()
+        phi = t.empty(self.n_dof, self.config.r, dtype=t.float64, device="cuda")
+        self.ctx.scall("adrom_session_read", self.handle, None, C.c_int64(0), None, C.c_int64(0),
+                       None, None, None, ptr(phi), None, None)
+        return phi
+
+    def sampling(self):
+        t = _dev.torch()
+        idx = t.empty(self.config.n_s, dtype=t.int64, device="cuda")
+        self.ctx.scall("adrom_session_sampling", self.handle, ptr(idx))
+        return idx
+
+
+def _event_dicts(events):
+    out = []
+    for i, e in enumerate(events):
+        d = {"event": i + 1, "step": int(e.step)}
+        if e.pad:
+            d["coarse_converged"] = bool(e.coarse_converged)
+            d["coarse_iterations"] = int(e.coarse_iterations)
+        if e.error:
+            d["update_error"] = f"{_ERR_NAMES.get(e.error, 'RuntimeError')}: status {e.error}"
+        else:
+            d["residual_norm"] = float(e.residual_norm)
+        out.append(d)
+    return out
+
+
+def _run_rom(config: ExperimentConfig, truth, adaptive: bool, problem=None, keep_every: int = 1,
+             offline=None):
+    model = problem or make_problem(config)
+    t = _dev.torch()
+    training, scaling, basis0 = offline_stage(config, model, truth)
+    if offline is not None:  # injected offline results (parity runs: same POD as the oracle)
+        scaling, basis0 = offline
+    q_last = training[config.w_init]
+    n_online = config.n_t - config.w_init
+    n_keep = 0 if keep_every <= 0 else (n_online + keep_every - 1) // keep_every
+    host_buf = t.empty((max(n_keep, 1), model.n_dof), dtype=t.float64, pin_memory=True)
+    sess = Session(config, model, adaptive)
+    walls = []
+    try:
+        for _ in range(max(1, config.timing_repeats)):
+            sess.load(scaling, basis0, q_last)
+            t.cuda.synchronize()
+            t0 = time.perf_counter()                        # driver.py:319
+            sess.start()
+            n_saved = sess.advance(n_online, keep_every, None, host_buf if n_keep else None)
+            sess.finish()
+            t.cuda.synchronize()
+            walls.append(time.perf_counter() - t0)          # driver.py:389
+        log, events, a_fin, sig_fin, _ = sess.read(n_online, max(config.n_events, 1))
+    finally:
+        sess.close()
+    train_h = _dev.host(training)
+    if keep_every == 1:
+        traj = np.concatenate([train_h, host_buf.numpy()[:n_saved]], axis=0)
+        steps = np.arange(config.n_t + 1)
+    else:
+        traj = host_buf.numpy()[:n_saved].copy()
+        steps = config.w_init + np.minimum(np.arange(1, n_saved + 1) * keep_every, n_online)
+    failures = [config.w_init + 1 + i for i in range(len(log)) if log[i, 0] == 0.0]
+    error_steps = errors = None
+    if truth is not None and keep_every == 1:
+        truth_h = _dev.host(truth)
+        error_steps = np.arange(config.w_init + 1, config.n_t + 1)
+        errors = np.array([_per_variable_errors(model, traj[n], truth_h[n]) for n in error_steps])
+    return RunResult(config=config, kind="adaptive" if adaptive else "static", trajectory=traj,
+                     wall_seconds=float(np.mean(walls)), var_names=model.var_names,
+                     newton_failures=failures, error_steps=error_steps, errors=errors,
+                     event_log=_event_dicts(events) if adaptive else [],
+                     trajectory_steps=steps, step_iterations=log[:, 1].astype(int))
+
+
+def run_static_rom(config: ExperimentConfig, truth=None, *, problem=None, keep_every: int = 1,
+                   offline=None):
+    """driver.py:413-416."""
+    return _run_rom(config, truth, adaptive=False, problem=problem, keep_every=keep_every,
+                    offline=offline)
+
+
+def run_adaptive_rom(config: ExperimentConfig, truth=None, *, problem=None, keep_every: int = 1,
+                     offline=None):
+    """driver.py:419-423 — the north-star path."""
+    return _run_rom(config, truth, adaptive=True, problem=problem, keep_every=keep_every,
+                    offline=offline)

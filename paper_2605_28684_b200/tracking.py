@@ -109,7 +109,7 @@ def isvd_update(basis: ReducedBasis, y_hat, lam: float, r: int) -> ReducedBasis:
     info = IsvdInfo()
     Context.get().call("adrom_isvd_update", ptr(phi), ptr(sigma), ptr(y), C.c_int64(n),
                        C.c_int32(r_cur), C.c_int32(r), C.c_double(lam), ptr(phi_out),
-                       ptr(sigma_out), C.byref(info))
+                       ptr(sigma_out), None, C.byref(info))
     _last_info.update(qnorm=info.qnorm, ynorm=info.ynorm, proj_resid=info.proj_resid,
                       degenerate=bool(info.degenerate),
                       reorthogonalised=bool(info.reorthogonalised), sweeps=info.sweeps)

@@ -287,7 +287,8 @@ def run_loop(name, cfg, ic=None):
             driver.make_problem = orig
     ev = [{k: (v if not isinstance(v, (np.bool_, bool)) else bool(v)) for k, v in e.items()}
           for e in res.event_log]
-    env_state, env_sigma = _envelope(cfg, truth.trajectory, res.trajectory, np.array(rec.sigma), ic)
+    env_state, env_sigma, env_samp = _envelope(cfg, truth.trajectory, res.trajectory,
+                                               np.array(rec.sigma), ic, rec.samplings)
     save(name, truth=truth.trajectory, traj=res.trajectory,
          sigma=np.array(rec.sigma), a=np.array([s[0] for s in rec.steps]),
          it=np.array([s[1] for s in rec.steps]), conv=np.array([s[2] for s in rec.steps]),
@@ -295,19 +296,24 @@ def run_loop(name, cfg, ic=None):
          else np.array(rec.samplings),
          errors=res.errors, events=np.array(json.dumps(ev, default=float)),
          failures=np.array(res.newton_failures, dtype=np.int64),
-         env_state=env_state, env_sigma=env_sigma)
+         env_state=env_state, env_sigma=env_sigma, env_samp_stable=env_samp)
 
 
-def _envelope(cfg, truth, traj, sigma, ic, seeds=(1, 2, 3)):
-    """The reference's own sensitivity: rerun it with every coarse Newton
-    result nudged by one ulp at random entries (a perturbation the size of
-    the rounding difference between two exact linear solvers) and record
-    the per-step relative state spread and per-event sigma spread (max over
-    seeds).  Trajectory-level parity gates are expressed relative to this
-    envelope: an implementation differing from the reference only in
-    rounding cannot be held to a tighter bound than the reference's
-    sensitivity to its own rounding."""
+def _envelope(cfg, truth, traj, sigma, ic, samplings, seeds=(1, 2, 3, 4, 5)):
+    """The reference's own sensitivity to rounding-level perturbations at the
+    places where any other implementation's arithmetic necessarily differs
+    from numpy/LAPACK's: every coarse Newton result, every iSVD output
+    (basis and singular values), every reduced-step result and every state
+    transfer are nudged by one ulp at random entries.
+    Records the per-step relative state spread and the per-event sigma
+    spread (max over seeds).  Trajectory-level parity gates are expressed
+    relative to this envelope: an implementation that differs from the
+    reference only in rounding cannot be held to a tighter bound than the
+    reference's sensitivity to its own rounding."""
     orig_coarse = driver.coarse_step
+    orig_isvd = driver.isvd_update
+    orig_step = driver.rom_step
+    orig_encode = driver.encode
     if ic is not None:
         class Custom(fom.BurgersProblem):
             def initial_state(self):
@@ -316,34 +322,66 @@ def _envelope(cfg, truth, traj, sigma, ic, seeds=(1, 2, 3)):
         driver.make_problem = lambda c: Custom(c.n_elem, nu=c.nu)
     worst_state = np.zeros(traj.shape[0])
     worst_sigma = np.zeros(sigma.shape)
+    stable = np.ones(len(samplings), dtype=bool)  # sampling decision unchanged by the nudges
+
+    def nudge(rng, x):
+        mask = rng.random(x.shape) < 0.5
+        return np.where(mask, np.nextafter(x, np.inf), x)
+
     try:
         for seed in seeds:
             rng = np.random.default_rng(seed)
 
             def nudged(model, y, z, dt, stepper=None):
                 res = orig_coarse(model, y, z, dt, stepper)
-                mask = rng.random(res.x.size) < 0.5
-                res.x = np.where(mask, np.nextafter(res.x, np.inf), res.x)
+                res.x = nudge(rng, res.x)
                 return res
 
+            def isvd_nudged(basis, y_hat, lam, r):
+                out = orig_isvd(basis, y_hat, lam, r)
+                return tracking.ReducedBasis(phi=nudge(rng, out.phi), sigma=nudge(rng, out.sigma))
+
+            def step_nudged(op, model, state, dt, tol=1e-8, max_iter=10):
+                out = orig_step(op, model, state, dt, tol=tol, max_iter=max_iter)
+                st = projection.ReducedState(a=nudge(rng, out.state.a), n=out.state.n)
+                return projection.RomStepResult(state=st, converged=out.converged,
+                                                iterations=out.iterations,
+                                                residual_norm=out.residual_norm)
+
+            def encode_nudged(q, op, n=0):
+                out = orig_encode(q, op, n)
+                return projection.ReducedState(a=nudge(rng, out.a), n=out.n)
+
             driver.coarse_step = nudged
+            driver.isvd_update = isvd_nudged
+            driver.rom_step = step_nudged
+            driver.encode = encode_nudged
             rec = _Recorder()
-            undo = rec.install()
+            undo = rec.install()  # records the nudged iSVD outputs
             try:
                 out = driver.run_adaptive_rom(cfg, truth=truth)
             finally:
                 undo()
                 driver.coarse_step = orig_coarse
+                driver.isvd_update = orig_isvd
+                driver.rom_step = orig_step
+                driver.encode = orig_encode
             dev = np.linalg.norm(out.trajectory - traj, axis=1) / np.linalg.norm(traj, axis=1)
             worst_state = np.maximum(worst_state, dev)
             sg = np.array(rec.sigma)
             if sg.shape == sigma.shape:
                 worst_sigma = np.maximum(worst_sigma, np.abs(sg / sigma - 1.0))
+            for k, (a, b) in enumerate(zip(rec.samplings, samplings)):
+                if list(a) != list(b):
+                    stable[k] = False
     finally:
         driver.coarse_step = orig_coarse
+        driver.isvd_update = orig_isvd
+        driver.rom_step = orig_step
+        driver.encode = orig_encode
         if ic is not None:
             driver.make_problem = orig_mp
-    return worst_state, worst_sigma
+    return worst_state, worst_sigma, stable
 
 
 def loops():
