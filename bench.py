@@ -509,7 +509,7 @@ def cpu_baseline_rom(case, steps=3, n_sample=None, timed_steps=None):
     n_sample = n_sample or min(case.n_elem, 1 << 14 if case.model == "sod" else 1 << 16)
     small = case.scaled(n_elem=n_sample)
     m = physics.Model(small.model, small.n_elem, nu=small.nu, gamma=small.gamma)
-    w_init = min(small.w_init, 64)
+    w_init = small.w_init
     ocfg = online.LoopConfig(model=m, dt=small.dt, n_t=w_init + steps + 1, w_init=w_init, r=small.r,
                              n_s=small.n_s, z=small.z, lam=small.lam, projection=small.projection,
                              sampling=small.sampling, feature=small.feature, n_extra=small.n_extra)

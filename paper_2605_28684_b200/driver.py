@@ -344,7 +344,7 @@ def _run_rom(config: ExperimentConfig, truth, adaptive: bool, problem=None, keep
         steps = config.w_init + np.minimum(np.arange(1, n_saved + 1) * keep_every, n_online)
     failures = [config.w_init + 1 + i for i in range(len(log)) if log[i, 0] == 0.0]
     error_steps = errors = None
-    if truth is not None and keep_every == 1:
+    if truth is not None and keep_every == 1 and len(truth) > config.n_t:
         truth_h = _dev.host(truth)
         error_steps = np.arange(config.w_init + 1, config.n_t + 1)
         errors = np.array([_per_variable_errors(model, traj[n], truth_h[n]) for n in error_steps])
