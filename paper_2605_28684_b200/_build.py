@@ -35,6 +35,7 @@ UNITS = {
     "btsolve.cu": [],
     "linalg.cu": [],
     "sampling.cu": [],
+    "qdeim.cu": [],
     "session.cu": [],
     "capi.cu": [],
 }

@@ -587,17 +587,21 @@ int ts_rotate(adrom_ctx* ctx, const RotArgs& a) {
 // ---------------------------------------------------------------------------
 // Gram matrix G = Phi^T Phi (tracked across updates; computed afresh once)
 // ---------------------------------------------------------------------------
+// 16 x 16 thread grid; thread (ti, tj) owns G[ti + 16 a][tj + 16 b],
+// a, b < RB = ceil(r / 16): register accumulators, rows staged in smem
+template <int RB>
 __global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ phi, int64_t n,
                                                    int r, double* __restrict__ partial) {
   extern __shared__ double sm[];
-  const int T = 64;
+  constexpr int T = 64;
   const int S = r | 1;
-  double* tile = sm;  // T x S
-  const int tid = threadIdx.x;
-  const int rr2 = r * r;
-  double acc[64];
-  const int mine = (rr2 + 255) / 256;
-  for (int k = 0; k < mine && k < 64; ++k) acc[k] = 0.0;
+  double* tile = sm;  // T x S, zero-padded to 16 * RB columns
+  const int tid = threadIdx.x, ti = tid & 15, tj = tid >> 4;
+  double acc[RB][RB];
+#pragma unroll
+  for (int x = 0; x < RB; ++x)
+#pragma unroll
+    for (int y = 0; y < RB; ++y) acc[x][y] = 0.0;
   const int64_t ntiles = (n + T - 1) / T;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int64_t row0 = t * T;
@@ -608,19 +612,29 @@ __global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ ph
       tile[a * S + c] = phi[row0 * r + e];
     }
     __syncthreads();
-    for (int k = 0; k < mine && k < 64; ++k) {
-      const int e = tid + 256 * k;
-      if (e >= rr2) break;
-      const int i = e / r, j = e - i * r;
-      double s = acc[k];
-      for (int a = 0; a < rows; ++a) s = fma(tile[a * S + i], tile[a * S + j], s);
-      acc[k] = s;
+    for (int a = 0; a < rows; ++a) {
+      const double* row = tile + a * S;
+      double u[RB], v[RB];
+#pragma unroll
+      for (int x = 0; x < RB; ++x) {
+        const int i = ti + 16 * x, j = tj + 16 * x;
+        u[x] = (i < r) ? row[i] : 0.0;
+        v[x] = (j < r) ? row[j] : 0.0;
+      }
+#pragma unroll
+      for (int x = 0; x < RB; ++x)
+#pragma unroll
+        for (int y = 0; y < RB; ++y) acc[x][y] = fma(u[x], v[y], acc[x][y]);
     }
   }
-  for (int k = 0; k < mine && k < 64; ++k) {
-    const int e = tid + 256 * k;
-    if (e < rr2) partial[(size_t)blockIdx.x * rr2 + e] = acc[k];
-  }
+  const int rr2 = r * r;
+#pragma unroll
+  for (int x = 0; x < RB; ++x)
+#pragma unroll
+    for (int y = 0; y < RB; ++y) {
+      const int i = ti + 16 * x, j = tj + 16 * y;
+      if (i < r && j < r) partial[(size_t)blockIdx.x * rr2 + i * r + j] = acc[x][y];
+    }
 }
 
 int ts_gram(adrom_ctx* ctx, const double* phi, int64_t n, int r, double* gram, double* partial) {
@@ -633,8 +647,12 @@ int ts_gram(adrom_ctx* ctx, const double* phi, int64_t n, int r, double* gram, d
   if (g > lim) g = lim;
   if (g < 1) g = 1;
   const size_t sm = sizeof(double) * 64 * (r | 1);
-  cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  gram_kernel<<<(int)g, 256, sm, ctx->stream>>>(phi, n, r, partial);
+  auto kern = (r <= 16)   ? gram_kernel<1>
+              : (r <= 32) ? gram_kernel<2>
+              : (r <= 64) ? gram_kernel<4>
+                          : gram_kernel<8>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  kern<<<(int)g, 256, sm, ctx->stream>>>(phi, n, r, partial);
   ADROM_LAUNCH_CK(ctx);
   reduce_partials_kernel<<<r * r, 256, 0, ctx->stream>>>(partial, (int)g, r * r, gram, nullptr);
   ADROM_LAUNCH_CK(ctx);

@@ -15,6 +15,11 @@ struct QdeimGuess {
 };
 
 size_t qdeim_workspace_bytes(adrom_ctx* ctx, int r, int count);
+// Exact greedy via a certified candidate pool (qdeim.cu): the path used by
+// the session and the C-ABI.  Blocking (one sync per pass).
+size_t qdeim_pool_workspace_bytes(int64_t n, int r, int count);
+int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int count,
+                      int64_t* out_idx, void* ws, int* passes_out);
 // First `count` pivots of the restarted column-pivoted QR of phi^T
 // (sampling.py:77-104), exact greedy, ties to the lowest row.  Blocking
 // (synchronises once per verification pass).  `guess` may be null.

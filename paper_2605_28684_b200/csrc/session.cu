@@ -151,7 +151,7 @@ int build_sampling_operator(adrom_session* s, const double* phi, adrom_rom_op& o
   if (s->cfg.sampling == 1) {
     const int n_base = n_s - s->cfg.n_extra;
     if (n_base > 0) {
-      st = qdeim_select(ctx, phi, s->N, s->r, n_base, op.idx, &s->guess, s->qd_ws, &it);
+      st = qdeim_pool_select(ctx, phi, s->N, s->r, n_base, op.idx, s->qd_ws, &it);
       if (st) return st;
     }
     st = reset_flags(ctx);
@@ -159,7 +159,7 @@ int build_sampling_operator(adrom_session* s, const double* phi, adrom_rom_op& o
     st = fgs_extend(ctx, m, y_corr, s->cfg.feature, op.idx, n_base, s->cfg.n_extra, nullptr);
     if (st) return st;
   } else {
-    st = qdeim_select(ctx, phi, s->N, s->r, n_s, op.idx, &s->guess, s->qd_ws, &it);
+    st = qdeim_pool_select(ctx, phi, s->N, s->r, n_s, op.idx, s->qd_ws, &it);
     if (st) return st;
     st = reset_flags(ctx);
     if (st) return st;
@@ -313,7 +313,7 @@ int adrom_session_create(adrom_ctx* ctx, const adrom_session_config* cfg, adrom_
   const size_t iws = isvd_workspace_bytes(ctx, N, r, r);
   cudaMalloc(&s->isvd_ws, iws);
   s->allocs.push_back(s->isvd_ws);
-  cudaMalloc(&s->qd_ws, qdeim_workspace_bytes(ctx, r, cfg->n_s));
+  cudaMalloc(&s->qd_ws, qdeim_pool_workspace_bytes(N, r, cfg->n_s));
   s->allocs.push_back(s->qd_ws);
   s->guess.r = r;
   s->guess.max_chunks = (cfg->n_s + r - 1) / r;
@@ -497,9 +497,9 @@ int adrom_session_sampling(adrom_session* s, int64_t* dev_idx) {
 int adrom_qdeim(adrom_ctx* ctx, const double* phi, int64_t n, int32_t r, int32_t n_s,
                 int64_t* idx) {
   if (!ctx) return ADROM_ERR_ARG;
-  int st = ensure_scratch(ctx, qdeim_workspace_bytes(ctx, r, n_s) + 4096);
+  int st = ensure_scratch(ctx, qdeim_pool_workspace_bytes(n, r, n_s) + 4096);
   if (st) return st;
-  return qdeim_select(ctx, phi, n, r, n_s, idx, nullptr, ctx->scratch, nullptr);
+  return qdeim_pool_select(ctx, phi, n, r, n_s, idx, ctx->scratch, nullptr);
 }
 
 int adrom_fgs(adrom_ctx* ctx, const adrom_model* m, const double* phi, int32_t r,
@@ -508,10 +508,10 @@ int adrom_fgs(adrom_ctx* ctx, const adrom_model* m, const double* phi, int32_t r
   if (n_extra > n_s) return set_error(ctx, ADROM_ERR_ARG, "n_extra cannot exceed the total number of sampling points");
   const int64_t N = m->n_elem * m->n_var;
   const int n_base = n_s - n_extra;
-  int st = ensure_scratch(ctx, qdeim_workspace_bytes(ctx, r, n_s) + 4096);
+  int st = ensure_scratch(ctx, qdeim_pool_workspace_bytes(N, r, n_s) + 4096);
   if (st) return st;
   if (n_base > 0) {
-    st = qdeim_select(ctx, phi, N, r, n_base, idx, nullptr, ctx->scratch, nullptr);
+    st = qdeim_pool_select(ctx, phi, N, r, n_base, idx, ctx->scratch, nullptr);
     if (st) return st;
   }
   st = reset_flags(ctx);

@@ -62,7 +62,9 @@ def test_qdeim_rank_deficiency_raises():
 
 
 @pytest.mark.parametrize("n,r,n_s", [(4096, 16, 16), (8192, 32, 32), (1 << 16, 64, 64),
-                                     (3000, 16, 40), (1 << 14, 128, 128)])
+                                     (3000, 16, 40), (1 << 14, 128, 128),
+                                     # above the all-rows pool limit: certified candidate pool
+                                     (1 << 18, 16, 16), (1 << 17, 64, 64), (100003, 32, 70)])
 def test_qdeim_vs_oracle_greedy(n, r, n_s):
     P = _pkg()
     rng = np.random.default_rng(n + r)
