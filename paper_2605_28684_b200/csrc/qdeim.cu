@@ -480,13 +480,97 @@ __device__ __forceinline__ Cand cand_block_reduce(Cand c, Cand* sc) {
   return out;
 }
 
+// Row update of the pool against the accepted direction d (smem): R > 0 uses
+// R/8 lanes per row (8 values per lane, 32/(R/8) rows per warp); R == 0 is
+// the generic warp-per-row path.  Tracks the best updated candidate.
+template <int R>
+__device__ __forceinline__ void qp_pool_update(const GreedyArgs& A, const double* d, int64_t gs,
+                                               bool apply, Cand& best) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t total_warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  if constexpr (R > 0) {
+    constexpr int LPR = R / 8, RPW = 32 / LPR;
+    const int seg = lane / LPR, sl = lane - seg * LPR;
+    double2 dv[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) dv[h] = reinterpret_cast<const double2*>(d)[sl + LPR * h];
+    for (int64_t p0 = gw * RPW; p0 < A.P; p0 += total_warps * RPW) {
+      const int64_t p = p0 + seg;
+      const bool valid = p < A.P;
+      const double old = valid ? A.pres2[p] : -1.0;
+      const bool live = old >= 0.0 && p != gs;
+      double2* rv = reinterpret_cast<double2*>(A.Rv + p * R);
+      double2 x[4];
+      double s = 0.0;
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        x[h] = live ? rv[sl + LPR * h] : make_double2(0.0, 0.0);
+        s += x[h].x * dv[h].x + x[h].y * dv[h].y;
+      }
+#pragma unroll
+      for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (!apply) s = 0.0;
+      double nr = 0.0;
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        x[h].x -= s * dv[h].x;
+        x[h].y -= s * dv[h].y;
+        nr += x[h].x * x[h].x + x[h].y * x[h].y;
+      }
+#pragma unroll
+      for (int o = LPR / 2; o > 0; o >>= 1) nr += __shfl_xor_sync(0xffffffffu, nr, o);
+      if (live && apply) {
+#pragma unroll
+        for (int h = 0; h < 4; ++h) rv[sl + LPR * h] = x[h];
+      }
+      const double nv = live ? (apply ? nr : old) : -1.0;
+      if (sl == 0 && valid && (old >= 0.0) && apply) A.pres2[p] = nv;
+      if (nv >= 0.0) {
+        const int64_t row = A.pool_idx[p];
+        if (cand_better(nv, row, best.v, best.row)) best = Cand{nv, row, p};
+      }
+    }
+  } else {
+    const int r = A.r;
+    for (int64_t p = gw; p < A.P; p += total_warps) {
+      const double old = A.pres2[p];
+      if (old < 0.0) continue;
+      if (p == gs) {
+        if (lane == 0 && apply) A.pres2[p] = -1.0;
+        continue;
+      }
+      double nv = old;
+      if (apply) {
+        double* rv = A.Rv + p * r;
+        double s = 0.0;
+        for (int c = lane; c < r; c += 32) s += rv[c] * d[c];
+        s = warp_sum(s);
+        double nr = 0.0;
+        for (int c = lane; c < r; c += 32) {
+          const double x = rv[c] - s * d[c];
+          rv[c] = x;
+          nr += x * x;
+        }
+        nv = warp_sum(nr);
+        if (lane == 0) A.pres2[p] = nv;
+      }
+      const int64_t row = A.pool_idx[p];
+      if (cand_better(nv, row, best.v, best.row)) best = Cand{nv, row, p};
+    }
+  }
+}
+
+// One grid barrier per accepted pivot: the update of step k also produces the
+// per-block candidates of step k + 1 (double-buffered per parity).
+template <int R>
 __global__ void __launch_bounds__(256) qp_greedy_kernel(GreedyArgs A) {
   cg::grid_group grid = cg::this_grid();
-  extern __shared__ double dsm[];
+  extern __shared__ __align__(16) double dsm[];
   double* d = dsm;  // r
   __shared__ Cand sc[8];
   __shared__ double tau_sh;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const int r = A.r;
   {
     double t = -1.0;
@@ -498,26 +582,25 @@ __global__ void __launch_bounds__(256) qp_greedy_kernel(GreedyArgs A) {
     __syncthreads();
   }
   const double tau = tau_sh;
+  const int G = gridDim.x;
   int k = A.state[0];
-  while (k < A.m) {
+  // initial candidates (no update)
+  {
     Cand c{-1.0, LLONG_MAX, -1};
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + tid; p < A.P;
-         p += (int64_t)gridDim.x * blockDim.x) {
-      const double v = A.pres2[p];
-      if (v < 0.0 || v < c.v) continue;
-      const int64_t row = A.pool_idx[p];
-      if (cand_better(v, row, c.v, c.row)) c = Cand{v, row, p};
-    }
+    qp_pool_update<R>(A, d, -1, false, c);
     c = cand_block_reduce(c, sc);
     if (tid == 0) {
       A.bv[blockIdx.x] = c.v;
       A.brow[blockIdx.x] = c.row;
       A.bi[blockIdx.x] = c.slot;
     }
-    grid.sync();
+  }
+  grid.sync();
+  int par = 0;
+  while (k < A.m) {
     Cand gc{-1.0, LLONG_MAX, -1};
-    for (int q = tid; q < (int)gridDim.x; q += blockDim.x) {
-      const Cand t{A.bv[q], A.brow[q], A.bi[q]};
+    for (int q = tid; q < G; q += blockDim.x) {
+      const Cand t{A.bv[par * G + q], A.brow[par * G + q], A.bi[par * G + q]};
       if (t.slot >= 0) cand_merge(gc, t);
     }
     gc = cand_block_reduce(gc, sc);
@@ -536,32 +619,22 @@ __global__ void __launch_bounds__(256) qp_greedy_kernel(GreedyArgs A) {
       break;
     }
     const double inv = 1.0 / sqrt(g);
+    // row gs itself is never rewritten (only its pres2), so no barrier here
     for (int c = tid; c < r; c += blockDim.x) d[c] = A.Rv[gs * r + c] * inv;
     __syncthreads();
     if (blockIdx.x == 0) {
       for (int c = tid; c < r; c += blockDim.x) A.D[c * r + k] = d[c];
       if (tid == 0) A.piv[k] = gc.row;
     }
-    grid.sync();  // everyone has read Rv[gs] before it is modified
-    const int64_t total_warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; p < A.P; p += total_warps) {
-      if (A.pool_idx[p] < 0 || A.pres2[p] < 0.0) continue;
-      if (p == gs) {
-        if (lane == 0) A.pres2[p] = -1.0;
-        continue;
-      }
-      double* rv = A.Rv + p * r;
-      double s = 0.0;
-      for (int c = lane; c < r; c += 32) s += rv[c] * d[c];
-      s = warp_sum(s);
-      double nr = 0.0;
-      for (int c = lane; c < r; c += 32) {
-        const double x = rv[c] - s * d[c];
-        rv[c] = x;
-        nr += x * x;
-      }
-      nr = warp_sum(nr);
-      if (lane == 0) A.pres2[p] = nr;
+    if (blockIdx.x == (int)(gs % G) && tid == 0) A.pres2[gs] = -1.0;
+    Cand c{-1.0, LLONG_MAX, -1};
+    qp_pool_update<R>(A, d, gs, true, c);
+    c = cand_block_reduce(c, sc);
+    par ^= 1;
+    if (tid == 0) {
+      A.bv[par * G + blockIdx.x] = c.v;
+      A.brow[par * G + blockIdx.x] = c.row;
+      A.bi[par * G + blockIdx.x] = c.slot;
     }
     ++k;
     grid.sync();
@@ -680,12 +753,17 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
   double* hres = (double*)((char*)ctx->pinned + 64);
   int bpm = 0;
   const size_t gsm = sizeof(double) * r;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, qp_greedy_kernel, 256, gsm);
+  void* gkern = (r == 16)    ? (void*)qp_greedy_kernel<16>
+                : (r == 32)  ? (void*)qp_greedy_kernel<32>
+                : (r == 64)  ? (void*)qp_greedy_kernel<64>
+                : (r == 128) ? (void*)qp_greedy_kernel<128>
+                             : (void*)qp_greedy_kernel<0>;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, gkern, 256, gsm);
   if (bpm < 1) return set_error(ctx, ADROM_ERR_CUDA, "qdeim: greedy kernel cannot be resident");
   int ggrid = ctx->num_sms * (bpm < 2 ? bpm : 2);
   const int64_t need_blocks = (P + 255) / 256;
   if (ggrid > need_blocks) ggrid = (int)(need_blocks < 1 ? 1 : need_blocks);
-  if (ggrid > 4096) ggrid = 4096;
+  if (ggrid > 2048) ggrid = 2048;  // bests are double-buffered in 4096 slots
   auto pass = [&](int lo, int hi, bool first, int n_ex) -> int {
     if (r == 16) return qp_pass_stream<16>(ctx, phi, n, D, lo, hi, first, res2, bnd2, ex, n_ex);
     if (r == 32) return qp_pass_stream<32>(ctx, phi, n, D, lo, hi, first, res2, bnd2, ex, n_ex);
@@ -739,7 +817,7 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
       GreedyArgs ga{pool_idx, P, Rv, pres2, cbound, (int)nchunks, D, piv, m, r, state, bv, bi, brow,
                     err_res, all ? 1 : 0};
       void* args[] = {&ga};
-      ADROM_CK(ctx, cudaLaunchCooperativeKernel((void*)qp_greedy_kernel, ggrid, 256, args, gsm,
+      ADROM_CK(ctx, cudaLaunchCooperativeKernel(gkern, ggrid, 256, args, gsm,
                                                 ctx->stream));
       ++ctx->launches;
       prof_end(ctx, pr);
