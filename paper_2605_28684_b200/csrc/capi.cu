@@ -99,9 +99,11 @@ int adrom_decode(adrom_ctx* ctx, const double* phi, const double* q_ref, const d
 
 int adrom_gram(adrom_ctx* ctx, const double* phi, int64_t n, int32_t r, double* gram) {
   if (!ctx) return ADROM_ERR_ARG;
-  int st = ensure_scratch(ctx, sizeof(double) * 2 * (size_t)partial_rows(ctx) * (r + 1) + 4096);
+  if (r < 1 || r > 128) return set_error(ctx, ADROM_ERR_ARG, "gram: rank %d unsupported", r);
+  const size_t cap = gram_partial_doubles(ctx, r);
+  int st = ensure_scratch(ctx, sizeof(double) * cap + 4096);
   if (st) return st;
-  return ts_gram(ctx, phi, n, r, gram, (double*)ctx->scratch);
+  return ts_gram(ctx, phi, n, r, gram, (double*)ctx->scratch, cap);
 }
 
 int adrom_isvd_update(adrom_ctx* ctx, const double* phi, const double* sigma,

@@ -637,11 +637,20 @@ __global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ ph
     }
 }
 
-int ts_gram(adrom_ctx* ctx, const double* phi, int64_t n, int r, double* gram, double* partial) {
+size_t gram_partial_doubles(const adrom_ctx* ctx, int r) {
+  return (size_t)ctx->num_sms * 2 * (size_t)r * r;
+}
+
+size_t isvd_partial_doubles(const adrom_ctx* ctx, int r_cur) {
+  const size_t a = (size_t)partial_rows(ctx) * (r_cur + 1), b = gram_partial_doubles(ctx, r_cur);
+  return a > b ? a : b;
+}
+
+int ts_gram(adrom_ctx* ctx, const double* phi, int64_t n, int r, double* gram, double* partial,
+            size_t cap_doubles) {
   if (r > 128) return set_error(ctx, ADROM_ERR_ARG, "gram: rank %d unsupported", r);
   int64_t g = (n + 63) / 64;
-  // partials hold 2 * partial_rows * (r + 1) doubles (isvd_workspace_bytes)
-  const int64_t cap = 2 * (int64_t)partial_rows(ctx) * (r + 1) / ((int64_t)r * r);
+  const int64_t cap = (int64_t)(cap_doubles / ((size_t)r * r));
   int64_t lim = (int64_t)ctx->num_sms * 2;
   if (lim > cap) lim = cap;
   if (g > lim) g = lim;
@@ -881,8 +890,8 @@ size_t isvd_workspace_bytes(adrom_ctx* ctx, int64_t n, int r_cur, int r) {
   const int64_t grid = (int64_t)partial_rows(ctx);
   size_t b = 0;
   const int w = (r_cur * r_cur > r_cur + 1) ? r_cur * r_cur : r_cur + 1;
-  b += align_up(sizeof(double) * grid * (w > r_cur + 1 ? (r_cur + 1) : w));  // partials
-  b += align_up(sizeof(double) * (size_t)partial_rows(ctx) * (r_cur + 1));     // (gram partials fit)
+  (void)w;
+  b += align_up(sizeof(double) * isvd_partial_doubles(ctx, r_cur));  // partials (Gram's too)
   b += 2 * align_up(sizeof(double) * (r_cur + 1));     // red1, red2
   b += align_up(sizeof(double) * r_cur);               // p (least squares)
   b += align_up(sizeof(double) * (r_cur + 1) * r);     // B
@@ -911,9 +920,7 @@ int isvd_update_async(adrom_ctx* ctx, const double* phi, const double* sigma, co
     w += align_up(bytes);
     return q;
   };
-  const int64_t grid = (int64_t)partial_rows(ctx);
-  double* partial = (double*)take(sizeof(double) * grid * (r_cur + 1));
-  take(sizeof(double) * (size_t)partial_rows(ctx) * (r_cur + 1));
+  double* partial = (double*)take(sizeof(double) * isvd_partial_doubles(ctx, r_cur));
   double* red1 = (double*)take(sizeof(double) * (r_cur + 1));
   double* red2 = (double*)take(sizeof(double) * (r_cur + 1));
   double* pls = (double*)take(sizeof(double) * r_cur);
@@ -928,7 +935,7 @@ int isvd_update_async(adrom_ctx* ctx, const double* phi, const double* sigma, co
   int st;
   const double* G = gram_in;
   if (!G) {  // Gram afresh (one extra N r^2 pass; the session tracks it instead)
-    st = ts_gram(ctx, phi, n, r_cur, Gloc, partial);
+    st = ts_gram(ctx, phi, n, r_cur, Gloc, partial, isvd_partial_doubles(ctx, r_cur));
     if (st) return st;
     G = Gloc;
   }

@@ -21,7 +21,12 @@ int ts_residual(adrom_ctx* ctx, const double* phi, int64_t n, int r, const doubl
                 const double* y, double* out, double* partial, int* flag, const int* skip,
                 double* qbuf);
 // G = phi^T phi (r x r); partial: >= 2*partial_rows*(r+1) doubles
-int ts_gram(adrom_ctx* ctx, const double* phi, int64_t n, int r, double* gram, double* partial);
+// G = Phi^T Phi; `partial` holds cap_doubles (gram_partial_doubles for full speed)
+int ts_gram(adrom_ctx* ctx, const double* phi, int64_t n, int r, double* gram, double* partial,
+            size_t cap_doubles);
+size_t gram_partial_doubles(const adrom_ctx* ctx, int r);
+// partial-sum region at the start of an iSVD workspace (fits ts_gram's)
+size_t isvd_partial_doubles(const adrom_ctx* ctx, int r_cur);
 
 size_t isvd_workspace_bytes(adrom_ctx* ctx, int64_t n, int r_cur, int r);
 // Asynchronous iSVD update (tracking.py:141-178).

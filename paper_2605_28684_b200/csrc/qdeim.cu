@@ -25,16 +25,37 @@
 #include "sampling_internal.cuh"
 
 #include <limits.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 namespace cg = cooperative_groups;
 
 namespace adrom {
 
-constexpr int QP_CH = 4096;        // rows per extraction chunk
-constexpr int QP_T = 32;           // pool rows per chunk
+// pool target size; ADROM_QDEIM_POOL_M overrides (tuning experiments)
+constexpr long long QP_M_DEFAULT = 1 << 16;
+// rows refreshed per round = factor x pool size (grows 4x on a stalled
+// round); ADROM_QDEIM_REFRESH overrides
+static long long qp_refresh_factor() {
+  static long long t = [] {
+    const char* e = getenv("ADROM_QDEIM_REFRESH");
+    const long long v = e ? atoll(e) : 0;
+    return (v >= 1 && v <= 4096) ? v : 64ll;
+  }();
+  return t;
+}
+
+static long long qp_pool_m() {
+  static long long t = [] {
+    const char* e = getenv("ADROM_QDEIM_POOL_M");
+    const long long v = e ? atoll(e) : 0;
+    return (v >= 64 && v <= (1ll << 24)) ? v : QP_M_DEFAULT;
+  }();
+  return t;
+}
+
 constexpr int64_t POOL_ALL = 1 << 16;
 constexpr double QP_EPS = 2.220446049250313e-16;
-constexpr int QP_TILE = 128;       // rows per pass tile (one thread per row)
 
 __device__ __forceinline__ bool excluded_row(int64_t i, const int64_t* ex, int n_ex) {
   int a = 0, b = n_ex - 1;
@@ -48,166 +69,6 @@ __device__ __forceinline__ bool excluded_row(int64_t i, const int64_t* ex, int n
   return false;
 }
 
-// ---------------------------------------------------------------------------
-// pass: res2 / bound update for the directions d_lo..d_hi-1 (D: r x r,
-// column l = d_l, row-major D[j*r + l]); the first pass seeds res2 =
-// ||phi_i||^2.  Excluded rows (earlier restarts, confirmed pivots) -> -1.
-// The tile is staged in smem (coalesced), one thread per row; for r <= 64
-// the row lives in registers, the directions are broadcast from smem.
-// ---------------------------------------------------------------------------
-template <int RMAX>
-__global__ void __launch_bounds__(QP_TILE) qp_pass_kernel(const double* __restrict__ phi,
-                                                          int64_t n, int r,
-                                                          const double* __restrict__ D, int lo,
-                                                          int hi, bool first,
-                                                          double* __restrict__ res2,
-                                                          double* __restrict__ bnd2,
-                                                          const int64_t* __restrict__ ex,
-                                                          int n_ex) {
-  extern __shared__ double sm[];
-  const int S = r | 1;
-  const int nd = hi - lo;
-  double* tile = sm;                   // QP_TILE x S
-  double* Ds = tile + QP_TILE * S;     // nd x r  (direction-major: Ds[l*r + j])
-  const int tid = threadIdx.x;
-  for (int e = tid; e < r * nd; e += blockDim.x) {
-    const int l = e / r, j = e - l * r;
-    Ds[l * r + j] = D[j * r + lo + l];
-  }
-  const int64_t ntiles = (n + QP_TILE - 1) / QP_TILE;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t row0 = t * QP_TILE;
-    const int rows = (int)((n - row0 < QP_TILE) ? (n - row0) : QP_TILE);
-    __syncthreads();
-    for (int e = tid; e < rows * r; e += blockDim.x) {
-      const int a = e / r, c = e - a * r;
-      tile[a * S + c] = phi[row0 * r + e];
-    }
-    __syncthreads();
-    if (tid < rows) {
-      const int64_t i = row0 + tid;
-      const double* rowp = tile + tid * S;
-      double v[RMAX <= 64 ? RMAX : 1];
-      double nrm = 0.0;
-      if (RMAX <= 64) {
-#pragma unroll
-        for (int c = 0; c < (RMAX <= 64 ? RMAX : 1); ++c) {
-          v[c] = (c < r) ? rowp[c] : 0.0;
-          nrm = fma(v[c], v[c], nrm);
-        }
-      } else {
-        for (int c = 0; c < r; ++c) nrm = fma(rowp[c], rowp[c], nrm);
-      }
-      const double old = first ? 0.0 : res2[i];
-      bool excl = (!first && old < 0.0) || excluded_row(i, ex, n_ex);
-      double r2 = first ? nrm : old;
-      if (!excl && !first) {
-        for (int l = 0; l < nd; ++l) {
-          const double* dl = Ds + l * r;
-          double s = 0.0;
-          if (RMAX <= 64) {
-#pragma unroll
-            for (int c = 0; c < (RMAX <= 64 ? RMAX : 1); ++c)
-              if (c < r) s = fma(v[c], dl[c], s);
-          } else {
-            for (int c = 0; c < r; ++c) s = fma(rowp[c], dl[c], s);
-          }
-          r2 -= s * s;
-        }
-      }
-      res2[i] = excl ? -1.0 : r2;
-      // downdating error bound (geqp3-style norm updates)
-      bnd2[i] = excl ? -1.0 : r2 + 8.0 * (double)(hi + 2) * QP_EPS * nrm;
-    }
-  }
-}
-
-// streaming variant for r in {16, 32, 64, 128}: LPR lanes per row, 16-byte
-// loads straight from global, U rows in flight per warp, segmented shuffles
-template <int R>
-__global__ void __launch_bounds__(256) qp_pass_stream_kernel(const double* __restrict__ phi,
-                                                             int64_t n,
-                                                             const double* __restrict__ D,
-                                                             int lo, int hi, bool first,
-                                                             double* __restrict__ res2,
-                                                             double* __restrict__ bnd2,
-                                                             const int64_t* __restrict__ ex,
-                                                             int n_ex) {
-  constexpr int LPR = R / 8;  // 8 doubles per lane: 32/LPR rows share a warp
-  constexpr int VPL = R / LPR;
-  constexpr int RPW = 32 / LPR;
-  constexpr int U = 4;
-  extern __shared__ __align__(16) double Ds[];  // nd x R (direction-major)
-  const int nd = hi - lo;
-  for (int e = threadIdx.x; e < R * nd; e += blockDim.x) {
-    const int l = e / R, j = e - l * R;
-    Ds[l * R + j] = D[j * R + lo + l];
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int seg = lane / LPR, sl = lane - seg * LPR;
-  const int64_t total_warps = (int64_t)gridDim.x * 8;
-  const int64_t rows_per_iter = (int64_t)RPW * U;
-  for (int64_t g = (int64_t)blockIdx.x * 8 + warp; g * rows_per_iter < n; g += total_warps) {
-    const int64_t base = g * rows_per_iter;
-    double2 val[U][VPL / 2];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t i = base + u * RPW + seg;
-      if (i < n) {
-        const double2* rowp = reinterpret_cast<const double2*>(phi + i * R);
-#pragma unroll
-        for (int h = 0; h < VPL / 2; ++h) val[u][h] = rowp[sl + LPR * h];
-      } else {
-#pragma unroll
-        for (int h = 0; h < VPL / 2; ++h) val[u][h] = make_double2(0.0, 0.0);
-      }
-    }
-    double nrm[U], sub[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      double a = 0.0;
-#pragma unroll
-      for (int h = 0; h < VPL / 2; ++h) a += val[u][h].x * val[u][h].x + val[u][h].y * val[u][h].y;
-#pragma unroll
-      for (int o = LPR / 2; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-      nrm[u] = a;
-      sub[u] = 0.0;
-    }
-    for (int l = 0; l < nd; ++l) {
-      const double2* dl = reinterpret_cast<const double2*>(Ds + l * R);
-      double2 d2[VPL / 2];
-#pragma unroll
-      for (int h = 0; h < VPL / 2; ++h) d2[h] = dl[sl + LPR * h];
-      double s[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        double a = 0.0;
-#pragma unroll
-        for (int h = 0; h < VPL / 2; ++h) a += val[u][h].x * d2[h].x + val[u][h].y * d2[h].y;
-        s[u] = a;
-      }
-#pragma unroll
-      for (int o = LPR / 2; o > 0; o >>= 1)
-#pragma unroll
-        for (int u = 0; u < U; ++u) s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
-#pragma unroll
-      for (int u = 0; u < U; ++u) sub[u] += s[u] * s[u];
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t i = base + u * RPW + seg;
-      if (sl == 0 && i < n) {
-        const double old = first ? 0.0 : res2[i];
-        const bool excl = (!first && old < 0.0) || excluded_row(i, ex, n_ex);
-        const double r2 = first ? nrm[u] : old - sub[u];
-        res2[i] = excl ? -1.0 : r2;
-        bnd2[i] = excl ? -1.0 : r2 + 8.0 * (double)(hi + 2) * QP_EPS * nrm[u];
-      }
-    }
-  }
-}
-
 // mark confirmed pivots as excluded
 __global__ void qp_mark_kernel(const int64_t* __restrict__ piv, int lo, int hi,
                                double* __restrict__ res2, double* __restrict__ bnd2) {
@@ -217,136 +78,318 @@ __global__ void qp_mark_kernel(const int64_t* __restrict__ piv, int lo, int hi,
   }
 }
 
+// lazy refresh: the pool rows' exact residuals (w.r.t. the k confirmed
+// directions) tighten their bounds; rows outside the pool keep older, still
+// valid bounds (residual norms never increase)
+__global__ void qp_writeback_kernel(const int64_t* __restrict__ pool_idx, int64_t P,
+                                    const double* __restrict__ pres2,
+                                    const double* __restrict__ pn2, int k,
+                                    const double* __restrict__ res2, double* __restrict__ bnd2) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = pool_idx[p];
+    if (i < 0) continue;
+    const double v = pres2[p];
+    if (v < 0.0 || res2[i] < 0.0) continue;
+    const double b = v + 8.0 * (double)(k + 2) * QP_EPS * pn2[p];
+    if (b < bnd2[i]) bnd2[i] = b;
+  }
+}
+
 // ---------------------------------------------------------------------------
-// extract: per chunk, the T largest res2 (ties: lower row first) -> pool;
-// bound = max bnd2 over the other (non-excluded) rows of the chunk
+// pool selection: the M rows with the largest bounds (global radix select on
+// the bound's bit pattern, 8 digits of 8 bits, stopping early once the rows
+// sharing the selected prefix fit the pool), then stream compaction.
+// tau = an upper bound on every bound left outside the pool.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ unsigned long long qp_key(double v) {
-  // non-negative doubles order like their bit patterns; excluded (-1) -> 0
+  // non-negative doubles order like their bit patterns; excluded (< 0) -> 0
   return v < 0.0 ? 0ull : (unsigned long long)__double_as_longlong(v) + 1ull;
 }
 
-constexpr int QP_EX_NT = 256;
+struct SelState {
+  unsigned long long prefix, mask;
+  unsigned long long theta;  // pool = rows with key >= theta (theta >= 1)
+  long long above;           // rows known to have key above the prefix
+  long long need;            // rows still to take from the prefix bin
+  int done;
+  int pad;
+  double tau;
+  unsigned long long count;  // compaction counter
+};
 
-// exclusive block scan (blockDim.x multiple of 32, <= 1024); *total = sum
-__device__ __forceinline__ int block_excl_scan(int v, int* wsum, int* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  int x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
+__global__ void qs_init_kernel(SelState* st, long long M, unsigned int* hist) {
+  if (threadIdx.x == 0) {
+    st->prefix = 0ull;
+    st->mask = 0ull;
+    st->theta = 1ull;
+    st->above = 0;
+    st->need = M;
+    st->done = 0;
+    st->tau = -1.0;
+    st->count = 0ull;
   }
-  __syncthreads();
-  if (lane == 31) wsum[warp] = x;
-  __syncthreads();
-  int off = 0, tot = 0;
-  for (int w = 0; w < nw; ++w) {
-    const int s = wsum[w];
-    if (w < warp) off += s;
-    tot += s;
-  }
-  *total = tot;
-  return off + x - v;
+  for (int j = threadIdx.x; j < 256; j += blockDim.x) hist[j] = 0u;
 }
 
-__global__ void __launch_bounds__(QP_EX_NT) qp_extract_kernel(const double* __restrict__ res2,
-                                                              const double* __restrict__ bnd2,
-                                                              int64_t n, int ch, int T,
-                                                              int64_t* __restrict__ pool_idx,
-                                                              double* __restrict__ chunk_bound) {
-  __shared__ unsigned long long keys[QP_CH];
-  __shared__ int cnt_sh, dig_sh, above_sh;
-  __shared__ int hist[256], wsum[QP_EX_NT / 32];
-  __shared__ double bred[QP_EX_NT / 32];
-  const int64_t c0 = (int64_t)blockIdx.x * ch;
-  const int rows = (int)((n - c0 < ch) ? (n - c0) : ch);
-  const int tid = threadIdx.x;
-  for (int j = tid; j < rows; j += blockDim.x) keys[j] = qp_key(res2[c0 + j]);
+// candidates: rows 0..n-1, or (list != null) the rows list[0..n) (-1 = empty)
+__global__ void __launch_bounds__(256) qs_hist_kernel(const double* __restrict__ bnd2, int64_t n,
+                                                      const int64_t* __restrict__ list,
+                                                      const SelState* __restrict__ st, int shift,
+                                                      unsigned int* __restrict__ hist) {
+  if (st->done) return;
+  __shared__ unsigned int sh[256];
+  sh[threadIdx.x] = 0u;
   __syncthreads();
-  // threshold = T-th largest key: radix select, 8 digits of 8 bits
-  unsigned long long thr = 0ull;
-  if (rows >= T) {
-    unsigned long long mask = 0ull;
-    int need = T;
-    for (int shift = 56; shift >= 0; shift -= 8) {
-      hist[tid] = 0;
-      __syncthreads();
-      for (int j = tid; j < rows; j += blockDim.x) {
-        const unsigned long long k = keys[j];
-        if ((k & mask) == thr) atomicAdd(&hist[(int)((k >> shift) & 255ull)], 1);
-      }
-      __syncthreads();
-      // suffix counts: thread t holds bins >= 255 - t ... via inclusive scan of
-      // the reversed histogram
-      int v = hist[255 - tid];
-      const int lane = tid & 31, warp = tid >> 5;
+  const unsigned long long prefix = st->prefix, mask = st->mask;
+  const int lane = threadIdx.x & 31;
+  // bounds crowd into a few bins: aggregate equal digits per warp first
+  for (int64_t b0 = blockIdx.x * (int64_t)blockDim.x; b0 < n; b0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = b0 + threadIdx.x;
+    const int64_t i = (j < n) ? (list ? list[j] : j) : -1;
+    int dig = -1;
+    if (i >= 0) {
+      const unsigned long long k = qp_key(bnd2[i]);
+      if (k != 0ull && (k & mask) == prefix) dig = (int)((k >> shift) & 255ull);
+    }
+    const unsigned int peers = __match_any_sync(0xffffffffu, dig);
+    if (dig >= 0 && lane == __ffs(peers) - 1) atomicAdd(&sh[dig], (unsigned int)__popc(peers));
+  }
+  __syncthreads();
+  const unsigned int c = sh[threadIdx.x];
+  if (c) atomicAdd(&hist[threadIdx.x], c);
+}
+
+// one block of 256: pick the digit holding the need-th largest remaining key
+__global__ void __launch_bounds__(256) qs_digit_kernel(SelState* st, int shift,
+                                                       unsigned int* __restrict__ hist,
+                                                       long long pcap) {
+  if (st->done) return;
+  __shared__ long long wsum[8];
+  __shared__ int dig_sh;
+  __shared__ long long excl_sh, bin_sh;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long h = hist[255 - tid];
+  long long v = h;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int x = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += x;
-      }
-      if (lane == 31) wsum[warp] = v;
-      __syncthreads();
-      int off = 0;
-      for (int w = 0; w < warp; ++w) off += wsum[w];
-      const int incl = v + off;                    // keys with digit >= 255 - tid
-      const int excl = incl - hist[255 - tid];     // keys with digit >  255 - tid
-      if (excl < need && incl >= need) {
-        dig_sh = 255 - tid;
-        above_sh = excl;
-      }
-      __syncthreads();
-      thr |= (unsigned long long)dig_sh << shift;
-      mask |= 255ull << shift;
-      need -= above_sh;
-      __syncthreads();
-    }
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long x = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += x;
   }
-  // each thread owns a contiguous run of rows (index order preserved)
-  const int per = (rows + QP_EX_NT - 1) / QP_EX_NT;
-  const int j0 = tid * per, j1 = (j0 + per < rows) ? j0 + per : rows;
-  int gt = 0, eq = 0;
-  for (int j = j0; j < j1; ++j) {
-    const unsigned long long k = keys[j];
-    if (k == 0ull) continue;
-    if (k > thr) ++gt;
-    else if (k == thr) ++eq;
-  }
-  int tot_gt, tot_eq;
-  const int gpos0 = block_excl_scan(gt, wsum, &tot_gt);
-  const int epos0 = block_excl_scan(eq, wsum, &tot_eq);
-  if (tid == 0) cnt_sh = tot_gt;  // total above the threshold (< T when ties fill the rest)
+  if (lane == 31) wsum[warp] = v;
+  if (tid == 0) dig_sh = -1;
   __syncthreads();
-  const int total_gt = cnt_sh;
-  const int eq_allowed = T - total_gt;
-  int64_t* out = pool_idx + (int64_t)blockIdx.x * T;
-  int gpos = gpos0, epos = epos0;
-  double bmax = -1.0;
-  for (int j = j0; j < j1; ++j) {
-    const unsigned long long k = keys[j];
-    if (k == 0ull) continue;
-    bool in = false;
-    if (k > thr) {
-      in = true;
-      out[gpos++] = c0 + j;
-    } else if (k == thr && epos < eq_allowed) {
-      in = true;
-      out[total_gt + epos] = c0 + j;
-      ++epos;
-    } else if (k == thr) {
-      ++epos;
-    }
-    if (!in) bmax = fmax(bmax, bnd2[c0 + j]);
+  long long off = 0;
+  for (int w = 0; w < warp; ++w) off += wsum[w];
+  const long long incl = v + off, excl = incl - h;
+  const long long need = st->need;
+  if (excl < need && incl >= need) {
+    dig_sh = 255 - tid;
+    excl_sh = excl;
+    bin_sh = h;
   }
-  // (pool slots beyond the chunk's valid rows keep the -1 of qp_fill_kernel)
-  for (int o = 16; o > 0; o >>= 1) bmax = fmax(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
-  if ((tid & 31) == 0) bred[tid >> 5] = bmax;
   __syncthreads();
+  hist[tid] = 0u;  // ready for the next round
   if (tid == 0) {
-    double b = -1.0;
-    for (int q = 0; q < QP_EX_NT / 32; ++q) b = fmax(b, bred[q]);
-    chunk_bound[blockIdx.x] = b;
+    if (dig_sh < 0) {  // fewer candidates than M: take every live row
+      st->theta = 1ull;
+      st->tau = -1.0;
+      st->done = 1;
+      return;
+    }
+    const unsigned long long d = (unsigned long long)dig_sh;
+    st->prefix |= d << shift;
+    st->mask |= 255ull << shift;
+    st->above += excl_sh;
+    st->need = need - excl_sh;
+    const long long with_bin = st->above + bin_sh;
+    if (with_bin <= pcap || shift == 0) {
+      // take the whole bin if it fits, else (last digit: exact ties) only above it
+      const unsigned long long lo = st->prefix;  // smallest key carrying the prefix
+      const unsigned long long th = (with_bin <= pcap) ? lo : lo + 1ull;
+      st->theta = th < 1ull ? 1ull : th;
+      // largest key outside: theta - 1 -> bound bits theta - 2
+      st->tau = (st->theta >= 2ull) ? __longlong_as_double((long long)(st->theta - 2ull)) : -1.0;
+      st->done = 1;
+    }
+  }
+}
+
+// rows with key >= theta -> out[0..), one atomic per block and round
+__global__ void __launch_bounds__(256) qs_compact_kernel(const double* __restrict__ bnd2, int64_t n,
+                                                         const int64_t* __restrict__ list,
+                                                         SelState* __restrict__ st,
+                                                         int64_t* __restrict__ out, long long cap) {
+  constexpr int ITEMS = 4;
+  __shared__ int wcnt[8];
+  __shared__ unsigned long long base_sh;
+  const unsigned long long theta = st->theta;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t tile = (int64_t)blockDim.x * ITEMS;
+  for (int64_t t0 = blockIdx.x * tile; t0 < n; t0 += (int64_t)gridDim.x * tile) {
+    int64_t rows[ITEMS];
+    unsigned int balls[ITEMS];
+    int mine = 0;
+#pragma unroll
+    for (int q = 0; q < ITEMS; ++q) {
+      const int64_t j = t0 + (int64_t)q * blockDim.x + threadIdx.x;
+      const int64_t i = (j < n) ? (list ? list[j] : j) : -1;
+      const bool take = i >= 0 && qp_key(bnd2[i]) >= theta;
+      rows[q] = take ? i : -1;
+      balls[q] = __ballot_sync(0xffffffffu, take);
+      mine += __popc(balls[q]);
+    }
+    if (lane == 0) wcnt[warp] = mine;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int w = 0; w < 8; ++w) tot += wcnt[w];
+      base_sh = tot ? atomicAdd(&st->count, (unsigned long long)tot) : 0ull;
+    }
+    __syncthreads();
+    unsigned long long pos = base_sh;
+    for (int w = 0; w < warp; ++w) pos += wcnt[w];
+#pragma unroll
+    for (int q = 0; q < ITEMS; ++q) {
+      if (rows[q] >= 0) {
+        const unsigned long long slot = pos + __popc(balls[q] & ((1u << lane) - 1u));
+        if ((long long)slot < cap) out[slot] = rows[q];
+      }
+      pos += __popc(balls[q]);
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// row pass (D: r x r, column l = d_l, row-major D[j*r + l]):
+//   QP_SEED     res2 = bnd2 = ||phi_i||^2 for every row (rows of `ex` -> -1)
+//   QP_REFRESH  the rows of `list` (n slots, -1 = empty): res2 -= sum over
+//               the directions the row has not seen yet (ver_i <= l < hi) of
+//               (phi_i . d_l)^2 (geqp3-style downdating); other rows keep
+//               their older (still valid, larger) bounds
+// R/8 lanes per row (8 columns each), 32/(R/8) rows per warp, 4 row groups
+// in flight; EXACT (r == R) uses 16-byte loads, else scalar loads with the
+// columns >= r zero.  Excluded rows (res2 < 0) are never touched.
+// ---------------------------------------------------------------------------
+enum { QP_SEED = 0, QP_REFRESH = 1 };
+
+template <int R, bool EXACT>
+__global__ void __launch_bounds__(256) qp_rows_kernel(const double* __restrict__ phi, int64_t n,
+                                                      int r, const double* __restrict__ D, int hi,
+                                                      int mode, const int64_t* __restrict__ list,
+                                                      double* __restrict__ res2,
+                                                      double* __restrict__ bnd2,
+                                                      unsigned char* __restrict__ ver,
+                                                      const int64_t* __restrict__ ex, int n_ex) {
+  constexpr int LPR = R / 8;
+  constexpr int RPW = 32 / LPR;
+  constexpr int U = 4;
+  extern __shared__ __align__(16) double Ds[];  // hi x R (direction-major, zero padded)
+  const int nd = (mode == QP_SEED) ? 0 : hi;
+  for (int e = threadIdx.x; e < R * nd; e += blockDim.x) {
+    const int l = e / R, j = e - l * R;
+    Ds[e] = (j < r) ? D[j * r + l] : 0.0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int seg = lane / LPR, sl = lane - seg * LPR;
+  const int64_t total_warps = (int64_t)gridDim.x * 8;
+  const int64_t rows_per_iter = (int64_t)RPW * U;
+  for (int64_t g = (int64_t)blockIdx.x * 8 + warp; g * rows_per_iter < n; g += total_warps) {
+    const int64_t base = g * rows_per_iter;
+    double2 val[U][4];
+    bool act[U];
+    int64_t rowi[U];
+    int lv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t pos = base + u * RPW + seg;
+      const int64_t i = (pos < n) ? (list ? list[pos] : pos) : -1;
+      const bool a = i >= 0;
+      rowi[u] = i;
+      act[u] = a;
+      lv[u] = (a && mode != QP_SEED) ? (int)ver[i] : nd;
+      if (a) {
+        if (EXACT) {
+          const double2* rowp = reinterpret_cast<const double2*>(phi + i * R);
+#pragma unroll
+          for (int h = 0; h < 4; ++h) val[u][h] = rowp[sl + LPR * h];
+        } else {
+          const double* rowp = phi + i * r;
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const int c = 2 * (sl + LPR * h);
+            val[u][h].x = (c < r) ? rowp[c] : 0.0;
+            val[u][h].y = (c + 1 < r) ? rowp[c + 1] : 0.0;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int h = 0; h < 4; ++h) val[u][h] = make_double2(0.0, 0.0);
+      }
+    }
+    bool any = false;
+#pragma unroll
+    for (int u = 0; u < U; ++u) any |= act[u];
+    if (!__any_sync(0xffffffffu, any)) continue;
+    double nrm[U], sub[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      double a = 0.0;
+#pragma unroll
+      for (int h = 0; h < 4; ++h) a += val[u][h].x * val[u][h].x + val[u][h].y * val[u][h].y;
+#pragma unroll
+      for (int o = LPR / 2; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+      nrm[u] = a;
+      sub[u] = 0.0;
+    }
+    // downdate with the directions this row has not seen (ver_i .. hi-1)
+    int lmin = nd;
+#pragma unroll
+    for (int u = 0; u < U; ++u) lmin = min(lmin, lv[u]);
+    lmin = __reduce_min_sync(0xffffffffu, lmin);
+    for (int l = lmin; l < nd; ++l) {
+      const double2* dl = reinterpret_cast<const double2*>(Ds + l * R);
+      double2 d2[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) d2[h] = dl[sl + LPR * h];
+      double s[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        double a = 0.0;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) a += val[u][h].x * d2[h].x + val[u][h].y * d2[h].y;
+        s[u] = a;
+      }
+#pragma unroll
+      for (int o = LPR / 2; o > 0; o >>= 1)
+#pragma unroll
+        for (int u = 0; u < U; ++u) s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (l >= lv[u]) sub[u] += s[u] * s[u];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = rowi[u];
+      if (sl == 0 && act[u]) {
+        if (mode == QP_SEED && excluded_row(i, ex, n_ex)) {
+          res2[i] = -1.0;
+          bnd2[i] = -1.0;
+        } else if (mode == QP_SEED) {
+          res2[i] = nrm[u];
+          bnd2[i] = nrm[u] + 16.0 * QP_EPS * nrm[u];
+          ver[i] = 0;
+        } else {
+          const double r2 = res2[i] - sub[u];
+          res2[i] = r2;
+          ver[i] = (unsigned char)nd;
+          // min of two valid bounds (a pool write-back may be tighter)
+          bnd2[i] = fmin(bnd2[i], r2 + 8.0 * (double)(nd + 2) * QP_EPS * nrm[u]);
+        }
+      }
+    }
   }
 }
 
@@ -361,56 +404,120 @@ __global__ void qp_fill_kernel(int64_t* __restrict__ p, int64_t P) {
 // exact residual vectors of the pool rows (CGS2 against confirmed d_0..d_k-1)
 // warp per pool row; R row-major P x r; excluded rows -> pres2 = -1
 // ---------------------------------------------------------------------------
-template <int RMAX>
+template <int R, bool EXACT>
 __global__ void __launch_bounds__(256) qp_resvec_kernel(const double* __restrict__ phi, int r,
                                                         const int64_t* __restrict__ pool_idx,
                                                         int64_t P, const double* __restrict__ D,
                                                         int k, const double* __restrict__ res2,
                                                         double* __restrict__ Rv,
-                                                        double* __restrict__ pres2) {
-  constexpr int H = (RMAX + 31) / 32;
-  extern __shared__ double Ds[];  // r x 65
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int e = threadIdx.x; e < r * k; e += blockDim.x) {
-    const int j = e / k, l = e - j * k;
-    Ds[j * 65 + l] = D[j * r + l];
+                                                        double* __restrict__ pres2,
+                                                        double* __restrict__ pn2) {
+  constexpr int LPR = R / 8;
+  constexpr int RPW = 32 / LPR;
+  constexpr int U = 4;
+  extern __shared__ __align__(16) double Ds[];  // k x R (direction-major, zero padded)
+  for (int e = threadIdx.x; e < R * k; e += blockDim.x) {
+    const int l = e / R, j = e - l * R;
+    Ds[e] = (j < r) ? D[j * r + l] : 0.0;
   }
   __syncthreads();
-  const int64_t total_warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; p < P; p += total_warps) {
-    const int64_t i = pool_idx[p];
-    const bool live = i >= 0 && res2[i] >= 0.0;
-    double v[H];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int seg = lane / LPR, sl = lane - seg * LPR;
+  const int64_t total_warps = (int64_t)gridDim.x * 8;
+  const int64_t per_iter = (int64_t)RPW * U;
+  for (int64_t g = (int64_t)blockIdx.x * 8 + warp; g * per_iter < P; g += total_warps) {
+    double2 v[U][4];
+    bool live[U];
 #pragma unroll
-    for (int h = 0; h < H; ++h) {
-      const int c = lane + 32 * h;
-      v[h] = (live && c < r) ? phi[i * r + c] : 0.0;
+    for (int u = 0; u < U; ++u) {
+      const int64_t p = g * per_iter + u * RPW + seg;
+      const int64_t i = (p < P) ? pool_idx[p] : -1;
+      live[u] = i >= 0 && res2[i] >= 0.0;
+      if (live[u]) {
+        if (EXACT) {
+          const double2* rowp = reinterpret_cast<const double2*>(phi + i * R);
+#pragma unroll
+          for (int h = 0; h < 4; ++h) v[u][h] = rowp[sl + LPR * h];
+        } else {
+          const double* rowp = phi + i * r;
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const int c = 2 * (sl + LPR * h);
+            v[u][h].x = (c < r) ? rowp[c] : 0.0;
+            v[u][h].y = (c + 1 < r) ? rowp[c + 1] : 0.0;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int h = 0; h < 4; ++h) v[u][h] = make_double2(0.0, 0.0);
+      }
     }
+    double nrm[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      double a = 0.0;
+#pragma unroll
+      for (int h = 0; h < 4; ++h) a += v[u][h].x * v[u][h].x + v[u][h].y * v[u][h].y;
+#pragma unroll
+      for (int o = LPR / 2; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+      nrm[u] = a;
+    }
+    // CGS2 against d_0..d_k-1
     for (int pass = 0; pass < 2; ++pass) {
       for (int l = 0; l < k; ++l) {
-        double s = 0.0;
+        const double2* dl = reinterpret_cast<const double2*>(Ds + l * R);
+        double2 d2[4];
 #pragma unroll
-        for (int h = 0; h < H; ++h) {
-          const int c = lane + 32 * h;
-          if (c < r) s += v[h] * Ds[c * 65 + l];
+        for (int h = 0; h < 4; ++h) d2[h] = dl[sl + LPR * h];
+        double s[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          double a = 0.0;
+#pragma unroll
+          for (int h = 0; h < 4; ++h) a += v[u][h].x * d2[h].x + v[u][h].y * d2[h].y;
+          s[u] = a;
         }
-        s = warp_sum(s);
 #pragma unroll
-        for (int h = 0; h < H; ++h) {
-          const int c = lane + 32 * h;
-          if (c < r) v[h] -= s * Ds[c * 65 + l];
+        for (int o = LPR / 2; o > 0; o >>= 1)
+#pragma unroll
+          for (int u = 0; u < U; ++u) s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            v[u][h].x -= s[u] * d2[h].x;
+            v[u][h].y -= s[u] * d2[h].y;
+          }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t p = g * per_iter + u * RPW + seg;
+      double a = 0.0;
+#pragma unroll
+      for (int h = 0; h < 4; ++h) a += v[u][h].x * v[u][h].x + v[u][h].y * v[u][h].y;
+#pragma unroll
+      for (int o = LPR / 2; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+      if (p < P) {
+        if (EXACT) {
+          double2* out = reinterpret_cast<double2*>(Rv + p * R);
+#pragma unroll
+          for (int h = 0; h < 4; ++h) out[sl + LPR * h] = v[u][h];
+        } else {
+          double* out = Rv + p * r;
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const int c = 2 * (sl + LPR * h);
+            if (c < r) out[c] = v[u][h].x;
+            if (c + 1 < r) out[c + 1] = v[u][h].y;
+          }
+        }
+        if (sl == 0) {
+          pres2[p] = live[u] ? a : -1.0;
+          pn2[p] = nrm[u];
         }
       }
     }
-    double nr = 0.0;
-#pragma unroll
-    for (int h = 0; h < H; ++h) {
-      const int c = lane + 32 * h;
-      if (c < r) Rv[p * r + c] = v[h];
-      nr += v[h] * v[h];
-    }
-    nr = warp_sum(nr);
-    if (lane == 0) pres2[p] = live ? nr : -1.0;
   }
 }
 
@@ -423,8 +530,8 @@ struct GreedyArgs {
   int64_t P;
   double* Rv;        // P x r
   double* pres2;     // P
-  const double* chunk_bound;
-  int nchunks;
+  const double* tau_ptr;   // bound on the candidates left out of the pool
+  const double* tau_ptr2;  // bound on the rows outside the candidate list
   double* D;         // r x r (column l = d_l)
   int64_t* piv;      // pivots (chunk-local list, m entries)
   int m;             // pivots wanted in this restart chunk
@@ -574,8 +681,7 @@ __global__ void __launch_bounds__(256) qp_greedy_kernel(GreedyArgs A) {
   const int r = A.r;
   {
     double t = -1.0;
-    if (!A.all_in_pool)
-      for (int c = tid; c < A.nchunks; c += blockDim.x) t = fmax(t, A.chunk_bound[c]);
+    if (!A.all_in_pool) t = fmax(*A.tau_ptr, *A.tau_ptr2);
     Cand c{t, 0, 0};
     c = cand_block_reduce(c, sc);
     if (tid == 0) tau_sh = c.v;
@@ -642,15 +748,22 @@ __global__ void __launch_bounds__(256) qp_greedy_kernel(GreedyArgs A) {
   if (blockIdx.x == 0 && tid == 0) A.state[0] = k;
 }
 
+static int64_t qp_pool_capacity(int64_t n) {
+  if (n <= POOL_ALL) return n;
+  const int64_t cap = 2 * qp_pool_m();
+  return cap < n ? cap : n;
+}
+
 size_t qdeim_pool_workspace_bytes(int64_t n, int r, int count) {
-  const int64_t nchunks = (n + QP_CH - 1) / QP_CH;
-  const int64_t P = (n <= POOL_ALL) ? n : nchunks * QP_T;
+  const int64_t P = qp_pool_capacity(n);
   size_t b = 0;
   b += 2 * align_up(sizeof(double) * (size_t)n);           // res2, bnd2
   b += align_up(sizeof(int64_t) * (size_t)P);              // pool idx
   b += align_up(sizeof(double) * (size_t)P * r);           // Rv
-  b += align_up(sizeof(double) * (size_t)P);               // pres2
-  b += align_up(sizeof(double) * (size_t)nchunks);         // chunk bounds
+  b += 2 * align_up(sizeof(double) * (size_t)P);           // pres2, pn2
+  b += 2 * align_up(sizeof(SelState)) + align_up(sizeof(unsigned int) * 256);  // selection
+  b += align_up(sizeof(int64_t) * (size_t)n);              // refresh list
+  b += align_up((size_t)n);                                // per-row downdate version
   b += align_up(sizeof(double) * (size_t)r * r);           // D
   b += align_up(sizeof(int64_t) * (size_t)r);              // local pivots
   b += align_up(sizeof(int) * 8) + align_up(sizeof(double) * 2);
@@ -677,46 +790,35 @@ __global__ void qp_all_rows_kernel(int64_t* __restrict__ pool_idx, int64_t n) {
     pool_idx[i] = i;
 }
 
-template <int RMAX>
-static int qp_pass(adrom_ctx* ctx, const double* phi, int64_t n, int r, const double* D, int lo,
-                   int hi, bool first, double* res2, double* bnd2, const int64_t* ex, int n_ex) {
-  const int64_t ntiles = (n + QP_TILE - 1) / QP_TILE;
-  int64_t g = (int64_t)ctx->num_sms * 8;
-  if (g > ntiles) g = ntiles;
-  const size_t sm = sizeof(double) * ((size_t)QP_TILE * (r | 1) + (size_t)r * (hi - lo > 0 ? hi - lo : 1));
-  cudaFuncSetAttribute(qp_pass_kernel<RMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  qp_pass_kernel<RMAX><<<(int)(g < 1 ? 1 : g), QP_TILE, sm, ctx->stream>>>(
-      phi, n, r, D, lo, hi, first, res2, bnd2, ex, n_ex);
-  ADROM_LAUNCH_CK(ctx);
-  return ADROM_OK;
-}
-
-template <int R>
-static int qp_pass_stream(adrom_ctx* ctx, const double* phi, int64_t n, const double* D, int lo,
-                          int hi, bool first, double* res2, double* bnd2, const int64_t* ex,
-                          int n_ex) {
-  constexpr int LPR = R / 8;  // 8 doubles per lane: 32/LPR rows share a warp
+template <int R, bool EXACT>
+static int qp_rows_launch(adrom_ctx* ctx, const double* phi, int64_t n, int r, const double* D,
+                          int hi, int mode, const int64_t* list, double* res2, double* bnd2,
+                          unsigned char* ver, const int64_t* ex, int n_ex) {
+  constexpr int LPR = R / 8;
   const int64_t rows_per_warp_iter = (int64_t)(32 / LPR) * 4;
   const int64_t warps = (n + rows_per_warp_iter - 1) / rows_per_warp_iter;
   int64_t g = (int64_t)ctx->num_sms * 8;
   if (g > (warps + 7) / 8) g = (warps + 7) / 8;
-  const size_t sm = sizeof(double) * (size_t)R * (hi - lo > 0 ? hi - lo : 1);
-  cudaFuncSetAttribute(qp_pass_stream_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  qp_pass_stream_kernel<R><<<(int)(g < 1 ? 1 : g), 256, sm, ctx->stream>>>(
-      phi, n, D, lo, hi, first, res2, bnd2, ex, n_ex);
+  const int nd = (mode == QP_SEED) ? 0 : hi;
+  const size_t sm = sizeof(double) * (size_t)R * (nd > 0 ? nd : 1);
+  cudaFuncSetAttribute(qp_rows_kernel<R, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  qp_rows_kernel<R, EXACT><<<(int)(g < 1 ? 1 : g), 256, sm, ctx->stream>>>(
+      phi, n, r, D, hi, mode, list, res2, bnd2, ver, ex, n_ex);
   ADROM_LAUNCH_CK(ctx);
   return ADROM_OK;
 }
 
-template <int RMAX>
+template <int R, bool EXACT>
 static int qp_resvec(adrom_ctx* ctx, const double* phi, int r, const int64_t* pool_idx, int64_t P,
-                     const double* D, int k, const double* res2, double* Rv, double* pres2) {
-  int64_t g = (P + 7) / 8;
-  if (g > (int64_t)ctx->num_sms * 16) g = (int64_t)ctx->num_sms * 16;
-  const size_t sm = sizeof(double) * (size_t)r * 65;
-  cudaFuncSetAttribute(qp_resvec_kernel<RMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  qp_resvec_kernel<RMAX><<<(int)(g < 1 ? 1 : g), 256, sm, ctx->stream>>>(phi, r, pool_idx, P, D, k,
-                                                                        res2, Rv, pres2);
+                     const double* D, int k, const double* res2, double* Rv, double* pres2,
+                     double* pn2) {
+  const int64_t per_block = (int64_t)(32 / (R / 8)) * 4 * 8;
+  int64_t g = (P + per_block - 1) / per_block;
+  if (g > (int64_t)ctx->num_sms * 8) g = (int64_t)ctx->num_sms * 8;
+  const size_t sm = sizeof(double) * (size_t)R * (k > 0 ? k : 1);
+  cudaFuncSetAttribute(qp_resvec_kernel<R, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  qp_resvec_kernel<R, EXACT><<<(int)(g < 1 ? 1 : g), 256, sm, ctx->stream>>>(
+      phi, r, pool_idx, P, D, k, res2, Rv, pres2, pn2);
   ADROM_LAUNCH_CK(ctx);
   return ADROM_OK;
 }
@@ -726,9 +828,8 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
   if (count > n) return set_error(ctx, ADROM_ERR_DENSE, "cannot select %d pivots from %lld columns",
                                   count, (long long)n);
   if (r < 1 || r > 128) return set_error(ctx, ADROM_ERR_ARG, "qdeim: rank %d unsupported", r);
-  const int64_t nchunks = (n + QP_CH - 1) / QP_CH;
   const bool all = n <= POOL_ALL;
-  const int64_t P = all ? n : nchunks * QP_T;
+  const int64_t P = qp_pool_capacity(n);
   char* w = (char*)ws;
   auto take = [&](size_t bytes) {
     void* p = w;
@@ -740,7 +841,12 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
   int64_t* pool_idx = (int64_t*)take(sizeof(int64_t) * (size_t)P);
   double* Rv = (double*)take(sizeof(double) * (size_t)P * r);
   double* pres2 = (double*)take(sizeof(double) * (size_t)P);
-  double* cbound = (double*)take(sizeof(double) * (size_t)nchunks);
+  double* pn2 = (double*)take(sizeof(double) * (size_t)P);
+  SelState* sel = (SelState*)take(sizeof(SelState));
+  SelState* selR = (SelState*)take(sizeof(SelState));
+  int64_t* rlist = (int64_t*)take(sizeof(int64_t) * (size_t)n);
+  unsigned char* ver = (unsigned char*)take((size_t)n);
+  unsigned int* hist = (unsigned int*)take(sizeof(unsigned int) * 256);
   double* D = (double*)take(sizeof(double) * (size_t)r * r);
   int64_t* piv = (int64_t*)take(sizeof(int64_t) * (size_t)r);
   int* state = (int*)take(sizeof(int) * 8);
@@ -764,21 +870,44 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
   const int64_t need_blocks = (P + 255) / 256;
   if (ggrid > need_blocks) ggrid = (int)(need_blocks < 1 ? 1 : need_blocks);
   if (ggrid > 2048) ggrid = 2048;  // bests are double-buffered in 4096 slots
-  auto pass = [&](int lo, int hi, bool first, int n_ex) -> int {
-    if (r == 16) return qp_pass_stream<16>(ctx, phi, n, D, lo, hi, first, res2, bnd2, ex, n_ex);
-    if (r == 32) return qp_pass_stream<32>(ctx, phi, n, D, lo, hi, first, res2, bnd2, ex, n_ex);
-    if (r == 64) return qp_pass_stream<64>(ctx, phi, n, D, lo, hi, first, res2, bnd2, ex, n_ex);
-    if (r == 128) return qp_pass_stream<128>(ctx, phi, n, D, lo, hi, first, res2, bnd2, ex, n_ex);
-    if (r <= 32) return qp_pass<32>(ctx, phi, n, r, D, lo, hi, first, res2, bnd2, ex, n_ex);
-    if (r <= 64) return qp_pass<64>(ctx, phi, n, r, D, lo, hi, first, res2, bnd2, ex, n_ex);
-    return qp_pass<128>(ctx, phi, n, r, D, lo, hi, first, res2, bnd2, ex, n_ex);
+  auto rows_pass = [&](int64_t nn, int hi, int mode, const int64_t* sl, int n_ex) -> int {
+    if (r == 16) return qp_rows_launch<16, true>(ctx, phi, nn, r, D, hi, mode, sl, res2, bnd2, ver, ex, n_ex);
+    if (r == 32) return qp_rows_launch<32, true>(ctx, phi, nn, r, D, hi, mode, sl, res2, bnd2, ver, ex, n_ex);
+    if (r == 64) return qp_rows_launch<64, true>(ctx, phi, nn, r, D, hi, mode, sl, res2, bnd2, ver, ex, n_ex);
+    if (r == 128) return qp_rows_launch<128, true>(ctx, phi, nn, r, D, hi, mode, sl, res2, bnd2, ver, ex, n_ex);
+    if (r < 16) return qp_rows_launch<16, false>(ctx, phi, nn, r, D, hi, mode, sl, res2, bnd2, ver, ex, n_ex);
+    if (r < 32) return qp_rows_launch<32, false>(ctx, phi, nn, r, D, hi, mode, sl, res2, bnd2, ver, ex, n_ex);
+    if (r < 64) return qp_rows_launch<64, false>(ctx, phi, nn, r, D, hi, mode, sl, res2, bnd2, ver, ex, n_ex);
+    return qp_rows_launch<128, false>(ctx, phi, nn, r, D, hi, mode, sl, res2, bnd2, ver, ex, n_ex);
   };
   auto resvec = [&](int k) -> int {
-    if (r <= 32) return qp_resvec<32>(ctx, phi, r, pool_idx, P, D, k, res2, Rv, pres2);
-    if (r <= 64) return qp_resvec<64>(ctx, phi, r, pool_idx, P, D, k, res2, Rv, pres2);
-    return qp_resvec<128>(ctx, phi, r, pool_idx, P, D, k, res2, Rv, pres2);
+#define QP_RV(RR, EX) return qp_resvec<RR, EX>(ctx, phi, r, pool_idx, P, D, k, res2, Rv, pres2, pn2)
+    if (r == 16) QP_RV(16, true);
+    if (r == 32) QP_RV(32, true);
+    if (r == 64) QP_RV(64, true);
+    if (r == 128) QP_RV(128, true);
+    if (r < 16) QP_RV(16, false);
+    if (r < 32) QP_RV(32, false);
+    if (r < 64) QP_RV(64, false);
+    QP_RV(128, false);
+#undef QP_RV
   };
-  int chosen = 0, passes = 0;
+  const int sg = ctx->num_sms * 4;
+  // theta/tau of the rows holding the M largest bounds (<= cap rows taken)
+  auto select = [&](SelState* st, const int64_t* list, int64_t nn, long long M,
+                    long long cap) -> int {
+    qs_init_kernel<<<1, 256, 0, ctx->stream>>>(st, M, hist);
+    ADROM_LAUNCH_CK(ctx);
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      qs_hist_kernel<<<sg, 256, 0, ctx->stream>>>(bnd2, nn, list, st, shift, hist);
+      ADROM_LAUNCH_CK(ctx);
+      qs_digit_kernel<<<1, 256, 0, ctx->stream>>>(st, shift, hist, cap);
+      ADROM_LAUNCH_CK(ctx);
+    }
+    return ADROM_OK;
+  };
+  const long long M = qp_pool_m();
+  int chosen = 0, rounds = 0, refreshed = 0;
   while (chosen < count) {
     const int m = (count - chosen < r) ? (count - chosen) : r;
     const int n_ex = chosen;
@@ -787,38 +916,61 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
       ADROM_LAUNCH_CK(ctx);
     }
     ADROM_CK(ctx, cudaMemsetAsync(state, 0, sizeof(int) * 8, ctx->stream));
-    int k = 0, lo = 0;
-    bool first = true;
+    // seed: every bound = ||phi_i||^2 (fresh for k = 0)
+    int st = rows_pass(n, 0, QP_SEED, nullptr, n_ex);
+    if (st) return st;
+    int k = 0;
+    bool fresh = true;                       // bounds of the top rows are current
+    int64_t rl_n = 0;                        // refresh-list slots (0: none this round)
+    long long mref = qp_refresh_factor() * M;  // rows refreshed per round
     while (k < m) {
-      ++passes;
+      ++rounds;
       const int pr = prof_begin(ctx, PROBE_QDEIM_SCAN);
-      int st = pass(first ? 0 : lo, first ? 0 : k, first, n_ex);
-      if (st) return st;
-      if (!first && k > 0) {
-        qp_mark_kernel<<<1, 128, 0, ctx->stream>>>(piv, 0, k, res2, bnd2);
-        ADROM_LAUNCH_CK(ctx);
-      }
-      first = false;
-      lo = k;
       int64_t gg = (P + 255) / 256;
       if (gg > ctx->num_sms * 8) gg = ctx->num_sms * 8;
+      if (!fresh && !all) {
+        // refresh the mref rows with the largest (possibly stale) bounds
+        const long long cap = (2 * mref < n) ? 2 * mref : n;
+        st = select(selR, nullptr, n, mref, cap);
+        if (st) return st;
+        int64_t fg = (cap + 255) / 256;
+        if (fg > ctx->num_sms * 8) fg = ctx->num_sms * 8;
+        qp_fill_kernel<<<(int)fg, 256, 0, ctx->stream>>>(rlist, cap);
+        ADROM_LAUNCH_CK(ctx);
+        qs_compact_kernel<<<sg, 256, 0, ctx->stream>>>(bnd2, n, nullptr, selR, rlist, cap);
+        ADROM_LAUNCH_CK(ctx);
+        st = rows_pass(cap, k, QP_REFRESH, rlist, n_ex);
+        if (st) return st;
+        ++refreshed;
+        rl_n = cap;
+      } else {
+        rl_n = 0;  // pool straight from every row's bound; nothing else outside
+        if (!all) {
+          qs_init_kernel<<<1, 256, 0, ctx->stream>>>(selR, 0, hist);
+          ADROM_LAUNCH_CK(ctx);
+        }
+      }
       if (all) {
         qp_all_rows_kernel<<<(int)gg, 256, 0, ctx->stream>>>(pool_idx, n);
         ADROM_LAUNCH_CK(ctx);
       } else {
+        // pool = the M largest bounds among the refreshed rows (rows outside the
+        // refresh list are bounded by selR->tau), or among all rows
+        const int64_t* cl = rl_n ? rlist : nullptr;
+        const int64_t cn = rl_n ? rl_n : n;
+        st = select(sel, cl, cn, M, (long long)P);
+        if (st) return st;
         qp_fill_kernel<<<(int)gg, 256, 0, ctx->stream>>>(pool_idx, P);
         ADROM_LAUNCH_CK(ctx);
-        qp_extract_kernel<<<(int)nchunks, QP_EX_NT, 0, ctx->stream>>>(res2, bnd2, n, QP_CH, QP_T,
-                                                                       pool_idx, cbound);
+        qs_compact_kernel<<<sg, 256, 0, ctx->stream>>>(bnd2, cn, cl, sel, pool_idx, (long long)P);
         ADROM_LAUNCH_CK(ctx);
       }
       st = resvec(k);
       if (st) return st;
-      GreedyArgs ga{pool_idx, P, Rv, pres2, cbound, (int)nchunks, D, piv, m, r, state, bv, bi, brow,
+      GreedyArgs ga{pool_idx, P, Rv, pres2, &sel->tau, &selR->tau, D, piv, m, r, state, bv, bi, brow,
                     err_res, all ? 1 : 0};
       void* args[] = {&ga};
-      ADROM_CK(ctx, cudaLaunchCooperativeKernel(gkern, ggrid, 256, args, gsm,
-                                                ctx->stream));
+      ADROM_CK(ctx, cudaLaunchCooperativeKernel(gkern, ggrid, 256, args, gsm, ctx->stream));
       ++ctx->launches;
       prof_end(ctx, pr);
       ADROM_CK(ctx, cudaMemcpyAsync(hstate, state, sizeof(int) * 4, cudaMemcpyDeviceToHost,
@@ -832,8 +984,13 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
                          chosen + hstate[2] - 1, hres[0]);
       const int knew = hstate[0];
       if (knew == k) {
-        // nothing certifiable: only possible when the remaining residuals are
-        // ties at (numerically) zero, i.e. the basis is rank deficient
+        if (!all && mref < n) {  // stale bounds block progress: refresh more rows
+          mref = (mref * 4 < n) ? mref * 4 : n;
+          fresh = false;
+          continue;
+        }
+        // nothing certifiable with every bound fresh: only possible when the
+        // remaining residuals tie at (numerically) zero -> rank deficient
         if (!(hres[0] >= 1e-14))
           return set_error(ctx, ADROM_ERR_SINGULAR,
                            "rank deficiency at pivot step %d (residual column norm %.3e)",
@@ -841,12 +998,24 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
         return set_error(ctx, ADROM_ERR_DENSE, "qdeim: no certified pivot at step %d", chosen + k);
       }
       k = knew;
+      fresh = false;
+      if (k < m && !all) {
+        // exclude the new pivots; the pool rows' exact residuals tighten their bounds
+        qp_mark_kernel<<<1, 128, 0, ctx->stream>>>(piv, 0, k, res2, bnd2);
+        ADROM_LAUNCH_CK(ctx);
+        qp_writeback_kernel<<<(int)gg, 256, 0, ctx->stream>>>(pool_idx, P, pres2, pn2, k, res2,
+                                                             bnd2);
+        ADROM_LAUNCH_CK(ctx);
+      }
     }
     ADROM_CK(ctx, cudaMemcpyAsync(out_idx + chosen, piv, sizeof(int64_t) * m,
                                   cudaMemcpyDeviceToDevice, ctx->stream));
     chosen += m;
   }
-  if (passes_out) *passes_out = passes;
+  if (getenv("ADROM_QDEIM_TRACE"))
+    fprintf(stderr, "qdeim: n=%lld r=%d count=%d rounds=%d refreshes=%d\n", (long long)n, r, count,
+            rounds, refreshed);
+  if (passes_out) *passes_out = rounds;
   return ADROM_OK;
 }
 

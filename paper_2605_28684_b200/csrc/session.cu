@@ -360,7 +360,8 @@ int adrom_session_load(adrom_session* s, const double* q_ref, const double* d, c
                                 ctx->stream));
   ADROM_CK(ctx, cudaMemcpyAsync(s->sigma[0], sigma0, 8 * s->r, cudaMemcpyDeviceToDevice,
                                 ctx->stream));
-  int st = ts_gram(ctx, s->phi[0], s->N, s->r, s->gram[0], (double*)s->isvd_ws);
+  int st = ts_gram(ctx, s->phi[0], s->N, s->r, s->gram[0], (double*)s->isvd_ws,
+                   isvd_partial_doubles(ctx, s->r));
   if (st) return st;
   ADROM_CK(ctx, cudaMemcpyAsync(s->q_tilde, q_last, 8 * N, cudaMemcpyDeviceToDevice,
                                 ctx->stream));
