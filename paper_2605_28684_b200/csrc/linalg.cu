@@ -504,6 +504,140 @@ __global__ void __launch_bounds__(256) rot_tiled_kernel(RotArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// FP64 tensor-core rotation (R in {32, 64}): out = [phi | q_hat] B on DMMA
+// (mma.sync m8n8k4 f64).  64-row tiles double-buffered in smem by cp.async
+// (row stride R + 4: conflict-free fragment loads; column R holds q_hat);
+// 4 warps as 2 (rows) x 2 (cols), each warp 32 rows x R/2 columns; two
+// blocks per SM so one block's epilogue overlaps the other's MMAs.  The
+// q_hat column is a rank-1 FMA update in the epilogue.
+// ---------------------------------------------------------------------------
+template <int R>
+struct RotTC {
+  static constexpr int TM = 64;            // rows per tile; 2 blocks per SM
+  static constexpr int NTHR = TM / 32 * 64;  // (TM/32) x 2 warps
+  static constexpr int S = R + 4;          // smem row stride (doubles)
+  static constexpr int WN = R / 2;         // columns per warp
+  static constexpr int NT = WN / 8;        // 8-wide column tiles per warp
+  static constexpr int MT = 4;             // 8-row tiles per warp (32 rows)
+  static constexpr size_t smem_doubles = 2 * (size_t)TM * S + (size_t)(R + 1) * S + R;
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int R>
+__global__ void __launch_bounds__(RotTC<R>::NTHR, 2) rot_tc_kernel(RotArgs a) {
+  using C = RotTC<R>;
+  extern __shared__ __align__(16) double sm[];
+  double* As0 = sm;                      // 2 stages x TM x S
+  double* Bs = sm + 2 * C::TM * C::S;    // (R+1) x S
+  double* ps = Bs + (R + 1) * C::S;      // R
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;  // warp tile: rows 32 wm.., cols WN wn..
+  const bool use_q = a.qbuf && (a.need == nullptr || *a.need != 0);
+  for (int e = tid; e < (R + 1) * R; e += C::NTHR) Bs[(e / R) * C::S + (e % R)] = a.B[e];
+  for (int e = tid; e < R; e += C::NTHR) ps[e] = use_q ? 0.0 : a.p[e];
+  const double qinv = *a.qinv;
+  const int64_t n = a.n;
+  const int64_t ntiles = (n + C::TM - 1) / C::TM;
+  constexpr int CHUNKS = C::TM * R / 2;  // 16-byte chunks per tile
+  auto load_tile = [&](int64_t t, double* As) {
+    const int64_t row0 = t * C::TM;
+    for (int c = tid; c < CHUNKS; c += C::NTHR) {
+      const int rr = c / (R / 2), cc = 2 * (c % (R / 2));
+      const bool ok = row0 + rr < n;
+      const double* src = a.phi + (ok ? (row0 + rr) * R + cc : 0);
+      cp_async16(As + rr * C::S + cc, src, ok ? 16 : 0);
+    }
+    cp_async_commit();
+  };
+  int64_t t = blockIdx.x;
+  if (t < ntiles) load_tile(t, As0);
+  int stage = 0;
+  for (; t < ntiles; t += gridDim.x) {
+    double* As = As0 + stage * C::TM * C::S;
+    const int64_t tn = t + gridDim.x;
+    if (tn < ntiles) {
+      load_tile(tn, As0 + (stage ^ 1) * C::TM * C::S);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const int64_t row0 = t * C::TM;
+    // q_hat into column R (2 threads per row)
+    for (int e = tid; e < 2 * C::TM; e += C::NTHR) {
+      const int rr = e >> 1, half = e & 1;
+      double qv = 0.0;
+      if (!use_q) {
+        double s = 0.0;
+#pragma unroll 8
+        for (int k = half * (R / 2); k < (half + 1) * (R / 2); ++k) s = fma(As[rr * C::S + k], ps[k], s);
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        qv = (row0 + rr < n) ? a.y[row0 + rr] - s : 0.0;
+      } else {
+        qv = (row0 + rr < n) ? a.qbuf[row0 + rr] : 0.0;
+      }
+      if (half == 0) As[rr * C::S + R] = qv * qinv;
+    }
+    double acc[C::MT][C::NT][2];
+#pragma unroll
+    for (int i = 0; i < C::MT; ++i)
+#pragma unroll
+      for (int j = 0; j < C::NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    const int ar = wm * 32 + (lane >> 2), ak = lane & 3;
+    const int bn = wn * C::WN + (lane >> 2), bk = lane & 3;
+#pragma unroll 2
+    for (int k0 = 0; k0 < R; k0 += 4) {
+      double af[C::MT], bf[C::NT];
+#pragma unroll
+      for (int i = 0; i < C::MT; ++i) af[i] = As[(ar + 8 * i) * C::S + k0 + ak];
+#pragma unroll
+      for (int j = 0; j < C::NT; ++j) bf[j] = Bs[(k0 + bk) * C::S + bn + 8 * j];
+#pragma unroll
+      for (int i = 0; i < C::MT; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();  // q_hat column visible
+    // epilogue: + q_hat (x) B[R, :], store
+    const int er = wm * 32 + (lane >> 2), ec = wn * C::WN + 2 * (lane & 3);
+#pragma unroll
+    for (int i = 0; i < C::MT; ++i) {
+      const int rr = er + 8 * i;
+      const double qh = As[rr * C::S + R];
+      if (row0 + rr < n) {
+        double* dst = a.out + (row0 + rr) * R;
+#pragma unroll
+        for (int j = 0; j < C::NT; ++j) {
+          const int cc = ec + 8 * j;
+          double2 v;
+          v.x = fma(qh, Bs[R * C::S + cc], acc[i][j][0]);
+          v.y = fma(qh, Bs[R * C::S + cc + 1], acc[i][j][1]);
+          *reinterpret_cast<double2*>(dst + cc) = v;
+        }
+      }
+    }
+    __syncthreads();  // this stage is reloaded next-next iteration
+    stage ^= 1;
+  }
+}
+
 // generic sizes: out (n x r_out) = [phi | q_hat] B
 __global__ void __launch_bounds__(256) rot_generic_kernel(RotArgs a) {
   extern __shared__ double sm[];
@@ -557,6 +691,20 @@ __global__ void __launch_bounds__(256) rot_generic_kernel(RotArgs a) {
 int ts_rotate(adrom_ctx* ctx, const RotArgs& a) {
   const int64_t n = a.n;
   const int r_in = a.r_in, r_out = a.r_out;
+  if (r_in == r_out && (r_in == 32 || r_in == 64) && !getenv("ADROM_NO_TC_ROT")) {
+    auto launch_tc = [&](auto kern, size_t sm_doubles) -> int {
+      const size_t sm = sizeof(double) * sm_doubles;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      const int64_t nt = (n + 63) / 64;
+      int64_t gg = (int64_t)ctx->num_sms * 2;
+      if (gg > nt) gg = nt;
+      kern<<<(int)(gg < 1 ? 1 : gg), 128, sm, ctx->stream>>>(a);
+      ADROM_LAUNCH_CK(ctx);
+      return ADROM_OK;
+    };
+    if (r_in == 32) return launch_tc(rot_tc_kernel<32>, RotTC<32>::smem_doubles);
+    return launch_tc(rot_tc_kernel<64>, RotTC<64>::smem_doubles);
+  }
   if (r_in == r_out && (r_in == 16 || r_in == 32 || r_in == 64 || r_in == 128)) {
     int64_t g = (int64_t)ctx->num_sms * 2;
     auto launch = [&](auto kern, int TM, int R) -> int {
