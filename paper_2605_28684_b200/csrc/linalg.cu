@@ -145,8 +145,7 @@ __global__ void reduce_partials_kernel(const double* __restrict__ partial, int n
 // ---------------------------------------------------------------------------
 template <int R, bool ROWDOT, bool DECODE, int WKIND>
 __global__ void __launch_bounds__(256) stream_kernel(TileArgs a) {
-  constexpr int LPR = (R >= 64) ? 32 : R / 2;  // lanes per row
-  constexpr int VPL = R / LPR;                 // doubles per lane (2 or 4)
+  constexpr int LPR = R / 8;                   // lanes per row (8 columns each)
   constexpr int RPW = 32 / LPR;                // rows per warp per sub-iteration
   constexpr int U = 4;                         // sub-iterations in flight
   __shared__ double red[8 * R];
@@ -154,66 +153,78 @@ __global__ void __launch_bounds__(256) stream_kernel(TileArgs a) {
   if (a.skip && *a.skip == 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int seg = lane / LPR, sl = lane - seg * LPR;
-  // lane columns: 2sl, 2sl+1 and (VPL == 4) 2sl+2LPR, 2sl+2LPR+1
-  double vv[VPL];
+  // lane columns: 2 (sl + LPR h) + {0, 1}, h < 4
+  double2 vv[4];
   if (ROWDOT) {
 #pragma unroll
-    for (int h = 0; h < VPL / 2; ++h) {
-      vv[2 * h] = a.v[2 * sl + 2 * LPR * h];
-      vv[2 * h + 1] = a.v[2 * sl + 2 * LPR * h + 1];
+    for (int h = 0; h < 4; ++h) {
+      vv[h].x = a.v[2 * (sl + LPR * h)];
+      vv[h].y = a.v[2 * (sl + LPR * h) + 1];
     }
   }
-  double acc[VPL];
+  double2 acc[4];
 #pragma unroll
-  for (int c = 0; c < VPL; ++c) acc[c] = 0.0;
+  for (int h = 0; h < 4; ++h) acc[h] = make_double2(0.0, 0.0);
   double sacc = 0.0;
   bool bad = false;
   const int64_t total_warps = (int64_t)gridDim.x * 8;
   const int64_t rows_per_iter = (int64_t)RPW * U;
   for (int64_t g = (int64_t)blockIdx.x * 8 + warp; g * rows_per_iter < a.n; g += total_warps) {
     const int64_t base = g * rows_per_iter;
-    double2 val[U][VPL / 2];
+    double2 val[U][4];
+    double xw[U], qr[U], dd[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t i = base + u * RPW + seg;
-      if (i < a.n) {
+      const bool live = i < a.n;
+      if (live) {
         const double2* rowp = reinterpret_cast<const double2*>(a.phi + i * R);
 #pragma unroll
-        for (int h = 0; h < VPL / 2; ++h) val[u][h] = rowp[sl + LPR * h];
+        for (int h = 0; h < 4; ++h) val[u][h] = rowp[sl + LPR * h];
       } else {
 #pragma unroll
-        for (int h = 0; h < VPL / 2; ++h) val[u][h] = make_double2(0.0, 0.0);
+        for (int h = 0; h < 4; ++h) val[u][h] = make_double2(0.0, 0.0);
       }
+      xw[u] = (WKIND != W_NONE && live) ? a.x[i] : 0.0;
+      qr[u] = ((DECODE || WKIND == W_ENCODE) && live) ? a.q_ref[i] : 0.0;
+      dd[u] = ((DECODE || WKIND == W_ENCODE) && live) ? a.d[i] : 1.0;
+    }
+    double rd[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      double t = 0.0;
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        bad |= !(isfinite(val[u][h].x) && isfinite(val[u][h].y));
+        if (ROWDOT) t += val[u][h].x * vv[h].x + val[u][h].y * vv[h].y;
+      }
+      rd[u] = t;
+    }
+    if (ROWDOT) {
+#pragma unroll
+      for (int o = LPR / 2; o > 0; o >>= 1)
+#pragma unroll
+        for (int u = 0; u < U; ++u) rd[u] += __shfl_xor_sync(0xffffffffu, rd[u], o);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t i = base + u * RPW + seg;
       const bool live = i < a.n;
-      double rd = 0.0;
-#pragma unroll
-      for (int h = 0; h < VPL / 2; ++h) {
-        bad |= !(isfinite(val[u][h].x) && isfinite(val[u][h].y));
-        if (ROWDOT) rd += val[u][h].x * vv[2 * h] + val[u][h].y * vv[2 * h + 1];
-      }
-      if (ROWDOT) {
-#pragma unroll
-        for (int o = LPR / 2; o > 0; o >>= 1) rd += __shfl_xor_sync(0xffffffffu, rd, o);
-      }
-      if (DECODE && live && sl == 0) a.out_q[i] = a.q_ref[i] + rd / a.d[i];
+      if (DECODE && live && sl == 0) a.out_q[i] = qr[u] + rd[u] / dd[u];
       if (WKIND != W_NONE && live) {
         double w;
-        if (WKIND == W_X) w = a.x[i];
-        else if (WKIND == W_ENCODE) w = a.d[i] * (a.x[i] - a.q_ref[i]);
-        else w = a.x[i] - rd;
+        if (WKIND == W_X) w = xw[u];
+        else if (WKIND == W_ENCODE) w = dd[u] * (xw[u] - qr[u]);
+        else w = xw[u] - rd[u];
         bad |= !isfinite(w);
         if (sl == 0) {
           sacc += w * w;
           if (a.out_w) a.out_w[i] = w;
         }
 #pragma unroll
-        for (int h = 0; h < VPL / 2; ++h) {
-          acc[2 * h] += val[u][h].x * w;
-          acc[2 * h + 1] += val[u][h].y * w;
+        for (int h = 0; h < 4; ++h) {
+          acc[h].x += val[u][h].x * w;
+          acc[h].y += val[u][h].y * w;
         }
       }
     }
@@ -226,12 +237,15 @@ __global__ void __launch_bounds__(256) stream_kernel(TileArgs a) {
 #pragma unroll
   for (int o = LPR; o < 32; o <<= 1)
 #pragma unroll
-    for (int c = 0; c < VPL; ++c) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+    for (int h = 0; h < 4; ++h) {
+      acc[h].x += __shfl_xor_sync(0xffffffffu, acc[h].x, o);
+      acc[h].y += __shfl_xor_sync(0xffffffffu, acc[h].y, o);
+    }
   if (seg == 0) {
 #pragma unroll
-    for (int h = 0; h < VPL / 2; ++h) {
-      red[warp * R + 2 * sl + 2 * LPR * h] = acc[2 * h];
-      red[warp * R + 2 * sl + 2 * LPR * h + 1] = acc[2 * h + 1];
+    for (int h = 0; h < 4; ++h) {
+      red[warp * R + 2 * (sl + LPR * h)] = acc[h].x;
+      red[warp * R + 2 * (sl + LPR * h) + 1] = acc[h].y;
     }
   }
   __syncthreads();
@@ -419,6 +433,7 @@ struct RotArgs {
   int64_t n;
   int r_in, r_out;
   double* out;
+  RotFuse fuse;  // fused epilogue work (rot_tc_kernel only)
 };
 
 template <int R>
@@ -520,7 +535,7 @@ struct RotTC {
   static constexpr int WN = R / 2;         // columns per warp
   static constexpr int NT = WN / 8;        // 8-wide column tiles per warp
   static constexpr int MT = 4;             // 8-row tiles per warp (32 rows)
-  static constexpr size_t smem_doubles = 2 * (size_t)TM * S + (size_t)(R + 1) * S + R;
+  static constexpr size_t smem_doubles = 2 * (size_t)TM * S + (size_t)(R + 1) * S + R + 2 * TM;
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
@@ -550,6 +565,11 @@ __global__ void __launch_bounds__(RotTC<R>::NTHR, 2) rot_tc_kernel(RotArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 1, wn = warp & 1;  // warp tile: rows 32 wm.., cols WN wn..
   const bool use_q = a.qbuf && (a.need == nullptr || *a.need != 0);
+  const bool enc = a.fuse.enc_partial != nullptr, seed = a.fuse.seed_res2 != nullptr;
+  double* rn = ps + R;  // 2 x TM row-norm halves
+  double enc_acc[C::NT][2];
+#pragma unroll
+  for (int j = 0; j < C::NT; ++j) enc_acc[j][0] = enc_acc[j][1] = 0.0;
   for (int e = tid; e < (R + 1) * R; e += C::NTHR) Bs[(e / R) * C::S + (e % R)] = a.B[e];
   for (int e = tid; e < R; e += C::NTHR) ps[e] = use_q ? 0.0 : a.p[e];
   const double qinv = *a.qinv;
@@ -615,26 +635,79 @@ __global__ void __launch_bounds__(RotTC<R>::NTHR, 2) rot_tc_kernel(RotArgs a) {
         for (int j = 0; j < C::NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
     __syncthreads();  // q_hat column visible
-    // epilogue: + q_hat (x) B[R, :], store
+    // epilogue: + q_hat (x) B[R, :], store; fused encode / QDEIM seed
     const int er = wm * 32 + (lane >> 2), ec = wn * C::WN + 2 * (lane & 3);
 #pragma unroll
     for (int i = 0; i < C::MT; ++i) {
       const int rr = er + 8 * i;
       const double qh = As[rr * C::S + R];
-      if (row0 + rr < n) {
-        double* dst = a.out + (row0 + rr) * R;
+      const bool ok = row0 + rr < n;
+      double w = 0.0;
+      if (enc && ok) {
+        const int64_t gi = row0 + rr;
+        w = a.fuse.enc_d[gi] * (a.fuse.enc_x[gi] - a.fuse.enc_q_ref[gi]);
+      }
+      double nrm = 0.0;
+      double* dst = a.out + (row0 + rr) * R;
 #pragma unroll
-        for (int j = 0; j < C::NT; ++j) {
-          const int cc = ec + 8 * j;
-          double2 v;
-          v.x = fma(qh, Bs[R * C::S + cc], acc[i][j][0]);
-          v.y = fma(qh, Bs[R * C::S + cc + 1], acc[i][j][1]);
-          *reinterpret_cast<double2*>(dst + cc) = v;
+      for (int j = 0; j < C::NT; ++j) {
+        const int cc = ec + 8 * j;
+        double2 v;
+        v.x = fma(qh, Bs[R * C::S + cc], acc[i][j][0]);
+        v.y = fma(qh, Bs[R * C::S + cc + 1], acc[i][j][1]);
+        if (ok) *reinterpret_cast<double2*>(dst + cc) = v;
+        nrm += v.x * v.x + v.y * v.y;
+        enc_acc[j][0] = fma(v.x, w, enc_acc[j][0]);
+        enc_acc[j][1] = fma(v.y, w, enc_acc[j][1]);
+      }
+      if (seed) {
+        nrm += __shfl_xor_sync(0xffffffffu, nrm, 1);
+        nrm += __shfl_xor_sync(0xffffffffu, nrm, 2);
+        if ((lane & 3) == 0) rn[wn * C::TM + rr] = nrm;
+      }
+    }
+    __syncthreads();  // this stage is reloaded next-next iteration; row norms visible
+    if (seed) {
+      for (int rr = tid; rr < C::TM; rr += C::NTHR) {
+        const int64_t gi = row0 + rr;
+        if (gi < n) {
+          const double nv = rn[rr] + rn[C::TM + rr];
+          a.fuse.seed_res2[gi] = nv;
+          a.fuse.seed_bnd2[gi] = nv + 16.0 * 2.220446049250313e-16 * nv;
+          a.fuse.seed_ver[gi] = 0;
         }
       }
     }
-    __syncthreads();  // this stage is reloaded next-next iteration
     stage ^= 1;
+  }
+  if (enc) {
+    // column sums: lanes with equal (lane & 3) share columns; then the wm warps
+#pragma unroll
+    for (int j = 0; j < C::NT; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double v = enc_acc[j][h];
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 16);
+        enc_acc[j][h] = v;
+      }
+    __syncthreads();
+    double* red = As0;  // (TM/32) x R
+    if (lane < 4) {
+#pragma unroll
+      for (int j = 0; j < C::NT; ++j) {
+        const int cc = wn * C::WN + 2 * lane + 8 * j;
+        red[wm * R + cc] = enc_acc[j][0];
+        red[wm * R + cc + 1] = enc_acc[j][1];
+      }
+    }
+    __syncthreads();
+    for (int c = tid; c < R; c += C::NTHR) {
+      double sum = 0.0;
+      for (int q = 0; q < C::TM / 32; ++q) sum += red[q * R + c];
+      a.fuse.enc_partial[(size_t)blockIdx.x * R + c] = sum;
+    }
   }
 }
 
@@ -688,17 +761,36 @@ __global__ void __launch_bounds__(256) rot_generic_kernel(RotArgs a) {
   }
 }
 
+bool rot_fusable(int r_in, int r_out) {
+  return r_in == r_out && (r_in == 32 || r_in == 64) && !getenv("ADROM_NO_TC_ROT");
+}
+
+static int64_t rot_tc_grid(const adrom_ctx* ctx, int64_t n) {
+  const int64_t nt = (n + 63) / 64;
+  int64_t gg = (int64_t)ctx->num_sms * 2;
+  if (gg > nt) gg = nt;
+  return gg < 1 ? 1 : gg;
+}
+
+size_t rot_fuse_partial_doubles(const adrom_ctx* ctx, int r) {
+  return (size_t)ctx->num_sms * 2 * (size_t)r;
+}
+
+int rot_encode_finish(adrom_ctx* ctx, const RotFuse& f, int64_t n, int r, double* out) {
+  reduce_partials_kernel<<<r, 256, 0, ctx->stream>>>(f.enc_partial, (int)rot_tc_grid(ctx, n), r,
+                                                     out, nullptr);
+  ADROM_LAUNCH_CK(ctx);
+  return ADROM_OK;
+}
+
 int ts_rotate(adrom_ctx* ctx, const RotArgs& a) {
   const int64_t n = a.n;
   const int r_in = a.r_in, r_out = a.r_out;
-  if (r_in == r_out && (r_in == 32 || r_in == 64) && !getenv("ADROM_NO_TC_ROT")) {
+  if (rot_fusable(r_in, r_out)) {
     auto launch_tc = [&](auto kern, size_t sm_doubles) -> int {
       const size_t sm = sizeof(double) * sm_doubles;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      const int64_t nt = (n + 63) / 64;
-      int64_t gg = (int64_t)ctx->num_sms * 2;
-      if (gg > nt) gg = nt;
-      kern<<<(int)(gg < 1 ? 1 : gg), 128, sm, ctx->stream>>>(a);
+      kern<<<(int)rot_tc_grid(ctx, n), 128, sm, ctx->stream>>>(a);
       ADROM_LAUNCH_CK(ctx);
       return ADROM_OK;
     };
@@ -1055,7 +1147,10 @@ int isvd_update_async(adrom_ctx* ctx, const double* phi, const double* sigma, co
                       int64_t n, int r_cur, int r, double lam, double* phi_out,
                       double* sigma_out, const double* gram_in, double* gram_out, void* ws,
                       int* flag, double reorth_ratio, double* stats_out, const double* dec_a,
-                      const double* q_ref, const double* d, double* dec_out) {
+                      const double* q_ref, const double* d, double* dec_out,
+                      const RotFuse* fuse) {
+  if (fuse && !rot_fusable(r_cur, r))
+    return set_error(ctx, ADROM_ERR_ARG, "isvd_update: fused epilogue needs r in {32, 64}");
   if (r_cur < 1 || r_cur > 110 || r < 1 || r > r_cur + 1)
     return set_error(ctx, ADROM_ERR_ARG, "isvd_update: bad ranks r_cur=%d r=%d", r_cur, r);
   if (phi_out == phi && r != r_cur)
@@ -1114,6 +1209,7 @@ int isvd_update_async(adrom_ctx* ctx, const double* phi, const double* sigma, co
   ADROM_LAUNCH_CK(ctx);
   // the rotation reads q from pass 2 when it ran, else forms it from y and p
   RotArgs ra{phi, y, qbuf, need, pls, qinv, B, n, r_cur, r, phi_out};
+  if (fuse) ra.fuse = *fuse;
   pr = prof_begin(ctx, PROBE_ISVD_ROTATE);
   st = ts_rotate(ctx, ra);
   prof_end(ctx, pr);

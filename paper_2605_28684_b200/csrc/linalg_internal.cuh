@@ -28,6 +28,25 @@ size_t gram_partial_doubles(const adrom_ctx* ctx, int r);
 // partial-sum region at the start of an iSVD workspace (fits ts_gram's)
 size_t isvd_partial_doubles(const adrom_ctx* ctx, int r_cur);
 
+// Work fused into the rotation's epilogue (the rotated rows are in registers):
+//   encode: enc_partial[block][0..r) = sum_i phi'_i d_i (x_i - q_ref_i)
+//           (projection.py:98-99; reduced by rot_encode_finish)
+//   seed  : QDEIM bounds res2 = bnd2(1 + 16 eps) = ||phi'_i||^2, ver = 0
+struct RotFuse {
+  const double* enc_x = nullptr;
+  const double* enc_q_ref = nullptr;
+  const double* enc_d = nullptr;
+  double* enc_partial = nullptr;  // rot_fuse_partial_doubles(ctx, r)
+  double* seed_res2 = nullptr;
+  double* seed_bnd2 = nullptr;
+  unsigned char* seed_ver = nullptr;
+};
+// true when ts_rotate runs the fused epilogue for this shape
+bool rot_fusable(int r_in, int r_out);
+size_t rot_fuse_partial_doubles(const adrom_ctx* ctx, int r);
+// out[0..r) = sum over the rotation blocks of enc_partial
+int rot_encode_finish(adrom_ctx* ctx, const RotFuse& f, int64_t n, int r, double* out);
+
 size_t isvd_workspace_bytes(adrom_ctx* ctx, int64_t n, int r_cur, int r);
 // Asynchronous iSVD update (tracking.py:141-178).
 //   gram_in  : tracked Phi^T Phi (r_cur x r_cur) or null (then computed here)
@@ -39,7 +58,8 @@ int isvd_update_async(adrom_ctx* ctx, const double* phi, const double* sigma, co
                       int64_t n, int r_cur, int r, double lam, double* phi_out,
                       double* sigma_out, const double* gram_in, double* gram_out, void* ws,
                       int* flag, double reorth_ratio, double* stats_out, const double* dec_a,
-                      const double* q_ref, const double* d, double* dec_out);
+                      const double* q_ref, const double* d, double* dec_out,
+                      const RotFuse* fuse = nullptr);
 
 int dense_small_svd(adrom_ctx* ctx, const double* a, int m, int n, double* u, double* s,
                     double* v, int* flag);

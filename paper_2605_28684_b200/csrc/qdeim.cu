@@ -823,8 +823,17 @@ static int qp_resvec(adrom_ctx* ctx, const double* phi, int r, const int64_t* po
   return ADROM_OK;
 }
 
+void qdeim_seed_buffers(void* ws, int64_t n, double** res2, double** bnd2, unsigned char** ver) {
+  char* w = (char*)ws;
+  *res2 = (double*)w;
+  w += align_up(sizeof(double) * (size_t)n);
+  *bnd2 = (double*)w;
+  w += align_up(sizeof(double) * (size_t)n);
+  *ver = (unsigned char*)w;
+}
+
 int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int count,
-                      int64_t* out_idx, void* ws, int* passes_out) {
+                      int64_t* out_idx, void* ws, int* passes_out, bool seeded) {
   if (count > n) return set_error(ctx, ADROM_ERR_DENSE, "cannot select %d pivots from %lld columns",
                                   count, (long long)n);
   if (r < 1 || r > 128) return set_error(ctx, ADROM_ERR_ARG, "qdeim: rank %d unsupported", r);
@@ -838,6 +847,7 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
   };
   double* res2 = (double*)take(sizeof(double) * (size_t)n);
   double* bnd2 = (double*)take(sizeof(double) * (size_t)n);
+  unsigned char* ver = (unsigned char*)take((size_t)n);  // (qdeim_seed_buffers)
   int64_t* pool_idx = (int64_t*)take(sizeof(int64_t) * (size_t)P);
   double* Rv = (double*)take(sizeof(double) * (size_t)P * r);
   double* pres2 = (double*)take(sizeof(double) * (size_t)P);
@@ -845,7 +855,6 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
   SelState* sel = (SelState*)take(sizeof(SelState));
   SelState* selR = (SelState*)take(sizeof(SelState));
   int64_t* rlist = (int64_t*)take(sizeof(int64_t) * (size_t)n);
-  unsigned char* ver = (unsigned char*)take((size_t)n);
   unsigned int* hist = (unsigned int*)take(sizeof(unsigned int) * 256);
   double* D = (double*)take(sizeof(double) * (size_t)r * r);
   int64_t* piv = (int64_t*)take(sizeof(int64_t) * (size_t)r);
@@ -916,9 +925,13 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
       ADROM_LAUNCH_CK(ctx);
     }
     ADROM_CK(ctx, cudaMemsetAsync(state, 0, sizeof(int) * 8, ctx->stream));
-    // seed: every bound = ||phi_i||^2 (fresh for k = 0)
-    int st = rows_pass(n, 0, QP_SEED, nullptr, n_ex);
-    if (st) return st;
+    // seed: every bound = ||phi_i||^2 (fresh for k = 0); the first chunk's
+    // seed may come from the rotation epilogue
+    if (!(seeded && chosen == 0)) {
+      int st0 = rows_pass(n, 0, QP_SEED, nullptr, n_ex);
+      if (st0) return st0;
+    }
+    int st = ADROM_OK;
     int k = 0;
     bool fresh = true;                       // bounds of the top rows are current
     int64_t rl_n = 0;                        // refresh-list slots (0: none this round)

@@ -18,8 +18,11 @@ size_t qdeim_workspace_bytes(adrom_ctx* ctx, int r, int count);
 // Exact greedy via a certified candidate pool (qdeim.cu): the path used by
 // the session and the C-ABI.  Blocking (one sync per pass).
 size_t qdeim_pool_workspace_bytes(int64_t n, int r, int count);
+// seeded: the workspace's res2/bnd2/ver already hold the k = 0 bounds
+// (||phi_i||^2, written by the rotation epilogue: qdeim_seed_buffers)
 int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int count,
-                      int64_t* out_idx, void* ws, int* passes_out);
+                      int64_t* out_idx, void* ws, int* passes_out, bool seeded = false);
+void qdeim_seed_buffers(void* ws, int64_t n, double** res2, double** bnd2, unsigned char** ver);
 // First `count` pivots of the restarted column-pivoted QR of phi^T
 // (sampling.py:77-104), exact greedy, ties to the lowest row.  Blocking
 // (synchronises once per verification pass).  `guess` may be null.

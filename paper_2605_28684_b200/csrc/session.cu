@@ -91,6 +91,7 @@ struct adrom_session {
   double* isvd_stats = nullptr;
   void* isvd_ws = nullptr;
   void* qd_ws = nullptr;
+  double* enc_partial = nullptr;  // fused encode partial sums (rotation epilogue)
   double* step_log = nullptr;    // n_t_online x 3
   int* fail_step = nullptr;
   int64_t n_online = 0;          // steps done
@@ -142,7 +143,7 @@ int alloc_op(adrom_session* s, adrom_rom_op& op) {
 
 // sampling (driver.py:264-273) + closure + operator for basis `phi` into op
 int build_sampling_operator(adrom_session* s, const double* phi, adrom_rom_op& op,
-                            const double* y_corr) {
+                            const double* y_corr, bool seeded = false) {
   adrom_ctx* ctx = s->ctx;
   const adrom_model m = model_of(s);
   const int n_s = s->cfg.n_s;
@@ -151,7 +152,7 @@ int build_sampling_operator(adrom_session* s, const double* phi, adrom_rom_op& o
   if (s->cfg.sampling == 1) {
     const int n_base = n_s - s->cfg.n_extra;
     if (n_base > 0) {
-      st = qdeim_pool_select(ctx, phi, s->N, s->r, n_base, op.idx, s->qd_ws, &it);
+      st = qdeim_pool_select(ctx, phi, s->N, s->r, n_base, op.idx, s->qd_ws, &it, seeded);
       if (st) return st;
     }
     st = reset_flags(ctx);
@@ -159,7 +160,7 @@ int build_sampling_operator(adrom_session* s, const double* phi, adrom_rom_op& o
     st = fgs_extend(ctx, m, y_corr, s->cfg.feature, op.idx, n_base, s->cfg.n_extra, nullptr);
     if (st) return st;
   } else {
-    st = qdeim_pool_select(ctx, phi, s->N, s->r, n_s, op.idx, s->qd_ws, &it);
+    st = qdeim_pool_select(ctx, phi, s->N, s->r, n_s, op.idx, s->qd_ws, &it, seeded);
     if (st) return st;
     st = reset_flags(ctx);
     if (st) return st;
@@ -212,10 +213,23 @@ int rom_step(adrom_session* s) {
   return ADROM_OK;
 }
 
-// one adaptation event (driver.py:351-387, history-aware branch)
-int run_event(adrom_session* s, adrom_event_record& ev) {
+// q~ = q_ref + (Phi a) / d with the current basis (projection.py:104)
+int decode_state(adrom_session* s) {
+  adrom_ctx* ctx = s->ctx;
+  const int pr = prof_begin(ctx, PROBE_DECODE);
+  const int st = ts_decode(ctx, s->phi[s->cur], s->N, s->r, s->a, s->q_ref, s->d, s->q_tilde);
+  prof_end(ctx, pr);
+  return st;
+}
+
+// one adaptation event (driver.py:351-387, history-aware branch).  The
+// decode of the reduced state (driver.py:345) rides on the iSVD's first pass
+// over the old basis (*decoded = true); the state transfer (encode, :376) and
+// the QDEIM seed bounds ride on the rotation that writes the new basis.
+int run_event(adrom_session* s, adrom_event_record& ev, bool* decoded) {
   adrom_ctx* ctx = s->ctx;
   const adrom_model m = model_of(s);
+  *decoded = false;
   ev.error = 0;
   ev.residual_norm = 0.0;
   // advance_signal: coarse backward-Euler step of size z*dt (driver.py:354-358)
@@ -238,13 +252,23 @@ int run_event(adrom_session* s, adrom_event_record& ev) {
   ADROM_LAUNCH_CK(ctx);
   // iSVD into the spare buffers
   const int nxt = 1 - s->cur;
+  const bool fused = rot_fusable(s->r, s->r);
+  RotFuse fz;
+  if (fused) {
+    fz.enc_x = s->q_tilde;
+    fz.enc_q_ref = s->q_ref;
+    fz.enc_d = s->d;
+    fz.enc_partial = s->enc_partial;
+    qdeim_seed_buffers(s->qd_ws, s->N, &fz.seed_res2, &fz.seed_bnd2, &fz.seed_ver);
+  }
   st = reset_flags(ctx);
   if (st) return st;
   st = isvd_update_async(ctx, s->phi[s->cur], s->sigma[s->cur], s->y_hat, s->N, s->r, s->r,
                          s->cfg.lam, s->phi[nxt], s->sigma[nxt], s->gram[s->cur], s->gram[nxt],
-                         s->isvd_ws, ctx->dflags, ISVD_REORTH_RATIO, s->isvd_stats, nullptr,
-                         nullptr, nullptr, nullptr);
+                         s->isvd_ws, ctx->dflags, ISVD_REORTH_RATIO, s->isvd_stats, s->a,
+                         s->q_ref, s->d, s->q_tilde, fused ? &fz : nullptr);
   if (st) return st;
+  *decoded = true;
   int flags[16];
   ADROM_CK(ctx, cudaMemcpyAsync((char*)ctx->pinned + 512, s->isvd_stats, sizeof(double) * 8,
                                 cudaMemcpyDeviceToHost, ctx->stream));
@@ -262,15 +286,24 @@ int run_event(adrom_session* s, adrom_event_record& ev) {
   ev.residual_norm = hs[2];  // ||y - Phi Phi^T y|| with the old basis (driver.py:366-367)
   // sampling + operator for the new basis (driver.py:369-374)
   const int onx = 1 - s->opcur;
-  st = build_sampling_operator(s, s->phi[nxt], s->op[onx], s->y_corr);
+  st = build_sampling_operator(s, s->phi[nxt], s->op[onx], s->y_corr, fused);
   if (st == ADROM_ERR_CUDA) return st;
   if (st) {
     ev.error = st;
     return ADROM_OK;
   }
   // state transfer a = Phi'^T D (q~ - q_ref)  (driver.py:376)
-  st = encode_into(s, s->phi[nxt], s->q_tilde, s->a);
-  if (st) return st;
+  if (fused) {
+    const int pr = prof_begin(ctx, PROBE_ENCODE);
+    st = rot_encode_finish(ctx, fz, s->N, s->r, s->rom_info + 16);
+    prof_end(ctx, pr);
+    if (st) return st;
+    ADROM_CK(ctx, cudaMemcpyAsync(s->a, s->rom_info + 16, sizeof(double) * s->r,
+                                  cudaMemcpyDeviceToDevice, ctx->stream));
+  } else {
+    st = encode_into(s, s->phi[nxt], s->q_tilde, s->a);
+    if (st) return st;
+  }
   s->cur = nxt;
   s->opcur = onx;
   return ADROM_OK;
@@ -315,6 +348,7 @@ int adrom_session_create(adrom_ctx* ctx, const adrom_session_config* cfg, adrom_
   s->allocs.push_back(s->isvd_ws);
   cudaMalloc(&s->qd_ws, qdeim_pool_workspace_bytes(N, r, cfg->n_s));
   s->allocs.push_back(s->qd_ws);
+  s->enc_partial = s->alloc_d(rot_fuse_partial_doubles(ctx, r));
   s->guess.r = r;
   s->guess.max_chunks = (cfg->n_s + r - 1) / r;
   if (s->guess.max_chunks > 64) s->guess.max_chunks = 64;
@@ -407,12 +441,21 @@ int adrom_session_advance(adrom_session* s, int64_t n_steps, int64_t save_every,
     const int64_t n = s->cfg.w_init + s->n_online;  // driver loop index
     int st = rom_step(s);
     if (st) return st;
-    const int pr = prof_begin(ctx, PROBE_DECODE);
-    st = ts_decode(ctx, s->phi[s->cur], N, s->r, s->a, s->q_ref, s->d, s->q_tilde);
-    prof_end(ctx, pr);
-    if (st) return st;
     ++s->n_online;
-    if (save_every > 0 && (s->n_online % save_every == 0 || k == n_steps - 1)) {
+    const bool save = save_every > 0 && (s->n_online % save_every == 0 || k == n_steps - 1);
+    const bool at_event = s->cfg.adaptive && ((n + 1 - s->cfg.w_init) % s->cfg.z == 0);
+    adrom_event_record ev{};
+    bool decoded = false;
+    if (at_event) {
+      ev.step = n + 1;
+      st = run_event(s, ev, &decoded);  // decodes q~ in its first basis pass
+      if (st) return st;
+    }
+    if (!decoded) {
+      st = decode_state(s);
+      if (st) return st;
+    }
+    if (save) {
       if (dev_out)
         ADROM_CK(ctx, cudaMemcpyAsync(dev_out + saved * N, s->q_tilde, 8 * N,
                                       cudaMemcpyDeviceToDevice, ctx->stream));
@@ -421,12 +464,7 @@ int adrom_session_advance(adrom_session* s, int64_t n_steps, int64_t save_every,
                                       cudaMemcpyDeviceToHost, ctx->stream));
       ++saved;
     }
-    const bool at_event = s->cfg.adaptive && ((n + 1 - s->cfg.w_init) % s->cfg.z == 0);
     if (at_event) {
-      adrom_event_record ev{};
-      ev.step = n + 1;
-      st = run_event(s, ev);
-      if (st) return st;
       s->events.push_back(ev);
       // a failed reduced step aborts the run like the reference (driver.py:338)
       int fs = -1;
