@@ -88,7 +88,9 @@ __device__ bool block_qr_certified_solve(double* jA, int ld, int r, double* rhs,
     if (tid == 0) col[k] = sh_alpha;
     __syncthreads();
   }
-  // ||R||_F and ||R^{-1}||_F (column c of R^{-1} by back substitution)
+  // ||R||_F and ||R^{-1}||_F.  Column c of R^{-1} (R x = e_c) by
+  // column-oriented back substitution, one warp per column: x_i = b_i / R_ii,
+  // then b_j -= R_ji x_i for j < i (column i of R is contiguous in jA).
   double rf = 0.0;
   for (int e = tid; e < r * r; e += blockDim.x) {
     const int l = e / r, k = e - l * r;
@@ -97,20 +99,33 @@ __device__ bool block_qr_certified_solve(double* jA, int ld, int r, double* rhs,
   rf = block_sum_dyn(rf, red);
   double inv2 = 0.0;
   bool bad = false;
-  for (int c = tid; c < r; c += blockDim.x) {
-    // solve R x = e_c (x_i = 0 for i > c)
-    double xs[128];
+  for (int c = warp; c < r; c += nw) {
+    // lane holds b_j for j = lane + 32 t (t < 4, r <= 128)
+    double b[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) b[t] = (lane + 32 * t == c) ? 1.0 : 0.0;
     for (int i = c; i >= 0; --i) {
-      double s = (i == c) ? 1.0 : 0.0;
-      for (int l = i + 1; l <= c; ++l) s -= jA[(size_t)l * ld + i] * xs[l];
+      const int ti = i >> 5, li = i & 31;
+      double bi = 0.0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (t == ti) bi = b[t];
+      bi = __shfl_sync(0xffffffffu, bi, li);
       const double d = jA[(size_t)i * ld + i];
+      double xi;
       if (d == 0.0) {
         bad = true;
-        xs[i] = 0.0;
+        xi = 0.0;
       } else {
-        xs[i] = s / d;
+        xi = bi / d;
       }
-      inv2 += xs[i] * xs[i];
+      if (lane == 0) inv2 += xi * xi;
+      const double* col = jA + (size_t)i * ld;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int j = lane + 32 * t;
+        if (j < i) b[t] -= col[j] * xi;
+      }
     }
   }
   inv2 = block_sum_dyn(inv2, red);
@@ -120,11 +135,26 @@ __device__ bool block_qr_certified_solve(double* jA, int ld, int r, double* rhs,
   if (bad) sh_bad = 1;
   __syncthreads();
   const bool cert = !sh_bad && isfinite(inv2) && isfinite(rf) && sqrt(rf) * sqrt(inv2) <= LS_CERT;
-  if (cert && tid == 0) {
+  if (cert && warp == 0) {
+    // R out = rhs, same column-oriented substitution on one warp
+    double b[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) b[t] = (lane + 32 * t < r) ? rhs[lane + 32 * t] : 0.0;
     for (int i = r - 1; i >= 0; --i) {
-      double s = rhs[i];
-      for (int l = i + 1; l < r; ++l) s -= jA[(size_t)l * ld + i] * out[l];
-      out[i] = s / jA[(size_t)i * ld + i];
+      const int ti = i >> 5, li = i & 31;
+      double bi = 0.0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (t == ti) bi = b[t];
+      bi = __shfl_sync(0xffffffffu, bi, li);
+      const double xi = bi / jA[(size_t)i * ld + i];
+      if (lane == 0) out[i] = xi;
+      const double* col = jA + (size_t)i * ld;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int j = lane + 32 * t;
+        if (j < i) b[t] -= col[j] * xi;
+      }
     }
   }
   __syncthreads();
@@ -202,13 +232,24 @@ __global__ void __launch_bounds__(512) lspg_kernel(RomStepArgs A) {
       test[e] = A.op.phi_s[e] - A.dt * (A.op.d_s[j] * df);
     }
     __syncthreads();
-    // jac = pinv @ test  -> stored column-major in jA
-    for (int o = warp; o < r * r; o += nw) {
+    // jac = pinv @ test -> stored column-major in jA; thread per entry
+    // (consecutive threads: consecutive l, coalesced rows of test).  The sum
+    // keeps the 32-lane strided + butterfly order of a warp reduction.
+    for (int o = tid; o < r * r; o += blockDim.x) {
       const int k = o / r, l = o - k * r;
-      double s = 0.0;
-      for (int j = lane; j < n_s; j += 32) s += A.op.pinv[(int64_t)k * n_s + j] * test[j * r + l];
-      s = warp_sum(s);
-      if (lane == 0) jA[l * ld + k] = s;
+      const double* pk = A.op.pinv + (int64_t)k * n_s;
+      double v[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        double t = 0.0;
+        for (int j = q; j < n_s; j += 32) t += pk[j] * test[j * r + l];
+        v[q] = t;
+      }
+#pragma unroll
+      for (int w = 16; w > 0; w >>= 1)
+#pragma unroll
+        for (int q = 0; q < w; ++q) v[q] = v[q] + v[q + w];
+      jA[l * ld + k] = v[0];
     }
     __syncthreads();
     // grad = jac^T rho
