@@ -790,6 +790,93 @@ __global__ void qp_all_rows_kernel(int64_t* __restrict__ pool_idx, int64_t n) {
     pool_idx[i] = i;
 }
 
+// ---------------------------------------------------------------------------
+// QP_REFRESH on the FP64 tensor cores (r in {32, 64, 128}): a warp takes 8
+// list rows, S = X_rows D[:, lo:k] by DMMA m8n8k4 (A fragments straight from
+// the rows in global memory, B fragments from smem), then
+// res2 -= sum_{ver_i <= l < k} S_il^2 as in qp_rows_kernel.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void qp_dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) qp_refresh_tc_kernel(const double* __restrict__ phi,
+                                                            const int64_t* __restrict__ list,
+                                                            int64_t cap,
+                                                            const double* __restrict__ D, int k,
+                                                            double* __restrict__ res2,
+                                                            double* __restrict__ bnd2,
+                                                            unsigned char* __restrict__ ver) {
+  constexpr int S = R + 4;     // smem row stride: conflict-free B fragments
+  constexpr int KS = R / 4;    // k-steps over the basis columns
+  constexpr int DT = R / 8;    // direction tiles
+  extern __shared__ __align__(16) double Ds[];  // R x S: Ds[j*S + l] = D[j][l] (l < k)
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int j = e / R, l = e - j * R;
+    Ds[j * S + l] = (l < k) ? D[j * R + l] : 0.0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rq = lane >> 2, cq = lane & 3;  // fragment row / column quad
+  const int64_t tiles = (cap + 7) / 8;
+  for (int64_t t = (int64_t)blockIdx.x * 8 + warp; t < tiles; t += (int64_t)gridDim.x * 8) {
+    const int64_t pos = t * 8 + rq;
+    const int64_t i = (pos < cap) ? list[pos] : -1;
+    const int v = (i >= 0) ? (int)ver[i] : k;
+    const int vmin = __reduce_min_sync(0xffffffffu, v);
+    if (vmin >= k) continue;  // nothing new for any of the 8 rows
+    double af[KS];
+    double nrm = 0.0;
+    const double* row = phi + (i >= 0 ? i : 0) * R;
+#pragma unroll
+    for (int j = 0; j < KS; ++j) {
+      af[j] = (i >= 0) ? row[4 * j + cq] : 0.0;
+      nrm = fma(af[j], af[j], nrm);
+    }
+    nrm += __shfl_xor_sync(0xffffffffu, nrm, 1);
+    nrm += __shfl_xor_sync(0xffffffffu, nrm, 2);
+    double sub = 0.0;
+    const int t0 = vmin >> 3, t1 = (k + 7) >> 3;
+#pragma unroll
+    for (int dt = 0; dt < DT; ++dt) {
+      if (dt < t0 || dt >= t1) continue;
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < KS; ++j) qp_dmma(c0, c1, af[j], Ds[(4 * j + cq) * S + 8 * dt + rq]);
+      // c0, c1 = S[row rq][dir 8 dt + 2 cq + {0, 1}]
+      const int l0 = 8 * dt + 2 * cq;
+      // rows of the C fragment are lane >> 2 as well: same row as this lane's A
+      if (l0 >= v && l0 < k) sub = fma(c0, c0, sub);
+      if (l0 + 1 >= v && l0 + 1 < k) sub = fma(c1, c1, sub);
+    }
+    sub += __shfl_xor_sync(0xffffffffu, sub, 1);
+    sub += __shfl_xor_sync(0xffffffffu, sub, 2);
+    if (cq == 0 && i >= 0 && v < k) {
+      const double r2 = res2[i] - sub;
+      res2[i] = r2;
+      ver[i] = (unsigned char)k;
+      bnd2[i] = fmin(bnd2[i], r2 + 8.0 * (double)(k + 2) * QP_EPS * nrm);
+    }
+  }
+}
+
+template <int R>
+static int qp_refresh_tc(adrom_ctx* ctx, const double* phi, const int64_t* list, int64_t cap,
+                         const double* D, int k, double* res2, double* bnd2, unsigned char* ver) {
+  const size_t sm = sizeof(double) * (size_t)R * (R + 4);
+  const int64_t tiles = (cap + 7) / 8;
+  int64_t g = (tiles + 7) / 8;
+  if (g > (int64_t)ctx->num_sms * 8) g = (int64_t)ctx->num_sms * 8;
+  cudaFuncSetAttribute(qp_refresh_tc_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  qp_refresh_tc_kernel<R><<<(int)(g < 1 ? 1 : g), 256, sm, ctx->stream>>>(phi, list, cap, D, k,
+                                                                          res2, bnd2, ver);
+  ADROM_LAUNCH_CK(ctx);
+  return ADROM_OK;
+}
+
 template <int R, bool EXACT>
 static int qp_rows_launch(adrom_ctx* ctx, const double* phi, int64_t n, int r, const double* D,
                           int hi, int mode, const int64_t* list, double* res2, double* bnd2,
@@ -952,7 +1039,13 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
         ADROM_LAUNCH_CK(ctx);
         qs_compact_kernel<<<sg, 256, 0, ctx->stream>>>(bnd2, n, nullptr, selR, rlist, cap);
         ADROM_LAUNCH_CK(ctx);
-        st = rows_pass(cap, k, QP_REFRESH, rlist, n_ex);
+        if (r == 32 || r == 64 || r == 128) {
+          st = (r == 32)   ? qp_refresh_tc<32>(ctx, phi, rlist, cap, D, k, res2, bnd2, ver)
+               : (r == 64) ? qp_refresh_tc<64>(ctx, phi, rlist, cap, D, k, res2, bnd2, ver)
+                           : qp_refresh_tc<128>(ctx, phi, rlist, cap, D, k, res2, bnd2, ver);
+        } else {
+          st = rows_pass(cap, k, QP_REFRESH, rlist, n_ex);
+        }
         if (st) return st;
         ++refreshed;
         rl_n = cap;
