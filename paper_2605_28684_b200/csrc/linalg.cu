@@ -523,19 +523,21 @@ __global__ void __launch_bounds__(256) rot_tiled_kernel(RotArgs a) {
 // FP64 tensor-core rotation (R in {32, 64}): out = [phi | q_hat] B on DMMA
 // (mma.sync m8n8k4 f64).  64-row tiles double-buffered in smem by cp.async
 // (row stride R + 4: conflict-free fragment loads; column R holds q_hat);
-// 4 warps as 2 (rows) x 2 (cols), each warp 32 rows x R/2 columns; two
+// 8 warps as 4 (rows) x 2 (cols), each warp 16 rows x R/2 columns; two
 // blocks per SM so one block's epilogue overlaps the other's MMAs.  The
 // q_hat column is a rank-1 FMA update in the epilogue.
 // ---------------------------------------------------------------------------
 template <int R>
 struct RotTC {
   static constexpr int TM = 64;            // rows per tile; 2 blocks per SM
-  static constexpr int NTHR = TM / 32 * 64;  // (TM/32) x 2 warps
+  static constexpr int WGN = 2;            // column groups of warps
+  static constexpr int MT = 2;             // 8-row tiles per warp
+  static constexpr int WR = 8 * MT;        // rows per warp
+  static constexpr int NTHR = TM / WR * WGN * 32;
   static constexpr int S = R + 4;          // smem row stride (doubles)
-  static constexpr int WN = R / 2;         // columns per warp
+  static constexpr int WN = R / WGN;       // columns per warp
   static constexpr int NT = WN / 8;        // 8-wide column tiles per warp
-  static constexpr int MT = 4;             // 8-row tiles per warp (32 rows)
-  static constexpr size_t smem_doubles = 2 * (size_t)TM * S + (size_t)(R + 1) * S + R + 2 * TM;
+  static constexpr size_t smem_doubles = 2 * (size_t)TM * S + (size_t)(R + 1) * S + R + WGN * TM;
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
@@ -563,10 +565,10 @@ __global__ void __launch_bounds__(RotTC<R>::NTHR, 2) rot_tc_kernel(RotArgs a) {
   double* Bs = sm + 2 * C::TM * C::S;    // (R+1) x S
   double* ps = Bs + (R + 1) * C::S;      // R
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 1, wn = warp & 1;  // warp tile: rows 32 wm.., cols WN wn..
+  const int wm = warp / C::WGN, wn = warp % C::WGN;  // warp tile: rows WR wm.., cols WN wn..
   const bool use_q = a.qbuf && (a.need == nullptr || *a.need != 0);
   const bool enc = a.fuse.enc_partial != nullptr, seed = a.fuse.seed_res2 != nullptr;
-  double* rn = ps + R;  // 2 x TM row-norm halves
+  double* rn = ps + R;  // WGN x TM row-norm parts
   double enc_acc[C::NT][2];
 #pragma unroll
   for (int j = 0; j < C::NT; ++j) enc_acc[j][0] = enc_acc[j][1] = 0.0;
@@ -620,7 +622,7 @@ __global__ void __launch_bounds__(RotTC<R>::NTHR, 2) rot_tc_kernel(RotArgs a) {
     for (int i = 0; i < C::MT; ++i)
 #pragma unroll
       for (int j = 0; j < C::NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    const int ar = wm * 32 + (lane >> 2), ak = lane & 3;
+    const int ar = wm * C::WR + (lane >> 2), ak = lane & 3;
     const int bn = wn * C::WN + (lane >> 2), bk = lane & 3;
 #pragma unroll 2
     for (int k0 = 0; k0 < R; k0 += 4) {
@@ -636,7 +638,7 @@ __global__ void __launch_bounds__(RotTC<R>::NTHR, 2) rot_tc_kernel(RotArgs a) {
     }
     __syncthreads();  // q_hat column visible
     // epilogue: + q_hat (x) B[R, :], store; fused encode / QDEIM seed
-    const int er = wm * 32 + (lane >> 2), ec = wn * C::WN + 2 * (lane & 3);
+    const int er = wm * C::WR + (lane >> 2), ec = wn * C::WN + 2 * (lane & 3);
 #pragma unroll
     for (int i = 0; i < C::MT; ++i) {
       const int rr = er + 8 * i;
@@ -671,7 +673,9 @@ __global__ void __launch_bounds__(RotTC<R>::NTHR, 2) rot_tc_kernel(RotArgs a) {
       for (int rr = tid; rr < C::TM; rr += C::NTHR) {
         const int64_t gi = row0 + rr;
         if (gi < n) {
-          const double nv = rn[rr] + rn[C::TM + rr];
+          double nv = 0.0;
+#pragma unroll
+          for (int q = 0; q < C::WGN; ++q) nv += rn[q * C::TM + rr];
           a.fuse.seed_res2[gi] = nv;
           a.fuse.seed_bnd2[gi] = nv + 16.0 * 2.220446049250313e-16 * nv;
           a.fuse.seed_ver[gi] = 0;
@@ -693,7 +697,7 @@ __global__ void __launch_bounds__(RotTC<R>::NTHR, 2) rot_tc_kernel(RotArgs a) {
         enc_acc[j][h] = v;
       }
     __syncthreads();
-    double* red = As0;  // (TM/32) x R
+    double* red = As0;  // (TM/WR) x R
     if (lane < 4) {
 #pragma unroll
       for (int j = 0; j < C::NT; ++j) {
@@ -705,7 +709,7 @@ __global__ void __launch_bounds__(RotTC<R>::NTHR, 2) rot_tc_kernel(RotArgs a) {
     __syncthreads();
     for (int c = tid; c < R; c += C::NTHR) {
       double sum = 0.0;
-      for (int q = 0; q < C::TM / 32; ++q) sum += red[q * R + c];
+      for (int q = 0; q < C::TM / C::WR; ++q) sum += red[q * R + c];
       a.fuse.enc_partial[(size_t)blockIdx.x * R + c] = sum;
     }
   }
@@ -790,7 +794,7 @@ int ts_rotate(adrom_ctx* ctx, const RotArgs& a) {
     auto launch_tc = [&](auto kern, size_t sm_doubles) -> int {
       const size_t sm = sizeof(double) * sm_doubles;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      kern<<<(int)rot_tc_grid(ctx, n), 128, sm, ctx->stream>>>(a);
+      kern<<<(int)rot_tc_grid(ctx, n), RotTC<64>::NTHR, sm, ctx->stream>>>(a);
       ADROM_LAUNCH_CK(ctx);
       return ADROM_OK;
     };
