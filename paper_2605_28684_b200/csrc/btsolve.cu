@@ -255,6 +255,106 @@ __global__ void part_solve_kernel(const double* __restrict__ sys, const double* 
 }
 
 // ---------------------------------------------------------------------------
+// scalar (n_var = 1) partitions: the same elimination, staged through smem so
+// that global traffic is coalesced.  A warp owns 32 consecutive partitions
+// (1024 rows); lane p walks partition p in smem (stride 33: conflict-free).
+// G lives in D's slot, the outputs Y / V / W overwrite rhs / L / U.
+// ---------------------------------------------------------------------------
+constexpr int PS_WARPS = 2;
+constexpr int PS_LD = BT_M + 1;
+
+__global__ void __launch_bounds__(32 * PS_WARPS) part_solve_scalar_kernel(
+    const double* __restrict__ sys, const double* __restrict__ rhs, double sign, int64_t n,
+    double* __restrict__ Y, double* __restrict__ V, double* __restrict__ W, int* __restrict__ flag) {
+  extern __shared__ double sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* sL = sm + (size_t)warp * 4 * 32 * PS_LD;
+  double* sD = sL + 32 * PS_LD;
+  double* sU = sD + 32 * PS_LD;
+  double* sB = sU + 32 * PS_LD;
+  const int64_t P = (n + BT_M - 1) / BT_M;
+  const int64_t groups = (P + 31) / 32;
+  bool ok = true;
+  for (int64_t gidx = (int64_t)blockIdx.x * PS_WARPS + warp; gidx < groups;
+       gidx += (int64_t)gridDim.x * PS_WARPS) {
+    const int64_t row0 = gidx * 32 * BT_M;
+    const int rows = (int)((n - row0 < 32 * BT_M) ? (n - row0) : 32 * BT_M);
+    __syncwarp();
+    for (int j = lane; j < rows; j += 32) {
+      const int pp = j / BT_M, ii = j - pp * BT_M, o = pp * PS_LD + ii;
+      const int64_t gi = row0 + j;
+      sL[o] = sys[gi * 3 + 0];
+      sD[o] = sys[gi * 3 + 1];
+      sU[o] = sys[gi * 3 + 2];
+      sB[o] = sign * rhs[gi];
+    }
+    __syncwarp();
+    // lane = partition within the group
+    const int64_t s = row0 + (int64_t)lane * BT_M;
+    const int m = (s < n) ? (int)(((s + BT_M < n) ? s + BT_M : n) - s) : 0;  // rows in it
+    const int base = lane * PS_LD;
+    if (m > 1) {
+      const int last = m - 1;  // local index of the interface row e
+      double cb = 0.0, cV = 0.0, Gp = 0.0, cW = 0.0;
+      for (int i = 0; i < last; ++i) {
+        const double L = sL[base + i];
+        double D = sD[base + i];
+        const double U = sU[base + i];
+        double b = sB[base + i];
+        double fV;
+        if (i > 0) {
+          D -= L * Gp;
+          b -= L * cb;
+          fV = -(L * cV);
+        } else {
+          fV = -L;
+        }
+        if (D == 0.0 || !isfinite(D)) ok = false;
+        // lu<1> / lu_solve<1>: multiply by the reciprocal pivot, then divide
+        b /= D;
+        fV /= D;
+        cb = b;
+        cV = fV;
+        if (i < last - 1) {
+          Gp = U / D;
+        } else {
+          cW = (-U) / D;
+          Gp = 0.0;
+        }
+        sB[base + i] = cb;
+        sL[base + i] = cV;
+        sD[base + i] = Gp;
+      }
+      // backward sweep (as part_solve_kernel)
+      double yn = cb, Vn = cV, Wn = cW;
+      sU[base + last - 1] = Wn;
+      for (int i = last - 2; i >= 0; --i) {
+        const double Gi = sD[base + i];
+        yn = sB[base + i] - Gi * yn;
+        Vn = sL[base + i] - Gi * Vn;
+        Wn = -(Gi * Wn);
+        sB[base + i] = yn;
+        sL[base + i] = Vn;
+        sU[base + i] = Wn;
+      }
+    }
+    __syncwarp();
+    for (int j = lane; j < rows; j += 32) {
+      const int pp = j / BT_M, ii = j - pp * BT_M, o = pp * PS_LD + ii;
+      const int64_t ps = row0 + (int64_t)pp * BT_M;
+      const int64_t pe = ((ps + BT_M < n) ? ps + BT_M : n) - 1;
+      const int64_t gi = row0 + j;
+      if (gi < pe) {  // interior rows only (the interface row keeps no Y/V/W)
+        Y[gi] = sB[o];
+        V[gi] = sL[o];
+        W[gi] = sU[o];
+      }
+    }
+  }
+  if (!ok) atomicOr(flag, 2);
+}
+
+// ---------------------------------------------------------------------------
 // interface rows -> reduced system (or, with one partition, its solution)
 // ---------------------------------------------------------------------------
 template <int NV>
@@ -444,8 +544,19 @@ static int bt_solve_t(adrom_ctx* ctx, const double* sys, const double* rhs, doub
     double* nsol = take(sizeof(double) * P * NV);
     const int nt = 128;
     const int gb = (int)((P + nt - 1) / nt);
-    part_solve_kernel<NV><<<gb, nt, 0, ctx->stream>>>(L.sys, L.rhs, L.sign, L.n, L.Y, L.V, L.W,
-                                                      L.G, flag);
+    if (NV == 1) {
+      const size_t sm = sizeof(double) * PS_WARPS * 4 * 32 * PS_LD;
+      const int64_t groups = (P + 31) / 32;
+      int64_t g = (groups + PS_WARPS - 1) / PS_WARPS;
+      if (g > (int64_t)ctx->num_sms * 16) g = (int64_t)ctx->num_sms * 16;
+      cudaFuncSetAttribute(part_solve_scalar_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sm);
+      part_solve_scalar_kernel<<<(int)(g < 1 ? 1 : g), 32 * PS_WARPS, sm, ctx->stream>>>(
+          L.sys, L.rhs, L.sign, L.n, L.Y, L.V, L.W, flag);
+    } else {
+      part_solve_kernel<NV><<<gb, nt, 0, ctx->stream>>>(L.sys, L.rhs, L.sign, L.n, L.Y, L.V, L.W,
+                                                        L.G, flag);
+    }
     ADROM_LAUNCH_CK(ctx);
     assemble_kernel<NV><<<gb, nt, 0, ctx->stream>>>(L.sys, L.rhs, L.sign, L.n, cyclic, L.Y, L.V,
                                                     L.W, nsys, nrhs, nsol, flag);
