@@ -47,6 +47,22 @@ except Exception:  # noqa: BLE001
 HBM_PEAK = float(PEAKS.get("hbm_gbs", 6650.0))
 HBM_PEAK_SRC = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in PEAKS else \
     "fallback 6.65 TB/s (B200_PROFILING.md)"
+# FP64 tensor-core (DMMA m8n8k4) peak measured on this pool with
+# tools/fp64_peak.cu (profiles/r1_fp64_peak.txt); MEASURED_PEAKS.json carries
+# only HBM and bf16, and the whole path computes in fp64.
+FP64_DMMA_PEAK = 37.0
+FP64_DMMA_SRC = "measured FP64 DMMA peak (tools/fp64_peak.cu, profiles/r1_fp64_peak.txt)"
+
+
+def ncu_traffic(kernel: str, workload: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
+    the committed `ncu --set full` capture (profiles/traffic.json), if any."""
+    try:
+        t = json.loads((ROOT / "profiles" / "traffic.json").read_text())
+        e = t.get(workload, {}).get(kernel)
+        return e["bytes"] if e else None
+    except Exception:  # noqa: BLE001
+        return None
 
 
 # --------------------------------------------------------------------------- utils
@@ -415,17 +431,27 @@ def bench_rom(args, rank, world):
     value = world * K / (ms * 1e-3)
     per = {k: (v[0] / max(v[1], 1), v[1]) for k, v in probes.items()}
     share = {k: round(v[0] / ms, 4) for k, v in probes.items()}
-    # dominant kernel by share of the step
-    dom = max(probes, key=lambda k: probes[k][0]) if probes else None
-    bytes_per = {
-        "isvd_rotate": 8.0 * (2 * N * r + N), "isvd_project": 8.0 * (N * r + N),
-        "isvd_resid": 8.0 * (N * r + N), "qdeim_scan": 8.0 * N * r, "decode": 8.0 * (N * r + 3 * N),
-        "encode": 8.0 * (N * r + 3 * N), "fom_residual": 8.0 * 3 * N,
-    }
+    # Roofline of the dominant single kernel: the iSVD rotation
+    # Phi' = [Phi | q_hat] B (rot_tc_kernel, FP64 DMMA; its epilogue also
+    # produces the state transfer and the QDEIM seed bounds).  Algorithmic
+    # work per launch: 2 N r (r+1) flops; bytes 8(2Nr + N) + 8*7N (fused
+    # encode reads d, q~, q_ref; seed writes res2, bnd2 and 1 B of version).
+    # QDEIM is larger in total but is a sequence of rounds of small kernels
+    # (qdeim_rounds_per_step below).
     roof = None
-    if dom in bytes_per:
-        roof = roofline(bytes_per[dom], per[dom][0])
-        roof["kernel"] = dom
+    if "isvd_rotate" in per:
+        rot_ms = per["isvd_rotate"][0]
+        flops = 2.0 * N * r * (r + 1)
+        rbytes = 8.0 * (2 * N * r + N) + 8.0 * 5 * N + 1.0 * N
+        tf = flops / (rot_ms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": round(tf, 2), "peak": FP64_DMMA_PEAK,
+                "unit": "TFLOP/s", "frac": round(tf / FP64_DMMA_PEAK, 4),
+                "traffic": ncu_traffic("rot_tc_kernel<64>", case.name), "peak_source": FP64_DMMA_SRC,
+                "kernel": "isvd_rotate (rot_tc_kernel, FP64 DMMA)",
+                "work_per_launch": {"flops": flops, "bytes": rbytes},
+                "hbm_achieved_gbs": round(rbytes / (rot_ms * 1e-3) / 1e9, 1),
+                "hbm_frac": round(rbytes / (rot_ms * 1e-3) / 1e9 / HBM_PEAK, 4),
+                "share_of_step": round(probes["isvd_rotate"][0] / ms, 4)}
     isvd_keys = ("isvd_project", "isvd_resid", "isvd_core", "isvd_rotate")
     isvd_ms = sum(probes.get(k, (0, 0))[0] for k in isvd_keys) / max(probes.get("isvd_rotate", (0, 1))[1], 1)
     canon = 8.0 * (3 * N * r + 2 * N)
@@ -452,6 +478,7 @@ def bench_rom(args, rank, world):
         "share_of_step": share,
         "setup_s": {"offline": round(t_off, 3), "start": round(t_start, 3)},
         "rom_iterations_mean": float(np.mean(log[:, 1])) if len(log) else None,
+        "qdeim_rounds_per_step": round(probes.get("qdeim_scan", (0, 0))[1] / K, 2),
         "event_errors": sum(1 for e in events if e.error),
     }
     line["clocks"] = clk.summary()
