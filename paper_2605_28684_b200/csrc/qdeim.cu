@@ -590,9 +590,12 @@ __device__ __forceinline__ Cand cand_block_reduce(Cand c, Cand* sc) {
 // Row update of the pool against the accepted direction d (smem): R > 0 uses
 // R/8 lanes per row (8 values per lane, 32/(R/8) rows per warp); R == 0 is
 // the generic warp-per-row path.  Tracks the best updated candidate.
+// Rows whose residual is already <= tau can never be accepted in this round
+// (residuals only decrease): they are left untouched, their stale pres2 stays
+// a valid upper bound for the write-back.
 template <int R>
 __device__ __forceinline__ void qp_pool_update(const GreedyArgs& A, const double* d, int64_t gs,
-                                               bool apply, Cand& best) {
+                                               bool apply, double tau, Cand& best) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t total_warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
@@ -606,7 +609,11 @@ __device__ __forceinline__ void qp_pool_update(const GreedyArgs& A, const double
       const int64_t p = p0 + seg;
       const bool valid = p < A.P;
       const double old = valid ? A.pres2[p] : -1.0;
-      const bool live = old >= 0.0 && p != gs;
+      const bool live = old >= 0.0 && old > tau && p != gs;
+      if (!__any_sync(0xffffffffu, live)) {
+        if (valid && p == gs && apply && sl == 0) A.pres2[p] = -1.0;
+        continue;
+      }
       double2* rv = reinterpret_cast<double2*>(A.Rv + p * R);
       double2 x[4];
       double s = 0.0;
@@ -632,7 +639,10 @@ __device__ __forceinline__ void qp_pool_update(const GreedyArgs& A, const double
         for (int h = 0; h < 4; ++h) rv[sl + LPR * h] = x[h];
       }
       const double nv = live ? (apply ? nr : old) : -1.0;
-      if (sl == 0 && valid && (old >= 0.0) && apply) A.pres2[p] = nv;
+      if (sl == 0 && valid && apply) {
+        if (live) A.pres2[p] = nv;
+        else if (p == gs) A.pres2[p] = -1.0;
+      }
       if (nv >= 0.0) {
         const int64_t row = A.pool_idx[p];
         if (cand_better(nv, row, best.v, best.row)) best = Cand{nv, row, p};
@@ -642,11 +652,11 @@ __device__ __forceinline__ void qp_pool_update(const GreedyArgs& A, const double
     const int r = A.r;
     for (int64_t p = gw; p < A.P; p += total_warps) {
       const double old = A.pres2[p];
-      if (old < 0.0) continue;
       if (p == gs) {
         if (lane == 0 && apply) A.pres2[p] = -1.0;
         continue;
       }
+      if (old < 0.0 || !(old > tau)) continue;
       double nv = old;
       if (apply) {
         double* rv = A.Rv + p * r;
@@ -693,7 +703,7 @@ __global__ void __launch_bounds__(256) qp_greedy_kernel(GreedyArgs A) {
   // initial candidates (no update)
   {
     Cand c{-1.0, LLONG_MAX, -1};
-    qp_pool_update<R>(A, d, -1, false, c);
+    qp_pool_update<R>(A, d, -1, false, tau, c);
     c = cand_block_reduce(c, sc);
     if (tid == 0) {
       A.bv[blockIdx.x] = c.v;
@@ -734,7 +744,7 @@ __global__ void __launch_bounds__(256) qp_greedy_kernel(GreedyArgs A) {
     }
     if (blockIdx.x == (int)(gs % G) && tid == 0) A.pres2[gs] = -1.0;
     Cand c{-1.0, LLONG_MAX, -1};
-    qp_pool_update<R>(A, d, gs, true, c);
+    qp_pool_update<R>(A, d, gs, true, tau, c);
     c = cand_block_reduce(c, sc);
     par ^= 1;
     if (tid == 0) {
