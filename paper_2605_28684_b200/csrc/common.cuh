@@ -94,6 +94,9 @@ struct adrom_ctx {
   cudaEvent_t* prof_ev = nullptr;  // 2 * ADROM_PROF_SLOTS events
   int* prof_id = nullptr;          // probe id per slot
   long long launches = 0;          // kernels launched through this context
+  // a helper context (own stream) that records its probes into the parent's
+  // probe table, e.g. the session's coarse-step stream
+  adrom_ctx* prof_parent = nullptr;
 };
 
 #define ADROM_PROF_SLOTS 8192

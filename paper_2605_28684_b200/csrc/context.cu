@@ -56,16 +56,18 @@ int ensure_pinned(adrom_ctx* ctx, size_t bytes) {
 }
 
 int prof_begin(adrom_ctx* ctx, int id) {
-  if (!ctx->prof || ctx->prof_used >= ADROM_PROF_SLOTS) return -1;
-  const int slot = ctx->prof_used++;
-  ctx->prof_id[slot] = id;
-  cudaEventRecord(ctx->prof_ev[2 * slot], ctx->stream);
+  adrom_ctx* P = ctx->prof_parent ? ctx->prof_parent : ctx;
+  if (!P->prof || P->prof_used >= ADROM_PROF_SLOTS) return -1;
+  const int slot = P->prof_used++;
+  P->prof_id[slot] = id;
+  cudaEventRecord(P->prof_ev[2 * slot], ctx->stream);
   return slot;
 }
 
 void prof_end(adrom_ctx* ctx, int slot) {
   if (slot < 0) return;
-  cudaEventRecord(ctx->prof_ev[2 * slot + 1], ctx->stream);
+  adrom_ctx* P = ctx->prof_parent ? ctx->prof_parent : ctx;
+  cudaEventRecord(P->prof_ev[2 * slot + 1], ctx->stream);
 }
 
 }  // namespace adrom
@@ -94,6 +96,7 @@ int adrom_prof_read(adrom_ctx* ctx, double* host_ms, int32_t* host_count) {
   if (!ctx->prof_ev) return ADROM_OK;
   ADROM_CK(ctx, cudaStreamSynchronize(ctx->stream));
   for (int s = 0; s < ctx->prof_used; ++s) {
+    ADROM_CK(ctx, cudaEventSynchronize(ctx->prof_ev[2 * s + 1]));  // probes of helper streams
     float ms = 0.f;
     ADROM_CK(ctx, cudaEventElapsedTime(&ms, ctx->prof_ev[2 * s], ctx->prof_ev[2 * s + 1]));
     const int id = ctx->prof_id[s];

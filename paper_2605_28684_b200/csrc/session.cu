@@ -14,6 +14,7 @@
 #include "rom_internal.cuh"
 #include "sampling_internal.cuh"
 
+#include <stdio.h>
 #include <string.h>
 
 #include <vector>
@@ -92,6 +93,11 @@ struct adrom_session {
   void* isvd_ws = nullptr;
   void* qd_ws = nullptr;
   double* enc_partial = nullptr;  // fused encode partial sums (rotation epilogue)
+  // coarse-step stream: the advance_signal Newton solve only depends on the
+  // previous coarse state, so it runs concurrently with the reduced step
+  adrom_ctx* fctx = nullptr;
+  cudaStream_t fstream = nullptr;
+  cudaEvent_t main_mark = nullptr, fom_done = nullptr;
   double* step_log = nullptr;    // n_t_online x 3
   int* fail_step = nullptr;
   int64_t n_online = 0;          // steps done
@@ -233,11 +239,20 @@ int run_event(adrom_session* s, adrom_event_record& ev, bool* decoded) {
   ev.error = 0;
   ev.residual_norm = 0.0;
   // advance_signal: coarse backward-Euler step of size z*dt (driver.py:354-358)
+  // on the coarse-step stream, after every main-stream operation that came
+  // before this step's reduced step (main_mark), overlapping that step
   adrom_newton_info ni{};
-  int st = fom_implicit_step(ctx, m, s->y_corr, s->cfg.z * s->cfg.dt, s->cfg.newton_tol,
+  adrom_ctx* fc = s->fctx;
+  ADROM_CK(ctx, cudaStreamWaitEvent(fc->stream, s->main_mark, 0));
+  const long long l0 = fc->launches;
+  int st = fom_implicit_step(fc, m, s->y_corr, s->cfg.z * s->cfg.dt, s->cfg.newton_tol,
                              s->cfg.newton_max_iter, s->y_next, &ni);
-  if (st == ADROM_ERR_CUDA) return st;
+  ctx->launches += fc->launches - l0;
+  ADROM_CK(ctx, cudaEventRecord(s->fom_done, fc->stream));
+  ADROM_CK(ctx, cudaStreamWaitEvent(ctx->stream, s->fom_done, 0));
   if (st) {
+    snprintf(ctx->err, sizeof(ctx->err), "%s", fc->err);
+    if (st == ADROM_ERR_CUDA) return st;
     ev.error = st;
     return ADROM_OK;
   }
@@ -365,9 +380,18 @@ int adrom_session_create(adrom_ctx* ctx, const adrom_session_config* cfg, adrom_
   cudaMemsetAsync(s->fail_step, 0xff, sizeof(int), ctx->stream);  // -1
   size_t need = fom_newton_workspace(cfg->model) + 4096;
   st = ensure_scratch(ctx, need);
+  if (!st && cudaStreamCreateWithFlags(&s->fstream, cudaStreamNonBlocking) != cudaSuccess)
+    st = set_error(ctx, ADROM_ERR_CUDA, "session: stream creation failed");
+  if (!st) st = adrom_ctx_create(&s->fctx, s->fstream);
+  if (!st) {
+    s->fctx->prof_parent = ctx;
+    st = ensure_scratch(s->fctx, need);
+  }
+  if (!st && (cudaEventCreateWithFlags(&s->main_mark, cudaEventDisableTiming) != cudaSuccess ||
+              cudaEventCreateWithFlags(&s->fom_done, cudaEventDisableTiming) != cudaSuccess))
+    st = set_error(ctx, ADROM_ERR_CUDA, "session: event creation failed");
   if (st) {
-    for (void* p : s->allocs) cudaFree(p);
-    delete s;
+    adrom_session_destroy(s);
     return st;
   }
   *out = s;
@@ -377,6 +401,10 @@ int adrom_session_create(adrom_ctx* ctx, const adrom_session_config* cfg, adrom_
 void adrom_session_destroy(adrom_session* s) {
   if (!s) return;
   cudaStreamSynchronize(s->ctx->stream);
+  if (s->fctx) adrom_ctx_destroy(s->fctx);
+  if (s->fstream) cudaStreamDestroy(s->fstream);
+  if (s->main_mark) cudaEventDestroy(s->main_mark);
+  if (s->fom_done) cudaEventDestroy(s->fom_done);
   for (void* p : s->allocs) cudaFree(p);
   delete s;
 }
@@ -439,6 +467,7 @@ int adrom_session_advance(adrom_session* s, int64_t n_steps, int64_t save_every,
   const int64_t N = s->N;
   for (int64_t k = 0; k < n_steps; ++k) {
     const int64_t n = s->cfg.w_init + s->n_online;  // driver loop index
+    ADROM_CK(ctx, cudaEventRecord(s->main_mark, ctx->stream));
     int st = rom_step(s);
     if (st) return st;
     ++s->n_online;
