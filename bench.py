@@ -478,7 +478,7 @@ def bench_rom(args, rank, world):
         "share_of_step": share,
         "setup_s": {"offline": round(t_off, 3), "start": round(t_start, 3)},
         "rom_iterations_mean": float(np.mean(log[:, 1])) if len(log) else None,
-        "qdeim_rounds_per_step": round(probes.get("qdeim_scan", (0, 0))[1] / K, 2),
+        "qdeim_rounds_per_step": round(probes.get("qdeim_round", (0, 0))[1] / K, 2),
         "event_errors": sum(1 for e in events if e.error),
     }
     line["clocks"] = clk.summary()

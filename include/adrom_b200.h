@@ -80,7 +80,7 @@ int64_t adrom_ctx_launch_count(const adrom_ctx* ctx);
 enum adrom_probe {
   ADROM_PROBE_ISVD_ROTATE = 0, ADROM_PROBE_ISVD_PROJECT = 1, ADROM_PROBE_ISVD_RESID = 2,
   ADROM_PROBE_ISVD_CORE = 3, ADROM_PROBE_FOM_RESIDUAL = 4, ADROM_PROBE_FOM_JACOBIAN = 5,
-  ADROM_PROBE_FOM_SOLVE = 6, ADROM_PROBE_QDEIM_SCAN = 7, ADROM_PROBE_ROM_STEP = 8,
+  ADROM_PROBE_FOM_SOLVE = 6, ADROM_PROBE_QDEIM_ROUND = 7, ADROM_PROBE_ROM_STEP = 8,
   ADROM_PROBE_DECODE = 9, ADROM_PROBE_OPERATOR = 10, ADROM_PROBE_ENCODE = 11,
   ADROM_PROBE_COUNT = 16
 };

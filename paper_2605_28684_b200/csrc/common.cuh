@@ -124,7 +124,7 @@ enum ProbeId {
   PROBE_FOM_RESIDUAL = 4,
   PROBE_FOM_JACOBIAN = 5,
   PROBE_FOM_SOLVE = 6,
-  PROBE_QDEIM_SCAN = 7,
+  PROBE_QDEIM_ROUND = 7,
   PROBE_ROM_STEP = 8,
   PROBE_DECODE = 9,
   PROBE_OPERATOR = 10,

@@ -1035,7 +1035,7 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
     long long mref = qp_refresh_factor() * M;  // rows refreshed per round
     while (k < m) {
       ++rounds;
-      const int pr = prof_begin(ctx, PROBE_QDEIM_SCAN);
+      const int pr = prof_begin(ctx, PROBE_QDEIM_ROUND);
       int64_t gg = (P + 255) / 256;
       if (gg > ctx->num_sms * 8) gg = ctx->num_sms * 8;
       if (!fresh && !all) {

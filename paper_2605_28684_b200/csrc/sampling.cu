@@ -1,22 +1,8 @@
-// Hyper-reduction sampling on the device: exact-greedy QDEIM (sampling.py:77-114),
-// feature-guided sampling (sampling.py:117-159), stencil closure + gather plan
-// (sampling.py:178-189, fom.py:119-158) and the reduced-operator assembly
-// with the DEIM pseudo-inverse (sampling.py:162-175, projection.py:61-80).
-//
-// QDEIM = the pivots of a column-pivoted QR of phi^T, i.e. greedy selection of
-// the row with the largest residual norm after projecting out the directions
-// of the rows already chosen (ties -> lowest row, LAPACK idamax).  Done
-// naively that is r passes over the N x r basis.  Here it is a
-// guess-and-verify loop:
-//   * directions D = MGS of the guessed pivot rows, completed to an
-//     orthonormal basis of R^r (one block);
-//   * one pass over the basis computes C_i = D^T phi_i for every row; the
-//     residual of row i after k steps is sum_{l>=k} C_il^2, so the exact
-//     argmax of every step k is found in the same pass (tiled FP64 GEMM with
-//     an argmax epilogue);
-//   * the argmax at step k is exact as soon as guesses 0..k-1 are confirmed,
-//     so every pass confirms at least one more pivot; with the previous
-//     event's pivots as guesses a pass usually confirms all of them.
+// Hyper-reduction sampling on the device: feature-guided sampling
+// (sampling.py:117-159), stencil closure + gather plan (sampling.py:178-189,
+// fom.py:119-158) and the reduced-operator assembly with the DEIM
+// pseudo-inverse (sampling.py:162-175, projection.py:61-80).  The exact
+// greedy QDEIM (sampling.py:77-114) is in qdeim.cu.
 #include "common.cuh"
 #include "jacobi.cuh"
 #include "sampling_internal.cuh"
@@ -24,558 +10,6 @@
 #include <limits.h>
 
 namespace adrom {
-
-// ---------------------------------------------------------------------------
-// directions: D (r x r, row-major, padded stride r+1) from guessed rows
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) qd_dirs_kernel(const double* __restrict__ phi, int r,
-                                                      const int64_t* __restrict__ L, int g,
-                                                      double* __restrict__ Dout,
-                                                      double* __restrict__ tau) {
-  extern __shared__ double sm[];
-  const int S = r + 1;
-  double* Ds = sm;          // r x S: Ds[j*S + k] component j of direction k
-  double* v = Ds + r * S;   // r
-  double* c = v + r;        // r
-  double* red = c + r;      // 32
-  __shared__ int sh_j;
-  const int tid = threadIdx.x;
-  for (int k = 0; k < r; ++k) {
-    if (k < g) {
-      for (int j = tid; j < r; j += blockDim.x) v[j] = phi[L[k] * r + j];
-    } else {
-      // completion: the unit vector with the largest residual
-      double best = -1.0;
-      int bj = 0;
-      for (int j = tid; j < r; j += blockDim.x) {
-        double s = 1.0;
-        for (int l = 0; l < k; ++l) s -= Ds[j * S + l] * Ds[j * S + l];
-        if (s > best) {
-          best = s;
-          bj = j;
-        }
-      }
-      // block argmax (lowest j on ties)
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
-        if (ob > best || (ob == best && oj < bj)) {
-          best = ob;
-          bj = oj;
-        }
-      }
-      __shared__ double wb[32];
-      __shared__ int wj[32];
-      if ((tid & 31) == 0) {
-        wb[tid >> 5] = best;
-        wj[tid >> 5] = bj;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        double b = wb[0];
-        int jj = wj[0];
-        for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
-          if (wb[w] > b || (wb[w] == b && wj[w] < jj)) {
-            b = wb[w];
-            jj = wj[w];
-          }
-        sh_j = jj;
-      }
-      __syncthreads();
-      for (int j = tid; j < r; j += blockDim.x) v[j] = (j == sh_j) ? 1.0 : 0.0;
-    }
-    __syncthreads();
-    // CGS2 against directions 0..k-1
-    for (int pass = 0; pass < 2; ++pass) {
-      for (int l = tid; l < k; l += blockDim.x) {
-        double s = 0.0;
-        for (int j = 0; j < r; ++j) s += v[j] * Ds[j * S + l];
-        c[l] = s;
-      }
-      __syncthreads();
-      for (int j = tid; j < r; j += blockDim.x) {
-        double s = 0.0;
-        for (int l = 0; l < k; ++l) s += c[l] * Ds[j * S + l];
-        v[j] -= s;
-      }
-      __syncthreads();
-    }
-    double a = 0.0;
-    for (int j = tid; j < r; j += blockDim.x) a += v[j] * v[j];
-    a = block_sum_dyn(a, red);
-    const double nrm = sqrt(a);
-    if (tid == 0 && k < g) tau[k] = nrm;
-    for (int j = tid; j < r; j += blockDim.x) Ds[j * S + k] = nrm > 0.0 ? v[j] / nrm : 0.0;
-    __syncthreads();
-  }
-  for (int e = tid; e < r * r; e += blockDim.x) {
-    const int j = e / r, k = e - j * r;
-    Dout[j * r + k] = Ds[j * S + k];
-  }
-}
-
-// per-row exclusion: a row that is guess L[pos] leaves the candidate set after
-// step pos; rows of earlier restarts (ex) are excluded from every step.
-struct Excl {
-  const int64_t* lrow;  // sorted guessed rows (smem)
-  const int* lpos;      // their positions
-  int g;
-  const int64_t* ex;    // sorted excluded rows (global)
-  int n_ex;
-  __device__ __forceinline__ int first_excluded_step(int64_t i) const {
-    // rows of earlier restarts first: a stale guess may name one of them
-    int lo = 0, hi = n_ex - 1;
-    while (lo <= hi) {
-      const int mid = (lo + hi) >> 1;
-      const int64_t v = ex[mid];
-      if (v == i) return 0;
-      if (v < i) lo = mid + 1;
-      else hi = mid - 1;
-    }
-    lo = 0;
-    hi = g - 1;
-    while (lo <= hi) {
-      const int mid = (lo + hi) >> 1;
-      const int64_t v = lrow[mid];
-      if (v == i) return lpos[mid] + 1;
-      if (v < i) lo = mid + 1;
-      else hi = mid - 1;
-    }
-    return INT_MAX;
-  }
-};
-
-__device__ __forceinline__ bool better(double v, int64_t i, double bv, int64_t bi) {
-  return v > bv || (v == bv && i < bi && i >= 0) || (bi < 0 && i >= 0);
-}
-
-__device__ void load_guess_sorted(const int64_t* L, int g, int64_t* lrow, int* lpos) {
-  // insertion rank (g <= 256): lrow sorted ascending with original positions
-  for (int k = threadIdx.x; k < g; k += blockDim.x) {
-    const int64_t x = L[k];
-    int rank = 0;
-    for (int j = 0; j < g; ++j) {
-      const int64_t y = L[j];
-      if (y < x || (y == x && j < k)) ++rank;
-    }
-    lrow[rank] = x;
-    lpos[rank] = k;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// scan, tiled FP64 GEMM C = Phi_tile * D with an argmax epilogue (R in
-// {16, 32, 64, 128}); thread (rg, cg) owns rows rg*RM.. and columns cg+16q
-// ---------------------------------------------------------------------------
-template <int R>
-struct ScanCfg {
-  static constexpr int TM = (R <= 64) ? 128 : 64;
-  static constexpr int RM = TM / 16;
-  static constexpr int RN = R / 16;
-  static constexpr int SA = R + 1;
-};
-
-template <int R>
-__global__ void __launch_bounds__(256) qd_scan_kernel(const double* __restrict__ phi, int64_t n,
-                                                      const double* __restrict__ D, int m_eval,
-                                                      const int64_t* __restrict__ L, int g,
-                                                      const int64_t* __restrict__ ex, int n_ex,
-                                                      double* __restrict__ pv,
-                                                      int64_t* __restrict__ pi) {
-  using C = ScanCfg<R>;
-  extern __shared__ double sm[];
-  double* As = sm;                            // TM x SA
-  double* Bs = As + C::TM * C::SA;            // R x R
-  int64_t* lrow = (int64_t*)(Bs + R * R);     // R
-  int* lpos = (int*)(lrow + R);               // R
-  const int tid = threadIdx.x;
-  for (int e = tid; e < R * R; e += 256) Bs[e] = D[e];
-  load_guess_sorted(L, g, lrow, lpos);
-  const Excl exc{lrow, lpos, g, ex, n_ex};
-  const int rg = tid >> 4, cg = tid & 15;
-  double bv[C::RN];
-  int64_t bi[C::RN];
-#pragma unroll
-  for (int q = 0; q < C::RN; ++q) {
-    bv[q] = -1.0;
-    bi[q] = -1;
-  }
-  const int64_t ntiles = (n + C::TM - 1) / C::TM;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t row0 = t * C::TM;
-    const int rows = (int)((n - row0 < C::TM) ? (n - row0) : C::TM);
-    __syncthreads();
-    const double2* src = reinterpret_cast<const double2*>(phi + row0 * R);
-    const int cnt2 = rows * R / 2;
-    for (int e = tid; e < cnt2; e += 256) {
-      const double2 v = src[e];
-      const int rr = (2 * e) / R, cc = (2 * e) - rr * R;
-      As[rr * C::SA + cc] = v.x;
-      As[rr * C::SA + cc + 1] = v.y;
-    }
-    for (int e = rows * R + tid; e < C::TM * R; e += 256) {
-      const int rr = e / R, cc = e - rr * R;
-      As[rr * C::SA + cc] = 0.0;
-    }
-    __syncthreads();
-    double acc[C::RM][C::RN];
-#pragma unroll
-    for (int m = 0; m < C::RM; ++m)
-#pragma unroll
-      for (int q = 0; q < C::RN; ++q) acc[m][q] = 0.0;
-#pragma unroll 4
-    for (int k = 0; k < R; ++k) {
-      double av[C::RM], bw[C::RN];
-#pragma unroll
-      for (int m = 0; m < C::RM; ++m) av[m] = As[(rg * C::RM + m) * C::SA + k];
-#pragma unroll
-      for (int q = 0; q < C::RN; ++q) bw[q] = Bs[k * R + cg + 16 * q];
-#pragma unroll
-      for (int m = 0; m < C::RM; ++m)
-#pragma unroll
-        for (int q = 0; q < C::RN; ++q) acc[m][q] = fma(av[m], bw[q], acc[m][q]);
-    }
-    // epilogue: residual after step l = sum_{c >= l} C_c^2, column c = cg + 16 q
-#pragma unroll
-    for (int m = 0; m < C::RM; ++m) {
-      const int64_t i = row0 + rg * C::RM + m;
-      double incl[C::RN], tot[C::RN];
-#pragma unroll
-      for (int q = 0; q < C::RN; ++q) {
-        double x = acc[m][q] * acc[m][q];
-        // inclusive suffix over cg' >= cg within the 16-lane row group
-#pragma unroll
-        for (int o = 1; o < 16; o <<= 1) {
-          const double y = __shfl_down_sync(0xffffffffu, x, o, 16);
-          if (cg + o < 16) x += y;
-        }
-        incl[q] = x;
-        tot[q] = __shfl_sync(0xffffffffu, x, 0, 16);
-      }
-      if (i < n) {
-        const int fx = exc.first_excluded_step(i);
-        double later = 0.0;
-#pragma unroll
-        for (int q = C::RN - 1; q >= 0; --q) {
-          const int l = cg + 16 * q;
-          const double s = incl[q] + later;
-          if (l < m_eval && l < fx && better(s, i, bv[q], bi[q])) {
-            bv[q] = s;
-            bi[q] = i;
-          }
-          later += tot[q];
-        }
-      }
-    }
-  }
-  // block reduction over the 16 row groups: reuse As as scratch
-  __syncthreads();
-  double* rv = As;                       // 16 x R
-  int64_t* ri = (int64_t*)(As + 16 * R); // 16 x R
-#pragma unroll
-  for (int q = 0; q < C::RN; ++q) {
-    rv[rg * R + cg + 16 * q] = bv[q];
-    ri[rg * R + cg + 16 * q] = bi[q];
-  }
-  __syncthreads();
-  for (int l = tid; l < m_eval; l += 256) {
-    double b = -1.0;
-    int64_t bidx = -1;
-    for (int w = 0; w < 16; ++w)
-      if (better(rv[w * R + l], ri[w * R + l], b, bidx)) {
-        b = rv[w * R + l];
-        bidx = ri[w * R + l];
-      }
-    pv[(size_t)blockIdx.x * R + l] = b;
-    pi[(size_t)blockIdx.x * R + l] = bidx;
-  }
-}
-
-// generic r (<= 64): thread per row, local arrays
-__global__ void __launch_bounds__(128) qd_scan_generic_kernel(
-    const double* __restrict__ phi, int64_t n, int r, const double* __restrict__ D, int m_eval,
-    const int64_t* __restrict__ L, int g, const int64_t* __restrict__ ex, int n_ex,
-    double* __restrict__ pv, int64_t* __restrict__ pi) {
-  extern __shared__ double sm[];
-  double* Ds = sm;                           // r x r
-  int64_t* lrow = (int64_t*)(Ds + r * r);    // r
-  int* lpos = (int*)(lrow + r);              // r
-  const int tid = threadIdx.x;
-  for (int e = tid; e < r * r; e += blockDim.x) Ds[e] = D[e];
-  load_guess_sorted(L, g, lrow, lpos);
-  __syncthreads();
-  const Excl exc{lrow, lpos, g, ex, n_ex};
-  double bv[64];
-  int64_t bi[64];
-  for (int l = 0; l < m_eval; ++l) {
-    bv[l] = -1.0;
-    bi[l] = -1;
-  }
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + tid; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    double row[64], cc[64];
-    for (int j = 0; j < r; ++j) row[j] = phi[i * r + j];
-    for (int l = 0; l < r; ++l) {
-      double s = 0.0;
-      for (int j = 0; j < r; ++j) s = fma(row[j], Ds[j * r + l], s);
-      cc[l] = s;
-    }
-    const int fx = exc.first_excluded_step(i);
-    double suf = 0.0;
-    for (int l = r - 1; l >= 0; --l) {
-      suf += cc[l] * cc[l];
-      if (l < m_eval && l < fx && better(suf, i, bv[l], bi[l])) {
-        bv[l] = suf;
-        bi[l] = i;
-      }
-    }
-  }
-  // block reduce per step through shared memory (128 threads, one step at a time)
-  __shared__ double wv[128];
-  __shared__ int64_t wi[128];
-  for (int l = 0; l < m_eval; ++l) {
-    __syncthreads();
-    wv[tid] = bv[l];
-    wi[tid] = bi[l];
-    __syncthreads();
-    if (tid == 0) {
-      double b = -1.0;
-      int64_t bidx = -1;
-      for (int w = 0; w < (int)blockDim.x; ++w)
-        if (better(wv[w], wi[w], b, bidx)) {
-          b = wv[w];
-          bidx = wi[w];
-        }
-      pv[(size_t)blockIdx.x * r + l] = b;
-      pi[(size_t)blockIdx.x * r + l] = bidx;
-    }
-  }
-}
-
-// best per step across blocks (one block per step)
-__global__ void qd_reduce_kernel(const double* __restrict__ pv, const int64_t* __restrict__ pi,
-                                 int nb, int ld, double* __restrict__ bestv,
-                                 int64_t* __restrict__ besti) {
-  const int l = blockIdx.x;
-  double b = -1.0;
-  int64_t bidx = -1;
-  for (int k = threadIdx.x; k < nb; k += blockDim.x) {
-    const double v = pv[(size_t)k * ld + l];
-    const int64_t i = pi[(size_t)k * ld + l];
-    if (better(v, i, b, bidx)) {
-      b = v;
-      bidx = i;
-    }
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ov = __shfl_xor_sync(0xffffffffu, b, o);
-    const int64_t oi = __shfl_xor_sync(0xffffffffu, bidx, o);
-    if (better(ov, oi, b, bidx)) {
-      b = ov;
-      bidx = oi;
-    }
-  }
-  __shared__ double wv[32];
-  __shared__ int64_t wi[32];
-  if ((threadIdx.x & 31) == 0) {
-    wv[threadIdx.x >> 5] = b;
-    wi[threadIdx.x >> 5] = bidx;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
-      if (better(wv[w], wi[w], b, bidx)) {
-        b = wv[w];
-        bidx = wi[w];
-      }
-    bestv[l] = b;
-    besti[l] = bidx;
-  }
-}
-
-// status[0] = done, [1] = new g, [2] = error (1 + pivot step) or 0,
-// [3] = step of the error, [4..5] = error residual (double bits)
-__global__ void qd_check_kernel(int64_t* __restrict__ L, int g, int m, int m_eval,
-                                const double* __restrict__ bestv,
-                                const int64_t* __restrict__ besti, int* __restrict__ status,
-                                double* __restrict__ err_resid) {
-  int kstar = -1;
-  const int lim = g < m_eval ? g : m_eval;
-  for (int k = 0; k < lim; ++k)
-    if (besti[k] != L[k]) {
-      kstar = k;
-      break;
-    }
-  int newg, done = 0, confirmed;
-  if (kstar >= 0) {
-    // keep the remaining old guesses (the pivot SET usually survives a basis
-    // update, only its order changes): L[0..k*) + [exact pivot] + old
-    // guesses after k* without the exact pivot
-    const int64_t piv = besti[kstar];
-    int w = kstar + 1;
-    int64_t carry = L[kstar];
-    for (int j = kstar + 1; j <= g && w < m; ++j) {
-      const int64_t nxt = (j < g) ? L[j] : -1;
-      if (carry != piv && carry >= 0) L[w++] = carry;
-      carry = nxt;
-    }
-    L[kstar] = piv;
-    newg = w;
-    confirmed = kstar + 1;
-  } else if (g < m) {
-    L[g] = besti[g];
-    newg = g + 1;
-    confirmed = newg;
-    done = (newg == m);
-  } else {
-    newg = g;
-    confirmed = g;
-    done = 1;
-  }
-  int err = 0;
-  for (int k = 0; k < confirmed && k < m_eval; ++k) {
-    if (besti[k] < 0 || !(sqrt(bestv[k]) >= 1e-14)) {  // sampling.py:97-101
-      err = k + 1;
-      *err_resid = besti[k] < 0 ? 0.0 : sqrt(bestv[k]);
-      break;
-    }
-  }
-  status[0] = done;
-  status[1] = newg;
-  status[2] = err;
-}
-
-// sort rows[0..n) ascending (single thread; n <= a few thousand)
-__global__ void sort_rows_kernel(const int64_t* __restrict__ in, int n, int64_t* __restrict__ out) {
-  for (int i = 0; i < n; ++i) {
-    const int64_t x = in[i];
-    int j = i - 1;
-    while (j >= 0 && out[j] > x) {
-      out[j + 1] = out[j];
-      --j;
-    }
-    out[j + 1] = x;
-  }
-}
-
-size_t qdeim_workspace_bytes(adrom_ctx* ctx, int r, int count) {
-  const int nb = partial_rows(ctx);
-  size_t b = 0;
-  b += align_up(sizeof(double) * r * r);             // D
-  b += align_up(sizeof(double) * r);                 // tau
-  b += align_up(sizeof(double) * (size_t)nb * r);    // pv
-  b += align_up(sizeof(int64_t) * (size_t)nb * r);   // pi
-  b += align_up(sizeof(double) * r);                 // bestv
-  b += align_up(sizeof(int64_t) * r);                // besti
-  b += align_up(sizeof(int) * 8) + align_up(sizeof(double) * 2);
-  b += align_up(sizeof(int64_t) * (size_t)(count + 1));  // sorted exclusions
-  b += align_up(sizeof(int64_t) * (size_t)r);            // local guess list
-  return b;
-}
-
-int qdeim_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int count, int64_t* out_idx,
-                 QdeimGuess* guess, void* ws, int* iterations_out) {
-  if (count > n) return set_error(ctx, ADROM_ERR_DENSE, "cannot select %d pivots from %lld columns",
-                                  count, (long long)n);
-  if (r < 1 || r > 128) return set_error(ctx, ADROM_ERR_ARG, "qdeim: rank %d unsupported", r);
-  const int nb = partial_rows(ctx);
-  char* w = (char*)ws;
-  auto take = [&](size_t bytes) {
-    void* p = w;
-    w += align_up(bytes);
-    return p;
-  };
-  double* D = (double*)take(sizeof(double) * r * r);
-  double* tau = (double*)take(sizeof(double) * r);
-  double* pv = (double*)take(sizeof(double) * (size_t)nb * r);
-  int64_t* pi = (int64_t*)take(sizeof(int64_t) * (size_t)nb * r);
-  double* bestv = (double*)take(sizeof(double) * r);
-  int64_t* besti = (int64_t*)take(sizeof(int64_t) * r);
-  int* status = (int*)take(sizeof(int) * 8);
-  double* err_resid = (double*)take(sizeof(double) * 2);
-  int64_t* ex = (int64_t*)take(sizeof(int64_t) * (size_t)(count + 1));
-  int64_t* Lloc = (int64_t*)take(sizeof(int64_t) * (size_t)r);
-  const bool fast = (r == 16 || r == 32 || r == 64 || r == 128);
-  if (!fast && r > 64) return set_error(ctx, ADROM_ERR_ARG, "qdeim: rank %d unsupported", r);
-  int* hstat = (int*)ctx->pinned;
-  double* hres = (double*)((char*)ctx->pinned + 64);
-  int chosen = 0, chunk = 0, iters = 0;
-  const size_t dsm = sizeof(double) * ((size_t)r * (r + 1) + 2 * r + 32);
-  cudaFuncSetAttribute(qd_dirs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
-  while (chosen < count) {
-    const int m = (count - chosen < r) ? (count - chosen) : r;
-    int64_t* L = (guess && chunk < guess->max_chunks) ? guess->rows + (size_t)chunk * guess->r : Lloc;
-    int g = (guess && chunk < guess->max_chunks) ? guess->g[chunk] : 0;
-    if (g > m) g = m;
-    const int n_ex = chosen;
-    if (n_ex > 0) {
-      sort_rows_kernel<<<1, 1, 0, ctx->stream>>>(out_idx, n_ex, ex);
-      ADROM_LAUNCH_CK(ctx);
-    }
-    bool done = false;
-    for (int pass = 0; pass < m + 8 && !done; ++pass) {
-      ++iters;
-      qd_dirs_kernel<<<1, 256, dsm, ctx->stream>>>(phi, r, L, g, D, tau);
-      ADROM_LAUNCH_CK(ctx);
-      const int m_eval = (g + 1 < m) ? g + 1 : m;
-      const int pr = prof_begin(ctx, PROBE_QDEIM_SCAN);
-      int grid;
-      if (fast) {
-        auto launch = [&](auto kern, int TM, int R) -> int {
-          const size_t sm = sizeof(double) * ((size_t)TM * (R + 1) + (size_t)R * R) +
-                            (sizeof(int64_t) + sizeof(int)) * R + 64;
-          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-          int64_t gg = (int64_t)ctx->num_sms * 2;
-          const int64_t nt = (n + TM - 1) / TM;
-          if (gg > nt) gg = nt;
-          if (gg > nb) gg = nb;
-          grid = (int)(gg < 1 ? 1 : gg);
-          kern<<<grid, 256, sm, ctx->stream>>>(phi, n, D, m_eval, L, g, ex, n_ex, pv, pi);
-          ADROM_LAUNCH_CK(ctx);
-          return ADROM_OK;
-        };
-        int st2;
-        if (r == 16) st2 = launch(qd_scan_kernel<16>, ScanCfg<16>::TM, 16);
-        else if (r == 32) st2 = launch(qd_scan_kernel<32>, ScanCfg<32>::TM, 32);
-        else if (r == 64) st2 = launch(qd_scan_kernel<64>, ScanCfg<64>::TM, 64);
-        else st2 = launch(qd_scan_kernel<128>, ScanCfg<128>::TM, 128);
-        if (st2) return st2;
-      } else {
-        int64_t gg = (n + 127) / 128;
-        if (gg > nb) gg = nb;
-        grid = (int)(gg < 1 ? 1 : gg);
-        const size_t sm = sizeof(double) * r * r + (sizeof(int64_t) + sizeof(int)) * r + 64;
-        qd_scan_generic_kernel<<<grid, 128, sm, ctx->stream>>>(phi, n, r, D, m_eval, L, g, ex, n_ex,
-                                                               pv, pi);
-        ADROM_LAUNCH_CK(ctx);
-      }
-      prof_end(ctx, pr);
-      qd_reduce_kernel<<<m_eval, 256, 0, ctx->stream>>>(pv, pi, grid, r, bestv, besti);
-      ADROM_LAUNCH_CK(ctx);
-      qd_check_kernel<<<1, 1, 0, ctx->stream>>>(L, g, m, m_eval, bestv, besti, status, err_resid);
-      ADROM_LAUNCH_CK(ctx);
-      ADROM_CK(ctx, cudaMemcpyAsync(hstat, status, sizeof(int) * 4, cudaMemcpyDeviceToHost,
-                                    ctx->stream));
-      ADROM_CK(ctx, cudaMemcpyAsync(hres, err_resid, sizeof(double), cudaMemcpyDeviceToHost,
-                                    ctx->stream));
-      ADROM_CK(ctx, cudaStreamSynchronize(ctx->stream));
-      if (hstat[2])
-        return set_error(ctx, ADROM_ERR_SINGULAR,
-                         "rank deficiency at pivot step %d (residual column norm %.3e)",
-                         chosen + hstat[2] - 1, hres[0]);
-      g = hstat[1];
-      done = hstat[0] != 0;
-    }
-    if (!done) return set_error(ctx, ADROM_ERR_DENSE, "qdeim: verification did not settle");
-    ADROM_CK(ctx, cudaMemcpyAsync(out_idx + chosen, L, sizeof(int64_t) * m,
-                                  cudaMemcpyDeviceToDevice, ctx->stream));
-    if (guess && chunk < guess->max_chunks) guess->g[chunk] = m;
-    chosen += m;
-    ++chunk;
-  }
-  if (iterations_out) *iterations_out = iters;
-  return ADROM_OK;
-}
 
 // ---------------------------------------------------------------------------
 // feature-guided sampling (sampling.py:117-159)

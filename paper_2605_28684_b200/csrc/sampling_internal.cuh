@@ -6,15 +6,6 @@
 
 namespace adrom {
 
-// Persistent pivot guesses (one chunk of <= r pivots per QDEIM restart).
-struct QdeimGuess {
-  int64_t* rows = nullptr;  // device, max_chunks * r
-  int g[64] = {0};          // confirmed/guessed length per chunk (host mirror)
-  int max_chunks = 0;
-  int r = 0;
-};
-
-size_t qdeim_workspace_bytes(adrom_ctx* ctx, int r, int count);
 // Exact greedy via a certified candidate pool (qdeim.cu): the path used by
 // the session and the C-ABI.  Blocking (one sync per pass).
 size_t qdeim_pool_workspace_bytes(int64_t n, int r, int count);
@@ -23,12 +14,6 @@ size_t qdeim_pool_workspace_bytes(int64_t n, int r, int count);
 int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int count,
                       int64_t* out_idx, void* ws, int* passes_out, bool seeded = false);
 void qdeim_seed_buffers(void* ws, int64_t n, double** res2, double** bnd2, unsigned char** ver);
-// First `count` pivots of the restarted column-pivoted QR of phi^T
-// (sampling.py:77-104), exact greedy, ties to the lowest row.  Blocking
-// (synchronises once per verification pass).  `guess` may be null.
-int qdeim_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int count, int64_t* out_idx,
-                 QdeimGuess* guess, void* ws, int* iterations_out);
-
 // FGS (sampling.py:117-159): idx[0..n_base) must already hold the QDEIM
 // rows; appends n_extra rows ranked by |grad feature(y_corr)|.
 int fgs_extend(adrom_ctx* ctx, const adrom_model& m, const double* y_corr, int feature_kind,

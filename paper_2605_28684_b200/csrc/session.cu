@@ -86,7 +86,6 @@ struct adrom_session {
   double *a = nullptr;
   adrom_rom_op op[2]{};
   int opcur = 0;
-  QdeimGuess guess;
   double* rom_work = nullptr;
   double* rom_info = nullptr;
   double* isvd_stats = nullptr;
@@ -364,10 +363,6 @@ int adrom_session_create(adrom_ctx* ctx, const adrom_session_config* cfg, adrom_
   cudaMalloc(&s->qd_ws, qdeim_pool_workspace_bytes(N, r, cfg->n_s));
   s->allocs.push_back(s->qd_ws);
   s->enc_partial = s->alloc_d(rot_fuse_partial_doubles(ctx, r));
-  s->guess.r = r;
-  s->guess.max_chunks = (cfg->n_s + r - 1) / r;
-  if (s->guess.max_chunks > 64) s->guess.max_chunks = 64;
-  s->guess.rows = s->alloc_t<int64_t>((size_t)s->guess.max_chunks * r);
   s->cap_steps = cfg->n_t > cfg->w_init ? cfg->n_t - cfg->w_init : 1;
   s->step_log = s->alloc_d((size_t)s->cap_steps * 3);
   s->fail_step = s->alloc_t<int>(1);
@@ -432,7 +427,6 @@ int adrom_session_load(adrom_session* s, const double* q_ref, const double* d, c
   s->opcur = 0;
   s->n_online = 0;
   s->events.clear();
-  memset(s->guess.g, 0, sizeof(s->guess.g));
   ADROM_CK(ctx, cudaMemsetAsync(s->fail_step, 0xff, sizeof(int), ctx->stream));
   return ADROM_OK;
 }

@@ -19,7 +19,7 @@ ctx.prof_enable(True)
 for k in range(6):
     sess.advance(1)
     p = ctx.prof_read()
-    q = p.get("qdeim_scan", (0, 0))
+    q = p.get("qdeim_round", (0, 0))
     print("step", k, "qdeim passes", q[1], "qdeim ms %.2f" % q[0], "rom", p.get("rom_step"))
 log, ev, *_ = sess.read(6, 6)
 print("rom log [conv, it, res]:", log.tolist())
