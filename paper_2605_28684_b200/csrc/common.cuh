@@ -70,6 +70,25 @@ __device__ __forceinline__ double block_sum_dyn(double v, double* sh) {
   return t;
 }
 
+// Block max (values >= 0 or NaN-free); result valid in all threads.
+__device__ __forceinline__ double block_max_dyn(double v, double* sh) {
+  v = warp_max(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double t = -INFINITY;
+  if (threadIdx.x < 32) {
+    t = (lane < nw) ? sh[lane] : -INFINITY;
+    t = warp_max(t);
+    if (lane == 0) sh[0] = t;
+  }
+  __syncthreads();
+  t = sh[0];
+  __syncthreads();
+  return t;
+}
+
 }  // namespace adrom
 
 // ---------------------------------------------------------------------------

@@ -32,10 +32,11 @@ __device__ __forceinline__ double hw_sum(double v) {
 __device__ inline JacobiResult block_jacobi(double* A, int lda, int m, int n, double* V, int ldv,
                                             int max_sweeps, double tol, int* sh_flag) {
   const int tid = threadIdx.x, hl = tid & 15, hw = tid >> 4, nhw = blockDim.x >> 4;
-  for (int e = tid; e < n * n; e += blockDim.x) {
-    const int c = e / n, rr = e - c * n;
-    V[c * ldv + rr] = (c == rr) ? 1.0 : 0.0;
-  }
+  if (V)  // V == nullptr: right rotations not accumulated
+    for (int e = tid; e < n * n; e += blockDim.x) {
+      const int c = e / n, rr = e - c * n;
+      V[c * ldv + rr] = (c == rr) ? 1.0 : 0.0;
+    }
   __syncthreads();
   const int ne = n + (n & 1);  // pad to even: index n (if odd) is a virtual zero column
   JacobiResult res{0, 0};
@@ -90,12 +91,14 @@ __device__ inline JacobiResult block_jacobi(double* A, int lda, int m, int n, do
           ca[i] = c * x - s * y;
           cb[i] = s * x + c * y;
         }
-        double* va = V + (size_t)a * ldv;
-        double* vb = V + (size_t)b * ldv;
-        for (int i = hl; i < n; i += 16) {
-          const double x = va[i], y = vb[i];
-          va[i] = c * x - s * y;
-          vb[i] = s * x + c * y;
+        if (V) {
+          double* va = V + (size_t)a * ldv;
+          double* vb = V + (size_t)b * ldv;
+          for (int i = hl; i < n; i += 16) {
+            const double x = va[i], y = vb[i];
+            va[i] = c * x - s * y;
+            vb[i] = s * x + c * y;
+          }
         }
         if (hl == 0) *sh_flag = 1;
       }

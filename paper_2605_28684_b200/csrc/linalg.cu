@@ -1041,19 +1041,27 @@ __global__ void __launch_bounds__(1024) isvd_core_kernel(
   const double qnorm = sh_q[0], ynorm = sh_q[1];
   // tracking.py:169 — degenerate residual keeps the subspace
   const bool degenerate = qnorm <= 1e-12 * fmax(ynorm, 1e-300);
-  for (int e = tid; e < n * ld; e += blockDim.x) A[e] = 0.0;
-  __syncthreads();
+  // Fast path: one-sided Jacobi on K's own columns (A = K column-major):
+  // K V = U S, so U (all the rotation needs) is read off the converged
+  // columns and V is never formed — half the work of the K^T form.  The
+  // result is verified (kept singular values > 0, max |U^T U - I| <= 1e-13);
+  // otherwise (rank-deficient K: a column at rounding level never converges
+  // in the relative sense) the K^T form with accumulated rotations runs.
+  auto fill_k = [&](bool transposed) {
+    for (int e = tid; e < n * ld; e += blockDim.x) A[e] = 0.0;
+    __syncthreads();
+    for (int j = tid; j < r_cur; j += blockDim.x) {
+      A[j * ld + j] = lam * sigma[j];                      // K[j][j] (tracking.py:167)
+      if (transposed) A[j * ld + r_cur] = p[j];            // A = K^T
+      else A[r_cur * ld + j] = p[j];                       // K[j][r] (tracking.py:168)
+    }
+    if (tid == 0) A[r_cur * ld + r_cur] = degenerate ? 0.0 : qnorm;  // tracking.py:172
+    __syncthreads();
+  };
   bool bad = false;
-  for (int j = tid; j < r_cur; j += blockDim.x) {
-    const double dj = lam * sigma[j];
-    A[j * ld + j] = dj;       // K[j][j]   (tracking.py:167)
-    A[j * ld + r_cur] = p[j]; // K[j][r]   (tracking.py:168)
-    bad |= !isfinite(dj) || !isfinite(p[j]);
-  }
-  if (tid == 0) {
-    A[r_cur * ld + r_cur] = degenerate ? 0.0 : qnorm;  // tracking.py:172
-    bad |= !isfinite(qnorm) || !isfinite(ynorm);
-  }
+  for (int j = tid; j < r_cur; j += blockDim.x)
+    bad |= !isfinite(lam * sigma[j]) || !isfinite(p[j]);
+  if (tid == 0) bad |= !isfinite(qnorm) || !isfinite(ynorm);
   __shared__ int sh_bad;
   if (tid == 0) sh_bad = 0;
   __syncthreads();
@@ -1067,10 +1075,35 @@ __global__ void __launch_bounds__(1024) isvd_core_kernel(
     if (tid == 0) *qinv_out = 0.0;
     return;
   }
-  const JacobiResult jr = block_jacobi(A, ld, n, n, V, ld, 60, 1e-15, &sh_flag);
+  fill_k(false);
+  JacobiResult jr = block_jacobi(A, ld, n, n, nullptr, ld, 30, 1e-15, &sh_flag);
   column_norms_sorted(A, ld, n, n, s, order);
-  // rotation factors B[k][c] = U[k][order[c]] (k = r_cur is u_bot), left
-  // singular vectors of K = accumulated rotations of the one-sided Jacobi on K^T
+  // U column j = A column j / s_j, stored as V[j][k] = U[k][j]
+  for (int e = tid; e < n * n; e += blockDim.x) {
+    const int j = e / n, k = e - j * n;
+    V[j * ld + k] = (s[j] > 0.0) ? A[j * ld + k] / s[j] : 0.0;
+  }
+  __syncthreads();
+  double defect = 0.0;
+  for (int e = tid; e < r * r; e += blockDim.x) {
+    const int a = e / r, b = e - a * r;
+    const double* ua = V + (size_t)order[a] * ld;
+    const double* ub = V + (size_t)order[b] * ld;
+    double dot = 0.0;
+    for (int k = 0; k < n; ++k) dot += ua[k] * ub[k];
+    defect = fmax(defect, fabs(dot - (a == b ? 1.0 : 0.0)));
+  }
+  defect = block_max_dyn(defect, red);
+  __shared__ int sh_fallback;
+  if (tid == 0) sh_fallback = (!jr.converged || !(defect <= 1e-13) || !(s[order[r - 1]] > 0.0)) ? 1 : 0;
+  __syncthreads();
+  if (sh_fallback) {
+    // one-sided Jacobi on K^T with accumulated rotations: U of K = V
+    fill_k(true);
+    jr = block_jacobi(A, ld, n, n, V, ld, 60, 1e-15, &sh_flag);
+    column_norms_sorted(A, ld, n, n, s, order);
+  }
+  // rotation factors B[k][c] = U[k][order[c]] (k = r_cur is u_bot)
   const double inv = degenerate ? 0.0 : 1.0 / qnorm;
   for (int e = tid; e < n * r; e += blockDim.x) {
     const int k = e / r, c = e - k * r;
