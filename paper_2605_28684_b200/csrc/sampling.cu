@@ -282,8 +282,139 @@ __global__ void op_gather_kernel(DevOp op, const double* __restrict__ phi,
   }
 }
 
-__global__ void __launch_bounds__(1024) deim_pinv_kernel(DevOp op, int n_s, int* flag) {
+// ---------------------------------------------------------------------------
+// DEIM pseudo-inverse, fast path: Householder QR of phi_s (n_s x r) with a
+// certified condition bound ||R||_F ||R^-1||_F <= 1e10.  Then phi_s has full
+// column rank with s_min > 1e-10 s_max, the reference's test
+// (s_min <= 1e-12 s_max, sampling.py:171-174) cannot fire, and
+// pinv = R^{-1} Q_1^T equals the SVD pseudo-inverse.  Otherwise *need_svd = 1
+// and deim_pinv_kernel (Jacobi SVD, the reference's formulation) runs.
+// ---------------------------------------------------------------------------
+constexpr double PINV_CERT = 1e10;
+
+__global__ void __launch_bounds__(512) deim_pinv_qr_kernel(DevOp op, int n_s,
+                                                           int* __restrict__ need_svd) {
   extern __shared__ double sm[];
+  const int r = op.r, m = n_s;
+  const int ld = m | 1, ldr = r | 1;
+  double* A = sm;                      // r columns of length m (Householder vectors below R)
+  double* M = A + (size_t)r * ld;      // r columns of length m: pinv^T accumulator
+  double* Ri = M + (size_t)r * ld;     // R^{-1}, column c at Ri[c * ldr]
+  double* Rd = Ri + (size_t)r * ldr;   // diag(R)
+  double* beta = Rd + r;               // r
+  double* red = beta + r;              // 32
+  __shared__ int sh_bad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  for (int e = tid; e < m * r; e += blockDim.x) {
+    const int j = e / r, c = e - j * r;
+    A[c * ld + j] = op.phi_s[e];
+  }
+  if (tid == 0) sh_bad = 0;
+  __syncthreads();
+  for (int k = 0; k < r; ++k) {
+    double* col = A + (size_t)k * ld;
+    double a = 0.0;
+    for (int i = k + tid; i < m; i += blockDim.x) a += col[i] * col[i];
+    a = block_sum_dyn(a, red);
+    if (tid == 0) {
+      const double x0 = col[k], nrm = sqrt(a);
+      const double alpha = (x0 >= 0.0) ? -nrm : nrm;
+      const double vtv_half = a - x0 * alpha;
+      beta[k] = (vtv_half > 0.0) ? 1.0 / vtv_half : 0.0;
+      Rd[k] = alpha;
+      col[k] = x0 - alpha;  // v_k (v_i = col[i] below)
+    }
+    __syncthreads();
+    const double bk = beta[k];
+    for (int j = k + 1 + warp; j < r; j += nw) {
+      double* cj = A + (size_t)j * ld;
+      double sdot = 0.0;
+      for (int i = k + lane; i < m; i += 32) sdot += col[i] * cj[i];
+      sdot = warp_sum(sdot) * bk;
+      for (int i = k + lane; i < m; i += 32) cj[i] -= sdot * col[i];
+    }
+    __syncthreads();
+  }
+  // R^{-1} (column c: R x = e_c, column-oriented substitution, warp per column)
+  double rf = 0.0;
+  for (int e = tid; e < r * r; e += blockDim.x) {
+    const int l = e / r, k = e - l * r;  // R[k][l], k <= l
+    if (k < l) rf += A[(size_t)l * ld + k] * A[(size_t)l * ld + k];
+    else if (k == l) rf += Rd[k] * Rd[k];
+  }
+  rf = block_sum_dyn(rf, red);
+  double inv2 = 0.0;
+  bool bad = false;
+  for (int c = warp; c < r; c += nw) {
+    double b[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) b[t] = (lane + 32 * t == c) ? 1.0 : 0.0;
+    for (int i = c; i >= 0; --i) {
+      const int ti = i >> 5, li = i & 31;
+      double bi = 0.0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (t == ti) bi = b[t];
+      bi = __shfl_sync(0xffffffffu, bi, li);
+      const double d = Rd[i];
+      double xi = 0.0;
+      if (d == 0.0 || !isfinite(d)) bad = true;
+      else xi = bi / d;
+      if (lane == 0) {
+        Ri[(size_t)c * ldr + i] = xi;
+        inv2 += xi * xi;
+      }
+      const double* coli = A + (size_t)i * ld;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int j = lane + 32 * t;
+        if (j < i) b[t] -= coli[j] * xi;
+      }
+    }
+    for (int i = c + 1 + lane; i < r; i += 32) Ri[(size_t)c * ldr + i] = 0.0;
+  }
+  inv2 = block_sum_dyn(inv2, red);
+  if (bad) sh_bad = 1;
+  __syncthreads();
+  const bool cert = !sh_bad && isfinite(rf) && isfinite(inv2) && sqrt(rf) * sqrt(inv2) <= PINV_CERT;
+  if (!cert) {
+    if (tid == 0) *need_svd = 1;
+    return;
+  }
+  if (tid == 0) *need_svd = 0;
+  // M = [R^{-T}; 0]: column c of M is row c of R^{-1}
+  for (int e = tid; e < r * m; e += blockDim.x) {
+    const int c = e / m, i = e - c * m;
+    M[(size_t)c * ld + i] = (i < r) ? Ri[(size_t)i * ldr + c] : 0.0;
+  }
+  __syncthreads();
+  // pinv^T = H_0 ... H_{r-1} M
+  for (int k = r - 1; k >= 0; --k) {
+    const double* v = A + (size_t)k * ld;
+    const double bk = beta[k];
+    for (int c = warp; c < r; c += nw) {
+      double* mc = M + (size_t)c * ld;
+      double sdot = 0.0;
+      for (int i = k + lane; i < m; i += 32) sdot += v[i] * mc[i];
+      sdot = warp_sum(sdot) * bk;
+      for (int i = k + lane; i < m; i += 32) mc[i] -= sdot * v[i];
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < r * m; e += blockDim.x) {
+    const int c = e / m, j = e - c * m;
+    op.pinv[e] = M[(size_t)c * ld + j];  // pinv[c][j] = (pinv^T)[j][c]
+  }
+}
+
+static size_t pinv_qr_smem(int n_s, int r) {
+  return sizeof(double) * (2 * (size_t)r * (n_s | 1) + (size_t)r * (r | 1) + 2 * r + 32) + 64;
+}
+
+__global__ void __launch_bounds__(1024) deim_pinv_kernel(DevOp op, int n_s, int* flag,
+                                                         const int* need) {
+  extern __shared__ double sm[];
+  if (need && *need == 0) return;  // the certified QR path produced pinv
   const int r = op.r;
   const int ld = n_s | 1, ldv = r | 1;
   double* A = sm;                        // r columns of length n_s
@@ -315,6 +446,27 @@ __global__ void __launch_bounds__(1024) deim_pinv_kernel(DevOp op, int n_s, int*
   }
 }
 
+// certified QR fast path, Jacobi SVD when it cannot certify (device-side choice)
+static int deim_pinv_launch(adrom_ctx* ctx, DevOp& op, int n_s, int* flag) {
+  const int r = op.r;
+  const size_t sm = sizeof(double) * ((size_t)r * (n_s | 1) + (size_t)r * (r | 1) + r) +
+                    sizeof(int) * r + 64;
+  if (sm > 220 * 1024)
+    return set_error(ctx, ADROM_ERR_ARG, "deim pinv: %d x %d exceeds one block", n_s, r);
+  int* need = ctx->dflags + 32;  // 1 = SVD path needed
+  const size_t qsm = pinv_qr_smem(n_s, r);
+  const bool qr_ok = n_s >= r && r <= 128 && qsm <= 220 * 1024;
+  if (qr_ok) {
+    cudaFuncSetAttribute(deim_pinv_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsm);
+    deim_pinv_qr_kernel<<<1, 512, qsm, ctx->stream>>>(op, n_s, need);
+    ADROM_LAUNCH_CK(ctx);
+  }
+  cudaFuncSetAttribute(deim_pinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  deim_pinv_kernel<<<1, 1024, sm, ctx->stream>>>(op, n_s, flag, qr_ok ? need : nullptr);
+  ADROM_LAUNCH_CK(ctx);
+  return ADROM_OK;
+}
+
 int operator_fill(adrom_ctx* ctx, DevOp& op, const double* phi, const double* q_ref,
                   const double* d, int n_s, int* flag) {
   const int r = op.r;
@@ -323,14 +475,7 @@ int operator_fill(adrom_ctx* ctx, DevOp& op, const double* phi, const double* q_
   if (g > ctx->num_sms * 8) g = ctx->num_sms * 8;
   op_gather_kernel<<<(int)g, 256, 0, ctx->stream>>>(op, phi, q_ref, d, n_s);
   ADROM_LAUNCH_CK(ctx);
-  const size_t sm = sizeof(double) * ((size_t)r * (n_s | 1) + (size_t)r * (r | 1) + r) +
-                    sizeof(int) * r + 64;
-  if (sm > 220 * 1024)
-    return set_error(ctx, ADROM_ERR_ARG, "deim pinv: %d x %d exceeds one block", n_s, r);
-  cudaFuncSetAttribute(deim_pinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  deim_pinv_kernel<<<1, 1024, sm, ctx->stream>>>(op, n_s, flag);
-  ADROM_LAUNCH_CK(ctx);
-  return ADROM_OK;
+  return deim_pinv_launch(ctx, op, n_s, flag);
 }
 
 }  // namespace adrom
@@ -354,14 +499,7 @@ int deim_pinv_only(adrom_ctx* ctx, const double* phi, const int64_t* idx, int n_
   op.r = r;
   op.phi_s = phi_s;
   op.pinv = pinv;
-  const size_t sm = sizeof(double) * ((size_t)r * (n_s | 1) + (size_t)r * (r | 1) + r) +
-                    sizeof(int) * r + 64;
-  if (sm > 220 * 1024)
-    return set_error(ctx, ADROM_ERR_ARG, "deim pinv: %d x %d exceeds one block", n_s, r);
-  cudaFuncSetAttribute(deim_pinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  deim_pinv_kernel<<<1, 1024, sm, ctx->stream>>>(op, n_s, flag);
-  ADROM_LAUNCH_CK(ctx);
-  return ADROM_OK;
+  return deim_pinv_launch(ctx, op, n_s, flag);
 }
 
 }  // namespace adrom
