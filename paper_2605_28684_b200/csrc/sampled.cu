@@ -164,6 +164,9 @@ __device__ bool block_qr_certified_solve(double* jA, int ld, int r, double* rhs,
 // ---------------------------------------------------------------------------
 // LSPG (projection.py:158-204)
 // ---------------------------------------------------------------------------
+// STAGE: the pseudo-inverse and the sampled test basis live in shared memory
+// (both are re-read r times per Gauss-Newton iteration by the Jacobian product)
+template <bool STAGE>
 __global__ void __launch_bounds__(512) lspg_kernel(RomStepArgs A) {
   extern __shared__ double sm[];
   const int r = A.op.r;
@@ -190,6 +193,15 @@ __global__ void __launch_bounds__(512) lspg_kernel(RomStepArgs A) {
   double* prev = fs + A.op.ns_cap;        // n_s
   double* res = prev + A.op.ns_cap;       // n_s
   double* test = res + A.op.ns_cap;       // n_s x r
+  const double* pinv = A.op.pinv;         // r x n_s
+  if (STAGE) {
+    double* st = reinterpret_cast<double*>(reinterpret_cast<char*>(order) +
+                                           ((sizeof(int) * r + 15) & ~(size_t)15));
+    double* ps = st;                      // r x n_s
+    test = ps + (size_t)r * A.op.ns_cap;  // n_s x r
+    for (int e = tid; e < r * n_s; e += blockDim.x) ps[e] = A.op.pinv[e];
+    pinv = ps;
+  }
   const double* Dc = A.op.dinv_phi_c;
   for (int k = tid; k < r; k += blockDim.x) a[k] = A.a_prev[k];
   __syncthreads();
@@ -221,7 +233,7 @@ __global__ void __launch_bounds__(512) lspg_kernel(RomStepArgs A) {
     // rho = pinv @ res
     for (int k = warp; k < r; k += nw) {
       double s = 0.0;
-      for (int j = lane; j < n_s; j += 32) s += A.op.pinv[(int64_t)k * n_s + j] * res[j];
+      for (int j = lane; j < n_s; j += 32) s += pinv[(int64_t)k * n_s + j] * res[j];
       s = warp_sum(s);
       if (lane == 0) rho[k] = s;
     }
@@ -237,7 +249,7 @@ __global__ void __launch_bounds__(512) lspg_kernel(RomStepArgs A) {
     // keeps the 32-lane strided + butterfly order of a warp reduction.
     for (int o = tid; o < r * r; o += blockDim.x) {
       const int k = o / r, l = o - k * r;
-      const double* pk = A.op.pinv + (int64_t)k * n_s;
+      const double* pk = pinv + (int64_t)k * n_s;
       double v[32];
 #pragma unroll
       for (int q = 0; q < 32; ++q) {
@@ -457,9 +469,16 @@ int rom_step_async(adrom_ctx* ctx, const RomStepArgs& args, bool lspg) {
   if (lspg) {
     const int ld = r | 1;
     const size_t sm = sizeof(double) * (7 * (size_t)r + 2 * (size_t)r * ld + r + 32) +
-                      sizeof(int) * r + 64;
-    cudaFuncSetAttribute(lspg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    lspg_kernel<<<1, 512, sm, ctx->stream>>>(args);
+                      ((sizeof(int) * r + 15) & ~(size_t)15) + 64;
+    const size_t sm_stage = sm + sizeof(double) * 2 * (size_t)r * args.op.ns_cap;
+    if (sm_stage <= 200 * 1024) {
+      cudaFuncSetAttribute(lspg_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sm_stage);
+      lspg_kernel<true><<<1, 512, sm_stage, ctx->stream>>>(args);
+    } else {
+      cudaFuncSetAttribute(lspg_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      lspg_kernel<false><<<1, 512, sm, ctx->stream>>>(args);
+    }
   } else {
     const size_t sm = sizeof(double) * (7 * (size_t)r + (size_t)r * r + 32) + 64;
     cudaFuncSetAttribute(galerkin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
