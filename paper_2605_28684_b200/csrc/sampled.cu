@@ -52,17 +52,39 @@ __device__ __forceinline__ double eval_row(const PlanView& p, int j, const doubl
 // ---------------------------------------------------------------------------
 constexpr double LS_CERT = 1e10;
 
+// sum of col[k..r)^2 with exactly the rounding of block_sum_dyn over a
+// thread-per-element layout (element k + t on thread t, r - k <= 128), but
+// computed by one warp: the four per-warp butterflies, then the second-level
+// butterfly (w0 + w2) + (w1 + w3)
+__device__ __forceinline__ double warp_colnorm2(const double* col, int k, int r, int lane) {
+  double w[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int i = k + 32 * t + lane;
+    double e = 0.0;
+    if (i < r) e = 0.0 + col[i] * col[i];
+    w[t] = warp_sum(e);
+  }
+  return (w[0] + w[2]) + (w[1] + w[3]);
+}
+
 __device__ bool block_qr_certified_solve(double* jA, int ld, int r, double* rhs, double* out,
                                          double* vbuf, double* red) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  __shared__ double sh_beta, sh_alpha;
+  __shared__ double sh_beta, sh_alpha, sh_nrm2;
+  // Householder QR, two barriers per column: the warp that updates column
+  // k+1 also forms its trailing norm for the next step.  v_k lives in col[k]
+  // during step k; R's diagonal is written back one step later.
+  {
+    const double a0 = warp_colnorm2(jA, 0, r, lane);
+    if (tid == 0) sh_nrm2 = a0;
+  }
+  __syncthreads();
   for (int k = 0; k < r; ++k) {
     double* col = jA + (size_t)k * ld;
-    // norm of col[k:]
-    double a = 0.0;
-    for (int i = k + tid; i < r; i += blockDim.x) a += col[i] * col[i];
-    a = block_sum_dyn(a, red);
     if (tid == 0) {
+      if (k > 0) jA[(size_t)(k - 1) * ld + (k - 1)] = sh_alpha;
+      const double a = sh_nrm2;
       const double x0 = col[k];
       const double nrm = sqrt(a);
       const double alpha = (x0 >= 0.0) ? -nrm : nrm;
@@ -70,24 +92,29 @@ __device__ bool block_qr_certified_solve(double* jA, int ld, int r, double* rhs,
       // v = x - alpha e1, beta = 1 / (v^T v / 2) = 1 / (nrm^2 - x0 alpha)
       const double vtv_half = a - x0 * alpha;
       sh_beta = (vtv_half > 0.0) ? 1.0 / vtv_half : 0.0;
-      vbuf[k] = x0 - alpha;
+      col[k] = x0 - alpha;
     }
-    __syncthreads();
-    for (int i = k + 1 + tid; i < r; i += blockDim.x) vbuf[i] = col[i];
     __syncthreads();
     const double beta = sh_beta;
     // apply H = I - beta v v^T to trailing columns and the rhs (warp per column)
     for (int j = k + 1 + warp; j <= r; j += nw) {
       double* cj = (j < r) ? jA + (size_t)j * ld : rhs;
       double s = 0.0;
-      for (int i = k + lane; i < r; i += 32) s += vbuf[i] * cj[i];
+      for (int i = k + lane; i < r; i += 32) s += col[i] * cj[i];
       s = warp_sum(s) * beta;
-      for (int i = k + lane; i < r; i += 32) cj[i] -= s * vbuf[i];
+      for (int i = k + lane; i < r; i += 32) cj[i] -= s * col[i];
+      if (j == k + 1 && j < r) {
+        __syncwarp();
+        const double a1 = warp_colnorm2(cj, j, r, lane);
+        if (lane == 0) sh_nrm2 = a1;
+      }
     }
     __syncthreads();
-    if (tid == 0) col[k] = sh_alpha;
-    __syncthreads();
   }
+  if (tid == 0) jA[(size_t)(r - 1) * ld + (r - 1)] = sh_alpha;
+  __syncthreads();
+  (void)vbuf;
+  (void)red;
   // ||R||_F and ||R^{-1}||_F.  Column c of R^{-1} (R x = e_c) by
   // column-oriented back substitution, one warp per column: x_i = b_i / R_ii,
   // then b_j -= R_ji x_i for j < i (column i of R is contiguous in jA).
