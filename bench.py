@@ -576,13 +576,84 @@ def reference_rom(args, rank, world):
 
 # --------------------------------------------------------------------------- main
 
+# --------------------------------------------------------------------------- cfg4
+
+CFG4_METRIC = "reacting Euler residual Gcell/s (cfg4: 2^20 cells x 13 vars)"
+
+
+def bench_cfg4(args, rank, world):
+    """Configuration-4 residual (208 B/cell, HBM
+    bound).  Only the residual exists for this model in this revision; a
+    step = one residual evaluation over the grid.  The reference has no such
+    model, so there is no reference arm (cpu_baseline: the numpy oracle that
+    defines the model, timed on a bounded sample)."""
+    import torch
+    import paper_2605_28684_b200 as P
+    from paper_2605_28684_b200 import _lib
+    n = args.n or (1 << 20)
+    m = P.ReactingEulerProblem(n)
+    q = torch.from_numpy(m.initial_state()).cuda()
+    out = torch.empty_like(q)
+    ctx = _lib.Context.get()
+    mabi = m.abi()
+    import ctypes as C
+    call = lambda: ctx.call("adrom_rhs", C.byref(mabi), _lib.ptr(q), _lib.ptr(out))  # noqa: E731
+    for _ in range(max(args.warmup, 3)):
+        call()
+    torch.cuda.synchronize()
+    barrier(world)
+    K = max(args.steps, 20)
+    l0 = ctx.launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        ev0.record()
+        for _ in range(K):
+            call()
+        ev1.record()
+        torch.cuda.synchronize()
+    ms = max_over_ranks(ev0.elapsed_time(ev1), world) / K
+    gcells = world * n / (ms * 1e-3) / 1e9
+    line = {
+        "metric": CFG4_METRIC, "value": round(gcells, 2), "unit": "Gcell/s", "n_gpus": world,
+        "steps": K, "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded mechanism and pulse IC, DESIGN.md §9)",
+        "config": {"workload": "cfg4-reacting-residual-2^20", "n_elem": n, "n_var": 13,
+                   "l2": "inputs larger than L2 (%.0f MB state)" % (8 * 13 * n / 1e6),
+                   "parallelism": f"replicas{world}"},
+        "roofline": roofline(208.0 * n, ms),
+        "gpu_launches": ctx.launches() - l0,
+        "clocks": clk.summary(),
+    }
+    line["roofline"]["kernel"] = "reacting_rhs_kernel (208 B/cell)"
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import reacting as R
+        ns = 1 << 16
+        qh = R.initial_state(ns)
+        t0 = time.perf_counter()
+        reps = 0
+        while time.perf_counter() - t0 < 5.0:
+            R.rhs(qh, ns, 1.0 / ns, 1.4, R.mechanism())
+            reps += 1
+        dt = (time.perf_counter() - t0) / reps
+        line["cpu_baseline"] = {"value": round(ns / dt / 1e9, 5), "unit": "Gcell/s", "cores": 1,
+                                "kind": "port",
+                                "sample": f"oracle/reacting.rhs (numpy) at 2^16 cells, {reps} reps"}
+    return line
+
+
+def reference_cfg4(args, rank, world):
+    return {"impl": "reference",
+            "unavailable": "the reference has no reacting model (SPEC.md:8); see cpu_baseline"}
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg3", choices=["cfg0", "cfg1", "cfg2", "cfg3"])
+    ap.add_argument("--config", default="cfg3", choices=["cfg0", "cfg1", "cfg2", "cfg3", "cfg4"])
     ap.add_argument("--n", type=int, default=0, help="override grid size (testing)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -593,14 +664,15 @@ def main(argv=None):
         rank = int(os.environ.get("RANK", "0"))
         world = int(os.environ.get("WORLD_SIZE", "1"))
         fn = {"cfg2": reference_cfg2, "cfg0": reference_rom, "cfg1": reference_rom,
-              "cfg3": reference_rom}.get(args.config)
+              "cfg3": reference_rom, "cfg4": reference_cfg4}.get(args.config)
         line = fn(args, rank, world) if fn else None
         if rank == 0:
             print(json.dumps(line if line else {"impl": "reference",
                                                 "unavailable": f"{args.config} not wired yet"}))
         return 0
     rank, world, _ = dist_setup()
-    fn = {"cfg2": bench_cfg2, "cfg0": bench_rom, "cfg1": bench_rom, "cfg3": bench_rom}[args.config]
+    fn = {"cfg2": bench_cfg2, "cfg0": bench_rom, "cfg1": bench_rom, "cfg3": bench_rom,
+          "cfg4": bench_cfg4}[args.config]
     line = fn(args, rank, world)
     if rank == 0:
         print(json.dumps(line))

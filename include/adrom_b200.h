@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define ADROM_ABI_VERSION 1
+#define ADROM_ABI_VERSION 2
 
 enum adrom_status {
   ADROM_OK = 0,
@@ -48,7 +48,10 @@ enum adrom_status {
 
 enum adrom_model_kind {
   ADROM_BURGERS = 1, /* fom.BurgersProblem (fom.py:161-201): periodic, n_var=1 */
-  ADROM_SOD = 2      /* fom.SodProblem (fom.py:249-282): zero-gradient, n_var=3 */
+  ADROM_SOD = 2,     /* fom.SodProblem (fom.py:249-282): zero-gradient, n_var=3 */
+  ADROM_REACTING = 3 /* configuration-4 reacting Euler (no reference code, SPEC.md:8;
+                        defined by oracle/reacting.py): periodic, n_var=13.
+                        Residual only in this revision (adrom_rhs). */
 };
 
 /* Physics + grid of one full-order model (replaces the FomProblem instance). */
@@ -59,6 +62,8 @@ typedef struct adrom_model {
   double dx;      /* length / n_elem (fom.py:74)                   */
   double nu;      /* Burgers viscosity (fom.py:173)                */
   double gamma;   /* Euler specific-heat ratio (fom.py:260)        */
+  const double* mech; /* ADROM_REACTING: device array 5 x 12 (a, b, A, Ta, q
+                         per reaction); NULL otherwise                 */
 } adrom_model;
 
 typedef struct adrom_ctx adrom_ctx;

@@ -12,12 +12,14 @@ from .fom import (
     BurgersProblem,
     FomProblem,
     NewtonResult,
+    ReactingEulerProblem,
     SodProblem,
     TimeStepper,
     coarse_step,
     fd_jacobian,
     fd_jacobian_blocks,
     implicit_step,
+    reacting_mechanism,
     sod_initial_state,
 )
 from .dense import SvdResult, thin_svd, max_principal_angle

@@ -32,6 +32,7 @@ UNITS = {
     "context.cu": [],
     "fom.cu": ["--fmad=false"],      # bitwise numpy parity of residual / Jacobian
     "sampled.cu": ["--fmad=false"],  # LSPG/Galerkin evaluate the residual too
+    "reacting.cu": ["--fmad=false"], # configuration-4 residual (mirrors oracle/reacting.py)
     "btsolve.cu": [],
     "linalg.cu": [],
     "sampling.cu": [],

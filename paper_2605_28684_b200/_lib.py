@@ -19,7 +19,7 @@ _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / "lib" / "libadrom_b200.so"
 
 OK, ERR_NONFINITE, ERR_SINGULAR, ERR_ROMSTEP, ERR_ARG, ERR_CUDA, ERR_NOCONV, ERR_DENSE = range(8)
-BURGERS, SOD = 1, 2
+BURGERS, SOD, REACTING = 1, 2, 3
 
 _p = C.c_void_p
 _i32, _i64, _f64 = C.c_int32, C.c_int64, C.c_double
@@ -29,7 +29,7 @@ class Model(C.Structure):
     """``adrom_model`` (include/adrom_b200.h)."""
 
     _fields_ = [("kind", _i32), ("n_var", _i32), ("n_elem", _i64),
-                ("dx", _f64), ("nu", _f64), ("gamma", _f64)]
+                ("dx", _f64), ("nu", _f64), ("gamma", _f64), ("mech", _p)]
 
 
 class NewtonInfo(C.Structure):
@@ -230,8 +230,9 @@ def ptr(t) -> _p:
     return _p(t.data_ptr())
 
 
-def model_struct(kind: int, n_var: int, n_elem: int, dx: float, nu: float, gamma: float) -> Model:
-    return Model(kind, n_var, n_elem, dx, nu, gamma)
+def model_struct(kind: int, n_var: int, n_elem: int, dx: float, nu: float, gamma: float,
+                 mech=None) -> Model:
+    return Model(kind, n_var, n_elem, dx, nu, gamma, ptr(mech))
 
 
 __all__ = ["Context", "load", "ptr", "Model", "NewtonInfo", "IsvdInfo", "SIGNATURES",

@@ -360,6 +360,9 @@ static inline BurgersParams burgers_params(const adrom_model& m) {
 static int check_model(adrom_ctx* ctx, const adrom_model& m) {
   if (m.kind == ADROM_BURGERS && m.n_var == 1 && m.n_elem >= 4) return ADROM_OK;
   if (m.kind == ADROM_SOD && m.n_var == 3 && m.n_elem >= 4) return ADROM_OK;
+  if (m.kind == ADROM_REACTING)
+    return set_error(ctx, ADROM_ERR_ARG,
+                     "reacting model: only the residual (adrom_rhs) is implemented in this revision");
   return set_error(ctx, ADROM_ERR_ARG, "unsupported model (kind=%d, n_var=%d, n_elem=%lld)",
                    m.kind, m.n_var, (long long)m.n_elem);
 }
@@ -392,6 +395,14 @@ static int launch_residual(adrom_ctx* ctx, const adrom_model& m, const double* x
 }
 
 int fom_rhs(adrom_ctx* ctx, const adrom_model& m, const double* q, double* f) {
+  if (m.kind == ADROM_REACTING) {
+    if (m.n_var != 13 || m.n_elem < 4)
+      return set_error(ctx, ADROM_ERR_ARG, "reacting model needs n_var=13, n_elem>=4");
+    const int pr = prof_begin(ctx, PROBE_FOM_RESIDUAL);
+    const int st = reacting_rhs(ctx, m, q, f);
+    prof_end(ctx, pr);
+    return st;
+  }
   int st = check_model(ctx, m);
   if (st) return st;
   const int pr = prof_begin(ctx, PROBE_FOM_RESIDUAL);

@@ -17,10 +17,11 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _dev
-from ._lib import BURGERS, SOD, Context, Model, NewtonInfo, ptr
+from ._lib import BURGERS, REACTING, SOD, Context, Model, NewtonInfo, ptr
 from .errors import DenseError
 
-__all__ = ["TimeStepper", "FomProblem", "BurgersProblem", "SodProblem", "NewtonResult",
+__all__ = ["TimeStepper", "FomProblem", "BurgersProblem", "SodProblem", "ReactingEulerProblem",
+           "reacting_mechanism", "NewtonResult",
            "fd_jacobian", "fd_jacobian_blocks", "implicit_step", "coarse_step",
            "sod_initial_state", "PRIM_FLOOR", "FD_EPS"]
 
@@ -76,8 +77,9 @@ class FomProblem:
         return (np.arange(self.n_elem) + 0.5) * self.dx
 
     def abi(self) -> Model:
+        mech = getattr(self, "_mech_dev", None)
         return Model(self.kind, self.n_var, self.n_elem, self.dx,
-                     getattr(self, "nu", 0.0), getattr(self, "gamma", 1.4))
+                     getattr(self, "nu", 0.0), getattr(self, "gamma", 1.4), ptr(mech))
 
     def neighbor_cells(self, cells):
         """fom.py:92-97."""
@@ -183,6 +185,68 @@ class SodProblem(FomProblem):
         vel = u[:, 1] / rho
         p = np.maximum((self.gamma - 1.0) * (u[:, 2] - 0.5 * rho * vel ** 2), PRIM_FLOOR)
         return {"rho": rho, "v": vel, "p": p}
+
+
+N_SPECIES, N_REACT = 10, 12
+
+
+def reacting_mechanism(seed: int = 4) -> np.ndarray:
+    """Seeded configuration-4 mechanism (SURVEY §8d cfg 4), shape (5, 12):
+    reactant a_j, product b_j, A_j = 10**U[8,12] * 1e-10, Ta_j = U[5e3,2e4]/1e3,
+    q_j = U[1e5,1e6]/1e6 (nondimensional; time / temperature / energy scales
+    1e-10, 1e3, 1e6)."""
+    rng = np.random.default_rng([seed, 4])
+    a = rng.integers(0, N_SPECIES, N_REACT)
+    b = (a + rng.integers(1, N_SPECIES, N_REACT)) % N_SPECIES
+    A = 10.0 ** rng.uniform(8.0, 12.0, N_REACT) * 1e-10
+    Ta = rng.uniform(5e3, 2e4, N_REACT) / 1e3
+    q = rng.uniform(1e5, 1e6, N_REACT) / 1e6
+    return np.stack([a.astype(float), b.astype(float), A, Ta, q])
+
+
+class ReactingEulerProblem(FomProblem):
+    """Configuration-4 reacting Euler model.
+
+    The reference has no reacting model; the model is defined in
+    DESIGN.md §9 / oracle/reacting.py: conserved [rho, m, E, rho Y_0..9],
+    periodic, Rusanov fluxes as ``SodProblem`` plus 12 first-order Arrhenius
+    reactions a_j -> b_j releasing q_j.  Only the residual (``rhs``) runs on
+    the device in this revision.
+    """
+
+    n_var = 3 + N_SPECIES
+    boundary = "periodic"
+    var_names = ("rho", "m", "E") + tuple(f"rhoY{k}" for k in range(N_SPECIES))
+    kind = REACTING
+
+    def __init__(self, n_elem: int, gamma: float = 1.4, length: float = 1.0, seed: int = 4):
+        super().__init__(n_elem, length)
+        if gamma <= 1.0:
+            raise ValueError("gamma must exceed 1")
+        self.gamma = float(gamma)
+        self.mechanism = reacting_mechanism(seed)
+        self._mech_dev = None
+
+    def abi(self) -> Model:
+        if self._mech_dev is None:  # uploaded on first device use
+            self._mech_dev = _dev.dev(self.mechanism.ravel().copy())
+        return Model(self.kind, self.n_var, self.n_elem, self.dx, 0.0, self.gamma,
+                     ptr(self._mech_dev))
+
+    def initial_state(self) -> np.ndarray:
+        """Sinusoidal density, drift 0.1, Gaussian pressure pulse, Y_k=(k+1)/55."""
+        n = self.n_elem
+        x = (np.arange(n) + 0.5) / n
+        rho = 1.0 + 0.1 * np.sin(2.0 * np.pi * x)
+        u = np.full(n, 0.1)
+        p = 1.0 + 0.5 * np.exp(-0.5 * ((x - 0.5) / 0.05) ** 2)
+        out = np.empty((n, self.n_var))
+        out[:, 0] = rho
+        out[:, 1] = rho * u
+        out[:, 2] = p / (self.gamma - 1.0) + (0.5 * rho) * (u * u)
+        for k in range(N_SPECIES):
+            out[:, 3 + k] = rho * ((k + 1) / 55.0)
+        return out.ravel()
 
 
 def _check_model(model):

@@ -47,7 +47,7 @@ def test_ctypes_signatures_cover_header(lib_path):
 def test_library_loads_and_reports_abi_version(lib_path):
     import ctypes
     lib = ctypes.CDLL(str(lib_path))
-    assert lib.adrom_abi_version() == 1
+    assert lib.adrom_abi_version() == 2
 
 
 def test_kernels_are_sm100a(lib_path):
