@@ -7,7 +7,8 @@ SURVEY.md §8a row a3: "no reference code ... numpy oracle (builder-defined)").
 This module *is* the definition of the model; the CUDA kernel
 is checked against it, and both against the conservation identities below.
 
-Model (nondimensional, periodic, n_var = 13, layout q[cell*13 + var]):
+Model (nondimensional, periodic, n_var = 13, layout q[cell*13 + var]; the
+initial state follows BASELINE.json configs[4]):
 
   U = [rho, m, E, rho Y_0 .. rho Y_9]
   primitives as the Sod model (fom.py:204-210): rho = max(U0, 1e-10),
@@ -50,17 +51,20 @@ def mechanism(seed: int = 4) -> np.ndarray:
     return np.stack([a.astype(float), b.astype(float), A, Ta, q])
 
 
-def initial_state(n_elem: int, gamma: float = 1.4) -> np.ndarray:
-    """Sinusoidal density, uniform drift, Gaussian pressure pulse, graded
-    species fractions Y_k = (k+1)/55."""
+def initial_state(n_elem: int, gamma: float = 1.4, seed: int = 4) -> np.ndarray:
+    """BASELINE cfg 4: base state rho = 1, p = 1, u = 0 with a seeded
+    sinusoidal pressure (hence temperature, T = p/rho) pulse
+    p = 1 + a (1 + cos(2 pi (x - c) / w)) / 2 for |x - c| < w/2, a ~ U[0.5, 1],
+    c ~ U[0.3, 0.7], w = 0.1; species fractions Y_k = (k+1)/55."""
+    rng = np.random.default_rng([seed, 5])
+    amp, cen, wid = rng.uniform(0.5, 1.0), rng.uniform(0.3, 0.7), 0.1
     x = (np.arange(n_elem) + 0.5) / n_elem
-    rho = 1.0 + 0.1 * np.sin(2.0 * np.pi * x)
-    u = np.full(n_elem, 0.1)
-    p = 1.0 + 0.5 * np.exp(-0.5 * ((x - 0.5) / 0.05) ** 2)
-    out = np.empty((n_elem, N_VAR))
+    rho = np.ones(n_elem)
+    d = x - cen
+    p = 1.0 + np.where(np.abs(d) < 0.5 * wid, amp * 0.5 * (1.0 + np.cos(2.0 * np.pi * d / wid)), 0.0)
+    out = np.zeros((n_elem, N_VAR))
     out[:, 0] = rho
-    out[:, 1] = rho * u
-    out[:, 2] = p / (gamma - 1.0) + (0.5 * rho) * (u * u)
+    out[:, 2] = p / (gamma - 1.0)
     for k in range(N_SPECIES):
         out[:, 3 + k] = rho * ((k + 1) / 55.0)
     return out.ravel()

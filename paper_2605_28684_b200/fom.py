@@ -224,6 +224,7 @@ class ReactingEulerProblem(FomProblem):
         if gamma <= 1.0:
             raise ValueError("gamma must exceed 1")
         self.gamma = float(gamma)
+        self.seed = int(seed)
         self.mechanism = reacting_mechanism(seed)
         self._mech_dev = None
 
@@ -234,18 +235,21 @@ class ReactingEulerProblem(FomProblem):
                      ptr(self._mech_dev))
 
     def initial_state(self) -> np.ndarray:
-        """Sinusoidal density, drift 0.1, Gaussian pressure pulse, Y_k=(k+1)/55."""
+        """BASELINE cfg 4: rho = 1, u = 0, p = 1 plus a seeded sinusoidal
+        pressure/temperature pulse (amplitude U[0.5, 1], centre U[0.3, 0.7],
+        width 0.1); species fractions Y_k = (k+1)/55."""
         n = self.n_elem
+        rng = np.random.default_rng([self.seed, 5])
+        amp, cen, wid = rng.uniform(0.5, 1.0), rng.uniform(0.3, 0.7), 0.1
         x = (np.arange(n) + 0.5) / n
-        rho = 1.0 + 0.1 * np.sin(2.0 * np.pi * x)
-        u = np.full(n, 0.1)
-        p = 1.0 + 0.5 * np.exp(-0.5 * ((x - 0.5) / 0.05) ** 2)
-        out = np.empty((n, self.n_var))
-        out[:, 0] = rho
-        out[:, 1] = rho * u
-        out[:, 2] = p / (self.gamma - 1.0) + (0.5 * rho) * (u * u)
+        d = x - cen
+        p = 1.0 + np.where(np.abs(d) < 0.5 * wid,
+                           amp * 0.5 * (1.0 + np.cos(2.0 * np.pi * d / wid)), 0.0)
+        out = np.zeros((n, self.n_var))
+        out[:, 0] = 1.0
+        out[:, 2] = p / (self.gamma - 1.0)
         for k in range(N_SPECIES):
-            out[:, 3 + k] = rho * ((k + 1) / 55.0)
+            out[:, 3 + k] = 1.0 * ((k + 1) / 55.0)
         return out.ravel()
 
 
