@@ -498,7 +498,7 @@ def e2e_rom(args, case):
     import torch
     from paper_2605_28684_b200.driver import Session, offline_stage
     cfg, model = rom_experiment(case)
-    K = min(args.steps, 10)
+    K = args.steps
     N, r = model.n_dof, case.r
     training, scaling, basis0 = offline_stage(cfg, model)
     pin = lambda x: x.detach().to("cpu").pin_memory()  # noqa: E731

@@ -97,6 +97,12 @@ struct adrom_session {
   adrom_ctx* fctx = nullptr;
   cudaStream_t fstream = nullptr;
   cudaEvent_t main_mark = nullptr, fom_done = nullptr;
+  // trajectory download: q~ is staged (D2D) into one of two device buffers
+  // and copied to host memory on its own stream, overlapping the next steps
+  cudaStream_t cstream = nullptr;
+  double* stage[2] = {nullptr, nullptr};
+  cudaEvent_t st_ready[2] = {nullptr, nullptr}, st_done[2] = {nullptr, nullptr};
+  int64_t n_down = 0;
   double* step_log = nullptr;    // n_t_online x 3
   int* fail_step = nullptr;
   int64_t n_online = 0;          // steps done
@@ -225,6 +231,38 @@ int decode_state(adrom_session* s) {
   const int st = ts_decode(ctx, s->phi[s->cur], s->N, s->r, s->a, s->q_ref, s->d, s->q_tilde);
   prof_end(ctx, pr);
   return st;
+}
+
+// Copy q~ to (pinned) host memory without stalling the loop: D2D into a
+// staging slot on the main stream, D2H on the copy stream.
+int download_state(adrom_session* s, double* host_dst) {
+  adrom_ctx* ctx = s->ctx;
+  const size_t bytes = sizeof(double) * (size_t)s->N;
+  if (!s->cstream) {
+    if (cudaStreamCreateWithFlags(&s->cstream, cudaStreamNonBlocking) != cudaSuccess)
+      return set_error(ctx, ADROM_ERR_CUDA, "session: copy stream creation failed");
+    for (int b = 0; b < 2; ++b) {
+      s->stage[b] = s->alloc_d((size_t)s->N);
+      if (!s->stage[b] || cudaEventCreateWithFlags(&s->st_ready[b], cudaEventDisableTiming) ||
+          cudaEventCreateWithFlags(&s->st_done[b], cudaEventDisableTiming))
+        return set_error(ctx, ADROM_ERR_CUDA, "session: staging allocation failed");
+    }
+  }
+  const int b = (int)(s->n_down & 1);
+  if (s->n_down >= 2) ADROM_CK(ctx, cudaStreamWaitEvent(ctx->stream, s->st_done[b], 0));
+  ADROM_CK(ctx, cudaMemcpyAsync(s->stage[b], s->q_tilde, bytes, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+  ADROM_CK(ctx, cudaEventRecord(s->st_ready[b], ctx->stream));
+  ADROM_CK(ctx, cudaStreamWaitEvent(s->cstream, s->st_ready[b], 0));
+  ADROM_CK(ctx, cudaMemcpyAsync(host_dst, s->stage[b], bytes, cudaMemcpyDeviceToHost, s->cstream));
+  ADROM_CK(ctx, cudaEventRecord(s->st_done[b], s->cstream));
+  ++s->n_down;
+  return ADROM_OK;
+}
+
+int drain_downloads(adrom_session* s) {
+  if (s->cstream) ADROM_CK(s->ctx, cudaStreamSynchronize(s->cstream));
+  return ADROM_OK;
 }
 
 // one adaptation event (driver.py:351-387, history-aware branch).  The
@@ -400,6 +438,14 @@ void adrom_session_destroy(adrom_session* s) {
   if (s->fstream) cudaStreamDestroy(s->fstream);
   if (s->main_mark) cudaEventDestroy(s->main_mark);
   if (s->fom_done) cudaEventDestroy(s->fom_done);
+  if (s->cstream) {
+    cudaStreamSynchronize(s->cstream);
+    cudaStreamDestroy(s->cstream);
+  }
+  for (int b = 0; b < 2; ++b) {
+    if (s->st_ready[b]) cudaEventDestroy(s->st_ready[b]);
+    if (s->st_done[b]) cudaEventDestroy(s->st_done[b]);
+  }
   for (void* p : s->allocs) cudaFree(p);
   delete s;
 }
@@ -482,9 +528,10 @@ int adrom_session_advance(adrom_session* s, int64_t n_steps, int64_t save_every,
       if (dev_out)
         ADROM_CK(ctx, cudaMemcpyAsync(dev_out + saved * N, s->q_tilde, 8 * N,
                                       cudaMemcpyDeviceToDevice, ctx->stream));
-      if (host_out)
-        ADROM_CK(ctx, cudaMemcpyAsync(host_out + saved * N, s->q_tilde, 8 * N,
-                                      cudaMemcpyDeviceToHost, ctx->stream));
+      if (host_out) {
+        st = download_state(s, host_out + saved * N);
+        if (st) return st;
+      }
       ++saved;
     }
     if (at_event) {
@@ -501,12 +548,15 @@ int adrom_session_advance(adrom_session* s, int64_t n_steps, int64_t save_every,
     }
   }
   if (n_saved) *n_saved = saved;
-  return ADROM_OK;
+  // host_out is complete when advance returns (the copies overlapped the steps)
+  return drain_downloads(s);
 }
 
 int adrom_session_finish(adrom_session* s) {
   if (!s) return ADROM_ERR_ARG;
   adrom_ctx* ctx = s->ctx;
+  int st = drain_downloads(s);
+  if (st) return st;
   int fs = -1;
   ADROM_CK(ctx, cudaMemcpyAsync(ctx->pinned, s->fail_step, sizeof(int), cudaMemcpyDeviceToHost,
                                 ctx->stream));
