@@ -13,78 +13,102 @@
 namespace adrom {
 
 // ---------------------------------------------------------------------------
-// kernel 1a: Burgers residual, smem-tiled, vectorised fp64 loads/stores
+// kernel 1a: Burgers residual, register-streamed: a lane owns 4 consecutive
+// cells (two 16-byte loads), neighbours come from the adjacent lanes by
+// shuffle and, at the warp edges, from one scalar load each (periodic wrap).
+// No shared memory, no block barriers: 2 warp-chunks in flight per warp.
 // ---------------------------------------------------------------------------
 constexpr int BURG_NT = 256;
-constexpr int BURG_VPT = 4;                    // cells per thread
-constexpr int BURG_TILE = BURG_NT * BURG_VPT;  // 1024 cells per tile
+constexpr int BURG_VPT = 4;                    // cells per lane
+constexpr int BURG_WCH = 32 * BURG_VPT;        // cells per warp chunk
+constexpr int BURG_U = 1;                      // warp chunks in flight
+constexpr int BURG_TILE = BURG_NT * BURG_VPT * BURG_U;  // cells per block iteration
 
 // MODE 0: out = f(q)                                     (fom.py:180-188)
 // MODE 1: out = (q - qprev) - dt * f(q)                  (fom.py:340-341)
 //         + per-block partial sums of out^2 + non-finite flag (dense.py:153)
 template <int MODE>
-__global__ void __launch_bounds__(BURG_NT) burgers_rhs_kernel(
+__global__ void __launch_bounds__(BURG_NT, 4) burgers_rhs_kernel(
     const double* __restrict__ q, double* __restrict__ out, int64_t n, BurgersParams p,
     const double* __restrict__ qprev, double dt, double* __restrict__ partial,
     int* __restrict__ flag) {
-  __shared__ double tile[BURG_TILE + 2];
   __shared__ double red[BURG_NT / 32];
-  const int64_t ntiles = (n + BURG_TILE - 1) / BURG_TILE;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nchunks = (n + BURG_WCH - 1) / BURG_WCH;
+  const int64_t wstride = (int64_t)gridDim.x * (BURG_NT / 32) * BURG_U;
   double acc = 0.0;
   bool bad = false;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t base = t * BURG_TILE;
-    const int cnt = (int)((n - base < BURG_TILE) ? (n - base) : BURG_TILE);
-    __syncthreads();
-    if (cnt == BURG_TILE) {
-      const double2* src = reinterpret_cast<const double2*>(q + base);
-      const double2 a = src[2 * threadIdx.x];
-      const double2 b = src[2 * threadIdx.x + 1];
-      tile[1 + 4 * threadIdx.x] = a.x;
-      tile[2 + 4 * threadIdx.x] = a.y;
-      tile[3 + 4 * threadIdx.x] = b.x;
-      tile[4 + 4 * threadIdx.x] = b.y;
-    } else {
-      for (int i = threadIdx.x; i < cnt; i += BURG_NT) tile[1 + i] = q[base + i];
-    }
-    if (threadIdx.x == 0) tile[0] = q[base == 0 ? n - 1 : base - 1];
-    if (threadIdx.x == BURG_NT - 1) tile[cnt + 1] = q[(base + cnt == n) ? 0 : base + cnt];
-    __syncthreads();
-    double res[BURG_VPT];
-    double2 prev0 = make_double2(0.0, 0.0), prev1 = make_double2(0.0, 0.0);
-    if (MODE == 1 && cnt == BURG_TILE) {
-      const double2* pv = reinterpret_cast<const double2*>(qprev + base);
-      prev0 = pv[2 * threadIdx.x];
-      prev1 = pv[2 * threadIdx.x + 1];
+  for (int64_t c0 = ((int64_t)blockIdx.x * (BURG_NT / 32) + warp) * BURG_U; c0 < nchunks;
+       c0 += wstride) {
+    double v[BURG_U][BURG_VPT], pv[BURG_U][BURG_VPT], lft[BURG_U], rgt[BURG_U];
+#pragma unroll
+    for (int u = 0; u < BURG_U; ++u) {
+      const int64_t ch = c0 + u;
+      const int64_t i0 = ch * BURG_WCH + (int64_t)lane * BURG_VPT;
+      const bool full = (ch + 1) * BURG_WCH <= n;
+      if (ch < nchunks && full) {
+        const double2 a = *reinterpret_cast<const double2*>(q + i0);
+        const double2 b = *reinterpret_cast<const double2*>(q + i0 + 2);
+        v[u][0] = a.x; v[u][1] = a.y; v[u][2] = b.x; v[u][3] = b.y;
+        if (MODE == 1) {
+          const double2 c = *reinterpret_cast<const double2*>(qprev + i0);
+          const double2 d = *reinterpret_cast<const double2*>(qprev + i0 + 2);
+          pv[u][0] = c.x; pv[u][1] = c.y; pv[u][2] = d.x; pv[u][3] = d.y;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < BURG_VPT; ++k) {
+          const bool ok = ch < nchunks && i0 + k < n;
+          v[u][k] = ok ? q[i0 + k] : 0.0;
+          if (MODE == 1) pv[u][k] = ok ? qprev[i0 + k] : 0.0;
+        }
+      }
+      // warp-edge neighbours (periodic)
+      const int64_t cs = ch * BURG_WCH;
+      const int64_t ce = ((cs + BURG_WCH < n) ? cs + BURG_WCH : n);  // one past the chunk
+      lft[u] = (ch < nchunks && lane == 0) ? q[cs == 0 ? n - 1 : cs - 1] : 0.0;
+      rgt[u] = (ch < nchunks && lane == 31) ? q[ce == n ? 0 : ce] : 0.0;
     }
 #pragma unroll
-    for (int k = 0; k < BURG_VPT; ++k) {
-      const int i = BURG_VPT * threadIdx.x + k;
-      res[k] = 0.0;
-      if (i < cnt) {
-        double f = burgers_cell(tile[i], tile[i + 1], tile[i + 2], p);
-        if (MODE == 1) {
-          double qp;
-          if (cnt == BURG_TILE)
-            qp = (k == 0) ? prev0.x : (k == 1) ? prev0.y : (k == 2) ? prev1.x : prev1.y;
-          else
-            qp = qprev[base + i];
-          f = (tile[i + 1] - qp) - dt * f;
-          acc += f * f;
-          bad |= !isfinite(f);
-        }
-        res[k] = f;
-      }
-    }
-    if (cnt == BURG_TILE) {
-      double2* dst = reinterpret_cast<double2*>(out + base);
-      dst[2 * threadIdx.x] = make_double2(res[0], res[1]);
-      dst[2 * threadIdx.x + 1] = make_double2(res[2], res[3]);
-    } else {
+    for (int u = 0; u < BURG_U; ++u) {
+      const int64_t ch = c0 + u;
+      const int64_t i0 = ch * BURG_WCH + (int64_t)lane * BURG_VPT;
+      const double up_from = __shfl_down_sync(0xffffffffu, v[u][0], 1);  // next lane's first
+      const double dn_from = __shfl_up_sync(0xffffffffu, v[u][3], 1);    // prev lane's last
+      if (ch >= nchunks) continue;
+      const int64_t cs = ch * BURG_WCH;
+      const int64_t ce = ((cs + BURG_WCH < n) ? cs + BURG_WCH : n);
+      // neighbours of this lane's first / last cell
+      const double left0 = (lane == 0) ? lft[u] : dn_from;
+      double right3;
+      if (i0 + BURG_VPT < ce) right3 = (lane == 31) ? rgt[u] : up_from;
+      else right3 = q[ce == n ? 0 : ce];  // ragged tail: the cell after the chunk's last
+      double res[BURG_VPT];
 #pragma unroll
       for (int k = 0; k < BURG_VPT; ++k) {
-        const int i = BURG_VPT * threadIdx.x + k;
-        if (i < cnt) out[base + i] = res[k];
+        res[k] = 0.0;
+        if (i0 + k < n) {
+          const double um = (k == 0) ? left0 : v[u][k - 1];
+          // the right neighbour of the chunk's last valid cell wraps at n
+          double up;
+          if (k < BURG_VPT - 1) up = (i0 + k + 1 < n) ? v[u][k + 1] : q[0];
+          else up = right3;
+          double f = burgers_cell(um, v[u][k], up, p);
+          if (MODE == 1) {
+            f = (v[u][k] - pv[u][k]) - dt * f;
+            acc += f * f;
+            bad |= !isfinite(f);
+          }
+          res[k] = f;
+        }
+      }
+      if ((ch + 1) * BURG_WCH <= n) {
+        *reinterpret_cast<double2*>(out + i0) = make_double2(res[0], res[1]);
+        *reinterpret_cast<double2*>(out + i0 + 2) = make_double2(res[2], res[3]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < BURG_VPT; ++k)
+          if (i0 + k < n) out[i0 + k] = res[k];
       }
     }
   }
