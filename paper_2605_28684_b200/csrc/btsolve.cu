@@ -21,7 +21,7 @@
 
 namespace adrom {
 
-constexpr int BT_M = 32;  // rows per partition
+constexpr int BT_M = 16;  // rows per partition
 
 template <int NV>
 struct Blk {
@@ -260,7 +260,7 @@ __global__ void part_solve_kernel(const double* __restrict__ sys, const double* 
 // (1024 rows); lane p walks partition p in smem (stride 33: conflict-free).
 // G lives in D's slot, the outputs Y / V / W overwrite rhs / L / U.
 // ---------------------------------------------------------------------------
-constexpr int PS_WARPS = 2;
+constexpr int PS_WARPS = 4;
 constexpr int PS_LD = BT_M + 1;
 
 __global__ void __launch_bounds__(32 * PS_WARPS) part_solve_scalar_kernel(
@@ -449,7 +449,7 @@ __global__ void assemble_kernel(const double* __restrict__ sys, const double* __
 template <int NV>
 __global__ void backsub_kernel(int64_t n, bool cyclic, const double* __restrict__ Y,
                                const double* __restrict__ V, const double* __restrict__ W,
-                               const double* __restrict__ X, double* __restrict__ out) {
+                               const double* __restrict__ X, double* out, const double* add_to) {
   constexpr int NV2 = NV * NV;
   const int64_t P = (n + BT_M - 1) / BT_M;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -478,8 +478,13 @@ __global__ void backsub_kernel(int64_t n, bool cyclic, const double* __restrict_
         for (int a = 0; a < NV; ++a) xo[a] += t[a];
       }
     }
+    if (add_to) {  // out = add_to + solution (the Newton update x += delta, in place)
 #pragma unroll
-    for (int a = 0; a < NV; ++a) out[i * NV + a] = xo[a];
+      for (int a = 0; a < NV; ++a) out[i * NV + a] = add_to[i * NV + a] + xo[a];
+    } else {
+#pragma unroll
+      for (int a = 0; a < NV; ++a) out[i * NV + a] = xo[a];
+    }
   }
 }
 
@@ -515,7 +520,8 @@ size_t bt_workspace_bytes(int64_t n, int nv) {
 
 template <int NV>
 static int bt_solve_t(adrom_ctx* ctx, const double* sys, const double* rhs, double sign,
-                      int64_t n, bool cyclic, double* out, void* ws, int* flag) {
+                      int64_t n, bool cyclic, double* out, void* ws, int* flag,
+                      const double* add_to) {
   constexpr int NV2 = NV * NV;
   LevelBufs lv[16];
   int nl = 0;
@@ -577,16 +583,17 @@ static int bt_solve_t(adrom_ctx* ctx, const double* sys, const double* rhs, doub
     int64_t gb = (L.n + 255) / 256;
     if (gb > (int64_t)ctx->num_sms * 16) gb = (int64_t)ctx->num_sms * 16;
     backsub_kernel<NV><<<(int)gb, 256, 0, ctx->stream>>>(L.n, cyclic, L.Y, L.V, L.W,
-                                                         lv[l + 1].sol, L.sol);
+                                                         lv[l + 1].sol, L.sol,
+                                                         l == 0 ? add_to : nullptr);
     ADROM_LAUNCH_CK(ctx);
   }
   return ADROM_OK;
 }
 
 int bt_solve(adrom_ctx* ctx, const double* sys, const double* rhs, double rhs_sign, int64_t n,
-             int nv, bool cyclic, double* out, void* ws, int* flag) {
-  if (nv == 1) return bt_solve_t<1>(ctx, sys, rhs, rhs_sign, n, cyclic, out, ws, flag);
-  if (nv == 3) return bt_solve_t<3>(ctx, sys, rhs, rhs_sign, n, cyclic, out, ws, flag);
+             int nv, bool cyclic, double* out, void* ws, int* flag, const double* add_to) {
+  if (nv == 1) return bt_solve_t<1>(ctx, sys, rhs, rhs_sign, n, cyclic, out, ws, flag, add_to);
+  if (nv == 3) return bt_solve_t<3>(ctx, sys, rhs, rhs_sign, n, cyclic, out, ws, flag, add_to);
   return set_error(ctx, ADROM_ERR_ARG, "bt_solve: unsupported block size %d", nv);
 }
 

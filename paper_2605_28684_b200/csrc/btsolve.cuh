@@ -15,6 +15,7 @@ size_t bt_workspace_bytes(int64_t n, int nv);
 // neighbour is row n-1 and row n-1's right neighbour is row 0.  A zero pivot
 // sets bit 2 of *flag.  Asynchronous (no host sync).
 int bt_solve(adrom_ctx* ctx, const double* sys, const double* rhs, double rhs_sign, int64_t n,
-             int nv, bool cyclic, double* out, void* ws, int* flag);
+             int nv, bool cyclic, double* out, void* ws, int* flag,
+             const double* add_to = nullptr);
 
 }  // namespace adrom
