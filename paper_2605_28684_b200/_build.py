@@ -37,6 +37,7 @@ UNITS = {
     "linalg.cu": [],
     "sampling.cu": [],
     "qdeim.cu": [],
+    "factored.cu": [],
     "session.cu": [],
     "capi.cu": [],
 }

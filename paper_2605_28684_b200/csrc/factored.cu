@@ -1,0 +1,719 @@
+// Factored basis for the session's iSVD (r in {32, 64}).
+//
+// The explicit update rotates the whole basis every event, Phi' = [Phi | q^] B
+// (tracking.py:176-177): 2 N r (r+1) flop, FP64-tensor bound at N = 2^24.
+// Here the basis is kept as
+//
+//     Phi = X W,   X = [A | Q_0 .. Q_{k-1}]   (A: N x r anchor, Q: raw residuals)
+//
+// with W ((r+k) x r) on the device.  An event appends its residual q as
+// column k of Q and maps W' = [[W, 0], [0, 1/||q||]] B — O(r^3) instead of
+// O(N r^2).  Every pass over the basis reads X (r + k columns) and applies W
+// to r-vectors; after KQ appended columns the anchor is rebuilt, A = X W, on
+// the FP64 tensor cores (reanchor_kernel).  Mathematically the basis is the
+// reference's Phi' = [Phi, q^] U[:, :r] at every event; only the rounding
+// differs (tests/test_gpu_rom.py compares both representations).
+//
+//   pass 1 (xpass MODE 1): X^T y, ||y||^2 and the fused decode
+//                          q~ = q_ref + (X (W a)) / d        (projection.py:104)
+//   pass 2 (xpass MODE 2): q = y - X (W p) stored as Q[:, k];  X^T q, ||q||^2;
+//                          X^T w, q.w with w = d (q~ - q_ref) (state transfer,
+//                          projection.py:98-99, for the new basis)
+#include "common.cuh"
+#include "factored_internal.cuh"
+#include "linalg_internal.cuh"
+
+namespace adrom {
+
+struct XPassArgs {
+  const double* A;
+  const double* Q;
+  int64_t n;
+  int k, kq;
+  const double* v;      // r + k: decode vector W a (MODE 1) or W p (MODE 2)
+  const double* y;      // snapshot y_hat
+  const double* q_ref;
+  const double* d;
+  double* qt;           // MODE 1: decoded q~ (out); MODE 2: q~ (in)
+  double* Qw;           // MODE 2: Q (column k written)
+  double* qv;           // MODE 2: the residual q also as a contiguous vector
+  double* partial;      // per block: see xpass_partial_width
+  int* flag;
+  const double* vdrop;  // MODE 1 (optional): the previous event's dropped direction in X
+  double* nrm2;         //   coordinates; nrm2[i] -= (X_i . vdrop)^2 (bound -> exact norm)
+};
+
+__host__ __device__ inline int xpass_width(int r, int kq, int mode) {
+  return mode == 1 ? r + kq + 1 : 2 * (r + kq) + 2;
+}
+
+template <int R, int MODE>
+__global__ void __launch_bounds__(256, 2) xpass_kernel(XPassArgs a) {
+  constexpr int LPR = R / 8;        // lanes per row: 8 A columns each
+  constexpr int RPW = 32 / LPR;     // rows per warp per sub-iteration
+  constexpr int QPL = FACT_KQ / LPR;  // Q columns per lane
+  constexpr int U = 2;
+  constexpr int NW = (MODE == 1) ? 1 : 2;  // weight vectors
+  const int kq = a.kq, k = a.k;
+  __shared__ double red[8 * (R + FACT_KQ) * NW];
+  __shared__ double sred[3][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int seg = lane / LPR, sl = lane - seg * LPR;
+  // the row-dot vectors live in shared memory (registers hold the rows)
+  __shared__ __align__(16) double sv[R + FACT_KQ];
+  __shared__ __align__(16) double sg[R + FACT_KQ];
+  const bool drop = (MODE == 1) && a.vdrop != nullptr;
+  for (int j = threadIdx.x; j < R + FACT_KQ; j += blockDim.x) {
+    const bool ok = j < R + k;
+    sv[j] = ok ? a.v[j] : 0.0;
+    sg[j] = (drop && ok) ? a.vdrop[j] : 0.0;
+  }
+  __syncthreads();
+  const double2* vA = reinterpret_cast<const double2*>(sv);
+  const double2* gA = reinterpret_cast<const double2*>(sg);
+  const double* vQ = sv + R;
+  const double* gQ = sg + R;
+  double2 accA[NW][4];
+  double accQ[NW][QPL];
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+#pragma unroll
+    for (int h = 0; h < 4; ++h) accA[w][h] = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int t = 0; t < QPL; ++t) accQ[w][t] = 0.0;
+  }
+  double s0 = 0.0, s1 = 0.0;
+  bool bad = false;
+  const int64_t total_warps = (int64_t)gridDim.x * 8;
+  const int64_t rows_per_iter = (int64_t)RPW * U;
+  for (int64_t g = (int64_t)blockIdx.x * 8 + warp; g * rows_per_iter < a.n; g += total_warps) {
+    const int64_t base = g * rows_per_iter;
+    double2 xa[U][4];
+    double xq[U][QPL];
+    double yv[U], qr[U], dd[U], qt[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + u * RPW + seg;
+      const bool live = i < a.n;
+      if (live) {
+        const double2* rowp = reinterpret_cast<const double2*>(a.A + i * R);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) xa[u][h] = rowp[sl + LPR * h];
+#pragma unroll
+        for (int t = 0; t < QPL; ++t) {
+          const int j = sl + LPR * t;
+          xq[u][t] = (j < k) ? a.Q[i * kq + j] : 0.0;
+        }
+      } else {
+#pragma unroll
+        for (int h = 0; h < 4; ++h) xa[u][h] = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int t = 0; t < QPL; ++t) xq[u][t] = 0.0;
+      }
+      yv[u] = (live && a.y) ? a.y[i] : 0.0;
+      qr[u] = live ? a.q_ref[i] : 0.0;
+      dd[u] = live ? a.d[i] : 1.0;
+      qt[u] = (MODE == 2 && live) ? a.qt[i] : 0.0;
+    }
+    double rd[U], dd2[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      double t0 = 0.0, t2 = 0.0;
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        bad |= !(isfinite(xa[u][h].x) && isfinite(xa[u][h].y));
+        const double2 vv = vA[sl + LPR * h];
+        t0 += xa[u][h].x * vv.x + xa[u][h].y * vv.y;
+        if (MODE == 1 && drop) {
+          const double2 gg = gA[sl + LPR * h];
+          t2 += xa[u][h].x * gg.x + xa[u][h].y * gg.y;
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < QPL; ++t) {
+        t0 += xq[u][t] * vQ[sl + LPR * t];
+        if (MODE == 1 && drop) t2 += xq[u][t] * gQ[sl + LPR * t];
+      }
+      rd[u] = t0;
+      dd2[u] = t2;
+    }
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1)
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        rd[u] += __shfl_xor_sync(0xffffffffu, rd[u], o);
+        if (MODE == 1 && drop) dd2[u] += __shfl_xor_sync(0xffffffffu, dd2[u], o);
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + u * RPW + seg;
+      if (i >= a.n) continue;
+      double w0, w1 = 0.0;
+      if (MODE == 1) {
+        if (sl == 0) a.qt[i] = qr[u] + rd[u] / dd[u];  // decode (projection.py:104)
+        if (drop && sl == 0) a.nrm2[i] = fmax(a.nrm2[i] - dd2[u] * dd2[u], 0.0);
+        w0 = yv[u];
+        bad |= !isfinite(w0);
+        if (sl == 0) s0 += w0 * w0;
+      } else {
+        w0 = yv[u] - rd[u];                    // q = y - Phi p (tracking.py:162)
+        w1 = dd[u] * (qt[u] - qr[u]);          // projection.py:98-99
+        bad |= !isfinite(w0);
+        if (sl == 0) {
+          a.Qw[i * kq + k] = w0;
+          a.qv[i] = w0;
+          s0 += w0 * w0;
+          s1 += w0 * w1;
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        accA[0][h].x += xa[u][h].x * w0;
+        accA[0][h].y += xa[u][h].y * w0;
+        if (NW == 2) {
+          accA[NW - 1][h].x += xa[u][h].x * w1;
+          accA[NW - 1][h].y += xa[u][h].y * w1;
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < QPL; ++t) {
+        accQ[0][t] += xq[u][t] * w0;
+        if (NW == 2) accQ[NW - 1][t] += xq[u][t] * w1;
+      }
+    }
+  }
+  // fold the row segments sharing columns, then the warps (fixed order)
+#pragma unroll
+  for (int o = LPR; o < 32; o <<= 1)
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        accA[w][h].x += __shfl_xor_sync(0xffffffffu, accA[w][h].x, o);
+        accA[w][h].y += __shfl_xor_sync(0xffffffffu, accA[w][h].y, o);
+      }
+#pragma unroll
+      for (int t = 0; t < QPL; ++t) accQ[w][t] += __shfl_xor_sync(0xffffffffu, accQ[w][t], o);
+    }
+  constexpr int WD = R + FACT_KQ;
+  if (seg == 0) {
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        red[(w * 8 + warp) * WD + 2 * (sl + LPR * h)] = accA[w][h].x;
+        red[(w * 8 + warp) * WD + 2 * (sl + LPR * h) + 1] = accA[w][h].y;
+      }
+#pragma unroll
+      for (int t = 0; t < QPL; ++t) red[(w * 8 + warp) * WD + R + sl + LPR * t] = accQ[w][t];
+    }
+  }
+  __syncthreads();
+  const int width = xpass_width(R, kq, MODE);
+  double* out = a.partial + (size_t)blockIdx.x * width;
+  for (int c = threadIdx.x; c < R + kq; c += 256) {
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s += red[(w * 8 + q) * WD + c];
+      out[w * (R + kq + 1) + c] = s;
+    }
+  }
+  const double t0 = block_sum<256>(s0, sred[0]);
+  const double t1 = (MODE == 2) ? block_sum<256>(s1, sred[1]) : 0.0;
+  if (threadIdx.x == 0) {
+    out[R + kq] = t0;
+    if (MODE == 2) out[2 * (R + kq) + 1] = t1;
+  }
+  if (bad && a.flag) atomicOr(a.flag, 1);
+}
+
+// ---------------------------------------------------------------------------
+// small dense helpers (one block)
+// ---------------------------------------------------------------------------
+// out[c] = sum_j M[j][c] x[j]  (M rows x cols, row-major), i.e. M^T x
+__global__ void matT_vec_kernel(const double* __restrict__ M, int rows, int cols,
+                                const double* __restrict__ x, double* __restrict__ out) {
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < rows; ++j) s += M[(size_t)j * cols + c] * x[j];
+    out[c] = s;
+  }
+}
+
+// out[j] = sum_c M[j][c] x[c]  (M x)
+__global__ void mat_vec_kernel(const double* __restrict__ M, int rows, int cols,
+                               const double* __restrict__ x, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = warp; j < rows; j += nw) {
+    double s = 0.0;
+    for (int c = lane; c < cols; c += 32) s += M[(size_t)j * cols + c] * x[c];
+    s = warp_sum(s);
+    if (lane == 0) out[j] = s;
+  }
+}
+
+// W' ((r+k+1) x r) = [[W, 0], [0, qinv]] B  with B ((r+1) x r) from the core
+__global__ void wnext_kernel(const double* __restrict__ W, int rk, int r,
+                             const double* __restrict__ B, const double* __restrict__ qinv,
+                             double* __restrict__ Wn) {
+  const double qi = *qinv;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < (rk + 1) * r; e += gridDim.x * blockDim.x) {
+    const int i = e / r, c = e - i * r;
+    double s = 0.0;
+    if (i < rk) {
+      if (W) {
+        for (int j = 0; j < r; ++j) s += W[(size_t)i * r + j] * B[(size_t)j * r + c];
+      } else {
+        s = B[(size_t)i * r + c];  // W = I (k = 0, i < r)
+      }
+    } else {
+      s = qi * B[(size_t)r * r + c];
+    }
+    Wn[e] = s;
+  }
+}
+
+// pack [W^T t_x ; qinv * s_qw] -> z (r+1), then a = B^T z   (state transfer)
+__global__ void encode_factored_kernel(const double* __restrict__ W, int rk, int r,
+                                       const double* __restrict__ tx, const double* __restrict__ sqw,
+                                       const double* __restrict__ qinv,
+                                       const double* __restrict__ B, double* __restrict__ a_out) {
+  __shared__ double z[129];
+  for (int c = threadIdx.x; c < r; c += blockDim.x) {
+    double s = 0.0;
+    if (W) {
+      for (int j = 0; j < rk; ++j) s += W[(size_t)j * r + c] * tx[j];
+    } else {
+      s = tx[c];
+    }
+    z[c] = s;
+  }
+  if (threadIdx.x == 0) z[r] = (*qinv) * (*sqw);
+  __syncthreads();
+  for (int c = threadIdx.x; c < r; c += blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j <= r; ++j) s += B[(size_t)j * r + c] * z[j];
+    a_out[c] = s;
+  }
+}
+
+// v_drop ((rk + 1)) = [W u_top ; qinv u_bot]  (u = dropped left singular vector of K)
+__global__ void vdrop_kernel(const double* __restrict__ W, int rk, int r,
+                             const double* __restrict__ u, const double* __restrict__ qinv,
+                             double* __restrict__ out) {
+  for (int i = threadIdx.x; i <= rk; i += blockDim.x) {
+    double s = 0.0;
+    if (i < rk) {
+      if (W) {
+        for (int j = 0; j < r; ++j) s += W[(size_t)i * r + j] * u[j];
+      } else {
+        s = u[i];
+      }
+    } else {
+      s = (*qinv) * u[r];
+    }
+    out[i] = s;
+  }
+}
+
+// QDEIM k = 0 bounds of the new basis: ||Phi'_i||^2 <= ||Phi_i||^2 + (q_i / ||q||)^2
+// (B has orthonormal columns); nrm2_next keeps the bound for the next event
+__global__ void seed_bounds_kernel(const double* __restrict__ nrm2, const double* __restrict__ qv,
+                                   const double* __restrict__ qinv, int64_t n,
+                                   double* __restrict__ res2, double* __restrict__ bnd2,
+                                   unsigned char* __restrict__ ver, double* __restrict__ nrm2_next) {
+  const double qi = *qinv;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double qh = qv[i] * qi;
+    const double b = (nrm2[i] + qh * qh) * (1.0 + 64.0 * 2.220446049250313e-16);
+    nrm2_next[i] = b;
+    res2[i] = b;
+    bnd2[i] = b;
+    ver[i] = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// re-anchor: A_out = X W on the FP64 tensor cores (DMMA m8n8k4), exact row
+// norms into nrm2.  X = [A (R cols) | Q (k of FACT_KQ cols)], W ((R+k) x R).
+// 64-row tiles staged by cp.async (stride R + FACT_KQ + 4), 8 warps as
+// 4 (rows) x 2 (cols); B fragments (W) from smem.
+// ---------------------------------------------------------------------------
+template <int R>
+struct ReTC {
+  static constexpr int TM = 64;
+  static constexpr int KX = R + FACT_KQ;      // padded inner dimension
+  static constexpr int S = KX + 4;            // row stride (doubles)
+  static constexpr int SW = R + 4;            // W row stride
+  static constexpr int WN = R / 2, NT = WN / 8, MT = 2, WR = 16;
+  static constexpr size_t smem_doubles = 2 * (size_t)TM * S + (size_t)KX * SW + 2 * TM;
+};
+
+__device__ __forceinline__ void re_cp16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void re_dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int R>
+__global__ void __launch_bounds__(256, 1) reanchor_kernel(const double* __restrict__ A,
+                                                          const double* __restrict__ Q, int k,
+                                                          const double* __restrict__ W, int64_t n,
+                                                          double* __restrict__ out,
+                                                          double* __restrict__ nrm2) {
+  using C = ReTC<R>;
+  extern __shared__ __align__(16) double sm[];
+  double* X0 = sm;                          // 2 stages x TM x S
+  double* Ws = sm + 2 * C::TM * C::S;       // KX x SW (rows >= R + k zero)
+  double* rn = Ws + C::KX * C::SW;          // 2 x TM
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;
+  for (int e = tid; e < C::KX * R; e += 256) {
+    const int j = e / R, c = e - j * R;
+    Ws[j * C::SW + c] = (j < R + k) ? W[(size_t)j * R + c] : 0.0;
+  }
+  const int64_t ntiles = (n + C::TM - 1) / C::TM;
+  auto load_tile = [&](int64_t t, double* Xs) {
+    const int64_t row0 = t * C::TM;
+    for (int c = tid; c < C::TM * (R / 2); c += 256) {
+      const int rr = c / (R / 2), cc = 2 * (c % (R / 2));
+      const bool ok = row0 + rr < n;
+      re_cp16(Xs + rr * C::S + cc, A + (ok ? (row0 + rr) * R + cc : 0), ok ? 16 : 0);
+    }
+    for (int c = tid; c < C::TM * (FACT_KQ / 2); c += 256) {
+      const int rr = c / (FACT_KQ / 2), cc = 2 * (c % (FACT_KQ / 2));
+      const bool ok = row0 + rr < n && cc < k;
+      re_cp16(Xs + rr * C::S + R + cc, Q + (ok ? (row0 + rr) * FACT_KQ + cc : 0), ok ? 16 : 0);
+    }
+    asm volatile("cp.async.commit_group;\n");
+  };
+  int64_t t = blockIdx.x;
+  if (t < ntiles) load_tile(t, X0);
+  int stage = 0;
+  const int ksteps = (R + k + 3) / 4;
+  for (; t < ntiles; t += gridDim.x) {
+    double* Xs = X0 + stage * C::TM * C::S;
+    const int64_t tn = t + gridDim.x;
+    if (tn < ntiles) {
+      load_tile(tn, X0 + (stage ^ 1) * C::TM * C::S);
+      asm volatile("cp.async.wait_group 1;\n");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n");
+    }
+    __syncthreads();
+    // zero the Q columns >= k of this tile (cp.async zero-filled them only
+    // for 16-byte chunks with cc >= k; an odd k leaves column k in a live chunk)
+    if (k & 1)
+      for (int rr = tid; rr < C::TM; rr += 256) Xs[rr * C::S + R + k] = 0.0;
+    __syncthreads();
+    const int64_t row0 = t * C::TM;
+    double acc[C::MT][C::NT][2];
+#pragma unroll
+    for (int i = 0; i < C::MT; ++i)
+#pragma unroll
+      for (int j = 0; j < C::NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    const int ar = wm * C::WR + (lane >> 2), ak = lane & 3;
+    const int bn = wn * C::WN + (lane >> 2), bk = lane & 3;
+    for (int ks = 0; ks < ksteps; ++ks) {
+      const int k0 = 4 * ks;
+      double af[C::MT], bf[C::NT];
+#pragma unroll
+      for (int i = 0; i < C::MT; ++i) af[i] = Xs[(ar + 8 * i) * C::S + k0 + ak];
+#pragma unroll
+      for (int j = 0; j < C::NT; ++j) bf[j] = Ws[(k0 + bk) * C::SW + bn + 8 * j];
+#pragma unroll
+      for (int i = 0; i < C::MT; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NT; ++j) re_dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    const int er = wm * C::WR + (lane >> 2), ec = wn * C::WN + 2 * (lane & 3);
+#pragma unroll
+    for (int i = 0; i < C::MT; ++i) {
+      const int rr = er + 8 * i;
+      double nr = 0.0;
+      if (row0 + rr < n) {
+        double* dst = out + (row0 + rr) * R;
+#pragma unroll
+        for (int j = 0; j < C::NT; ++j) {
+          const double2 v = make_double2(acc[i][j][0], acc[i][j][1]);
+          *reinterpret_cast<double2*>(dst + ec + 8 * j) = v;
+          nr += v.x * v.x + v.y * v.y;
+        }
+      }
+      nr += __shfl_xor_sync(0xffffffffu, nr, 1);
+      nr += __shfl_xor_sync(0xffffffffu, nr, 2);
+      if ((lane & 3) == 0) rn[wn * C::TM + rr] = nr;
+    }
+    __syncthreads();
+    if (nrm2)
+      for (int rr = tid; rr < C::TM; rr += 256)
+        if (row0 + rr < n) nrm2[row0 + rr] = rn[rr] + rn[C::TM + rr];
+    stage ^= 1;
+  }
+}
+
+// rows_out[p][c] = sum_j X_{rows[p]}[j] W[j][c]; warp per row, W in smem
+__global__ void __launch_bounds__(256) gather_rows_kernel(FactBasis b, const int64_t* __restrict__ rows,
+                                                          int64_t count, const int* dcount,
+                                                          double* __restrict__ out) {
+  if (dcount && *dcount < count) count = *dcount;
+  extern __shared__ double wsm[];  // (r + k) x r, then 8 warps x (r + k)
+  const int r = b.r, rk = b.r + b.k;
+  double* Ws = wsm;
+  double* xs = wsm + (size_t)rk * r;
+  for (int e = threadIdx.x; e < rk * r; e += blockDim.x) Ws[e] = b.W ? b.W[e] : ((e / r == e % r) ? 1.0 : 0.0);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* x = xs + (size_t)warp * rk;
+  for (int64_t p = (int64_t)blockIdx.x * 8 + warp; p < count; p += (int64_t)gridDim.x * 8) {
+    const int64_t i = rows[p];
+    for (int j = lane; j < rk; j += 32)
+      x[j] = (i < 0) ? 0.0 : (j < r ? b.A[i * r + j] : b.Q[i * FACT_KQ + (j - r)]);
+    __syncwarp();
+    for (int c = lane; c < r; c += 32) {
+      double s = 0.0;
+      for (int j = 0; j < rk; ++j) s += x[j] * Ws[(size_t)j * r + c];
+      out[p * r + c] = s;
+    }
+    __syncwarp();
+  }
+}
+
+// DMMA variant (r in {32, 64}): a warp takes 8 rows, Phi_rows = X_rows W with
+// A fragments from the rows in global memory and W fragments from smem
+template <int R>
+__global__ void __launch_bounds__(256) gather_rows_tc_kernel(FactBasis b, const int64_t* __restrict__ rows,
+                                                             int64_t count, const int* dcount,
+                                                             double* __restrict__ out) {
+  constexpr int KX = R + FACT_KQ, KS = KX / 4, S = R + 4, NT = R / 8;
+  extern __shared__ __align__(16) double Ws[];  // KX x S
+  if (dcount && *dcount < count) count = *dcount;
+  const int k = b.k;
+  for (int e = threadIdx.x; e < KX * R; e += blockDim.x) {
+    const int j = e / R, c = e - j * R;
+    Ws[j * S + c] = (j < R + k) ? (b.W ? b.W[(size_t)j * R + c] : (j == c ? 1.0 : 0.0)) : 0.0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rq = lane >> 2, cq = lane & 3;
+  const int64_t tiles = (count + 7) / 8;
+  for (int64_t t = (int64_t)blockIdx.x * 8 + warp; t < tiles; t += (int64_t)gridDim.x * 8) {
+    const int64_t p = t * 8 + rq;
+    const int64_t i = (p < count) ? rows[p] : -1;
+    double af[KS];
+#pragma unroll
+    for (int j = 0; j < KS; ++j) {
+      const int c = 4 * j + cq;
+      double x = 0.0;
+      if (i >= 0) {
+        if (c < R) x = b.A[i * R + c];
+        else if (c - R < k) x = b.Q[i * FACT_KQ + (c - R)];
+      }
+      af[j] = x;
+    }
+    double acc[NT][2];
+#pragma unroll
+    for (int ct = 0; ct < NT; ++ct) {
+      acc[ct][0] = acc[ct][1] = 0.0;
+#pragma unroll
+      for (int j = 0; j < KS; ++j) re_dmma(acc[ct][0], acc[ct][1], af[j], Ws[(4 * j + cq) * S + 8 * ct + rq]);
+    }
+    if (p < count) {
+#pragma unroll
+      for (int ct = 0; ct < NT; ++ct)
+        *reinterpret_cast<double2*>(out + p * R + 8 * ct + 2 * cq) = make_double2(acc[ct][0], acc[ct][1]);
+    }
+  }
+}
+
+int fact_gather_rows(adrom_ctx* ctx, const FactBasis& b, const int64_t* rows, int64_t count,
+                     double* rows_out, const int* dcount) {
+  if (count <= 0) return ADROM_OK;
+  if (b.r == 32 || b.r == 64) {
+    auto launch = [&](auto kern, int R) -> int {
+      const size_t sm = sizeof(double) * (size_t)(R + FACT_KQ) * (R + 4);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      int64_t g = ((count + 7) / 8 + 7) / 8;
+      if (g > (int64_t)ctx->num_sms * 4) g = (int64_t)ctx->num_sms * 4;
+      kern<<<(int)(g < 1 ? 1 : g), 256, sm, ctx->stream>>>(b, rows, count, dcount, rows_out);
+      ADROM_LAUNCH_CK(ctx);
+      return ADROM_OK;
+    };
+    return b.r == 32 ? launch(gather_rows_tc_kernel<32>, 32) : launch(gather_rows_tc_kernel<64>, 64);
+  }
+  const int rk = b.r + b.k;
+  const size_t sm = sizeof(double) * ((size_t)rk * b.r + 8 * (size_t)rk);
+  cudaFuncSetAttribute(gather_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  int64_t g = (count + 7) / 8;
+  if (g > (int64_t)ctx->num_sms * 4) g = (int64_t)ctx->num_sms * 4;
+  gather_rows_kernel<<<(int)g, 256, sm, ctx->stream>>>(b, rows, count, dcount, rows_out);
+  ADROM_LAUNCH_CK(ctx);
+  return ADROM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static int xpass_grid(adrom_ctx* ctx, int64_t n) {
+  int64_t g = (int64_t)ctx->num_sms * 2;  // resident blocks (<= 128 registers)
+  const int64_t need = (n + 31) / 32;
+  if (g > need) g = need;
+  return (int)(g < 1 ? 1 : g);
+}
+
+int fact_decode(adrom_ctx* ctx, const FactBasis& b, const double* a, const double* q_ref,
+                const double* d, double* q_tilde, double* small, double* partial) {
+  const int r = b.r, rk = r + b.k;
+  double* v = small;
+  if (b.W) {
+    mat_vec_kernel<<<1, 256, 0, ctx->stream>>>(b.W, rk, r, a, v);
+    ADROM_LAUNCH_CK(ctx);
+  } else {
+    ADROM_CK(ctx, cudaMemcpyAsync(v, a, sizeof(double) * r, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  const int grid = xpass_grid(ctx, b.n);
+  XPassArgs a1{b.A, b.Q, b.n, b.k, FACT_KQ, v, nullptr, q_ref, d, q_tilde, nullptr, nullptr, partial,
+               nullptr};
+  if (r == 64) xpass_kernel<64, 1><<<grid, 256, 0, ctx->stream>>>(a1);
+  else if (r == 32) xpass_kernel<32, 1><<<grid, 256, 0, ctx->stream>>>(a1);
+  else return set_error(ctx, ADROM_ERR_ARG, "factored decode: rank %d", r);
+  ADROM_LAUNCH_CK(ctx);
+  return ADROM_OK;
+}
+
+size_t fact_partial_doubles(adrom_ctx* ctx, int r) {
+  return (size_t)ctx->num_sms * 2 * xpass_width(r, FACT_KQ, 2);
+}
+
+int fact_reanchor(adrom_ctx* ctx, const FactBasis& b, double* out, double* nrm2) {
+  auto launch = [&](auto kern, size_t smd) -> int {
+    const size_t sm = sizeof(double) * smd;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    const int64_t nt = (b.n + 63) / 64;
+    int64_t g = (int64_t)ctx->num_sms;
+    if (g > nt) g = nt;
+    kern<<<(int)(g < 1 ? 1 : g), 256, sm, ctx->stream>>>(b.A, b.Q, b.k, b.W, b.n, out, nrm2);
+    ADROM_LAUNCH_CK(ctx);
+    return ADROM_OK;
+  };
+  if (!b.W) return set_error(ctx, ADROM_ERR_ARG, "reanchor: identity transform");
+  if (b.r == 32) return launch(reanchor_kernel<32>, ReTC<32>::smem_doubles);
+  if (b.r == 64) return launch(reanchor_kernel<64>, ReTC<64>::smem_doubles);
+  return set_error(ctx, ADROM_ERR_ARG, "reanchor: rank %d unsupported", b.r);
+}
+
+int fact_isvd_event(adrom_ctx* ctx, const FactBasis& b, const FactEventArgs& e) {
+  const int r = b.r, k = b.k, rk = r + k;
+  if (!(r == 32 || r == 64) || k < 0 || k >= FACT_KQ)
+    return set_error(ctx, ADROM_ERR_ARG, "factored iSVD: r=%d k=%d", r, k);
+  double* w = e.small;  // small device scratch
+  double* vdec = w;                 // r + KQ
+  double* vp = vdec + r + FACT_KQ;  // r + KQ
+  double* red1 = vp + r + FACT_KQ;  // r + 1: [p1, ||y||^2]
+  double* red2 = red1 + r + 1;      // r + 1: [Phi^T q, ||q||^2]
+  double* pls = red2 + r + 1;       // r
+  double* t1 = pls + r;             // r + KQ + 1   (reduced pass-1 sums)
+  double* t2 = t1 + r + FACT_KQ + 1;  // 2 (r + KQ) + 2 (reduced pass-2 sums)
+  double* Bm = t2 + 2 * (r + FACT_KQ) + 2;  // (r + 1) x r
+  double* Tm = Bm + (r + 1) * r;            // (r + 1) x r
+  double* sb = Tm + (r + 1) * r;            // [0] qinv, [2 .. r+3) dropped vector
+  int* need = (int*)(sb + r + 8);
+  const int grid = xpass_grid(ctx, b.n);
+  // decode vector W a (identity when k == 0 and W == null)
+  if (b.W) {
+    mat_vec_kernel<<<1, 256, 0, ctx->stream>>>(b.W, rk, r, e.a, vdec);
+    ADROM_LAUNCH_CK(ctx);
+  } else {
+    ADROM_CK(ctx, cudaMemcpyAsync(vdec, e.a, sizeof(double) * r, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  // pass 1
+  int pr = prof_begin(ctx, PROBE_ISVD_PROJECT);
+  XPassArgs a1{b.A, b.Q, b.n, k, FACT_KQ, vdec, e.y, e.q_ref, e.d, e.q_tilde, nullptr, nullptr,
+               e.partial, e.flag, e.vdrop_in, e.vdrop_in ? e.nrm2_inout : nullptr};
+  if (r == 64) xpass_kernel<64, 1><<<grid, 256, 0, ctx->stream>>>(a1);
+  else xpass_kernel<32, 1><<<grid, 256, 0, ctx->stream>>>(a1);
+  ADROM_LAUNCH_CK(ctx);
+  const int w1 = xpass_width(r, FACT_KQ, 1);
+  reduce_partials_kernel<<<w1, 256, 0, ctx->stream>>>(e.partial, grid, w1, t1, nullptr);
+  ADROM_LAUNCH_CK(ctx);
+  prof_end(ctx, pr);
+  // p1 = W^T (X^T y), ||y||^2
+  if (b.W) {
+    matT_vec_kernel<<<1, 128, 0, ctx->stream>>>(b.W, rk, r, t1, red1);
+    ADROM_LAUNCH_CK(ctx);
+  } else {
+    ADROM_CK(ctx, cudaMemcpyAsync(red1, t1, sizeof(double) * r, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  ADROM_CK(ctx, cudaMemcpyAsync(red1 + r, t1 + r + FACT_KQ, sizeof(double), cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+  // least squares p = G^{-1} p1; the explicit residual pass always runs here
+  int st = isvd_solve_launch(ctx, red1, e.G, r, pls, need);
+  if (st) return st;
+  set_need_kernel<<<1, 1, 0, ctx->stream>>>(need);
+  ADROM_LAUNCH_CK(ctx);
+  if (b.W) {
+    mat_vec_kernel<<<1, 256, 0, ctx->stream>>>(b.W, rk, r, pls, vp);
+    ADROM_LAUNCH_CK(ctx);
+  } else {
+    ADROM_CK(ctx, cudaMemcpyAsync(vp, pls, sizeof(double) * r, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  // pass 2
+  pr = prof_begin(ctx, PROBE_ISVD_RESID);
+  XPassArgs a2{b.A, b.Q, b.n, k, FACT_KQ, vp, e.y, e.q_ref, e.d, e.q_tilde, e.Qw, e.qv, e.partial,
+               e.flag};
+  if (r == 64) xpass_kernel<64, 2><<<grid, 256, 0, ctx->stream>>>(a2);
+  else xpass_kernel<32, 2><<<grid, 256, 0, ctx->stream>>>(a2);
+  ADROM_LAUNCH_CK(ctx);
+  const int w2 = xpass_width(r, FACT_KQ, 2);
+  reduce_partials_kernel<<<w2, 256, 0, ctx->stream>>>(e.partial, grid, w2, t2, nullptr);
+  ADROM_LAUNCH_CK(ctx);
+  prof_end(ctx, pr);
+  // Phi^T q = W^T (X^T q), ||q||^2
+  if (b.W) {
+    matT_vec_kernel<<<1, 128, 0, ctx->stream>>>(b.W, rk, r, t2, red2);
+    ADROM_LAUNCH_CK(ctx);
+  } else {
+    ADROM_CK(ctx, cudaMemcpyAsync(red2, t2, sizeof(double) * r, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  ADROM_CK(ctx, cudaMemcpyAsync(red2 + r, t2 + r + FACT_KQ, sizeof(double), cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+  // core: K, its SVD, B, qinv, the tracked Gram of the new basis, sigma'
+  pr = prof_begin(ctx, PROBE_ISVD_CORE);
+  double* udrop = sb + 2;  // r + 1 doubles after qinv (sb has 16 + r + 1 slots)
+  st = isvd_core_launch(ctx, e.sigma, red1, pls, red2, need, e.G, r, e.lam, Bm, sb, Tm,
+                        e.G_out, e.sigma_out, e.stats, e.flag, udrop);
+  prof_end(ctx, pr);
+  if (st) return st;
+  // W' and the state transfer for the new basis
+  wnext_kernel<<<(rk + 1) * r / 256 + 1, 256, 0, ctx->stream>>>(b.W, rk, r, Bm, sb, e.W_out);
+  ADROM_LAUNCH_CK(ctx);
+  const double* tw = t2 + r + FACT_KQ + 1;  // X^T w (r + KQ), then q.w
+  encode_factored_kernel<<<1, 128, 0, ctx->stream>>>(b.W, rk, r, tw, tw + r + FACT_KQ, sb, Bm,
+                                                     e.a_out);
+  ADROM_LAUNCH_CK(ctx);
+  // the dropped direction in the new X coordinates: [W u_top ; qinv u_bot]
+  if (e.vdrop_out) {
+    vdrop_kernel<<<1, 128, 0, ctx->stream>>>(b.W, rk, r, udrop, sb, e.vdrop_out);
+    ADROM_LAUNCH_CK(ctx);
+  }
+  // QDEIM seed bounds of the new basis
+  if (e.seed_res2) {
+    int64_t g = (b.n + 255) / 256;
+    if (g > (int64_t)ctx->num_sms * 8) g = (int64_t)ctx->num_sms * 8;
+    seed_bounds_kernel<<<(int)g, 256, 0, ctx->stream>>>(e.nrm2_inout, e.qv, sb, b.n,
+                                                        e.seed_res2, e.seed_bnd2, e.seed_ver,
+                                                        e.nrm2_out);
+    ADROM_LAUNCH_CK(ctx);
+  }
+  return ADROM_OK;
+}
+
+}  // namespace adrom

@@ -1,0 +1,74 @@
+// Host-side internal API of the factored basis (factored.cu), see its header.
+#pragma once
+
+#include "common.cuh"
+
+namespace adrom {
+
+constexpr int FACT_KQ = 16;  // residual columns kept before re-anchoring
+
+// Phi = [A | Q_0 .. Q_{k-1}] W;  W == nullptr means W = I (then k == 0)
+struct FactBasis {
+  const double* A;  // n x r row-major anchor
+  const double* Q;  // n x FACT_KQ row-major residual columns
+  int r, k;
+  const double* W;  // (r + k) x r row-major, or null
+  int64_t n;
+};
+
+struct FactEventArgs {
+  const double* y;        // snapshot y_hat
+  const double* a;        // reduced state to decode
+  const double* q_ref;
+  const double* d;
+  double* q_tilde;        // decoded state (out)
+  double* Qw;             // Q (column k is written)
+  double* qv;             // N-vector: the residual q, contiguous (seed bounds)
+  const double* sigma;    // current sigma (r)
+  const double* G;        // tracked Phi^T Phi (r x r)
+  double lam;
+  double* partial;        // fact_partial_doubles
+  double* small;          // fact_small_doubles
+  double* W_out;          // (r + k + 1) x r
+  double* sigma_out;
+  double* G_out;
+  double* a_out;          // state transfer a' = Phi'^T D (q~ - q_ref)
+  double* stats;          // isvd stats (>= 8 doubles)
+  int* flag;
+  // row norms: nrm2_inout holds bounds of ||Phi_i||^2 for the current basis;
+  // with vdrop_in (the previous event's dropped direction in the current X
+  // coordinates) pass 1 turns them into exact norms (in place).  vdrop_out
+  // receives this event's dropped direction for the next one.
+  double* nrm2_inout;
+  const double* vdrop_in;
+  double* vdrop_out;      // r + k + 1
+  // QDEIM k = 0 bounds of the new basis (optional)
+  double* nrm2_out;
+  double* seed_res2;
+  double* seed_bnd2;
+  unsigned char* seed_ver;
+};
+
+inline size_t fact_small_doubles(int r) {
+  return 8 * (size_t)(r + FACT_KQ + 2) + 2 * (size_t)(r + 1) * r + 3 * (size_t)r + 256;
+}
+size_t fact_partial_doubles(adrom_ctx* ctx, int r);
+
+// one history-aware iSVD event on the factored basis (tracking.py:141-178):
+// decode, both passes, core SVD, W', state transfer, QDEIM seed bounds.
+// Asynchronous; flags as isvd_update_async.
+int fact_isvd_event(adrom_ctx* ctx, const FactBasis& b, const FactEventArgs& e);
+
+// q~ = q_ref + (X (W a)) / d   (projection.py:104 on the factored basis)
+int fact_decode(adrom_ctx* ctx, const FactBasis& b, const double* a, const double* q_ref,
+                const double* d, double* q_tilde, double* small, double* partial);
+
+// out (n x r) = X W (tensor cores); exact row norms into nrm2 (optional)
+int fact_reanchor(adrom_ctx* ctx, const FactBasis& b, double* out, double* nrm2);
+
+// rows_out[p] = Phi_{rows[p]} (r doubles each) for p < min(count, *dcount)
+// (rows[p] < 0 -> zeros; dcount: optional device-side count)
+int fact_gather_rows(adrom_ctx* ctx, const FactBasis& b, const int64_t* rows, int64_t count,
+                     double* rows_out, const int* dcount = nullptr);
+
+}  // namespace adrom

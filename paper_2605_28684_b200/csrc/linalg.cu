@@ -994,7 +994,7 @@ __global__ void __launch_bounds__(1024) isvd_core_kernel(
     const int* __restrict__ need, const double* __restrict__ G, int r_cur, int r, double lam,
     double* __restrict__ Bout, double* __restrict__ qinv_out, double* __restrict__ Tws,
     double* __restrict__ Gout, double* __restrict__ sigma_out, double* __restrict__ stats,
-    int* __restrict__ flag) {
+    int* __restrict__ flag, double* __restrict__ udrop_out) {
   extern __shared__ double sm[];
   const int n = r_cur + 1;
   const int ld = n + ((n & 1) ? 0 : 1);  // odd leading dimension
@@ -1109,6 +1109,9 @@ __global__ void __launch_bounds__(1024) isvd_core_kernel(
     const int k = e / r, c = e - k * r;
     Bout[e] = V[order[c] * ld + k];
   }
+  // the left singular vector the truncation drops (factored basis: exact row norms)
+  if (udrop_out && r < n)
+    for (int k = tid; k < n; k += blockDim.x) udrop_out[k] = V[order[r] * ld + k];
   if (tid == 0) *qinv_out = inv;
   // c_hat = Phi^T q / ||q||: explicit (pass 2) or p1 - G p (normal equations)
   for (int k = tid; k < r_cur; k += blockDim.x) {
@@ -1241,7 +1244,7 @@ int isvd_update_async(adrom_ctx* ctx, const double* phi, const double* sigma, co
   // Gout may alias G: the kernel reads G completely before its final barrier
   double* Gout = gram_out ? gram_out : Gloc;
   isvd_core_kernel<<<1, 1024, csm, ctx->stream>>>(sigma, red1, pls, red2, need, G, r_cur, r, lam,
-                                                  B, qinv, T, Gout, sigma_out, stats, flag);
+                                                  B, qinv, T, Gout, sigma_out, stats, flag, nullptr);
   prof_end(ctx, pr);
   ADROM_LAUNCH_CK(ctx);
   // the rotation reads q from pass 2 when it ran, else forms it from y and p
@@ -1251,6 +1254,27 @@ int isvd_update_async(adrom_ctx* ctx, const double* phi, const double* sigma, co
   st = ts_rotate(ctx, ra);
   prof_end(ctx, pr);
   return st;
+}
+
+int isvd_solve_launch(adrom_ctx* ctx, const double* red1, const double* G, int r, double* p,
+                      int* need) {
+  isvd_solve_kernel<<<1, 128, 0, ctx->stream>>>(red1, G, r, ISVD_REORTH_RATIO, p, need);
+  ADROM_LAUNCH_CK(ctx);
+  return ADROM_OK;
+}
+
+__global__ void set_need_kernel(int* need) { need[0] = 1; }
+
+int isvd_core_launch(adrom_ctx* ctx, const double* sigma, const double* red1, const double* pls,
+                     const double* red2, const int* need, const double* G, int r, double lam,
+                     double* B, double* qinv, double* T, double* Gout, double* sigma_out,
+                     double* stats, int* flag, double* udrop) {
+  const size_t csm = core_smem(r);
+  cudaFuncSetAttribute(isvd_core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
+  isvd_core_kernel<<<1, 1024, csm, ctx->stream>>>(sigma, red1, pls, red2, need, G, r, r, lam, B,
+                                                  qinv, T, Gout, sigma_out, stats, flag, udrop);
+  ADROM_LAUNCH_CK(ctx);
+  return ADROM_OK;
 }
 
 // ---------------------------------------------------------------------------

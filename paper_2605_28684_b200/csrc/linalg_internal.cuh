@@ -61,6 +61,17 @@ int isvd_update_async(adrom_ctx* ctx, const double* phi, const double* sigma, co
                       const double* q_ref, const double* d, double* dec_out,
                       const RotFuse* fuse = nullptr);
 
+// pieces of the iSVD used by the factored-basis event (factored.cu)
+__global__ void reduce_partials_kernel(const double* __restrict__ partial, int nb, int w,
+                                       double* __restrict__ out, const int* skip);
+__global__ void set_need_kernel(int* need);
+int isvd_solve_launch(adrom_ctx* ctx, const double* red1, const double* G, int r, double* p,
+                      int* need);
+int isvd_core_launch(adrom_ctx* ctx, const double* sigma, const double* red1, const double* pls,
+                     const double* red2, const int* need, const double* G, int r, double lam,
+                     double* B, double* qinv, double* T, double* Gout, double* sigma_out,
+                     double* stats, int* flag, double* udrop = nullptr);
+
 int dense_small_svd(adrom_ctx* ctx, const double* a, int m, int n, double* u, double* s,
                     double* v, int* flag);
 

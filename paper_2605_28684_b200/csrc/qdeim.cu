@@ -23,6 +23,7 @@
 
 #include "common.cuh"
 #include "sampling_internal.cuh"
+#include "factored_internal.cuh"
 
 #include <limits.h>
 #include <stdio.h>
@@ -411,7 +412,8 @@ __global__ void __launch_bounds__(256) qp_resvec_kernel(const double* __restrict
                                                         int k, const double* __restrict__ res2,
                                                         double* __restrict__ Rv,
                                                         double* __restrict__ pres2,
-                                                        double* __restrict__ pn2) {
+                                                        double* __restrict__ pn2,
+                                                        bool rows_in_rv) {
   constexpr int LPR = R / 8;
   constexpr int RPW = 32 / LPR;
   constexpr int U = 4;
@@ -435,7 +437,8 @@ __global__ void __launch_bounds__(256) qp_resvec_kernel(const double* __restrict
       live[u] = i >= 0 && res2[i] >= 0.0;
       if (live[u]) {
         if (EXACT) {
-          const double2* rowp = reinterpret_cast<const double2*>(phi + i * R);
+          // rows_in_rv: the pool rows were materialised into Rv (factored basis)
+          const double2* rowp = reinterpret_cast<const double2*>(rows_in_rv ? Rv + p * R : phi + i * R);
 #pragma unroll
           for (int h = 0; h < 4; ++h) v[u][h] = rowp[sl + LPR * h];
         } else {
@@ -773,6 +776,7 @@ size_t qdeim_pool_workspace_bytes(int64_t n, int r, int count) {
   b += 2 * align_up(sizeof(double) * (size_t)P);           // pres2, pn2
   b += 2 * align_up(sizeof(SelState)) + align_up(sizeof(unsigned int) * 256);  // selection
   b += align_up(sizeof(int64_t) * (size_t)n);              // refresh list
+  b += align_up(sizeof(double) * (size_t)(r + FACT_KQ) * r);  // W D (factored rows)
   b += align_up((size_t)n);                                // per-row downdate version
   b += align_up(sizeof(double) * (size_t)r * r);           // D
   b += align_up(sizeof(int64_t) * (size_t)r);              // local pivots
@@ -812,21 +816,27 @@ __device__ __forceinline__ void qp_dmma(double& d0, double& d1, double a, double
                : "d"(a), "d"(b));
 }
 
-template <int R>
+// FACT: rows are X_i = [A_i | Q_i] of a factored basis Phi = X W (factored.cu)
+// and Mm = W D ((R + FACT_KQ) x R, rows >= R + kf zero); the bound's norm term
+// comes from nrmb (bounds of ||Phi_i||^2).  Otherwise rows are phi_i and Mm = D.
+template <int R, bool FACT>
 __global__ void __launch_bounds__(256) qp_refresh_tc_kernel(const double* __restrict__ phi,
+                                                            const double* __restrict__ Qx, int kf,
+                                                            const double* __restrict__ nrmb,
                                                             const int64_t* __restrict__ list,
                                                             int64_t cap,
-                                                            const double* __restrict__ D, int k,
+                                                            const double* __restrict__ Mm, int k,
                                                             double* __restrict__ res2,
                                                             double* __restrict__ bnd2,
                                                             unsigned char* __restrict__ ver) {
-  constexpr int S = R + 4;     // smem row stride: conflict-free B fragments
-  constexpr int KS = R / 4;    // k-steps over the basis columns
-  constexpr int DT = R / 8;    // direction tiles
-  extern __shared__ __align__(16) double Ds[];  // R x S: Ds[j*S + l] = D[j][l] (l < k)
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+  constexpr int S = R + 4;                          // smem row stride
+  constexpr int KX = FACT ? R + FACT_KQ : R;        // inner dimension
+  constexpr int KS = KX / 4;                        // k-steps
+  constexpr int DT = R / 8;                         // direction tiles
+  extern __shared__ __align__(16) double Ds[];      // KX x S: Ds[j*S + l] = Mm[j][l] (l < k)
+  for (int e = threadIdx.x; e < KX * R; e += blockDim.x) {
     const int j = e / R, l = e - j * R;
-    Ds[j * S + l] = (l < k) ? D[j * R + l] : 0.0;
+    Ds[j * S + l] = (l < k) ? Mm[j * R + l] : 0.0;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -843,11 +853,21 @@ __global__ void __launch_bounds__(256) qp_refresh_tc_kernel(const double* __rest
     const double* row = phi + (i >= 0 ? i : 0) * R;
 #pragma unroll
     for (int j = 0; j < KS; ++j) {
-      af[j] = (i >= 0) ? row[4 * j + cq] : 0.0;
-      nrm = fma(af[j], af[j], nrm);
+      const int c = 4 * j + cq;
+      double x = 0.0;
+      if (i >= 0) {
+        if (c < R) x = row[c];
+        else if (c - R < kf) x = Qx[i * FACT_KQ + (c - R)];
+      }
+      af[j] = x;
+      if (!FACT) nrm = fma(x, x, nrm);
     }
-    nrm += __shfl_xor_sync(0xffffffffu, nrm, 1);
-    nrm += __shfl_xor_sync(0xffffffffu, nrm, 2);
+    if (FACT) {
+      nrm = (i >= 0) ? nrmb[i] : 0.0;
+    } else {
+      nrm += __shfl_xor_sync(0xffffffffu, nrm, 1);
+      nrm += __shfl_xor_sync(0xffffffffu, nrm, 2);
+    }
     double sub = 0.0;
     const int t0 = vmin >> 3, t1 = (k + 7) >> 3;
 #pragma unroll
@@ -873,18 +893,34 @@ __global__ void __launch_bounds__(256) qp_refresh_tc_kernel(const double* __rest
   }
 }
 
-template <int R>
-static int qp_refresh_tc(adrom_ctx* ctx, const double* phi, const int64_t* list, int64_t cap,
-                         const double* D, int k, double* res2, double* bnd2, unsigned char* ver) {
-  const size_t sm = sizeof(double) * (size_t)R * (R + 4);
+template <int R, bool FACT>
+static int qp_refresh_tc(adrom_ctx* ctx, const double* phi, const double* Qx, int kf,
+                         const double* nrmb, const int64_t* list, int64_t cap, const double* Mm,
+                         int k, double* res2, double* bnd2, unsigned char* ver) {
+  constexpr int KX = FACT ? R + FACT_KQ : R;
+  const size_t sm = sizeof(double) * (size_t)KX * (R + 4);
   const int64_t tiles = (cap + 7) / 8;
   int64_t g = (tiles + 7) / 8;
   if (g > (int64_t)ctx->num_sms * 8) g = (int64_t)ctx->num_sms * 8;
-  cudaFuncSetAttribute(qp_refresh_tc_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  qp_refresh_tc_kernel<R><<<(int)(g < 1 ? 1 : g), 256, sm, ctx->stream>>>(phi, list, cap, D, k,
-                                                                          res2, bnd2, ver);
+  cudaFuncSetAttribute(qp_refresh_tc_kernel<R, FACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sm);
+  qp_refresh_tc_kernel<R, FACT><<<(int)(g < 1 ? 1 : g), 256, sm, ctx->stream>>>(
+      phi, Qx, kf, nrmb, list, cap, Mm, k, res2, bnd2, ver);
   ADROM_LAUNCH_CK(ctx);
   return ADROM_OK;
+}
+
+// Mm ((r + FACT_KQ) x r) = W D for the directions l < k (rows >= r + kf zero)
+__global__ void qp_wd_kernel(const double* __restrict__ W, int rkf, int r,
+                             const double* __restrict__ D, int k, double* __restrict__ Mm) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < (r + FACT_KQ) * r;
+       e += gridDim.x * blockDim.x) {
+    const int j = e / r, l = e - j * r;
+    double s = 0.0;
+    if (j < rkf && l < k)
+      for (int c = 0; c < r; ++c) s += W[(size_t)j * r + c] * D[(size_t)c * r + l];
+    Mm[e] = s;
+  }
 }
 
 template <int R, bool EXACT>
@@ -908,14 +944,14 @@ static int qp_rows_launch(adrom_ctx* ctx, const double* phi, int64_t n, int r, c
 template <int R, bool EXACT>
 static int qp_resvec(adrom_ctx* ctx, const double* phi, int r, const int64_t* pool_idx, int64_t P,
                      const double* D, int k, const double* res2, double* Rv, double* pres2,
-                     double* pn2) {
+                     double* pn2, bool rows_in_rv = false) {
   const int64_t per_block = (int64_t)(32 / (R / 8)) * 4 * 8;
   int64_t g = (P + per_block - 1) / per_block;
   if (g > (int64_t)ctx->num_sms * 8) g = (int64_t)ctx->num_sms * 8;
   const size_t sm = sizeof(double) * (size_t)R * (k > 0 ? k : 1);
   cudaFuncSetAttribute(qp_resvec_kernel<R, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   qp_resvec_kernel<R, EXACT><<<(int)(g < 1 ? 1 : g), 256, sm, ctx->stream>>>(
-      phi, r, pool_idx, P, D, k, res2, Rv, pres2, pn2);
+      phi, r, pool_idx, P, D, k, res2, Rv, pres2, pn2, rows_in_rv);
   ADROM_LAUNCH_CK(ctx);
   return ADROM_OK;
 }
@@ -930,10 +966,16 @@ void qdeim_seed_buffers(void* ws, int64_t n, double** res2, double** bnd2, unsig
 }
 
 int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int count,
-                      int64_t* out_idx, void* ws, int* passes_out, bool seeded) {
+                      int64_t* out_idx, void* ws, int* passes_out, bool seeded,
+                      const FactBasis* fb, const double* nrmb) {
   if (count > n) return set_error(ctx, ADROM_ERR_DENSE, "cannot select %d pivots from %lld columns",
                                   count, (long long)n);
   if (r < 1 || r > 128) return set_error(ctx, ADROM_ERR_ARG, "qdeim: rank %d unsupported", r);
+  // factored basis rows (Phi = X W): the k = 0 bounds must come seeded, one
+  // restart chunk only (count <= r); the caller materialises Phi otherwise
+  const bool fact = fb && fb->W;
+  if (fact && (!seeded || count > r || !(r == 32 || r == 64) || !nrmb))
+    return set_error(ctx, ADROM_ERR_ARG, "qdeim: factored rows need a seeded single chunk");
   const bool all = n <= POOL_ALL;
   const int64_t P = qp_pool_capacity(n);
   char* w = (char*)ws;
@@ -953,6 +995,7 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
   SelState* selR = (SelState*)take(sizeof(SelState));
   int64_t* rlist = (int64_t*)take(sizeof(int64_t) * (size_t)n);
   unsigned int* hist = (unsigned int*)take(sizeof(unsigned int) * 256);
+  double* Mw = (double*)take(sizeof(double) * (size_t)(r + FACT_KQ) * r);
   double* D = (double*)take(sizeof(double) * (size_t)r * r);
   int64_t* piv = (int64_t*)take(sizeof(int64_t) * (size_t)r);
   int* state = (int*)take(sizeof(int) * 8);
@@ -987,6 +1030,12 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
     return qp_rows_launch<128, false>(ctx, phi, nn, r, D, hi, mode, sl, res2, bnd2, ver, ex, n_ex);
   };
   auto resvec = [&](int k) -> int {
+    if (fact) {  // pool rows of Phi = X W materialised into Rv, CGS2 in place
+      int st2 = fact_gather_rows(ctx, *fb, pool_idx, P, Rv);
+      if (st2) return st2;
+      return (r == 32) ? qp_resvec<32, true>(ctx, fb->A, r, pool_idx, P, D, k, res2, Rv, pres2, pn2, true)
+                       : qp_resvec<64, true>(ctx, fb->A, r, pool_idx, P, D, k, res2, Rv, pres2, pn2, true);
+    }
 #define QP_RV(RR, EX) return qp_resvec<RR, EX>(ctx, phi, r, pool_idx, P, D, k, res2, Rv, pres2, pn2)
     if (r == 16) QP_RV(16, true);
     if (r == 32) QP_RV(32, true);
@@ -1049,10 +1098,20 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
         ADROM_LAUNCH_CK(ctx);
         qs_compact_kernel<<<sg, 256, 0, ctx->stream>>>(bnd2, n, nullptr, selR, rlist, cap);
         ADROM_LAUNCH_CK(ctx);
-        if (r == 32 || r == 64 || r == 128) {
-          st = (r == 32)   ? qp_refresh_tc<32>(ctx, phi, rlist, cap, D, k, res2, bnd2, ver)
-               : (r == 64) ? qp_refresh_tc<64>(ctx, phi, rlist, cap, D, k, res2, bnd2, ver)
-                           : qp_refresh_tc<128>(ctx, phi, rlist, cap, D, k, res2, bnd2, ver);
+        if (fact) {
+          qp_wd_kernel<<<(r + FACT_KQ) * r / 256 + 1, 256, 0, ctx->stream>>>(fb->W, r + fb->k, r, D,
+                                                                            k, Mw);
+          ADROM_LAUNCH_CK(ctx);
+          st = (r == 32) ? qp_refresh_tc<32, true>(ctx, fb->A, fb->Q, fb->k, nrmb, rlist, cap, Mw,
+                                                   k, res2, bnd2, ver)
+                         : qp_refresh_tc<64, true>(ctx, fb->A, fb->Q, fb->k, nrmb, rlist, cap, Mw,
+                                                   k, res2, bnd2, ver);
+        } else if (r == 32 || r == 64 || r == 128) {
+          st = (r == 32)
+                   ? qp_refresh_tc<32, false>(ctx, phi, nullptr, 0, nullptr, rlist, cap, D, k, res2, bnd2, ver)
+               : (r == 64)
+                   ? qp_refresh_tc<64, false>(ctx, phi, nullptr, 0, nullptr, rlist, cap, D, k, res2, bnd2, ver)
+                   : qp_refresh_tc<128, false>(ctx, phi, nullptr, 0, nullptr, rlist, cap, D, k, res2, bnd2, ver);
         } else {
           st = rows_pass(cap, k, QP_REFRESH, rlist, n_ex);
         }
@@ -1105,6 +1164,9 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
           fresh = false;
           continue;
         }
+        // factored rows: the bounds keep the seed's slack, so a stall does not
+        // prove rank deficiency -> the caller reruns on the materialised basis
+        if (fact) return QDEIM_NEEDS_EXPLICIT;
         // nothing certifiable with every bound fresh: only possible when the
         // remaining residuals tie at (numerically) zero -> rank deficient
         if (!(hres[0] >= 1e-14))

@@ -6,6 +6,7 @@
 #include "common.cuh"
 #include "jacobi.cuh"
 #include "sampling_internal.cuh"
+#include "factored_internal.cuh"
 
 #include <limits.h>
 
@@ -260,9 +261,12 @@ int plan_build(adrom_ctx* ctx, const adrom_model& m, DevOp& op, int n_s, int* fl
 // ---------------------------------------------------------------------------
 // reduced operator: gathers (projection.py:72-80) + DEIM pinv (sampling.py:162-175)
 // ---------------------------------------------------------------------------
+// rows_c / rows_s (factored basis): the closure / sampled rows of Phi
+// materialised by fact_gather_rows (row j at j * r); otherwise gathered from phi
 __global__ void op_gather_kernel(DevOp op, const double* __restrict__ phi,
                                  const double* __restrict__ q_ref, const double* __restrict__ d,
-                                 int n_s) {
+                                 int n_s, const double* __restrict__ rows_c,
+                                 const double* __restrict__ rows_s) {
   const int r = op.r;
   const int n_c = op.sizes[1];
   const int64_t total = (int64_t)(n_c + n_s) * (r + 1);
@@ -271,12 +275,14 @@ __global__ void op_gather_kernel(DevOp op, const double* __restrict__ phi,
     const int row = (int)(t / (r + 1)), col = (int)(t % (r + 1));
     if (row < n_c) {
       const int64_t g = op.closure[row];
-      if (col < r) op.dinv_phi_c[(int64_t)row * r + col] = phi[g * r + col] / d[g];
+      if (col < r)
+        op.dinv_phi_c[(int64_t)row * r + col] =
+            (rows_c ? rows_c[(int64_t)row * r + col] : phi[g * r + col]) / d[g];
       else op.q_ref_c[row] = q_ref[g];
     } else {
       const int j = row - n_c;
       const int64_t g = op.idx[j];
-      if (col < r) op.phi_s[(int64_t)j * r + col] = phi[g * r + col];
+      if (col < r) op.phi_s[(int64_t)j * r + col] = rows_s ? rows_s[(int64_t)j * r + col] : phi[g * r + col];
       else op.d_s[j] = d[g];
     }
   }
@@ -468,12 +474,22 @@ static int deim_pinv_launch(adrom_ctx* ctx, DevOp& op, int n_s, int* flag) {
 }
 
 int operator_fill(adrom_ctx* ctx, DevOp& op, const double* phi, const double* q_ref,
-                  const double* d, int n_s, int* flag) {
+                  const double* d, int n_s, int* flag, const FactBasis* fb, double* fact_rows) {
   const int r = op.r;
   const int64_t total = (int64_t)(op.nc_cap + n_s) * (r + 1);
   int64_t g = (total + 255) / 256;
   if (g > ctx->num_sms * 8) g = ctx->num_sms * 8;
-  op_gather_kernel<<<(int)g, 256, 0, ctx->stream>>>(op, phi, q_ref, d, n_s);
+  double* rows_c = nullptr;
+  double* rows_s = nullptr;
+  if (fb && fb->W) {
+    rows_c = fact_rows;
+    rows_s = fact_rows + (size_t)op.nc_cap * r;
+    int st = fact_gather_rows(ctx, *fb, op.closure, op.nc_cap, rows_c, op.sizes + 1);
+    if (st) return st;
+    st = fact_gather_rows(ctx, *fb, op.idx, n_s, rows_s);
+    if (st) return st;
+  }
+  op_gather_kernel<<<(int)g, 256, 0, ctx->stream>>>(op, phi, q_ref, d, n_s, rows_c, rows_s);
   ADROM_LAUNCH_CK(ctx);
   return deim_pinv_launch(ctx, op, n_s, flag);
 }

@@ -13,8 +13,10 @@
 #include "linalg_internal.cuh"
 #include "rom_internal.cuh"
 #include "sampling_internal.cuh"
+#include "factored_internal.cuh"
 
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <vector>
@@ -92,6 +94,21 @@ struct adrom_session {
   void* isvd_ws = nullptr;
   void* qd_ws = nullptr;
   double* enc_partial = nullptr;  // fused encode partial sums (rotation epilogue)
+  // factored basis (factored.cu): Phi = [phi[acur] | Qb[:, :kf]] W, W = Wd[cur]
+  // (identity while w_id); sigma / gram / Wd / nrm2 are indexed by cur, the
+  // anchor by acur (it only changes on a re-anchor)
+  bool fact = false;
+  int kf = 0, acur = 0;
+  bool w_id = true;
+  double* Qb = nullptr;
+  double* Wd[2] = {nullptr, nullptr};
+  double* nrm2[2] = {nullptr, nullptr};
+  double* vdrop[2] = {nullptr, nullptr};  // dropped direction of the event that made cur
+  bool nrm2_exact = true;                 // nrm2[cur] exact (else apply vdrop[cur])
+  double* fact_small = nullptr;
+  double* fact_partial = nullptr;
+  double* fact_rows = nullptr;
+  double* fact_qv = nullptr;
   // coarse-step stream: the advance_signal Newton solve only depends on the
   // previous coarse state, so it runs concurrently with the reduced step
   adrom_ctx* fctx = nullptr;
@@ -129,6 +146,22 @@ namespace {
 
 adrom_model model_of(const adrom_session* s) { return s->cfg.model; }
 
+// the current basis as a factored view (W = null: phi[acur] itself)
+FactBasis basis_view(const adrom_session* s) {
+  return FactBasis{s->phi[s->acur], s->Qb, s->r, s->w_id ? 0 : s->kf,
+                   s->w_id ? nullptr : s->Wd[s->cur], s->N};
+}
+
+__global__ void row_norms_kernel(const double* __restrict__ phi, int64_t n, int r,
+                                 double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < r; ++c) s += phi[i * r + c] * phi[i * r + c];
+    out[i] = s;
+  }
+}
+
 int alloc_op(adrom_session* s, adrom_rom_op& op) {
   const int ns = s->cfg.n_s, nv = s->cfg.model.n_var, r = s->r;
   op.r = r;
@@ -154,16 +187,38 @@ int alloc_op(adrom_session* s, adrom_rom_op& op) {
 
 // sampling (driver.py:264-273) + closure + operator for basis `phi` into op
 int build_sampling_operator(adrom_session* s, const double* phi, adrom_rom_op& op,
-                            const double* y_corr, bool seeded = false) {
+                            const double* y_corr, bool seeded = false,
+                            const FactBasis* fb = nullptr, const double* nrmb = nullptr) {
   adrom_ctx* ctx = s->ctx;
   const adrom_model m = model_of(s);
   const int n_s = s->cfg.n_s;
   int st;
   int it = 0;
+  const int n_q = (s->cfg.sampling == 1) ? n_s - s->cfg.n_extra : n_s;  // QDEIM rows
+  if (fb && fb->W && n_q > s->r) {
+    // restarted QDEIM on a factored basis: materialise Phi into the spare
+    // anchor buffer and run the explicit path (unseeded)
+    st = fact_reanchor(ctx, *fb, s->phi[1 - s->acur], nullptr);
+    if (st) return st;
+    phi = s->phi[1 - s->acur];
+    fb = nullptr;
+    seeded = false;
+  }
+  // factored rows that stall the certification: materialise and rerun
+  auto qdeim = [&](int count) -> int {
+    int st2 = qdeim_pool_select(ctx, phi, s->N, s->r, count, op.idx, s->qd_ws, &it, seeded, fb, nrmb);
+    if (st2 != QDEIM_NEEDS_EXPLICIT) return st2;
+    st2 = fact_reanchor(ctx, *fb, s->phi[1 - s->acur], nullptr);
+    if (st2) return st2;
+    phi = s->phi[1 - s->acur];
+    fb = nullptr;
+    seeded = false;
+    return qdeim_pool_select(ctx, phi, s->N, s->r, count, op.idx, s->qd_ws, &it, false);
+  };
   if (s->cfg.sampling == 1) {
     const int n_base = n_s - s->cfg.n_extra;
     if (n_base > 0) {
-      st = qdeim_pool_select(ctx, phi, s->N, s->r, n_base, op.idx, s->qd_ws, &it, seeded);
+      st = qdeim(n_base);
       if (st) return st;
     }
     st = reset_flags(ctx);
@@ -171,7 +226,7 @@ int build_sampling_operator(adrom_session* s, const double* phi, adrom_rom_op& o
     st = fgs_extend(ctx, m, y_corr, s->cfg.feature, op.idx, n_base, s->cfg.n_extra, nullptr);
     if (st) return st;
   } else {
-    st = qdeim_pool_select(ctx, phi, s->N, s->r, n_s, op.idx, s->qd_ws, &it, seeded);
+    st = qdeim(n_s);
     if (st) return st;
     st = reset_flags(ctx);
     if (st) return st;
@@ -179,7 +234,7 @@ int build_sampling_operator(adrom_session* s, const double* phi, adrom_rom_op& o
   const int pr = prof_begin(ctx, PROBE_OPERATOR);
   st = plan_build(ctx, m, op, n_s, ctx->dflags);
   if (st) return st;
-  st = operator_fill(ctx, op, phi, s->q_ref, s->d, n_s, ctx->dflags);
+  st = operator_fill(ctx, op, phi, s->q_ref, s->d, n_s, ctx->dflags, fb, s->fact_rows);
   prof_end(ctx, pr);
   if (st) return st;
   int flags[16];
@@ -228,7 +283,12 @@ int rom_step(adrom_session* s) {
 int decode_state(adrom_session* s) {
   adrom_ctx* ctx = s->ctx;
   const int pr = prof_begin(ctx, PROBE_DECODE);
-  const int st = ts_decode(ctx, s->phi[s->cur], s->N, s->r, s->a, s->q_ref, s->d, s->q_tilde);
+  int st;
+  if (s->fact && !s->w_id)
+    st = fact_decode(ctx, basis_view(s), s->a, s->q_ref, s->d, s->q_tilde, s->fact_small,
+                     s->fact_partial);
+  else
+    st = ts_decode(ctx, s->phi[s->acur], s->N, s->r, s->a, s->q_ref, s->d, s->q_tilde);
   prof_end(ctx, pr);
   return st;
 }
@@ -262,6 +322,86 @@ int download_state(adrom_session* s, double* host_dst) {
 
 int drain_downloads(adrom_session* s) {
   if (s->cstream) ADROM_CK(s->ctx, cudaStreamSynchronize(s->cstream));
+  return ADROM_OK;
+}
+
+// the rest of an event on the factored basis (after the coarse step and
+// preprocess): no rotation — the residual becomes column kf of Qb and
+// W' = [[W, 0], [0, 1/||q||]] B; committed only if every stage succeeds
+int run_event_factored(adrom_session* s, adrom_event_record& ev, bool* decoded) {
+  adrom_ctx* ctx = s->ctx;
+  int st;
+  if (s->kf == FACT_KQ) {  // re-anchor: A = X W (same basis), exact row norms
+    st = fact_reanchor(ctx, basis_view(s), s->phi[1 - s->acur], s->nrm2[s->cur]);
+    if (st) return st;
+    s->acur = 1 - s->acur;
+    s->kf = 0;
+    s->w_id = true;
+    s->nrm2_exact = true;
+  }
+  const int nxt = 1 - s->cur;
+  const FactBasis b = basis_view(s);
+  FactEventArgs e{};
+  e.y = s->y_hat;
+  e.a = s->a;
+  e.q_ref = s->q_ref;
+  e.d = s->d;
+  e.q_tilde = s->q_tilde;
+  e.Qw = s->Qb;
+  e.qv = s->fact_qv;
+  e.sigma = s->sigma[s->cur];
+  e.G = s->gram[s->cur];
+  e.lam = s->cfg.lam;
+  e.partial = s->fact_partial;
+  e.small = s->fact_small;
+  e.W_out = s->Wd[nxt];
+  e.sigma_out = s->sigma[nxt];
+  e.G_out = s->gram[nxt];
+  double* a_new = s->rom_info + 16;
+  e.a_out = a_new;
+  e.stats = s->isvd_stats;
+  e.flag = ctx->dflags;
+  e.nrm2_inout = s->nrm2[s->cur];
+  e.vdrop_in = s->nrm2_exact ? nullptr : s->vdrop[s->cur];
+  e.vdrop_out = s->vdrop[nxt];
+  e.nrm2_out = s->nrm2[nxt];
+  qdeim_seed_buffers(s->qd_ws, s->N, &e.seed_res2, &e.seed_bnd2, &e.seed_ver);
+  st = reset_flags(ctx);
+  if (st) return st;
+  st = fact_isvd_event(ctx, b, e);
+  if (st) return st;
+  *decoded = true;
+  s->nrm2_exact = true;  // pass 1 made nrm2[cur] exact for the current basis
+  int flags[16];
+  ADROM_CK(ctx, cudaMemcpyAsync((char*)ctx->pinned + 512, s->isvd_stats, sizeof(double) * 8,
+                                cudaMemcpyDeviceToHost, ctx->stream));
+  st = read_flags(ctx, flags);
+  if (st) return st;
+  const double* hs = (const double*)((char*)ctx->pinned + 512);
+  if (flags[0] & 1) {
+    ev.error = ADROM_ERR_NONFINITE;
+    return ADROM_OK;
+  }
+  if (flags[0] & 8) {
+    ev.error = ADROM_ERR_NOCONV;
+    return ADROM_OK;
+  }
+  ev.residual_norm = hs[2];
+  const FactBasis b2{s->phi[s->acur], s->Qb, s->r, b.k + 1, s->Wd[nxt], s->N};
+  const int onx = 1 - s->opcur;
+  st = build_sampling_operator(s, nullptr, s->op[onx], s->y_corr, true, &b2, s->nrm2[nxt]);
+  if (st == ADROM_ERR_CUDA) return st;
+  if (st) {
+    ev.error = st;
+    return ADROM_OK;
+  }
+  ADROM_CK(ctx, cudaMemcpyAsync(s->a, a_new, sizeof(double) * s->r, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+  s->kf = b.k + 1;
+  s->w_id = false;
+  s->cur = nxt;
+  s->opcur = onx;
+  s->nrm2_exact = false;  // nrm2[cur] is the seed bound; vdrop[cur] corrects it
   return ADROM_OK;
 }
 
@@ -302,6 +442,7 @@ int run_event(adrom_session* s, adrom_event_record& ev, bool* decoded) {
                                                                    : ctx->num_sms * 8),
                       256, 0, ctx->stream>>>(s->y_corr, s->q_ref, s->d, s->N, s->y_hat);
   ADROM_LAUNCH_CK(ctx);
+  if (s->fact) return run_event_factored(s, ev, decoded);
   // iSVD into the spare buffers
   const int nxt = 1 - s->cur;
   const bool fused = rot_fusable(s->r, s->r);
@@ -357,6 +498,7 @@ int run_event(adrom_session* s, adrom_event_record& ev, bool* decoded) {
     if (st) return st;
   }
   s->cur = nxt;
+  s->acur = nxt;
   s->opcur = onx;
   return ADROM_OK;
 }
@@ -401,9 +543,30 @@ int adrom_session_create(adrom_ctx* ctx, const adrom_session_config* cfg, adrom_
   cudaMalloc(&s->qd_ws, qdeim_pool_workspace_bytes(N, r, cfg->n_s));
   s->allocs.push_back(s->qd_ws);
   s->enc_partial = s->alloc_d(rot_fuse_partial_doubles(ctx, r));
+  {
+    // factored basis: r in {32, 64} at scale (ADROM_FACTORED=0/1 overrides)
+    const char* ev = getenv("ADROM_FACTORED");
+    const bool shape_ok = (r == 32 || r == 64);
+    s->fact = shape_ok && (ev ? atoi(ev) != 0 : N >= (1 << 18));
+  }
+  if (s->fact) {
+    s->Qb = s->alloc_d((size_t)N * FACT_KQ);
+    for (int b = 0; b < 2; ++b) {
+      s->Wd[b] = s->alloc_d((size_t)(r + FACT_KQ + 1) * r);
+      s->nrm2[b] = s->alloc_d((size_t)N);
+      s->vdrop[b] = s->alloc_d((size_t)(r + FACT_KQ + 1));
+    }
+    s->fact_small = s->alloc_d(fact_small_doubles(r));
+    s->fact_partial = s->alloc_d(fact_partial_doubles(ctx, r));
+    s->fact_rows = s->alloc_d((size_t)(3 * cfg->n_s * cfg->model.n_var + cfg->n_s) * r);
+    s->fact_qv = s->alloc_d((size_t)N);
+    if (s->Qb) cudaMemsetAsync(s->Qb, 0, sizeof(double) * (size_t)N * FACT_KQ, ctx->stream);
+  }
   s->cap_steps = cfg->n_t > cfg->w_init ? cfg->n_t - cfg->w_init : 1;
   s->step_log = s->alloc_d((size_t)s->cap_steps * 3);
   s->fail_step = s->alloc_t<int>(1);
+  if (s->fact && (!s->Qb || !s->nrm2[1] || !s->fact_rows || !s->fact_partial || !s->fact_qv))
+    st = set_error(ctx, ADROM_ERR_CUDA, "session: device allocation failed (factored basis)");
   if (st || !s->phi[1] || !s->step_log || !s->fail_step || !s->qd_ws || !s->isvd_ws) {
     for (void* p : s->allocs) cudaFree(p);
     delete s;
@@ -470,8 +633,18 @@ int adrom_session_load(adrom_session* s, const double* q_ref, const double* d, c
                                 ctx->stream));
   ADROM_CK(ctx, cudaMemcpyAsync(s->y_corr, q_last, 8 * N, cudaMemcpyDeviceToDevice, ctx->stream));
   s->cur = 0;
+  s->acur = 0;
+  s->kf = 0;
+  s->w_id = true;
+  s->nrm2_exact = true;
   s->opcur = 0;
   s->n_online = 0;
+  if (s->fact) {
+    int64_t g = (s->N + 255) / 256;
+    if (g > (int64_t)ctx->num_sms * 8) g = (int64_t)ctx->num_sms * 8;
+    row_norms_kernel<<<(int)g, 256, 0, ctx->stream>>>(s->phi[0], s->N, s->r, s->nrm2[0]);
+    ADROM_LAUNCH_CK(ctx);
+  }
   s->events.clear();
   ADROM_CK(ctx, cudaMemsetAsync(s->fail_step, 0xff, sizeof(int), ctx->stream));
   return ADROM_OK;
@@ -491,9 +664,9 @@ int adrom_session_start(adrom_session* s) {
     if (st) return st;
     std::swap(s->y_corr, s->y_next);
   }
-  int st = build_sampling_operator(s, s->phi[s->cur], s->op[s->opcur], s->y_corr);
+  int st = build_sampling_operator(s, s->phi[s->acur], s->op[s->opcur], s->y_corr);
   if (st) return st;
-  return encode_into(s, s->phi[s->cur], s->q_tilde, s->a);
+  return encode_into(s, s->phi[s->acur], s->q_tilde, s->a);
 }
 
 // Advance n_steps online steps (driver.py:337-387).  For saved steps (every
@@ -581,7 +754,11 @@ int adrom_session_read(adrom_session* s, double* host_step_log, int64_t max_step
   if (dev_a)
     ADROM_CK(ctx, cudaMemcpyAsync(dev_a, s->a, 8 * s->r, cudaMemcpyDeviceToDevice, ctx->stream));
   if (dev_phi)
-    ADROM_CK(ctx, cudaMemcpyAsync(dev_phi, s->phi[s->cur], 8 * (size_t)s->N * s->r,
+    if (s->fact && !s->w_id) {
+      int st = fact_reanchor(ctx, basis_view(s), dev_phi, nullptr);
+      if (st) return st;
+    } else
+    ADROM_CK(ctx, cudaMemcpyAsync(dev_phi, s->phi[s->acur], 8 * (size_t)s->N * s->r,
                                   cudaMemcpyDeviceToDevice, ctx->stream));
   if (dev_sigma)
     ADROM_CK(ctx, cudaMemcpyAsync(dev_sigma, s->sigma[s->cur], 8 * s->r, cudaMemcpyDeviceToDevice,
