@@ -431,13 +431,16 @@ def bench_rom(args, rank, world):
     value = world * K / (ms * 1e-3)
     per = {k: (v[0] / max(v[1], 1), v[1]) for k, v in probes.items()}
     share = {k: round(v[0] / ms, 4) for k, v in probes.items()}
-    # Roofline of the dominant single kernel: the iSVD rotation
-    # Phi' = [Phi | q_hat] B (rot_tc_kernel, FP64 DMMA; its epilogue also
-    # produces the state transfer and the QDEIM seed bounds).  Algorithmic
-    # work per launch: 2 N r (r+1) flops; bytes 8(2Nr + N) + 8*7N (fused
-    # encode reads d, q~, q_ref; seed writes res2, bnd2 and 1 B of version).
-    # QDEIM is larger in total but is a sequence of rounds of small kernels
-    # (qdeim_rounds_per_step below).
+    # Roofline.  Explicit basis (r not in {32, 64} or small N): the iSVD
+    # rotation Phi' = [Phi | q_hat] B (rot_tc_kernel, FP64 DMMA), 2 N r (r+1)
+    # flop.  Factored basis (csrc/factored.cu, the cfg-3 path): no rotation;
+    # the largest single kernel is the first basis pass (xpass MODE 1: X^T y,
+    # fused decode, exact row norms), HBM bound with algorithmic bytes
+    # 8 N (r + k + 6): A, the k active residual columns, y, q_ref, d, the
+    # norm read + write and the decoded state.  k cycles 0..15 between
+    # re-anchors (one event per step here); the mean over the timed events is
+    # used.  QDEIM is larger in total but is a sequence of rounds of small
+    # kernels (qdeim_rounds_per_step below).
     roof = None
     if "isvd_rotate" in per:
         rot_ms = per["isvd_rotate"][0]
@@ -452,8 +455,18 @@ def bench_rom(args, rank, world):
                 "hbm_achieved_gbs": round(rbytes / (rot_ms * 1e-3) / 1e9, 1),
                 "hbm_frac": round(rbytes / (rot_ms * 1e-3) / 1e9 / HBM_PEAK, 4),
                 "share_of_step": round(probes["isvd_rotate"][0] / ms, 4)}
+    elif "isvd_project" in per:
+        kq = 16
+        k_mean = float(np.mean([(j % kq) for j in range(W, W + K)])) if case.z == 1 else 0.0
+        xbytes = 8.0 * N * (r + k_mean + 6)
+        roof = roofline(xbytes, per["isvd_project"][0],
+                        ncu_traffic("xpass_kernel<64, 1>", case.name))
+        roof.update({"kernel": "isvd_project (xpass_kernel<64,1>: X^T y + fused decode + row norms)",
+                     "work_per_launch": {"bytes": xbytes, "k_mean": k_mean},
+                     "share_of_step": round(probes["isvd_project"][0] / ms, 4)})
     isvd_keys = ("isvd_project", "isvd_resid", "isvd_core", "isvd_rotate")
-    isvd_ms = sum(probes.get(k, (0, 0))[0] for k in isvd_keys) / max(probes.get("isvd_rotate", (0, 1))[1], 1)
+    n_upd = max(probes.get("isvd_project", (0, 1))[1], 1)
+    isvd_ms = sum(probes.get(k, (0, 0))[0] for k in isvd_keys) / n_upd
     canon = 8.0 * (3 * N * r + 2 * N)
     fres = per.get("fom_residual")
     line = {
@@ -472,7 +485,11 @@ def bench_rom(args, rank, world):
         "gpu_launches": launches,
         "fom_residual_gcells": round(model.n_elem / (fres[0] * 1e-3) / 1e9, 2) if fres else None,
         "isvd_update_ms": round(isvd_ms, 4),
+        # canonical bytes of one update (2 reads + 1 write of Phi) over the
+        # measured update time; the factored basis skips the write, so this
+        # "fraction of the canonical roofline" can approach or pass 1
         "isvd_update_hbm_frac": round(canon / (isvd_ms * 1e-3) / 1e9 / HBM_PEAK, 4) if isvd_ms else None,
+        "isvd_basis": "factored" if "isvd_rotate" not in per else "explicit",
         "probes_ms_per_launch": {k: round(v[0], 4) for k, v in per.items()},
         "probes_launches": {k: v[1] for k, v in per.items()},
         "share_of_step": share,

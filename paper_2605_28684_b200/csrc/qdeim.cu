@@ -46,6 +46,17 @@ static long long qp_refresh_factor() {
   return t;
 }
 
+// refresh-set capacity over its target, in percent (the selection stops once
+// the rows sharing the selected bound prefix fit); ADROM_QDEIM_CAPF overrides
+static long long qp_refresh_slack() {
+  static long long t = [] {
+    const char* e = getenv("ADROM_QDEIM_CAPF");
+    const long long v = e ? atoll(e) : -1;
+    return (v >= 1 && v <= 1000) ? v : 25ll;
+  }();
+  return t;
+}
+
 static long long qp_pool_m() {
   static long long t = [] {
     const char* e = getenv("ADROM_QDEIM_POOL_M");
@@ -1089,7 +1100,8 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
       if (gg > ctx->num_sms * 8) gg = ctx->num_sms * 8;
       if (!fresh && !all) {
         // refresh the mref rows with the largest (possibly stale) bounds
-        const long long cap = (2 * mref < n) ? 2 * mref : n;
+        const long long capm = mref + (mref * qp_refresh_slack()) / 100;
+        const long long cap = (capm < n) ? capm : n;
         st = select(selR, nullptr, n, mref, cap);
         if (st) return st;
         int64_t fg = (cap + 255) / 256;
