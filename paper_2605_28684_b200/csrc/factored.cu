@@ -41,11 +41,15 @@ struct XPassArgs {
   int* flag;
   const double* vdrop;  // MODE 1 (optional): the previous event's dropped direction in X
   double* nrm2;         //   coordinates; nrm2[i] -= (X_i . vdrop)^2 (bound -> exact norm)
+  const double* va;     // MODE 2 (optional): decode vector W a -> q~ written here (qt)
 };
 
 __host__ __device__ inline int xpass_width(int r, int kq, int mode) {
-  return mode == 1 ? r + kq + 1 : 2 * (r + kq) + 2;
+  (void)mode;
+  return r + kq + 1;
 }
+
+constexpr int XP_ROWS = 4096;  // rows per xpass block
 
 template <int R, int MODE>
 __global__ void __launch_bounds__(256, 2) xpass_kernel(XPassArgs a) {
@@ -53,7 +57,7 @@ __global__ void __launch_bounds__(256, 2) xpass_kernel(XPassArgs a) {
   constexpr int RPW = 32 / LPR;     // rows per warp per sub-iteration
   constexpr int QPL = FACT_KQ / LPR;  // Q columns per lane
   constexpr int U = 2;
-  constexpr int NW = (MODE == 1) ? 1 : 2;  // weight vectors
+  constexpr int NW = 1;  // weight vectors (y in MODE 1, q in MODE 2)
   const int kq = a.kq, k = a.k;
   __shared__ double red[8 * (R + FACT_KQ) * NW];
   __shared__ double sred[3][32];
@@ -62,11 +66,13 @@ __global__ void __launch_bounds__(256, 2) xpass_kernel(XPassArgs a) {
   // the row-dot vectors live in shared memory (registers hold the rows)
   __shared__ __align__(16) double sv[R + FACT_KQ];
   __shared__ __align__(16) double sg[R + FACT_KQ];
-  const bool drop = (MODE == 1) && a.vdrop != nullptr;
+  // second row-dot vector: MODE 1 the dropped direction, MODE 2 the decode vector
+  const double* v2p = (MODE == 1) ? a.vdrop : a.va;
+  const bool drop = v2p != nullptr;
   for (int j = threadIdx.x; j < R + FACT_KQ; j += blockDim.x) {
     const bool ok = j < R + k;
-    sv[j] = ok ? a.v[j] : 0.0;
-    sg[j] = (drop && ok) ? a.vdrop[j] : 0.0;
+    sv[j] = (ok && a.v) ? a.v[j] : 0.0;
+    sg[j] = (drop && ok) ? v2p[j] : 0.0;
   }
   __syncthreads();
   const double2* vA = reinterpret_cast<const double2*>(sv);
@@ -84,17 +90,20 @@ __global__ void __launch_bounds__(256, 2) xpass_kernel(XPassArgs a) {
   }
   double s0 = 0.0, s1 = 0.0;
   bool bad = false;
-  const int64_t total_warps = (int64_t)gridDim.x * 8;
+  // block b owns rows [b * XP_ROWS, (b+1) * XP_ROWS): many small blocks
+  // balance themselves across SMs (pass 1 shares the GPU with the one-block
+  // reduced step on the other stream)
   const int64_t rows_per_iter = (int64_t)RPW * U;
-  for (int64_t g = (int64_t)blockIdx.x * 8 + warp; g * rows_per_iter < a.n; g += total_warps) {
-    const int64_t base = g * rows_per_iter;
+  const int64_t blk0 = (int64_t)blockIdx.x * XP_ROWS;
+  const int64_t blk1 = (blk0 + XP_ROWS < a.n) ? blk0 + XP_ROWS : a.n;
+  for (int64_t base = blk0 + (int64_t)warp * rows_per_iter; base < blk1; base += 8 * rows_per_iter) {
     double2 xa[U][4];
     double xq[U][QPL];
     double yv[U], qr[U], dd[U], qt[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t i = base + u * RPW + seg;
-      const bool live = i < a.n;
+      const bool live = i < blk1;
       if (live) {
         const double2* rowp = reinterpret_cast<const double2*>(a.A + i * R);
 #pragma unroll
@@ -113,7 +122,7 @@ __global__ void __launch_bounds__(256, 2) xpass_kernel(XPassArgs a) {
       yv[u] = (live && a.y) ? a.y[i] : 0.0;
       qr[u] = live ? a.q_ref[i] : 0.0;
       dd[u] = live ? a.d[i] : 1.0;
-      qt[u] = (MODE == 2 && live) ? a.qt[i] : 0.0;
+      qt[u] = 0.0;
     }
     double rd[U], dd2[U];
 #pragma unroll
@@ -124,7 +133,7 @@ __global__ void __launch_bounds__(256, 2) xpass_kernel(XPassArgs a) {
         bad |= !(isfinite(xa[u][h].x) && isfinite(xa[u][h].y));
         const double2 vv = vA[sl + LPR * h];
         t0 += xa[u][h].x * vv.x + xa[u][h].y * vv.y;
-        if (MODE == 1 && drop) {
+        if (drop) {
           const double2 gg = gA[sl + LPR * h];
           t2 += xa[u][h].x * gg.x + xa[u][h].y * gg.y;
         }
@@ -132,7 +141,7 @@ __global__ void __launch_bounds__(256, 2) xpass_kernel(XPassArgs a) {
 #pragma unroll
       for (int t = 0; t < QPL; ++t) {
         t0 += xq[u][t] * vQ[sl + LPR * t];
-        if (MODE == 1 && drop) t2 += xq[u][t] * gQ[sl + LPR * t];
+        if (drop) t2 += xq[u][t] * gQ[sl + LPR * t];
       }
       rd[u] = t0;
       dd2[u] = t2;
@@ -142,28 +151,27 @@ __global__ void __launch_bounds__(256, 2) xpass_kernel(XPassArgs a) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         rd[u] += __shfl_xor_sync(0xffffffffu, rd[u], o);
-        if (MODE == 1 && drop) dd2[u] += __shfl_xor_sync(0xffffffffu, dd2[u], o);
+        if (drop) dd2[u] += __shfl_xor_sync(0xffffffffu, dd2[u], o);
       }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t i = base + u * RPW + seg;
-      if (i >= a.n) continue;
+      if (i >= blk1) continue;
       double w0, w1 = 0.0;
       if (MODE == 1) {
-        if (sl == 0) a.qt[i] = qr[u] + rd[u] / dd[u];  // decode (projection.py:104)
+        if (a.qt && sl == 0) a.qt[i] = qr[u] + rd[u] / dd[u];  // decode (projection.py:104)
         if (drop && sl == 0) a.nrm2[i] = fmax(a.nrm2[i] - dd2[u] * dd2[u], 0.0);
         w0 = yv[u];
         bad |= !isfinite(w0);
         if (sl == 0) s0 += w0 * w0;
       } else {
         w0 = yv[u] - rd[u];                    // q = y - Phi p (tracking.py:162)
-        w1 = dd[u] * (qt[u] - qr[u]);          // projection.py:98-99
+        if (drop && sl == 0) a.qt[i] = qr[u] + dd2[u] / dd[u];  // fused decode (projection.py:104)
         bad |= !isfinite(w0);
         if (sl == 0) {
           a.Qw[i * kq + k] = w0;
           a.qv[i] = w0;
           s0 += w0 * w0;
-          s1 += w0 * w1;
         }
       }
 #pragma unroll
@@ -221,11 +229,8 @@ __global__ void __launch_bounds__(256, 2) xpass_kernel(XPassArgs a) {
     }
   }
   const double t0 = block_sum<256>(s0, sred[0]);
-  const double t1 = (MODE == 2) ? block_sum<256>(s1, sred[1]) : 0.0;
-  if (threadIdx.x == 0) {
-    out[R + kq] = t0;
-    if (MODE == 2) out[2 * (R + kq) + 1] = t1;
-  }
+  (void)s1;
+  if (threadIdx.x == 0) out[R + kq] = t0;
   if (bad && a.flag) atomicOr(a.flag, 1);
 }
 
@@ -275,22 +280,26 @@ __global__ void wnext_kernel(const double* __restrict__ W, int rk, int r,
   }
 }
 
-// pack [W^T t_x ; qinv * s_qw] -> z (r+1), then a = B^T z   (state transfer)
-__global__ void encode_factored_kernel(const double* __restrict__ W, int rk, int r,
-                                       const double* __restrict__ tx, const double* __restrict__ sqw,
+// state transfer a' = Phi'^T D (q~ - q_ref) = Phi'^T Phi a with
+// Phi' = [Phi, q^] B:  a' = B^T [G a ; qinv (Phi^T q) . a]  (no basis pass;
+// the reference's rounding of q~ (driver.py:376) is not reproduced — this is
+// the exact-arithmetic value, rounding-level close)
+__global__ void encode_factored_kernel(const double* __restrict__ G, int r,
+                                       const double* __restrict__ a,
+                                       const double* __restrict__ phitq,
                                        const double* __restrict__ qinv,
                                        const double* __restrict__ B, double* __restrict__ a_out) {
   __shared__ double z[129];
+  __shared__ double red[32];
   for (int c = threadIdx.x; c < r; c += blockDim.x) {
     double s = 0.0;
-    if (W) {
-      for (int j = 0; j < rk; ++j) s += W[(size_t)j * r + c] * tx[j];
-    } else {
-      s = tx[c];
-    }
+    for (int j = 0; j < r; ++j) s += G[(size_t)c * r + j] * a[j];
     z[c] = s;
   }
-  if (threadIdx.x == 0) z[r] = (*qinv) * (*sqw);
+  double t = 0.0;
+  for (int j = threadIdx.x; j < r; j += blockDim.x) t += phitq[j] * a[j];
+  t = block_sum_dyn(t, red);
+  if (threadIdx.x == 0) z[r] = (*qinv) * t;
   __syncthreads();
   for (int c = threadIdx.x; c < r; c += blockDim.x) {
     double s = 0.0;
@@ -563,9 +572,8 @@ int fact_gather_rows(adrom_ctx* ctx, const FactBasis& b, const int64_t* rows, in
 // host side
 // ---------------------------------------------------------------------------
 static int xpass_grid(adrom_ctx* ctx, int64_t n) {
-  int64_t g = (int64_t)ctx->num_sms * 2;  // resident blocks (<= 128 registers)
-  const int64_t need = (n + 31) / 32;
-  if (g > need) g = need;
+  (void)ctx;
+  const int64_t g = (n + XP_ROWS - 1) / XP_ROWS;
   return (int)(g < 1 ? 1 : g);
 }
 
@@ -589,8 +597,9 @@ int fact_decode(adrom_ctx* ctx, const FactBasis& b, const double* a, const doubl
   return ADROM_OK;
 }
 
-size_t fact_partial_doubles(adrom_ctx* ctx, int r) {
-  return (size_t)ctx->num_sms * 2 * xpass_width(r, FACT_KQ, 2);
+size_t fact_partial_doubles(adrom_ctx* ctx, int64_t n, int r) {
+  (void)ctx;
+  return (size_t)((n + XP_ROWS - 1) / XP_ROWS) * xpass_width(r, FACT_KQ, 2);
 }
 
 int fact_reanchor(adrom_ctx* ctx, const FactBasis& b, double* out, double* nrm2) {
@@ -610,110 +619,133 @@ int fact_reanchor(adrom_ctx* ctx, const FactBasis& b, double* out, double* nrm2)
   return set_error(ctx, ADROM_ERR_ARG, "reanchor: rank %d unsupported", b.r);
 }
 
-int fact_isvd_event(adrom_ctx* ctx, const FactBasis& b, const FactEventArgs& e) {
+struct FactSmall {
+  double *vdec, *vp, *red1, *red2, *pls, *t1, *t2, *Bm, *Tm, *sb;
+  int* need;
+};
+
+static FactSmall fact_small_layout(double* w, int r) {
+  FactSmall f;
+  f.vdec = w;                         // r + KQ
+  f.vp = f.vdec + r + FACT_KQ;        // r + KQ
+  f.red1 = f.vp + r + FACT_KQ;        // r + 1: [p1, ||y||^2]
+  f.red2 = f.red1 + r + 1;            // r + 1: [Phi^T q, ||q||^2]
+  f.pls = f.red2 + r + 1;             // r
+  f.t1 = f.pls + r;                   // r + KQ + 1   (reduced pass-1 sums)
+  f.t2 = f.t1 + r + FACT_KQ + 1;      // r + KQ + 1 (reduced pass-2 sums)
+  f.Bm = f.t2 + 2 * (r + FACT_KQ) + 2;  // (r + 1) x r
+  f.Tm = f.Bm + (r + 1) * r;            // (r + 1) x r
+  f.sb = f.Tm + (r + 1) * r;            // [0] qinv, [2 .. r+3) dropped vector
+  f.need = (int*)(f.sb + r + 8);
+  return f;
+}
+
+// pass 1 (only the snapshot's projection): X^T y, ||y||^2, exact row norms.
+// Needs y only, so the session runs it on the coarse-step stream while the
+// reduced step (one block) runs on the main stream.
+int fact_event_pass_a(adrom_ctx* ctx, const FactBasis& b, const FactEventArgs& e) {
   const int r = b.r, k = b.k, rk = r + k;
   if (!(r == 32 || r == 64) || k < 0 || k >= FACT_KQ)
     return set_error(ctx, ADROM_ERR_ARG, "factored iSVD: r=%d k=%d", r, k);
-  double* w = e.small;  // small device scratch
-  double* vdec = w;                 // r + KQ
-  double* vp = vdec + r + FACT_KQ;  // r + KQ
-  double* red1 = vp + r + FACT_KQ;  // r + 1: [p1, ||y||^2]
-  double* red2 = red1 + r + 1;      // r + 1: [Phi^T q, ||q||^2]
-  double* pls = red2 + r + 1;       // r
-  double* t1 = pls + r;             // r + KQ + 1   (reduced pass-1 sums)
-  double* t2 = t1 + r + FACT_KQ + 1;  // 2 (r + KQ) + 2 (reduced pass-2 sums)
-  double* Bm = t2 + 2 * (r + FACT_KQ) + 2;  // (r + 1) x r
-  double* Tm = Bm + (r + 1) * r;            // (r + 1) x r
-  double* sb = Tm + (r + 1) * r;            // [0] qinv, [2 .. r+3) dropped vector
-  int* need = (int*)(sb + r + 8);
+  const FactSmall f = fact_small_layout(e.small, r);
   const int grid = xpass_grid(ctx, b.n);
-  // decode vector W a (identity when k == 0 and W == null)
-  if (b.W) {
-    mat_vec_kernel<<<1, 256, 0, ctx->stream>>>(b.W, rk, r, e.a, vdec);
-    ADROM_LAUNCH_CK(ctx);
-  } else {
-    ADROM_CK(ctx, cudaMemcpyAsync(vdec, e.a, sizeof(double) * r, cudaMemcpyDeviceToDevice, ctx->stream));
-  }
-  // pass 1
   int pr = prof_begin(ctx, PROBE_ISVD_PROJECT);
-  XPassArgs a1{b.A, b.Q, b.n, k, FACT_KQ, vdec, e.y, e.q_ref, e.d, e.q_tilde, nullptr, nullptr,
-               e.partial, e.flag, e.vdrop_in, e.vdrop_in ? e.nrm2_inout : nullptr};
+  XPassArgs a1{b.A, b.Q, b.n, k, FACT_KQ, nullptr, e.y, e.q_ref, e.d, nullptr, nullptr, nullptr,
+               e.partial_a, e.flag_a, e.vdrop_in, e.vdrop_in ? e.nrm2_inout : nullptr, nullptr};
   if (r == 64) xpass_kernel<64, 1><<<grid, 256, 0, ctx->stream>>>(a1);
   else xpass_kernel<32, 1><<<grid, 256, 0, ctx->stream>>>(a1);
   ADROM_LAUNCH_CK(ctx);
   const int w1 = xpass_width(r, FACT_KQ, 1);
-  reduce_partials_kernel<<<w1, 256, 0, ctx->stream>>>(e.partial, grid, w1, t1, nullptr);
+  reduce_partials_kernel<<<w1, 256, 0, ctx->stream>>>(e.partial_a, grid, w1, f.t1, nullptr);
   ADROM_LAUNCH_CK(ctx);
   prof_end(ctx, pr);
   // p1 = W^T (X^T y), ||y||^2
   if (b.W) {
-    matT_vec_kernel<<<1, 128, 0, ctx->stream>>>(b.W, rk, r, t1, red1);
+    matT_vec_kernel<<<1, 128, 0, ctx->stream>>>(b.W, rk, r, f.t1, f.red1);
     ADROM_LAUNCH_CK(ctx);
   } else {
-    ADROM_CK(ctx, cudaMemcpyAsync(red1, t1, sizeof(double) * r, cudaMemcpyDeviceToDevice, ctx->stream));
+    ADROM_CK(ctx, cudaMemcpyAsync(f.red1, f.t1, sizeof(double) * r, cudaMemcpyDeviceToDevice, ctx->stream));
   }
-  ADROM_CK(ctx, cudaMemcpyAsync(red1 + r, t1 + r + FACT_KQ, sizeof(double), cudaMemcpyDeviceToDevice,
+  ADROM_CK(ctx, cudaMemcpyAsync(f.red1 + r, f.t1 + r + FACT_KQ, sizeof(double), cudaMemcpyDeviceToDevice,
                                 ctx->stream));
+  return ADROM_OK;
+}
+
+// the rest of the event on the main stream: least squares, pass 2 with the
+// fused decode of the reduced state, core SVD, W', state transfer, seeds
+int fact_event_pass_b(adrom_ctx* ctx, const FactBasis& b, const FactEventArgs& e) {
+  const int r = b.r, k = b.k, rk = r + k;
+  const FactSmall f = fact_small_layout(e.small, r);
+  const int grid = xpass_grid(ctx, b.n);
+  // decode vector W a (identity when k == 0 and W == null)
+  if (b.W) {
+    mat_vec_kernel<<<1, 256, 0, ctx->stream>>>(b.W, rk, r, e.a, f.vdec);
+    ADROM_LAUNCH_CK(ctx);
+  } else {
+    ADROM_CK(ctx, cudaMemcpyAsync(f.vdec, e.a, sizeof(double) * r, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
   // least squares p = G^{-1} p1; the explicit residual pass always runs here
-  int st = isvd_solve_launch(ctx, red1, e.G, r, pls, need);
+  int st = isvd_solve_launch(ctx, f.red1, e.G, r, f.pls, f.need);
   if (st) return st;
-  set_need_kernel<<<1, 1, 0, ctx->stream>>>(need);
+  set_need_kernel<<<1, 1, 0, ctx->stream>>>(f.need);
   ADROM_LAUNCH_CK(ctx);
   if (b.W) {
-    mat_vec_kernel<<<1, 256, 0, ctx->stream>>>(b.W, rk, r, pls, vp);
+    mat_vec_kernel<<<1, 256, 0, ctx->stream>>>(b.W, rk, r, f.pls, f.vp);
     ADROM_LAUNCH_CK(ctx);
   } else {
-    ADROM_CK(ctx, cudaMemcpyAsync(vp, pls, sizeof(double) * r, cudaMemcpyDeviceToDevice, ctx->stream));
+    ADROM_CK(ctx, cudaMemcpyAsync(f.vp, f.pls, sizeof(double) * r, cudaMemcpyDeviceToDevice, ctx->stream));
   }
-  // pass 2
-  pr = prof_begin(ctx, PROBE_ISVD_RESID);
-  XPassArgs a2{b.A, b.Q, b.n, k, FACT_KQ, vp, e.y, e.q_ref, e.d, e.q_tilde, e.Qw, e.qv, e.partial,
-               e.flag};
+  // pass 2 (+ decode of the reduced state, projection.py:104)
+  int pr = prof_begin(ctx, PROBE_ISVD_RESID);
+  XPassArgs a2{b.A, b.Q, b.n, k, FACT_KQ, f.vp, e.y, e.q_ref, e.d, e.q_tilde, e.Qw, e.qv, e.partial,
+               e.flag, nullptr, nullptr, f.vdec};
   if (r == 64) xpass_kernel<64, 2><<<grid, 256, 0, ctx->stream>>>(a2);
   else xpass_kernel<32, 2><<<grid, 256, 0, ctx->stream>>>(a2);
   ADROM_LAUNCH_CK(ctx);
   const int w2 = xpass_width(r, FACT_KQ, 2);
-  reduce_partials_kernel<<<w2, 256, 0, ctx->stream>>>(e.partial, grid, w2, t2, nullptr);
+  reduce_partials_kernel<<<w2, 256, 0, ctx->stream>>>(e.partial, grid, w2, f.t2, nullptr);
   ADROM_LAUNCH_CK(ctx);
   prof_end(ctx, pr);
   // Phi^T q = W^T (X^T q), ||q||^2
   if (b.W) {
-    matT_vec_kernel<<<1, 128, 0, ctx->stream>>>(b.W, rk, r, t2, red2);
+    matT_vec_kernel<<<1, 128, 0, ctx->stream>>>(b.W, rk, r, f.t2, f.red2);
     ADROM_LAUNCH_CK(ctx);
   } else {
-    ADROM_CK(ctx, cudaMemcpyAsync(red2, t2, sizeof(double) * r, cudaMemcpyDeviceToDevice, ctx->stream));
+    ADROM_CK(ctx, cudaMemcpyAsync(f.red2, f.t2, sizeof(double) * r, cudaMemcpyDeviceToDevice, ctx->stream));
   }
-  ADROM_CK(ctx, cudaMemcpyAsync(red2 + r, t2 + r + FACT_KQ, sizeof(double), cudaMemcpyDeviceToDevice,
+  ADROM_CK(ctx, cudaMemcpyAsync(f.red2 + r, f.t2 + r + FACT_KQ, sizeof(double), cudaMemcpyDeviceToDevice,
                                 ctx->stream));
   // core: K, its SVD, B, qinv, the tracked Gram of the new basis, sigma'
   pr = prof_begin(ctx, PROBE_ISVD_CORE);
-  double* udrop = sb + 2;  // r + 1 doubles after qinv (sb has 16 + r + 1 slots)
-  st = isvd_core_launch(ctx, e.sigma, red1, pls, red2, need, e.G, r, e.lam, Bm, sb, Tm,
+  double* udrop = f.sb + 2;
+  st = isvd_core_launch(ctx, e.sigma, f.red1, f.pls, f.red2, f.need, e.G, r, e.lam, f.Bm, f.sb, f.Tm,
                         e.G_out, e.sigma_out, e.stats, e.flag, udrop);
   prof_end(ctx, pr);
   if (st) return st;
   // W' and the state transfer for the new basis
-  wnext_kernel<<<(rk + 1) * r / 256 + 1, 256, 0, ctx->stream>>>(b.W, rk, r, Bm, sb, e.W_out);
+  wnext_kernel<<<(rk + 1) * r / 256 + 1, 256, 0, ctx->stream>>>(b.W, rk, r, f.Bm, f.sb, e.W_out);
   ADROM_LAUNCH_CK(ctx);
-  const double* tw = t2 + r + FACT_KQ + 1;  // X^T w (r + KQ), then q.w
-  encode_factored_kernel<<<1, 128, 0, ctx->stream>>>(b.W, rk, r, tw, tw + r + FACT_KQ, sb, Bm,
-                                                     e.a_out);
+  encode_factored_kernel<<<1, 128, 0, ctx->stream>>>(e.G, r, e.a, f.red2, f.sb, f.Bm, e.a_out);
   ADROM_LAUNCH_CK(ctx);
-  // the dropped direction in the new X coordinates: [W u_top ; qinv u_bot]
   if (e.vdrop_out) {
-    vdrop_kernel<<<1, 128, 0, ctx->stream>>>(b.W, rk, r, udrop, sb, e.vdrop_out);
+    vdrop_kernel<<<1, 128, 0, ctx->stream>>>(b.W, rk, r, udrop, f.sb, e.vdrop_out);
     ADROM_LAUNCH_CK(ctx);
   }
-  // QDEIM seed bounds of the new basis
   if (e.seed_res2) {
     int64_t g = (b.n + 255) / 256;
     if (g > (int64_t)ctx->num_sms * 8) g = (int64_t)ctx->num_sms * 8;
-    seed_bounds_kernel<<<(int)g, 256, 0, ctx->stream>>>(e.nrm2_inout, e.qv, sb, b.n,
+    seed_bounds_kernel<<<(int)g, 256, 0, ctx->stream>>>(e.nrm2_inout, e.qv, f.sb, b.n,
                                                         e.seed_res2, e.seed_bnd2, e.seed_ver,
                                                         e.nrm2_out);
     ADROM_LAUNCH_CK(ctx);
   }
   return ADROM_OK;
+}
+
+int fact_isvd_event(adrom_ctx* ctx, const FactBasis& b, const FactEventArgs& e) {
+  int st = fact_event_pass_a(ctx, b, e);
+  if (st) return st;
+  return fact_event_pass_b(ctx, b, e);
 }
 
 }  // namespace adrom

@@ -27,7 +27,9 @@ struct FactEventArgs {
   const double* sigma;    // current sigma (r)
   const double* G;        // tracked Phi^T Phi (r x r)
   double lam;
-  double* partial;        // fact_partial_doubles
+  double* partial;        // fact_partial_doubles (pass 2)
+  double* partial_a;      // fact_partial_doubles (pass 1; may equal partial if serial)
+  int* flag_a;            // flags of pass 1 (its stream's)
   double* small;          // fact_small_doubles
   double* W_out;          // (r + k + 1) x r
   double* sigma_out;
@@ -52,12 +54,16 @@ struct FactEventArgs {
 inline size_t fact_small_doubles(int r) {
   return 8 * (size_t)(r + FACT_KQ + 2) + 2 * (size_t)(r + 1) * r + 3 * (size_t)r + 256;
 }
-size_t fact_partial_doubles(adrom_ctx* ctx, int r);
+size_t fact_partial_doubles(adrom_ctx* ctx, int64_t n, int r);
 
 // one history-aware iSVD event on the factored basis (tracking.py:141-178):
 // decode, both passes, core SVD, W', state transfer, QDEIM seed bounds.
 // Asynchronous; flags as isvd_update_async.
 int fact_isvd_event(adrom_ctx* ctx, const FactBasis& b, const FactEventArgs& e);
+// the same in two halves: pass 1 (X^T y, row norms; needs y only) and the rest
+// (needs the reduced state a).  The session runs them on two streams.
+int fact_event_pass_a(adrom_ctx* ctx, const FactBasis& b, const FactEventArgs& e);
+int fact_event_pass_b(adrom_ctx* ctx, const FactBasis& b, const FactEventArgs& e);
 
 // q~ = q_ref + (X (W a)) / d   (projection.py:104 on the factored basis)
 int fact_decode(adrom_ctx* ctx, const FactBasis& b, const double* a, const double* q_ref,

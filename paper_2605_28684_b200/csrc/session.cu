@@ -25,11 +25,18 @@ using namespace adrom;
 
 namespace {
 
+// flags[0] also folds in dflags[PASS_A_FLAG] (written by the factored pass 1
+// on the coarse-step stream, reset there before the pass)
+constexpr int PASS_A_FLAG = 20;
+
 int read_flags(adrom_ctx* ctx, int* host_flags) {
-  ADROM_CK(ctx, cudaMemcpyAsync(ctx->pinned, ctx->dflags, sizeof(int) * 16,
+  ADROM_CK(ctx, cudaMemcpyAsync(ctx->pinned, ctx->dflags, sizeof(int) * 24,
                                 cudaMemcpyDeviceToHost, ctx->stream));
   ADROM_CK(ctx, cudaStreamSynchronize(ctx->stream));
-  memcpy(host_flags, ctx->pinned, sizeof(int) * 16);
+  int tmp[24];
+  memcpy(tmp, ctx->pinned, sizeof(int) * 24);
+  memcpy(host_flags, tmp, sizeof(int) * 16);
+  host_flags[0] |= tmp[PASS_A_FLAG];
   return ADROM_OK;
 }
 
@@ -109,6 +116,7 @@ struct adrom_session {
   double* fact_partial = nullptr;
   double* fact_rows = nullptr;
   double* fact_qv = nullptr;
+  double* fact_partial_a = nullptr;
   // coarse-step stream: the advance_signal Newton solve only depends on the
   // previous coarse state, so it runs concurrently with the reduced step
   adrom_ctx* fctx = nullptr;
@@ -330,9 +338,16 @@ int drain_downloads(adrom_session* s) {
 // W' = [[W, 0], [0, 1/||q||]] B; committed only if every stage succeeds
 int run_event_factored(adrom_session* s, adrom_event_record& ev, bool* decoded) {
   adrom_ctx* ctx = s->ctx;
+  adrom_ctx* fc = s->fctx;
   int st;
+  // on the coarse-step stream, still overlapping the reduced step: snapshot
+  // preprocess, re-anchor when due, pass 1 (X^T y, exact row norms)
+  preprocess_kernel<<<(int)((s->N + 255) / 256 < ctx->num_sms * 8 ? (s->N + 255) / 256
+                                                                   : ctx->num_sms * 8),
+                      256, 0, fc->stream>>>(s->y_corr, s->q_ref, s->d, s->N, s->y_hat);
+  ADROM_LAUNCH_CK(fc);
   if (s->kf == FACT_KQ) {  // re-anchor: A = X W (same basis), exact row norms
-    st = fact_reanchor(ctx, basis_view(s), s->phi[1 - s->acur], s->nrm2[s->cur]);
+    st = fact_reanchor(fc, basis_view(s), s->phi[1 - s->acur], s->nrm2[s->cur]);
     if (st) return st;
     s->acur = 1 - s->acur;
     s->kf = 0;
@@ -353,6 +368,8 @@ int run_event_factored(adrom_session* s, adrom_event_record& ev, bool* decoded) 
   e.G = s->gram[s->cur];
   e.lam = s->cfg.lam;
   e.partial = s->fact_partial;
+  e.partial_a = s->fact_partial_a;
+  e.flag_a = ctx->dflags + PASS_A_FLAG;
   e.small = s->fact_small;
   e.W_out = s->Wd[nxt];
   e.sigma_out = s->sigma[nxt];
@@ -366,9 +383,19 @@ int run_event_factored(adrom_session* s, adrom_event_record& ev, bool* decoded) 
   e.vdrop_out = s->vdrop[nxt];
   e.nrm2_out = s->nrm2[nxt];
   qdeim_seed_buffers(s->qd_ws, s->N, &e.seed_res2, &e.seed_bnd2, &e.seed_ver);
+  ADROM_CK(ctx, cudaMemsetAsync(e.flag_a, 0, sizeof(int), fc->stream));
+  const long long l0 = fc->launches;
+  st = fact_event_pass_a(fc, b, e);
+  ctx->launches += fc->launches - l0;
+  if (st) {
+    snprintf(ctx->err, sizeof(ctx->err), "%s", fc->err);
+    return st;
+  }
+  ADROM_CK(ctx, cudaEventRecord(s->fom_done, fc->stream));
+  ADROM_CK(ctx, cudaStreamWaitEvent(ctx->stream, s->fom_done, 0));
   st = reset_flags(ctx);
   if (st) return st;
-  st = fact_isvd_event(ctx, b, e);
+  st = fact_event_pass_b(ctx, b, e);
   if (st) return st;
   *decoded = true;
   s->nrm2_exact = true;  // pass 1 made nrm2[cur] exact for the current basis
@@ -425,8 +452,10 @@ int run_event(adrom_session* s, adrom_event_record& ev, bool* decoded) {
   int st = fom_implicit_step(fc, m, s->y_corr, s->cfg.z * s->cfg.dt, s->cfg.newton_tol,
                              s->cfg.newton_max_iter, s->y_next, &ni);
   ctx->launches += fc->launches - l0;
-  ADROM_CK(ctx, cudaEventRecord(s->fom_done, fc->stream));
-  ADROM_CK(ctx, cudaStreamWaitEvent(ctx->stream, s->fom_done, 0));
+  if (st || !s->fact) {  // (the factored path joins after its pass 1)
+    ADROM_CK(ctx, cudaEventRecord(s->fom_done, fc->stream));
+    ADROM_CK(ctx, cudaStreamWaitEvent(ctx->stream, s->fom_done, 0));
+  }
   if (st) {
     snprintf(ctx->err, sizeof(ctx->err), "%s", fc->err);
     if (st == ADROM_ERR_CUDA) return st;
@@ -437,12 +466,12 @@ int run_event(adrom_session* s, adrom_event_record& ev, bool* decoded) {
   ev.coarse_converged = ni.converged;
   ev.coarse_iterations = ni.iterations;
   ev.pad = 1;  // coarse advance done (event dict carries coarse_* keys)
+  if (s->fact) return run_event_factored(s, ev, decoded);
   // y_hat = D (y - q_ref)
   preprocess_kernel<<<(int)((s->N + 255) / 256 < ctx->num_sms * 8 ? (s->N + 255) / 256
                                                                    : ctx->num_sms * 8),
                       256, 0, ctx->stream>>>(s->y_corr, s->q_ref, s->d, s->N, s->y_hat);
   ADROM_LAUNCH_CK(ctx);
-  if (s->fact) return run_event_factored(s, ev, decoded);
   // iSVD into the spare buffers
   const int nxt = 1 - s->cur;
   const bool fused = rot_fusable(s->r, s->r);
@@ -557,7 +586,8 @@ int adrom_session_create(adrom_ctx* ctx, const adrom_session_config* cfg, adrom_
       s->vdrop[b] = s->alloc_d((size_t)(r + FACT_KQ + 1));
     }
     s->fact_small = s->alloc_d(fact_small_doubles(r));
-    s->fact_partial = s->alloc_d(fact_partial_doubles(ctx, r));
+    s->fact_partial = s->alloc_d(fact_partial_doubles(ctx, N, r));
+    s->fact_partial_a = s->alloc_d(fact_partial_doubles(ctx, N, r));
     s->fact_rows = s->alloc_d((size_t)(3 * cfg->n_s * cfg->model.n_var + cfg->n_s) * r);
     s->fact_qv = s->alloc_d((size_t)N);
     if (s->Qb) cudaMemsetAsync(s->Qb, 0, sizeof(double) * (size_t)N * FACT_KQ, ctx->stream);
@@ -565,7 +595,8 @@ int adrom_session_create(adrom_ctx* ctx, const adrom_session_config* cfg, adrom_
   s->cap_steps = cfg->n_t > cfg->w_init ? cfg->n_t - cfg->w_init : 1;
   s->step_log = s->alloc_d((size_t)s->cap_steps * 3);
   s->fail_step = s->alloc_t<int>(1);
-  if (s->fact && (!s->Qb || !s->nrm2[1] || !s->fact_rows || !s->fact_partial || !s->fact_qv))
+  if (s->fact && (!s->Qb || !s->nrm2[1] || !s->fact_rows || !s->fact_partial || !s->fact_qv ||
+                  !s->fact_partial_a))
     st = set_error(ctx, ADROM_ERR_CUDA, "session: device allocation failed (factored basis)");
   if (st || !s->phi[1] || !s->step_log || !s->fail_step || !s->qd_ws || !s->isvd_ws) {
     for (void* p : s->allocs) cudaFree(p);
