@@ -34,14 +34,14 @@ namespace cg = cooperative_groups;
 namespace adrom {
 
 // pool target size; ADROM_QDEIM_POOL_M overrides (tuning experiments)
-constexpr long long QP_M_DEFAULT = 1 << 16;
+constexpr long long QP_M_DEFAULT = 1 << 15;
 // rows refreshed per round = factor x pool size (grows 4x on a stalled
 // round); ADROM_QDEIM_REFRESH overrides
 static long long qp_refresh_factor() {
   static long long t = [] {
     const char* e = getenv("ADROM_QDEIM_REFRESH");
     const long long v = e ? atoll(e) : 0;
-    return (v >= 1 && v <= 4096) ? v : 64ll;
+    return (v >= 1 && v <= 4096) ? v : 128ll;
   }();
   return t;
 }
