@@ -57,8 +57,10 @@ int ensure_pinned(adrom_ctx* ctx, size_t bytes) {
 
 int prof_begin(adrom_ctx* ctx, int id) {
   adrom_ctx* P = ctx->prof_parent ? ctx->prof_parent : ctx;
-  if (!P->prof || P->prof_used >= ADROM_PROF_SLOTS) return -1;
-  const int slot = P->prof_used++;
+  if (!P->prof) return -1;
+  // helper contexts may record from their own host thread
+  const int slot = __atomic_fetch_add(&P->prof_used, 1, __ATOMIC_RELAXED);
+  if (slot >= ADROM_PROF_SLOTS) return -1;
   P->prof_id[slot] = id;
   cudaEventRecord(P->prof_ev[2 * slot], ctx->stream);
   return slot;
@@ -95,7 +97,8 @@ int adrom_prof_read(adrom_ctx* ctx, double* host_ms, int32_t* host_count) {
   }
   if (!ctx->prof_ev) return ADROM_OK;
   ADROM_CK(ctx, cudaStreamSynchronize(ctx->stream));
-  for (int s = 0; s < ctx->prof_used; ++s) {
+  const int used = ctx->prof_used < ADROM_PROF_SLOTS ? ctx->prof_used : ADROM_PROF_SLOTS;
+  for (int s = 0; s < used; ++s) {
     ADROM_CK(ctx, cudaEventSynchronize(ctx->prof_ev[2 * s + 1]));  // probes of helper streams
     float ms = 0.f;
     ADROM_CK(ctx, cudaEventElapsedTime(&ms, ctx->prof_ev[2 * s], ctx->prof_ev[2 * s + 1]));

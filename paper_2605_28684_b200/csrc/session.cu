@@ -19,6 +19,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <thread>
 #include <vector>
 
 using namespace adrom;
@@ -122,6 +123,14 @@ struct adrom_session {
   adrom_ctx* fctx = nullptr;
   cudaStream_t fstream = nullptr;
   cudaEvent_t main_mark = nullptr, fom_done = nullptr;
+  // factored path: the next event's coarse Newton solve runs on a host thread
+  // (its host-side convergence checks would otherwise block the issue of this
+  // event's work), started as soon as its input y_corr exists
+  std::thread fom_thread;
+  bool fom_pending = false;  // thread running
+  bool fom_ready = false;    // finished, result not consumed yet
+  int fom_status = 0;
+  adrom_newton_info fom_ni{};
   // trajectory download: q~ is staged (D2D) into one of two device buffers
   // and copied to host memory on its own stream, overlapping the next steps
   cudaStream_t cstream = nullptr;
@@ -333,6 +342,33 @@ int drain_downloads(adrom_session* s) {
   return ADROM_OK;
 }
 
+void fom_launch_async(adrom_session* s) {
+  if (s->fom_pending || s->fom_ready) return;
+  const adrom_model m = model_of(s);
+  const double* in = s->y_corr;
+  double* out = s->y_next;
+  s->fom_pending = true;
+  s->fom_thread = std::thread([s, m, in, out]() {
+    s->fom_status = fom_implicit_step(s->fctx, m, in, s->cfg.z * s->cfg.dt, s->cfg.newton_tol,
+                                      s->cfg.newton_max_iter, out, &s->fom_ni);
+  });
+}
+
+void fom_wait(adrom_session* s) {
+  if (!s->fom_pending) return;
+  s->fom_thread.join();
+  s->fom_pending = false;
+  s->fom_ready = true;
+}
+
+// result of the started coarse step (consumed)
+int fom_join(adrom_session* s, adrom_newton_info* ni) {
+  fom_wait(s);
+  s->fom_ready = false;
+  *ni = s->fom_ni;
+  return s->fom_status;
+}
+
 // the rest of an event on the factored basis (after the coarse step and
 // preprocess): no rotation — the residual becomes column kf of Qb and
 // W' = [[W, 0], [0, 1/||q||]] B; committed only if every stage succeeds
@@ -393,6 +429,9 @@ int run_event_factored(adrom_session* s, adrom_event_record& ev, bool* decoded) 
   }
   ADROM_CK(ctx, cudaEventRecord(s->fom_done, fc->stream));
   ADROM_CK(ctx, cudaStreamWaitEvent(ctx->stream, s->fom_done, 0));
+  // the next event's coarse step only needs this y_corr: start it now (it
+  // queues behind pass 1 on the coarse-step stream)
+  fom_launch_async(s);
   st = reset_flags(ctx);
   if (st) return st;
   st = fact_event_pass_b(ctx, b, e);
@@ -447,10 +486,18 @@ int run_event(adrom_session* s, adrom_event_record& ev, bool* decoded) {
   // before this step's reduced step (main_mark), overlapping that step
   adrom_newton_info ni{};
   adrom_ctx* fc = s->fctx;
-  ADROM_CK(ctx, cudaStreamWaitEvent(fc->stream, s->main_mark, 0));
   const long long l0 = fc->launches;
-  int st = fom_implicit_step(fc, m, s->y_corr, s->cfg.z * s->cfg.dt, s->cfg.newton_tol,
-                             s->cfg.newton_max_iter, s->y_next, &ni);
+  int st;
+  if (s->fact) {
+    // started early (fom_launch_async) unless this is the first event or the
+    // previous coarse step failed
+    fom_launch_async(s);  // no-op when already started / finished
+    st = fom_join(s, &ni);
+  } else {
+    ADROM_CK(ctx, cudaStreamWaitEvent(fc->stream, s->main_mark, 0));
+    st = fom_implicit_step(fc, m, s->y_corr, s->cfg.z * s->cfg.dt, s->cfg.newton_tol,
+                           s->cfg.newton_max_iter, s->y_next, &ni);
+  }
   ctx->launches += fc->launches - l0;
   if (st || !s->fact) {  // (the factored path joins after its pass 1)
     ADROM_CK(ctx, cudaEventRecord(s->fom_done, fc->stream));
@@ -627,6 +674,7 @@ int adrom_session_create(adrom_ctx* ctx, const adrom_session_config* cfg, adrom_
 
 void adrom_session_destroy(adrom_session* s) {
   if (!s) return;
+  fom_wait(s);
   cudaStreamSynchronize(s->ctx->stream);
   if (s->fctx) adrom_ctx_destroy(s->fctx);
   if (s->fstream) cudaStreamDestroy(s->fstream);
@@ -663,6 +711,8 @@ int adrom_session_load(adrom_session* s, const double* q_ref, const double* d, c
   ADROM_CK(ctx, cudaMemcpyAsync(s->q_tilde, q_last, 8 * N, cudaMemcpyDeviceToDevice,
                                 ctx->stream));
   ADROM_CK(ctx, cudaMemcpyAsync(s->y_corr, q_last, 8 * N, cudaMemcpyDeviceToDevice, ctx->stream));
+  fom_wait(s);
+  s->fom_ready = false;  // a coarse step of a previous run is discarded
   s->cur = 0;
   s->acur = 0;
   s->kf = 0;
@@ -752,6 +802,10 @@ int adrom_session_advance(adrom_session* s, int64_t n_steps, int64_t save_every,
     }
   }
   if (n_saved) *n_saved = saved;
+  // a coarse step started for the next event is finished before returning
+  // (its result is kept: fom_pending stays false, the output is consumed by
+  // the next event through fom_join's saved status)
+  fom_wait(s);
   // host_out is complete when advance returns (the copies overlapped the steps)
   return drain_downloads(s);
 }
