@@ -37,19 +37,20 @@ class Model:
     ``SodProblem`` (fom.py:249-260) that the residual needs.
     """
 
-    kind: str           # "burgers" | "sod"
+    kind: str           # "burgers" | "sod" | "reacting" (configuration 4, oracle/reacting.py)
     n_elem: int
     nu: float = 0.01
     gamma: float = 1.4
     length: float = 1.0
+    mech: tuple | None = None  # reacting: the (5, 12) mechanism, flattened
 
     @property
     def n_var(self) -> int:
-        return 1 if self.kind == "burgers" else 3
+        return {"burgers": 1, "sod": 3, "reacting": 13}[self.kind]
 
     @property
     def periodic(self) -> bool:
-        return self.kind == "burgers"
+        return self.kind in ("burgers", "reacting")
 
     @property
     def dx(self) -> float:
@@ -137,6 +138,10 @@ def rhs(model: Model, q: np.ndarray) -> np.ndarray:
         ext = np.concatenate([cells[:1], cells, cells[-1:]], axis=0)
         face = rusanov(ext[:-1], ext[1:], model.gamma)
         return (-(face[1:] - face[:-1]) / model.dx).ravel()
+    if model.kind == "reacting":
+        from . import reacting
+        mech = np.asarray(model.mech, dtype=float).reshape(5, reacting.N_REACT)
+        return reacting.rhs(q, model.n_elem, model.dx, model.gamma, mech)
     raise ValueError(f"unknown model kind {model.kind!r}")
 
 

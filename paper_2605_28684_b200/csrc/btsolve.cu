@@ -594,6 +594,9 @@ int bt_solve(adrom_ctx* ctx, const double* sys, const double* rhs, double rhs_si
              int nv, bool cyclic, double* out, void* ws, int* flag, const double* add_to) {
   if (nv == 1) return bt_solve_t<1>(ctx, sys, rhs, rhs_sign, n, cyclic, out, ws, flag, add_to);
   if (nv == 3) return bt_solve_t<3>(ctx, sys, rhs, rhs_sign, n, cyclic, out, ws, flag, add_to);
+  // configuration-4 reacting model: 13 x 13 blocks (thread-per-partition,
+  // blocks in local memory; correctness first, round 2 makes it warp-wide)
+  if (nv == 13) return bt_solve_t<13>(ctx, sys, rhs, rhs_sign, n, cyclic, out, ws, flag, add_to);
   return set_error(ctx, ADROM_ERR_ARG, "bt_solve: unsupported block size %d", nv);
 }
 

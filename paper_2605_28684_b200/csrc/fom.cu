@@ -381,6 +381,17 @@ static inline BurgersParams burgers_params(const adrom_model& m) {
   return p;
 }
 
+// the reacting model (kind 3) runs the residual, the FD Jacobian and the
+// implicit step; its sampled-residual paths are round-2 work
+static int check_model_fom(adrom_ctx* ctx, const adrom_model& m) {
+  if (m.kind == ADROM_REACTING) {
+    if (m.n_var != 13 || m.n_elem < 4 || !m.mech)
+      return set_error(ctx, ADROM_ERR_ARG, "reacting model needs n_var=13, n_elem>=4, mech");
+    return ADROM_OK;
+  }
+  return ADROM_OK;
+}
+
 static int check_model(adrom_ctx* ctx, const adrom_model& m) {
   if (m.kind == ADROM_BURGERS && m.n_var == 1 && m.n_elem >= 4) return ADROM_OK;
   if (m.kind == ADROM_SOD && m.n_var == 3 && m.n_elem >= 4) return ADROM_OK;
@@ -392,10 +403,43 @@ static int check_model(adrom_ctx* ctx, const adrom_model& m) {
 }
 
 // residual launch; MODE 1 writes per-block partials into `partial`
+__global__ void __launch_bounds__(256) newton_resid_kernel(const double* __restrict__ x,
+                                                            const double* __restrict__ qprev,
+                                                            double dt, double* __restrict__ out,
+                                                            int64_t n, double* __restrict__ partial,
+                                                            int* __restrict__ flag) {
+  __shared__ double red[8];
+  double acc = 0.0;
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double f = (x[i] - qprev[i]) - dt * out[i];
+    out[i] = f;
+    acc += f * f;
+    bad |= !isfinite(f);
+  }
+  const double s2 = block_sum<256>(acc, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s2;
+  if (bad) atomicOr(flag, 1);
+}
+
 static int launch_residual(adrom_ctx* ctx, const adrom_model& m, const double* x, double* out,
                            bool newton, const double* qprev, double dt, double* partial,
                            int* flag, int* nblocks_out) {
   int nb;
+  if (m.kind == ADROM_REACTING) {
+    int st = reacting_rhs(ctx, m, x, out);
+    if (st) return st;
+    nb = 0;
+    if (newton) {  // r = (x - q) - dt f(x), per-block sums of r^2 (fom.py:340-341)
+      nb = grid_for(ctx, m.n_elem * 13, 256);
+      newton_resid_kernel<<<nb, 256, 0, ctx->stream>>>(x, qprev, dt, out, m.n_elem * 13, partial,
+                                                       flag);
+    }
+    if (nblocks_out) *nblocks_out = nb;
+    ADROM_LAUNCH_CK(ctx);
+    return ADROM_OK;
+  }
   if (m.kind == ADROM_BURGERS) {
     nb = grid_for(ctx, m.n_elem, BURG_TILE);
     if (newton)
@@ -466,6 +510,7 @@ int fom_plan_evaluate(adrom_ctx* ctx, const adrom_model& m, const int64_t* gathe
 
 static int launch_jacobian(adrom_ctx* ctx, const adrom_model& m, const double* q, double* blocks,
                            bool apply_dt, double dt, int* flag) {
+  if (m.kind == ADROM_REACTING) return reacting_jacobian(ctx, m, q, blocks, apply_dt, dt, flag);
   if (m.kind == ADROM_BURGERS)
     burgers_jac_kernel<<<grid_for(ctx, m.n_elem, 256), 256, 0, ctx->stream>>>(
         q, m.n_elem, burgers_params(m), blocks, apply_dt, dt, flag);
@@ -478,7 +523,7 @@ static int launch_jacobian(adrom_ctx* ctx, const adrom_model& m, const double* q
 
 int fom_fd_jacobian(adrom_ctx* ctx, const adrom_model& m, const double* q, double* blocks,
                     bool apply_dt, double dt) {
-  int st = check_model(ctx, m);
+  int st = (m.kind == ADROM_REACTING) ? check_model_fom(ctx, m) : check_model(ctx, m);
   if (st) return st;
   st = ensure_scratch(ctx, 256);
   if (st) return st;
@@ -503,7 +548,7 @@ size_t fom_newton_workspace(const adrom_model& m) {
 
 int fom_implicit_step(adrom_ctx* ctx, const adrom_model& m, const double* q, double dt,
                       double tol, int max_iter, double* x, adrom_newton_info* info) {
-  int st = check_model(ctx, m);
+  int st = (m.kind == ADROM_REACTING) ? check_model_fom(ctx, m) : check_model(ctx, m);
   if (st) return st;
   if (!(tol > 0)) return set_error(ctx, ADROM_ERR_DENSE, "newton_solve requires tol > 0");
   const int64_t N = m.n_elem * m.n_var;
@@ -561,7 +606,7 @@ int fom_implicit_step(adrom_ctx* ctx, const adrom_model& m, const double* q, dou
     // solve (I - dt J) delta = -r, then x += delta
     pr = prof_begin(ctx, PROBE_FOM_SOLVE);
     // x += delta fused into the solver's last back-substitution
-    st = bt_solve(ctx, A, r, -1.0, m.n_elem, m.n_var, m.kind == ADROM_BURGERS, x, btws, flag, x);
+    st = bt_solve(ctx, A, r, -1.0, m.n_elem, m.n_var, m.kind != ADROM_SOD, x, btws, flag, x);
     prof_end(ctx, pr);
     if (st) return st;
     (void)delta;

@@ -8,6 +8,8 @@ namespace adrom {
 int fom_rhs(adrom_ctx* ctx, const adrom_model& m, const double* q, double* f);
 // configuration-4 reacting Euler residual (reacting.cu)
 int reacting_rhs(adrom_ctx* ctx, const adrom_model& m, const double* q, double* f);
+int reacting_jacobian(adrom_ctx* ctx, const adrom_model& m, const double* q, double* blocks,
+                      bool apply_dt, double dt, int* flag);
 int fom_rhs_at_cells(adrom_ctx* ctx, const adrom_model& m, const double* gathered, int64_t k,
                      double* out);
 int fom_plan_evaluate(adrom_ctx* ctx, const adrom_model& m, const int64_t* gather,

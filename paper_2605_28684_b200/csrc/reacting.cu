@@ -125,6 +125,119 @@ __global__ void __launch_bounds__(RX_NT) reacting_rhs_kernel(const double* __res
   }
 }
 
+// residual of one cell from its stencil (l, c, r): -(F(c,r) - F(l,c))/dx + S(c),
+// the same operations as the full kernel (faces computed identically)
+__device__ void rx_cell_res(const double* l, const double* c, const double* r, double gamma,
+                            double dx, const double* mk, double* out) {
+  double fl[RX_NV], fr[RX_NV];
+  rx_rusanov(l, c, gamma, fl);
+  rx_rusanov(c, r, gamma, fr);
+  double s[RX_NV];
+#pragma unroll
+  for (int v = 0; v < RX_NV; ++v) s[v] = 0.0;
+  double rho, vel, p;
+  rx_prim(c, gamma, rho, vel, p);
+  const double temp = p / rho;
+#pragma unroll 1
+  for (int j = 0; j < RX_NR; ++j) {
+    const int a = (int)mk[j], b = (int)mk[RX_NR + j];
+    const double w = (mk[2 * RX_NR + j] * exp(-mk[3 * RX_NR + j] / temp)) * np_max(c[3 + a], 0.0);
+#pragma unroll
+    for (int k = 0; k < RX_NS; ++k) {
+      if (k == a) s[3 + k] = s[3 + k] - w;
+      if (k == b) s[3 + k] = s[3 + k] + w;
+    }
+    s[2] = s[2] + mk[4 * RX_NR + j] * w;
+  }
+#pragma unroll
+  for (int v = 0; v < RX_NV; ++v) out[v] = (-(fr[v] - fl[v])) / dx + s[v];
+}
+
+// Banded FD Jacobian (fom.py:301-328 generalised; oracle/physics.py
+// fd_jacobian_blocks): column (cell g, var v) with eps = 1e-7 max(1, |q|)
+// touches rows g-1 (right block), g (centre), g+1 (left block).  A tile of
+// RJ_T cells is staged with a 2-cell halo and its base residuals.
+// apply_dt: A = I - dt J (fom.py:343-344).
+constexpr int RJ_T = 32;
+
+__global__ void __launch_bounds__(128) reacting_jac_kernel(const double* __restrict__ q, int64_t n,
+                                                            double dx, double gamma,
+                                                            const double* __restrict__ mech,
+                                                            double* __restrict__ blocks,
+                                                            bool apply_dt, double dt,
+                                                            int* __restrict__ flag) {
+  __shared__ double cs[RX_NV * (RJ_T + 4)];   // cells base-2 .. base+T+1
+  __shared__ double fb[RX_NV * (RJ_T + 2)];   // base residuals of rows base-1 .. base+T
+  __shared__ double mk[5 * RX_NR];
+  for (int e = threadIdx.x; e < 5 * RX_NR; e += blockDim.x) mk[e] = mech[e];
+  constexpr int NV2 = RX_NV * RX_NV;
+  const int64_t ntiles = (n + RJ_T - 1) / RJ_T;
+  bool bad = false;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t base = t * RJ_T;
+    const int cnt = (int)((n - base < RJ_T) ? (n - base) : RJ_T);
+    __syncthreads();
+    for (int e = threadIdx.x; e < RX_NV * (cnt + 4); e += blockDim.x) {
+      const int j = e / RX_NV, v = e - j * RX_NV;
+      int64_t g = base - 2 + j;
+      g = ((g % n) + n) % n;
+      cs[e] = q[g * RX_NV + v];
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < cnt + 2; j += blockDim.x)  // row base-1+j: cells j, j+1, j+2
+      rx_cell_res(cs + RX_NV * j, cs + RX_NV * (j + 1), cs + RX_NV * (j + 2), gamma, dx, mk,
+                  fb + RX_NV * j);
+    __syncthreads();
+    for (int item = threadIdx.x; item < cnt * RX_NV; item += blockDim.x) {
+      const int il = item / RX_NV, v = item - il * RX_NV;  // cell base+il, var v
+      const int jc = il + 2;                                // its index in cs
+      const double qv = cs[RX_NV * jc + v];
+      const double eps = fd_eps(qv);
+      double pc[RX_NV];
+#pragma unroll
+      for (int a = 0; a < RX_NV; ++a) pc[a] = cs[RX_NV * jc + a];
+      pc[v] = qv + eps;
+      const int64_t g = base + il;
+      // rows g-1 (slot 2), g (slot 1), g+1 (slot 0)
+#pragma unroll 1
+      for (int rr = 0; rr < 3; ++rr) {
+        double fp[RX_NV];
+        const double* l = cs + RX_NV * (jc - 2 + rr);
+        const double* c = cs + RX_NV * (jc - 1 + rr);
+        const double* r = cs + RX_NV * (jc + rr);
+        if (rr == 0) rx_cell_res(l, c, pc, gamma, dx, mk, fp);
+        else if (rr == 1) rx_cell_res(l, pc, r, gamma, dx, mk, fp);
+        else rx_cell_res(pc, c, r, gamma, dx, mk, fp);
+        int64_t row = g - 1 + rr;
+        row = ((row % n) + n) % n;
+        const int slot = 2 - rr;
+        const double* f0 = fb + RX_NV * (il + rr);  // base residual of that row
+        double* B = blocks + ((row * 3 + slot) * NV2);
+#pragma unroll
+        for (int a = 0; a < RX_NV; ++a) {
+          const double jv = (fp[a] - f0[a]) / eps;
+          bad |= !isfinite(jv);
+          B[a * RX_NV + v] = apply_dt ? ((slot == 1 && a == v) ? 1.0 : 0.0) - dt * jv : jv;
+        }
+      }
+    }
+  }
+  if (bad) atomicOr(flag, 4);
+}
+
+int reacting_jacobian(adrom_ctx* ctx, const adrom_model& m, const double* q, double* blocks,
+                      bool apply_dt, double dt, int* flag) {
+  if (!m.mech) return set_error(ctx, ADROM_ERR_ARG, "reacting model: mechanism pointer is null");
+  const int64_t ntiles = (m.n_elem + RJ_T - 1) / RJ_T;
+  int64_t g = (int64_t)ctx->num_sms * 8;
+  if (g > ntiles) g = ntiles;
+  reacting_jac_kernel<<<(int)(g < 1 ? 1 : g), 128, 0, ctx->stream>>>(q, m.n_elem, m.dx, m.gamma,
+                                                                    m.mech, blocks, apply_dt, dt,
+                                                                    flag);
+  ADROM_LAUNCH_CK(ctx);
+  return ADROM_OK;
+}
+
 int reacting_rhs(adrom_ctx* ctx, const adrom_model& m, const double* q, double* f) {
   if (!m.mech) return set_error(ctx, ADROM_ERR_ARG, "reacting model: mechanism pointer is null");
   const int64_t ntiles = (m.n_elem + RX_TILE - 1) / RX_TILE;

@@ -254,7 +254,7 @@ class ReactingEulerProblem(FomProblem):
 
 
 def _check_model(model):
-    if not isinstance(model, (BurgersProblem, SodProblem)):
+    if not isinstance(model, (BurgersProblem, SodProblem, ReactingEulerProblem)):
         raise TypeError(
             f"{type(model).__name__} has no device implementation; the B200 path "
             "supports BurgersProblem and SodProblem (subclasses may override "

@@ -81,3 +81,38 @@ def test_reacting_rhs_device_resident_and_errors():
     assert np.linalg.norm(f.cpu().numpy() - ref) <= 1e-13 * np.linalg.norm(ref)
     with pytest.raises(ValueError):
         m.rhs(np.zeros(5))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [7, 64])
+def test_reacting_fd_jacobian_vs_oracle(n):
+    """Banded FD Jacobian (the reference's colouring scheme, fom.py:301-328,
+    on the builder-defined model).  The difference quotients amplify the
+    ulp-level exp() differences by 1/eps: normwise 1e-7 per block row."""
+    P = _pkg()
+    from oracle import physics
+    m = P.ReactingEulerProblem(n)
+    q = m.initial_state() * (1.0 + 0.01 * np.random.default_rng(n).standard_normal(n * 13))
+    om = physics.Model("reacting", n, gamma=1.4, mech=tuple(m.mechanism.ravel()))
+    ref = physics.fd_jacobian_blocks(om, q)
+    got = np.asarray(P.fd_jacobian_blocks(m, q))
+    assert got.shape == ref.shape
+    err = np.linalg.norm((got - ref).reshape(n, -1), axis=1) / np.linalg.norm(ref.reshape(n, -1), axis=1)
+    assert err.max() <= 1e-7, err.max()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,dt", [(64, 1e-3), (1000, 2e-4)])
+def test_reacting_implicit_step_vs_oracle(n, dt):
+    """Backward-Euler Newton on the reacting model (a4 for configuration 4):
+    13 x 13 block-tridiagonal cyclic solve on the device vs the oracle's
+    sparse LU of the same matrix."""
+    P = _pkg()
+    from oracle import physics
+    m = P.ReactingEulerProblem(n)
+    q = m.initial_state()
+    om = physics.Model("reacting", n, gamma=1.4, mech=tuple(m.mechanism.ravel()))
+    ref = physics.implicit_step(om, q, dt)
+    res = P.implicit_step(m, q, dt)
+    assert res.converged == ref.converged and res.iterations == ref.iterations
+    assert np.linalg.norm(np.asarray(res.x) - ref.x) <= 1e-12 * np.linalg.norm(ref.x)
