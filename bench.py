@@ -643,6 +643,17 @@ def bench_cfg4(args, rank, world):
         "clocks": clk.summary(),
     }
     line["roofline"]["kernel"] = "reacting_rhs_kernel (208 B/cell)"
+    # one backward-Euler step on the same grid (a4 for configuration 4)
+    dt4 = 2e-5
+    P.implicit_step(m, q, dt4)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    res = P.implicit_step(m, q, dt4)
+    e1.record()
+    torch.cuda.synchronize()
+    line["implicit_step"] = {"ms": round(e0.elapsed_time(e1), 3), "dt": dt4,
+                             "iterations": int(res.iterations), "converged": bool(res.converged)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import reacting as R
         ns = 1 << 16
