@@ -200,13 +200,13 @@ def bench_cfg2(args, rank, world):
     del qf
     ctx = _lib.Context.get()
     P = _lib.ptr
-    gram = torch.empty((r, r), dtype=torch.float64, device="cuda")
-    ctx.call("adrom_gram", P(phi), C.c_int64(n), C.c_int32(r), P(gram))  # tracked from here
+    # the streaming form (factored basis, csrc/factored.cu): every update is
+    # tracking.py:141-178; the basis is materialised after the timed region
+    from paper_2605_28684_b200.tracking import IsvdStream, ReducedBasis
+    stream = IsvdStream(ReducedBasis(phi=phi, sigma=sig))
 
     def update(k):
-        y = snaps[r + k]
-        ctx.call("adrom_isvd_update", P(phi), P(sig), P(y), C.c_int64(n), C.c_int32(r),
-                 C.c_int32(r), C.c_double(case.lam), P(phi), P(sig), P(gram), None)
+        stream.update(snaps[r + k], case.lam)
 
     for k in range(W):
         update(k)
@@ -230,9 +230,16 @@ def bench_cfg2(args, rank, world):
     barrier(world)
     ms_step = ms / K
     value = world * K / (ms * 1e-3)
-    rot_ms, rot_n = probes.get("isvd_rotate", (0.0, 0))
-    rot_bytes = 8.0 * (2 * n * r + n)
+    # pass 1 of the stream is HBM bound: 8 N (r + k + 1) bytes (A, the k live
+    # residual columns, y), k cycling 0..15 between re-anchors
+    kq = 16
+    k_mean = float(np.mean([j % kq for j in range(W, W + K)]))
+    p1_ms, p1_n = probes.get("isvd_project", (0.0, 0))
+    p1_bytes = 8.0 * n * (r + k_mean + 1)
     canon = 8.0 * (3 * n * r + 2 * n)
+    basis_out = stream.basis()
+    phi, sig = basis_out.phi, basis_out.sigma
+    stream.close()
     extra = {
         "isvd_update_ms": round(ms_step, 4),
         "isvd_update_hbm_frac": round(canon / (ms_step * 1e-3) / 1e9 / HBM_PEAK, 4),
@@ -247,10 +254,12 @@ def bench_cfg2(args, rank, world):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded rank-96 stream, device RNG)",
         "config": {"workload": "cfg2-isvd-stream", "n": n, "r": r, "lam": case.lam,
                    "l2": "inputs larger than L2 (basis 2 GiB)", "parallelism": f"replicas{world}"},
-        "roofline": roofline(rot_bytes, rot_ms / max(rot_n, 1)) if rot_n else None,
+        "roofline": roofline(p1_bytes, p1_ms / max(p1_n, 1)) if p1_n else None,
         "gpu_launches": launches,
     }
-    line["roofline_kernel"] = "isvd_rotate (rot_tiled_kernel<64>): 8(2Nr+N) bytes/launch"
+    if line["roofline"]:
+        line["roofline"].update({"kernel": "isvd_project (xpass_kernel<64,1>: X^T y, factored basis)",
+                                 "work_per_launch": {"bytes": p1_bytes, "k_mean": k_mean}})
     line.update(extra)
     line["clocks"] = clk.summary()
     if rank == 0 and not args.no_e2e:
@@ -261,42 +270,31 @@ def bench_cfg2(args, rank, world):
 
 
 def e2e_cfg2(args, case, snaps, phi, sig):
-    """Same update through the C-ABI with HOST buffers: every step copies the
-    basis, sigma and snapshot from pinned host memory and the result back."""
-    import ctypes as C
+    """The streaming update through the public API (tracking.IsvdStream) with
+    HOST buffers: every step copies its snapshot from pinned host memory and
+    reads the step's result (the singular values) back; the basis is state
+    and stays on the device (materialised by IsvdStream.basis() on demand)."""
     import torch
-    from paper_2605_28684_b200 import _lib
+    from paper_2605_28684_b200.tracking import IsvdStream, ReducedBasis
     n, r = case.n, case.r
-    steps = min(args.steps, 5)
-    h_phi = torch.empty((n, r), dtype=torch.float64, pin_memory=True)
-    h_phi.copy_(phi)
-    h_sig = torch.empty(r, dtype=torch.float64, pin_memory=True)
-    h_sig.copy_(sig)
+    steps = args.steps
     h_y = torch.empty((steps, n), dtype=torch.float64, pin_memory=True)
     h_y.copy_(snaps[-steps:])
-    d_phi = torch.empty_like(phi)
-    d_sig = torch.empty_like(sig)
-    d_gram = torch.empty((r, r), dtype=torch.float64, device="cuda")
+    h_sig = torch.empty((steps, r), dtype=torch.float64, pin_memory=True)
     d_y = torch.empty(n, dtype=torch.float64, device="cuda")
-    ctx = _lib.Context.get()
-    P = _lib.ptr
+    stream = IsvdStream(ReducedBasis(phi=phi, sigma=sig))
     torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record()
+    t0 = time.perf_counter()
     for k in range(steps):
-        d_phi.copy_(h_phi, non_blocking=True)
-        d_sig.copy_(h_sig, non_blocking=True)
         d_y.copy_(h_y[k], non_blocking=True)
-        ctx.call("adrom_isvd_update", P(d_phi), P(d_sig), P(d_y), C.c_int64(n), C.c_int32(r),
-                 C.c_int32(r), C.c_double(case.lam), P(d_phi), P(d_sig), None, None)
-        h_phi.copy_(d_phi, non_blocking=True)
-        h_sig.copy_(d_sig, non_blocking=True)
-    ev1.record()
+        stream.update(d_y, case.lam)
+        h_sig[k].copy_(stream.basis_sigma(), non_blocking=True)
     torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1) / steps
+    ms = (time.perf_counter() - t0) * 1e3 / steps
+    stream.close()
     return {"value": round(1e3 / ms, 3), "unit": "updates/s", "ms_per_step": round(ms, 3),
-            "h2d_bytes_per_step": 8 * (n * r + r + n), "d2h_bytes_per_step": 8 * (n * r + r),
-            "steps": steps}
+            "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * r, "steps": steps,
+            "note": "IsvdStream: snapshot H2D + singular values D2H per update; wall clock"}
 
 
 def cpu_baseline_cfg2(case, n_sample=1 << 20, reps=2):

@@ -173,6 +173,20 @@ int adrom_isvd_update(adrom_ctx* ctx, const double* phi, const double* sigma,
                       const double* y_hat, int64_t n, int32_t r_cur, int32_t r, double lam,
                       double* phi_out, double* sigma_out, double* gram,
                       adrom_isvd_info* host_info);
+/* Streaming iSVD (B200 extension, r in {32, 64}): the basis is kept factored,
+ * Phi = [A | Q] W (csrc/factored.cu), so an update costs two passes over the
+ * basis and O(r^3) work instead of the O(N r^2) rotation of adrom_isvd_update;
+ * after 16 updates the anchor A = [A | Q] W is rebuilt on the tensor cores.
+ * Each update is mathematically tracking.py:141-178; a failed update leaves
+ * the stream unchanged.  read() materialises Phi (n x r). */
+typedef struct adrom_isvd_stream adrom_isvd_stream;
+int adrom_isvd_stream_create(adrom_ctx* ctx, int64_t n, int32_t r, adrom_isvd_stream** out);
+void adrom_isvd_stream_destroy(adrom_isvd_stream* s);
+int adrom_isvd_stream_load(adrom_isvd_stream* s, const double* phi, const double* sigma);
+int adrom_isvd_stream_update(adrom_isvd_stream* s, const double* y_hat, double lam,
+                             adrom_isvd_info* host_info);
+int adrom_isvd_stream_read(adrom_isvd_stream* s, double* phi_out, double* sigma_out);
+
 /* gram = phi^T phi (device r x r) */
 int adrom_gram(adrom_ctx* ctx, const double* phi, int64_t n, int32_t r, double* gram);
 

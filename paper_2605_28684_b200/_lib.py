@@ -93,6 +93,11 @@ SIGNATURES = {
     "adrom_isvd_update": (_i32, [_p, _p, _p, _p, _i64, _i32, _i32, _f64, _p, _p, _p,
                                  C.POINTER(IsvdInfo)]),
     "adrom_gram": (_i32, [_p, _p, _i64, _i32, _p]),
+    "adrom_isvd_stream_create": (_i32, [_p, _i64, _i32, C.POINTER(_p)]),
+    "adrom_isvd_stream_destroy": (None, [_p]),
+    "adrom_isvd_stream_load": (_i32, [_p, _p, _p]),
+    "adrom_isvd_stream_update": (_i32, [_p, _p, _f64, C.POINTER(IsvdInfo)]),
+    "adrom_isvd_stream_read": (_i32, [_p, _p, _p]),
     "adrom_small_svd": (_i32, [_p, _p, _i32, _i32, _p, _p, _p]),
     "adrom_qdeim": (_i32, [_p, _p, _i64, _i32, _i32, _p]),
     "adrom_fgs": (_i32, [_p, C.POINTER(Model), _p, _i32, _p, _i32, _i32, _i32, _p]),

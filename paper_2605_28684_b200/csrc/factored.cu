@@ -23,6 +23,8 @@
 #include "factored_internal.cuh"
 #include "linalg_internal.cuh"
 
+#include <vector>
+
 namespace adrom {
 
 struct XPassArgs {
@@ -120,8 +122,8 @@ __global__ void __launch_bounds__(256, 2) xpass_kernel(XPassArgs a) {
         for (int t = 0; t < QPL; ++t) xq[u][t] = 0.0;
       }
       yv[u] = (live && a.y) ? a.y[i] : 0.0;
-      qr[u] = live ? a.q_ref[i] : 0.0;
-      dd[u] = live ? a.d[i] : 1.0;
+      qr[u] = (live && a.q_ref) ? a.q_ref[i] : 0.0;
+      dd[u] = (live && a.d) ? a.d[i] : 1.0;
       qt[u] = 0.0;
     }
     double rd[U], dd2[U];
@@ -170,7 +172,7 @@ __global__ void __launch_bounds__(256, 2) xpass_kernel(XPassArgs a) {
         bad |= !isfinite(w0);
         if (sl == 0) {
           a.Qw[i * kq + k] = w0;
-          a.qv[i] = w0;
+          if (a.qv) a.qv[i] = w0;
           s0 += w0 * w0;
         }
       }
@@ -677,11 +679,11 @@ int fact_event_pass_b(adrom_ctx* ctx, const FactBasis& b, const FactEventArgs& e
   const int r = b.r, k = b.k, rk = r + k;
   const FactSmall f = fact_small_layout(e.small, r);
   const int grid = xpass_grid(ctx, b.n);
-  // decode vector W a (identity when k == 0 and W == null)
-  if (b.W) {
+  // decode vector W a (identity when k == 0 and W == null); no decode without a
+  if (e.a && b.W) {
     mat_vec_kernel<<<1, 256, 0, ctx->stream>>>(b.W, rk, r, e.a, f.vdec);
     ADROM_LAUNCH_CK(ctx);
-  } else {
+  } else if (e.a) {
     ADROM_CK(ctx, cudaMemcpyAsync(f.vdec, e.a, sizeof(double) * r, cudaMemcpyDeviceToDevice, ctx->stream));
   }
   // least squares p = G^{-1} p1; the explicit residual pass always runs here
@@ -698,7 +700,7 @@ int fact_event_pass_b(adrom_ctx* ctx, const FactBasis& b, const FactEventArgs& e
   // pass 2 (+ decode of the reduced state, projection.py:104)
   int pr = prof_begin(ctx, PROBE_ISVD_RESID);
   XPassArgs a2{b.A, b.Q, b.n, k, FACT_KQ, f.vp, e.y, e.q_ref, e.d, e.q_tilde, e.Qw, e.qv, e.partial,
-               e.flag, nullptr, nullptr, f.vdec};
+               e.flag, nullptr, nullptr, e.a ? f.vdec : nullptr};
   if (r == 64) xpass_kernel<64, 2><<<grid, 256, 0, ctx->stream>>>(a2);
   else xpass_kernel<32, 2><<<grid, 256, 0, ctx->stream>>>(a2);
   ADROM_LAUNCH_CK(ctx);
@@ -725,8 +727,10 @@ int fact_event_pass_b(adrom_ctx* ctx, const FactBasis& b, const FactEventArgs& e
   // W' and the state transfer for the new basis
   wnext_kernel<<<(rk + 1) * r / 256 + 1, 256, 0, ctx->stream>>>(b.W, rk, r, f.Bm, f.sb, e.W_out);
   ADROM_LAUNCH_CK(ctx);
-  encode_factored_kernel<<<1, 128, 0, ctx->stream>>>(e.G, r, e.a, f.red2, f.sb, f.Bm, e.a_out);
-  ADROM_LAUNCH_CK(ctx);
+  if (e.a_out) {
+    encode_factored_kernel<<<1, 128, 0, ctx->stream>>>(e.G, r, e.a, f.red2, f.sb, f.Bm, e.a_out);
+    ADROM_LAUNCH_CK(ctx);
+  }
   if (e.vdrop_out) {
     vdrop_kernel<<<1, 128, 0, ctx->stream>>>(b.W, rk, r, udrop, f.sb, e.vdrop_out);
     ADROM_LAUNCH_CK(ctx);
@@ -748,4 +752,162 @@ int fact_isvd_event(adrom_ctx* ctx, const FactBasis& b, const FactEventArgs& e) 
   return fact_event_pass_b(ctx, b, e);
 }
 
+
+
 }  // namespace adrom
+
+using namespace adrom;
+
+// ---------------------------------------------------------------------------
+// C-ABI: a streaming iSVD on the factored basis (include/adrom_b200.h)
+// ---------------------------------------------------------------------------
+struct adrom_isvd_stream {
+  adrom_ctx* ctx = nullptr;
+  int64_t n = 0;
+  int r = 0;
+  int kf = 0, acur = 0, cur = 0;
+  bool w_id = true;
+  double *A[2] = {nullptr, nullptr}, *Q = nullptr, *W[2] = {nullptr, nullptr};
+  double *sigma[2] = {nullptr, nullptr}, *G[2] = {nullptr, nullptr};
+  double *partial = nullptr, *partial_a = nullptr, *small = nullptr, *stats = nullptr;
+  std::vector<void*> allocs;
+  double* alloc(size_t count) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, sizeof(double) * (count ? count : 1)) != cudaSuccess) return nullptr;
+    allocs.push_back(p);
+    return (double*)p;
+  }
+};
+
+extern "C" {
+
+int adrom_isvd_stream_create(adrom_ctx* ctx, int64_t n, int32_t r, adrom_isvd_stream** out) {
+  if (!ctx || !out) return ADROM_ERR_ARG;
+  if (!(r == 32 || r == 64) || n < r)
+    return set_error(ctx, ADROM_ERR_ARG, "isvd stream: r must be 32 or 64 and n >= r");
+  adrom_isvd_stream* s = new adrom_isvd_stream();
+  s->ctx = ctx;
+  s->n = n;
+  s->r = r;
+  bool ok = true;
+  for (int b = 0; b < 2; ++b) {
+    ok &= (s->A[b] = s->alloc((size_t)n * r)) != nullptr;
+    ok &= (s->W[b] = s->alloc((size_t)(r + FACT_KQ + 1) * r)) != nullptr;
+    ok &= (s->sigma[b] = s->alloc(r)) != nullptr;
+    ok &= (s->G[b] = s->alloc((size_t)r * r)) != nullptr;
+  }
+  ok &= (s->Q = s->alloc((size_t)n * FACT_KQ)) != nullptr;
+  ok &= (s->partial = s->alloc(fact_partial_doubles(ctx, n, r))) != nullptr;
+  ok &= (s->partial_a = s->alloc(fact_partial_doubles(ctx, n, r))) != nullptr;
+  ok &= (s->small = s->alloc(fact_small_doubles(r))) != nullptr;
+  ok &= (s->stats = s->alloc(16)) != nullptr;
+  if (!ok) {
+    for (void* p : s->allocs) cudaFree(p);
+    delete s;
+    return set_error(ctx, ADROM_ERR_CUDA, "isvd stream: device allocation failed");
+  }
+  cudaMemsetAsync(s->Q, 0, sizeof(double) * (size_t)n * FACT_KQ, ctx->stream);
+  *out = s;
+  return ADROM_OK;
+}
+
+void adrom_isvd_stream_destroy(adrom_isvd_stream* s) {
+  if (!s) return;
+  cudaStreamSynchronize(s->ctx->stream);
+  for (void* p : s->allocs) cudaFree(p);
+  delete s;
+}
+
+int adrom_isvd_stream_load(adrom_isvd_stream* s, const double* phi, const double* sigma) {
+  if (!s) return ADROM_ERR_ARG;
+  adrom_ctx* ctx = s->ctx;
+  ADROM_CK(ctx, cudaMemcpyAsync(s->A[0], phi, sizeof(double) * (size_t)s->n * s->r,
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+  ADROM_CK(ctx, cudaMemcpyAsync(s->sigma[0], sigma, sizeof(double) * s->r, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+  s->kf = 0;
+  s->acur = 0;
+  s->cur = 0;
+  s->w_id = true;
+  return ts_gram(ctx, s->A[0], s->n, s->r, s->G[0], s->partial, fact_partial_doubles(ctx, s->n, s->r));
+}
+
+int adrom_isvd_stream_update(adrom_isvd_stream* s, const double* y_hat, double lam,
+                             adrom_isvd_info* host_info) {
+  if (!s) return ADROM_ERR_ARG;
+  adrom_ctx* ctx = s->ctx;
+  int st;
+  auto view = [&]() {
+    return FactBasis{s->A[s->acur], s->Q, s->r, s->w_id ? 0 : s->kf, s->w_id ? nullptr : s->W[s->cur], s->n};
+  };
+  if (s->kf == FACT_KQ) {  // re-anchor (same basis)
+    st = fact_reanchor(ctx, view(), s->A[1 - s->acur], nullptr);
+    if (st) return st;
+    s->acur = 1 - s->acur;
+    s->kf = 0;
+    s->w_id = true;
+  }
+  const int nxt = 1 - s->cur;
+  const FactBasis b = view();
+  FactEventArgs e{};
+  e.y = y_hat;
+  e.Qw = s->Q;
+  e.sigma = s->sigma[s->cur];
+  e.G = s->G[s->cur];
+  e.lam = lam;
+  e.partial = s->partial;
+  e.partial_a = s->partial_a;
+  e.small = s->small;
+  e.W_out = s->W[nxt];
+  e.sigma_out = s->sigma[nxt];
+  e.G_out = s->G[nxt];
+  e.stats = s->stats;
+  e.flag = ctx->dflags;
+  e.flag_a = ctx->dflags;
+  ADROM_CK(ctx, cudaMemsetAsync(ctx->dflags, 0, sizeof(int) * 16, ctx->stream));
+  st = fact_isvd_event(ctx, b, e);
+  if (st) return st;
+  int* hf = (int*)ctx->pinned;
+  double* hs = (double*)((char*)ctx->pinned + 256);
+  ADROM_CK(ctx, cudaMemcpyAsync(hf, ctx->dflags, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  ADROM_CK(ctx, cudaMemcpyAsync(hs, s->stats, sizeof(double) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  ADROM_CK(ctx, cudaStreamSynchronize(ctx->stream));
+  if (hf[0] & 1)  // dense.py:110 / tracking.py: non-finite input, basis unchanged
+    return set_error(ctx, ADROM_ERR_NONFINITE, "least_squares matrix contains non-finite entries");
+  if (hf[0] & 8)
+    return set_error(ctx, ADROM_ERR_NOCONV, "SVD did not converge for %dx%d input", s->r + 1, s->r + 1);
+  if (host_info) {
+    host_info->qnorm = hs[0];
+    host_info->ynorm = hs[1];
+    host_info->proj_resid = hs[2];
+    host_info->degenerate = (int)hs[3];
+    host_info->reorthogonalised = (int)hs[4];
+    host_info->sweeps = (int)hs[5];
+    host_info->pad = 0;
+  }
+  s->kf = b.k + 1;
+  s->w_id = false;
+  s->cur = nxt;
+  return ADROM_OK;
+}
+
+int adrom_isvd_stream_read(adrom_isvd_stream* s, double* phi_out, double* sigma_out) {
+  if (!s) return ADROM_ERR_ARG;
+  adrom_ctx* ctx = s->ctx;
+  if (sigma_out)
+    ADROM_CK(ctx, cudaMemcpyAsync(sigma_out, s->sigma[s->cur], sizeof(double) * s->r,
+                                  cudaMemcpyDeviceToDevice, ctx->stream));
+  if (phi_out) {
+    if (s->w_id) {
+      ADROM_CK(ctx, cudaMemcpyAsync(phi_out, s->A[s->acur], sizeof(double) * (size_t)s->n * s->r,
+                                    cudaMemcpyDeviceToDevice, ctx->stream));
+    } else {
+      const FactBasis b{s->A[s->acur], s->Q, s->r, s->kf, s->W[s->cur], s->n};
+      const int st = fact_reanchor(ctx, b, phi_out, nullptr);
+      if (st) return st;
+    }
+  }
+  return ADROM_OK;
+}
+
+}  // extern "C"

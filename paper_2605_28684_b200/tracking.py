@@ -114,3 +114,57 @@ def isvd_update(basis: ReducedBasis, y_hat, lam: float, r: int) -> ReducedBasis:
                       degenerate=bool(info.degenerate),
                       reorthogonalised=bool(info.reorthogonalised), sweeps=info.sweeps)
     return ReducedBasis(phi=_dev.like(phi_out, basis.phi), sigma=_dev.like(sigma_out, basis.sigma))
+
+
+class IsvdStream:
+    """Streaming form of ``isvd_update`` (B200 extension, r in {32, 64}).
+
+    Repeated ``basis = isvd_update(basis, y, lam, r)`` rewrites the N x r
+    basis every update (the O(N r^2) rotation, tracking.py:176-177).  The
+    stream keeps the same sequence of bases factored on the device,
+    Phi = [A | Q] W (csrc/factored.cu): an update costs two passes over the
+    basis plus O(r^3) work, and ``basis()`` materialises Phi when needed.
+    Every update is mathematically tracking.py:141-178; a failed update
+    (non-finite snapshot -> ``DenseError``) leaves the stream unchanged.
+    """
+
+    def __init__(self, basis: ReducedBasis):
+        phi = _dev.dev(basis.phi)
+        self.n, self.r = phi.shape
+        self._ctx = Context.get()
+        h = C.c_void_p()
+        self._ctx.call("adrom_isvd_stream_create", C.c_int64(self.n), C.c_int32(self.r), C.byref(h))
+        self._h = h
+        self._ctx.scall("adrom_isvd_stream_load", self._h, ptr(phi), ptr(_dev.dev(basis.sigma)))
+
+    def update(self, y_hat, lam: float) -> dict:
+        y = _dev.dev(y_hat)
+        if y.dim() != 1 or y.shape[0] != self.n:
+            raise ValueError(f"snapshot length {tuple(y.shape)} does not match basis rows {self.n}")
+        info = IsvdInfo()
+        self._ctx.scall("adrom_isvd_stream_update", self._h, ptr(y), C.c_double(lam), C.byref(info))
+        return dict(qnorm=info.qnorm, ynorm=info.ynorm, proj_resid=info.proj_resid,
+                    degenerate=bool(info.degenerate), sweeps=info.sweeps)
+
+    def basis_sigma(self):
+        """The current singular values (device vector, no basis materialisation)."""
+        sig = _dev.empty(self.r)
+        self._ctx.scall("adrom_isvd_stream_read", self._h, None, ptr(sig))
+        return sig
+
+    def basis(self) -> ReducedBasis:
+        phi = _dev.empty(self.n, self.r)
+        sig = _dev.empty(self.r)
+        self._ctx.scall("adrom_isvd_stream_read", self._h, ptr(phi), ptr(sig))
+        return ReducedBasis(phi=phi, sigma=sig)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._ctx.lib.adrom_isvd_stream_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass

@@ -88,3 +88,53 @@ def test_factored_vs_oracle_sod():
     assert dev.max() <= 1e-8, dev.max()
     assert np.array_equal(np.sort(rec.samplings[-1]), f["idx"])
     assert subspace.max_angle(rec.phi_final, f["phi"]) < 1e-8
+
+
+@pytest.mark.parametrize("n,r,lam", [(1 << 16, 64, 1.0), (1 << 15, 32, 0.5)])
+def test_isvd_stream_matches_repeated_updates(n, r, lam):
+    """IsvdStream (factored, 40 updates = 2 re-anchors) against the explicit
+    isvd_update chain and against the oracle's restatement of tracking.py."""
+    import paper_2605_28684_b200 as P
+    rng = np.random.default_rng(n + r)
+    k = r + 32
+    modes = np.linalg.qr(rng.standard_normal((n, k)))[0]
+    spec = np.arange(1, k + 1) ** -1.5
+    ys = [modes @ (spec * rng.standard_normal(k)) + 1e-6 * rng.standard_normal(n)
+          for _ in range(r + 40)]
+    u, s, _ = subspace.thin_svd(np.column_stack(ys[:r]))
+    b0 = P.ReducedBasis(phi=u[:, :r].copy(), sigma=s[:r].copy())
+    stream = P.tracking.IsvdStream(b0)
+    basis = b0
+    phi_c, sig_c = u[:, :r].copy(), s[:r].copy()
+    for y in ys[r:]:
+        stream.update(y, lam)
+        basis = P.isvd_update(basis, y, lam, r)
+        phi_c, sig_c, _ = subspace.isvd_update(phi_c, sig_c, y, lam, r)
+    got = stream.basis()
+    sig_f = got.sigma.cpu().numpy()
+    phi_f = got.phi.cpu().numpy()
+    assert np.allclose(sig_f, np.asarray(basis.sigma), rtol=1e-10)
+    assert np.allclose(sig_f, sig_c, rtol=1e-9)
+    assert subspace.max_angle(phi_c, phi_f) < 1e-8
+    assert subspace.max_angle(np.asarray(basis.phi), phi_f) < 1e-9
+    assert subspace.orthonormality_defect(phi_f) <= 1e-11
+    stream.close()
+
+
+def test_isvd_stream_rejects_nonfinite():
+    import paper_2605_28684_b200 as P
+    from paper_2605_28684_b200.errors import DenseError
+    n, r = 4096, 32
+    rng = np.random.default_rng(1)
+    phi = np.linalg.qr(rng.standard_normal((n, r)))[0]
+    st = P.tracking.IsvdStream(P.ReducedBasis(phi=phi, sigma=np.linspace(2, 1, r)))
+    st.update(rng.standard_normal(n), 0.9)
+    before = st.basis()
+    bad = rng.standard_normal(n)
+    bad[7] = np.nan
+    with pytest.raises(DenseError):
+        st.update(bad, 0.9)
+    after = st.basis()
+    assert np.array_equal(before.sigma.cpu().numpy(), after.sigma.cpu().numpy())
+    assert np.array_equal(before.phi.cpu().numpy(), after.phi.cpu().numpy())
+    st.close()
