@@ -29,9 +29,20 @@ __device__ __forceinline__ double hw_sum(double v) {
   return v;
 }
 
+template <int LP>
+__device__ __forceinline__ double lp_sum(double v) {
+#pragma unroll
+  for (int o = LP / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, LP);
+  return v;
+}
+
+// LP lanes per column pair (a power of two <= 32): fewer lanes -> fewer
+// warps per round and a cheaper barrier (the iSVD core uses 8).
+template <int LP = 16>
 __device__ inline JacobiResult block_jacobi(double* A, int lda, int m, int n, double* V, int ldv,
                                             int max_sweeps, double tol, int* sh_flag) {
-  const int tid = threadIdx.x, hl = tid & 15, hw = tid >> 4, nhw = blockDim.x >> 4;
+  constexpr int LSH = (LP == 32) ? 5 : (LP == 16) ? 4 : (LP == 8) ? 3 : (LP == 4) ? 2 : 1;
+  const int tid = threadIdx.x, hl = tid & (LP - 1), hw = tid >> LSH, nhw = blockDim.x >> LSH;
   if (V)  // V == nullptr: right rotations not accumulated
     for (int e = tid; e < n * n; e += blockDim.x) {
       const int c = e / n, rr = e - c * n;
@@ -50,8 +61,9 @@ __device__ inline JacobiResult block_jacobi(double* A, int lda, int m, int n, do
     for (int round = 0; round < ne - 1; ++round) {
       // pb is warp-uniform so both half-warps run the same iterations (the
       // 16-wide shuffles below are issued with the full warp mask)
-      for (int pb = (hw & ~1); pb < ne / 2; pb += nhw) {
-        const int pr = pb + (hw & 1);
+      constexpr int GPW = 32 / LP;  // pair groups per warp (loop stays warp-uniform)
+      for (int pb = (hw & ~(GPW - 1)); pb < ne / 2; pb += nhw) {
+        const int pr = pb + (hw & (GPW - 1));
         int a = 0, b = 0;
         if (pr == 0) {
           a = round;
@@ -70,23 +82,23 @@ __device__ inline JacobiResult block_jacobi(double* A, int lda, int m, int n, do
         double* ca = A + (size_t)a * lda;
         double* cb = A + (size_t)b * lda;
         if (live) {
-          for (int i = hl; i < m; i += 16) {
+          for (int i = hl; i < m; i += LP) {
             const double x = ca[i], y = cb[i];
             al += x * x;
             be += y * y;
             ga += x * y;
           }
         }
-        al = hw_sum(al);
-        be = hw_sum(be);
-        ga = hw_sum(ga);
+        al = lp_sum<LP>(al);
+        be = lp_sum<LP>(be);
+        ga = lp_sum<LP>(ga);
         if (!live || al == 0.0 || be == 0.0) continue;
         if (!(fabs(ga) > tol * sqrt(al * be))) continue;
         const double zeta = (be - al) / (2.0 * ga);
         const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
         const double c = 1.0 / sqrt(1.0 + t * t);
         const double s = c * t;
-        for (int i = hl; i < m; i += 16) {
+        for (int i = hl; i < m; i += LP) {
           const double x = ca[i], y = cb[i];
           ca[i] = c * x - s * y;
           cb[i] = s * x + c * y;
@@ -94,7 +106,7 @@ __device__ inline JacobiResult block_jacobi(double* A, int lda, int m, int n, do
         if (V) {
           double* va = V + (size_t)a * ldv;
           double* vb = V + (size_t)b * ldv;
-          for (int i = hl; i < n; i += 16) {
+          for (int i = hl; i < n; i += LP) {
             const double x = va[i], y = vb[i];
             va[i] = c * x - s * y;
             vb[i] = s * x + c * y;

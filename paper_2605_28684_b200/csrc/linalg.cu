@@ -1076,7 +1076,7 @@ __global__ void __launch_bounds__(1024) isvd_core_kernel(
     return;
   }
   fill_k(false);
-  JacobiResult jr = block_jacobi(A, ld, n, n, nullptr, ld, 30, 1e-15, &sh_flag);
+  JacobiResult jr = block_jacobi<16>(A, ld, n, n, nullptr, ld, 30, 1e-15, &sh_flag);
   column_norms_sorted(A, ld, n, n, s, order);
   // U column j = A column j / s_j, stored as V[j][k] = U[k][j]
   for (int e = tid; e < n * n; e += blockDim.x) {
@@ -1100,7 +1100,7 @@ __global__ void __launch_bounds__(1024) isvd_core_kernel(
   if (sh_fallback) {
     // one-sided Jacobi on K^T with accumulated rotations: U of K = V
     fill_k(true);
-    jr = block_jacobi(A, ld, n, n, V, ld, 60, 1e-15, &sh_flag);
+    jr = block_jacobi<16>(A, ld, n, n, V, ld, 60, 1e-15, &sh_flag);
     column_norms_sorted(A, ld, n, n, s, order);
   }
   // rotation factors B[k][c] = U[k][order[c]] (k = r_cur is u_bot)
@@ -1158,6 +1158,14 @@ __global__ void __launch_bounds__(1024) isvd_core_kernel(
     stats[6] = jr.converged;
     if (!jr.converged) atomicOr(flag, 8);
   }
+}
+
+// one column pair per half-warp: ceil((r+2)/2) pairs, rounded up to whole
+// warps (no idle warps in the per-round barrier)
+static int core_threads(int r_cur) {
+  const int pairs = (r_cur + 2) / 2;
+  const int t = ((pairs * 16 + 31) / 32) * 32;
+  return t < 64 ? 64 : (t > 1024 ? 1024 : t);
 }
 
 static size_t core_smem(int r_cur) {
@@ -1243,8 +1251,9 @@ int isvd_update_async(adrom_ctx* ctx, const double* phi, const double* sigma, co
   pr = prof_begin(ctx, PROBE_ISVD_CORE);
   // Gout may alias G: the kernel reads G completely before its final barrier
   double* Gout = gram_out ? gram_out : Gloc;
-  isvd_core_kernel<<<1, 1024, csm, ctx->stream>>>(sigma, red1, pls, red2, need, G, r_cur, r, lam,
-                                                  B, qinv, T, Gout, sigma_out, stats, flag, nullptr);
+  isvd_core_kernel<<<1, core_threads(r_cur), csm, ctx->stream>>>(sigma, red1, pls, red2, need, G,
+                                                                 r_cur, r, lam, B, qinv, T, Gout,
+                                                                 sigma_out, stats, flag, nullptr);
   prof_end(ctx, pr);
   ADROM_LAUNCH_CK(ctx);
   // the rotation reads q from pass 2 when it ran, else forms it from y and p
@@ -1271,8 +1280,9 @@ int isvd_core_launch(adrom_ctx* ctx, const double* sigma, const double* red1, co
                      double* stats, int* flag, double* udrop) {
   const size_t csm = core_smem(r);
   cudaFuncSetAttribute(isvd_core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
-  isvd_core_kernel<<<1, 1024, csm, ctx->stream>>>(sigma, red1, pls, red2, need, G, r, r, lam, B,
-                                                  qinv, T, Gout, sigma_out, stats, flag, udrop);
+  isvd_core_kernel<<<1, core_threads(r), csm, ctx->stream>>>(sigma, red1, pls, red2, need, G, r, r,
+                                                             lam, B, qinv, T, Gout, sigma_out, stats,
+                                                             flag, udrop);
   ADROM_LAUNCH_CK(ctx);
   return ADROM_OK;
 }
