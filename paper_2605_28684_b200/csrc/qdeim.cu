@@ -20,6 +20,7 @@
 //            greedy choice.
 // Small grids (N <= POOL_ALL) put every row in the pool: one pass.
 #include <cooperative_groups.h>
+#include <cuda_bf16.h>
 
 #include "common.cuh"
 #include "sampling_internal.cuh"
@@ -28,6 +29,8 @@
 #include <limits.h>
 #include <stdio.h>
 #include <stdlib.h>
+
+#include <vector>
 
 namespace cg = cooperative_groups;
 
@@ -921,6 +924,306 @@ static int qp_refresh_tc(adrom_ctx* ctx, const double* phi, const double* Qx, in
   return ADROM_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Split-bf16 refresh (the default).  A refresh only has to produce valid UPPER
+// bounds of the residuals -- the pool rows' exact residuals come from
+// qp_resvec in fp64 and decide every pivot -- so S = X_rows Mm[:, v:k] runs on
+// the bf16 tensor cores (mma.sync m16n8k16, 15x the FP64 DMMA rate here):
+// x = x0 + x1 and m = m0 + m1 (bf16 each), x0 m0 + x0 m1 + x1 m0 accumulated
+// in fp32.  Rows of Mm are scaled by exact powers of two to max |m| in
+// [1/2, 1) and the matching columns of X by the inverse, so
+//   |S^_il - S_il| <= delta_l = QP_BF_GAMMA ||x~_i|| ||m~_l|| + tiny
+// (Cauchy-Schwarz; the dropped terms are ~3.1 u_bf16^2 |x||m| plus fp32
+// accumulation; QP_BF_GAMMA = 8 u_bf16^2 leaves a factor > 2), and the bound
+// subtracts only (|S^_il| - delta_l)_+^2 <= S_il^2.  res2 stays an upper
+// bound of the residual; bnd2 adds the fp64 slack as before.
+// ---------------------------------------------------------------------------
+constexpr double QP_BF_GAMMA = 8.0 / 65536.0;
+constexpr double QP_BF_TINY = 1e-33;
+
+__device__ __forceinline__ void qp_bmma(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                        uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// fast split for the row fragments: x -> f = fp32(x) (error 2^-24 |x|, inside
+// the dropped terms), hi = bf16(f), lo = bf16(f - hi) (f - hi exact in fp32)
+__device__ __forceinline__ void qp_split2f(double x, double y, uint32_t& hi, uint32_t& lo) {
+  const float2 f = make_float2((float)x, (float)y);
+  const __nv_bfloat162 h = __float22bfloat162_rn(f);
+  const float2 hf = __bfloat1622float2(h);
+  const __nv_bfloat162 l = __float22bfloat162_rn(make_float2(f.x - hf.x, f.y - hf.y));
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+
+// (x, y) -> packed bf16 pairs hi = (x0, y0), lo = (x1, y1); lower half = x
+__device__ __forceinline__ void qp_split2(double x, double y, uint32_t& hi, uint32_t& lo) {
+  const __nv_bfloat16 xh = __float2bfloat16_rn((float)x), yh = __float2bfloat16_rn((float)y);
+  const __nv_bfloat16 xl = __float2bfloat16_rn((float)(x - (double)__bfloat162float(xh)));
+  const __nv_bfloat16 yl = __float2bfloat16_rn((float)(y - (double)__bfloat162float(yh)));
+  hi = (uint32_t)__bfloat16_as_ushort(xh) | ((uint32_t)__bfloat16_as_ushort(yh) << 16);
+  lo = (uint32_t)__bfloat16_as_ushort(xl) | ((uint32_t)__bfloat16_as_ushort(yl) << 16);
+}
+
+template <int R, bool FACT>
+struct QpBf {
+  static constexpr int KX = FACT ? R + FACT_KQ : R;  // inner dimension (multiple of 16)
+  static constexpr int KS = KX / 16;                 // k-steps
+  static constexpr int NT = R / 8;                   // direction tiles
+  static constexpr int CPR = KX / 2;                 // 16-byte chunks per row
+  static constexpr int RS = KX + 8;                  // staged row stride (doubles): rows g,
+                                                     // g+1 land on opposite bank halves
+  static constexpr int WPB = (R >= 128) ? 4 : 8;     // warps per block
+  static constexpr int STAGE = 16 * RS;              // one 16-row tile (doubles)
+  // smem: B fragments (KS x NT x 32 lanes x uint4), x scales (KX), ||m~_l|| (R),
+  // two staged tiles per warp
+  static constexpr size_t smem_bytes =
+      sizeof(uint4) * KS * NT * 32 + sizeof(double) * (KX + R + (size_t)WPB * 2 * STAGE) +
+      sizeof(float) * R;
+};
+
+__device__ __forceinline__ void qp_cp16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem),
+               "r"(src_bytes));
+}
+
+// Each warp owns 16-row tiles of the refresh list and stages the next tile's
+// rows (gathered, 16-byte cp.async) while the current one is on the tensor
+// cores: the gather is latency bound otherwise.
+template <int R, bool FACT>
+__global__ void __launch_bounds__(QpBf<R, FACT>::WPB * 32, 1)
+    qp_refresh_bf_kernel(const double* __restrict__ phi, const double* __restrict__ Qx, int kf,
+                         const double* __restrict__ nrmb, const int64_t* __restrict__ list,
+                         int64_t cap, const double* __restrict__ Mm, int k,
+                         double* __restrict__ res2, double* __restrict__ bnd2,
+                         unsigned char* __restrict__ ver) {
+  using C = QpBf<R, FACT>;
+  constexpr int KX = C::KX, KS = C::KS, NT = C::NT, CPR = C::CPR, RS = C::RS, WPB = C::WPB;
+  extern __shared__ __align__(16) unsigned char qbf_sm[];
+  uint4* Bs = reinterpret_cast<uint4*>(qbf_sm);
+  double* xsc = reinterpret_cast<double*>(Bs + KS * NT * 32);  // 2^e_j (x side)
+  double* mn = xsc + KX;                                       // ||m~_l|| (rounded up)
+  double* stg_all = mn + R;
+  float* mnf = reinterpret_cast<float*>(stg_all + (size_t)WPB * 2 * C::STAGE);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t tiles = (cap + 15) / 16;
+  const int64_t tstride = (int64_t)gridDim.x * WPB;
+  int64_t tl = (int64_t)blockIdx.x * WPB + warp;
+  double* stg = stg_all + (size_t)warp * 2 * C::STAGE;
+  auto load_list = [&](int64_t tt) -> int64_t {
+    const int64_t pos = tt * 16 + (lane & 15);
+    return (tt < tiles && pos < cap) ? list[pos] : -1;
+  };
+  // 8 lanes per row (128-byte lines), 4 rows per instruction
+  auto issue = [&](int64_t li, double* dst) {
+    const int sub = lane & 7;
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      const int p = (lane >> 3) + 4 * rr;
+      const int64_t i = __shfl_sync(0xffffffffu, li, p);
+      const int nb = i >= 0 ? 16 : 0;
+      const int64_t ii = i >= 0 ? i : 0;
+      const double* srcA = phi + ii * R + 2 * sub;
+      double* d = dst + p * RS + 2 * sub;
+#pragma unroll
+      for (int j = 0; j < CPR / 8; ++j) {
+        if (8 * j < R / 2) qp_cp16(d + 16 * j, srcA + 16 * j, nb);
+        else qp_cp16(d + 16 * j, Qx + ii * FACT_KQ + 2 * sub + 16 * (j - R / 16), nb);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n");
+  };
+  // first tile's gather overlaps the prologue
+  int64_t li_cur = load_list(tl);
+  issue(li_cur, stg);
+  int v_cur = (lane < 16 && li_cur >= 0) ? (int)ver[li_cur] : k;
+  int64_t li_next = load_list(tl + tstride);
+  // row scales of Mm (directions l < k only)
+  for (int j = threadIdx.x; j < KX; j += blockDim.x) {
+    double mx = 0.0;
+    for (int l = 0; l < k; ++l) mx = fmax(mx, fabs(Mm[j * R + l]));
+    int e = 0;
+    if (mx > 0.0 && isfinite(mx)) frexp(mx, &e);
+    xsc[j] = ldexp(1.0, e);
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < R; l += blockDim.x) {
+    double sm = 0.0;
+    if (l < k)
+      for (int j = 0; j < KX; ++j) {
+        const double m = Mm[j * R + l] / xsc[j];
+        sm = fma(m, m, sm);
+      }
+    mn[l] = sqrt(sm) * (1.0 + 1e-14);
+    mnf[l] = __double2float_ru(mn[l]);
+  }
+  for (int e = threadIdx.x; e < KS * NT * 32; e += blockDim.x) {
+    const int ln = e & 31, nt = (e >> 5) % NT, ks = (e >> 5) / NT;
+    const int gg = ln >> 2, tt = ln & 3, l = 8 * nt + gg;
+    const int j0 = 16 * ks + 2 * tt, j1 = j0 + 8;
+    auto m = [&](int j) { return (l < k) ? Mm[j * R + l] / xsc[j] : 0.0; };
+    uint4 b;
+    qp_split2(m(j0), m(j0 + 1), b.x, b.z);
+    qp_split2(m(j1), m(j1 + 1), b.y, b.w);
+    Bs[e] = b;
+  }
+  __syncthreads();
+  int s = 0;
+  for (; tl < tiles; tl += tstride) {
+    const int64_t tn = tl + tstride;
+    issue(li_next, stg + (s ^ 1) * C::STAGE);  // empty rows when tn >= tiles
+    const int v_next = (lane < 16 && li_next >= 0) ? (int)ver[li_next] : k;
+    const int64_t li_nn = load_list(tn + tstride);
+    const int vmin = __reduce_min_sync(0xffffffffu, v_cur);
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    __syncwarp();
+    if (vmin < k) {
+      int64_t ir[2];
+      int vr[2];
+      double r2o[2] = {0.0, 0.0}, b2o[2] = {0.0, 0.0}, nrm[2] = {0.0, 0.0};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        ir[h] = __shfl_sync(0xffffffffu, li_cur, g + 8 * h);
+        vr[h] = __shfl_sync(0xffffffffu, v_cur, g + 8 * h);
+        if (t == 0 && ir[h] >= 0 && vr[h] < k) {  // consumed after the MMAs
+          r2o[h] = res2[ir[h]];
+          b2o[h] = bnd2[ir[h]];
+          if (FACT) nrm[h] = nrmb[ir[h]];
+        }
+      }
+      const double* st = stg + s * C::STAGE;
+      uint32_t ah[KS][4], al[KS][4];
+      double ss[2] = {0.0, 0.0}, nn[2] = {0.0, 0.0};
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {  // fragment register q: row g + 8 (q & 1), cols + 8 (q >> 1)
+          const int h = q & 1;
+          const int c = 16 * ks + 8 * (q >> 1) + 2 * t;
+          double2 x = *reinterpret_cast<const double2*>(st + (g + 8 * h) * RS + c);
+          if (FACT && c >= R) {  // Q columns >= kf may hold a rejected event's data
+            if (c - R >= kf) x.x = 0.0;
+            if (c + 1 - R >= kf) x.y = 0.0;
+          }
+          if (!FACT) nn[h] = fma(x.x, x.x, fma(x.y, x.y, nn[h]));
+          x.x *= xsc[c];
+          x.y *= xsc[c + 1];
+          ss[h] = fma(x.x, x.x, fma(x.y, x.y, ss[h]));
+          qp_split2f(x.x, x.y, ah[ks][q], al[ks][q]);
+        }
+      }
+      // per-row error scale in fp32, rounded up (covers the fp32 rounding of
+      // delta = dx * mn_l + tiny)
+      float dx[2], dt0[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        ss[h] += __shfl_xor_sync(0xffffffffu, ss[h], 1);
+        ss[h] += __shfl_xor_sync(0xffffffffu, ss[h], 2);
+        const double xn = sqrt(ss[h]) * (1.0 + 1e-14);
+        dx[h] = __double2float_ru(QP_BF_GAMMA * xn * (1.0 + 1e-6));
+        dt0[h] = __double2float_ru(QP_BF_TINY * (1.0 + xn) * (1.0 + 1e-6));
+        if (!FACT) {
+          nn[h] += __shfl_xor_sync(0xffffffffu, nn[h], 1);
+          nn[h] += __shfl_xor_sync(0xffffffffu, nn[h], 2);
+          nrm[h] = nn[h];
+        }
+      }
+      // sum of (|S^| - delta)_+^2 in fp32; every rounding can only inflate it
+      // by (1 + 2^-24) per operation (<= KX + 8 operations per term and sum),
+      // removed by the (1 - 2^-14) factor below
+      float sub[2] = {0.f, 0.f};
+      const int t0 = vmin >> 3, t1 = (k + 7) >> 3;
+      // two direction tiles per iteration, the three products in separate
+      // accumulators: six independent MMA chains
+      for (int d0 = t0; d0 < t1; d0 += 2) {
+        const bool two = d0 + 1 < t1;
+        float c[2][3][4];
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int p = 0; p < 3; ++p)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) c[u][p][e] = 0.f;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const uint4 b0 = Bs[(ks * NT + d0) * 32 + lane];
+          qp_bmma(c[0][0], ah[ks], b0.x, b0.y);
+          qp_bmma(c[0][1], ah[ks], b0.z, b0.w);
+          qp_bmma(c[0][2], al[ks], b0.x, b0.y);
+          if (two) {
+            const uint4 b1 = Bs[(ks * NT + d0 + 1) * 32 + lane];
+            qp_bmma(c[1][0], ah[ks], b1.x, b1.y);
+            qp_bmma(c[1][1], ah[ks], b1.z, b1.w);
+            qp_bmma(c[1][2], al[ks], b1.x, b1.y);
+          }
+        }
+        // c[u][.][2h + e] = S^[row g + 8h][direction 8 (d0 + u) + 2t + e]
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (u == 1 && !two) break;
+          const float2 m2 = *reinterpret_cast<const float2*>(mnf + 8 * (d0 + u) + 2 * t);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int h = q >> 1, l = 8 * (d0 + u) + 2 * t + (q & 1);
+            const float sv = (c[u][0][q] + c[u][1][q]) + c[u][2][q];
+            float a = fabsf(sv) - fmaf(dx[h], (q & 1) ? m2.y : m2.x, dt0[h]);
+            a = (l >= vr[h] && l < k && a > 0.f) ? a : 0.f;
+            sub[h] = fmaf(a, a, sub[h]);
+          }
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        sub[h] += __shfl_xor_sync(0xffffffffu, sub[h], 1);
+        sub[h] += __shfl_xor_sync(0xffffffffu, sub[h], 2);
+        const int64_t i = ir[h];
+        if (t == 0 && i >= 0 && vr[h] < k && isfinite(sub[h])) {
+          const double r2 = fmax(r2o[h] - (double)sub[h] * (1.0 - 1.0 / 16384.0), 0.0);
+          res2[i] = r2;
+          ver[i] = (unsigned char)k;
+          bnd2[i] = fmin(b2o[h], r2 + 8.0 * (double)(k + 2) * QP_EPS * nrm[h]);
+        }
+      }
+    }
+    __syncwarp();  // stage s is re-filled by the next iteration's issue
+    li_cur = li_next;
+    v_cur = v_next;
+    li_next = li_nn;
+    s ^= 1;
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+static bool qp_refresh_fp64() {
+  static const bool v = getenv("ADROM_QDEIM_REFRESH_FP64") && atoi(getenv("ADROM_QDEIM_REFRESH_FP64"));
+  return v;
+}
+
+template <int R, bool FACT>
+static int qp_refresh_bf(adrom_ctx* ctx, const double* phi, const double* Qx, int kf,
+                         const double* nrmb, const int64_t* list, int64_t cap, const double* Mm,
+                         int k, double* res2, double* bnd2, unsigned char* ver) {
+  if (qp_refresh_fp64()) return qp_refresh_tc<R, FACT>(ctx, phi, Qx, kf, nrmb, list, cap, Mm, k, res2, bnd2, ver);
+  using C = QpBf<R, FACT>;
+  const size_t sm = C::smem_bytes;
+  const int64_t tiles = (cap + 15) / 16;
+  int64_t g = (tiles + C::WPB - 1) / C::WPB;
+  if (g > (int64_t)ctx->num_sms) g = (int64_t)ctx->num_sms;
+  cudaFuncSetAttribute(qp_refresh_bf_kernel<R, FACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sm);
+  qp_refresh_bf_kernel<R, FACT><<<(int)(g < 1 ? 1 : g), C::WPB * 32, sm, ctx->stream>>>(
+      phi, Qx, kf, nrmb, list, cap, Mm, k, res2, bnd2, ver);
+  ADROM_LAUNCH_CK(ctx);
+  return ADROM_OK;
+}
+
 // Mm ((r + FACT_KQ) x r) = W D for the directions l < k (rows >= r + kf zero)
 __global__ void qp_wd_kernel(const double* __restrict__ W, int rkf, int r,
                              const double* __restrict__ D, int k, double* __restrict__ Mm) {
@@ -1110,20 +1413,43 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
         ADROM_LAUNCH_CK(ctx);
         qs_compact_kernel<<<sg, 256, 0, ctx->stream>>>(bnd2, n, nullptr, selR, rlist, cap);
         ADROM_LAUNCH_CK(ctx);
+        if (getenv("ADROM_QDEIM_TRACE") && atoi(getenv("ADROM_QDEIM_TRACE")) >= 2) {
+          // refresh work: direction tiles of 8 computed per 8-row tile vs per row
+          std::vector<int64_t> hl(cap);
+          std::vector<unsigned char> hv(n);
+          cudaMemcpyAsync(hl.data(), rlist, sizeof(int64_t) * cap, cudaMemcpyDeviceToHost, ctx->stream);
+          cudaMemcpyAsync(hv.data(), ver, n, cudaMemcpyDeviceToHost, ctx->stream);
+          cudaStreamSynchronize(ctx->stream);
+          long long rows = 0, v0 = 0, tile_work = 0, row_work = 0;
+          for (int64_t t = 0; t < cap; t += 8) {
+            int vmin = k;
+            for (int64_t p = t; p < t + 8 && p < cap; ++p) {
+              if (hl[p] < 0) continue;
+              const int v = hv[hl[p]];
+              ++rows;
+              v0 += v == 0;
+              if (v < vmin) vmin = v;
+              if (v < k) row_work += (k + 7) / 8 - v / 8;
+            }
+            if (vmin < k) tile_work += 8LL * ((k + 7) / 8 - vmin / 8);
+          }
+          fprintf(stderr, "qdeim refresh: k=%d rows=%lld ver0=%lld tile_work=%lld row_work=%lld\n", k,
+                  rows, v0, tile_work, row_work);
+        }
         if (fact) {
           qp_wd_kernel<<<(r + FACT_KQ) * r / 256 + 1, 256, 0, ctx->stream>>>(fb->W, r + fb->k, r, D,
                                                                             k, Mw);
           ADROM_LAUNCH_CK(ctx);
-          st = (r == 32) ? qp_refresh_tc<32, true>(ctx, fb->A, fb->Q, fb->k, nrmb, rlist, cap, Mw,
+          st = (r == 32) ? qp_refresh_bf<32, true>(ctx, fb->A, fb->Q, fb->k, nrmb, rlist, cap, Mw,
                                                    k, res2, bnd2, ver)
-                         : qp_refresh_tc<64, true>(ctx, fb->A, fb->Q, fb->k, nrmb, rlist, cap, Mw,
+                         : qp_refresh_bf<64, true>(ctx, fb->A, fb->Q, fb->k, nrmb, rlist, cap, Mw,
                                                    k, res2, bnd2, ver);
         } else if (r == 32 || r == 64 || r == 128) {
           st = (r == 32)
-                   ? qp_refresh_tc<32, false>(ctx, phi, nullptr, 0, nullptr, rlist, cap, D, k, res2, bnd2, ver)
+                   ? qp_refresh_bf<32, false>(ctx, phi, nullptr, 0, nullptr, rlist, cap, D, k, res2, bnd2, ver)
                : (r == 64)
-                   ? qp_refresh_tc<64, false>(ctx, phi, nullptr, 0, nullptr, rlist, cap, D, k, res2, bnd2, ver)
-                   : qp_refresh_tc<128, false>(ctx, phi, nullptr, 0, nullptr, rlist, cap, D, k, res2, bnd2, ver);
+                   ? qp_refresh_bf<64, false>(ctx, phi, nullptr, 0, nullptr, rlist, cap, D, k, res2, bnd2, ver)
+                   : qp_refresh_bf<128, false>(ctx, phi, nullptr, 0, nullptr, rlist, cap, D, k, res2, bnd2, ver);
         } else {
           st = rows_pass(cap, k, QP_REFRESH, rlist, n_ex);
         }
