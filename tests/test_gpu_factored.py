@@ -48,7 +48,9 @@ def _run(case, steps, fact, offline=None):
 @pytest.mark.parametrize("name,n,steps,tol", [
     ("cfg1", 4096, 40, 1e-10),     # Sod, r = 32, FGS: well conditioned
     ("cfg3", 1 << 16, 40, 1e-6),   # Burgers, r = 64, z = 1: ~59 noise directions,
-])                                 # 40 events = 2 re-anchors
+                                   # 40 events = 2 re-anchors
+    ("cfg3", 1 << 18, 20, 1e-6),   # above the all-rows pool limit: the factored
+])                                 # refresh of the certified QDEIM pool
 def test_factored_matches_explicit(name, n, steps, tol):
     case = bench.rom_case(name, n)
     e = _run(case, steps, fact=False)

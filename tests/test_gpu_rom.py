@@ -73,6 +73,19 @@ def test_qdeim_vs_oracle_greedy(n, r, n_s):
     assert list(P.qdeim_sample(_basis(phi), n_s).indices) == want
 
 
+@pytest.mark.parametrize("n,r,span", [(1 << 17, 128, 4), (1 << 17, 64, 12), (150001, 32, 30)])
+def test_qdeim_pool_graded_rows(n, r, span):
+    """Pool path (refresh on the bf16 tensor cores with certified bounds) on
+    bases whose row norms span 10^span: the bounds must stay valid across
+    the whole range for the pivots to equal the exact greedy's."""
+    P = _pkg()
+    rng = np.random.default_rng(n + r + span)
+    w = 10.0 ** (-span * rng.random(n))
+    phi = np.linalg.qr(w[:, None] * rng.standard_normal((n, r)))[0]
+    want, _ = hyper.greedy_pivots(phi, r)
+    assert list(P.qdeim_sample(_basis(phi), r).indices) == want
+
+
 def test_qdeim_pod_basis_vs_lapack():
     # realistic smooth basis (Burgers POD, cfg-0 physics at N=4096): geqp3 pivots
     P = _pkg()
