@@ -60,6 +60,12 @@ static long long qp_refresh_slack() {
   return t;
 }
 
+// the refresh set may also grow to its capacity (ADROM_QDEIM_EXTEND_REFRESH)
+static int qp_extend_refresh() {
+  static const int v = getenv("ADROM_QDEIM_EXTEND_REFRESH") ? atoi(getenv("ADROM_QDEIM_EXTEND_REFRESH")) : 0;
+  return v;
+}
+
 static long long qp_pool_m() {
   static long long t = [] {
     const char* e = getenv("ADROM_QDEIM_POOL_M");
@@ -133,6 +139,12 @@ struct SelState {
   unsigned long long count;  // compaction counter
 };
 
+// radix select in 12-bit digits: bits 63..52 (sign + exponent) first, then
+// the mantissa 12 bits at a time (passes at shifts 52, 40, 28, 16, 4, 0; the
+// last one is 4 bits wide)
+constexpr int QS_BITS = 12, QS_BINS = 1 << QS_BITS;
+__host__ __device__ inline int qs_bits(int shift) { return shift == 0 ? 4 : QS_BITS; }
+
 __global__ void qs_init_kernel(SelState* st, long long M, unsigned int* hist) {
   if (threadIdx.x == 0) {
     st->prefix = 0ull;
@@ -144,47 +156,68 @@ __global__ void qs_init_kernel(SelState* st, long long M, unsigned int* hist) {
     st->tau = -1.0;
     st->count = 0ull;
   }
-  for (int j = threadIdx.x; j < 256; j += blockDim.x) hist[j] = 0u;
+  for (int j = threadIdx.x; j < QS_BINS; j += blockDim.x) hist[j] = 0u;
 }
 
-// candidates: rows 0..n-1, or (list != null) the rows list[0..n) (-1 = empty)
-__global__ void __launch_bounds__(256) qs_hist_kernel(const double* __restrict__ bnd2, int64_t n,
-                                                      const int64_t* __restrict__ list,
+// histogram of the next digit over the candidates vals[0..n) (contiguous:
+// the bounds of every row, or of the refresh list's rows in list order)
+__global__ void __launch_bounds__(256) qs_hist_kernel(const double* __restrict__ vals, int64_t n,
                                                       const SelState* __restrict__ st, int shift,
                                                       unsigned int* __restrict__ hist) {
   if (st->done) return;
-  __shared__ unsigned int sh[256];
-  sh[threadIdx.x] = 0u;
+  constexpr int ITEMS = 8;
+  __shared__ unsigned int sh[QS_BINS];
+  for (int b = threadIdx.x; b < QS_BINS; b += blockDim.x) sh[b] = 0u;
   __syncthreads();
   const unsigned long long prefix = st->prefix, mask = st->mask;
+  const unsigned long long dmask = (1ull << qs_bits(shift)) - 1ull;
   const int lane = threadIdx.x & 31;
-  // bounds crowd into a few bins: aggregate equal digits per warp first
-  for (int64_t b0 = blockIdx.x * (int64_t)blockDim.x; b0 < n; b0 += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = b0 + threadIdx.x;
-    const int64_t i = (j < n) ? (list ? list[j] : j) : -1;
-    int dig = -1;
-    if (i >= 0) {
-      const unsigned long long k = qp_key(bnd2[i]);
-      if (k != 0ull && (k & mask) == prefix) dig = (int)((k >> shift) & 255ull);
+  const int64_t tile = (int64_t)blockDim.x * ITEMS;
+  for (int64_t t0 = blockIdx.x * tile; t0 < n; t0 += (int64_t)gridDim.x * tile) {
+    double v[ITEMS];
+#pragma unroll
+    for (int q = 0; q < ITEMS; ++q) {
+      const int64_t j = t0 + (int64_t)q * blockDim.x + threadIdx.x;
+      v[q] = (j < n) ? vals[j] : -1.0;
     }
-    const unsigned int peers = __match_any_sync(0xffffffffu, dig);
-    if (dig >= 0 && lane == __ffs(peers) - 1) atomicAdd(&sh[dig], (unsigned int)__popc(peers));
+#pragma unroll
+    for (int q = 0; q < ITEMS; ++q) {
+      const unsigned long long k = qp_key(v[q]);
+      const int dig = (k != 0ull && (k & mask) == prefix) ? (int)((k >> shift) & dmask) : -1;
+      // bounds crowd into a few bins: aggregate equal digits per warp first
+      const int d0 = __shfl_sync(0xffffffffu, dig, 0);
+      if (__all_sync(0xffffffffu, dig == d0)) {
+        if (lane == 0 && d0 >= 0) atomicAdd(&sh[d0], 32u);
+      } else {
+        const unsigned int peers = __match_any_sync(0xffffffffu, dig);
+        if (dig >= 0 && lane == __ffs(peers) - 1) atomicAdd(&sh[dig], (unsigned int)__popc(peers));
+      }
+    }
   }
   __syncthreads();
-  const unsigned int c = sh[threadIdx.x];
-  if (c) atomicAdd(&hist[threadIdx.x], c);
+  for (int b = threadIdx.x; b < QS_BINS; b += blockDim.x) {
+    const unsigned int c = sh[b];
+    if (c) atomicAdd(&hist[b], c);
+  }
 }
 
-// one block of 256: pick the digit holding the need-th largest remaining key
-__global__ void __launch_bounds__(256) qs_digit_kernel(SelState* st, int shift,
-                                                       unsigned int* __restrict__ hist,
-                                                       long long pcap) {
+// one block of 1024 (4 bins each, from the top): pick the digit holding the
+// need-th largest remaining key
+__global__ void __launch_bounds__(1024) qs_digit_kernel(SelState* st, int shift,
+                                                        unsigned int* __restrict__ hist,
+                                                        long long pcap, int extend) {
   if (st->done) return;
-  __shared__ long long wsum[8];
-  __shared__ int dig_sh;
+  __shared__ long long wsum[32];
+  __shared__ int dig_sh, dlow_sh;
   __shared__ long long excl_sh, bin_sh;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const long long h = hist[255 - tid];
+  long long hb[4];
+  long long h = 0;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    hb[e] = hist[QS_BINS - 1 - (4 * tid + e)];
+    h += hb[e];
+  }
   long long v = h;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -192,19 +225,41 @@ __global__ void __launch_bounds__(256) qs_digit_kernel(SelState* st, int shift,
     if (lane >= o) v += x;
   }
   if (lane == 31) wsum[warp] = v;
-  if (tid == 0) dig_sh = -1;
+  if (tid == 0) {
+    dig_sh = -1;
+    dlow_sh = QS_BINS;
+  }
   __syncthreads();
   long long off = 0;
   for (int w = 0; w < warp; ++w) off += wsum[w];
-  const long long incl = v + off, excl = incl - h;
+  const long long incl = v + off;
+  long long excl = incl - h;
   const long long need = st->need;
+  // the pool may take every bin from the top down to the lowest one whose
+  // cumulative count still fits the capacity (and holds the need-th key)
+  if (extend) {
+    const long long limit = pcap - st->above;
+    long long c = excl;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      c += hb[e];
+      if (hb[e] > 0 && c >= need && c <= limit) atomicMin(&dlow_sh, QS_BINS - 1 - (4 * tid + e));
+    }
+  }
   if (excl < need && incl >= need) {
-    dig_sh = 255 - tid;
-    excl_sh = excl;
-    bin_sh = h;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (excl < need && excl + hb[e] >= need) {
+        dig_sh = QS_BINS - 1 - (4 * tid + e);
+        excl_sh = excl;
+        bin_sh = hb[e];
+      }
+      excl += hb[e];
+    }
   }
   __syncthreads();
-  hist[tid] = 0u;  // ready for the next round
+#pragma unroll
+  for (int e = 0; e < 4; ++e) hist[4 * tid + e] = 0u;  // ready for the next pass
   if (tid == 0) {
     if (dig_sh < 0) {  // fewer candidates than M: take every live row
       st->theta = 1ull;
@@ -212,9 +267,16 @@ __global__ void __launch_bounds__(256) qs_digit_kernel(SelState* st, int shift,
       st->done = 1;
       return;
     }
+    if (dlow_sh < QS_BINS) {  // bins dlow.. of this prefix fit: done
+      const unsigned long long th = st->prefix | ((unsigned long long)dlow_sh << shift);
+      st->theta = th < 1ull ? 1ull : th;
+      st->tau = (st->theta >= 2ull) ? __longlong_as_double((long long)(st->theta - 2ull)) : -1.0;
+      st->done = 1;
+      return;
+    }
     const unsigned long long d = (unsigned long long)dig_sh;
     st->prefix |= d << shift;
-    st->mask |= 255ull << shift;
+    st->mask |= ((1ull << qs_bits(shift)) - 1ull) << shift;
     st->above += excl_sh;
     st->need = need - excl_sh;
     const long long with_bin = st->above + bin_sh;
@@ -231,7 +293,7 @@ __global__ void __launch_bounds__(256) qs_digit_kernel(SelState* st, int shift,
 }
 
 // rows with key >= theta -> out[0..), one atomic per block and round
-__global__ void __launch_bounds__(256) qs_compact_kernel(const double* __restrict__ bnd2, int64_t n,
+__global__ void __launch_bounds__(256) qs_compact_kernel(const double* __restrict__ vals, int64_t n,
                                                          const int64_t* __restrict__ list,
                                                          SelState* __restrict__ st,
                                                          int64_t* __restrict__ out, long long cap) {
@@ -248,9 +310,8 @@ __global__ void __launch_bounds__(256) qs_compact_kernel(const double* __restric
 #pragma unroll
     for (int q = 0; q < ITEMS; ++q) {
       const int64_t j = t0 + (int64_t)q * blockDim.x + threadIdx.x;
-      const int64_t i = (j < n) ? (list ? list[j] : j) : -1;
-      const bool take = i >= 0 && qp_key(bnd2[i]) >= theta;
-      rows[q] = take ? i : -1;
+      const bool take = j < n && qp_key(vals[j]) >= theta;
+      rows[q] = take ? (list ? list[j] : j) : -1;
       balls[q] = __ballot_sync(0xffffffffu, take);
       mine += __popc(balls[q]);
     }
@@ -788,7 +849,8 @@ size_t qdeim_pool_workspace_bytes(int64_t n, int r, int count) {
   b += align_up(sizeof(int64_t) * (size_t)P);              // pool idx
   b += align_up(sizeof(double) * (size_t)P * r);           // Rv
   b += 2 * align_up(sizeof(double) * (size_t)P);           // pres2, pn2
-  b += 2 * align_up(sizeof(SelState)) + align_up(sizeof(unsigned int) * 256);  // selection
+  b += 2 * align_up(sizeof(SelState)) + align_up(sizeof(unsigned int) * QS_BINS);  // selection
+  b += align_up(sizeof(double) * (size_t)n);               // bounds in refresh-list order
   b += align_up(sizeof(int64_t) * (size_t)n);              // refresh list
   b += align_up(sizeof(double) * (size_t)(r + FACT_KQ) * r);  // W D (factored rows)
   b += align_up((size_t)n);                                // per-row downdate version
@@ -1002,7 +1064,7 @@ __global__ void __launch_bounds__(QpBf<R, FACT>::WPB * 32, 1)
                          const double* __restrict__ nrmb, const int64_t* __restrict__ list,
                          int64_t cap, const double* __restrict__ Mm, int k,
                          double* __restrict__ res2, double* __restrict__ bnd2,
-                         unsigned char* __restrict__ ver) {
+                         unsigned char* __restrict__ ver, double* __restrict__ blist) {
   using C = QpBf<R, FACT>;
   constexpr int KX = C::KX, KS = C::KS, NT = C::NT, CPR = C::CPR, RS = C::RS, WPB = C::WPB;
   extern __shared__ __align__(16) unsigned char qbf_sm[];
@@ -1084,7 +1146,10 @@ __global__ void __launch_bounds__(QpBf<R, FACT>::WPB * 32, 1)
     const int vmin = __reduce_min_sync(0xffffffffu, v_cur);
     asm volatile("cp.async.wait_group 1;\n" ::: "memory");
     __syncwarp();
-    if (vmin < k) {
+    if (vmin >= k) {  // nothing new: the list-order bounds only
+      const int64_t pos = tl * 16 + lane;
+      if (lane < 16 && pos < cap) blist[pos] = (li_cur >= 0) ? bnd2[li_cur] : -1.0;
+    } else {
       int64_t ir[2];
       int vr[2];
       double r2o[2] = {0.0, 0.0}, b2o[2] = {0.0, 0.0}, nrm[2] = {0.0, 0.0};
@@ -1092,10 +1157,12 @@ __global__ void __launch_bounds__(QpBf<R, FACT>::WPB * 32, 1)
       for (int h = 0; h < 2; ++h) {
         ir[h] = __shfl_sync(0xffffffffu, li_cur, g + 8 * h);
         vr[h] = __shfl_sync(0xffffffffu, v_cur, g + 8 * h);
-        if (t == 0 && ir[h] >= 0 && vr[h] < k) {  // consumed after the MMAs
-          r2o[h] = res2[ir[h]];
+        if (t == 0 && ir[h] >= 0) {  // consumed after the MMAs
           b2o[h] = bnd2[ir[h]];
-          if (FACT) nrm[h] = nrmb[ir[h]];
+          if (vr[h] < k) {
+            r2o[h] = res2[ir[h]];
+            if (FACT) nrm[h] = nrmb[ir[h]];
+          }
         }
       }
       const double* st = stg + s * C::STAGE;
@@ -1184,11 +1251,17 @@ __global__ void __launch_bounds__(QpBf<R, FACT>::WPB * 32, 1)
         sub[h] += __shfl_xor_sync(0xffffffffu, sub[h], 1);
         sub[h] += __shfl_xor_sync(0xffffffffu, sub[h], 2);
         const int64_t i = ir[h];
-        if (t == 0 && i >= 0 && vr[h] < k && isfinite(sub[h])) {
-          const double r2 = fmax(r2o[h] - (double)sub[h] * (1.0 - 1.0 / 16384.0), 0.0);
-          res2[i] = r2;
-          ver[i] = (unsigned char)k;
-          bnd2[i] = fmin(b2o[h], r2 + 8.0 * (double)(k + 2) * QP_EPS * nrm[h]);
+        const int64_t pos = tl * 16 + g + 8 * h;
+        if (t == 0 && pos < cap) {
+          double b = (i >= 0) ? b2o[h] : -1.0;
+          if (i >= 0 && vr[h] < k && isfinite(sub[h])) {
+            const double r2 = fmax(r2o[h] - (double)sub[h] * (1.0 - 1.0 / 16384.0), 0.0);
+            res2[i] = r2;
+            ver[i] = (unsigned char)k;
+            b = fmin(b, r2 + 8.0 * (double)(k + 2) * QP_EPS * nrm[h]);
+            bnd2[i] = b;
+          }
+          blist[pos] = b;
         }
       }
     }
@@ -1206,11 +1279,34 @@ static bool qp_refresh_fp64() {
   return v;
 }
 
+// blist[p] = bound of list[p] (-1 for empty slots): the pool selection reads
+// the refreshed bounds contiguously
+__global__ void qp_list_bounds_kernel(const int64_t* __restrict__ list, int64_t cap,
+                                      const double* __restrict__ bnd2, double* __restrict__ blist) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < cap;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = list[p];
+    blist[p] = (i >= 0) ? bnd2[i] : -1.0;
+  }
+}
+
+static int qp_list_bounds(adrom_ctx* ctx, const int64_t* list, int64_t cap, const double* bnd2,
+                          double* blist) {
+  int64_t g = (cap + 255) / 256;
+  if (g > (int64_t)ctx->num_sms * 8) g = (int64_t)ctx->num_sms * 8;
+  qp_list_bounds_kernel<<<(int)(g < 1 ? 1 : g), 256, 0, ctx->stream>>>(list, cap, bnd2, blist);
+  ADROM_LAUNCH_CK(ctx);
+  return ADROM_OK;
+}
+
 template <int R, bool FACT>
 static int qp_refresh_bf(adrom_ctx* ctx, const double* phi, const double* Qx, int kf,
                          const double* nrmb, const int64_t* list, int64_t cap, const double* Mm,
-                         int k, double* res2, double* bnd2, unsigned char* ver) {
-  if (qp_refresh_fp64()) return qp_refresh_tc<R, FACT>(ctx, phi, Qx, kf, nrmb, list, cap, Mm, k, res2, bnd2, ver);
+                         int k, double* res2, double* bnd2, unsigned char* ver, double* blist) {
+  if (qp_refresh_fp64()) {
+    const int st = qp_refresh_tc<R, FACT>(ctx, phi, Qx, kf, nrmb, list, cap, Mm, k, res2, bnd2, ver);
+    return st ? st : qp_list_bounds(ctx, list, cap, bnd2, blist);
+  }
   using C = QpBf<R, FACT>;
   const size_t sm = C::smem_bytes;
   const int64_t tiles = (cap + 15) / 16;
@@ -1219,7 +1315,7 @@ static int qp_refresh_bf(adrom_ctx* ctx, const double* phi, const double* Qx, in
   cudaFuncSetAttribute(qp_refresh_bf_kernel<R, FACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sm);
   qp_refresh_bf_kernel<R, FACT><<<(int)(g < 1 ? 1 : g), C::WPB * 32, sm, ctx->stream>>>(
-      phi, Qx, kf, nrmb, list, cap, Mm, k, res2, bnd2, ver);
+      phi, Qx, kf, nrmb, list, cap, Mm, k, res2, bnd2, ver, blist);
   ADROM_LAUNCH_CK(ctx);
   return ADROM_OK;
 }
@@ -1308,7 +1404,8 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
   SelState* sel = (SelState*)take(sizeof(SelState));
   SelState* selR = (SelState*)take(sizeof(SelState));
   int64_t* rlist = (int64_t*)take(sizeof(int64_t) * (size_t)n);
-  unsigned int* hist = (unsigned int*)take(sizeof(unsigned int) * 256);
+  unsigned int* hist = (unsigned int*)take(sizeof(unsigned int) * QS_BINS);
+  double* blist = (double*)take(sizeof(double) * (size_t)n);  // bounds in refresh-list order
   double* Mw = (double*)take(sizeof(double) * (size_t)(r + FACT_KQ) * r);
   double* D = (double*)take(sizeof(double) * (size_t)r * r);
   int64_t* piv = (int64_t*)take(sizeof(int64_t) * (size_t)r);
@@ -1363,15 +1460,19 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
   };
   const int sg = ctx->num_sms * 4;
   // theta/tau of the rows holding the M largest bounds (<= cap rows taken)
-  auto select = [&](SelState* st, const int64_t* list, int64_t nn, long long M,
-                    long long cap) -> int {
+  auto select = [&](SelState* st, const double* vals, int64_t nn, long long M,
+                    long long cap, int extend) -> int {
     qs_init_kernel<<<1, 256, 0, ctx->stream>>>(st, M, hist);
     ADROM_LAUNCH_CK(ctx);
-    for (int shift = 56; shift >= 0; shift -= 8) {
-      qs_hist_kernel<<<sg, 256, 0, ctx->stream>>>(bnd2, nn, list, st, shift, hist);
+    int64_t hg = (nn + 2047) / 2048;
+    if (hg > sg) hg = sg;
+    for (int shift = 64 - QS_BITS;; shift -= QS_BITS) {
+      if (shift < 0) shift = 0;
+      qs_hist_kernel<<<(int)(hg < 1 ? 1 : hg), 256, 0, ctx->stream>>>(vals, nn, st, shift, hist);
       ADROM_LAUNCH_CK(ctx);
-      qs_digit_kernel<<<1, 256, 0, ctx->stream>>>(st, shift, hist, cap);
+      qs_digit_kernel<<<1, 1024, 0, ctx->stream>>>(st, shift, hist, cap, extend);
       ADROM_LAUNCH_CK(ctx);
+      if (shift == 0) break;
     }
     return ADROM_OK;
   };
@@ -1405,7 +1506,7 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
         // refresh the mref rows with the largest (possibly stale) bounds
         const long long capm = mref + (mref * qp_refresh_slack()) / 100;
         const long long cap = (capm < n) ? capm : n;
-        st = select(selR, nullptr, n, mref, cap);
+        st = select(selR, bnd2, n, mref, cap, qp_extend_refresh());
         if (st) return st;
         int64_t fg = (cap + 255) / 256;
         if (fg > ctx->num_sms * 8) fg = ctx->num_sms * 8;
@@ -1441,17 +1542,18 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
                                                                             k, Mw);
           ADROM_LAUNCH_CK(ctx);
           st = (r == 32) ? qp_refresh_bf<32, true>(ctx, fb->A, fb->Q, fb->k, nrmb, rlist, cap, Mw,
-                                                   k, res2, bnd2, ver)
+                                                   k, res2, bnd2, ver, blist)
                          : qp_refresh_bf<64, true>(ctx, fb->A, fb->Q, fb->k, nrmb, rlist, cap, Mw,
-                                                   k, res2, bnd2, ver);
+                                                   k, res2, bnd2, ver, blist);
         } else if (r == 32 || r == 64 || r == 128) {
           st = (r == 32)
-                   ? qp_refresh_bf<32, false>(ctx, phi, nullptr, 0, nullptr, rlist, cap, D, k, res2, bnd2, ver)
+                   ? qp_refresh_bf<32, false>(ctx, phi, nullptr, 0, nullptr, rlist, cap, D, k, res2, bnd2, ver, blist)
                : (r == 64)
-                   ? qp_refresh_bf<64, false>(ctx, phi, nullptr, 0, nullptr, rlist, cap, D, k, res2, bnd2, ver)
-                   : qp_refresh_bf<128, false>(ctx, phi, nullptr, 0, nullptr, rlist, cap, D, k, res2, bnd2, ver);
+                   ? qp_refresh_bf<64, false>(ctx, phi, nullptr, 0, nullptr, rlist, cap, D, k, res2, bnd2, ver, blist)
+                   : qp_refresh_bf<128, false>(ctx, phi, nullptr, 0, nullptr, rlist, cap, D, k, res2, bnd2, ver, blist);
         } else {
           st = rows_pass(cap, k, QP_REFRESH, rlist, n_ex);
+          if (!st) st = qp_list_bounds(ctx, rlist, cap, bnd2, blist);
         }
         if (st) return st;
         ++refreshed;
@@ -1470,12 +1572,13 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
         // pool = the M largest bounds among the refreshed rows (rows outside the
         // refresh list are bounded by selR->tau), or among all rows
         const int64_t* cl = rl_n ? rlist : nullptr;
+        const double* cv = rl_n ? blist : bnd2;
         const int64_t cn = rl_n ? rl_n : n;
-        st = select(sel, cl, cn, M, (long long)P);
+        st = select(sel, cv, cn, M, (long long)P, 1);
         if (st) return st;
         qp_fill_kernel<<<(int)gg, 256, 0, ctx->stream>>>(pool_idx, P);
         ADROM_LAUNCH_CK(ctx);
-        qs_compact_kernel<<<sg, 256, 0, ctx->stream>>>(bnd2, cn, cl, sel, pool_idx, (long long)P);
+        qs_compact_kernel<<<sg, 256, 0, ctx->stream>>>(cv, cn, cl, sel, pool_idx, (long long)P);
         ADROM_LAUNCH_CK(ctx);
       }
       st = resvec(k);
