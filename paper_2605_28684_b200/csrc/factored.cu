@@ -379,7 +379,8 @@ __global__ void __launch_bounds__(256, 1) reanchor_kernel(const double* __restri
                                                           const double* __restrict__ Q, int k,
                                                           const double* __restrict__ W, int64_t n,
                                                           double* __restrict__ out,
-                                                          double* __restrict__ nrm2) {
+                                                          double* __restrict__ nrm2,
+                                                          float* __restrict__ out32) {
   using C = ReTC<R>;
   extern __shared__ __align__(16) double sm[];
   double* X0 = sm;                          // 2 stages x TM x S
@@ -456,6 +457,9 @@ __global__ void __launch_bounds__(256, 1) reanchor_kernel(const double* __restri
         for (int j = 0; j < C::NT; ++j) {
           const double2 v = make_double2(acc[i][j][0], acc[i][j][1]);
           *reinterpret_cast<double2*>(dst + ec + 8 * j) = v;
+          if (out32)
+            *reinterpret_cast<float2*>(out32 + (row0 + rr) * R + ec + 8 * j) =
+                make_float2((float)v.x, (float)v.y);
           nr += v.x * v.x + v.y * v.y;
         }
       }
@@ -604,14 +608,15 @@ size_t fact_partial_doubles(adrom_ctx* ctx, int64_t n, int r) {
   return (size_t)((n + XP_ROWS - 1) / XP_ROWS) * xpass_width(r, FACT_KQ, 2);
 }
 
-int fact_reanchor(adrom_ctx* ctx, const FactBasis& b, double* out, double* nrm2) {
+int fact_reanchor(adrom_ctx* ctx, const FactBasis& b, double* out, double* nrm2, float* out32) {
   auto launch = [&](auto kern, size_t smd) -> int {
     const size_t sm = sizeof(double) * smd;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     const int64_t nt = (b.n + 63) / 64;
     int64_t g = (int64_t)ctx->num_sms;
     if (g > nt) g = nt;
-    kern<<<(int)(g < 1 ? 1 : g), 256, sm, ctx->stream>>>(b.A, b.Q, b.k, b.W, b.n, out, nrm2);
+    kern<<<(int)(g < 1 ? 1 : g), 256, sm, ctx->stream>>>(b.A, b.Q, b.k, b.W, b.n, out, nrm2,
+                                                         out32);
     ADROM_LAUNCH_CK(ctx);
     return ADROM_OK;
   };

@@ -14,6 +14,8 @@ struct FactBasis {
   int r, k;
   const double* W;  // (r + k) x r row-major, or null
   int64_t n;
+  // optional fp32 shadow of A (the QDEIM refresh gathers it)
+  const float* A32 = nullptr;
 };
 
 struct FactEventArgs {
@@ -70,7 +72,9 @@ int fact_decode(adrom_ctx* ctx, const FactBasis& b, const double* a, const doubl
                 const double* d, double* q_tilde, double* small, double* partial);
 
 // out (n x r) = X W (tensor cores); exact row norms into nrm2 (optional)
-int fact_reanchor(adrom_ctx* ctx, const FactBasis& b, double* out, double* nrm2);
+// (out32: optional fp32 copy of out)
+int fact_reanchor(adrom_ctx* ctx, const FactBasis& b, double* out, double* nrm2,
+                  float* out32 = nullptr);
 
 // rows_out[p] = Phi_{rows[p]} (r doubles each) for p < min(count, *dcount)
 // (rows[p] < 0 -> zeros; dcount: optional device-side count)

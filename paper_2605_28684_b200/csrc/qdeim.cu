@@ -1032,21 +1032,31 @@ __device__ __forceinline__ void qp_split2(double x, double y, uint32_t& hi, uint
   lo = (uint32_t)__bfloat16_as_ushort(xl) | ((uint32_t)__bfloat16_as_ushort(yl) << 16);
 }
 
-template <int R, bool FACT>
+// T: element type of the staged anchor rows -- the fp64 basis itself, or
+// (factored session) its fp32 shadow, half the gather bytes; the fragments
+// are fp32 splits either way, so the results are identical.  The residual
+// columns Q (factored rows) are gathered in fp64.
+template <int R, bool FACT, typename T>
 struct QpBf {
   static constexpr int KX = FACT ? R + FACT_KQ : R;  // inner dimension (multiple of 16)
   static constexpr int KS = KX / 16;                 // k-steps
   static constexpr int NT = R / 8;                   // direction tiles
-  static constexpr int CPR = KX / 2;                 // 16-byte chunks per row
-  static constexpr int RS = KX + 8;                  // staged row stride (doubles): rows g,
-                                                     // g+1 land on opposite bank halves
-  static constexpr int WPB = (R >= 128) ? 4 : 8;     // warps per block
-  static constexpr int STAGE = 16 * RS;              // one 16-row tile (doubles)
+  static constexpr int EPC = 16 / (int)sizeof(T);    // elements per 16-byte chunk
+  static constexpr int LC = (sizeof(T) == 8) ? 8 : 4;  // lanes per anchor row in the gather
+  static constexpr int RPI = 32 / LC;                // anchor rows per gather instruction
+  static constexpr int RS = R + 8;                   // staged anchor row stride (elements):
+                                                     // fragment loads are conflict-free
+  static constexpr int RSQ = FACT_KQ + 8;            // staged Q row stride (doubles)
+  static constexpr int WPB = (R >= 128) ? 4 : (sizeof(T) == 4 ? 12 : 8);  // warps per block
+  static constexpr int STAGE = 16 * RS;              // one 16-row anchor tile (elements)
+  static constexpr int STAGEQ = FACT ? 16 * RSQ : 0;  // one 16-row Q tile (doubles)
+  static constexpr size_t STAGE_BYTES = sizeof(T) * STAGE + sizeof(double) * STAGEQ;
   // smem: B fragments (KS x NT x 32 lanes x uint4), x scales (KX), ||m~_l|| (R),
-  // two staged tiles per warp
-  static constexpr size_t smem_bytes =
-      sizeof(uint4) * KS * NT * 32 + sizeof(double) * (KX + R + (size_t)WPB * 2 * STAGE) +
-      sizeof(float) * R;
+  // two staged tiles per warp, ||m~_l|| in fp32 (R), x scales in fp32 (KX)
+  static constexpr size_t smem_bytes = sizeof(uint4) * KS * NT * 32 +
+                                       sizeof(double) * (KX + R) +
+                                       (size_t)WPB * 2 * STAGE_BYTES + sizeof(float) * (R + KX);
+  static_assert((R / EPC) % LC == 0 && STAGE_BYTES % 16 == 0, "gather split");
 };
 
 __device__ __forceinline__ void qp_cp16(void* smem, const void* gmem, int src_bytes) {
@@ -1058,53 +1068,68 @@ __device__ __forceinline__ void qp_cp16(void* smem, const void* gmem, int src_by
 // Each warp owns 16-row tiles of the refresh list and stages the next tile's
 // rows (gathered, 16-byte cp.async) while the current one is on the tensor
 // cores: the gather is latency bound otherwise.
-template <int R, bool FACT>
-__global__ void __launch_bounds__(QpBf<R, FACT>::WPB * 32, 1)
-    qp_refresh_bf_kernel(const double* __restrict__ phi, const double* __restrict__ Qx, int kf,
+template <int R, bool FACT, typename T>
+__global__ void __launch_bounds__(QpBf<R, FACT, T>::WPB * 32, 1)
+    qp_refresh_bf_kernel(const T* __restrict__ phi, const double* __restrict__ Qx, int kf,
                          const double* __restrict__ nrmb, const int64_t* __restrict__ list,
                          int64_t cap, const double* __restrict__ Mm, int k,
                          double* __restrict__ res2, double* __restrict__ bnd2,
                          unsigned char* __restrict__ ver, double* __restrict__ blist) {
-  using C = QpBf<R, FACT>;
-  constexpr int KX = C::KX, KS = C::KS, NT = C::NT, CPR = C::CPR, RS = C::RS, WPB = C::WPB;
+  using C = QpBf<R, FACT, T>;
+  constexpr int KX = C::KX, KS = C::KS, NT = C::NT, RS = C::RS, WPB = C::WPB;
+  constexpr int EPC = C::EPC, LC = C::LC, RPI = C::RPI;
   extern __shared__ __align__(16) unsigned char qbf_sm[];
   uint4* Bs = reinterpret_cast<uint4*>(qbf_sm);
   double* xsc = reinterpret_cast<double*>(Bs + KS * NT * 32);  // 2^e_j (x side)
   double* mn = xsc + KX;                                       // ||m~_l|| (rounded up)
-  double* stg_all = mn + R;
-  float* mnf = reinterpret_cast<float*>(stg_all + (size_t)WPB * 2 * C::STAGE);
+  unsigned char* stg_all = reinterpret_cast<unsigned char*>(mn + R);
+  float* mnf = reinterpret_cast<float*>(stg_all + (size_t)WPB * 2 * C::STAGE_BYTES);
+  float* xscf = mnf + R;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int64_t tiles = (cap + 15) / 16;
   const int64_t tstride = (int64_t)gridDim.x * WPB;
   int64_t tl = (int64_t)blockIdx.x * WPB + warp;
-  double* stg = stg_all + (size_t)warp * 2 * C::STAGE;
+  unsigned char* stg = stg_all + (size_t)warp * 2 * C::STAGE_BYTES;
+  auto tileA = [&](int b) { return reinterpret_cast<T*>(stg + b * C::STAGE_BYTES); };
+  auto tileQ = [&](int b) {
+    return reinterpret_cast<double*>(stg + b * C::STAGE_BYTES + sizeof(T) * C::STAGE);
+  };
   auto load_list = [&](int64_t tt) -> int64_t {
     const int64_t pos = tt * 16 + (lane & 15);
     return (tt < tiles && pos < cap) ? list[pos] : -1;
   };
-  // 8 lanes per row (128-byte lines), 4 rows per instruction
-  auto issue = [&](int64_t li, double* dst) {
-    const int sub = lane & 7;
+  // anchor rows: LC lanes per row (whole 128-byte lines per instruction); Q
+  // rows (fp64, 128 bytes): 8 lanes per row
+  auto issue = [&](int64_t li, int b) {
+    T* dA = tileA(b);
+    const int sub = lane % LC;
 #pragma unroll
-    for (int rr = 0; rr < 4; ++rr) {
-      const int p = (lane >> 3) + 4 * rr;
+    for (int rr = 0; rr < 16 / RPI; ++rr) {
+      const int p = lane / LC + RPI * rr;
       const int64_t i = __shfl_sync(0xffffffffu, li, p);
       const int nb = i >= 0 ? 16 : 0;
-      const int64_t ii = i >= 0 ? i : 0;
-      const double* srcA = phi + ii * R + 2 * sub;
-      double* d = dst + p * RS + 2 * sub;
+      const T* srcA = phi + (i >= 0 ? i : 0) * R + EPC * sub;
+      T* d = dA + p * RS + EPC * sub;
 #pragma unroll
-      for (int j = 0; j < CPR / 8; ++j) {
-        if (8 * j < R / 2) qp_cp16(d + 16 * j, srcA + 16 * j, nb);
-        else qp_cp16(d + 16 * j, Qx + ii * FACT_KQ + 2 * sub + 16 * (j - R / 16), nb);
+      for (int j = 0; j < R / EPC / LC; ++j) qp_cp16(d + EPC * LC * j, srcA + EPC * LC * j, nb);
+    }
+    if (FACT) {
+      double* dQ = tileQ(b);
+      const int sq = lane & 7;
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr) {
+        const int p = (lane >> 3) + 4 * rr;
+        const int64_t i = __shfl_sync(0xffffffffu, li, p);
+        qp_cp16(dQ + p * C::RSQ + 2 * sq, Qx + (i >= 0 ? i : 0) * FACT_KQ + 2 * sq,
+                i >= 0 ? 16 : 0);
       }
     }
     asm volatile("cp.async.commit_group;\n");
   };
   // first tile's gather overlaps the prologue
   int64_t li_cur = load_list(tl);
-  issue(li_cur, stg);
+  issue(li_cur, 0);
   int v_cur = (lane < 16 && li_cur >= 0) ? (int)ver[li_cur] : k;
   int64_t li_next = load_list(tl + tstride);
   // row scales of Mm (directions l < k only)
@@ -1114,6 +1139,7 @@ __global__ void __launch_bounds__(QpBf<R, FACT>::WPB * 32, 1)
     int e = 0;
     if (mx > 0.0 && isfinite(mx)) frexp(mx, &e);
     xsc[j] = ldexp(1.0, e);
+    xscf[j] = (float)xsc[j];
   }
   __syncthreads();
   for (int l = threadIdx.x; l < R; l += blockDim.x) {
@@ -1140,7 +1166,7 @@ __global__ void __launch_bounds__(QpBf<R, FACT>::WPB * 32, 1)
   int s = 0;
   for (; tl < tiles; tl += tstride) {
     const int64_t tn = tl + tstride;
-    issue(li_next, stg + (s ^ 1) * C::STAGE);  // empty rows when tn >= tiles
+    issue(li_next, s ^ 1);  // empty rows when tn >= tiles
     const int v_next = (lane < 16 && li_next >= 0) ? (int)ver[li_next] : k;
     const int64_t li_nn = load_list(tn + tstride);
     const int vmin = __reduce_min_sync(0xffffffffu, v_cur);
@@ -1165,26 +1191,55 @@ __global__ void __launch_bounds__(QpBf<R, FACT>::WPB * 32, 1)
           }
         }
       }
-      const double* st = stg + s * C::STAGE;
+      const T* stA = tileA(s);
+      const double* stQ = tileQ(s);
       uint32_t ah[KS][4], al[KS][4];
       double ss[2] = {0.0, 0.0}, nn[2] = {0.0, 0.0};
+      float ssf[2] = {0.f, 0.f};
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {  // fragment register q: row g + 8 (q & 1), cols + 8 (q >> 1)
           const int h = q & 1;
           const int c = 16 * ks + 8 * (q >> 1) + 2 * t;
-          double2 x = *reinterpret_cast<const double2*>(st + (g + 8 * h) * RS + c);
-          if (FACT && c >= R) {  // Q columns >= kf may hold a rejected event's data
-            if (c - R >= kf) x.x = 0.0;
-            if (c + 1 - R >= kf) x.y = 0.0;
+          if (sizeof(T) == 8 || c >= R) {
+            double2 x;
+            if (c < R) {
+              x = *reinterpret_cast<const double2*>(stA + (g + 8 * h) * RS + c);
+            } else {  // Q columns >= kf may hold a rejected event's data
+              x = *reinterpret_cast<const double2*>(stQ + (g + 8 * h) * C::RSQ + c - R);
+              if (c - R >= kf) x.x = 0.0;
+              if (c + 1 - R >= kf) x.y = 0.0;
+            }
+            if (!FACT) nn[h] = fma(x.x, x.x, fma(x.y, x.y, nn[h]));
+            x.x *= xsc[c];
+            x.y *= xsc[c + 1];
+            if (sizeof(T) == 8) {
+              ss[h] = fma(x.x, x.x, fma(x.y, x.y, ss[h]));
+              qp_split2f(x.x, x.y, ah[ks][q], al[ks][q]);
+            } else {
+              const float2 f = make_float2((float)x.x, (float)x.y);
+              ssf[h] = fmaf(f.x, f.x, fmaf(f.y, f.y, ssf[h]));
+              qp_split2f(x.x, x.y, ah[ks][q], al[ks][q]);
+            }
+          } else {
+            // fp32 shadow: the same fp32 values qp_split2f would form
+            float2 x = *reinterpret_cast<const float2*>(stA + (g + 8 * h) * RS + c);
+            x.x *= xscf[c];
+            x.y *= xscf[c + 1];
+            ssf[h] = fmaf(x.x, x.x, fmaf(x.y, x.y, ssf[h]));
+            const __nv_bfloat162 hb = __float22bfloat162_rn(x);
+            const float2 hf = __bfloat1622float2(hb);
+            const __nv_bfloat162 lb = __float22bfloat162_rn(make_float2(x.x - hf.x, x.y - hf.y));
+            ah[ks][q] = *reinterpret_cast<const uint32_t*>(&hb);
+            al[ks][q] = *reinterpret_cast<const uint32_t*>(&lb);
           }
-          if (!FACT) nn[h] = fma(x.x, x.x, fma(x.y, x.y, nn[h]));
-          x.x *= xsc[c];
-          x.y *= xsc[c + 1];
-          ss[h] = fma(x.x, x.x, fma(x.y, x.y, ss[h]));
-          qp_split2f(x.x, x.y, ah[ks][q], al[ks][q]);
         }
+      }
+      if constexpr (sizeof(T) == 4) {
+        // fp32 sum of KX squares: relative error < KX 2^-24, covered by 1e-5
+#pragma unroll
+        for (int h = 0; h < 2; ++h) ss[h] = (double)ssf[h] * (1.0 + 1e-5);
       }
       // per-row error scale in fp32, rounded up (covers the fp32 rounding of
       // delta = dx * mn_l + tiny)
@@ -1299,25 +1354,40 @@ static int qp_list_bounds(adrom_ctx* ctx, const int64_t* list, int64_t cap, cons
   return ADROM_OK;
 }
 
-template <int R, bool FACT>
-static int qp_refresh_bf(adrom_ctx* ctx, const double* phi, const double* Qx, int kf,
-                         const double* nrmb, const int64_t* list, int64_t cap, const double* Mm,
-                         int k, double* res2, double* bnd2, unsigned char* ver, double* blist) {
-  if (qp_refresh_fp64()) {
-    const int st = qp_refresh_tc<R, FACT>(ctx, phi, Qx, kf, nrmb, list, cap, Mm, k, res2, bnd2, ver);
-    return st ? st : qp_list_bounds(ctx, list, cap, bnd2, blist);
-  }
-  using C = QpBf<R, FACT>;
+template <int R, bool FACT, typename T>
+static int qp_refresh_bf_launch(adrom_ctx* ctx, const T* phi, const double* Qx, int kf,
+                                const double* nrmb, const int64_t* list, int64_t cap,
+                                const double* Mm, int k, double* res2, double* bnd2,
+                                unsigned char* ver, double* blist) {
+  using C = QpBf<R, FACT, T>;
   const size_t sm = C::smem_bytes;
   const int64_t tiles = (cap + 15) / 16;
   int64_t g = (tiles + C::WPB - 1) / C::WPB;
   if (g > (int64_t)ctx->num_sms) g = (int64_t)ctx->num_sms;
-  cudaFuncSetAttribute(qp_refresh_bf_kernel<R, FACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)sm);
-  qp_refresh_bf_kernel<R, FACT><<<(int)(g < 1 ? 1 : g), C::WPB * 32, sm, ctx->stream>>>(
+  cudaFuncSetAttribute(qp_refresh_bf_kernel<R, FACT, T>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  qp_refresh_bf_kernel<R, FACT, T><<<(int)(g < 1 ? 1 : g), C::WPB * 32, sm, ctx->stream>>>(
       phi, Qx, kf, nrmb, list, cap, Mm, k, res2, bnd2, ver, blist);
   ADROM_LAUNCH_CK(ctx);
   return ADROM_OK;
+}
+
+// refresh on the bf16 tensor cores; factored rows come from the fp32 shadows
+// when the session keeps them (phi32, Qx32), else from the fp64 basis
+template <int R, bool FACT>
+static int qp_refresh_bf(adrom_ctx* ctx, const double* phi, const double* Qx, int kf,
+                         const double* nrmb, const int64_t* list, int64_t cap, const double* Mm,
+                         int k, double* res2, double* bnd2, unsigned char* ver, double* blist,
+                         const float* phi32 = nullptr) {
+  if (qp_refresh_fp64()) {
+    const int st = qp_refresh_tc<R, FACT>(ctx, phi, Qx, kf, nrmb, list, cap, Mm, k, res2, bnd2, ver);
+    return st ? st : qp_list_bounds(ctx, list, cap, bnd2, blist);
+  }
+  if (FACT && phi32)
+    return qp_refresh_bf_launch<R, FACT, float>(ctx, phi32, Qx, kf, nrmb, list, cap, Mm, k, res2,
+                                                bnd2, ver, blist);
+  return qp_refresh_bf_launch<R, FACT, double>(ctx, phi, Qx, kf, nrmb, list, cap, Mm, k, res2, bnd2,
+                                               ver, blist);
 }
 
 // Mm ((r + FACT_KQ) x r) = W D for the directions l < k (rows >= r + kf zero)
@@ -1542,9 +1612,9 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
                                                                             k, Mw);
           ADROM_LAUNCH_CK(ctx);
           st = (r == 32) ? qp_refresh_bf<32, true>(ctx, fb->A, fb->Q, fb->k, nrmb, rlist, cap, Mw,
-                                                   k, res2, bnd2, ver, blist)
+                                                   k, res2, bnd2, ver, blist, fb->A32)
                          : qp_refresh_bf<64, true>(ctx, fb->A, fb->Q, fb->k, nrmb, rlist, cap, Mw,
-                                                   k, res2, bnd2, ver, blist);
+                                                   k, res2, bnd2, ver, blist, fb->A32);
         } else if (r == 32 || r == 64 || r == 128) {
           st = (r == 32)
                    ? qp_refresh_bf<32, false>(ctx, phi, nullptr, 0, nullptr, rlist, cap, D, k, res2, bnd2, ver, blist)

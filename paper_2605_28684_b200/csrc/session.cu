@@ -109,6 +109,8 @@ struct adrom_session {
   int kf = 0, acur = 0;
   bool w_id = true;
   double* Qb = nullptr;
+  // fp32 shadows of phi[b] (A32[b]), gathered by the QDEIM refresh
+  float* A32[2] = {nullptr, nullptr};
   double* Wd[2] = {nullptr, nullptr};
   double* nrm2[2] = {nullptr, nullptr};
   double* vdrop[2] = {nullptr, nullptr};  // dropped direction of the event that made cur
@@ -166,7 +168,13 @@ adrom_model model_of(const adrom_session* s) { return s->cfg.model; }
 // the current basis as a factored view (W = null: phi[acur] itself)
 FactBasis basis_view(const adrom_session* s) {
   return FactBasis{s->phi[s->acur], s->Qb, s->r, s->w_id ? 0 : s->kf,
-                   s->w_id ? nullptr : s->Wd[s->cur], s->N};
+                   s->w_id ? nullptr : s->Wd[s->cur], s->N, s->A32[s->acur]};
+}
+
+__global__ void to_f32_kernel(const double* __restrict__ x, int64_t n, float* __restrict__ y) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = (float)x[i];
 }
 
 __global__ void row_norms_kernel(const double* __restrict__ phi, int64_t n, int r,
@@ -383,7 +391,8 @@ int run_event_factored(adrom_session* s, adrom_event_record& ev, bool* decoded) 
                       256, 0, fc->stream>>>(s->y_corr, s->q_ref, s->d, s->N, s->y_hat);
   ADROM_LAUNCH_CK(fc);
   if (s->kf == FACT_KQ) {  // re-anchor: A = X W (same basis), exact row norms
-    st = fact_reanchor(fc, basis_view(s), s->phi[1 - s->acur], s->nrm2[s->cur]);
+    st = fact_reanchor(fc, basis_view(s), s->phi[1 - s->acur], s->nrm2[s->cur],
+                       s->A32[1 - s->acur]);
     if (st) return st;
     s->acur = 1 - s->acur;
     s->kf = 0;
@@ -453,7 +462,7 @@ int run_event_factored(adrom_session* s, adrom_event_record& ev, bool* decoded) 
     return ADROM_OK;
   }
   ev.residual_norm = hs[2];
-  const FactBasis b2{s->phi[s->acur], s->Qb, s->r, b.k + 1, s->Wd[nxt], s->N};
+  const FactBasis b2{s->phi[s->acur], s->Qb, s->r, b.k + 1, s->Wd[nxt], s->N, s->A32[s->acur]};
   const int onx = 1 - s->opcur;
   st = build_sampling_operator(s, nullptr, s->op[onx], s->y_corr, true, &b2, s->nrm2[nxt]);
   if (st == ADROM_ERR_CUDA) return st;
@@ -638,6 +647,14 @@ int adrom_session_create(adrom_ctx* ctx, const adrom_session_config* cfg, adrom_
     s->fact_rows = s->alloc_d((size_t)(3 * cfg->n_s * cfg->model.n_var + cfg->n_s) * r);
     s->fact_qv = s->alloc_d((size_t)N);
     if (s->Qb) cudaMemsetAsync(s->Qb, 0, sizeof(double) * (size_t)N * FACT_KQ, ctx->stream);
+    if (!getenv("ADROM_NO_SHADOW") || !atoi(getenv("ADROM_NO_SHADOW"))) {
+      // fp32 anchor shadows for the QDEIM refresh (optional: null -> fp64 gathers)
+      for (int b = 0; b < 2; ++b) s->A32[b] = s->alloc_t<float>((size_t)N * r);
+      if (!s->A32[0] || !s->A32[1]) {
+        s->A32[0] = s->A32[1] = nullptr;
+        cudaGetLastError();
+      }
+    }
   }
   s->cap_steps = cfg->n_t > cfg->w_init ? cfg->n_t - cfg->w_init : 1;
   s->step_log = s->alloc_d((size_t)s->cap_steps * 3);
@@ -725,6 +742,10 @@ int adrom_session_load(adrom_session* s, const double* q_ref, const double* d, c
     if (g > (int64_t)ctx->num_sms * 8) g = (int64_t)ctx->num_sms * 8;
     row_norms_kernel<<<(int)g, 256, 0, ctx->stream>>>(s->phi[0], s->N, s->r, s->nrm2[0]);
     ADROM_LAUNCH_CK(ctx);
+    if (s->A32[0]) {
+      to_f32_kernel<<<(int)g, 256, 0, ctx->stream>>>(s->phi[0], s->N * s->r, s->A32[0]);
+      ADROM_LAUNCH_CK(ctx);
+    }
   }
   s->events.clear();
   ADROM_CK(ctx, cudaMemsetAsync(s->fail_step, 0xff, sizeof(int), ctx->stream));
