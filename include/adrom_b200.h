@@ -51,13 +51,13 @@ enum adrom_model_kind {
   ADROM_SOD = 2,     /* fom.SodProblem (fom.py:249-282): zero-gradient, n_var=3 */
   ADROM_REACTING = 3 /* configuration-4 reacting Euler (no reference code, SPEC.md:8;
                         defined by oracle/reacting.py): periodic, n_var=13.
-                        Residual only in this revision (adrom_rhs). */
+                        Every entry point below accepts it.                */
 };
 
 /* Physics + grid of one full-order model (replaces the FomProblem instance). */
 typedef struct adrom_model {
   int32_t kind;   /* adrom_model_kind                              */
-  int32_t n_var;  /* 1 (Burgers) or 3 (Sod)                        */
+  int32_t n_var;  /* 1 (Burgers), 3 (Sod) or 13 (reacting)         */
   int64_t n_elem; /* number of cells                               */
   double dx;      /* length / n_elem (fom.py:74)                   */
   double nu;      /* Burgers viscosity (fom.py:173)                */

@@ -149,7 +149,9 @@ def rhs_from_stencils(model: Model, stencil: np.ndarray) -> np.ndarray:
     """Residual at k cells from gathered (left, centre, right) states.
 
     ``stencil`` has shape (k, 3, n_var); returns (k, n_var).
-    Burgers: fom.py:190-198.  Sod: fom.py:271-277.
+    Burgers: fom.py:190-198.  Sod: fom.py:271-277.  Reacting (configuration
+    4, oracle/reacting.py): Rusanov faces of the 13-variable state plus the
+    centre cell's sources.
     """
     if model.kind == "burgers":
         val = burgers_point(stencil[:, 0, 0], stencil[:, 1, 0], stencil[:, 2, 0],
@@ -159,6 +161,12 @@ def rhs_from_stencils(model: Model, stencil: np.ndarray) -> np.ndarray:
         lo = rusanov(stencil[:, 0, :], stencil[:, 1, :], model.gamma)
         hi = rusanov(stencil[:, 1, :], stencil[:, 2, :], model.gamma)
         return -(hi - lo) / model.dx
+    if model.kind == "reacting":  # oracle/reacting.py: the same faces and sources as rhs()
+        from . import reacting
+        mech = np.asarray(model.mech, dtype=float).reshape(5, reacting.N_REACT)
+        lo = reacting.rusanov(stencil[:, 0, :], stencil[:, 1, :], model.gamma)
+        hi = reacting.rusanov(stencil[:, 1, :], stencil[:, 2, :], model.gamma)
+        return -(hi - lo) / model.dx + reacting.sources(stencil[:, 1, :], model.gamma, mech)
     raise ValueError(f"unknown model kind {model.kind!r}")
 
 
@@ -338,6 +346,6 @@ def primitive_fields(model: Model, q: np.ndarray) -> dict:
     """fom.py:200-201 / 279-282."""
     if model.kind == "burgers":
         return {"u": np.asarray(q, dtype=float)}
-    rho, vel, p = euler_primitives(np.asarray(q, dtype=float).reshape(model.n_elem, 3),
-                                   model.gamma)
+    cells = np.asarray(q, dtype=float).reshape(model.n_elem, model.n_var)[:, :3]
+    rho, vel, p = euler_primitives(cells, model.gamma)
     return {"rho": rho, "v": vel, "p": p}

@@ -4,6 +4,7 @@
 // Compiled with --fmad=false (see physics.cuh): every residual value and
 // every Jacobian entry is bitwise equal to the reference's numpy evaluation.
 #include "physics.cuh"
+#include "reacting.cuh"
 #include "fom_internal.cuh"
 #include "btsolve.cuh"
 
@@ -200,11 +201,15 @@ __global__ void sum_partials_kernel(const double* __restrict__ partial, int n,
 // kernel 2: gathered residual (rhs_at_cells, fom.py:190-198 / 271-277)
 // ---------------------------------------------------------------------------
 __global__ void cells_kernel(int kind, const double* __restrict__ g, int64_t k,
-                             BurgersParams bp, double gamma, double* __restrict__ out) {
+                             BurgersParams bp, double gamma, const double* __restrict__ mech,
+                             double* __restrict__ out) {
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < k;
        c += (int64_t)gridDim.x * blockDim.x) {
     if (kind == ADROM_BURGERS) {
       out[c] = burgers_cell(g[3 * c], g[3 * c + 1], g[3 * c + 2], bp);
+    } else if (kind == ADROM_REACTING) {
+      const double* s = g + 3 * RX_NV * c;
+      rx_cell_res(s, s + RX_NV, s + 2 * RX_NV, gamma, bp.dx, mech, out + RX_NV * c);
     } else {
       const double* s = g + 9 * c;
       const Cons l{s[0], s[1], s[2]}, m{s[3], s[4], s[5]}, r{s[6], s[7], s[8]};
@@ -230,7 +235,8 @@ __global__ void plan_kernel(int kind, const int64_t* __restrict__ gather,
                             const int64_t* __restrict__ out_var, int64_t n_s,
                             const double* __restrict__ cv, const double* __restrict__ h,
                             const double* __restrict__ dirs, int64_t ld, int n_dir,
-                            BurgersParams bp, double gamma, double* __restrict__ out) {
+                            BurgersParams bp, double gamma, const double* __restrict__ mech,
+                            double* __restrict__ out) {
   const int nd = n_dir > 0 ? n_dir : 1;
   const int64_t total = n_s * nd;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
@@ -245,6 +251,16 @@ __global__ void plan_kernel(int kind, const int64_t* __restrict__ gather,
       const int64_t* gp = gather + 3 * k;
       val = burgers_cell(plan_value(cv, dd, ld, d, hd, gp[0]), plan_value(cv, dd, ld, d, hd, gp[1]),
                          plan_value(cv, dd, ld, d, hd, gp[2]), bp);
+    } else if (kind == ADROM_REACTING) {
+      const int64_t* gp = gather + 3 * RX_NV * k;
+      double o[RX_NV];
+      rx_cell_res_get([&](int sl, int v) { return plan_value(cv, dd, ld, d, hd, gp[sl * RX_NV + v]); },
+                      gamma, bp.dx, mech, o);
+      const int var = (int)out_var[j];
+      val = o[0];
+#pragma unroll
+      for (int v = 1; v < RX_NV; ++v)
+        if (v == var) val = o[v];
     } else {
       const int64_t* gp = gather + 9 * k;
       Cons s[3];
@@ -395,9 +411,7 @@ static int check_model_fom(adrom_ctx* ctx, const adrom_model& m) {
 static int check_model(adrom_ctx* ctx, const adrom_model& m) {
   if (m.kind == ADROM_BURGERS && m.n_var == 1 && m.n_elem >= 4) return ADROM_OK;
   if (m.kind == ADROM_SOD && m.n_var == 3 && m.n_elem >= 4) return ADROM_OK;
-  if (m.kind == ADROM_REACTING)
-    return set_error(ctx, ADROM_ERR_ARG,
-                     "reacting model: only the residual (adrom_rhs) is implemented in this revision");
+  if (m.kind == ADROM_REACTING && m.n_var == 13 && m.n_elem >= 4 && m.mech) return ADROM_OK;
   return set_error(ctx, ADROM_ERR_ARG, "unsupported model (kind=%d, n_var=%d, n_elem=%lld)",
                    m.kind, m.n_var, (long long)m.n_elem);
 }
@@ -485,7 +499,8 @@ int fom_rhs_at_cells(adrom_ctx* ctx, const adrom_model& m, const double* gathere
   if (st) return st;
   if (k <= 0) return ADROM_OK;
   cells_kernel<<<grid_for(ctx, k, 256), 256, 0, ctx->stream>>>(m.kind, gathered, k,
-                                                               burgers_params(m), m.gamma, out);
+                                                               burgers_params(m), m.gamma, m.mech,
+                                                               out);
   ADROM_LAUNCH_CK(ctx);
   return ADROM_OK;
 }
@@ -503,7 +518,7 @@ int fom_plan_evaluate(adrom_ctx* ctx, const adrom_model& m, const int64_t* gathe
   const int64_t total = n_s * (n_dir > 0 ? n_dir : 1);
   plan_kernel<<<grid_for(ctx, total, 256), 256, 0, ctx->stream>>>(
       m.kind, gather, out_cell, out_var, n_s, closure_values, h, dirs, ld_dirs, n_dir,
-      burgers_params(m), m.gamma, out);
+      burgers_params(m), m.gamma, m.mech, out);
   ADROM_LAUNCH_CK(ctx);
   return ADROM_OK;
 }

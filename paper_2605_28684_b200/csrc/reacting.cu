@@ -8,51 +8,10 @@
 // Residual kernel: tiles of RX_TILE cells staged in shared memory with a
 // one-cell halo on each side (periodic wrap), one interface flux per face,
 // 13 x 8 B read + 13 x 8 B written per cell (208 B/cell, HBM bound).
-#include "physics.cuh"
+#include "reacting.cuh"
 #include "fom_internal.cuh"
 
 namespace adrom {
-
-constexpr int RX_NS = 10;          // species
-constexpr int RX_NR = 12;          // reactions
-constexpr int RX_NV = 3 + RX_NS;   // conserved variables
-constexpr int RX_TILE = 128;       // cells per tile
-constexpr int RX_NT = 128;
-
-// primitives (fom.py:204-210 semantics)
-__device__ __forceinline__ void rx_prim(const double* c, double gamma, double& rho, double& vel,
-                                        double& p) {
-  rho = np_max(c[0], PRIM_FLOOR);
-  vel = c[1] / rho;
-  const double kin = (0.5 * rho) * (vel * vel);
-  p = np_max((gamma - 1.0) * (c[2] - kin), PRIM_FLOOR);
-}
-
-// Rusanov interface flux between conserved states l and r -> f[13]
-__device__ __forceinline__ void rx_rusanov(const double* l, const double* r, double gamma,
-                                           double* f) {
-  double rl, vl, pl, rr, vr, pr;
-  rx_prim(l, gamma, rl, vl, pl);
-  rx_prim(r, gamma, rr, vr, pr);
-  const double s = np_max(fabs(vl) + sqrt((gamma * pl) / rl), fabs(vr) + sqrt((gamma * pr) / rr));
-  const double hs = 0.5 * s;
-  double fl, fr;
-  fl = l[1];
-  fr = r[1];
-  f[0] = 0.5 * (fl + fr) - hs * (r[0] - l[0]);
-  fl = l[1] * vl + pl;
-  fr = r[1] * vr + pr;
-  f[1] = 0.5 * (fl + fr) - hs * (r[1] - l[1]);
-  fl = vl * (l[2] + pl);
-  fr = vr * (r[2] + pr);
-  f[2] = 0.5 * (fl + fr) - hs * (r[2] - l[2]);
-#pragma unroll
-  for (int k = 0; k < RX_NS; ++k) {
-    fl = l[1] * (l[3 + k] / rl);
-    fr = r[1] * (r[3 + k] / rr);
-    f[3 + k] = 0.5 * (fl + fr) - hs * (r[3 + k] - l[3 + k]);
-  }
-}
 
 // mech (device, 5 x 12): a, b (as doubles), A, Ta, q
 __global__ void __launch_bounds__(RX_NT) reacting_rhs_kernel(const double* __restrict__ q,
@@ -123,34 +82,6 @@ __global__ void __launch_bounds__(RX_NT) reacting_rhs_kernel(const double* __res
     double* dst = out + base * RX_NV;
     for (int e = threadIdx.x; e < RX_NV * cnt; e += RX_NT) dst[e] = faces[e];
   }
-}
-
-// residual of one cell from its stencil (l, c, r): -(F(c,r) - F(l,c))/dx + S(c),
-// the same operations as the full kernel (faces computed identically)
-__device__ void rx_cell_res(const double* l, const double* c, const double* r, double gamma,
-                            double dx, const double* mk, double* out) {
-  double fl[RX_NV], fr[RX_NV];
-  rx_rusanov(l, c, gamma, fl);
-  rx_rusanov(c, r, gamma, fr);
-  double s[RX_NV];
-#pragma unroll
-  for (int v = 0; v < RX_NV; ++v) s[v] = 0.0;
-  double rho, vel, p;
-  rx_prim(c, gamma, rho, vel, p);
-  const double temp = p / rho;
-#pragma unroll 1
-  for (int j = 0; j < RX_NR; ++j) {
-    const int a = (int)mk[j], b = (int)mk[RX_NR + j];
-    const double w = (mk[2 * RX_NR + j] * exp(-mk[3 * RX_NR + j] / temp)) * np_max(c[3 + a], 0.0);
-#pragma unroll
-    for (int k = 0; k < RX_NS; ++k) {
-      if (k == a) s[3 + k] = s[3 + k] - w;
-      if (k == b) s[3 + k] = s[3 + k] + w;
-    }
-    s[2] = s[2] + mk[4 * RX_NR + j] * w;
-  }
-#pragma unroll
-  for (int v = 0; v < RX_NV; ++v) out[v] = (-(fr[v] - fl[v])) / dx + s[v];
 }
 
 // Banded FD Jacobian (fom.py:301-328 generalised; oracle/physics.py

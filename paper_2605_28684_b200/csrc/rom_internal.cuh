@@ -8,9 +8,10 @@ namespace adrom {
 
 struct RomStepArgs {
   DevOp op;              // reduced operator (device pointers, sizes on device)
-  int kind;              // ADROM_BURGERS / ADROM_SOD
+  int kind;              // ADROM_BURGERS / ADROM_SOD / ADROM_REACTING
   BurgersParams bp;      // dx, nu, dx^2
   double gamma;
+  const double* mech;    // ADROM_REACTING: 5 x 12 mechanism (device), else NULL
   const double* a_prev;  // device [r]
   double* a_out;         // device [r] (may alias a_prev)
   double dt, tol;

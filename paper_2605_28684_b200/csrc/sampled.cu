@@ -6,6 +6,7 @@
 // Compiled with --fmad=false: the sampled residual and the FD perturbations
 // `qc + h_j * dinv_phi_closure[:, j]` reproduce numpy's unfused arithmetic.
 #include "physics.cuh"
+#include "reacting.cuh"
 #include "jacobi.cuh"
 #include "rom_internal.cuh"
 
@@ -18,9 +19,31 @@ struct PlanView {
   const int64_t* gather;
   const int64_t* out_cell;
   const int64_t* out_var;
+  const double* mech;  // ADROM_REACTING: 5 x 12 mechanism (device)
 };
 
+// reacting cell (13 variables): kept out of line so its register footprint
+// does not spill the Burgers / Sod instantiations of the steppers
+__device__ __forceinline__ double eval_row_reacting(const PlanView& p, int j, const double* qc,
+                                                 const double* dir, int ldd, int k, double h) {
+  const int64_t* g = p.gather + 3 * RX_NV * p.out_cell[j];
+  double o[RX_NV];
+  rx_cell_res_get(
+      [&](int s, int v) {
+        const int64_t pos = g[s * RX_NV + v];
+        return dir ? qc[pos] + h * dir[pos * ldd + k] : qc[pos];
+      },
+      p.gamma, p.bp.dx, p.mech, o);
+  const int var = (int)p.out_var[j];
+  double out = o[0];
+#pragma unroll
+  for (int v = 1; v < RX_NV; ++v)
+    if (v == var) out = o[v];
+  return out;
+}
+
 // rhs at sampled row j from closure values (+ optional direction h * dir[:, k])
+template <bool RX>
 __device__ __forceinline__ double eval_row(const PlanView& p, int j, const double* qc,
                                            const double* dir, int ldd, int k, double h) {
   const int64_t cell = p.out_cell[j];
@@ -32,6 +55,7 @@ __device__ __forceinline__ double eval_row(const PlanView& p, int j, const doubl
       v[s] = dir ? qc[g[s]] + h * dir[g[s] * ldd + k] : qc[g[s]];
     return burgers_cell(v[0], v[1], v[2], p.bp);
   }
+  if (RX) return eval_row_reacting(p, j, qc, dir, ldd, k, h);
   const int64_t* g = p.gather + 9 * cell;
   double v[9];
 #pragma unroll
@@ -193,7 +217,7 @@ __device__ bool block_qr_certified_solve(double* jA, int ld, int r, double* rhs,
 // ---------------------------------------------------------------------------
 // STAGE: the pseudo-inverse and the sampled test basis live in shared memory
 // (both are re-read r times per Gauss-Newton iteration by the Jacobian product)
-template <bool STAGE>
+template <bool STAGE, bool RX>
 __global__ void __launch_bounds__(512) lspg_kernel(RomStepArgs A) {
   extern __shared__ double sm[];
   const int r = A.op.r;
@@ -214,7 +238,7 @@ __global__ void __launch_bounds__(512) lspg_kernel(RomStepArgs A) {
   __shared__ int sh_flag, sh_stop;
   __shared__ double sh_gn;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  PlanView pv{A.kind, A.op.n_var, A.bp, A.gamma, A.op.gather, A.op.out_cell, A.op.out_var};
+  PlanView pv{A.kind, A.op.n_var, A.bp, A.gamma, A.op.gather, A.op.out_cell, A.op.out_var, A.mech};
   double* qc = A.work;                    // n_c
   double* fs = qc + A.op.nc_cap;          // n_s
   double* prev = fs + A.op.ns_cap;        // n_s
@@ -251,7 +275,7 @@ __global__ void __launch_bounds__(512) lspg_kernel(RomStepArgs A) {
     }
     __syncthreads();
     for (int j = tid; j < n_s; j += blockDim.x) {
-      const double f = eval_row(pv, j, qc, nullptr, 0, 0, 0.0);
+      const double f = eval_row<RX>(pv, j, qc, nullptr, 0, 0, 0.0);
       fs[j] = f;
       res[j] = A.op.d_s[j] * ((qc[A.op.sample_pos[j]] - prev[j]) - A.dt * f);
     }
@@ -267,7 +291,7 @@ __global__ void __launch_bounds__(512) lspg_kernel(RomStepArgs A) {
     // test_sampled = phi_s - dt * (d_s * dfs)   (projection.py:183-186)
     for (int e = tid; e < n_s * r; e += blockDim.x) {
       const int j = e / r, k = e - j * r;
-      const double df = (eval_row(pv, j, qc, Dc, r, k, h[k]) - fs[j]) / h[k];
+      const double df = (eval_row<RX>(pv, j, qc, Dc, r, k, h[k]) - fs[j]) / h[k];
       test[e] = A.op.phi_s[e] - A.dt * (A.op.d_s[j] * df);
     }
     __syncthreads();
@@ -357,6 +381,7 @@ __global__ void __launch_bounds__(512) lspg_kernel(RomStepArgs A) {
 // Galerkin (projection.py:111-147)
 // ---------------------------------------------------------------------------
 // out = pinv @ (d_s * evaluate(q_ref_c + Dc @ av)), block-wide
+template <bool RX>
 __device__ void reduced_rhs(const RomStepArgs& A, const PlanView& pv, const double* av,
                             double* qc, double* fsd, double* out) {
   const int r = A.op.r, n_s = A.op.sizes[0], n_c = A.op.sizes[1];
@@ -368,7 +393,7 @@ __device__ void reduced_rhs(const RomStepArgs& A, const PlanView& pv, const doub
     qc[i] = A.op.q_ref_c[i] + s;
   }
   __syncthreads();
-  for (int j = tid; j < n_s; j += blockDim.x) fsd[j] = A.op.d_s[j] * eval_row(pv, j, qc, nullptr, 0, 0, 0.0);
+  for (int j = tid; j < n_s; j += blockDim.x) fsd[j] = A.op.d_s[j] * eval_row<RX>(pv, j, qc, nullptr, 0, 0, 0.0);
   __syncthreads();
   for (int k = warp; k < r; k += nw) {
     double s = 0.0;
@@ -379,6 +404,7 @@ __device__ void reduced_rhs(const RomStepArgs& A, const PlanView& pv, const doub
   __syncthreads();
 }
 
+template <bool RX>
 __global__ void __launch_bounds__(512) galerkin_kernel(RomStepArgs A) {
   extern __shared__ double sm[];
   const int r = A.op.r;
@@ -393,7 +419,7 @@ __global__ void __launch_bounds__(512) galerkin_kernel(RomStepArgs A) {
   double* red = J + r * r;    // 32
   __shared__ int sh_sing;
   const int tid = threadIdx.x;
-  PlanView pv{A.kind, A.op.n_var, A.bp, A.gamma, A.op.gather, A.op.out_cell, A.op.out_var};
+  PlanView pv{A.kind, A.op.n_var, A.bp, A.gamma, A.op.gather, A.op.out_cell, A.op.out_var, A.mech};
   double* qc = A.work;
   double* fsd = qc + A.op.nc_cap;
   for (int k = tid; k < r; k += blockDim.x) {
@@ -402,7 +428,7 @@ __global__ void __launch_bounds__(512) galerkin_kernel(RomStepArgs A) {
   }
   __syncthreads();
   auto residual = [&]() -> double {
-    reduced_rhs(A, pv, a, qc, fsd, fp);
+    reduced_rhs<RX>(A, pv, a, qc, fsd, fp);
     double s2 = 0.0;
     for (int k = tid; k < r; k += blockDim.x) {
       const double gk = (a[k] - a0[k]) - A.dt * fp[k];
@@ -416,11 +442,11 @@ __global__ void __launch_bounds__(512) galerkin_kernel(RomStepArgs A) {
   int it = 0, status = 0;
   while (gnorm > A.tol && it < A.max_iter) {
     for (int k = tid; k < r; k += blockDim.x) h[k] = FD_EPS * np_max(1.0, fabs(a[k]));
-    reduced_rhs(A, pv, a, qc, fsd, fa);
+    reduced_rhs<RX>(A, pv, a, qc, fsd, fa);
     for (int j = 0; j < r; ++j) {
       for (int k = tid; k < r; k += blockDim.x) ap[k] = (k == j) ? a[k] + h[k] : a[k];
       __syncthreads();
-      reduced_rhs(A, pv, ap, qc, fsd, fp);
+      reduced_rhs<RX>(A, pv, ap, qc, fsd, fp);
       for (int k = tid; k < r; k += blockDim.x)
         J[k * r + j] = ((k == j) ? 1.0 : 0.0) - (A.dt * (fp[k] - fa[k])) / h[j];
       __syncthreads();
@@ -498,18 +524,21 @@ int rom_step_async(adrom_ctx* ctx, const RomStepArgs& args, bool lspg) {
     const size_t sm = sizeof(double) * (7 * (size_t)r + 2 * (size_t)r * ld + r + 32) +
                       ((sizeof(int) * r + 15) & ~(size_t)15) + 64;
     const size_t sm_stage = sm + sizeof(double) * 2 * (size_t)r * args.op.ns_cap;
+    const bool rx = args.kind == ADROM_REACTING;
     if (sm_stage <= 200 * 1024) {
-      cudaFuncSetAttribute(lspg_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)sm_stage);
-      lspg_kernel<true><<<1, 512, sm_stage, ctx->stream>>>(args);
+      auto kern = rx ? lspg_kernel<true, true> : lspg_kernel<true, false>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_stage);
+      kern<<<1, 512, sm_stage, ctx->stream>>>(args);
     } else {
-      cudaFuncSetAttribute(lspg_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      lspg_kernel<false><<<1, 512, sm, ctx->stream>>>(args);
+      auto kern = rx ? lspg_kernel<false, true> : lspg_kernel<false, false>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      kern<<<1, 512, sm, ctx->stream>>>(args);
     }
   } else {
     const size_t sm = sizeof(double) * (7 * (size_t)r + (size_t)r * r + 32) + 64;
-    cudaFuncSetAttribute(galerkin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    galerkin_kernel<<<1, 512, sm, ctx->stream>>>(args);
+    auto kern = (args.kind == ADROM_REACTING) ? galerkin_kernel<true> : galerkin_kernel<false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    kern<<<1, 512, sm, ctx->stream>>>(args);
   }
   prof_end(ctx, pr);
   ADROM_LAUNCH_CK(ctx);

@@ -22,7 +22,7 @@ constexpr int FGS_MAX_CELLS = 8192;
 __device__ __forceinline__ double fgs_theta(const double* y, int64_t c, int kind, int nv,
                                             double gamma, int feature) {
   if (kind == ADROM_BURGERS) return y[c];
-  const double m0 = y[3 * c], m1 = y[3 * c + 1], m2 = y[3 * c + 2];
+  const double m0 = y[nv * c], m1 = y[nv * c + 1], m2 = y[nv * c + 2];
   const double rho = np_max(m0, 1e-10);
   const double vel = m1 / rho;
   if (feature == 1) return vel;
@@ -252,7 +252,7 @@ int plan_build(adrom_ctx* ctx, const adrom_model& m, DevOp& op, int n_s, int* fl
   while (np2 < 3 * n_s) np2 <<= 1;
   const size_t sm = sizeof(int) * 2 * np2;
   cudaFuncSetAttribute(plan_kernel_build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  plan_kernel_build<<<1, 1024, sm, ctx->stream>>>(m.n_elem, m.n_var, m.kind == ADROM_BURGERS, op,
+  plan_kernel_build<<<1, 1024, sm, ctx->stream>>>(m.n_elem, m.n_var, m.kind != ADROM_SOD, op,
                                                   n_s, flag);
   ADROM_LAUNCH_CK(ctx);
   return ADROM_OK;

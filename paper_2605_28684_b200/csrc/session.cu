@@ -287,6 +287,7 @@ int rom_step(adrom_session* s) {
   A.kind = s->cfg.model.kind;
   A.bp = make_bp(s->cfg.model);
   A.gamma = s->cfg.model.gamma;
+  A.mech = s->cfg.model.mech;
   A.a_prev = s->a;
   A.a_out = s->a;
   A.dt = s->cfg.dt;
@@ -970,6 +971,7 @@ int adrom_rom_step(adrom_ctx* ctx, const adrom_model* m, const adrom_rom_op* op,
   A.kind = m->kind;
   A.bp = make_bp(*m);
   A.gamma = m->gamma;
+  A.mech = m->mech;
   A.a_prev = a_prev;
   A.a_out = a_out;
   A.dt = dt;

@@ -20,7 +20,8 @@ import numpy as np
 from . import _dev
 from ._lib import Context, EventRecord, SessionConfig, _p, ptr
 from .errors import DenseError, RomStepError
-from .fom import BurgersProblem, FomProblem, SodProblem, TimeStepper, implicit_step
+from .fom import (BurgersProblem, FomProblem, ReactingEulerProblem, SodProblem, TimeStepper,
+                  implicit_step)
 from .snapshots import ScalingTransform, fit_scaling, pod
 from .tracking import UpdateRule
 
@@ -63,7 +64,7 @@ class ExperimentConfig:
     label: str = ""
 
     def __post_init__(self):
-        if self.model not in ("burgers", "sod"):
+        if self.model not in ("burgers", "sod", "reacting"):
             raise ValueError(f"unknown model {self.model!r}")
         if self.mode not in ("fom", "static", "adaptive"):
             raise ValueError(f"unknown mode {self.mode!r}")
@@ -97,6 +98,8 @@ def make_problem(config: ExperimentConfig) -> FomProblem:
     """driver.py:123-126."""
     if config.model == "burgers":
         return BurgersProblem(config.n_elem, nu=config.nu)
+    if config.model == "reacting":  # configuration 4 (no reference model, DESIGN.md §9)
+        return ReactingEulerProblem(config.n_elem, gamma=config.gamma)
     return SodProblem(config.n_elem, gamma=config.gamma)
 
 

@@ -210,8 +210,8 @@ class ReactingEulerProblem(FomProblem):
     The reference has no reacting model; the model is defined in
     DESIGN.md §9 / oracle/reacting.py: conserved [rho, m, E, rho Y_0..9],
     periodic, Rusanov fluxes as ``SodProblem`` plus 12 first-order Arrhenius
-    reactions a_j -> b_j releasing q_j.  Only the residual (``rhs``) runs on
-    the device in this revision.
+    reactions a_j -> b_j releasing q_j.  Residual, FD Jacobian, implicit
+    step, sampled residual and the adaptive-ROM session run on the device.
     """
 
     n_var = 3 + N_SPECIES
@@ -227,6 +227,22 @@ class ReactingEulerProblem(FomProblem):
         self.seed = int(seed)
         self.mechanism = reacting_mechanism(seed)
         self._mech_dev = None
+
+    def primitive_fields(self, q):
+        """rho, v, p as the Sod model (fom.py:279-282) from the first three
+        conserved variables; the FGS feature maps read these."""
+        if _dev.is_device(q):
+            t = _dev.torch()
+            u = q.reshape(self.n_elem, self.n_var)
+            rho = t.clamp_min(u[:, 0], PRIM_FLOOR)
+            vel = u[:, 1] / rho
+            p = t.clamp_min((self.gamma - 1.0) * (u[:, 2] - (0.5 * rho) * (vel * vel)), PRIM_FLOOR)
+            return {"rho": rho, "v": vel, "p": p}
+        u = np.asarray(q, dtype=float).reshape(self.n_elem, self.n_var)
+        rho = np.maximum(u[:, 0], PRIM_FLOOR)
+        vel = u[:, 1] / rho
+        p = np.maximum((self.gamma - 1.0) * (u[:, 2] - (0.5 * rho) * (vel * vel)), PRIM_FLOOR)
+        return {"rho": rho, "v": vel, "p": p}
 
     def abi(self) -> Model:
         if self._mech_dev is None:  # uploaded on first device use

@@ -116,3 +116,15 @@ def test_reacting_implicit_step_vs_oracle(n, dt):
     res = P.implicit_step(m, q, dt)
     assert res.converged == ref.converged and res.iterations == ref.iterations
     assert np.linalg.norm(np.asarray(res.x) - ref.x) <= 1e-12 * np.linalg.norm(ref.x)
+
+
+def test_oracle_sampled_residual_equals_full_residual():
+    """SamplingPlan.evaluate over every row == rhs, bitwise (the property the
+    reference has for Burgers and Sod), for the reacting model."""
+    from oracle import hyper, physics
+    n = 40
+    m = physics.Model("reacting", n, gamma=1.4, mech=tuple(R.mechanism().ravel()))
+    q = R.initial_state(n) * (1.0 + 0.01 * np.sin(np.arange(n * R.N_VAR)))
+    s = hyper.closure(hyper.Sampling(indices=np.arange(n * R.N_VAR), closure=None), m)
+    plan = hyper.gather_plan(m, s)
+    assert np.array_equal(plan.evaluate(m, q[s.closure]), physics.rhs(m, q))
