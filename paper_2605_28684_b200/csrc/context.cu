@@ -37,6 +37,21 @@ int ensure_scratch(adrom_ctx* ctx, size_t bytes) {
   return ADROM_OK;
 }
 
+int ensure_aux(adrom_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->aux_bytes && ctx->aux) return ADROM_OK;
+  size_t want = bytes < 1 << 20 ? (1 << 20) : bytes;
+  want = want + want / 4;
+  if (ctx->aux) {
+    ADROM_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    ADROM_CK(ctx, cudaFree(ctx->aux));
+    ctx->aux = nullptr;
+    ctx->aux_bytes = 0;
+  }
+  ADROM_CK(ctx, cudaMalloc(&ctx->aux, want));
+  ctx->aux_bytes = want;
+  return ADROM_OK;
+}
+
 void* scratch(adrom_ctx* ctx, size_t bytes, size_t offset_bytes) {
   (void)bytes;
   return (char*)ctx->scratch + offset_bytes;
@@ -156,6 +171,8 @@ void adrom_ctx_destroy(adrom_ctx* ctx) {
   if (!ctx) return;
   cudaStreamSynchronize(ctx->stream);
   if (ctx->scratch) cudaFree(ctx->scratch);
+  if (ctx->aux) cudaFree(ctx->aux);
+  adrom::blas_destroy(ctx);
   if (ctx->dflags) cudaFree(ctx->dflags);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->prof_ev) {

@@ -994,13 +994,15 @@ __global__ void __launch_bounds__(1024) isvd_core_kernel(
     const int* __restrict__ need, const double* __restrict__ G, int r_cur, int r, double lam,
     double* __restrict__ Bout, double* __restrict__ qinv_out, double* __restrict__ Tws,
     double* __restrict__ Gout, double* __restrict__ sigma_out, double* __restrict__ stats,
-    int* __restrict__ flag, double* __restrict__ udrop_out) {
+    int* __restrict__ flag, double* __restrict__ udrop_out, double* __restrict__ vglob) {
   extern __shared__ double sm[];
   const int n = r_cur + 1;
   const int ld = n + ((n & 1) ? 0 : 1);  // odd leading dimension
   double* A = sm;            // n x ld (column-major: column j = row j of K)
-  double* V = A + n * ld;    // n x ld
-  double* p = V + n * ld;    // r_cur
+  // V (n x ld) in shared memory, or in global memory (L2-resident) when
+  // both matrices do not fit (r_cur > 110)
+  double* V = vglob ? vglob : A + n * ld;
+  double* p = vglob ? A + n * ld : V + n * ld;    // r_cur
   double* s = p + r_cur;     // n
   double* chat = s + n;      // r_cur
   double* dv = chat + r_cur; // r_cur (p - p1)
@@ -1168,10 +1170,19 @@ static int core_threads(int r_cur) {
   return t < 64 ? 64 : (t > 1024 ? 1024 : t);
 }
 
-static size_t core_smem(int r_cur) {
+static size_t core_smem(int r_cur, bool v_global = false) {
   const int n = r_cur + 1;
   const int ld = n + ((n & 1) ? 0 : 1);
-  return sizeof(double) * (2 * (size_t)n * ld + 3 * (size_t)r_cur + n + 32) + sizeof(int) * n + 64;
+  return sizeof(double) * ((v_global ? 1 : 2) * (size_t)n * ld + 3 * (size_t)r_cur + n + 32) +
+         sizeof(int) * n + 64;
+}
+
+// V of the core SVD leaves shared memory above this size
+static bool core_v_global(int r_cur) { return core_smem(r_cur) > 220 * 1024; }
+
+static size_t core_vglob_doubles(int r_cur) {
+  const int n = r_cur + 1;
+  return (size_t)n * (n + ((n & 1) ? 0 : 1));
 }
 
 size_t isvd_workspace_bytes(adrom_ctx* ctx, int64_t n, int r_cur, int r) {
@@ -1188,6 +1199,7 @@ size_t isvd_workspace_bytes(adrom_ctx* ctx, int64_t n, int r_cur, int r) {
   b += align_up(sizeof(double) * 16);                  // stats + qinv
   b += align_up(sizeof(int) * 4);                      // need
   b += align_up(sizeof(double) * (size_t)n);           // residual q
+  b += align_up(sizeof(double) * core_vglob_doubles(r_cur));  // core V (r_cur > 110)
   return b;
 }
 
@@ -1199,7 +1211,7 @@ int isvd_update_async(adrom_ctx* ctx, const double* phi, const double* sigma, co
                       const RotFuse* fuse) {
   if (fuse && !rot_fusable(r_cur, r))
     return set_error(ctx, ADROM_ERR_ARG, "isvd_update: fused epilogue needs r in {32, 64}");
-  if (r_cur < 1 || r_cur > 110 || r < 1 || r > r_cur + 1)
+  if (r_cur < 1 || r_cur > 128 || r < 1 || r > r_cur + 1)
     return set_error(ctx, ADROM_ERR_ARG, "isvd_update: bad ranks r_cur=%d r=%d", r_cur, r);
   if (phi_out == phi && r != r_cur)
     return set_error(ctx, ADROM_ERR_ARG, "isvd_update: in-place update needs r == r_cur");
@@ -1221,6 +1233,7 @@ int isvd_update_async(adrom_ctx* ctx, const double* phi, const double* sigma, co
   double* sbuf = (double*)take(sizeof(double) * 16);
   int* need = (int*)take(sizeof(int) * 4);
   double* qbuf = (double*)take(sizeof(double) * (size_t)n);
+  double* vglob = (double*)take(sizeof(double) * core_vglob_doubles(r_cur));
   double* stats = stats_out ? stats_out : sbuf;
   double* qinv = sbuf + 12;
   int st;
@@ -1246,14 +1259,16 @@ int isvd_update_async(adrom_ctx* ctx, const double* phi, const double* sigma, co
   st = ts_residual(ctx, phi, n, r_cur, pls, y, red2, partial, flag, need, qbuf);
   prof_end(ctx, pr);
   if (st) return st;
-  const size_t csm = core_smem(r_cur);
+  const bool vg = core_v_global(r_cur);
+  const size_t csm = core_smem(r_cur, vg);
   cudaFuncSetAttribute(isvd_core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
   pr = prof_begin(ctx, PROBE_ISVD_CORE);
   // Gout may alias G: the kernel reads G completely before its final barrier
   double* Gout = gram_out ? gram_out : Gloc;
   isvd_core_kernel<<<1, core_threads(r_cur), csm, ctx->stream>>>(sigma, red1, pls, red2, need, G,
                                                                  r_cur, r, lam, B, qinv, T, Gout,
-                                                                 sigma_out, stats, flag, nullptr);
+                                                                 sigma_out, stats, flag, nullptr,
+                                                                 vg ? vglob : nullptr);
   prof_end(ctx, pr);
   ADROM_LAUNCH_CK(ctx);
   // the rotation reads q from pass 2 when it ran, else forms it from y and p
@@ -1282,7 +1297,7 @@ int isvd_core_launch(adrom_ctx* ctx, const double* sigma, const double* red1, co
   cudaFuncSetAttribute(isvd_core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
   isvd_core_kernel<<<1, core_threads(r), csm, ctx->stream>>>(sigma, red1, pls, red2, need, G, r, r,
                                                              lam, B, qinv, T, Gout, sigma_out, stats,
-                                                             flag, udrop);
+                                                             flag, udrop, nullptr);
   ADROM_LAUNCH_CK(ctx);
   return ADROM_OK;
 }

@@ -511,6 +511,127 @@ __global__ void __launch_bounds__(512) galerkin_kernel(RomStepArgs A) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// LSPG on a large sampled set (bigsample.cu): the r x r part of one
+// Gauss-Newton iteration, the same operations as lspg_kernel from
+// "grad = jac^T rho" on.  C = [jac | rho] column-major (ld r); st = [a, h,
+// it, done, gnorm, status, cond]; Vg: r x (r|1) global scratch (jA and V
+// do not both fit in shared memory at r = 128).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(512) lspg_update_kernel(const double* __restrict__ C, int r,
+                                                          double* __restrict__ st, double tol,
+                                                          int max_iter, double* __restrict__ V) {
+  extern __shared__ double sm[];
+  if (st[2 * r + 1] != 0.0) return;
+  const int ld = r | 1;
+  double* jA = sm;                  // r x ld (column-major: jA[l*ld + k] = jac[k][l])
+  double* rho = jA + (size_t)r * ld;
+  double* grad = rho + r;
+  double* sv = grad + r;
+  double* red = sv + r;             // 32
+  double* qrhs = red + 32;
+  double* qout = qrhs + r;
+  double* qv = qout + r;
+  int* order = (int*)(qv + r);
+  __shared__ int sh_flag, sh_stop;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  double* a = st;
+  double* h = st + r;
+  for (int e = tid; e < r * r; e += blockDim.x) {
+    const int l = e / r, k = e - l * r;
+    jA[l * ld + k] = C[e];
+  }
+  for (int k = tid; k < r; k += blockDim.x) rho[k] = C[(size_t)r * r + k];
+  __syncthreads();
+  double g2 = 0.0;
+  for (int l = tid; l < r; l += blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < r; ++k) s += jA[l * ld + k] * rho[k];
+    grad[l] = s;
+    g2 += s * s;
+  }
+  g2 = block_sum_dyn(g2, red);
+  const double gnorm = sqrt(g2);
+  if (tid == 0) st[2 * r + 2] = gnorm;
+  if (gnorm <= tol) {
+    if (tid == 0) st[2 * r + 1] = 1.0;
+    return;
+  }
+  for (int e = tid; e < r * ld; e += blockDim.x) V[e] = jA[e];
+  for (int k = tid; k < r; k += blockDim.x) qrhs[k] = -rho[k];
+  __syncthreads();
+  if (block_qr_certified_solve(V, ld, r, qrhs, qout, qv, red)) {
+    for (int k = tid; k < r; k += blockDim.x) a[k] = a[k] + qout[k];
+  } else {
+    const JacobiResult jr = block_jacobi(jA, ld, r, r, V, ld, 60, 1e-15, &sh_flag);
+    column_norms_sorted(jA, ld, r, r, sv, order);
+    const double smax = sv[order[0]], smin = sv[order[r - 1]];
+    if (tid == 0) sh_stop = (!(smin > 1e-14 * smax) || !jr.converged) ? 1 : 0;
+    __syncthreads();
+    if (sh_stop) {  // projection.py:193-198
+      if (tid == 0) {
+        st[2 * r + 3] = 1.0;
+        st[2 * r + 4] = smax / fmax(smin, 1e-300);
+        st[2 * r + 1] = 1.0;
+      }
+      return;
+    }
+    for (int c = warp; c < r; c += nw) {
+      double s = 0.0;
+      for (int k = lane; k < r; k += 32) s += jA[c * ld + k] * rho[k];
+      s = warp_sum(s);
+      if (lane == 0) {
+        const double sc = sv[c];
+        grad[c] = (sc > 1e-12 * smax) ? s / (sc * sc) : 0.0;
+      }
+    }
+    __syncthreads();
+    for (int k = tid; k < r; k += blockDim.x) {
+      double s = 0.0;
+      for (int c = 0; c < r; ++c) s += V[c * ld + k] * grad[c];
+      a[k] = a[k] + (-s);
+    }
+  }
+  __syncthreads();
+  for (int k = tid; k < r; k += blockDim.x) h[k] = FD_EPS * np_max(1.0, fabs(a[k]));
+  if (tid == 0) {
+    const double it = st[2 * r] + 1.0;
+    st[2 * r] = it;
+    if (it >= max_iter) st[2 * r + 1] = 1.0;
+  }
+}
+
+__global__ void lspg_finish_kernel(const double* __restrict__ st, int r, double tol,
+                                   double* __restrict__ a_out, double* __restrict__ info) {
+  for (int k = threadIdx.x; k < r; k += blockDim.x) a_out[k] = st[k];
+  if (threadIdx.x == 0) {
+    const double gnorm = st[2 * r + 2];
+    info[0] = (gnorm <= tol) ? 1.0 : 0.0;
+    info[1] = st[2 * r];
+    info[2] = gnorm;
+    info[3] = st[2 * r + 4];
+    info[4] = st[2 * r + 3];
+  }
+}
+
+int lspg_update_launch(adrom_ctx* ctx, const double* C, int r, double* st, double tol,
+                       int max_iter) {
+  const int ld = r | 1;
+  const size_t sm = sizeof(double) * ((size_t)r * ld + 6 * (size_t)r + 32) + sizeof(int) * r + 64;
+  cudaFuncSetAttribute(lspg_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  double* V = st + 2 * r + 8;  // r x ld scratch after the state scalars
+  lspg_update_kernel<<<1, 512, sm, ctx->stream>>>(C, r, st, tol, max_iter, V);
+  ADROM_LAUNCH_CK(ctx);
+  return ADROM_OK;
+}
+
+int lspg_finish_launch(adrom_ctx* ctx, const double* st, int r, double tol, double* a_out,
+                       double* info) {
+  lspg_finish_kernel<<<1, 128, 0, ctx->stream>>>(st, r, tol, a_out, info);
+  ADROM_LAUNCH_CK(ctx);
+  return ADROM_OK;
+}
+
 size_t rom_step_work_doubles(const DevOp& op) {
   return (size_t)op.nc_cap + 3 * (size_t)op.ns_cap + (size_t)op.ns_cap * op.r + 64;
 }

@@ -35,9 +35,11 @@ int plan_build(adrom_ctx* ctx, const adrom_model& m, DevOp& op, int n_s, int* fl
 // gathers + DEIM pseudo-inverse (sampling.py:162-175, projection.py:69-80)
 // fb (factored basis): rows are materialised into fact_rows
 // (>= (nc_cap + ns_cap) * r doubles) first
+// big_work (large sampled sets): the pseudo-inverse by CholeskyQR2
+// (bigsample.cu, deim_pinv_big_work_doubles) instead of the one-block QR
 int operator_fill(adrom_ctx* ctx, DevOp& op, const double* phi, const double* q_ref,
                   const double* d, int n_s, int* flag, const FactBasis* fb = nullptr,
-                  double* fact_rows = nullptr);
+                  double* fact_rows = nullptr, double* big_work = nullptr);
 
 int deim_pinv_only(adrom_ctx* ctx, const double* phi, const int64_t* idx, int n_s, int r,
                    double* phi_s, double* pinv, int* flag);

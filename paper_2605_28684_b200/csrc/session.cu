@@ -51,6 +51,10 @@ int sampling_flag_error(adrom_ctx* ctx, int f) {
   if (f & 16) return set_error(ctx, ADROM_ERR_DENSE, "not enough distinct rows to satisfy the sampling budget");
   if (f & 32) return set_error(ctx, ADROM_ERR_ARG, "sampling indices must be distinct");
   if (f & 64) return set_error(ctx, ADROM_ERR_SINGULAR, "sampled basis is rank deficient");
+  if (f & 128)
+    return set_error(ctx, ADROM_ERR_DENSE,
+                     "sampled basis too ill-conditioned for the large-sample pseudo-inverse "
+                     "(CholeskyQR2 certificate cond <= 1e8 failed)");
   if (f & 8) return set_error(ctx, ADROM_ERR_NOCONV, "SVD did not converge");
   if (f & 1) return set_error(ctx, ADROM_ERR_NONFINITE, "thin_svd input contains non-finite entries");
   return ADROM_OK;
@@ -96,6 +100,10 @@ struct adrom_session {
   double *a = nullptr;
   adrom_rom_op op[2]{};
   int opcur = 0;
+  // large sampled sets (n_s > 4096, configuration 4): grid-wide plan, FGS,
+  // CholeskyQR2 pseudo-inverse and Gauss-Newton step (bigsample.cu)
+  bool big = false;
+  BigOp bigop[2]{};
   double* rom_work = nullptr;
   double* rom_info = nullptr;
   double* isvd_stats = nullptr;
@@ -187,16 +195,24 @@ __global__ void row_norms_kernel(const double* __restrict__ phi, int64_t n, int 
   }
 }
 
-int alloc_op(adrom_session* s, adrom_rom_op& op) {
+int alloc_op(adrom_session* s, adrom_rom_op& op, BigOp& big) {
   const int ns = s->cfg.n_s, nv = s->cfg.model.n_var, r = s->r;
+  const int64_t ne = s->cfg.model.n_elem;
   op.r = r;
   op.n_var = nv;
   op.ns_cap = ns;
-  op.nc_cap = 3 * ns * nv;
-  op.ncell_cap = ns;
+  // at most 3 stencil cells per sampled cell, and never more than the grid
+  const int64_t cells_c = (3 * (int64_t)ns < ne) ? 3 * (int64_t)ns : ne;
+  op.nc_cap = (int32_t)(cells_c * nv);
+  op.ncell_cap = (int32_t)((ns < ne) ? ns : ne);
+  if (s->big) {
+    big.cell_start = s->alloc_t<int64_t>(op.ncell_cap);
+    big.cell_cnt = s->alloc_t<int32_t>(op.ncell_cap);
+    big.rows = s->alloc_t<int32_t>(ns);
+  }
   op.idx = s->alloc_t<int64_t>(ns);
   op.closure = s->alloc_t<int64_t>(op.nc_cap);
-  op.gather = s->alloc_t<int64_t>((size_t)ns * 3 * nv);
+  op.gather = s->alloc_t<int64_t>((size_t)op.ncell_cap * 3 * nv);
   op.out_cell = s->alloc_t<int64_t>(ns);
   op.out_var = s->alloc_t<int64_t>(ns);
   op.sample_pos = s->alloc_t<int64_t>(ns);
@@ -257,9 +273,11 @@ int build_sampling_operator(adrom_session* s, const double* phi, adrom_rom_op& o
     if (st) return st;
   }
   const int pr = prof_begin(ctx, PROBE_OPERATOR);
-  st = plan_build(ctx, m, op, n_s, ctx->dflags);
+  st = s->big ? plan_build_big(ctx, m, op, s->bigop[&op == &s->op[0] ? 0 : 1], n_s, ctx->dflags)
+              : plan_build(ctx, m, op, n_s, ctx->dflags);
   if (st) return st;
-  st = operator_fill(ctx, op, phi, s->q_ref, s->d, n_s, ctx->dflags, fb, s->fact_rows);
+  st = operator_fill(ctx, op, phi, s->q_ref, s->d, n_s, ctx->dflags, fb, s->fact_rows,
+                     s->big ? s->rom_work : nullptr);
   prof_end(ctx, pr);
   if (st) return st;
   int flags[16];
@@ -295,7 +313,13 @@ int rom_step(adrom_session* s) {
   A.max_iter = s->cfg.newton_max_iter;
   A.work = s->rom_work;
   A.info = s->rom_info;
-  int st = rom_step_async(s->ctx, A, s->cfg.projection == 0);
+  int st;
+  if (s->big)
+    st = (s->cfg.projection == 0)
+             ? lspg_step_big(s->ctx, A, s->bigop[s->opcur], s->cfg.n_s)
+             : set_error(s->ctx, ADROM_ERR_ARG, "galerkin on n_s > 4096 sampled rows is not supported");
+  else
+    st = rom_step_async(s->ctx, A, s->cfg.projection == 0);
   if (st) return st;
   if (s->n_online < s->cap_steps) {
     log_step_kernel<<<1, 1, 0, s->ctx->stream>>>(s->rom_info, s->step_log + 3 * s->n_online,
@@ -600,7 +624,7 @@ int adrom_session_create(adrom_ctx* ctx, const adrom_session_config* cfg, adrom_
   s->cfg = *cfg;
   s->N = cfg->model.n_elem * cfg->model.n_var;
   s->r = cfg->r;
-  if (cfg->r < 1 || cfg->r > 110 || cfg->n_s < cfg->r || cfg->z < 1) {
+  if (cfg->r < 1 || cfg->r > 128 || cfg->n_s < cfg->r || cfg->z < 1) {
     delete s;
     return set_error(ctx, ADROM_ERR_ARG, "session: bad r/n_s/z");
   }
@@ -618,9 +642,21 @@ int adrom_session_create(adrom_ctx* ctx, const adrom_session_config* cfg, adrom_
   s->y_hat = s->alloc_d(N);
   s->q_tilde = s->alloc_d(N);
   s->a = s->alloc_d(r);
-  int st = alloc_op(s, s->op[0]);
-  if (!st) st = alloc_op(s, s->op[1]);
-  s->rom_work = s->alloc_d(rom_step_work_doubles(s->op[0]));
+  {
+    const char* ev = getenv("ADROM_BIG_SAMPLES");  // tests: force the grid-wide path
+    s->big = cfg->n_s > 4096 || (ev && atoi(ev) != 0);
+  }
+  int st = alloc_op(s, s->op[0], s->bigop[0]);
+  if (!st) st = alloc_op(s, s->op[1], s->bigop[1]);
+  {
+    size_t w = rom_step_work_doubles(s->op[0]);
+    if (s->big) {
+      const size_t wb = big_work_doubles(s->op[0]);
+      const size_t wp = deim_pinv_big_work_doubles(cfg->n_s, r);
+      w = wb > wp ? wb : wp;
+    }
+    s->rom_work = s->alloc_d(w);
+  }
   s->rom_info = s->alloc_d(16 + r + 1 + 16);
   s->isvd_stats = s->alloc_d(16);
   const size_t iws = isvd_workspace_bytes(ctx, N, r, r);
@@ -633,7 +669,7 @@ int adrom_session_create(adrom_ctx* ctx, const adrom_session_config* cfg, adrom_
     // factored basis: r in {32, 64} at scale (ADROM_FACTORED=0/1 overrides)
     const char* ev = getenv("ADROM_FACTORED");
     const bool shape_ok = (r == 32 || r == 64);
-    s->fact = shape_ok && (ev ? atoi(ev) != 0 : N >= (1 << 18));
+    s->fact = shape_ok && !s->big && (ev ? atoi(ev) != 0 : N >= (1 << 18));
   }
   if (s->fact) {
     s->Qb = s->alloc_d((size_t)N * FACT_KQ);
