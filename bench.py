@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -356,7 +357,8 @@ def reference_cfg2(args, rank, world):
 
 def rom_case(name: str, n_override: int = 0):
     from paper_2605_28684_b200 import configs
-    case = {"cfg0": configs.cfg0, "cfg1": configs.cfg1, "cfg3": configs.cfg3}[name]()
+    case = {"cfg0": configs.cfg0, "cfg1": configs.cfg1, "cfg3": configs.cfg3,
+            "cfg4": configs.cfg4}[name]()
     if n_override:
         case = case.scaled(n_elem=n_override)
     return case
@@ -370,6 +372,8 @@ def rom_experiment(case):
         rule=P.UpdateRule("isvd", lam=case.lam), projection=case.projection,
         sampling=case.sampling, feature=case.feature, n_extra=case.n_extra)
     ic = case.initial_state()
+    if case.model == "reacting":  # configuration 4: the seeded pulse IC is the model's own
+        return cfg, P.ReactingEulerProblem(case.n_elem, gamma=case.gamma)
     base = P.BurgersProblem if case.model == "burgers" else P.SodProblem
 
     class Problem(base):  # the seeded IC of the case (driver.make_problem + custom IC)
@@ -398,6 +402,7 @@ def bench_rom(args, rank, world):
     q_last = training[cfg.w_init].clone()
     del training
     torch.cuda.synchronize()
+    torch.cuda.empty_cache()  # the offline window (17 GB at cfg4) leaves torch's cache
     t_off = time.perf_counter() - t_off
     ctx = _lib.Context.get()
     sess = Session(cfg, model, adaptive=True)
@@ -471,8 +476,9 @@ def bench_rom(args, rank, world):
         "metric": ROM_METRIC, "value": round(value, 3), "unit": "online steps/s", "n_gpus": world,
         "steps": K, "warmup": W, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded Burgers bump IC, configs.py)" if case.model == "burgers"
-                else "synthetic (Sod Riemann data)",
+        "data": {"burgers": "synthetic (seeded Burgers bump IC, configs.py)",
+                 "sod": "synthetic (Sod Riemann data)",
+                 "reacting": "synthetic (seeded mechanism and pulse IC, DESIGN.md §9)"}[case.model],
         "config": {"workload": case.name, "n_elem": case.n_elem, "r": r, "n_s": case.n_s,
                    "z": case.z, "lam": case.lam, "dt": case.dt, "projection": case.projection,
                    "sampling": case.sampling,
@@ -521,6 +527,7 @@ def e2e_rom(args, case):
              sig=pin(basis0.sigma), q_last=pin(training[cfg.w_init]))
     phi_norm = scaling.phi_norm
     del training, scaling, basis0
+    torch.cuda.empty_cache()
     out = torch.empty((K, N), dtype=torch.float64, pin_memory=True)
     sess = Session(cfg, model, adaptive=True)
     from paper_2605_28684_b200.snapshots import ScalingTransform
@@ -548,9 +555,15 @@ def cpu_baseline_rom(case, steps=3, n_sample=None, timed_steps=None):
     sample), scaled linearly in N to the case's grid (all per-step work of
     the loop is O(N r) or O(N r^2))."""
     from oracle import online, physics
-    n_sample = n_sample or min(case.n_elem, 1 << 14 if case.model == "sod" else 1 << 16)
+    n_sample = n_sample or min(case.n_elem, {"sod": 1 << 14, "reacting": 1 << 12}.get(case.model, 1 << 16))
     small = case.scaled(n_elem=n_sample)
-    m = physics.Model(small.model, small.n_elem, nu=small.nu, gamma=small.gamma)
+    if case.model == "reacting":
+        from oracle import reacting as R
+        n_s = math.ceil(0.03 * n_sample) * 13
+        small = case.scaled(n_elem=n_sample, n_s=n_s, n_extra=n_s - case.r)
+        m = physics.Model("reacting", n_sample, gamma=small.gamma, mech=tuple(R.mechanism().ravel()))
+    else:
+        m = physics.Model(small.model, small.n_elem, nu=small.nu, gamma=small.gamma)
     w_init = small.w_init
     ocfg = online.LoopConfig(model=m, dt=small.dt, n_t=w_init + steps + 1, w_init=w_init, r=small.r,
                              n_s=small.n_s, z=small.z, lam=small.lam, projection=small.projection,
@@ -679,7 +692,8 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg3", choices=["cfg0", "cfg1", "cfg2", "cfg3", "cfg4"])
+    ap.add_argument("--config", default="cfg3", choices=["cfg0", "cfg1", "cfg2", "cfg3", "cfg4",
+                                                         "cfg4-residual"])
     ap.add_argument("--n", type=int, default=0, help="override grid size (testing)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -690,7 +704,8 @@ def main(argv=None):
         rank = int(os.environ.get("RANK", "0"))
         world = int(os.environ.get("WORLD_SIZE", "1"))
         fn = {"cfg2": reference_cfg2, "cfg0": reference_rom, "cfg1": reference_rom,
-              "cfg3": reference_rom, "cfg4": reference_cfg4}.get(args.config)
+              "cfg3": reference_rom, "cfg4": reference_rom,
+              "cfg4-residual": reference_cfg4}.get(args.config)
         line = fn(args, rank, world) if fn else None
         if rank == 0:
             print(json.dumps(line if line else {"impl": "reference",
@@ -698,7 +713,7 @@ def main(argv=None):
         return 0
     rank, world, _ = dist_setup()
     fn = {"cfg2": bench_cfg2, "cfg0": bench_rom, "cfg1": bench_rom, "cfg3": bench_rom,
-          "cfg4": bench_cfg4}[args.config]
+          "cfg4": bench_rom, "cfg4-residual": bench_cfg4}[args.config]
     line = fn(args, rank, world)
     if rank == 0:
         print(json.dumps(line))

@@ -352,12 +352,13 @@ __global__ void __launch_bounds__(512) chol_kernel(const double* __restrict__ G,
                                                    const double* __restrict__ R1,
                                                    double* __restrict__ out,
                                                    double* __restrict__ out2,
+                                                   double* __restrict__ X,
                                                    int* __restrict__ flag) {
   extern __shared__ double sm[];
   const int ld = r + 1;
   double* A = sm;                 // r x ld, column-major; upper triangle -> R
-  double* X = A + (size_t)r * ld; // r x ld: R^{-1}
-  double* red = X + (size_t)r * ld;
+  double* red = A + (size_t)r * ld;
+  // X (r x ld, global scratch, L2-resident): R^{-1}
   __shared__ int sh_bad;
   const int tid = threadIdx.x;
   for (int e = tid; e < r * r; e += blockDim.x) {
@@ -439,7 +440,7 @@ __global__ void __launch_bounds__(512) chol_kernel(const double* __restrict__ G,
     atomicOr(flag, 128);
 }
 
-static size_t chol_smem(int r) { return sizeof(double) * (2 * (size_t)r * (r + 1) + 40); }
+static size_t chol_smem(int r) { return sizeof(double) * ((size_t)r * (r + 1) + 40); }
 
 int deim_pinv_big(adrom_ctx* ctx, DevOp& op, int n_s, double* work, int* flag) {
   const int r = op.r;
@@ -448,25 +449,28 @@ int deim_pinv_big(adrom_ctx* ctx, DevOp& op, int n_s, double* work, int* flag) {
   double* R1 = G + (size_t)r * r;          // r x r
   double* R1i = R1 + (size_t)r * r;        // r x r
   double* M = R1i + (size_t)r * r;         // r x r
-  double* Q1 = M + (size_t)r * r;          // n_s x r, column-major (ld n_s)
+  double* X = M + (size_t)r * r;           // r x (r+1) chol scratch
+  double* Q1 = X + (size_t)r * (r + 1);    // n_s x r, column-major (ld n_s)
   const size_t sm = chol_smem(r);
   cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   // phi_s is row-major n_s x r = column-major r x n_s (ld r): "A_cm"
   int st = dgemm(ctx, false, true, r, r, n_s, op.phi_s, r, op.phi_s, r, G, r);  // G = phi_s^T phi_s
   if (st) return st;
-  chol_kernel<<<1, 512, sm, ctx->stream>>>(G, r, 0, nullptr, R1, R1i, flag);
+  chol_kernel<<<1, 512, sm, ctx->stream>>>(G, r, 0, nullptr, R1, R1i, X, flag);
   ADROM_LAUNCH_CK(ctx);
   st = dgemm(ctx, true, false, n_s, r, r, op.phi_s, r, R1i, r, Q1, n_s);  // Q1 = phi_s R1^{-1}
   if (st) return st;
   st = dgemm(ctx, true, false, r, r, n_s, Q1, n_s, Q1, n_s, G, r);        // G2 = Q1^T Q1
   if (st) return st;
-  chol_kernel<<<1, 512, sm, ctx->stream>>>(G, r, 1, R1, M, R1i, flag);
+  chol_kernel<<<1, 512, sm, ctx->stream>>>(G, r, 1, R1, M, R1i, X, flag);
   ADROM_LAUNCH_CK(ctx);
   // pinv^T = phi_s (Rt^T Rt)^{-1}: column-major n_s x r == pinv row-major r x n_s
   return dgemm(ctx, true, false, n_s, r, r, op.phi_s, r, M, r, op.pinv, n_s);
 }
 
-size_t deim_pinv_big_work_doubles(int n_s, int r) { return 4 * (size_t)r * r + (size_t)n_s * r + 64; }
+size_t deim_pinv_big_work_doubles(int n_s, int r) {
+  return 5 * (size_t)r * (r + 1) + (size_t)n_s * r + 64;
+}
 
 // ---------------------------------------------------------------------------
 // LSPG Gauss-Newton step (projection.py:158-204) on a large sampled set

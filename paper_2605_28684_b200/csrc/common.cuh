@@ -171,8 +171,12 @@ void prof_end(adrom_ctx* ctx, int slot);
     if (_e != cudaSuccess) return adrom::check_cuda(ctx, _e, #call); \
   } while (0)
 
-#define ADROM_LAUNCH_CK(ctx)               \
-  do {                                     \
-    ++(ctx)->launches;                     \
-    ADROM_CK(ctx, cudaGetLastError());     \
+#define ADROM_STR2(x) #x
+#define ADROM_STR(x) ADROM_STR2(x)
+#define ADROM_LAUNCH_CK(ctx)                                                            \
+  do {                                                                                  \
+    ++(ctx)->launches;                                                                  \
+    cudaError_t _le = cudaGetLastError();                                               \
+    if (_le != cudaSuccess)                                                             \
+      return adrom::check_cuda(ctx, _le, "kernel launch at " __FILE__ ":" ADROM_STR(__LINE__)); \
   } while (0)

@@ -201,10 +201,18 @@ int alloc_op(adrom_session* s, adrom_rom_op& op, BigOp& big) {
   op.r = r;
   op.n_var = nv;
   op.ns_cap = ns;
-  // at most 3 stencil cells per sampled cell, and never more than the grid
-  const int64_t cells_c = (3 * (int64_t)ns < ne) ? 3 * (int64_t)ns : ne;
+  // sampled cells: at most n_s, the grid, and for FGS (whole cells on top of
+  // n_base QDEIM rows) 2 n_base + ceil(n_extra / n_var) + 1; at most 3
+  // stencil cells per sampled cell
+  int64_t cells = (ns < ne) ? ns : ne;
+  if (s->cfg.sampling == 1) {
+    const int64_t nb = ns - s->cfg.n_extra;
+    const int64_t fc = 2 * nb + (s->cfg.n_extra + nv - 1) / nv + 1;
+    if (fc < cells) cells = fc;
+  }
+  const int64_t cells_c = (3 * cells < ne) ? 3 * cells : ne;
   op.nc_cap = (int32_t)(cells_c * nv);
-  op.ncell_cap = (int32_t)((ns < ne) ? ns : ne);
+  op.ncell_cap = (int32_t)cells;
   if (s->big) {
     big.cell_start = s->alloc_t<int64_t>(op.ncell_cap);
     big.cell_cnt = s->alloc_t<int32_t>(op.ncell_cap);
@@ -662,7 +670,11 @@ int adrom_session_create(adrom_ctx* ctx, const adrom_session_config* cfg, adrom_
   const size_t iws = isvd_workspace_bytes(ctx, N, r, r);
   cudaMalloc(&s->isvd_ws, iws);
   s->allocs.push_back(s->isvd_ws);
-  cudaMalloc(&s->qd_ws, qdeim_pool_workspace_bytes(N, r, cfg->n_s));
+  {
+    // QDEIM picks n_s rows (qdeim) or the n_s - n_extra base rows (fgs)
+    const int n_q = (cfg->sampling == 1) ? cfg->n_s - cfg->n_extra : cfg->n_s;
+    cudaMalloc(&s->qd_ws, qdeim_pool_workspace_bytes(N, r, n_q > 0 ? n_q : 1));
+  }
   s->allocs.push_back(s->qd_ws);
   s->enc_partial = s->alloc_d(rot_fuse_partial_doubles(ctx, r));
   {
@@ -714,6 +726,7 @@ int adrom_session_create(adrom_ctx* ctx, const adrom_session_config* cfg, adrom_
   if (!st) {
     s->fctx->prof_parent = ctx;
     st = ensure_scratch(s->fctx, need);
+    if (st) set_error(ctx, st, "session: coarse-step workspace (%zu bytes): %s", need, s->fctx->err);
   }
   if (!st && (cudaEventCreateWithFlags(&s->main_mark, cudaEventDisableTiming) != cudaSuccess ||
               cudaEventCreateWithFlags(&s->fom_done, cudaEventDisableTiming) != cudaSuccess))
