@@ -417,12 +417,17 @@ def bench_rom(args, rank, world):
     ctx.prof_enable(True)
     l0 = ctx.launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    prof_timed = os.environ.get("ADROM_PROFILE_TIMED") == "1"  # ncu --profile-from-start off
     with ClockSampler(torch.cuda.current_device()) as clk:
         torch.cuda.synchronize()
+        if prof_timed:
+            torch.cuda.cudart().cudaProfilerStart()
         ev0.record()
         sess.advance(K)
         ev1.record()
         torch.cuda.synchronize()
+        if prof_timed:
+            torch.cuda.cudart().cudaProfilerStop()
     launches = ctx.launches() - l0
     probes = ctx.prof_read()
     ctx.prof_enable(False)

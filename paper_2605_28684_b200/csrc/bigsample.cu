@@ -562,31 +562,136 @@ __global__ void bl_base_kernel(DevOp op, BigOp big, PlanParams pp, const double*
   }
 }
 
-// finite-difference directions (projection.py:181-186): block = one sampled
-// cell, thread = direction d; test[j][d] = phi_s[j][d] - dt (d_s[j] dfs[j][d])
-template <int KIND, int NV>
-__global__ void __launch_bounds__(128) bl_dir_kernel(DevOp op, BigOp big, PlanParams pp,
-                                                     const double* __restrict__ qc,
-                                                     const double* __restrict__ fs, double dt,
-                                                     double* __restrict__ test,
-                                                     const double* __restrict__ st) {
+// finite-difference directions (projection.py:181-186): block = 128
+// directions, a grid-stride loop over sampled cells; thread d computes the
+// cell residual at qc + h_d Dc[:, d] and writes test[j][d] = phi_s[j][d] -
+// dt (d_s[j] dfs[j][d]) for the cell's sampled rows.  The next cell's
+// stencil rows of Dc (3 n_var rows, one column per thread) are staged into
+// shared memory by cp.async while the current cell is computed.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n"); }
+
+constexpr int BL_DIR_T = 128;
+
+template <int KIND, int NV, int NBUF>
+__global__ void __launch_bounds__(BL_DIR_T, NBUF == 1 ? 4 : 2)
+    bl_dir_kernel(DevOp op, BigOp big, PlanParams pp, const double* __restrict__ qc,
+                  const double* __restrict__ fs, double dt, double* __restrict__ test,
+                  const double* __restrict__ st) {
+  constexpr int NS = 3 * NV;
+  extern __shared__ double sdc[];  // [NBUF][NS][BL_DIR_T]
+  __shared__ int64_t spos[NBUF][NS];
+  __shared__ double sqc[NBUF][NS];
   const int r = op.r;
   if (st[2 * r + 1] != 0.0) return;
   const int k = op.sizes[2];
   const int d = threadIdx.x;
-  const double h = (d < r) ? st[r + d] : 1.0;
-  for (int64_t ks = blockIdx.x; ks < k; ks += gridDim.x) {
-    if (d >= r) continue;
-    double o[NV];
-    bl_cell<KIND, NV>(op, pp, ks, qc, op.dinv_phi_c, r, d, h, o);
-    const int64_t b = big.cell_start[ks];
-    const int cnt = big.cell_cnt[ks];
-    for (int q = 0; q < cnt; ++q) {
-      const int j = big.rows[b + q];
-      const double df = (pick<NV>(o, (int)op.out_var[j]) - fs[j]) / h;
-      test[(int64_t)j * (r + 1) + d] = op.phi_s[(int64_t)j * r + d] - dt * (op.d_s[j] * df);
+  const bool act = d < r;
+  const double h = act ? st[r + d] : 1.0;
+  const double* __restrict__ Dc = op.dinv_phi_c;
+  int64_t ks = blockIdx.x;
+  if (ks >= k) return;
+  auto stage = [&](int buf, int64_t cell) {
+    if (d < NS) {
+      const int64_t p = op.gather[cell * NS + d];
+      spos[buf][d] = p;
+      sqc[buf][d] = qc[p];
     }
+    __syncthreads();
+    if (act)
+#pragma unroll
+      for (int s = 0; s < NS; ++s) cp_async8(sdc + (buf * NS + s) * BL_DIR_T + d, Dc + spos[buf][s] * r + d);
+    cp_async_commit();
+  };
+  if (NBUF == 2) stage(0, ks);
+  for (int buf = 0; ks < k; buf ^= (NBUF - 1)) {
+    const int64_t nx = ks + gridDim.x;
+    if (NBUF == 2) {
+      if (nx < k) stage(buf ^ 1, nx);
+      else cp_async_commit();
+      cp_async_wait1();
+    } else {
+      stage(0, ks);
+      asm volatile("cp.async.wait_group 0;\n");
+    }
+    __syncthreads();
+    if (act) {
+      const double* sd = sdc + buf * NS * BL_DIR_T + d;
+      const double* sq = sqc[buf];
+      auto val = [&](int s, int v) { return sq[s * NV + v] + h * sd[(s * NV + v) * BL_DIR_T]; };
+      double o[NV];
+      if (KIND == ADROM_BURGERS) {
+        o[0] = burgers_cell(val(0, 0), val(1, 0), val(2, 0), pp.bp);
+      } else if (KIND == ADROM_SOD) {
+        const Cons l{val(0, 0), val(0, 1), val(0, 2)}, c{val(1, 0), val(1, 1), val(1, 2)},
+            rr{val(2, 0), val(2, 1), val(2, 2)};
+        const Cons x = sod_cell(l, c, rr, pp.gamma, pp.bp.dx);
+        o[0] = x.m0;
+        o[1] = x.m1;
+        o[2] = x.m2;
+      } else {
+        rx_cell_res_get(val, pp.gamma, pp.bp.dx, pp.mech, o);
+      }
+      const int64_t b = big.cell_start[ks];
+      const int cnt = big.cell_cnt[ks];
+      for (int q = 0; q < cnt; ++q) {
+        const int j = big.rows[b + q];
+        const double df = (pick<NV>(o, (int)op.out_var[j]) - fs[j]) / h;
+        test[(int64_t)j * (r + 1) + d] = op.phi_s[(int64_t)j * r + d] - dt * (op.d_s[j] * df);
+      }
+    }
+    __syncthreads();
+    ks = nx;
   }
+}
+
+// split-K reduction of the batched GEMM partials (fixed order: deterministic)
+__global__ void splitk_reduce_kernel(const double* __restrict__ part, int nb, int64_t sz,
+                                     double* __restrict__ C) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < sz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += part[b * sz + e];
+    C[e] = s;
+  }
+}
+
+constexpr int SPLITK_MAX = 148;
+
+// [jac | rho] (r x n, column-major) = pinv (r x K, row-major) [test | res]^T-ish:
+// C = P'^T T'^T with P' = pinv viewed column-major K x r and T' = test viewed
+// column-major n x K.  K is split into nb chunks (one batched DGEMM, a
+// partial per chunk) so the 128 x 129 output keeps every SM busy.
+static int gemm_jac(adrom_ctx* ctx, int r, int n, int64_t K, const double* pinv,
+                    const double* test, double* C, double* part) {
+  int nb = (int)(K / 1024);
+  if (nb > SPLITK_MAX) nb = SPLITK_MAX;
+  if (nb < 2) return dgemm(ctx, true, true, r, n, K, pinv, K, test, n, C, r);
+  cublasHandle_t h = blas(ctx);
+  if (!h) return set_error(ctx, ADROM_ERR_CUDA, "cuBLAS handle creation failed");
+  const int64_t kc = K / nb, rem = K - kc * nb;
+  const int64_t sz = (int64_t)r * n;
+  const double one = 1.0, zero = 0.0;
+  cublasStatus_t cs = cublasDgemmStridedBatched(
+      h, CUBLAS_OP_T, CUBLAS_OP_T, r, n, (int)kc, &one, pinv, (int)K, kc, test, n, kc * n, &zero,
+      part, r, sz, nb);
+  ++ctx->launches;
+  if (cs != CUBLAS_STATUS_SUCCESS)
+    return set_error(ctx, ADROM_ERR_CUDA, "cublasDgemmStridedBatched failed (%d)", (int)cs);
+  int nparts = nb;
+  if (rem > 0) {
+    const int st2 = dgemm(ctx, true, true, r, n, rem, pinv + nb * kc, K, test + nb * kc * n, n,
+                          part + (int64_t)nb * sz, r);
+    if (st2) return st2;
+    ++nparts;
+  }
+  splitk_reduce_kernel<<<(int)((sz + 255) / 256), 256, 0, ctx->stream>>>(part, nparts, sz, C);
+  ADROM_LAUNCH_CK(ctx);
+  return ADROM_OK;
 }
 
 __global__ void bl_init_kernel(const double* __restrict__ a_prev, int r, double* __restrict__ st) {
@@ -607,7 +712,7 @@ size_t big_work_doubles(const DevOp& op) {
   const size_t r = op.r;
   // qc, fs, prev, test, C, state (a, h, scalars) + the update's V scratch
   return (size_t)op.nc_cap + 2 * (size_t)op.ns_cap + (size_t)op.ns_cap * (r + 1) + r * (r + 1) +
-         2 * r + 8 + r * (r | 1) + 64;
+         2 * r + 8 + r * (r | 1) + (SPLITK_MAX + 1) * r * (r + 1) + 64;
 }
 
 int lspg_step_big(adrom_ctx* ctx, const RomStepArgs& A, const BigOp& big, int n_s) {
@@ -619,32 +724,44 @@ int lspg_step_big(adrom_ctx* ctx, const RomStepArgs& A, const BigOp& big, int n_
   double* prev = fs + op.ns_cap;
   double* test = prev + op.ns_cap;               // n_s x (r+1)
   double* C = test + (size_t)op.ns_cap * (r + 1);  // r x (r+1) column-major: [jac | rho]
-  double* st = C + (size_t)r * (r + 1);          // a, h, scalars
+  double* st = C + (size_t)r * (r + 1);          // a, h, scalars, update scratch
+  double* part = st + 2 * r + 8 + (size_t)r * (r | 1);  // split-K partials
   PlanParams pp{A.bp, A.gamma, A.mech};
   const int pr = prof_begin(ctx, PROBE_ROM_STEP);
   bl_init_kernel<<<1, 128, 0, ctx->stream>>>(A.a_prev, r, st);
   ADROM_LAUNCH_CK(ctx);
   const int grid = ctx->num_sms * 8;
-  const int dgrid = ctx->num_sms * 16;
   for (int it = 0; it < A.max_iter; ++it) {
     bl_decode_kernel<<<grid, 256, 0, ctx->stream>>>(op.dinv_phi_c, op.q_ref_c, op.sizes, r, st,
                                                     st + 2 * r + 1, qc);
     ADROM_LAUNCH_CK(ctx);
-    const int rt = ((r + 31) / 32) * 32;
+    // ADROM_BL_DIR_NBUF: 1 = one staged cell per block (4 blocks / SM),
+    // 2 = next cell prefetched by cp.async (2 blocks / SM)
+    static const int nbuf = getenv("ADROM_BL_DIR_NBUF") ? atoi(getenv("ADROM_BL_DIR_NBUF")) : 1;
+    auto dir1 = [&](auto kern, int nv, int nb) {
+      const size_t sm = sizeof(double) * nb * 3 * nv * BL_DIR_T;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      kern<<<ctx->num_sms * (nb == 1 ? 4 : 2), BL_DIR_T, sm, ctx->stream>>>(op, big, pp, qc, fs, A.dt,
+                                                                          test, st);
+    };
+    auto dir = [&](auto k1, auto k2, int nv) {
+      if (nbuf == 2) dir1(k2, nv, 2);
+      else dir1(k1, nv, 1);
+    };
     if (A.kind == ADROM_REACTING) {
       bl_base_kernel<ADROM_REACTING, RX_NV><<<grid, 128, 0, ctx->stream>>>(op, big, pp, qc, A.dt, fs, prev, test, st);
-      bl_dir_kernel<ADROM_REACTING, RX_NV><<<dgrid, rt, 0, ctx->stream>>>(op, big, pp, qc, fs, A.dt, test, st);
+      dir(bl_dir_kernel<ADROM_REACTING, RX_NV, 1>, bl_dir_kernel<ADROM_REACTING, RX_NV, 2>, RX_NV);
     } else if (A.kind == ADROM_SOD) {
       bl_base_kernel<ADROM_SOD, 3><<<grid, 128, 0, ctx->stream>>>(op, big, pp, qc, A.dt, fs, prev, test, st);
-      bl_dir_kernel<ADROM_SOD, 3><<<dgrid, rt, 0, ctx->stream>>>(op, big, pp, qc, fs, A.dt, test, st);
+      dir(bl_dir_kernel<ADROM_SOD, 3, 1>, bl_dir_kernel<ADROM_SOD, 3, 2>, 3);
     } else {
       bl_base_kernel<ADROM_BURGERS, 1><<<grid, 128, 0, ctx->stream>>>(op, big, pp, qc, A.dt, fs, prev, test, st);
-      bl_dir_kernel<ADROM_BURGERS, 1><<<dgrid, rt, 0, ctx->stream>>>(op, big, pp, qc, fs, A.dt, test, st);
+      dir(bl_dir_kernel<ADROM_BURGERS, 1, 1>, bl_dir_kernel<ADROM_BURGERS, 1, 2>, 1);
     }
     ctx->launches += 1;
     ADROM_LAUNCH_CK(ctx);
     // [jac | rho] = pinv [test | res]  (projection.py:176, :187)
-    int s2 = dgemm(ctx, true, true, r, r + 1, n_s, op.pinv, n_s, test, r + 1, C, r);
+    int s2 = gemm_jac(ctx, r, r + 1, n_s, op.pinv, test, C, part);
     if (s2) return s2;
     s2 = lspg_update_launch(ctx, C, r, st, A.tol, A.max_iter);
     if (s2) return s2;
