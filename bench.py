@@ -373,7 +373,7 @@ def rom_experiment(case):
         sampling=case.sampling, feature=case.feature, n_extra=case.n_extra)
     ic = case.initial_state()
     if case.model == "reacting":  # configuration 4: the seeded pulse IC is the model's own
-        return cfg, P.ReactingEulerProblem(case.n_elem, gamma=case.gamma)
+        return cfg, P.ReactingEulerProblem(case.n_elem, gamma=case.gamma, n_pulses=case.n_pulses)
     base = P.BurgersProblem if case.model == "burgers" else P.SodProblem
 
     class Problem(base):  # the seeded IC of the case (driver.make_problem + custom IC)

@@ -254,6 +254,275 @@ __global__ void part_solve_kernel(const double* __restrict__ sys, const double* 
   if (!ok) atomicOr(flag, 2);
 }
 
+
+// ---------------------------------------------------------------------------
+// wide blocks (n_var = 13, configuration 4): one half-warp per partition,
+// lane a owns row a of every nv x nv block (registers), rows are broadcast
+// by shuffles.  The same elimination as part_solve_kernel (block Thomas with
+// partial pivoting inside the diagonal blocks); the triangular solves are
+// column-oriented, so rounding differs from the thread-per-partition form at
+// the 1e-16 level (the Newton tests compare against the oracle's sparse LU).
+// ---------------------------------------------------------------------------
+template <int NV>
+struct HW {
+  unsigned mask;
+  int lane;  // 0..15 within the half-warp
+  __device__ __forceinline__ double bc(double v, int src) const {
+    return __shfl_sync(mask, v, src, 16);
+  }
+};
+
+// c_row = a_row * B (B row-distributed)
+template <int NV>
+__device__ __forceinline__ void hw_mm(const HW<NV>& h, const double* a, const double* b, double* c) {
+#pragma unroll
+  for (int j = 0; j < NV; ++j) c[j] = 0.0;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) c[j] += a[k] * h.bc(b[j], k);
+  }
+}
+// y_row = a_row . x (x distributed: x[k] in lane k)
+template <int NV>
+__device__ __forceinline__ double hw_mv(const HW<NV>& h, const double* a, double x) {
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) s += a[k] * h.bc(x, k);
+  return s;
+}
+// in-place LU with partial pivoting (rows physically swapped between lanes);
+// perm[k] = pivot row of step k (all lanes)
+template <int NV>
+__device__ __forceinline__ bool hw_lu(const HW<NV>& h, double* A, int* perm) {
+  bool ok = true;
+  const int a = h.lane;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    // argmax_{i >= k} |A[i][k]|, lowest row on ties (strict >, as lu())
+    double best = (a >= k && a < NV) ? fabs(A[k]) : -1.0;
+    int p = a;
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(h.mask, best, o, 16);
+      const int op = __shfl_xor_sync(h.mask, p, o, 16);
+      if (ob > best || (ob == best && op < p)) {
+        best = ob;
+        p = op;
+      }
+    }
+    perm[k] = p;
+    if (p != k) {
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        const double vk = h.bc(A[j], k), vp = h.bc(A[j], p);
+        if (a == k) A[j] = vp;
+        if (a == p) A[j] = vk;
+      }
+    }
+    const double d = h.bc(A[k], k);
+    if (d == 0.0 || !isfinite(d)) ok = false;
+    const double inv = 1.0 / d;
+    if (a > k) A[k] *= inv;
+    const double lik = A[k];
+#pragma unroll
+    for (int j = k + 1; j < NV; ++j) {
+      const double akj = h.bc(A[j], k);
+      if (a > k) A[j] -= lik * akj;
+    }
+  }
+  return ok;
+}
+// x <- A^{-1} x for x distributed (x[a] in lane a)
+template <int NV>
+__device__ __forceinline__ double hw_solve(const HW<NV>& h, const double* A, const int* perm, double x) {
+  const int a = h.lane;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int p = perm[k];
+    if (p != k) {
+      const double xk = h.bc(x, k), xp = h.bc(x, p);
+      if (a == k) x = xp;
+      if (a == p) x = xk;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const double xk = h.bc(x, k);
+    if (a > k) x -= A[k] * xk;
+  }
+#pragma unroll
+  for (int i = NV - 1; i >= 0; --i) {
+    if (a == i) x /= A[i];
+    const double xi = h.bc(x, i);
+    if (a < i) x -= A[i] * xi;
+  }
+  return x;
+}
+// B <- A^{-1} B, B row-distributed
+template <int NV>
+__device__ __forceinline__ void hw_solve_blk(const HW<NV>& h, const double* A, const int* perm, double* B) {
+  const int a = h.lane;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int p = perm[k];
+    if (p != k) {
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        const double vk = h.bc(B[j], k), vp = h.bc(B[j], p);
+        if (a == k) B[j] = vp;
+        if (a == p) B[j] = vk;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const double lak = A[k];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const double bkj = h.bc(B[j], k);
+      if (a > k) B[j] -= lak * bkj;
+    }
+  }
+#pragma unroll
+  for (int i = NV - 1; i >= 0; --i) {
+    if (a == i) {
+      const double dii = A[i];
+#pragma unroll
+      for (int j = 0; j < NV; ++j) B[j] /= dii;
+    }
+    const double ai = A[i];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const double bij = h.bc(B[j], i);
+      if (a < i) B[j] -= ai * bij;
+    }
+  }
+}
+
+template <int NV>
+__global__ void __launch_bounds__(128) part_solve_hw_kernel(
+    const double* __restrict__ sys, const double* __restrict__ rhs, double sign, int64_t n,
+    double* __restrict__ Y, double* __restrict__ V, double* __restrict__ W,
+    double* __restrict__ G, int* __restrict__ flag) {
+  constexpr int NV2 = NV * NV;
+  const int64_t P = (n + BT_M - 1) / BT_M;
+  const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t p = gt >> 4;
+  HW<NV> h;
+  h.lane = threadIdx.x & 15;
+  h.mask = 0xFFFFu << (threadIdx.x & 16);
+  if (p >= P) return;  // uniform per half-warp
+  const int64_t s = p * BT_M;
+  const int64_t e = ((s + BT_M < n) ? s + BT_M : n) - 1;
+  if (e == s) return;
+  const int a = h.lane;
+  const bool row = a < NV;
+  const int ar = row ? a : 0;
+  double cb = 0.0;
+  double cV[NV], Gp[NV], cW[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    Gp[j] = 0.0;
+    cW[j] = 0.0;
+    cV[j] = 0.0;
+  }
+  bool ok = true;
+  for (int64_t i = s; i < e; ++i) {
+    double L[NV], D[NV], U[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      L[j] = row ? sys[(i * 3 + 0) * NV2 + ar * NV + j] : 0.0;
+      D[j] = row ? sys[(i * 3 + 1) * NV2 + ar * NV + j] : 0.0;
+      U[j] = row ? sys[(i * 3 + 2) * NV2 + ar * NV + j] : 0.0;
+    }
+    double b = row ? sign * rhs[i * NV + ar] : 0.0;
+    double fV[NV];
+    if (i > s) {
+      double LG[NV];
+      hw_mm<NV>(h, L, Gp, LG);
+#pragma unroll
+      for (int c = 0; c < NV; ++c) D[c] -= LG[c];
+      b -= hw_mv<NV>(h, L, cb);
+      double LV[NV];
+      hw_mm<NV>(h, L, cV, LV);
+#pragma unroll
+      for (int c = 0; c < NV; ++c) fV[c] = -LV[c];
+    } else {
+#pragma unroll
+      for (int c = 0; c < NV; ++c) fV[c] = -L[c];
+    }
+    if (!row) {
+#pragma unroll
+      for (int c = 0; c < NV; ++c) D[c] = 0.0;
+    }
+    int perm[NV];
+    ok &= hw_lu<NV>(h, D, perm);
+    b = hw_solve<NV>(h, D, perm, b);
+    hw_solve_blk<NV>(h, D, perm, fV);
+    cb = b;
+#pragma unroll
+    for (int c = 0; c < NV; ++c) cV[c] = fV[c];
+    if (i < e - 1) {
+      hw_solve_blk<NV>(h, D, perm, U);
+#pragma unroll
+      for (int c = 0; c < NV; ++c) Gp[c] = U[c];
+    } else {
+#pragma unroll
+      for (int c = 0; c < NV; ++c) cW[c] = -U[c];
+      hw_solve_blk<NV>(h, D, perm, cW);
+#pragma unroll
+      for (int c = 0; c < NV; ++c) Gp[c] = 0.0;
+    }
+    if (row) {
+      Y[i * NV + a] = cb;
+#pragma unroll
+      for (int c = 0; c < NV; ++c) {
+        V[i * NV2 + a * NV + c] = cV[c];
+        G[i * NV2 + a * NV + c] = Gp[c];
+      }
+    }
+  }
+  // backward sweep: z_i = c_i - G_i z_{i+1}
+  double yn = cb;
+  double Vn[NV], Wn[NV];
+#pragma unroll
+  for (int c = 0; c < NV; ++c) {
+    Vn[c] = cV[c];
+    Wn[c] = cW[c];
+  }
+  if (row)
+#pragma unroll
+    for (int c = 0; c < NV; ++c) W[(e - 1) * NV2 + a * NV + c] = Wn[c];
+  for (int64_t i = e - 2; i >= s; --i) {
+    double Gi[NV], Vi[NV];
+#pragma unroll
+    for (int c = 0; c < NV; ++c) {
+      Gi[c] = row ? G[i * NV2 + a * NV + c] : 0.0;
+      Vi[c] = row ? V[i * NV2 + a * NV + c] : 0.0;
+    }
+    const double yi = row ? Y[i * NV + a] : 0.0;
+    yn = yi - hw_mv<NV>(h, Gi, yn);
+    double GV[NV], GW[NV];
+    hw_mm<NV>(h, Gi, Vn, GV);
+    hw_mm<NV>(h, Gi, Wn, GW);
+#pragma unroll
+    for (int c = 0; c < NV; ++c) {
+      Vn[c] = Vi[c] - GV[c];
+      Wn[c] = -GW[c];
+    }
+    if (row) {
+      Y[i * NV + a] = yn;
+#pragma unroll
+      for (int c = 0; c < NV; ++c) {
+        V[i * NV2 + a * NV + c] = Vn[c];
+        W[i * NV2 + a * NV + c] = Wn[c];
+      }
+    }
+  }
+  if (!ok && a == 0) atomicOr(flag, 2);
+}
+
 // ---------------------------------------------------------------------------
 // scalar (n_var = 1) partitions: the same elimination, staged through smem so
 // that global traffic is coalesced.  A warp owns 32 consecutive partitions
@@ -559,6 +828,10 @@ static int bt_solve_t(adrom_ctx* ctx, const double* sys, const double* rhs, doub
                            (int)sm);
       part_solve_scalar_kernel<<<(int)(g < 1 ? 1 : g), 32 * PS_WARPS, sm, ctx->stream>>>(
           L.sys, L.rhs, L.sign, L.n, L.Y, L.V, L.W, flag);
+    } else if (NV > 8) {  // half-warp per partition (13 x 13 blocks)
+      const int64_t g2 = (P * 16 + 127) / 128;
+      part_solve_hw_kernel<NV><<<(int)g2, 128, 0, ctx->stream>>>(L.sys, L.rhs, L.sign, L.n, L.Y,
+                                                                 L.V, L.W, L.G, flag);
     } else {
       part_solve_kernel<NV><<<gb, nt, 0, ctx->stream>>>(L.sys, L.rhs, L.sign, L.n, L.Y, L.V, L.W,
                                                         L.G, flag);
@@ -594,8 +867,7 @@ int bt_solve(adrom_ctx* ctx, const double* sys, const double* rhs, double rhs_si
              int nv, bool cyclic, double* out, void* ws, int* flag, const double* add_to) {
   if (nv == 1) return bt_solve_t<1>(ctx, sys, rhs, rhs_sign, n, cyclic, out, ws, flag, add_to);
   if (nv == 3) return bt_solve_t<3>(ctx, sys, rhs, rhs_sign, n, cyclic, out, ws, flag, add_to);
-  // configuration-4 reacting model: 13 x 13 blocks (thread-per-partition,
-  // blocks in local memory; correctness first, round 2 makes it warp-wide)
+  // configuration-4 reacting model: 13 x 13 blocks, half-warp per partition
   if (nv == 13) return bt_solve_t<13>(ctx, sys, rhs, rhs_sign, n, cyclic, out, ws, flag, add_to);
   return set_error(ctx, ADROM_ERR_ARG, "bt_solve: unsupported block size %d", nv);
 }

@@ -388,6 +388,11 @@ void fom_launch_async(adrom_session* s) {
   const adrom_model m = model_of(s);
   const double* in = s->y_corr;
   double* out = s->y_next;
+  // the coarse-step stream first waits for everything enqueued on the main
+  // stream so far (the input y_corr may come from it, and the output buffer
+  // was last read by it)
+  cudaEventRecord(s->main_mark, s->ctx->stream);
+  cudaStreamWaitEvent(s->fctx->stream, s->main_mark, 0);
   s->fom_pending = true;
   s->fom_thread = std::thread([s, m, in, out]() {
     s->fom_status = fom_implicit_step(s->fctx, m, in, s->cfg.z * s->cfg.dt, s->cfg.newton_tol,
@@ -530,16 +535,11 @@ int run_event(adrom_session* s, adrom_event_record& ev, bool* decoded) {
   adrom_ctx* fc = s->fctx;
   const long long l0 = fc->launches;
   int st;
-  if (s->fact) {
-    // started early (fom_launch_async) unless this is the first event or the
-    // previous coarse step failed
-    fom_launch_async(s);  // no-op when already started / finished
-    st = fom_join(s, &ni);
-  } else {
-    ADROM_CK(ctx, cudaStreamWaitEvent(fc->stream, s->main_mark, 0));
-    st = fom_implicit_step(fc, m, s->y_corr, s->cfg.z * s->cfg.dt, s->cfg.newton_tol,
-                           s->cfg.newton_max_iter, s->y_next, &ni);
-  }
+  // started early on a host thread (fom_launch_async, right after the
+  // previous event) unless this is the first event or the previous coarse
+  // step failed; it then overlapped the last z reduced steps
+  fom_launch_async(s);  // no-op when already started / finished
+  st = fom_join(s, &ni);
   ctx->launches += fc->launches - l0;
   if (st || !s->fact) {  // (the factored path joins after its pass 1)
     ADROM_CK(ctx, cudaEventRecord(s->fom_done, fc->stream));
@@ -844,6 +844,10 @@ int adrom_session_advance(adrom_session* s, int64_t n_steps, int64_t save_every,
       ev.step = n + 1;
       st = run_event(s, ev, &decoded);  // decodes q~ in its first basis pass
       if (st) return st;
+      // explicit basis: the next event's coarse step only needs this y_corr;
+      // start it now so it overlaps the next z reduced steps (the factored
+      // path starts it inside the event, after its pass 1)
+      if (!s->fact && ev.pad) fom_launch_async(s);
     }
     if (!decoded) {
       st = decode_state(s);

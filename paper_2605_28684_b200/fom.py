@@ -219,8 +219,10 @@ class ReactingEulerProblem(FomProblem):
     var_names = ("rho", "m", "E") + tuple(f"rhoY{k}" for k in range(N_SPECIES))
     kind = REACTING
 
-    def __init__(self, n_elem: int, gamma: float = 1.4, length: float = 1.0, seed: int = 4):
+    def __init__(self, n_elem: int, gamma: float = 1.4, length: float = 1.0, seed: int = 4,
+                 n_pulses: int = 1):
         super().__init__(n_elem, length)
+        self.n_pulses = int(n_pulses)
         if gamma <= 1.0:
             raise ValueError("gamma must exceed 1")
         self.gamma = float(gamma)
@@ -253,14 +255,27 @@ class ReactingEulerProblem(FomProblem):
     def initial_state(self) -> np.ndarray:
         """BASELINE cfg 4: rho = 1, u = 0, p = 1 plus a seeded sinusoidal
         pressure/temperature pulse (amplitude U[0.5, 1], centre U[0.3, 0.7],
-        width 0.1); species fractions Y_k = (k+1)/55."""
+        width 0.1), or n_pulses narrow ones (amplitude U[0.2, 1], centre
+        U[0, 1) periodic, width U[0.002, 0.01]); species fractions
+        Y_k = (k+1)/55.  Host-generated input data."""
         n = self.n_elem
-        rng = np.random.default_rng([self.seed, 5])
-        amp, cen, wid = rng.uniform(0.5, 1.0), rng.uniform(0.3, 0.7), 0.1
         x = (np.arange(n) + 0.5) / n
-        d = x - cen
-        p = 1.0 + np.where(np.abs(d) < 0.5 * wid,
-                           amp * 0.5 * (1.0 + np.cos(2.0 * np.pi * d / wid)), 0.0)
+        p = np.ones(n)
+        if self.n_pulses == 1:
+            rng = np.random.default_rng([self.seed, 5])
+            amp, cen, wid = rng.uniform(0.5, 1.0), rng.uniform(0.3, 0.7), 0.1
+            d = x - cen
+            p = 1.0 + np.where(np.abs(d) < 0.5 * wid,
+                               amp * 0.5 * (1.0 + np.cos(2.0 * np.pi * d / wid)), 0.0)
+        else:
+            rng = np.random.default_rng([self.seed, 6])
+            amp = rng.uniform(0.2, 1.0, self.n_pulses)
+            cen = rng.uniform(0.0, 1.0, self.n_pulses)
+            wid = rng.uniform(0.002, 0.01, self.n_pulses)
+            for a, c, w in zip(amp, cen, wid):
+                d = np.mod(x - c + 0.5, 1.0) - 0.5
+                p = p + np.where(np.abs(d) < 0.5 * w,
+                                 a * 0.5 * (1.0 + np.cos(2.0 * np.pi * d / w)), 0.0)
         out = np.zeros((n, self.n_var))
         out[:, 0] = 1.0
         out[:, 2] = p / (self.gamma - 1.0)
