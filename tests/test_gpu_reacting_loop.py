@@ -112,3 +112,42 @@ def test_reacting_session_events_vs_oracle():
         assert np.all(err <= 1e-8 * ref + 1e-10 * ref[0]), (ev, (err / ref).max())
         assert list(sess.sampling().cpu().numpy()) == list(rec.samplings[ev + 1]), ev
     sess.close()
+
+
+@pytest.mark.parametrize("grid_path", [False, True])
+def test_cfg4_recipe_scaled_vs_oracle(monkeypatch, grid_path):
+    """Configuration 4's recipe (configs.cfg4: seeded narrow pulses, FGS on 3 %
+    of the cells on top of r QDEIM rows, z = 20, lambda = 0.25) on 256 cells
+    (8 pulses, r = 12, dt = 5e-4: a well-conditioned reduced problem — the
+    LSPG Jacobian's condition number stays below 1e3 and every Gauss-Newton
+    solve converges), through the one-block and the grid-wide (bigsample.cu,
+    the full-size path) reduced operator."""
+    import math
+    if grid_path:
+        monkeypatch.setenv("ADROM_BIG_SAMPLES", "1")
+        monkeypatch.setenv("ADROM_FGS_GRID", "1")
+    P = _pkg()
+    n, r = 256, 12
+    n_s = math.ceil(0.03 * n) * 13
+    dt = 5e-4
+    m = _model(n)
+    ocfg = online.LoopConfig(model=m, dt=dt, n_t=40 + 60, w_init=40, r=r, n_s=n_s,
+                             n_extra=n_s - r, z=20, lam=0.25, sampling="fgs")
+    training = online.training_states(ocfg, R.initial_state(n, n_pulses=8))
+    q_ref, phi_norm = subspace.fit_scaling(list(training), 13)
+    _, d, phi0, sigma0 = online.offline(ocfg, training)
+    rec = online.run_online(ocfg, training, q_ref, d, phi0, sigma0)
+    cfg = P.ExperimentConfig(model="reacting", n_elem=n, dt=dt, n_t=ocfg.n_t, w_init=40, r=r,
+                             n_s=n_s, n_extra=n_s - r, z=20, sampling="fgs",
+                             rule=P.UpdateRule("isvd", lam=0.25))
+    res = P.run_adaptive_rom(cfg, truth=training, offline=(
+        P.ScalingTransform(q_ref=q_ref, phi_norm=phi_norm), P.ReducedBasis(phi0, sigma0)))
+    got = res.trajectory[cfg.w_init + 1:]
+    want = np.array(rec.states)
+    dev = np.linalg.norm(got - want, axis=1) / np.linalg.norm(want, axis=1)
+    assert dev.max() < 1e-8, dev.max()
+    assert len(res.event_log) == len(rec.events)
+    for e_ref, e in zip(rec.events, res.event_log):
+        assert "update_error" not in e
+        assert e_ref["coarse_iterations"] == e["coarse_iterations"]
+    assert res.newton_failures == rec.failures
