@@ -19,6 +19,8 @@
 // tests/test_gpu_fom.py.
 #include "btsolve.cuh"
 
+#include <stdlib.h>
+
 namespace adrom {
 
 constexpr int BT_M = 16;  // rows per partition
@@ -523,6 +525,239 @@ __global__ void __launch_bounds__(128) part_solve_hw_kernel(
   if (!ok && a == 0) atomicOr(flag, 2);
 }
 
+
+// ---------------------------------------------------------------------------
+// wide blocks (n_var = 13, configuration 4), tensor-core form: one warp per
+// partition, every nv x nv block padded to a 16 x 16 shared-memory tile.
+// The block products (L G, L V for the forward sweep, G V and G W for the
+// backward one) run on the FP64 tensor cores (DMMA m8n8k4, 16 per product);
+// the diagonal block is eliminated by Gauss-Jordan with partial pivoting on
+// the augmented [D' | b | -L V | U] with one column per lane (row swaps stay
+// in registers, one pivot column broadcast per step).  Rounding differs from
+// the thread-per-partition LU at the 1e-16 level.
+// ---------------------------------------------------------------------------
+constexpr int TC_LD = 20;   // tile leading dimension: conflict-free DMMA fragments
+constexpr int TC_TILE = 16 * TC_LD;
+constexpr int TC_WARPS = 4;
+constexpr int TC_TILES = 7;  // L, D, U, F, V, G, W
+__device__ __forceinline__ void dmma884_bt(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+// C = Cin + alpha A B (16 x 16 tiles, zero padding beyond nv); Cin may alias C
+__device__ __forceinline__ void tc_mm(const double* A, const double* B, double* C,
+                                      const double* Cin, double alpha, int lane) {
+  const int r = lane >> 2, k = lane & 3;
+#pragma unroll
+  for (int ti = 0; ti < 2; ++ti)
+#pragma unroll
+    for (int tj = 0; tj < 2; ++tj) {
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        dmma884_bt(d0, d1, A[(ti * 8 + r) * TC_LD + kk * 4 + k], B[(kk * 4 + k) * TC_LD + tj * 8 + r]);
+      const int row = ti * 8 + r, col = tj * 8 + 2 * k;
+      const double c0 = Cin ? Cin[row * TC_LD + col] : 0.0;
+      const double c1 = Cin ? Cin[row * TC_LD + col + 1] : 0.0;
+      C[row * TC_LD + col] = c0 + alpha * d0;
+      C[row * TC_LD + col + 1] = c1 + alpha * d1;
+    }
+}
+
+// one Gauss-Jordan step on lane-held columns (column K's owner is lane K);
+// recursive template so every register index is a compile-time constant
+template <int NV, int K>
+__device__ __forceinline__ void gj_step(double (&x1)[NV], double (&x2)[NV], bool& ok) {
+  int pr = K;
+  {
+    double best = fabs(x1[K]);
+#pragma unroll
+    for (int r = K + 1; r < NV; ++r)
+      if (fabs(x1[r]) > best) {
+        best = fabs(x1[r]);
+        pr = r;
+      }
+  }
+  pr = __shfl_sync(0xffffffffu, pr, K);
+  if (pr != K) {
+    double b1 = 0.0, b2 = 0.0;
+#pragma unroll
+    for (int r = K + 1; r < NV; ++r)
+      if (r == pr) {
+        b1 = x1[r];
+        b2 = x2[r];
+      }
+#pragma unroll
+    for (int r = K + 1; r < NV; ++r)
+      if (r == pr) {
+        x1[r] = x1[K];
+        x2[r] = x2[K];
+      }
+    x1[K] = b1;
+    x2[K] = b2;
+  }
+  const double d = __shfl_sync(0xffffffffu, x1[K], K);
+  if (d == 0.0 || !isfinite(d)) ok = false;
+  const double inv = 1.0 / d;
+  const double p1 = x1[K] * inv, p2 = x2[K] * inv;
+  x1[K] = p1;
+  x2[K] = p2;
+#pragma unroll
+  for (int r = 0; r < NV; ++r) {
+    if (r == K) continue;
+    const double m = __shfl_sync(0xffffffffu, x1[r], K);
+    x1[r] -= m * p1;
+    x2[r] -= m * p2;
+  }
+  if constexpr (K + 1 < NV) gj_step<NV, K + 1>(x1, x2, ok);
+}
+
+template <int NV>
+__global__ void __launch_bounds__(32 * TC_WARPS, 3) part_solve_tc_kernel(
+    const double* __restrict__ sys, const double* __restrict__ rhs, double sign, int64_t n,
+    double* __restrict__ Y, double* __restrict__ V, double* __restrict__ W,
+    double* __restrict__ G, int* __restrict__ flag) {
+  static_assert(NV <= 16 && 3 * NV <= 64, "tile size");
+  constexpr int NV2 = NV * NV;
+  extern __shared__ __align__(16) double tsm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* base = tsm + (size_t)wid * (TC_TILES * TC_TILE + 64);
+  double* tL = base;
+  double* tD = tL + TC_TILE;
+  double* tU = tD + TC_TILE;
+  double* tF = tU + TC_TILE;
+  double* tV = tF + TC_TILE;
+  double* tG = tV + TC_TILE;
+  double* tW = tG + TC_TILE;
+  double* vb = tW + TC_TILE;  // 32: b / y
+  double* vc = vb + 32;       // 32: c_b / y_n
+  const int64_t P = (n + BT_M - 1) / BT_M;
+  const int64_t p = blockIdx.x * (int64_t)TC_WARPS + wid;
+  if (p >= P) return;
+  const int64_t s = p * BT_M;
+  const int64_t e = ((s + BT_M < n) ? s + BT_M : n) - 1;
+  if (e == s) return;
+  for (int i = lane; i < TC_TILES * TC_TILE + 64; i += 32) base[i] = 0.0;
+  __syncwarp();
+  bool ok = true;
+  // augmented column j of lane: j = lane (0..31) and j2 = 32 + lane (lanes < 8)
+  // columns: [0, NV) D', NV b, [NV+1, 2NV+1) F = -L V, [2NV+1, 3NV+1) U
+  constexpr int NA = 3 * NV + 1;
+  auto colval = [&](int j, int i) -> double {
+    if (j < NV) return tD[i * TC_LD + j];
+    if (j == NV) return vb[i];
+    if (j < 2 * NV + 1) return tF[i * TC_LD + (j - NV - 1)];
+    if (j < NA) return tU[i * TC_LD + (j - 2 * NV - 1)];
+    return 0.0;
+  };
+  for (int64_t i = s; i < e; ++i) {
+    // stage L, D, U (rows of NV, contiguous in sys) and b
+    const double* src = sys + i * 3 * NV2;
+    for (int t = lane; t < 3 * NV2; t += 32) {
+      const int blk = t / NV2, rem = t - blk * NV2, rr = rem / NV, cc = rem - rr * NV;
+      (blk == 0 ? tL : blk == 1 ? tD : tU)[rr * TC_LD + cc] = src[t];
+    }
+    if (lane < NV) vb[lane] = sign * rhs[i * NV + lane];
+    __syncwarp();
+    if (i > s) {
+      tc_mm(tL, tG, tD, tD, -1.0, lane);   // D' = D - L G
+      tc_mm(tL, tV, tF, nullptr, -1.0, lane);  // F = -L V
+      if (lane < NV) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < NV; ++k) acc += tL[lane * TC_LD + k] * vc[k];
+        vb[lane] -= acc;  // b' = b - L c_b
+      }
+    } else {
+      for (int t = lane; t < NV2; t += 32) {
+        const int rr = t / NV, cc = t - rr * NV;
+        tF[rr * TC_LD + cc] = -tL[rr * TC_LD + cc];
+      }
+    }
+    __syncwarp();
+    // Gauss-Jordan on the augmented columns (one or two per lane)
+    double x1[NV], x2[NV];
+#pragma unroll
+    for (int r = 0; r < NV; ++r) {
+      x1[r] = colval(lane, r);
+      x2[r] = (lane + 32 < NA) ? colval(lane + 32, r) : 0.0;
+    }
+    gj_step<NV, 0>(x1, x2, ok);
+    // lanes' solved columns -> c_b, V (= D'^-1 F), G (= D'^-1 U) or W (last row)
+    __syncwarp();
+    const bool last = (i == e - 1);
+#define ADROM_BT_PUT(j, x)                                                                  \
+  do {                                                                                      \
+    if ((j) == NV) {                                                                        \
+      _Pragma("unroll") for (int r = 0; r < NV; ++r) vc[r] = x[r];                          \
+    } else if ((j) > NV && (j) < 2 * NV + 1) {                                              \
+      _Pragma("unroll") for (int r = 0; r < NV; ++r) tV[r * TC_LD + ((j) - NV - 1)] = x[r]; \
+    } else if ((j) >= 2 * NV + 1 && (j) < NA) {                                             \
+      double* t_ = last ? tW : tG;                                                          \
+      const double sg_ = last ? -1.0 : 1.0;                                                 \
+      _Pragma("unroll") for (int r = 0; r < NV; ++r) t_[r * TC_LD + ((j) - 2 * NV - 1)] =   \
+          sg_ * x[r];                                                                       \
+    }                                                                                       \
+  } while (0)
+    ADROM_BT_PUT(lane, x1);
+    if (lane + 32 < NA) ADROM_BT_PUT(lane + 32, x2);
+#undef ADROM_BT_PUT
+    __syncwarp();
+    if (last)
+      for (int t = lane; t < NV2; t += 32) tG[(t / NV) * TC_LD + (t % NV)] = 0.0;
+    __syncwarp();
+    if (lane < NV) Y[i * NV + lane] = vc[lane];
+    for (int t = lane; t < NV2; t += 32) {
+      const int rr = t / NV, cc = t - rr * NV;
+      V[i * NV2 + t] = tV[rr * TC_LD + cc];
+      G[i * NV2 + t] = tG[rr * TC_LD + cc];
+    }
+    __syncwarp();
+  }
+  // backward sweep: y_i = c_i - G_i y_{i+1}, V_i -= G_i V_{i+1}, W_i = -G_i W_{i+1}
+  for (int t = lane; t < NV2; t += 32) W[(e - 1) * NV2 + t] = tW[(t / NV) * TC_LD + (t % NV)];
+  double* cV = tV;
+  double* cW = tW;
+  double* nV = tF;
+  double* nW = tU;
+  for (int64_t i = e - 2; i >= s; --i) {
+    for (int t = lane; t < NV2; t += 32) {
+      const int rr = t / NV, cc = t - rr * NV;
+      tL[rr * TC_LD + cc] = G[i * NV2 + t];  // G_i
+      tD[rr * TC_LD + cc] = V[i * NV2 + t];  // V_i
+    }
+    if (lane < NV) vb[lane] = Y[i * NV + lane];
+    __syncwarp();
+    double yv = 0.0;
+    if (lane < NV) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) acc += tL[lane * TC_LD + k] * vc[k];
+      yv = vb[lane] - acc;
+    }
+    tc_mm(tL, cV, nV, tD, -1.0, lane);
+    tc_mm(tL, cW, nW, nullptr, -1.0, lane);
+    __syncwarp();
+    if (lane < NV) vc[lane] = yv;
+    double* t1 = cV;
+    cV = nV;
+    nV = t1;
+    t1 = cW;
+    cW = nW;
+    nW = t1;
+    __syncwarp();
+    if (lane < NV) Y[i * NV + lane] = vc[lane];
+    for (int t = lane; t < NV2; t += 32) {
+      const int rr = t / NV, cc = t - rr * NV;
+      V[i * NV2 + t] = cV[rr * TC_LD + cc];
+      W[i * NV2 + t] = cW[rr * TC_LD + cc];
+    }
+    __syncwarp();
+  }
+  if (!ok && lane == 0) atomicOr(flag, 2);
+}
+
 // ---------------------------------------------------------------------------
 // scalar (n_var = 1) partitions: the same elimination, staged through smem so
 // that global traffic is coalesced.  A warp owns 32 consecutive partitions
@@ -828,10 +1063,20 @@ static int bt_solve_t(adrom_ctx* ctx, const double* sys, const double* rhs, doub
                            (int)sm);
       part_solve_scalar_kernel<<<(int)(g < 1 ? 1 : g), 32 * PS_WARPS, sm, ctx->stream>>>(
           L.sys, L.rhs, L.sign, L.n, L.Y, L.V, L.W, flag);
-    } else if (NV > 8) {  // half-warp per partition (13 x 13 blocks)
-      const int64_t g2 = (P * 16 + 127) / 128;
-      part_solve_hw_kernel<NV><<<(int)g2, 128, 0, ctx->stream>>>(L.sys, L.rhs, L.sign, L.n, L.Y,
-                                                                 L.V, L.W, L.G, flag);
+    } else if (NV > 8) {  // warp per partition, DMMA block products (13 x 13 blocks)
+      static const bool hw = getenv("ADROM_BT_HALFWARP") && atoi(getenv("ADROM_BT_HALFWARP"));
+      if (hw) {
+        const int64_t g2 = (P * 16 + 127) / 128;
+        part_solve_hw_kernel<NV><<<(int)g2, 128, 0, ctx->stream>>>(L.sys, L.rhs, L.sign, L.n,
+                                                                   L.Y, L.V, L.W, L.G, flag);
+      } else {
+        const size_t sm = sizeof(double) * TC_WARPS * (TC_TILES * TC_TILE + 64);
+        cudaFuncSetAttribute(part_solve_tc_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sm);
+        const int64_t g2 = (P + TC_WARPS - 1) / TC_WARPS;
+        part_solve_tc_kernel<NV><<<(int)g2, 32 * TC_WARPS, sm, ctx->stream>>>(
+            L.sys, L.rhs, L.sign, L.n, L.Y, L.V, L.W, L.G, flag);
+      }
     } else {
       part_solve_kernel<NV><<<gb, nt, 0, ctx->stream>>>(L.sys, L.rhs, L.sign, L.n, L.Y, L.V, L.W,
                                                         L.G, flag);

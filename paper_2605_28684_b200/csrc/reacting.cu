@@ -86,8 +86,11 @@ __global__ void __launch_bounds__(RX_NT) reacting_rhs_kernel(const double* __res
 
 // Banded FD Jacobian (fom.py:301-328 generalised; oracle/physics.py
 // fd_jacobian_blocks): column (cell g, var v) with eps = 1e-7 max(1, |q|)
-// touches rows g-1 (right block), g (centre), g+1 (left block).  A tile of
-// RJ_T cells is staged with a 2-cell halo and its base residuals.
+// touches rows g-1 (right block), g (centre), g+1 (left block).  Perturbing
+// cell g changes only the faces g-1/2, g+1/2 and the sources of g, so each
+// column evaluates 2 fluxes + 1 source term and reuses the tile's base faces
+// and sources for the rest of the three rows — the same operations on the
+// same operands as re-evaluating whole cell residuals (bitwise equal).
 // apply_dt: A = I - dt J (fom.py:343-344).
 constexpr int RJ_T = 32;
 
@@ -98,7 +101,8 @@ __global__ void __launch_bounds__(128) reacting_jac_kernel(const double* __restr
                                                             bool apply_dt, double dt,
                                                             int* __restrict__ flag) {
   __shared__ double cs[RX_NV * (RJ_T + 4)];   // cells base-2 .. base+T+1
-  __shared__ double fb[RX_NV * (RJ_T + 2)];   // base residuals of rows base-1 .. base+T
+  __shared__ double ff[RX_NV * (RJ_T + 3)];   // base faces: face j between cs cells j and j+1
+  __shared__ double sb[RX_NV * (RJ_T + 2)];   // base sources of cs cells 1 .. T+2
   __shared__ double mk[5 * RX_NR];
   for (int e = threadIdx.x; e < 5 * RX_NR; e += blockDim.x) mk[e] = mech[e];
   constexpr int NV2 = RX_NV * RX_NV;
@@ -115,9 +119,14 @@ __global__ void __launch_bounds__(128) reacting_jac_kernel(const double* __restr
       cs[e] = q[g * RX_NV + v];
     }
     __syncthreads();
-    for (int j = threadIdx.x; j < cnt + 2; j += blockDim.x)  // row base-1+j: cells j, j+1, j+2
-      rx_cell_res(cs + RX_NV * j, cs + RX_NV * (j + 1), cs + RX_NV * (j + 2), gamma, dx, mk,
-                  fb + RX_NV * j);
+    // faces 0 .. cnt+2 and sources of cs cells 1 .. cnt+2 (rows base-1 .. base+cnt)
+    for (int j = threadIdx.x; j < 2 * cnt + 5; j += blockDim.x) {
+      if (j < cnt + 3) rx_rusanov(cs + RX_NV * j, cs + RX_NV * (j + 1), gamma, ff + RX_NV * j);
+      else {
+        const int c = j - (cnt + 3);  // 0 .. cnt+1  -> cs cell c+1
+        rx_sources(cs + RX_NV * (c + 1), gamma, mk, sb + RX_NV * c);
+      }
+    }
     __syncthreads();
     for (int item = threadIdx.x; item < cnt * RX_NV; item += blockDim.x) {
       const int il = item / RX_NV, v = item - il * RX_NV;  // cell base+il, var v
@@ -128,25 +137,29 @@ __global__ void __launch_bounds__(128) reacting_jac_kernel(const double* __restr
 #pragma unroll
       for (int a = 0; a < RX_NV; ++a) pc[a] = cs[RX_NV * jc + a];
       pc[v] = qv + eps;
+      double fl[RX_NV], fr[RX_NV], sp[RX_NV];
+      rx_rusanov(cs + RX_NV * (jc - 1), pc, gamma, fl);  // face g-1/2 (index jc-1)
+      rx_rusanov(pc, cs + RX_NV * (jc + 1), gamma, fr);  // face g+1/2 (index jc)
+      rx_sources(pc, gamma, mk, sp);
       const int64_t g = base + il;
-      // rows g-1 (slot 2), g (slot 1), g+1 (slot 0)
+      // rows g-1 (slot 2), g (slot 1), g+1 (slot 0); row with cs index m has
+      // base residual from faces m-1, m and sources sb[m-1]
 #pragma unroll 1
       for (int rr = 0; rr < 3; ++rr) {
-        double fp[RX_NV];
-        const double* l = cs + RX_NV * (jc - 2 + rr);
-        const double* c = cs + RX_NV * (jc - 1 + rr);
-        const double* r = cs + RX_NV * (jc + rr);
-        if (rr == 0) rx_cell_res(l, c, pc, gamma, dx, mk, fp);
-        else if (rr == 1) rx_cell_res(l, pc, r, gamma, dx, mk, fp);
-        else rx_cell_res(pc, c, r, gamma, dx, mk, fp);
+        const int m = jc - 1 + rr;  // cs index of the row's cell
         int64_t row = g - 1 + rr;
         row = ((row % n) + n) % n;
         const int slot = 2 - rr;
-        const double* f0 = fb + RX_NV * (il + rr);  // base residual of that row
         double* B = blocks + ((row * 3 + slot) * NV2);
 #pragma unroll
         for (int a = 0; a < RX_NV; ++a) {
-          const double jv = (fp[a] - f0[a]) / eps;
+          const double Flo = (rr == 2) ? fr[a] : (rr == 1 ? fl[a] : ff[RX_NV * (m - 1) + a]);
+          const double Fhi = (rr == 0) ? fl[a] : (rr == 1 ? fr[a] : ff[RX_NV * m + a]);
+          const double S = (rr == 1) ? sp[a] : sb[RX_NV * (m - 1) + a];
+          const double f0 = rx_combine(ff[RX_NV * m + a], ff[RX_NV * (m - 1) + a],
+                                       sb[RX_NV * (m - 1) + a], dx);
+          const double fp = rx_combine(Fhi, Flo, S, dx);
+          const double jv = (fp - f0) / eps;
           bad |= !isfinite(jv);
           B[a * RX_NV + v] = apply_dt ? ((slot == 1 && a == v) ? 1.0 : 0.0) - dt * jv : jv;
         }

@@ -51,14 +51,9 @@ __device__ __forceinline__ void rx_rusanov(const double* l, const double* r, dou
   }
 }
 
-// residual of one cell from its stencil (l, c, r): -(F(c,r) - F(l,c))/dx + S(c),
-// the same operations as the full kernel (faces computed identically)
-__device__ __forceinline__ void rx_cell_res(const double* l, const double* c, const double* r, double gamma,
-                            double dx, const double* mk, double* out) {
-  double fl[RX_NV], fr[RX_NV];
-  rx_rusanov(l, c, gamma, fl);
-  rx_rusanov(c, r, gamma, fr);
-  double s[RX_NV];
+// sources of one cell (12 first-order Arrhenius reactions)
+__device__ __forceinline__ void rx_sources(const double* c, double gamma, const double* mk,
+                                           double* s) {
 #pragma unroll
   for (int v = 0; v < RX_NV; ++v) s[v] = 0.0;
   double rho, vel, p;
@@ -75,8 +70,25 @@ __device__ __forceinline__ void rx_cell_res(const double* l, const double* c, co
     }
     s[2] = s[2] + mk[4 * RX_NR + j] * w;
   }
+}
+
+// residual of a cell from its two face fluxes and its sources
+__device__ __forceinline__ double rx_combine(double fr, double fl, double s, double dx) {
+  return (-(fr - fl)) / dx + s;
+}
+
+// residual of one cell from its stencil (l, c, r): -(F(c,r) - F(l,c))/dx + S(c),
+// the same operations as the full kernel (faces computed identically)
+__device__ __forceinline__ void rx_cell_res(const double* l, const double* c, const double* r,
+                                            double gamma, double dx, const double* mk,
+                                            double* out) {
+  double fl[RX_NV], fr[RX_NV];
+  rx_rusanov(l, c, gamma, fl);
+  rx_rusanov(c, r, gamma, fr);
+  double s[RX_NV];
+  rx_sources(c, gamma, mk, s);
 #pragma unroll
-  for (int v = 0; v < RX_NV; ++v) out[v] = (-(fr[v] - fl[v])) / dx + s[v];
+  for (int v = 0; v < RX_NV; ++v) out[v] = rx_combine(fr[v], fl[v], s[v], dx);
 }
 
 
