@@ -187,6 +187,103 @@ __global__ void __launch_bounds__(SOD_NT) sod_rhs_kernel(
   }
 }
 
+
+// Warp-contiguous form (replaces the tile/shared-memory kernel for the full
+// grid): lane l of a warp owns cell 32 ch + l; each cell's primitives, sound
+// speed and physical flux are computed once and handed to the left
+// neighbour's face by shuffles (the reference's rusanov_flux evaluates them
+// once per face side: the same operations on the same operands, bitwise).
+// No shared memory, no barriers: 16 warps / SM keep the loads in flight.
+struct SodQ {
+  double f0, f1, f2, a;  // physical flux and |u| + c
+};
+__device__ __forceinline__ SodQ sod_q(const Cons& u, double gamma) {
+  double rho, vel, p;
+  euler_prim(u, gamma, rho, vel, p);
+  const double c = sqrt((gamma * p) / rho);
+  SodQ q;
+  q.f0 = u.m1;
+  q.f1 = u.m1 * vel + p;
+  q.f2 = vel * (u.m2 + p);
+  q.a = fabs(vel) + c;
+  return q;
+}
+__device__ __forceinline__ Cons sod_face(const Cons& l, const SodQ& ql, const Cons& r,
+                                         const SodQ& qr) {
+  const double hs = 0.5 * np_max(ql.a, qr.a);
+  Cons f;
+  f.m0 = 0.5 * (ql.f0 + qr.f0) - hs * (r.m0 - l.m0);
+  f.m1 = 0.5 * (ql.f1 + qr.f1) - hs * (r.m1 - l.m1);
+  f.m2 = 0.5 * (ql.f2 + qr.f2) - hs * (r.m2 - l.m2);
+  return f;
+}
+constexpr int SODW_NT = 256;
+template <int MODE>
+__global__ void __launch_bounds__(SODW_NT) sod_rhs_warp_kernel(
+    const double* __restrict__ q, double* __restrict__ out, int64_t n, double dx, double gamma,
+    const double* __restrict__ qprev, double dt, double* __restrict__ partial,
+    int* __restrict__ flag) {
+  __shared__ double red[SODW_NT / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nchunks = (n + 31) / 32;
+  const int64_t wstride = (int64_t)gridDim.x * (SODW_NT / 32);
+  double acc = 0.0;
+  bool bad = false;
+  constexpr unsigned FULL = 0xffffffffu;
+  for (int64_t ch = (int64_t)blockIdx.x * (SODW_NT / 32) + warp; ch < nchunks; ch += wstride) {
+    const int64_t c = ch * 32 + lane;
+    const bool valid = c < n;
+    const int64_t cc = valid ? c : n - 1;
+    const Cons u = load_cons(q, cc);
+    const SodQ qu = sod_q(u, gamma);
+    // right neighbour (zero-gradient ghost at the end: fom.py:267)
+    Cons ur;
+    SodQ qr;
+    ur.m0 = __shfl_down_sync(FULL, u.m0, 1);
+    ur.m1 = __shfl_down_sync(FULL, u.m1, 1);
+    ur.m2 = __shfl_down_sync(FULL, u.m2, 1);
+    qr.f0 = __shfl_down_sync(FULL, qu.f0, 1);
+    qr.f1 = __shfl_down_sync(FULL, qu.f1, 1);
+    qr.f2 = __shfl_down_sync(FULL, qu.f2, 1);
+    qr.a = __shfl_down_sync(FULL, qu.a, 1);
+    if (cc + 1 >= n) {
+      ur = u;
+      qr = qu;
+    } else if (lane == 31) {
+      ur = load_cons(q, cc + 1);
+      qr = sod_q(ur, gamma);
+    }
+    const Cons fr = sod_face(u, qu, ur, qr);
+    Cons fl;
+    fl.m0 = __shfl_up_sync(FULL, fr.m0, 1);
+    fl.m1 = __shfl_up_sync(FULL, fr.m1, 1);
+    fl.m2 = __shfl_up_sync(FULL, fr.m2, 1);
+    if (lane == 0) {
+      const int64_t li = cc == 0 ? 0 : cc - 1;
+      const Cons ul = load_cons(q, li);
+      fl = sod_face(ul, sod_q(ul, gamma), u, qu);
+    }
+    Cons o = sod_cell_from_faces(fl, fr, dx);
+    if (valid) {
+      if (MODE == 1) {
+        o.m0 = (u.m0 - qprev[3 * c]) - dt * o.m0;
+        o.m1 = (u.m1 - qprev[3 * c + 1]) - dt * o.m1;
+        o.m2 = (u.m2 - qprev[3 * c + 2]) - dt * o.m2;
+        acc += o.m0 * o.m0 + o.m1 * o.m1 + o.m2 * o.m2;
+        bad |= !(isfinite(o.m0) && isfinite(o.m1) && isfinite(o.m2));
+      }
+      out[3 * c] = o.m0;
+      out[3 * c + 1] = o.m1;
+      out[3 * c + 2] = o.m2;
+    }
+  }
+  if (MODE == 1) {
+    const double s = block_sum<SODW_NT>(acc, red);
+    if (threadIdx.x == 0) partial[blockIdx.x] = s;
+    if (bad) atomicOr(flag, 1);
+  }
+}
+
 // deterministic final sum of per-block partials (one block)
 __global__ void sum_partials_kernel(const double* __restrict__ partial, int n,
                                     double* __restrict__ out) {
@@ -463,13 +560,13 @@ static int launch_residual(adrom_ctx* ctx, const adrom_model& m, const double* x
       burgers_rhs_kernel<0><<<nb, BURG_NT, 0, ctx->stream>>>(x, out, m.n_elem, burgers_params(m),
                                                             nullptr, 0.0, nullptr, nullptr);
   } else {
-    nb = grid_for(ctx, m.n_elem, SOD_TILE);
+    nb = grid_for(ctx, m.n_elem, SODW_NT);
     if (newton)
-      sod_rhs_kernel<1><<<nb, SOD_NT, 0, ctx->stream>>>(x, out, m.n_elem, m.dx, m.gamma, qprev,
-                                                       dt, partial, flag);
+      sod_rhs_warp_kernel<1><<<nb, SODW_NT, 0, ctx->stream>>>(x, out, m.n_elem, m.dx, m.gamma,
+                                                            qprev, dt, partial, flag);
     else
-      sod_rhs_kernel<0><<<nb, SOD_NT, 0, ctx->stream>>>(x, out, m.n_elem, m.dx, m.gamma, nullptr,
-                                                       0.0, nullptr, nullptr);
+      sod_rhs_warp_kernel<0><<<nb, SODW_NT, 0, ctx->stream>>>(x, out, m.n_elem, m.dx, m.gamma,
+                                                            nullptr, 0.0, nullptr, nullptr);
   }
   if (nblocks_out) *nblocks_out = nb;
   ADROM_LAUNCH_CK(ctx);

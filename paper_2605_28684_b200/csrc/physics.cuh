@@ -15,6 +15,19 @@ namespace adrom {
 constexpr double PRIM_FLOOR = 1e-10;  // fom.py:36
 constexpr double FD_EPS = 1e-7;       // fom.py:39
 
+// IEEE division a / b with a shortcut for an exact-zero numerator: for
+// b finite and nonzero, 0 / b is +-0 (sign = sign(a) xor sign(b)), which is
+// what div.rn.f64 returns — but its software sequence routes a zero
+// numerator through the slow path (a subroutine call per division).  Uniform
+// regions (zero velocity, zero flux differences) hit that case on every
+// cell.  Bitwise identical to a / b for every input.
+__device__ __forceinline__ double zdiv(double a, double b) {
+  if (a == 0.0 && b != 0.0 && isfinite(b))
+    return __longlong_as_double((__double_as_longlong(a) ^ __double_as_longlong(b)) &
+                                (long long)0x8000000000000000ull);
+  return a / b;
+}
+
 struct BurgersParams {
   double dx, nu, dx2;  // dx2 = dx**2 (fom.py:187)
 };
@@ -24,6 +37,8 @@ __device__ __forceinline__ double burgers_cell(double um, double u, double up,
                                                const BurgersParams& p) {
   // np.where(u > 0, back, fwd): only the selected one-sided difference is
   // divided (same value bit for bit, one division instead of two)
+  // plain IEEE division: the Burgers states are smooth (zdiv's test costs
+  // more than the rare zero-numerator slow path; measured 0.064 vs 0.074 ms)
   const double conv = (-u) * ((u > 0.0) ? (u - um) / p.dx : (up - u) / p.dx);
   const double lap = (um - 2.0 * u) + up;
   const double diff = (p.nu * lap) / p.dx2;
@@ -38,7 +53,7 @@ struct Cons {
 __device__ __forceinline__ void euler_prim(const Cons& c, double gamma, double& rho,
                                            double& vel, double& p) {
   rho = np_max(c.m0, PRIM_FLOOR);
-  vel = c.m1 / rho;
+  vel = zdiv(c.m1, rho);
   const double kinetic = (0.5 * rho) * (vel * vel);
   p = np_max((gamma - 1.0) * (c.m2 - kinetic), PRIM_FLOOR);
 }
@@ -65,9 +80,9 @@ __device__ __forceinline__ Cons rusanov(const Cons& l, const Cons& r, double gam
 // fom.py:269 / fom.py:277:  -(F_hi - F_lo) / dx
 __device__ __forceinline__ Cons sod_cell_from_faces(const Cons& lo, const Cons& hi, double dx) {
   Cons o;
-  o.m0 = (-(hi.m0 - lo.m0)) / dx;
-  o.m1 = (-(hi.m1 - lo.m1)) / dx;
-  o.m2 = (-(hi.m2 - lo.m2)) / dx;
+  o.m0 = zdiv(-(hi.m0 - lo.m0), dx);
+  o.m1 = zdiv(-(hi.m1 - lo.m1), dx);
+  o.m2 = zdiv(-(hi.m2 - lo.m2), dx);
   return o;
 }
 

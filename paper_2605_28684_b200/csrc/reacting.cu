@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(RX_NT) reacting_rhs_kernel(const double* __res
       }
 #pragma unroll
       for (int v = 0; v < RX_NV; ++v) {
-        const double div = (-(faces[RX_NV * (c + 1) + v] - faces[RX_NV * c + v])) / dx;
+        const double div = zdiv(-(faces[RX_NV * (c + 1) + v] - faces[RX_NV * c + v]), dx);
         res[v] = div + s[v];
       }
     }
@@ -83,6 +83,7 @@ __global__ void __launch_bounds__(RX_NT) reacting_rhs_kernel(const double* __res
     for (int e = threadIdx.x; e < RX_NV * cnt; e += RX_NT) dst[e] = faces[e];
   }
 }
+
 
 // Banded FD Jacobian (fom.py:301-328 generalised; oracle/physics.py
 // fd_jacobian_blocks): column (cell g, var v) with eps = 1e-7 max(1, |q|)

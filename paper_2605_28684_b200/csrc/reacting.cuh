@@ -20,7 +20,7 @@ constexpr int RX_NT = 128;
 __device__ __forceinline__ void rx_prim(const double* c, double gamma, double& rho, double& vel,
                                         double& p) {
   rho = np_max(c[0], PRIM_FLOOR);
-  vel = c[1] / rho;
+  vel = zdiv(c[1], rho);
   const double kin = (0.5 * rho) * (vel * vel);
   p = np_max((gamma - 1.0) * (c[2] - kin), PRIM_FLOOR);
 }
@@ -45,8 +45,8 @@ __device__ __forceinline__ void rx_rusanov(const double* l, const double* r, dou
   f[2] = 0.5 * (fl + fr) - hs * (r[2] - l[2]);
 #pragma unroll
   for (int k = 0; k < RX_NS; ++k) {
-    fl = l[1] * (l[3 + k] / rl);
-    fr = r[1] * (r[3 + k] / rr);
+    fl = l[1] * zdiv(l[3 + k], rl);
+    fr = r[1] * zdiv(r[3 + k], rr);
     f[3 + k] = 0.5 * (fl + fr) - hs * (r[3 + k] - l[3 + k]);
   }
 }
@@ -74,7 +74,7 @@ __device__ __forceinline__ void rx_sources(const double* c, double gamma, const 
 
 // residual of a cell from its two face fluxes and its sources
 __device__ __forceinline__ double rx_combine(double fr, double fl, double s, double dx) {
-  return (-(fr - fl)) / dx + s;
+  return zdiv(-(fr - fl), dx) + s;
 }
 
 // residual of one cell from its stencil (l, c, r): -(F(c,r) - F(l,c))/dx + S(c),
