@@ -651,14 +651,33 @@ __global__ void __launch_bounds__(32 * TC_WARPS, 3) part_solve_tc_kernel(
     if (j < NA) return tU[i * TC_LD + (j - 2 * NV - 1)];
     return 0.0;
   };
+  // row i's L, D, U and b are prefetched into registers while row i-1 is
+  // eliminated (PF values per lane), then scattered into the tiles
+  constexpr int PF = (3 * NV2 + 31) / 32;
+  double pre[PF];
+  double preb = 0.0;
+  auto fetch = [&](int64_t i) {
+    const double* src = sys + i * 3 * NV2;
+#pragma unroll
+    for (int m = 0; m < PF; ++m) {
+      const int t = lane + 32 * m;
+      pre[m] = (t < 3 * NV2) ? src[t] : 0.0;
+    }
+    preb = (lane < NV) ? sign * rhs[i * NV + lane] : 0.0;
+  };
+  fetch(s);
   for (int64_t i = s; i < e; ++i) {
     // stage L, D, U (rows of NV, contiguous in sys) and b
-    const double* src = sys + i * 3 * NV2;
-    for (int t = lane; t < 3 * NV2; t += 32) {
-      const int blk = t / NV2, rem = t - blk * NV2, rr = rem / NV, cc = rem - rr * NV;
-      (blk == 0 ? tL : blk == 1 ? tD : tU)[rr * TC_LD + cc] = src[t];
+#pragma unroll
+    for (int m = 0; m < PF; ++m) {
+      const int t = lane + 32 * m;
+      if (t < 3 * NV2) {
+        const int blk = t / NV2, rem = t - blk * NV2, rr = rem / NV, cc = rem - rr * NV;
+        (blk == 0 ? tL : blk == 1 ? tD : tU)[rr * TC_LD + cc] = pre[m];
+      }
     }
-    if (lane < NV) vb[lane] = sign * rhs[i * NV + lane];
+    if (lane < NV) vb[lane] = preb;
+    if (i + 1 < e) fetch(i + 1);
     __syncwarp();
     if (i > s) {
       tc_mm(tL, tG, tD, tD, -1.0, lane);   // D' = D - L G
@@ -721,13 +740,30 @@ __global__ void __launch_bounds__(32 * TC_WARPS, 3) part_solve_tc_kernel(
   double* cW = tW;
   double* nV = tF;
   double* nW = tU;
-  for (int64_t i = e - 2; i >= s; --i) {
-    for (int t = lane; t < NV2; t += 32) {
-      const int rr = t / NV, cc = t - rr * NV;
-      tL[rr * TC_LD + cc] = G[i * NV2 + t];  // G_i
-      tD[rr * TC_LD + cc] = V[i * NV2 + t];  // V_i
+  constexpr int PB = (NV2 + 31) / 32;
+  double pg[PB], pv[PB], py = 0.0;
+  auto fetch_b = [&](int64_t i) {
+#pragma unroll
+    for (int m = 0; m < PB; ++m) {
+      const int t = lane + 32 * m;
+      pg[m] = (t < NV2) ? G[i * NV2 + t] : 0.0;
+      pv[m] = (t < NV2) ? V[i * NV2 + t] : 0.0;
     }
-    if (lane < NV) vb[lane] = Y[i * NV + lane];
+    py = (lane < NV) ? Y[i * NV + lane] : 0.0;
+  };
+  if (e - 2 >= s) fetch_b(e - 2);
+  for (int64_t i = e - 2; i >= s; --i) {
+#pragma unroll
+    for (int m = 0; m < PB; ++m) {
+      const int t = lane + 32 * m;
+      if (t < NV2) {
+        const int rr = t / NV, cc = t - rr * NV;
+        tL[rr * TC_LD + cc] = pg[m];  // G_i
+        tD[rr * TC_LD + cc] = pv[m];  // V_i
+      }
+    }
+    if (lane < NV) vb[lane] = py;
+    if (i - 1 >= s) fetch_b(i - 1);
     __syncwarp();
     double yv = 0.0;
     if (lane < NV) {
