@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(RX_NT) reacting_rhs_kernel(const double* __res
 // apply_dt: A = I - dt J (fom.py:343-344).
 constexpr int RJ_T = 32;
 
-__global__ void __launch_bounds__(128, 4) reacting_jac_kernel(const double* __restrict__ q, int64_t n,
+__global__ void __launch_bounds__(128) reacting_jac_kernel(const double* __restrict__ q, int64_t n,
                                                             double dx, double gamma,
                                                             const double* __restrict__ mech,
                                                             double* __restrict__ blocks,

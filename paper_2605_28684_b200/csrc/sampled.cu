@@ -28,7 +28,7 @@ __device__ __forceinline__ double eval_row_reacting(const PlanView& p, int j, co
                                                  const double* dir, int ldd, int k, double h) {
   const int64_t* g = p.gather + 3 * RX_NV * p.out_cell[j];
   double o[RX_NV];
-  rx_cell_res_get(
+  rx_cell_res_get<false>(
       [&](int s, int v) {
         const int64_t pos = g[s * RX_NV + v];
         return dir ? qc[pos] + h * dir[pos * ldd + k] : qc[pos];

@@ -133,6 +133,13 @@ struct adrom_session {
   adrom_ctx* fctx = nullptr;
   cudaStream_t fstream = nullptr;
   cudaEvent_t main_mark = nullptr, fom_done = nullptr;
+  // the session's own stream at the device's greatest priority: the reduced
+  // steps and adaptation events (the critical path) win SM slots over the
+  // coarse Newton step overlapping them on the default-priority fstream.
+  // Entry points run on it with event hand-offs to and from the caller's
+  // stream (ADROM_SESSION_PRIORITY=0 keeps everything on the caller's stream)
+  cudaStream_t hstream = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   // factored path: the next event's coarse Newton solve runs on a host thread
   // (its host-side convergence checks would otherwise block the issue of this
   // event's work), started as soon as its input y_corr exists
@@ -194,6 +201,24 @@ __global__ void row_norms_kernel(const double* __restrict__ phi, int64_t n, int 
     out[i] = s;
   }
 }
+
+// runs an entry point on the session's high-priority stream
+struct HiPrio {
+  adrom_session* s;
+  cudaStream_t user;
+  explicit HiPrio(adrom_session* ss) : s(ss), user(ss->ctx->stream) {
+    if (!s->hstream) return;
+    cudaEventRecord(s->ev_in, user);
+    cudaStreamWaitEvent(s->hstream, s->ev_in, 0);
+    s->ctx->stream = s->hstream;
+  }
+  ~HiPrio() {
+    if (!s->hstream) return;
+    cudaEventRecord(s->ev_out, s->hstream);
+    cudaStreamWaitEvent(user, s->ev_out, 0);
+    s->ctx->stream = user;
+  }
+};
 
 int alloc_op(adrom_session* s, adrom_rom_op& op, BigOp& big) {
   const int ns = s->cfg.n_s, nv = s->cfg.model.n_var, r = s->r;
@@ -731,6 +756,17 @@ int adrom_session_create(adrom_ctx* ctx, const adrom_session_config* cfg, adrom_
   if (!st && (cudaEventCreateWithFlags(&s->main_mark, cudaEventDisableTiming) != cudaSuccess ||
               cudaEventCreateWithFlags(&s->fom_done, cudaEventDisableTiming) != cudaSuccess))
     st = set_error(ctx, ADROM_ERR_CUDA, "session: event creation failed");
+  if (!st) {
+    const char* ev = getenv("ADROM_SESSION_PRIORITY");
+    if (!ev || atoi(ev) != 0) {
+      int least = 0, greatest = 0;
+      cudaDeviceGetStreamPriorityRange(&least, &greatest);
+      if (cudaStreamCreateWithPriority(&s->hstream, cudaStreamNonBlocking, greatest) != cudaSuccess ||
+          cudaEventCreateWithFlags(&s->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&s->ev_out, cudaEventDisableTiming) != cudaSuccess)
+        st = set_error(ctx, ADROM_ERR_CUDA, "session: priority stream creation failed");
+    }
+  }
   if (st) {
     adrom_session_destroy(s);
     return st;
@@ -747,6 +783,12 @@ void adrom_session_destroy(adrom_session* s) {
   if (s->fstream) cudaStreamDestroy(s->fstream);
   if (s->main_mark) cudaEventDestroy(s->main_mark);
   if (s->fom_done) cudaEventDestroy(s->fom_done);
+  if (s->ev_in) cudaEventDestroy(s->ev_in);
+  if (s->ev_out) cudaEventDestroy(s->ev_out);
+  if (s->hstream) {
+    cudaStreamSynchronize(s->hstream);
+    cudaStreamDestroy(s->hstream);
+  }
   if (s->cstream) {
     cudaStreamSynchronize(s->cstream);
     cudaStreamDestroy(s->cstream);
@@ -806,6 +848,7 @@ int adrom_session_load(adrom_session* s, const double* q_ref, const double* d, c
 // encode(q_last).  Errors here propagate (they are outside the event try).
 int adrom_session_start(adrom_session* s) {
   if (!s) return ADROM_ERR_ARG;
+  HiPrio hp(s);
   adrom_ctx* ctx = s->ctx;
   const adrom_model m = model_of(s);
   const bool needs_signal = s->cfg.adaptive || s->cfg.sampling == 1;
@@ -827,6 +870,7 @@ int adrom_session_start(adrom_session* s) {
 int adrom_session_advance(adrom_session* s, int64_t n_steps, int64_t save_every, double* dev_out,
                           double* host_out, int64_t* n_saved) {
   if (!s) return ADROM_ERR_ARG;
+  HiPrio hp(s);
   adrom_ctx* ctx = s->ctx;
   int64_t saved = 0;
   const int64_t N = s->N;
@@ -887,6 +931,7 @@ int adrom_session_advance(adrom_session* s, int64_t n_steps, int64_t save_every,
 
 int adrom_session_finish(adrom_session* s) {
   if (!s) return ADROM_ERR_ARG;
+  HiPrio hp(s);
   adrom_ctx* ctx = s->ctx;
   int st = drain_downloads(s);
   if (st) return st;
