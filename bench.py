@@ -147,7 +147,8 @@ def max_over_ranks(x: float, world: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64,
+                     device="cuda" if torch.cuda.is_available() else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -699,7 +700,7 @@ def main(argv=None):
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg3", choices=["cfg0", "cfg1", "cfg2", "cfg3", "cfg4",
                                                          "cfg4-residual"])
-    ap.add_argument("--n", type=int, default=0, help="override grid size (testing)")
+    ap.add_argument("--n-elem", dest="n", type=int, default=0, help="override grid size (testing)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args(argv)
