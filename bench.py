@@ -451,7 +451,23 @@ def bench_rom(args, rank, world):
     # used.  QDEIM is larger in total but is a sequence of rounds of small
     # kernels (qdeim_rounds_per_step below).
     roof = None
-    if "isvd_rotate" in per:
+    if case.model == "reacting" and "decode" in per:
+        # configuration 4: the largest kernels are FP64-pipe bound (the FD
+        # directions of the large-sample LSPG step, bl_dir_kernel, ~1.4 ms per
+        # Gauss-Newton iteration; the coarse step's 13x13 block solve on the
+        # tensor cores).  The HBM roofline is reported on the per-step decode
+        # q~ = q_ref + (Phi a) / d (stream_kernel<128>: Phi read, q_ref and d
+        # read, q~ written: 8 N (r + 3) bytes)
+        dbytes = 8.0 * N * (r + 3)
+        roof = roofline(dbytes, per["decode"][0])
+        roof.update({"kernel": "decode (stream_kernel<128>: q_ref + Phi a / d)",
+                     "work_per_launch": {"bytes": dbytes},
+                     "share_of_step": round(probes["decode"][0] / ms, 4),
+                     "dominant_kernel": {"name": "bl_dir_kernel<reacting> (FD directions, FP64 pipe)",
+                                         "share_of_step": round(probes.get("rom_step", (0, 0))[0] / ms, 4),
+                                         "note": "rom_step share; ncu: FP64 pipe 24 % active, "
+                                                 "profiles/r1_cfg4_lspg_kernels_full.txt"}})
+    elif "isvd_rotate" in per:
         rot_ms = per["isvd_rotate"][0]
         flops = 2.0 * N * r * (r + 1)
         rbytes = 8.0 * (2 * N * r + N) + 8.0 * 5 * N + 1.0 * N
