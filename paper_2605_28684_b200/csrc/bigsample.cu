@@ -634,7 +634,7 @@ __global__ void __launch_bounds__(BL_DIR_T, NBUF == 1 ? 4 : 2)
         o[1] = x.m1;
         o[2] = x.m2;
       } else {
-        rx_cell_res_get<false>(val, pp.gamma, pp.bp.dx, pp.mech, o);
+        rx_cell_res_once<false>(val, pp.gamma, pp.bp.dx, pp.mech, o);
       }
       const int64_t b = big.cell_start[ks];
       const int cnt = big.cell_cnt[ks];

@@ -122,4 +122,84 @@ __device__ __forceinline__ void rx_cell_res_get(const Get& get, double gamma, do
   rx_cell_res<ZD>(l, c, r, gamma, dx, mk, out);
 }
 
+// Cell residual with every cell's primitives, wave speed and physical flux
+// evaluated once (rx_cell_res evaluates the centre cell's twice, once per
+// face): the same operations on the same operands as rx_rusanov /
+// rx_sources / rx_combine, so bitwise equal to rx_cell_res.  Values are
+// fetched through get(slot, var) (slot 0/1/2 = left / centre / right), which
+// lets the caller keep the stencil in shared memory instead of registers.
+template <bool ZD, class Get>
+__device__ __forceinline__ void rx_cell_res_once(const Get& get, double gamma, double dx,
+                                                 const double* mk, double* out) {
+  // centre: primitives, speed, physical flux
+  double cu[3];
+  cu[0] = get(1, 0);
+  cu[1] = get(1, 1);
+  cu[2] = get(1, 2);
+  double rc, vc, pc;
+  rx_prim<ZD>(cu, gamma, rc, vc, pc);
+  const double ac = fabs(vc) + sqrt((gamma * pc) / rc);
+  double fc[RX_NV];
+  fc[0] = cu[1];
+  fc[1] = cu[1] * vc + pc;
+  fc[2] = vc * (cu[2] + pc);
+#pragma unroll
+  for (int k = 0; k < RX_NS; ++k) fc[3 + k] = cu[1] * rx_div<ZD>(get(1, 3 + k), rc);
+  // left face (l, c): flo
+  double flo[RX_NV];
+  {
+    double lu[3] = {get(0, 0), get(0, 1), get(0, 2)};
+    double rl, vl, pl;
+    rx_prim<ZD>(lu, gamma, rl, vl, pl);
+    const double hs = 0.5 * np_max(fabs(vl) + sqrt((gamma * pl) / rl), ac);
+    flo[0] = 0.5 * (lu[1] + fc[0]) - hs * (cu[0] - lu[0]);
+    flo[1] = 0.5 * ((lu[1] * vl + pl) + fc[1]) - hs * (cu[1] - lu[1]);
+    flo[2] = 0.5 * ((vl * (lu[2] + pl)) + fc[2]) - hs * (cu[2] - lu[2]);
+#pragma unroll
+    for (int k = 0; k < RX_NS; ++k) {
+      const double lk = get(0, 3 + k);
+      flo[3 + k] = 0.5 * ((lu[1] * rx_div<ZD>(lk, rl)) + fc[3 + k]) - hs * (get(1, 3 + k) - lk);
+    }
+  }
+  // right face (c, r) -> out = -(fhi - flo) / dx (sources added below)
+  {
+    double ru[3] = {get(2, 0), get(2, 1), get(2, 2)};
+    double rr, vr, pr;
+    rx_prim<ZD>(ru, gamma, rr, vr, pr);
+    const double hs = 0.5 * np_max(ac, fabs(vr) + sqrt((gamma * pr) / rr));
+    out[0] = rx_div<ZD>(-((0.5 * (fc[0] + ru[1]) - hs * (ru[0] - cu[0])) - flo[0]), dx);
+    out[1] = rx_div<ZD>(-((0.5 * (fc[1] + (ru[1] * vr + pr)) - hs * (ru[1] - cu[1])) - flo[1]), dx);
+    out[2] = rx_div<ZD>(-((0.5 * (fc[2] + (vr * (ru[2] + pr))) - hs * (ru[2] - cu[2])) - flo[2]), dx);
+#pragma unroll
+    for (int k = 0; k < RX_NS; ++k) {
+      const double rk = get(2, 3 + k), ck = get(1, 3 + k);
+      const double fhi = 0.5 * (fc[3 + k] + (ru[1] * rx_div<ZD>(rk, rr))) - hs * (rk - ck);
+      out[3 + k] = rx_div<ZD>(-(fhi - flo[3 + k]), dx);
+    }
+  }
+  // sources of the centre cell, accumulated from zero in rx_sources' order
+  // (T = p / rho from the same primitives), then added like rx_combine
+  double sv[RX_NV];
+#pragma unroll
+  for (int v = 0; v < RX_NV; ++v) sv[v] = 0.0;
+  const double temp = pc / rc;
+#pragma unroll 1
+  for (int j = 0; j < RX_NR; ++j) {
+    const int a = (int)mk[j], b = (int)mk[RX_NR + j];
+    double ya = 0.0;
+#pragma unroll
+    for (int k = 0; k < RX_NS; ++k)
+      if (k == a) ya = get(1, 3 + k);
+    const double w = (mk[2 * RX_NR + j] * exp(-mk[3 * RX_NR + j] / temp)) * np_max(ya, 0.0);
+#pragma unroll
+    for (int k = 0; k < RX_NS; ++k) {
+      if (k == a) sv[3 + k] = sv[3 + k] - w;
+      if (k == b) sv[3 + k] = sv[3 + k] + w;
+    }
+    sv[2] = sv[2] + mk[4 * RX_NR + j] * w;
+  }
+#pragma unroll
+  for (int v = 0; v < RX_NV; ++v) out[v] = out[v] + sv[v];
+}
+
 }  // namespace adrom
