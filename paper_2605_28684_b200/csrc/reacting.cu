@@ -95,6 +95,22 @@ __global__ void __launch_bounds__(RX_NT) reacting_rhs_kernel(const double* __res
 // apply_dt: A = I - dt J (fom.py:343-344).
 constexpr int RJ_T = 32;
 
+// per-cell physical flux and wave speed (the side terms of rx_rusanov)
+__device__ __forceinline__ void rx_side(const double* u, double gamma, double* f, double& a) {
+  double rho, vel, p;
+  rx_prim<true>(u, gamma, rho, vel, p);
+  a = fabs(vel) + sqrt((gamma * p) / rho);
+  f[0] = u[1];
+  f[1] = u[1] * vel + p;
+  f[2] = vel * (u[2] + p);
+#pragma unroll
+  for (int k = 0; k < RX_NS; ++k) f[3 + k] = u[1] * rx_div<true>(u[3 + k], rho);
+}
+// rx_rusanov from precomputed sides (same operations, bitwise)
+__device__ __forceinline__ double rx_face_v(double fl, double fr, double hs, double ur, double ul) {
+  return 0.5 * (fl + fr) - hs * (ur - ul);
+}
+
 __global__ void __launch_bounds__(128) reacting_jac_kernel(const double* __restrict__ q, int64_t n,
                                                             double dx, double gamma,
                                                             const double* __restrict__ mech,
@@ -102,8 +118,11 @@ __global__ void __launch_bounds__(128) reacting_jac_kernel(const double* __restr
                                                             bool apply_dt, double dt,
                                                             int* __restrict__ flag) {
   __shared__ double cs[RX_NV * (RJ_T + 4)];   // cells base-2 .. base+T+1
+  __shared__ double fp[RX_NV * (RJ_T + 4)];   // their physical fluxes
+  __shared__ double av[RJ_T + 4];             // their wave speeds |u| + c
   __shared__ double ff[RX_NV * (RJ_T + 3)];   // base faces: face j between cs cells j and j+1
   __shared__ double sb[RX_NV * (RJ_T + 2)];   // base sources of cs cells 1 .. T+2
+  __shared__ double fb[RX_NV * (RJ_T + 2)];   // base residuals of cs cells 1 .. T+2
   __shared__ double mk[5 * RX_NR];
   for (int e = threadIdx.x; e < 5 * RX_NR; e += blockDim.x) mk[e] = mech[e];
   constexpr int NV2 = RX_NV * RX_NV;
@@ -120,12 +139,24 @@ __global__ void __launch_bounds__(128) reacting_jac_kernel(const double* __restr
       cs[e] = q[g * RX_NV + v];
     }
     __syncthreads();
-    // faces 0 .. cnt+2 and sources of cs cells 1 .. cnt+2 (rows base-1 .. base+cnt)
-    for (int j = threadIdx.x; j < 2 * cnt + 5; j += blockDim.x) {
-      if (j < cnt + 3) rx_rusanov(cs + RX_NV * j, cs + RX_NV * (j + 1), gamma, ff + RX_NV * j);
-      else {
-        const int c = j - (cnt + 3);  // 0 .. cnt+1  -> cs cell c+1
-        rx_sources(cs + RX_NV * (c + 1), gamma, mk, sb + RX_NV * c);
+    for (int j = threadIdx.x; j < cnt + 4; j += blockDim.x)
+      rx_side(cs + RX_NV * j, gamma, fp + RX_NV * j, av[j]);
+    __syncthreads();
+    for (int e = threadIdx.x; e < RX_NV * (cnt + 3); e += blockDim.x) {
+      const int j = e / RX_NV, v = e - j * RX_NV;
+      const double hs = 0.5 * np_max(av[j], av[j + 1]);
+      ff[e] = rx_face_v(fp[RX_NV * j + v], fp[RX_NV * (j + 1) + v], hs, cs[RX_NV * (j + 1) + v],
+                        cs[RX_NV * j + v]);
+    }
+    __syncthreads();
+    // base residuals of rows base-1 .. base+cnt (cs cells 1 .. cnt+2)
+    for (int c = threadIdx.x; c < cnt + 2; c += blockDim.x) {
+      double s0[RX_NV];
+      rx_sources<true>(cs + RX_NV * (c + 1), gamma, mk, s0);
+#pragma unroll
+      for (int v = 0; v < RX_NV; ++v) {
+        sb[RX_NV * c + v] = s0[v];
+        fb[RX_NV * c + v] = rx_combine<true>(ff[RX_NV * (c + 1) + v], ff[RX_NV * c + v], s0[v], dx);
       }
     }
     __syncthreads();
@@ -138,29 +169,36 @@ __global__ void __launch_bounds__(128) reacting_jac_kernel(const double* __restr
 #pragma unroll
       for (int a = 0; a < RX_NV; ++a) pc[a] = cs[RX_NV * jc + a];
       pc[v] = qv + eps;
-      double fl[RX_NV], fr[RX_NV], sp[RX_NV];
-      rx_rusanov(cs + RX_NV * (jc - 1), pc, gamma, fl);  // face g-1/2 (index jc-1)
-      rx_rusanov(pc, cs + RX_NV * (jc + 1), gamma, fr);  // face g+1/2 (index jc)
-      rx_sources(pc, gamma, mk, sp);
+      double fpc[RX_NV], apc;
+      rx_side(pc, gamma, fpc, apc);
+      double sp[RX_NV];
+      rx_sources<true>(pc, gamma, mk, sp);
+      const double hl = 0.5 * np_max(av[jc - 1], apc);
+      const double hr = 0.5 * np_max(apc, av[jc + 1]);
       const int64_t g = base + il;
-      // rows g-1 (slot 2), g (slot 1), g+1 (slot 0); row with cs index m has
-      // base residual from faces m-1, m and sources sb[m-1]
+      const double* ul = cs + RX_NV * (jc - 1);
+      const double* ur = cs + RX_NV * (jc + 1);
+      const double* fl0 = fp + RX_NV * (jc - 1);
+      const double* fr0 = fp + RX_NV * (jc + 1);
+      // rows g-1 (slot 2), g (slot 1), g+1 (slot 0); the row of cs cell m
+      // has faces m-1 (lo) and m (hi), sources and base residual fb[m-1]
 #pragma unroll 1
       for (int rr = 0; rr < 3; ++rr) {
-        const int m = jc - 1 + rr;  // cs index of the row's cell
+        const int m = jc - 1 + rr;
         int64_t row = g - 1 + rr;
         row = ((row % n) + n) % n;
         const int slot = 2 - rr;
         double* B = blocks + ((row * 3 + slot) * NV2);
 #pragma unroll
         for (int a = 0; a < RX_NV; ++a) {
-          const double Flo = (rr == 2) ? fr[a] : (rr == 1 ? fl[a] : ff[RX_NV * (m - 1) + a]);
-          const double Fhi = (rr == 0) ? fl[a] : (rr == 1 ? fr[a] : ff[RX_NV * m + a]);
+          const double Fl = rx_face_v(fl0[a], fpc[a], hl, pc[a], ul[a]);  // face g-1/2
+          const double Fr = rx_face_v(fpc[a], fr0[a], hr, ur[a], pc[a]);  // face g+1/2
+          const double Flo = (rr == 0) ? ff[RX_NV * (m - 1) + a] : (rr == 1 ? Fl : Fr);
+          const double Fhi = (rr == 0) ? Fl : (rr == 1 ? Fr : ff[RX_NV * m + a]);
           const double S = (rr == 1) ? sp[a] : sb[RX_NV * (m - 1) + a];
-          const double f0 = rx_combine(ff[RX_NV * m + a], ff[RX_NV * (m - 1) + a],
-                                       sb[RX_NV * (m - 1) + a], dx);
-          const double fp = rx_combine(Fhi, Flo, S, dx);
-          const double jv = (fp - f0) / eps;
+          const double f0 = fb[RX_NV * (m - 1) + a];
+          const double fpv = rx_combine<true>(Fhi, Flo, S, dx);
+          const double jv = (fpv - f0) / eps;
           bad |= !isfinite(jv);
           B[a * RX_NV + v] = apply_dt ? ((slot == 1 && a == v) ? 1.0 : 0.0) - dt * jv : jv;
         }
