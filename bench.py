@@ -532,16 +532,25 @@ def bench_rom(args, rank, world):
     return line
 
 
+E2E_MIN_STEPS = 200
+E2E_RING = 8
+
+
 def e2e_rom(args, case):
     """Online loop through the C-ABI session with HOST buffers: the offline
     results (basis, scaling, last training state) are copied in from pinned
-    host memory inside the timed region and every step's decoded state is
+    host memory inside the timed region, and every step's decoded state is
     copied back to pinned host memory (the reference keeps its trajectory on
-    the host, driver.py:306/344)."""
+    the host, driver.py:306/344) — into a ring of E2E_RING host slots, since a
+    full trajectory of 2^24-cell states does not fit in pinned memory.  The
+    horizon is max(K, 200) online steps of the reference's timed region
+    (driver.py:319-389 covers all n_t - w_init steps), so the one-time upload
+    of the offline basis (8.6 GB at cfg 3) is amortised over a realistic
+    stretch of the run instead of K = 20 steps."""
     import torch
     from paper_2605_28684_b200.driver import Session, offline_stage
     cfg, model = rom_experiment(case)
-    K = args.steps
+    K = min(case.n_t - case.w_init, max(args.steps, E2E_MIN_STEPS))
     N, r = model.n_dof, case.r
     training, scaling, basis0 = offline_stage(cfg, model)
     pin = lambda x: x.detach().to("cpu").pin_memory()  # noqa: E731
@@ -550,8 +559,9 @@ def e2e_rom(args, case):
     phi_norm = scaling.phi_norm
     del training, scaling, basis0
     torch.cuda.empty_cache()
-    out = torch.empty((K, N), dtype=torch.float64, pin_memory=True)
+    out = torch.empty((E2E_RING, N), dtype=torch.float64, pin_memory=True)
     sess = Session(cfg, model, adaptive=True)
+    sess.set_host_ring(E2E_RING)
     from paper_2605_28684_b200.snapshots import ScalingTransform
     from paper_2605_28684_b200.tracking import ReducedBasis
     torch.cuda.synchronize()
@@ -568,8 +578,10 @@ def e2e_rom(args, case):
     h2d = sum(v.numel() * 8 for v in h.values())
     return {"value": round(K / wall, 3), "unit": "online steps/s", "steps": K,
             "h2d_bytes_per_step": int(h2d / K), "d2h_bytes_per_step": 8 * N,
-            "note": "timed region = reference's (driver.py:319-389) incl. start, "
-                    "plus H2D of the offline results; wall clock"}
+            "note": f"timed region = reference's (driver.py:319-389) incl. start, over {K} online "
+                    f"steps, plus the H2D of the offline results ({h2d / 1e9:.2f} GB once) and a "
+                    f"D2H of every decoded state into pinned host memory "
+                    f"({E2E_RING}-slot ring); wall clock"}
 
 
 def cpu_baseline_rom(case, steps=3, n_sample=None, timed_steps=None):

@@ -307,6 +307,12 @@ int adrom_session_read(adrom_session* s, double* host_step_log, int64_t max_step
                        double* dev_q_tilde);
 /* current sampled rows (device int64[n_s]) */
 int adrom_session_sampling(adrom_session* s, int64_t* dev_idx);
+/* host_out of adrom_session_advance as a ring of `slots` states (state k of
+ * a call goes to slot k % slots; copies into a slot stay ordered); 0 = the
+ * default linear layout.  For streaming consumers of the decoded trajectory
+ * that do not keep all of it (driver.py:306 keeps it; this bounds the pinned
+ * memory a long run needs). */
+int adrom_session_set_host_ring(adrom_session* s, int64_t slots);
 
 #ifdef __cplusplus
 }

@@ -115,6 +115,7 @@ SIGNATURES = {
     "adrom_session_read": (_i32, [_p, _p, _i64, _p, _i64, C.POINTER(_i64), C.POINTER(_i64),
                                   _p, _p, _p, _p]),
     "adrom_session_sampling": (_i32, [_p, _p]),
+    "adrom_session_set_host_ring": (_i32, [_p, _i64]),
 }
 
 PROBES = ["isvd_rotate", "isvd_project", "isvd_resid", "isvd_core", "fom_residual",

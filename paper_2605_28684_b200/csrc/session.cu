@@ -140,6 +140,8 @@ struct adrom_session {
   // stream (ADROM_SESSION_PRIORITY=0 keeps everything on the caller's stream)
   cudaStream_t hstream = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  // host_out of advance() as a ring of this many states (0 = linear)
+  int64_t host_slots = 0;
   // factored path: the next event's coarse Newton solve runs on a host thread
   // (its host-side convergence checks would otherwise block the issue of this
   // event's work), started as soon as its input y_corr exists
@@ -902,7 +904,8 @@ int adrom_session_advance(adrom_session* s, int64_t n_steps, int64_t save_every,
         ADROM_CK(ctx, cudaMemcpyAsync(dev_out + saved * N, s->q_tilde, 8 * N,
                                       cudaMemcpyDeviceToDevice, ctx->stream));
       if (host_out) {
-        st = download_state(s, host_out + saved * N);
+        const int64_t slot = s->host_slots > 0 ? saved % s->host_slots : saved;
+        st = download_state(s, host_out + slot * N);
         if (st) return st;
       }
       ++saved;
@@ -977,6 +980,12 @@ int adrom_session_read(adrom_session* s, double* host_step_log, int64_t max_step
     for (int64_t i = 0; i < ne; ++i) host_events[i] = s->events[i];
   if (n_steps) *n_steps = s->n_online;
   if (n_events) *n_events = (int64_t)s->events.size();
+  return ADROM_OK;
+}
+
+int adrom_session_set_host_ring(adrom_session* s, int64_t slots) {
+  if (!s || slots < 0) return ADROM_ERR_ARG;
+  s->host_slots = slots;
   return ADROM_OK;
 }
 

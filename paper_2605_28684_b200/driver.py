@@ -266,6 +266,10 @@ class Session:
                        C.c_int64(save_every), ptr(dev_out), ptr(host_out), C.byref(n_saved))
         return int(n_saved.value)
 
+    def set_host_ring(self, slots: int):
+        """host_out of advance() as a ring of `slots` decoded states (0 = linear)."""
+        self.ctx.scall("adrom_session_set_host_ring", self.handle, C.c_int64(slots))
+
     def finish(self):
         self.ctx.scall("adrom_session_finish", self.handle)
 
