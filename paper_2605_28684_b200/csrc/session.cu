@@ -678,8 +678,15 @@ int adrom_session_create(adrom_ctx* ctx, const adrom_session_config* cfg, adrom_
   s->q_tilde = s->alloc_d(N);
   s->a = s->alloc_d(r);
   {
-    const char* ev = getenv("ADROM_BIG_SAMPLES");  // tests: force the grid-wide path
-    s->big = cfg->n_s > 4096 || (ev && atoi(ev) != 0);
+    // grid-wide reduced operator (bigsample.cu) from 256 sampled rows: the
+    // one-block kernels win below that (cfg 0: 16 rows, cfg 3: 64 rows) and
+    // lose above (cfg 1, 615 rows: 635 -> 1429 steps/s); they cannot hold
+    // more than 4096 rows.  ADROM_BIG_SAMPLES=0/1 overrides (tests)
+    const char* ev = getenv("ADROM_BIG_SAMPLES");
+    s->big = ev ? (atoi(ev) != 0 || cfg->n_s > 4096) : (cfg->n_s >= 256);
+    // the grid-wide path implements LSPG only (Galerkin keeps the one-block
+    // kernels up to their 4096-row limit)
+    if (cfg->projection != 0 && cfg->n_s <= 4096) s->big = false;
   }
   int st = alloc_op(s, s->op[0], s->bigop[0]);
   if (!st) st = alloc_op(s, s->op[1], s->bigop[1]);

@@ -91,3 +91,26 @@ def test_golden_loops_grid_path(golden, grid_path, name):
     diff = np.abs(it_ref - np.asarray(res.step_iterations))
     loose = env > 1e-9
     assert np.all(diff[~loose] == 0) and np.all(diff <= 1), np.flatnonzero(diff)
+
+
+def test_cfg1_grid_path_matches_one_block_path(monkeypatch):
+    """Configuration 1 (Sod 4096 cells, FGS 615 rows) takes the grid-wide
+    reduced operator by default (n_s >= 256); it must reproduce the one-block
+    path's trajectory (same offline stage, same events)."""
+    P = _pkg()
+    from paper_2605_28684_b200 import configs
+    case = configs.cfg1()
+    cfg = P.ExperimentConfig(model="sod", n_elem=case.n_elem, dt=case.dt,
+                             n_t=case.w_init + 25, w_init=case.w_init, r=case.r, n_s=case.n_s,
+                             z=case.z, sampling="fgs", n_extra=case.n_extra,
+                             rule=P.UpdateRule("isvd", lam=case.lam))
+    runs = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("ADROM_BIG_SAMPLES", flag)
+        runs[flag] = P.run_adaptive_rom(cfg)
+    a, b = runs["0"].trajectory, runs["1"].trajectory
+    dev = np.linalg.norm(a - b, axis=1) / np.linalg.norm(a, axis=1)
+    assert dev.max() < 1e-9, dev.max()
+    assert [e["coarse_iterations"] for e in runs["0"].event_log] == \
+        [e["coarse_iterations"] for e in runs["1"].event_log]
+    assert list(runs["0"].step_iterations) == list(runs["1"].step_iterations)
