@@ -660,7 +660,7 @@ __global__ void splitk_reduce_kernel(const double* __restrict__ part, int nb, in
   }
 }
 
-constexpr int SPLITK_MAX = 148;
+constexpr int SPLITK_MAX = 296;
 
 // [jac | rho] (r x n, column-major) = pinv (r x K, row-major) [test | res]^T-ish:
 // C = P'^T T'^T with P' = pinv viewed column-major K x r and T' = test viewed
@@ -668,7 +668,10 @@ constexpr int SPLITK_MAX = 148;
 // partial per chunk) so the 128 x 129 output keeps every SM busy.
 static int gemm_jac(adrom_ctx* ctx, int r, int n, int64_t K, const double* pinv,
                     const double* test, double* C, double* part) {
+  // 74 chunks measured best for the cfg-4 shape (148 / 296 within 1-2 %)
+  static const int cap = getenv("ADROM_SPLITK") ? atoi(getenv("ADROM_SPLITK")) : 74;
   int nb = (int)(K / 1024);
+  if (nb > cap) nb = cap;
   if (nb > SPLITK_MAX) nb = SPLITK_MAX;
   if (nb < 2) return dgemm(ctx, true, true, r, n, K, pinv, K, test, n, C, r);
   cublasHandle_t h = blas(ctx);

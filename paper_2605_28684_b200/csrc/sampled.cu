@@ -10,6 +10,8 @@
 #include "jacobi.cuh"
 #include "rom_internal.cuh"
 
+#include <stdlib.h>
+
 namespace adrom {
 
 struct PlanView {
@@ -524,7 +526,8 @@ __global__ void __launch_bounds__(512) galerkin_kernel(RomStepArgs A) {
 // it, done, gnorm, status, cond]; Vg: r x (r|1) global scratch (jA and V
 // do not both fit in shared memory at r = 128).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(512) lspg_update_kernel(const double* __restrict__ C, int r,
+template <int NT>
+__global__ void __launch_bounds__(NT) lspg_update_kernel(const double* __restrict__ C, int r,
                                                           double* __restrict__ st, double tol,
                                                           int max_iter, double* __restrict__ V) {
   extern __shared__ double sm[];
@@ -630,9 +633,19 @@ int lspg_update_launch(adrom_ctx* ctx, const double* C, int r, double* st, doubl
                        int max_iter) {
   const int ld = r | 1;
   const size_t sm = sizeof(double) * ((size_t)r * ld + 6 * (size_t)r + 32) + sizeof(int) * r + 64;
-  cudaFuncSetAttribute(lspg_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   double* V = st + 2 * r + 8;  // r x ld scratch after the state scalars
-  lspg_update_kernel<<<1, 512, sm, ctx->stream>>>(C, r, st, tol, max_iter, V);
+  // 1024 threads: the Householder trailing updates spread over 32 warps
+  static const int nt = getenv("ADROM_UPD_THREADS") ? atoi(getenv("ADROM_UPD_THREADS")) : 1024;
+  if (nt == 1024) {
+    cudaFuncSetAttribute(lspg_update_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    lspg_update_kernel<1024><<<1, 1024, sm, ctx->stream>>>(C, r, st, tol, max_iter, V);
+  } else if (nt == 256) {
+    cudaFuncSetAttribute(lspg_update_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    lspg_update_kernel<256><<<1, 256, sm, ctx->stream>>>(C, r, st, tol, max_iter, V);
+  } else {
+    cudaFuncSetAttribute(lspg_update_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    lspg_update_kernel<512><<<1, 512, sm, ctx->stream>>>(C, r, st, tol, max_iter, V);
+  }
   ADROM_LAUNCH_CK(ctx);
   return ADROM_OK;
 }
