@@ -1158,6 +1158,7 @@ __global__ void __launch_bounds__(1024) isvd_core_kernel(
     stats[4] = reorth ? 1.0 : 0.0;
     stats[5] = jr.sweeps;
     stats[6] = jr.converged;
+    stats[7] = sh_fallback;
     if (!jr.converged) atomicOr(flag, 8);
   }
 }

@@ -527,6 +527,8 @@ int run_event_factored(adrom_session* s, adrom_event_record& ev, bool* decoded) 
     return ADROM_OK;
   }
   ev.residual_norm = hs[2];
+  if (getenv("ADROM_DEBUG_CORE"))
+    fprintf(stderr, "core: sweeps %g converged %g fallback %g\n", hs[5], hs[6], hs[7]);
   const FactBasis b2{s->phi[s->acur], s->Qb, s->r, b.k + 1, s->Wd[nxt], s->N, s->A32[s->acur]};
   const int onx = 1 - s->opcur;
   st = build_sampling_operator(s, nullptr, s->op[onx], s->y_corr, true, &b2, s->nrm2[nxt]);
