@@ -39,6 +39,6 @@ try:  # noqa: SIM105 — optional until those modules exist in this build
         galerkin_step, lspg_objective, lspg_step, rom_step)
     from .driver import (  # noqa: F401
         ExperimentConfig, RunResult, acceleration, make_problem, relative_error,
-        run_adaptive_rom, run_static_rom)
+        run_adaptive_rom, run_fom, run_static_rom)
 except ImportError:  # pragma: no cover
     pass

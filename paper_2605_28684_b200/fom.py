@@ -216,7 +216,8 @@ class ReactingEulerProblem(FomProblem):
 
     n_var = 3 + N_SPECIES
     boundary = "periodic"
-    var_names = ("rho", "m", "E") + tuple(f"rhoY{k}" for k in range(N_SPECIES))
+    # primitive fields (the keys of primitive_fields, as SodProblem's)
+    var_names = ("rho", "v", "p") + tuple(f"Y{k}" for k in range(N_SPECIES))
     kind = REACTING
 
     def __init__(self, n_elem: int, gamma: float = 1.4, length: float = 1.0, seed: int = 4,
@@ -232,19 +233,23 @@ class ReactingEulerProblem(FomProblem):
 
     def primitive_fields(self, q):
         """rho, v, p as the Sod model (fom.py:279-282) from the first three
-        conserved variables; the FGS feature maps read these."""
+        conserved variables (the FGS feature maps read these) and the mass
+        fractions Y_k = (rho Y_k) / rho (diagnostics, driver.py:168-199)."""
         if _dev.is_device(q):
             t = _dev.torch()
             u = q.reshape(self.n_elem, self.n_var)
             rho = t.clamp_min(u[:, 0], PRIM_FLOOR)
             vel = u[:, 1] / rho
             p = t.clamp_min((self.gamma - 1.0) * (u[:, 2] - (0.5 * rho) * (vel * vel)), PRIM_FLOOR)
-            return {"rho": rho, "v": vel, "p": p}
-        u = np.asarray(q, dtype=float).reshape(self.n_elem, self.n_var)
-        rho = np.maximum(u[:, 0], PRIM_FLOOR)
-        vel = u[:, 1] / rho
-        p = np.maximum((self.gamma - 1.0) * (u[:, 2] - (0.5 * rho) * (vel * vel)), PRIM_FLOOR)
-        return {"rho": rho, "v": vel, "p": p}
+        else:
+            u = np.asarray(q, dtype=float).reshape(self.n_elem, self.n_var)
+            rho = np.maximum(u[:, 0], PRIM_FLOOR)
+            vel = u[:, 1] / rho
+            p = np.maximum((self.gamma - 1.0) * (u[:, 2] - (0.5 * rho) * (vel * vel)), PRIM_FLOOR)
+        out = {"rho": rho, "v": vel, "p": p}
+        for k in range(N_SPECIES):
+            out[f"Y{k}"] = u[:, 3 + k] / rho
+        return out
 
     def abi(self) -> Model:
         if self._mech_dev is None:  # uploaded on first device use

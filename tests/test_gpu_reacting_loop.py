@@ -151,3 +151,24 @@ def test_cfg4_recipe_scaled_vs_oracle(monkeypatch, grid_path):
         assert "update_error" not in e
         assert e_ref["coarse_iterations"] == e["coarse_iterations"]
     assert res.newton_failures == rec.failures
+
+
+def test_reacting_error_history_with_full_truth():
+    """driver.py:168-199 on the reacting model: with a truth trajectory over
+    the whole horizon the run records per-variable errors (rho, v, p, Y_k)
+    at the error steps, and run_fom's device trajectory is that truth."""
+    P = _pkg()
+    n = 64
+    cfg = P.ExperimentConfig(model="reacting", n_elem=n, dt=2e-3, n_t=30, w_init=10, r=6, n_s=6 + 13,
+                             n_extra=13, z=5, sampling="fgs", rule=P.UpdateRule("isvd", lam=0.25))
+    fom = P.run_fom(cfg)
+    m = _model(n)
+    ocfg = online.LoopConfig(model=m, dt=cfg.dt, n_t=cfg.n_t, w_init=cfg.w_init, r=cfg.r,
+                             n_s=cfg.n_s, n_extra=cfg.n_extra, z=cfg.z, lam=0.25, sampling="fgs")
+    truth = online.training_states(ocfg.__class__(**{**ocfg.__dict__, "w_init": cfg.n_t}),
+                                   R.initial_state(n))
+    dev = np.linalg.norm(np.asarray(fom.trajectory) - truth) / np.linalg.norm(truth)
+    assert dev < 1e-12, dev
+    res = P.run_adaptive_rom(cfg, truth=truth)
+    assert res.errors is not None and res.errors.shape[1] == len(res.var_names) == 13
+    assert np.all(np.isfinite(res.errors))
