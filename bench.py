@@ -490,7 +490,7 @@ def bench_rom(args, rank, world):
         # q~ = q_ref + (Phi a) / d (stream_kernel<128>: Phi read, q_ref and d
         # read, q~ written: 8 N (r + 3) bytes)
         dbytes = 8.0 * N * (r + 3)
-        roof = roofline(dbytes, per["decode"][0])
+        roof = roofline(dbytes, per["decode"][0], ncu_traffic("stream_kernel<128, 1, 1, 0>", case.name))
         roof.update({"kernel": "decode (stream_kernel<128>: q_ref + Phi a / d)",
                      "work_per_launch": {"bytes": dbytes},
                      "share_of_step": round(probes["decode"][0] / ms, 4),
