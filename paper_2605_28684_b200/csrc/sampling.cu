@@ -301,7 +301,7 @@ __global__ void op_gather_kernel(DevOp op, const double* __restrict__ phi,
 // ---------------------------------------------------------------------------
 constexpr double PINV_CERT = 1e10;
 
-__global__ void __launch_bounds__(512) deim_pinv_qr_kernel(DevOp op, int n_s,
+__global__ void __launch_bounds__(1024) deim_pinv_qr_kernel(DevOp op, int n_s,
                                                            int* __restrict__ need_svd) {
   extern __shared__ double sm[];
   const int r = op.r, m = n_s;
@@ -467,7 +467,7 @@ static int deim_pinv_launch(adrom_ctx* ctx, DevOp& op, int n_s, int* flag) {
   const bool qr_ok = n_s >= r && r <= 128 && qsm <= 220 * 1024;
   if (qr_ok) {
     cudaFuncSetAttribute(deim_pinv_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsm);
-    deim_pinv_qr_kernel<<<1, 512, qsm, ctx->stream>>>(op, n_s, need);
+    deim_pinv_qr_kernel<<<1, 1024, qsm, ctx->stream>>>(op, n_s, need);
     ADROM_LAUNCH_CK(ctx);
   }
   cudaFuncSetAttribute(deim_pinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
