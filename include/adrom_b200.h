@@ -156,8 +156,9 @@ typedef struct adrom_isvd_info {
   double proj_resid;     /* ||y - Phi Phi^T y|| (driver.py:366-367 diag)     */
   int32_t degenerate;    /* took the in-span branch (tracking.py:169-170)    */
   int32_t reorthogonalised; /* explicit residual pass was run                */
-  int32_t sweeps;        /* Jacobi sweeps of the core SVD                    */
-  int32_t pad;
+  int32_t sweeps;        /* Jacobi sweeps of the core SVD (0: secular path)  */
+  int32_t core_path;     /* core SVD: 0 secular equation, 1 Jacobi on K,
+                            2 Jacobi on K^T (fallbacks)                      */
 } adrom_isvd_info;
 
 /* isvd_update (tracking.py:141-178):

@@ -55,6 +55,7 @@ class LoopRecord:
     events: list = field(default_factory=list)       # dicts like driver.py:351-387
     samplings: list = field(default_factory=list)    # sampled indices per rebuild
     failures: list = field(default_factory=list)     # rom non-convergence steps
+    iterations: list = field(default_factory=list)   # Gauss-Newton iterations per step
     signal: list = field(default_factory=list)       # (step, y_corr) coarse snapshots
     phi_final: np.ndarray | None = None
     a_init: np.ndarray | None = None
@@ -90,10 +91,26 @@ def _sampling(cfg: LoopConfig, phi, y_corr):
     return hyper.closure(s, cfg.model)
 
 
+def _nudge(rng, x):
+    """One-ulp perturbation of random entries (the sensitivity envelope)."""
+    if rng is None:
+        return x
+    x = np.asarray(x, dtype=float)
+    return np.where(rng.random(x.shape) < 0.5, np.nextafter(x, np.inf), x)
+
+
 def run_online(cfg: LoopConfig, training, q_ref, d, phi0, sigma0, keep_stride=1,
-               n_steps=None) -> LoopRecord:
+               n_steps=None, nudge_seed=None) -> LoopRecord:
     """driver.py:304-390 (one timing pass).  ``n_steps`` truncates the
-    horizon to a prefix (for full-size prefix parity)."""
+    horizon to a prefix (for full-size prefix parity).
+
+    ``nudge_seed`` perturbs every coarse Newton result, iSVD output, reduced
+    step result and state transfer by one ulp at random entries — the places
+    where any other implementation's arithmetic necessarily differs from
+    numpy/LAPACK's — to measure the loop's own rounding sensitivity (the
+    envelope the parity gates are expressed in; like
+    ``tests/golden/make_golden._envelope`` on the reference itself)."""
+    rng = None if nudge_seed is None else np.random.default_rng(nudge_seed)
     model = cfg.model
     rec = LoopRecord()
     phi, sigma = np.array(phi0, dtype=float), np.array(sigma0, dtype=float)
@@ -116,7 +133,8 @@ def run_online(cfg: LoopConfig, training, q_ref, d, phi0, sigma0, keep_stride=1,
         out = step_fn(op, model, a, cfg.dt, cfg.newton_tol, cfg.newton_max_iter)
         if not out.converged:
             rec.failures.append(n + 1)
-        a = out.a
+        rec.iterations.append(int(out.iterations))
+        a = _nudge(rng, out.a)
         q_tilde = reduced.decode(op, a)
         rec.reduced.append(a.copy())
         if (n + 1 - cfg.w_init) % keep_stride == 0 or n + 1 == last:
@@ -128,19 +146,20 @@ def run_online(cfg: LoopConfig, training, q_ref, d, phi0, sigma0, keep_stride=1,
         try:                                             # driver.py:353-385
             res = physics.coarse_step(model, y_corr, cfg.z, cfg.dt, cfg.newton_tol,
                                       cfg.newton_max_iter)
-            y_corr = res.x
+            y_corr = _nudge(rng, res.x)
             rec.signal.append((n + 1 + cfg.z, y_corr.copy()))
             event["coarse_converged"] = res.converged
             event["coarse_iterations"] = res.iterations
             y_hat = d * (y_corr - q_ref)
             phi_new, sigma_new, _ = subspace.isvd_update(phi, sigma, y_hat, cfg.lam, cfg.r,
                                                          projection=cfg.isvd_projection)
+            phi_new, sigma_new = _nudge(rng, phi_new), _nudge(rng, sigma_new)
             event["residual_norm"] = float(np.linalg.norm(y_hat - phi @ (phi.T @ y_hat)))
             samp_new = _sampling(cfg, phi_new, y_corr)
             op = reduced.build_operator(model, phi_new, q_ref, d, samp_new)
             phi, sigma = phi_new, sigma_new
             rec.samplings.append(samp_new.indices.copy())
-            a = reduced.encode(op, q_tilde)
+            a = _nudge(rng, reduced.encode(op, q_tilde))
             event["a_transfer"] = a.copy()
         except Exception as exc:  # noqa: BLE001 — driver.py:384-385
             event["update_error"] = f"{type(exc).__name__}: {exc}"

@@ -20,6 +20,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 import numpy as np
+import scipy.linalg
 import scipy.sparse
 import scipy.sparse.linalg
 
@@ -268,6 +269,36 @@ def newton_matrix(model: Model, blocks: np.ndarray, dt: float) -> scipy.sparse.c
     return scipy.sparse.csc_matrix((vals, (rows, cols)), shape=(n * nv, n * nv))
 
 
+def _cyclic_tridiag_solve(model: Model, blocks: np.ndarray, dt: float, rhs_vec: np.ndarray):
+    """Solve ``(I - dt J) x = rhs`` for a scalar periodic model (cyclic
+    tridiagonal) by Sherman-Morrison around LAPACK's banded solver (gbsv).
+
+    Used beyond 2^20 cells, where SuperLU's workspace overflows (it fails at
+    2^24, configuration 3).  Same matrix entries as ``newton_matrix``; the
+    solve rounds differently at the 1e-16 level, like the sparse LU does
+    against the reference's dense LU."""
+    n = model.n_elem
+    sub = -dt * blocks[:, 0, 0, 0]       # A[i, i-1] (row i)
+    diag = 1.0 - dt * blocks[:, 1, 0, 0]
+    sup = -dt * blocks[:, 2, 0, 0]       # A[i, i+1]
+    alpha = sup[n - 1]                   # A[n-1, 0]
+    beta = sub[0]                        # A[0, n-1]
+    gamma = -diag[0]
+    ab = np.zeros((3, n))
+    ab[0, 1:] = sup[:-1]
+    ab[1] = diag
+    ab[1, 0] = diag[0] - gamma
+    ab[1, n - 1] = diag[n - 1] - alpha * beta / gamma
+    ab[2, :-1] = sub[1:]
+    u = np.zeros(n)
+    u[0], u[n - 1] = gamma, alpha
+    ys = scipy.linalg.solve_banded((1, 1), ab, np.column_stack([rhs_vec, u]),
+                                   overwrite_ab=True, check_finite=False)
+    y, zz = ys[:, 0], ys[:, 1]
+    fac = (y[0] + beta / gamma * y[n - 1]) / (1.0 + zz[0] + beta / gamma * zz[n - 1])
+    return y - fac * zz
+
+
 @dataclass
 class NewtonOutcome:
     """Mirror of ``dense.NewtonResult`` (dense.py:129-137)."""
@@ -312,6 +343,11 @@ def implicit_step(model: Model, q: np.ndarray, dt: float, tol: float = 1e-8,
         blocks = fd_jacobian_blocks(model, x)
         if not np.all(np.isfinite(blocks)):
             raise OracleDenseError("newton jacobian contains non-finite entries")
+        if model.n_var == 1 and model.periodic and model.n_elem > (1 << 20):
+            x = x + _cyclic_tridiag_solve(model, blocks, dt, -r)
+            r = residual(x)
+            rn = float(np.linalg.norm(r))
+            continue
         mat = newton_matrix(model, blocks, dt)
         try:
             lu = scipy.sparse.linalg.splu(mat, permc_spec="NATURAL",

@@ -27,18 +27,13 @@ from .tracking import ReducedBasis, UpdateRule, isvd_update
 
 __version__ = "0.1.0"
 
-# The remaining reference names (sampling, projection, driver) are exported
-# by their modules once imported; see __all__ extension below.
-try:  # noqa: SIM105 — optional until those modules exist in this build
-    from .sampling import (  # noqa: F401
-        FeatureMap, SamplingPlan, SamplingSet, build_deim_operator, fgs_sample, qdeim_sample,
-        stencil_closure)
-    from .snapshots import ScalingTransform, fit_scaling, pod  # noqa: F401
-    from .projection import (  # noqa: F401
-        ReducedState, RomOperator, RomStepResult, build_rom_operator, decode, encode,
-        galerkin_step, lspg_objective, lspg_step, rom_step)
-    from .driver import (  # noqa: F401
-        ExperimentConfig, RunResult, acceleration, make_problem, relative_error,
-        run_adaptive_rom, run_fom, run_static_rom)
-except ImportError:  # pragma: no cover
-    pass
+from .sampling import (  # noqa: F401
+    FeatureMap, SamplingPlan, SamplingSet, build_deim_operator, fgs_sample, qdeim_sample,
+    stencil_closure)
+from .snapshots import ScalingTransform, fit_scaling, pod  # noqa: F401
+from .projection import (  # noqa: F401
+    ReducedState, RomOperator, RomStepResult, build_rom_operator, decode, encode,
+    galerkin_step, lspg_objective, lspg_step, rom_step)
+from .driver import (  # noqa: F401
+    ExperimentConfig, RunResult, acceleration, make_problem, relative_error,
+    run_adaptive_rom, run_fom, run_static_rom)

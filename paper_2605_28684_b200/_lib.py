@@ -38,7 +38,8 @@ class NewtonInfo(C.Structure):
 
 class IsvdInfo(C.Structure):
     _fields_ = [("qnorm", _f64), ("ynorm", _f64), ("proj_resid", _f64),
-                ("degenerate", _i32), ("reorthogonalised", _i32), ("sweeps", _i32), ("pad", _i32)]
+                ("degenerate", _i32), ("reorthogonalised", _i32), ("sweeps", _i32),
+                ("core_path", _i32)]
 
 
 class RomOp(C.Structure):

@@ -138,7 +138,7 @@ int adrom_isvd_update(adrom_ctx* ctx, const double* phi, const double* sigma,
     host_info->degenerate = (int)hs[3];
     host_info->reorthogonalised = (int)hs[4];
     host_info->sweeps = (int)hs[5];
-    host_info->pad = 0;
+    host_info->core_path = (int)hs[7];
   }
   return ADROM_OK;
 }

@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(256, 2) xpass_kernel(XPassArgs a) {
 #pragma unroll
         for (int t = 0; t < QPL; ++t) {
           const int j = sl + LPR * t;
-          xq[u][t] = (j < k) ? a.Q[i * kq + j] : 0.0;
+          xq[u][t] = (j < k) ? a.Q[qpanel(i, j, a.n)] : 0.0;
         }
       } else {
 #pragma unroll
@@ -171,9 +171,16 @@ __global__ void __launch_bounds__(256, 2) xpass_kernel(XPassArgs a) {
         if (drop && sl == 0) a.qt[i] = qr[u] + dd2[u] / dd[u];  // fused decode (projection.py:104)
         bad |= !isfinite(w0);
         if (sl == 0) {
-          a.Qw[i * kq + k] = w0;
           if (a.qv) a.qv[i] = w0;
           s0 += w0 * w0;
+        }
+        // column k joins its 4-column panel: the 4 lanes owning that panel
+        // write the whole 32-byte sector (live columns rewritten unchanged,
+        // later ones zeroed), so no partial-sector write reaches L2
+#pragma unroll
+        for (int t = 0; t < QPL; ++t) {
+          const int j = sl + LPR * t;
+          if ((j >> 2) == (k >> 2)) a.Qw[qpanel(i, j, a.n)] = (j < k) ? xq[u][t] : (j == k ? w0 : 0.0);
         }
       }
 #pragma unroll
@@ -403,7 +410,7 @@ __global__ void __launch_bounds__(256, 1) reanchor_kernel(const double* __restri
     for (int c = tid; c < C::TM * (FACT_KQ / 2); c += 256) {
       const int rr = c / (FACT_KQ / 2), cc = 2 * (c % (FACT_KQ / 2));
       const bool ok = row0 + rr < n && cc < k;
-      re_cp16(Xs + rr * C::S + R + cc, Q + (ok ? (row0 + rr) * FACT_KQ + cc : 0), ok ? 16 : 0);
+      re_cp16(Xs + rr * C::S + R + cc, Q + (ok ? qpanel(row0 + rr, cc, n) : 0), ok ? 16 : 0);
     }
     asm volatile("cp.async.commit_group;\n");
   };
@@ -491,7 +498,7 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(FactBasis b, const int
   for (int64_t p = (int64_t)blockIdx.x * 8 + warp; p < count; p += (int64_t)gridDim.x * 8) {
     const int64_t i = rows[p];
     for (int j = lane; j < rk; j += 32)
-      x[j] = (i < 0) ? 0.0 : (j < r ? b.A[i * r + j] : b.Q[i * FACT_KQ + (j - r)]);
+      x[j] = (i < 0) ? 0.0 : (j < r ? b.A[i * r + j] : b.Q[qpanel(i, j - r, b.n)]);
     __syncwarp();
     for (int c = lane; c < r; c += 32) {
       double s = 0.0;
@@ -530,7 +537,7 @@ __global__ void __launch_bounds__(256) gather_rows_tc_kernel(FactBasis b, const 
       double x = 0.0;
       if (i >= 0) {
         if (c < R) x = b.A[i * R + c];
-        else if (c - R < k) x = b.Q[i * FACT_KQ + (c - R)];
+        else if (c - R < k) x = b.Q[qpanel(i, c - R, b.n)];
       }
       af[j] = x;
     }
@@ -888,7 +895,7 @@ int adrom_isvd_stream_update(adrom_isvd_stream* s, const double* y_hat, double l
     host_info->degenerate = (int)hs[3];
     host_info->reorthogonalised = (int)hs[4];
     host_info->sweeps = (int)hs[5];
-    host_info->pad = 0;
+    host_info->core_path = (int)hs[7];
   }
   s->kf = b.k + 1;
   s->w_id = false;

@@ -7,10 +7,19 @@ namespace adrom {
 
 constexpr int FACT_KQ = 16;  // residual columns kept before re-anchoring
 
+// Q (the residual columns) is stored as FACT_KQ / 4 panels of 4 columns:
+// panel P holds columns 4P..4P+3 as n rows of 32 bytes (one DRAM sector).
+// A pass over the basis with k live columns reads ceil(k / 4) sectors per
+// row instead of the whole 128-byte row of a row-major n x 16 store, and a
+// gathered row still costs ceil(k / 4) sectors.
+__host__ __device__ __forceinline__ int64_t qpanel(int64_t i, int j, int64_t n) {
+  return ((int64_t)(j >> 2) * n + i) * 4 + (j & 3);
+}
+
 // Phi = [A | Q_0 .. Q_{k-1}] W;  W == nullptr means W = I (then k == 0)
 struct FactBasis {
   const double* A;  // n x r row-major anchor
-  const double* Q;  // n x FACT_KQ row-major residual columns
+  const double* Q;  // n x FACT_KQ residual columns, 4-column panels (qpanel)
   int r, k;
   const double* W;  // (r + k) x r row-major, or null
   int64_t n;

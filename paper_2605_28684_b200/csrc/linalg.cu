@@ -3,6 +3,7 @@
 // whose order differs from BLAS anyway; FMA only improves them.
 #include "common.cuh"
 #include "jacobi.cuh"
+#include "secular.cuh"
 #include "linalg_internal.cuh"
 
 #include <math.h>
@@ -1077,15 +1078,60 @@ __global__ void __launch_bounds__(1024) isvd_core_kernel(
     if (tid == 0) *qinv_out = 0.0;
     return;
   }
-  fill_k(false);
-  JacobiResult jr = block_jacobi<16>(A, ld, n, n, nullptr, ld, 30, 1e-15, &sh_flag);
-  column_norms_sorted(A, ld, n, n, s, order);
-  // U column j = A column j / s_j, stored as V[j][k] = U[k][j]
-  for (int e = tid; e < n * n; e += blockDim.x) {
-    const int j = e / n, k = e - j * n;
-    V[j * ld + k] = (s[j] > 0.0) ? A[j * ld + k] / s[j] : 0.0;
+  // Fast path: the secular equation of K K^T = diag(d^2) + z z^T (secular.cuh),
+  // verified by the residual of every kept column and its orthonormality
+  __shared__ SecularShared sec;
+  __shared__ int sh_path;  // 0 secular, 1 Jacobi on K, 2 Jacobi on K^T
+  JacobiResult jr{0, 1};
+  {
+    const double rho = degenerate ? 0.0 : qnorm;
+    const bool conv = secular_core_svd(sigma, lam, p, rho, n, V, ld, s, A, ld, sec);
+    for (int j = tid; j < n; j += blockDim.x) {
+      int rank = 0;
+      const double sj = isnan(s[j]) ? -1.0 : s[j];
+      for (int k = 0; k < n; ++k) {
+        const double sk = isnan(s[k]) ? -1.0 : s[k];
+        if (sk > sj || (sk == sj && k < j)) ++rank;
+      }
+      order[rank] = j;
+    }
+    __syncthreads();
+    // || K K^T u - s^2 u ||_inf on the kept columns (K K^T = diag(d^2) + z z^T)
+    double zz = 0.0, dm = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const double zi = (i < r_cur) ? p[i] : rho;
+      zz += zi * zi;
+      if (i < r_cur) dm = fmax(dm, fabs(lam * sigma[i]));
+    }
+    double worst = 0.0;
+    for (int a = tid >> 5; a < r; a += blockDim.x >> 5) {
+      const double* u = V + (size_t)order[a] * ld;
+      double zu = 0.0;
+      for (int i = (tid & 31); i < n; i += 32) zu += ((i < r_cur) ? p[i] : rho) * u[i];
+      zu = warp_sum(zu);
+      const double s2 = s[order[a]] * s[order[a]];
+      for (int i = (tid & 31); i < n; i += 32) {
+        const double di = (i < r_cur) ? lam * sigma[i] : 0.0;
+        const double zi = (i < r_cur) ? p[i] : rho;
+        worst = fmax(worst, fabs(di * di * u[i] + zi * zu - s2 * u[i]));
+      }
+    }
+    worst = block_max_dyn(worst, red);
+    if (tid == 0)
+      sh_path = (conv && worst <= 256.0 * n * 2.220446049250313e-16 * (dm * dm + zz)) ? 0 : 1;
+    __syncthreads();
   }
-  __syncthreads();
+  if (sh_path) {
+    fill_k(false);
+    jr = block_jacobi<16>(A, ld, n, n, nullptr, ld, 30, 1e-15, &sh_flag);
+    column_norms_sorted(A, ld, n, n, s, order);
+    // U column j = A column j / s_j, stored as V[j][k] = U[k][j]
+    for (int e = tid; e < n * n; e += blockDim.x) {
+      const int j = e / n, k = e - j * n;
+      V[j * ld + k] = (s[j] > 0.0) ? A[j * ld + k] / s[j] : 0.0;
+    }
+    __syncthreads();
+  }
   double defect = 0.0;
   for (int e = tid; e < r * r; e += blockDim.x) {
     const int a = e / r, b = e - a * r;
@@ -1097,7 +1143,13 @@ __global__ void __launch_bounds__(1024) isvd_core_kernel(
   }
   defect = block_max_dyn(defect, red);
   __shared__ int sh_fallback;
-  if (tid == 0) sh_fallback = (!jr.converged || !(defect <= 1e-13) || !(s[order[r - 1]] > 0.0)) ? 1 : 0;
+  if (tid == 0) {
+    sh_fallback = (!jr.converged || !(defect <= 1e-13) || !(s[order[r - 1]] > 0.0)) ? 1 : 0;
+    // a rank-deficient K (a zero kept singular value) is legitimate on the
+    // secular path: its vectors are exact eigenvectors, not column norms
+    if (sh_path == 0 && jr.converged && defect <= 1e-13) sh_fallback = 0;
+    if (sh_fallback) sh_path = 2;
+  }
   __syncthreads();
   if (sh_fallback) {
     // one-sided Jacobi on K^T with accumulated rotations: U of K = V
@@ -1158,7 +1210,7 @@ __global__ void __launch_bounds__(1024) isvd_core_kernel(
     stats[4] = reorth ? 1.0 : 0.0;
     stats[5] = jr.sweeps;
     stats[6] = jr.converged;
-    stats[7] = sh_fallback;
+    stats[7] = sh_path;
     if (!jr.converged) atomicOr(flag, 8);
   }
 }

@@ -897,7 +897,7 @@ __device__ __forceinline__ void qp_dmma(double& d0, double& d1, double a, double
 // comes from nrmb (bounds of ||Phi_i||^2).  Otherwise rows are phi_i and Mm = D.
 template <int R, bool FACT>
 __global__ void __launch_bounds__(256) qp_refresh_tc_kernel(const double* __restrict__ phi,
-                                                            const double* __restrict__ Qx, int kf,
+                                                            const double* __restrict__ Qx, int kf, int64_t qn,
                                                             const double* __restrict__ nrmb,
                                                             const int64_t* __restrict__ list,
                                                             int64_t cap,
@@ -933,7 +933,7 @@ __global__ void __launch_bounds__(256) qp_refresh_tc_kernel(const double* __rest
       double x = 0.0;
       if (i >= 0) {
         if (c < R) x = row[c];
-        else if (c - R < kf) x = Qx[i * FACT_KQ + (c - R)];
+        else if (c - R < kf) x = Qx[qpanel(i, c - R, qn)];
       }
       af[j] = x;
       if (!FACT) nrm = fma(x, x, nrm);
@@ -970,7 +970,7 @@ __global__ void __launch_bounds__(256) qp_refresh_tc_kernel(const double* __rest
 }
 
 template <int R, bool FACT>
-static int qp_refresh_tc(adrom_ctx* ctx, const double* phi, const double* Qx, int kf,
+static int qp_refresh_tc(adrom_ctx* ctx, const double* phi, const double* Qx, int kf, int64_t qn,
                          const double* nrmb, const int64_t* list, int64_t cap, const double* Mm,
                          int k, double* res2, double* bnd2, unsigned char* ver) {
   constexpr int KX = FACT ? R + FACT_KQ : R;
@@ -981,7 +981,7 @@ static int qp_refresh_tc(adrom_ctx* ctx, const double* phi, const double* Qx, in
   cudaFuncSetAttribute(qp_refresh_tc_kernel<R, FACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sm);
   qp_refresh_tc_kernel<R, FACT><<<(int)(g < 1 ? 1 : g), 256, sm, ctx->stream>>>(
-      phi, Qx, kf, nrmb, list, cap, Mm, k, res2, bnd2, ver);
+      phi, Qx, kf, qn, nrmb, list, cap, Mm, k, res2, bnd2, ver);
   ADROM_LAUNCH_CK(ctx);
   return ADROM_OK;
 }
@@ -1070,7 +1070,7 @@ __device__ __forceinline__ void qp_cp16(void* smem, const void* gmem, int src_by
 // cores: the gather is latency bound otherwise.
 template <int R, bool FACT, typename T>
 __global__ void __launch_bounds__(QpBf<R, FACT, T>::WPB * 32, 1)
-    qp_refresh_bf_kernel(const T* __restrict__ phi, const double* __restrict__ Qx, int kf,
+    qp_refresh_bf_kernel(const T* __restrict__ phi, const double* __restrict__ Qx, int kf, int64_t qn,
                          const double* __restrict__ nrmb, const int64_t* __restrict__ list,
                          int64_t cap, const double* __restrict__ Mm, int k,
                          double* __restrict__ res2, double* __restrict__ bnd2,
@@ -1121,8 +1121,9 @@ __global__ void __launch_bounds__(QpBf<R, FACT, T>::WPB * 32, 1)
       for (int rr = 0; rr < 4; ++rr) {
         const int p = (lane >> 3) + 4 * rr;
         const int64_t i = __shfl_sync(0xffffffffu, li, p);
-        qp_cp16(dQ + p * C::RSQ + 2 * sq, Qx + (i >= 0 ? i : 0) * FACT_KQ + 2 * sq,
-                i >= 0 ? 16 : 0);
+        // only the live columns' sectors (zero fill beyond kf)
+        const bool live = i >= 0 && 2 * sq < kf;
+        qp_cp16(dQ + p * C::RSQ + 2 * sq, Qx + (live ? qpanel(i, 2 * sq, qn) : 0), live ? 16 : 0);
       }
     }
     asm volatile("cp.async.commit_group;\n");
@@ -1355,7 +1356,7 @@ static int qp_list_bounds(adrom_ctx* ctx, const int64_t* list, int64_t cap, cons
 }
 
 template <int R, bool FACT, typename T>
-static int qp_refresh_bf_launch(adrom_ctx* ctx, const T* phi, const double* Qx, int kf,
+static int qp_refresh_bf_launch(adrom_ctx* ctx, const T* phi, const double* Qx, int kf, int64_t qn,
                                 const double* nrmb, const int64_t* list, int64_t cap,
                                 const double* Mm, int k, double* res2, double* bnd2,
                                 unsigned char* ver, double* blist) {
@@ -1367,7 +1368,7 @@ static int qp_refresh_bf_launch(adrom_ctx* ctx, const T* phi, const double* Qx, 
   cudaFuncSetAttribute(qp_refresh_bf_kernel<R, FACT, T>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   qp_refresh_bf_kernel<R, FACT, T><<<(int)(g < 1 ? 1 : g), C::WPB * 32, sm, ctx->stream>>>(
-      phi, Qx, kf, nrmb, list, cap, Mm, k, res2, bnd2, ver, blist);
+      phi, Qx, kf, qn, nrmb, list, cap, Mm, k, res2, bnd2, ver, blist);
   ADROM_LAUNCH_CK(ctx);
   return ADROM_OK;
 }
@@ -1375,18 +1376,18 @@ static int qp_refresh_bf_launch(adrom_ctx* ctx, const T* phi, const double* Qx, 
 // refresh on the bf16 tensor cores; factored rows come from the fp32 shadows
 // when the session keeps them (phi32, Qx32), else from the fp64 basis
 template <int R, bool FACT>
-static int qp_refresh_bf(adrom_ctx* ctx, const double* phi, const double* Qx, int kf,
+static int qp_refresh_bf(adrom_ctx* ctx, const double* phi, const double* Qx, int kf, int64_t qn,
                          const double* nrmb, const int64_t* list, int64_t cap, const double* Mm,
                          int k, double* res2, double* bnd2, unsigned char* ver, double* blist,
                          const float* phi32 = nullptr) {
   if (qp_refresh_fp64()) {
-    const int st = qp_refresh_tc<R, FACT>(ctx, phi, Qx, kf, nrmb, list, cap, Mm, k, res2, bnd2, ver);
+    const int st = qp_refresh_tc<R, FACT>(ctx, phi, Qx, kf, qn, nrmb, list, cap, Mm, k, res2, bnd2, ver);
     return st ? st : qp_list_bounds(ctx, list, cap, bnd2, blist);
   }
   if (FACT && phi32)
-    return qp_refresh_bf_launch<R, FACT, float>(ctx, phi32, Qx, kf, nrmb, list, cap, Mm, k, res2,
+    return qp_refresh_bf_launch<R, FACT, float>(ctx, phi32, Qx, kf, qn, nrmb, list, cap, Mm, k, res2,
                                                 bnd2, ver, blist);
-  return qp_refresh_bf_launch<R, FACT, double>(ctx, phi, Qx, kf, nrmb, list, cap, Mm, k, res2, bnd2,
+  return qp_refresh_bf_launch<R, FACT, double>(ctx, phi, Qx, kf, qn, nrmb, list, cap, Mm, k, res2, bnd2,
                                                ver, blist);
 }
 
@@ -1611,16 +1612,16 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
           qp_wd_kernel<<<(r + FACT_KQ) * r / 256 + 1, 256, 0, ctx->stream>>>(fb->W, r + fb->k, r, D,
                                                                             k, Mw);
           ADROM_LAUNCH_CK(ctx);
-          st = (r == 32) ? qp_refresh_bf<32, true>(ctx, fb->A, fb->Q, fb->k, nrmb, rlist, cap, Mw,
+          st = (r == 32) ? qp_refresh_bf<32, true>(ctx, fb->A, fb->Q, fb->k, fb->n, nrmb, rlist, cap, Mw,
                                                    k, res2, bnd2, ver, blist, fb->A32)
-                         : qp_refresh_bf<64, true>(ctx, fb->A, fb->Q, fb->k, nrmb, rlist, cap, Mw,
+                         : qp_refresh_bf<64, true>(ctx, fb->A, fb->Q, fb->k, fb->n, nrmb, rlist, cap, Mw,
                                                    k, res2, bnd2, ver, blist, fb->A32);
         } else if (r == 32 || r == 64 || r == 128) {
           st = (r == 32)
-                   ? qp_refresh_bf<32, false>(ctx, phi, nullptr, 0, nullptr, rlist, cap, D, k, res2, bnd2, ver, blist)
+                   ? qp_refresh_bf<32, false>(ctx, phi, nullptr, 0, (int64_t)0, nullptr, rlist, cap, D, k, res2, bnd2, ver, blist)
                : (r == 64)
-                   ? qp_refresh_bf<64, false>(ctx, phi, nullptr, 0, nullptr, rlist, cap, D, k, res2, bnd2, ver, blist)
-                   : qp_refresh_bf<128, false>(ctx, phi, nullptr, 0, nullptr, rlist, cap, D, k, res2, bnd2, ver, blist);
+                   ? qp_refresh_bf<64, false>(ctx, phi, nullptr, 0, (int64_t)0, nullptr, rlist, cap, D, k, res2, bnd2, ver, blist)
+                   : qp_refresh_bf<128, false>(ctx, phi, nullptr, 0, (int64_t)0, nullptr, rlist, cap, D, k, res2, bnd2, ver, blist);
         } else {
           st = rows_pass(cap, k, QP_REFRESH, rlist, n_ex);
           if (!st) st = qp_list_bounds(ctx, rlist, cap, bnd2, blist);

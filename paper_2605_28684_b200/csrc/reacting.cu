@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(RX_NT) reacting_rhs_kernel(const double* __res
       }
 #pragma unroll
       for (int v = 0; v < RX_NV; ++v) {
-        const double div = zdiv(-(faces[RX_NV * (c + 1) + v] - faces[RX_NV * c + v]), dx);
+        const double div = div_h(-(faces[RX_NV * (c + 1) + v] - faces[RX_NV * c + v]), dx);
         res[v] = div + s[v];
       }
     }

@@ -87,7 +87,7 @@ __device__ __forceinline__ void rx_sources(const double* c, double gamma, const 
 // residual of a cell from its two face fluxes and its sources
 template <bool ZD = true>
 __device__ __forceinline__ double rx_combine(double fr, double fl, double s, double dx) {
-  return rx_div<ZD>(-(fr - fl), dx) + s;
+  return div_h(-(fr - fl), dx) + s;
 }
 
 // residual of one cell from its stencil (l, c, r): -(F(c,r) - F(l,c))/dx + S(c),
@@ -167,14 +167,14 @@ __device__ __forceinline__ void rx_cell_res_once(const Get& get, double gamma, d
     double rr, vr, pr;
     rx_prim<ZD>(ru, gamma, rr, vr, pr);
     const double hs = 0.5 * np_max(ac, fabs(vr) + sqrt((gamma * pr) / rr));
-    out[0] = rx_div<ZD>(-((0.5 * (fc[0] + ru[1]) - hs * (ru[0] - cu[0])) - flo[0]), dx);
-    out[1] = rx_div<ZD>(-((0.5 * (fc[1] + (ru[1] * vr + pr)) - hs * (ru[1] - cu[1])) - flo[1]), dx);
-    out[2] = rx_div<ZD>(-((0.5 * (fc[2] + (vr * (ru[2] + pr))) - hs * (ru[2] - cu[2])) - flo[2]), dx);
+    out[0] = div_h(-((0.5 * (fc[0] + ru[1]) - hs * (ru[0] - cu[0])) - flo[0]), dx);
+    out[1] = div_h(-((0.5 * (fc[1] + (ru[1] * vr + pr)) - hs * (ru[1] - cu[1])) - flo[1]), dx);
+    out[2] = div_h(-((0.5 * (fc[2] + (vr * (ru[2] + pr))) - hs * (ru[2] - cu[2])) - flo[2]), dx);
 #pragma unroll
     for (int k = 0; k < RX_NS; ++k) {
       const double rk = get(2, 3 + k), ck = get(1, 3 + k);
       const double fhi = 0.5 * (fc[3 + k] + (ru[1] * rx_div<ZD>(rk, rr))) - hs * (rk - ck);
-      out[3 + k] = rx_div<ZD>(-(fhi - flo[3 + k]), dx);
+      out[3 + k] = div_h(-(fhi - flo[3 + k]), dx);
     }
   }
   // sources of the centre cell, accumulated from zero in rx_sources' order

@@ -86,7 +86,8 @@ _last_info = {}
 
 def last_isvd_info() -> dict:
     """Diagnostics of the most recent ``isvd_update`` call (qnorm, ynorm,
-    proj_resid, degenerate, reorthogonalised, sweeps)."""
+    proj_resid, degenerate, reorthogonalised, sweeps, core_path: 0 = secular
+    equation, 1/2 = Jacobi fallbacks)."""
     return dict(_last_info)
 
 
@@ -94,8 +95,8 @@ def isvd_update(basis: ReducedBasis, y_hat, lam: float, r: int) -> ReducedBasis:
     """tracking.py:141-178 — rank-r incremental SVD with forgetting ``lam``.
 
     Runs three device passes (projection, optional re-orthogonalisation,
-    fused rotation) around a one-block Jacobi SVD of the (r+1)^2 core
-    matrix.  Returns a new basis (inputs are not modified), on the device
+    fused rotation) around a one-block SVD of the (r+1)^2 core matrix
+    (secular equation of the arrow structure; Jacobi as the verified fallback).  Returns a new basis (inputs are not modified), on the device
     if the inputs were device tensors, else as numpy arrays.
     """
     phi = _dev.dev(basis.phi)
@@ -112,7 +113,8 @@ def isvd_update(basis: ReducedBasis, y_hat, lam: float, r: int) -> ReducedBasis:
                        ptr(sigma_out), None, C.byref(info))
     _last_info.update(qnorm=info.qnorm, ynorm=info.ynorm, proj_resid=info.proj_resid,
                       degenerate=bool(info.degenerate),
-                      reorthogonalised=bool(info.reorthogonalised), sweeps=info.sweeps)
+                      reorthogonalised=bool(info.reorthogonalised), sweeps=info.sweeps,
+                      core_path=info.core_path)
     return ReducedBasis(phi=_dev.like(phi_out, basis.phi), sigma=_dev.like(sigma_out, basis.sigma))
 
 

@@ -404,6 +404,54 @@ def loops():
         sampling="fgs", feature="pressure-gradient", n_extra=13, rule=U("isvd", lam=0.25)))
 
 
+def cfg0_loop(n_online=500, stride=10):
+    """BASELINE configuration 0 as defined (Burgers N=1024, nu=1e-3, seeded
+    bump IC, dt=1e-4, w_init=2000 -> POD of 2001 states, r=n_s=16, z=10,
+    lambda=0.1, LSPG + QDEIM) over the first ``n_online`` online steps, run
+    by the real reference.  Stored compactly: the offline results the GPU
+    run injects (q_ref, basis, q_last), decoded states every ``stride``
+    steps, and every per-step / per-event decision."""
+    ic = burgers_bump_ic(1024)
+    cfg = driver.ExperimentConfig(
+        model="burgers", n_elem=1024, nu=1e-3, dt=1e-4, n_t=2000 + n_online, r=16, n_s=16,
+        w_init=2000, z=10, projection="lspg", sampling="qdeim", mode="adaptive",
+        rule=tracking.UpdateRule("isvd", lam=0.1))
+
+    class Custom(fom.BurgersProblem):
+        def initial_state(self):
+            return ic.copy()
+    orig = driver.make_problem
+    driver.make_problem = lambda c: Custom(c.n_elem, nu=c.nu)
+    try:
+        truth = driver.run_fom(driver.ExperimentConfig(**{**cfg.__dict__, "mode": "fom"}))
+        rec = _Recorder()
+        undo = rec.install()
+        try:
+            res = driver.run_adaptive_rom(cfg, truth=truth.trajectory)
+        finally:
+            undo()
+    finally:
+        driver.make_problem = orig
+    tr = truth.trajectory
+    training = tr[: cfg.w_init + 1]
+    scaling = snapshots.ScalingTransform(q_ref=training[0].copy(), phi_norm=np.ones(1))
+    y_train = np.column_stack([scaling.preprocess(q) for q in training])
+    basis0 = snapshots.pod(y_train, cfg.r)
+    ev = [{k: (v if not isinstance(v, (np.bool_, bool)) else bool(v)) for k, v in e.items()}
+          for e in res.event_log]
+    env_state, env_sigma, env_samp = _envelope(cfg, tr, res.trajectory, np.array(rec.sigma), ic,
+                                               rec.samplings, seeds=(1, 2, 3))
+    keep = np.arange(cfg.w_init + stride, cfg.n_t + 1, stride)
+    save("loop_cfg0", q_ref=training[0], q_last=training[-1], phi0=basis0.phi,
+         sigma0=basis0.sigma, steps=keep, traj=res.trajectory[keep], truth=tr[keep],
+         sigma=np.array(rec.sigma), it=np.array([s[1] for s in rec.steps]),
+         conv=np.array([s[2] for s in rec.steps]), samplings=np.array(rec.samplings),
+         errors=res.errors, events=np.array(json.dumps(ev, default=float)),
+         failures=np.array(res.newton_failures, dtype=np.int64),
+         env_state=env_state[keep], env_sigma=env_sigma, env_samp_stable=env_samp,
+         wall=np.array(res.wall_seconds), n_online=np.array(n_online))
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["residuals", "jacobians", "newton", "isvd", "sampling_cases",
                              "rom_steps", "loops"]

@@ -201,14 +201,16 @@ def test_online_loop_matches_reference(golden, name):
     events = json.loads(str(g["events"]))
     assert len(events) == len(rec.events)
     for j, (e_ref, e) in enumerate(zip(events, rec.events)):
-        # the residual norm is measured against the tracked basis, whose
-        # trailing directions sit at roundoff level late in ill-conditioned
-        # runs: gate it by the reference's own sigma envelope at that event
+        # the residual norm ||y - Phi Phi^T y|| is a cancellation: a basis
+        # perturbation of relative size e moves it by ~e ||y||.  Gate it by the
+        # reference's own sigma envelope at the previous event times ||y||
+        # (finite, so a gross mismatch still fails)
         prior = float(g["env_sigma"][j - 1].max()) if j > 0 else 0.0
-        rtol = 1e-8 if prior < 1e-10 else np.inf
+        y_hat = d * (rec.signal[j + 1][1] - q_ref)
+        atol = 10.0 * prior * float(np.linalg.norm(y_hat)) + 1e-14
         assert e_ref["coarse_iterations"] == e["coarse_iterations"]
         assert e_ref["coarse_converged"] == e["coarse_converged"]
         assert "update_error" not in e_ref and "update_error" not in e
-        assert np.isclose(e_ref["residual_norm"], e["residual_norm"], rtol=rtol, atol=1e-14)
+        assert abs(e_ref["residual_norm"] - e["residual_norm"]) <= 1e-8 * e_ref["residual_norm"] + atol
     samp_ref = [list(s) for s in g["samplings"]]
     assert samp_ref == [list(s) for s in rec.samplings]
