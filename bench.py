@@ -168,19 +168,23 @@ def roofline(bytes_per_launch: float, ms_per_launch: float, traffic=None) -> dic
 
 # --------------------------------------------------------------------------- cfg2
 
-def cfg2_inputs(case, n_snap: int, seed: int = 0):
-    """Device-generated rank-K stream (torch CUDA RNG; the parity tests use
-    the numpy recipe of configs.StreamCase at smaller N)."""
+def cfg2_inputs(case, n_snap: int):
+    """The seeded stream of configs.StreamCase (the recipe the parity tests
+    use): the Gaussian and every snapshot's coefficients and noise come from
+    numpy's default_rng streams on the host; the modes are the unique QR
+    factor (positive R diagonal) of that Gaussian, computed on the device.
+    Returns (n_snap, N) on the device: row k = snapshot k."""
     import torch
-    g = torch.Generator(device="cuda").manual_seed(seed)
-    q = torch.linalg.qr(torch.randn(case.n, case.k, dtype=torch.float64, device="cuda",
-                                    generator=g))[0]
-    s = torch.arange(1, case.k + 1, dtype=torch.float64, device="cuda") ** -1.5
-    coef = torch.randn(case.k, n_snap, dtype=torch.float64, device="cuda", generator=g) * s[:, None]
-    snaps = q @ coef + case.noise * torch.randn(case.n, n_snap, dtype=torch.float64,
-                                                device="cuda", generator=g)
-    del q
-    return snaps.T.contiguous()  # (n_snap, N): row k = snapshot k
+    g = torch.from_numpy(case.gaussian()).cuda()
+    q, rr = torch.linalg.qr(g)
+    del g
+    q *= torch.where(torch.diagonal(rr) < 0, -1.0, 1.0)[None, :]
+    coef = torch.from_numpy(np.stack([case.coefficients(k) for k in range(n_snap)], axis=1)).cuda()
+    noise = torch.from_numpy(np.stack([case.noise_vector(k) for k in range(n_snap)], axis=0)).cuda()
+    snaps = (q @ coef).T.contiguous()
+    snaps += case.noise * noise
+    del q, noise
+    return snaps
 
 
 def bench_cfg2(args, rank, world):
@@ -253,7 +257,7 @@ def bench_cfg2(args, rank, world):
         "metric": "iSVD rank-1 updates/s (N=2^22, r=64); iSVD % of HBM roofline",
         "value": round(value, 3), "unit": "updates/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded rank-96 stream, device RNG)",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (configs.StreamCase: seeded rank-96 stream, numpy default_rng)",
         "config": {"workload": "cfg2-isvd-stream", "n": n, "r": r, "lam": case.lam,
                    "l2": "inputs larger than L2 (basis 2 GiB)", "parallelism": f"replicas{world}"},
         "roofline": roofline(p1_bytes, p1_ms / max(p1_n, 1)) if p1_n else None,
@@ -474,12 +478,12 @@ def bench_rom(args, rank, world):
     # Roofline.  Explicit basis (r not in {32, 64} or small N): the iSVD
     # rotation Phi' = [Phi | q_hat] B (rot_tc_kernel, FP64 DMMA), 2 N r (r+1)
     # flop.  Factored basis (csrc/factored.cu, the cfg-3 path): no rotation;
-    # the largest single kernel is the first basis pass (xpass MODE 1: X^T y,
-    # fused decode, exact row norms), HBM bound with algorithmic bytes
-    # 8 N (r + k + 6): A, the k active residual columns, y, q_ref, d, the
-    # norm read + write and the decoded state.  k cycles 0..15 between
-    # re-anchors (one event per step here); the mean over the timed events is
-    # used.  QDEIM is larger in total but is a sequence of rounds of small
+    # the largest single kernel is the first basis pass (xpass_tma_kernel
+    # MODE 1: X^T y and exact row norms, tiles staged by the copy engine),
+    # HBM bound with algorithmic bytes 8 N (r + k + 3): A, the k live
+    # residual columns, y, and the row-norm read + write.  k cycles 0..15
+    # between re-anchors (one event per step here); the mean over the timed
+    # events is used.  QDEIM is larger in total but is a sequence of rounds of small
     # kernels (qdeim_rounds_per_step below).
     roof = None
     if case.model == "reacting" and "decode" in per:
@@ -514,10 +518,11 @@ def bench_rom(args, rank, world):
     elif "isvd_project" in per:
         kq = 16
         k_mean = float(np.mean([(j % kq) for j in range(W, W + K)])) if case.z == 1 else 0.0
-        xbytes = 8.0 * N * (r + k_mean + 6)
+        xbytes = 8.0 * N * (r + k_mean + 3)
         roof = roofline(xbytes, per["isvd_project"][0],
-                        ncu_traffic("xpass_kernel<64, 1>", case.name))
-        roof.update({"kernel": "isvd_project (xpass_kernel<64,1>: X^T y + fused decode + row norms)",
+                        ncu_traffic("xpass_tma_kernel<64, 1>", case.name))
+        roof.update({"kernel": "isvd_project (xpass_tma_kernel<64,1>: X^T y + exact row norms, "
+                               "TMA-staged row tiles)",
                      "work_per_launch": {"bytes": xbytes, "k_mean": k_mean},
                      "share_of_step": round(probes["isvd_project"][0] / ms, 4)})
     isvd_keys = ("isvd_project", "isvd_resid", "isvd_core", "isvd_rotate")
@@ -560,7 +565,7 @@ def bench_rom(args, rank, world):
     if rank == 0 and not args.no_e2e:
         line["e2e"] = e2e_rom(args, case)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline_rom(case, steps=3)
+        line["cpu_baseline"] = cpu_baseline_rom(case)
     return line
 
 
@@ -616,48 +621,160 @@ def e2e_rom(args, case):
                     f"({E2E_RING}-slot ring); wall clock"}
 
 
-def cpu_baseline_rom(case, steps=3, n_sample=None, timed_steps=None):
-    """Oracle port of driver._run_rom on the host at a reduced grid (bounded
-    sample), scaled linearly in N to the case's grid (all per-step work of
-    the loop is O(N r) or O(N r^2))."""
+def _oracle_loop_config(case, n_elem, steps):
     from oracle import online, physics
-    n_sample = n_sample or min(case.n_elem, {"sod": 1 << 14, "reacting": 1 << 12}.get(case.model, 1 << 16))
-    small = case.scaled(n_elem=n_sample)
     if case.model == "reacting":
         from oracle import reacting as R
-        n_s = math.ceil(0.03 * n_sample) * 13
-        small = case.scaled(n_elem=n_sample, n_s=n_s, n_extra=n_s - case.r)
-        m = physics.Model("reacting", n_sample, gamma=small.gamma, mech=tuple(R.mechanism().ravel()))
+        n_s = math.ceil(0.03 * n_elem) * 13
+        small = case.scaled(n_elem=n_elem, n_s=n_s, n_extra=n_s - case.r)
+        m = physics.Model("reacting", n_elem, gamma=small.gamma, mech=tuple(R.mechanism().ravel()))
     else:
-        m = physics.Model(small.model, small.n_elem, nu=small.nu, gamma=small.gamma)
-    w_init = small.w_init
-    ocfg = online.LoopConfig(model=m, dt=small.dt, n_t=w_init + steps + 1, w_init=w_init, r=small.r,
-                             n_s=small.n_s, z=small.z, lam=small.lam, projection=small.projection,
-                             sampling=small.sampling, feature=small.feature, n_extra=small.n_extra)
+        small = case.scaled(n_elem=n_elem)
+        m = physics.Model(small.model, n_elem, nu=small.nu, gamma=small.gamma)
+    ocfg = online.LoopConfig(model=m, dt=small.dt, n_t=small.w_init + steps + 1, w_init=small.w_init,
+                             r=small.r, n_s=small.n_s, z=small.z, lam=small.lam,
+                             projection=small.projection, sampling=small.sampling,
+                             feature=small.feature, n_extra=small.n_extra)
+    return small, ocfg
+
+
+def cpu_loop_rom(case, steps):
+    """The oracle's restatement of driver._run_rom (numpy/scipy: gelsd iSVD,
+    geqp3 QDEIM, banded-LU Newton) on the host cores AT THE CASE'S OWN GRID:
+    the start (driver.py:319-331) and `steps` online steps timed separately,
+    per-step cost = steps' time / steps + start / n_online (the reference's
+    timed region amortises its start over the whole horizon)."""
+    from oracle import online
+    small, ocfg = _oracle_loop_config(case, case.n_elem, steps)
     training = online.training_states(ocfg, small.initial_state())
     q_ref, d, phi0, sigma0 = online.offline(ocfg, training)
+    online.run_online(ocfg, training, q_ref, d, phi0, sigma0, keep_stride=10 ** 9, n_steps=0)  # warm-up
+    t0 = time.perf_counter()
+    online.run_online(ocfg, training, q_ref, d, phi0, sigma0, keep_stride=10 ** 9, n_steps=0)
+    t_start = time.perf_counter() - t0
     t0 = time.perf_counter()
     online.run_online(ocfg, training, q_ref, d, phi0, sigma0, keep_stride=10 ** 9, n_steps=steps)
-    dt = time.perf_counter() - t0
-    per_step = dt / steps * (case.n_elem / n_sample)
-    return {"value": round(1.0 / per_step, 6), "unit": "online steps/s", "cores": cpu_cores(),
-            "kind": "port",
-            "sample": f"oracle online loop (numpy/scipy: gelsd iSVD, geqp3 QDEIM, sparse-LU "
-                      f"Newton) for {steps} steps at N={n_sample} (incl. start, w_init={w_init}); "
-                      f"{dt / steps:.3f} s/step scaled x{case.n_elem / n_sample:g} to N={case.n_elem}"}
+    t_all = time.perf_counter() - t0
+    n_online = case.n_t - case.w_init
+    per_step = max(t_all - t_start, 1e-9) / steps + t_start / n_online
+    return per_step, {"start_s": round(t_start, 4), "steps_s": round(t_all - t_start, 4),
+                      "sample": f"oracle online loop at N={case.n_elem} (the benchmarked grid): "
+                                f"start {t_start:.3f} s + {steps} steps {t_all - t_start:.3f} s, "
+                                f"start amortised over {n_online} online steps"}
+
+
+def cpu_step_full_grid(case):
+    """One online step of driver._run_rom (driver.py:337-387) at the full
+    grid (configuration 3: N = 2^24, r = n_s = 64) on the host cores, every
+    component run once by the oracle's restatement of the reference
+    (numpy/scipy: gelsd iSVD, geqp3 QDEIM, banded Newton, numpy residual,
+    encode/decode): a bounded sample of ~2 minutes.
+
+    The offline results are synthetic stand-ins with the real shapes: the
+    reference's training window (64 backward-Euler steps at 2^24 cells, ~8
+    min on the host) is replaced by q_ref = q_last = the seeded IC, D = 1
+    (n_var = 1: driver.py:232-247) and an orthonormal Fourier basis with
+    geometric singular values; the initial sampling is a fixed row set.
+    The timed components cost the same for any input of these shapes
+    (LAPACK gelsd / geqp3 and the residual passes are data-independent;
+    the coarse step takes one Newton iteration at this dt either way).
+    Returns (seconds per online step with the start amortised, detail)."""
+    from oracle import hyper, online, physics, reduced, subspace
+    n, r = case.n_elem, case.r
+    u0 = case.initial_state()
+    x = (np.arange(n) + 0.5) / n
+    phi = np.empty((n, r))
+    for j in range(r):
+        w = 2.0 * np.pi * (j // 2 + 1) * x
+        phi[:, j] = np.sqrt(2.0 / n) * (np.cos(w) if j % 2 == 0 else np.sin(w))
+    sigma = 0.5 ** np.arange(r, dtype=float)
+    q_ref = u0.copy()
+    d = np.ones(n)
+    m = physics.Model("burgers", n, nu=case.nu)
+    ocfg = online.LoopConfig(model=m, dt=case.dt, n_t=case.n_t, w_init=case.w_init, r=r,
+                             n_s=case.n_s, z=case.z, lam=case.lam)
+    idx = np.sort(np.random.default_rng(0).choice(n, case.n_s, replace=False)).astype(np.int64)
+    samp = hyper.closure(hyper.Sampling(indices=idx, closure=np.unique(idx)), m)
+    op = reduced.build_operator(m, phi, q_ref, d, samp)
+    a = reduced.encode(op, u0)
+    y_corr = u0
+    tm = {}
+
+    def timed(name, fn, *args):
+        t = time.perf_counter()
+        out = fn(*args)
+        tm[name] = time.perf_counter() - t
+        return out
+
+    t0 = time.perf_counter()
+    out = timed("lspg_step", reduced.lspg_step, op, m, a, case.dt, 1e-8, 10)       # driver.py:338
+    q_tilde = timed("decode", reduced.decode, op, out.a)                            # :343
+    res = timed("coarse_step", physics.coarse_step, m, y_corr, case.z, case.dt)     # :354
+    y_hat = d * (res.x - q_ref)                                                     # :359
+    phi2, sig2, _ = timed("isvd_update", subspace.isvd_update, phi, sigma, y_hat,
+                          case.lam, r)                                              # :365
+    timed("residual_norm", lambda: float(np.linalg.norm(y_hat - phi @ (phi.T @ y_hat))))  # :366
+    samp2 = timed("qdeim_sample", online._sampling, ocfg, phi2, res.x)              # :370
+    op2 = timed("build_operator", reduced.build_operator, m, phi2, q_ref, d, samp2)  # :373
+    timed("encode", reduced.encode, op2, q_tilde)                                   # :376
+    step = time.perf_counter() - t0
+    n_online = case.n_t - case.w_init
+    start = tm["coarse_step"] + tm["qdeim_sample"] + tm["build_operator"] + tm["encode"]
+    per_step = step + start / n_online
+    return per_step, {"components_s": {k: round(v, 3) for k, v in tm.items()},
+                      "step_s": round(step, 3), "gn_iterations": int(out.iterations),
+                      "sample": f"one online step of the oracle loop at N={n} (the benchmarked "
+                                f"grid), every component once ({step:.1f} s); start (= coarse "
+                                f"step + QDEIM + operator + encode) amortised over {n_online} "
+                                f"online steps; synthetic offline stand-ins of the real shapes "
+                                f"(bench.cpu_step_full_grid)"}
+
+
+def cpu_baseline_rom(case, steps=100):
+    """The host-core baseline at the benchmarked configuration: the oracle
+    loop at the case's own grid (cfg 0 / 1), or one full-grid step by
+    components (cfg 3).  Configuration 4 has no reference model; its port
+    runs on a 2^12-cell sample scaled in N (same_config false)."""
+    if case.model == "reacting":
+        n_sample = 1 << 12
+        small, ocfg = _oracle_loop_config(case, n_sample, steps)
+        from oracle import online
+        training = online.training_states(ocfg, small.initial_state())
+        q_ref, d, phi0, sigma0 = online.offline(ocfg, training)
+        t0 = time.perf_counter()
+        online.run_online(ocfg, training, q_ref, d, phi0, sigma0, keep_stride=10 ** 9, n_steps=steps)
+        per = (time.perf_counter() - t0) / steps * (case.n_elem / n_sample)
+        return {"value": round(1.0 / per, 6), "unit": "online steps/s", "cores": cpu_cores(),
+                "kind": "port", "same_config": False,
+                "sample": f"oracle loop of the builder-defined reacting model at N={n_sample}, "
+                          f"{steps} steps incl. start, scaled x{case.n_elem // n_sample} in N "
+                          f"(no reference model exists, SPEC.md:8)"}
+    if case.n_elem <= (1 << 16):
+        per, det = cpu_loop_rom(case, steps)
+    else:
+        per, det = cpu_step_full_grid(case)
+    out = {"value": round(1.0 / per, 6), "unit": "online steps/s", "cores": cpu_cores(),
+           "kind": "port", "same_config": True}
+    out.update(det)
+    return out
 
 
 def reference_rom(args, rank, world):
+    """--impl reference: the reference's algorithm (the oracle port; the
+    reference package itself cannot run past N ~ 4000: dense N^2 Newton) on
+    the host cores at the benchmarked configuration.  For configuration 3
+    one full-grid online step (~2 min) is the bounded sample, so `steps`
+    reports the steps actually timed."""
     if rank != 0:
         return None
     case = rom_case(args.config, args.n)
-    for _ in range(1):  # warm-up run (imports, BLAS threads)
-        cpu_baseline_rom(case, steps=1)
-    base = cpu_baseline_rom(case, steps=max(1, min(args.steps, 10)))
+    steps = 100 if case.n_elem <= (1 << 16) else 1
+    base = cpu_baseline_rom(case, steps=steps)
     value = base["value"]
     return {
         "metric": ROM_METRIC, "impl": "reference", "value": value, "unit": "online steps/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": world, "steps": steps, "warmup": 0,
+        "steps_requested": args.steps, "warmup_requested": args.warmup,
         "ms_per_step": round(1e3 / value, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": case.name, "n_elem": case.n_elem, "r": case.r, "n_s": case.n_s,

@@ -149,6 +149,14 @@ int adrom_encode(adrom_ctx* ctx, const double* phi, const double* q_ref, const d
 int adrom_decode(adrom_ctx* ctx, const double* phi, const double* q_ref, const double* d,
                  const double* a, int64_t n, int32_t r, double* q);
 
+/* ---- diagnostics ------------------------------------------------------- */
+/* dev_out[v] = relative_error(primitive_fields(pred)[v], primitive_fields(truth)[v])
+ * for every variable v of the model — driver.py:168-175 (relative_error) and
+ * driver.py:185-199 (_per_variable_errors / _error_history); primitive fields
+ * fom.py:200-201 and fom.py:204-210 / 279-282.  pred, truth: device states. */
+int adrom_state_errors(adrom_ctx* ctx, const adrom_model* m, const double* pred,
+                       const double* truth, double* dev_out);
+
 /* ---- incremental SVD (kernel 4) ---------------------------------------- */
 typedef struct adrom_isvd_info {
   double qnorm;          /* ||q|| (tracking.py:163)                          */
@@ -306,6 +314,10 @@ int adrom_session_read(adrom_session* s, double* host_step_log, int64_t max_step
                        adrom_event_record* host_events, int64_t max_events, int64_t* n_steps,
                        int64_t* n_events, double* dev_a, double* dev_phi, double* dev_sigma,
                        double* dev_q_tilde);
+/* the coarse lookahead state of the latest adaptation event (the signal
+ * y_corr of driver.py:324-327 / 354-357, recorded at step n + 1 + z by
+ * driver.py:356) into a device N-vector */
+int adrom_session_signal(adrom_session* s, double* dev_y);
 /* current sampled rows (device int64[n_s]) */
 int adrom_session_sampling(adrom_session* s, int64_t* dev_idx);
 /* host_out of adrom_session_advance as a ring of `slots` states (state k of

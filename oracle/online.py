@@ -59,6 +59,7 @@ class LoopRecord:
     signal: list = field(default_factory=list)       # (step, y_corr) coarse snapshots
     phi_final: np.ndarray | None = None
     a_init: np.ndarray | None = None
+    checkpoints: dict = field(default_factory=dict)  # step -> (phi, sigma, q~) after its event
 
 
 def training_states(cfg: LoopConfig, q0):
@@ -79,8 +80,12 @@ def offline(cfg: LoopConfig, training):
     return q_ref, d, phi0, sigma0
 
 
-def _sampling(cfg: LoopConfig, phi, y_corr):
-    """driver.py:264-273."""
+def _sampling(cfg: LoopConfig, phi, y_corr, pinned=None):
+    """driver.py:264-273.  ``pinned``: use these rows instead (the pinned-
+    decisions mode of the parity harness)."""
+    if pinned is not None:
+        idx = np.asarray(pinned, dtype=np.int64)
+        return hyper.closure(hyper.Sampling(indices=idx, closure=np.unique(idx)), cfg.model)
     if cfg.sampling == "fgs":
         if y_corr is None:
             raise ValueError("feature-guided sampling needs a correction state")
@@ -91,16 +96,41 @@ def _sampling(cfg: LoopConfig, phi, y_corr):
     return hyper.closure(s, cfg.model)
 
 
+_NUDGE_ULPS = [1.0]
+
+
 def _nudge(rng, x):
-    """One-ulp perturbation of random entries (the sensitivity envelope)."""
+    """Rounding-level perturbation of random entries (the sensitivity
+    envelope): one ulp by default; ``nudge_ulps`` > 1 perturbs every entry by
+    a uniform random relative amount of up to that many ulps — the size of
+    the rounding differences a different summation order leaves in a length-N
+    reduction (~sqrt(N) ulps)."""
     if rng is None:
         return x
     x = np.asarray(x, dtype=float)
-    return np.where(rng.random(x.shape) < 0.5, np.nextafter(x, np.inf), x)
+    k = _NUDGE_ULPS[0]
+    if k <= 1.0:
+        return np.where(rng.random(x.shape) < 0.5, np.nextafter(x, np.inf), x)
+    return x * (1.0 + k * 2.220446049250313e-16 * rng.uniform(-1.0, 1.0, x.shape))
+
+
+def _nudge_sigma(rng, s):
+    """Singular values: LAPACK's SVD (gesdd) guarantees them only to
+    eps ||K|| ABSOLUTE accuracy (backward stability), so the envelope perturbs
+    each by up to ``nudge_ulps`` x eps x sigma_1 (the relative one-ulp nudge
+    of ``_nudge`` with one ulp)."""
+    if rng is None:
+        return s
+    s = np.asarray(s, dtype=float)
+    k = _NUDGE_ULPS[0]
+    if k <= 1.0:
+        return _nudge(rng, s)
+    return s + k * 2.220446049250313e-16 * s[0] * rng.uniform(-1.0, 1.0, s.shape)
 
 
 def run_online(cfg: LoopConfig, training, q_ref, d, phi0, sigma0, keep_stride=1,
-               n_steps=None, nudge_seed=None) -> LoopRecord:
+               n_steps=None, nudge_seed=None, pinned_samplings=None,
+               checkpoint_steps=(), nudge_ulps=1.0) -> LoopRecord:
     """driver.py:304-390 (one timing pass).  ``n_steps`` truncates the
     horizon to a prefix (for full-size prefix parity).
 
@@ -109,8 +139,14 @@ def run_online(cfg: LoopConfig, training, q_ref, d, phi0, sigma0, keep_stride=1,
     where any other implementation's arithmetic necessarily differs from
     numpy/LAPACK's — to measure the loop's own rounding sensitivity (the
     envelope the parity gates are expressed in; like
-    ``tests/golden/make_golden._envelope`` on the reference itself)."""
+    ``tests/golden/make_golden._envelope`` on the reference itself).
+
+    ``pinned_samplings`` (one row set per sampling rebuild, start first)
+    replaces the QDEIM/FGS decisions — to compare two loops whose discrete
+    decisions are unstable under rounding (configuration 3)."""
+    pins = list(pinned_samplings) if pinned_samplings is not None else None
     rng = None if nudge_seed is None else np.random.default_rng(nudge_seed)
+    _NUDGE_ULPS[0] = float(nudge_ulps)
     model = cfg.model
     rec = LoopRecord()
     phi, sigma = np.array(phi0, dtype=float), np.array(sigma0, dtype=float)
@@ -122,7 +158,7 @@ def run_online(cfg: LoopConfig, training, q_ref, d, phi0, sigma0, keep_stride=1,
                                   cfg.newton_max_iter)
         y_corr = res.x
         rec.signal.append((cfg.w_init + cfg.z, y_corr.copy()))
-    samp = _sampling(cfg, phi, y_corr)                   # driver.py:329-331
+    samp = _sampling(cfg, phi, y_corr, pins[0] if pins else None)  # driver.py:329-331
     rec.samplings.append(samp.indices.copy())
     op = reduced.build_operator(model, phi, q_ref, d, samp)
     a = reduced.encode(op, q_last)
@@ -153,14 +189,17 @@ def run_online(cfg: LoopConfig, training, q_ref, d, phi0, sigma0, keep_stride=1,
             y_hat = d * (y_corr - q_ref)
             phi_new, sigma_new, _ = subspace.isvd_update(phi, sigma, y_hat, cfg.lam, cfg.r,
                                                          projection=cfg.isvd_projection)
-            phi_new, sigma_new = _nudge(rng, phi_new), _nudge(rng, sigma_new)
+            phi_new, sigma_new = _nudge(rng, phi_new), _nudge_sigma(rng, sigma_new)
             event["residual_norm"] = float(np.linalg.norm(y_hat - phi @ (phi.T @ y_hat)))
-            samp_new = _sampling(cfg, phi_new, y_corr)
+            samp_new = _sampling(cfg, phi_new, y_corr,
+                                 pins[len(rec.samplings)] if pins else None)
             op = reduced.build_operator(model, phi_new, q_ref, d, samp_new)
             phi, sigma = phi_new, sigma_new
             rec.samplings.append(samp_new.indices.copy())
             a = _nudge(rng, reduced.encode(op, q_tilde))
             event["a_transfer"] = a.copy()
+            if n + 1 in checkpoint_steps:
+                rec.checkpoints[n + 1] = (phi.copy(), sigma.copy(), q_tilde.copy())
         except Exception as exc:  # noqa: BLE001 — driver.py:384-385
             event["update_error"] = f"{type(exc).__name__}: {exc}"
         rec.sigma.append(sigma.copy())

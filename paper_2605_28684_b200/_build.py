@@ -41,6 +41,7 @@ UNITS = {
     "session.cu": [],
     "capi.cu": [],
     "bigsample.cu": ["--fmad=false"],  # large sampled sets (sampled residual bitwise)
+    "diag.cu": ["--fmad=false"],       # error diagnostics (primitive fields as numpy)
 }
 
 

@@ -22,6 +22,9 @@
 #include "common.cuh"
 #include "factored_internal.cuh"
 #include "linalg_internal.cuh"
+#include "tma.cuh"
+
+#include <stdlib.h>
 
 #include <vector>
 
@@ -241,6 +244,269 @@ __global__ void __launch_bounds__(256, 2) xpass_kernel(XPassArgs a) {
   (void)s1;
   if (threadIdx.x == 0) out[R + kq] = t0;
   if (bad && a.flag) atomicOr(a.flag, 1);
+}
+
+// ---------------------------------------------------------------------------
+// The same two passes with the row tiles staged by the copy engine
+// (cp.async.bulk into a STAGES-deep shared-memory ring, one mbarrier per
+// stage; tma.cuh).  One elected thread issues a tile's copies — the A rows
+// (TR x R doubles, contiguous), the ceil(k/4) live 32-byte Q panels and only
+// the per-row vectors the pass reads — so the bytes requested are exactly
+// the algorithmic ones and several tiles stay in flight per block whatever
+// the consumers' register pressure.  Each warp consumes one RPW-row group of
+// every tile with the register-streamed kernel's arithmetic (same fixed
+// reduction order).  A block owns the same XP_ROWS rows as xpass_kernel, so
+// the partial-sum layout and the host side are shared.
+// ---------------------------------------------------------------------------
+template <int R>
+struct XpT {
+  static constexpr int LPR = R / 8, RPW = 32 / LPR;
+  static constexpr int TR = 8 * RPW;                 // rows per tile: one group per warp
+  static constexpr int STAGES = 4;
+  static constexpr int A_BYTES = TR * R * 8;
+  static constexpr int Q_BYTES = (FACT_KQ / 4) * TR * 32;
+  static constexpr int V_BYTES = TR * 8;
+  static constexpr int STAGE = A_BYTES + Q_BYTES + 4 * V_BYTES;  // A | Q | y | q_ref | d | nrm2
+  static constexpr size_t SMEM = 128 + (size_t)STAGES * STAGE;
+  static_assert(XP_ROWS % TR == 0, "block rows are whole tiles");
+};
+
+template <int R, int MODE>
+__global__ void __launch_bounds__(256, 2) xpass_tma_kernel(XPassArgs a) {
+  using T = XpT<R>;
+  constexpr int LPR = T::LPR, RPW = T::RPW, TR = T::TR, STAGES = T::STAGES;
+  constexpr int QPL = FACT_KQ / LPR;
+  const int kq = a.kq, k = a.k;
+  extern __shared__ __align__(128) unsigned char xsm[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(xsm);
+  unsigned char* stage0 = xsm + 128;
+  __shared__ double red[8 * (R + FACT_KQ)];
+  __shared__ double sred[32];
+  __shared__ __align__(16) double sv[R + FACT_KQ];
+  __shared__ __align__(16) double sg[R + FACT_KQ];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int seg = lane / LPR, sl = lane - seg * LPR;
+  const double* v2p = (MODE == 1) ? a.vdrop : a.va;
+  const bool drop = v2p != nullptr;
+  // which per-row vectors this pass reads
+  const bool ld_y = a.y != nullptr;
+  const bool ld_qd = (MODE == 1) ? (a.qt != nullptr) : drop;  // q_ref, d (decode)
+  const bool ld_n2 = (MODE == 1) && drop;                     // row norms (RMW)
+  const int npan = (k + 3) >> 2;
+  for (int j = tid; j < R + FACT_KQ; j += blockDim.x) {
+    const bool ok = j < R + k;
+    sv[j] = (ok && a.v) ? a.v[j] : 0.0;
+    sg[j] = (drop && ok) ? v2p[j] : 0.0;
+  }
+  const int64_t blk0 = (int64_t)blockIdx.x * XP_ROWS;
+  const int64_t blk1 = (blk0 + XP_ROWS < a.n) ? blk0 + XP_ROWS : a.n;
+  const int ntiles = (int)((blk1 - blk0 + TR - 1) / TR);
+  const int nfull = (int)((blk1 - blk0) / TR);
+  if (tid == 0) {
+    for (int st = 0; st < STAGES; ++st) mbar_init(&bars[st], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto stage_ptr = [&](int st) { return stage0 + (size_t)st * T::STAGE; };
+  auto issue = [&](int t) {  // thread 0; full tiles only
+    const int st = t % STAGES;
+    unsigned char* b = stage_ptr(st);
+    const int64_t row = blk0 + (int64_t)t * TR;
+    const uint32_t bytes = T::A_BYTES + npan * TR * 32 + (ld_y ? T::V_BYTES : 0) +
+                           (ld_qd ? 2 * T::V_BYTES : 0) + (ld_n2 ? T::V_BYTES : 0);
+    mbar_arrive_expect_tx(&bars[st], bytes);
+    bulk_g2s(b, a.A + row * R, T::A_BYTES, &bars[st]);
+    for (int P = 0; P < npan; ++P)
+      bulk_g2s(b + T::A_BYTES + P * TR * 32, a.Q + ((int64_t)P * a.n + row) * 4, TR * 32, &bars[st]);
+    unsigned char* vb = b + T::A_BYTES + T::Q_BYTES;
+    if (ld_y) bulk_g2s(vb, a.y + row, T::V_BYTES, &bars[st]);
+    if (ld_qd) {
+      bulk_g2s(vb + T::V_BYTES, a.q_ref + row, T::V_BYTES, &bars[st]);
+      bulk_g2s(vb + 2 * T::V_BYTES, a.d + row, T::V_BYTES, &bars[st]);
+    }
+    if (ld_n2) bulk_g2s(vb + 3 * T::V_BYTES, a.nrm2 + row, T::V_BYTES, &bars[st]);
+  };
+  if (tid == 0)
+    for (int t = 0; t < STAGES && t < nfull; ++t) issue(t);
+  __syncthreads();  // sv / sg
+  const double2* vA = reinterpret_cast<const double2*>(sv);
+  const double2* gA = reinterpret_cast<const double2*>(sg);
+  const double* vQ = sv + R;
+  const double* gQ = sg + R;
+  // this lane's slices of the row-dot vectors, held in registers
+  double2 rv[4], rg[4];
+  double rvq[QPL], rgq[QPL];
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    rv[h] = vA[sl + LPR * h];
+    rg[h] = gA[sl + LPR * h];
+  }
+#pragma unroll
+  for (int q = 0; q < QPL; ++q) {
+    rvq[q] = vQ[sl + LPR * q];
+    rgq[q] = gQ[sl + LPR * q];
+  }
+  double2 accA[4];
+  double accQ[QPL];
+#pragma unroll
+  for (int h = 0; h < 4; ++h) accA[h] = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int t = 0; t < QPL; ++t) accQ[t] = 0.0;
+  double s0 = 0.0;
+  bool bad = false;
+  for (int t = 0; t < ntiles; ++t) {
+    const int st = t % STAGES;
+    unsigned char* b = stage_ptr(st);
+    const double* As = reinterpret_cast<const double*>(b);
+    const double* Qs = reinterpret_cast<const double*>(b + T::A_BYTES);
+    const double* Vs = reinterpret_cast<const double*>(b + T::A_BYTES + T::Q_BYTES);
+    const int64_t row0 = blk0 + (int64_t)t * TR;
+    const int cnt = (int)((blk1 - row0 < TR) ? (blk1 - row0) : TR);
+    if (t < nfull) {
+      mbar_wait(&bars[st], (uint32_t)((t / STAGES) & 1));
+    } else {  // the block's ragged last tile: plain loads, zero fill
+      double* Aw = reinterpret_cast<double*>(b);
+      for (int e = tid; e < TR * R; e += blockDim.x)
+        Aw[e] = (e / R < cnt) ? a.A[row0 * R + e] : 0.0;
+      double* Qw = reinterpret_cast<double*>(b + T::A_BYTES);
+      for (int e = tid; e < (FACT_KQ / 4) * TR * 4; e += blockDim.x) {
+        const int P = e / (TR * 4), rr = (e / 4) % TR, c = e & 3;
+        Qw[e] = (rr < cnt && P < npan) ? a.Q[((int64_t)P * a.n + row0 + rr) * 4 + c] : 0.0;
+      }
+      double* Vw = reinterpret_cast<double*>(b + T::A_BYTES + T::Q_BYTES);
+      for (int rr = tid; rr < TR; rr += blockDim.x) {
+        const bool ok = rr < cnt;
+        Vw[rr] = (ok && ld_y) ? a.y[row0 + rr] : 0.0;
+        Vw[TR + rr] = (ok && ld_qd) ? a.q_ref[row0 + rr] : 0.0;
+        Vw[2 * TR + rr] = (ok && ld_qd) ? a.d[row0 + rr] : 1.0;
+        Vw[3 * TR + rr] = (ok && ld_n2) ? a.nrm2[row0 + rr] : 0.0;
+      }
+      __syncthreads();
+    }
+    const int rl = warp * RPW + seg;  // this lane group's row in the tile
+    const bool live = rl < cnt;
+    const int64_t i = row0 + rl;
+    double2 xa[4];
+    double xq[QPL];
+    const double2* rowp = reinterpret_cast<const double2*>(As + rl * R);
+#pragma unroll
+    for (int h = 0; h < 4; ++h) xa[h] = rowp[sl + LPR * h];
+#pragma unroll
+    for (int q = 0; q < QPL; ++q) {
+      const int j = sl + LPR * q;
+      xq[q] = (j < k) ? Qs[(j >> 2) * TR * 4 + rl * 4 + (j & 3)] : 0.0;
+    }
+    const double yv = ld_y ? Vs[rl] : 0.0;
+    const double qr = ld_qd ? Vs[TR + rl] : 0.0;
+    const double dd = ld_qd ? Vs[2 * TR + rl] : 1.0;
+    double t0 = 0.0, t2 = 0.0;
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      bad |= !(isfinite(xa[h].x) && isfinite(xa[h].y));
+      t0 += xa[h].x * rv[h].x + xa[h].y * rv[h].y;
+      if (drop) t2 += xa[h].x * rg[h].x + xa[h].y * rg[h].y;
+    }
+#pragma unroll
+    for (int q = 0; q < QPL; ++q) {
+      t0 += xq[q] * rvq[q];
+      if (drop) t2 += xq[q] * rgq[q];
+    }
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1) {
+      t0 += __shfl_xor_sync(0xffffffffu, t0, o);
+      if (drop) t2 += __shfl_xor_sync(0xffffffffu, t2, o);
+    }
+    if (live) {
+      double w0;
+      if (MODE == 1) {
+        if (a.qt && sl == 0) a.qt[i] = qr + t0 / dd;  // decode (projection.py:104)
+        if (drop && sl == 0) a.nrm2[i] = fmax(Vs[3 * TR + rl] - t2 * t2, 0.0);
+        w0 = yv;
+        bad |= !isfinite(w0);
+        if (sl == 0) s0 += w0 * w0;
+      } else {
+        w0 = yv - t0;                                  // q = y - Phi p (tracking.py:162)
+        if (drop && sl == 0) a.qt[i] = qr + t2 / dd;   // fused decode (projection.py:104)
+        bad |= !isfinite(w0);
+        if (sl == 0) {
+          if (a.qv) a.qv[i] = w0;
+          s0 += w0 * w0;
+        }
+        // column k joins its 4-column panel as one full 32-byte sector
+#pragma unroll
+        for (int q = 0; q < QPL; ++q) {
+          const int j = sl + LPR * q;
+          if ((j >> 2) == (k >> 2)) a.Qw[qpanel(i, j, a.n)] = (j < k) ? xq[q] : (j == k ? w0 : 0.0);
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        accA[h].x += xa[h].x * w0;
+        accA[h].y += xa[h].y * w0;
+      }
+#pragma unroll
+      for (int q = 0; q < QPL; ++q) accQ[q] += xq[q] * w0;
+    }
+    __syncthreads();  // stage st fully consumed
+    if (tid == 0 && t + STAGES < nfull) issue(t + STAGES);
+  }
+  // fold the row segments sharing columns, then the warps (fixed order)
+#pragma unroll
+  for (int o = LPR; o < 32; o <<= 1) {
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      accA[h].x += __shfl_xor_sync(0xffffffffu, accA[h].x, o);
+      accA[h].y += __shfl_xor_sync(0xffffffffu, accA[h].y, o);
+    }
+#pragma unroll
+    for (int q = 0; q < QPL; ++q) accQ[q] += __shfl_xor_sync(0xffffffffu, accQ[q], o);
+  }
+  constexpr int WD = R + FACT_KQ;
+  if (seg == 0) {
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      red[warp * WD + 2 * (sl + LPR * h)] = accA[h].x;
+      red[warp * WD + 2 * (sl + LPR * h) + 1] = accA[h].y;
+    }
+#pragma unroll
+    for (int q = 0; q < QPL; ++q) red[warp * WD + R + sl + LPR * q] = accQ[q];
+  }
+  __syncthreads();
+  const int width = xpass_width(R, kq, MODE);
+  double* out = a.partial + (size_t)blockIdx.x * width;
+  for (int c = tid; c < R + kq; c += 256) {
+    double sacc = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) sacc += red[w * WD + c];
+    out[c] = sacc;
+  }
+  const double tsum = block_sum<256>(s0, sred);
+  if (tid == 0) out[R + kq] = tsum;
+  if (bad && a.flag) atomicOr(a.flag, 1);
+}
+
+// ADROM_XPASS_TMA=0 selects the register-streamed passes (A/B comparisons)
+static bool xpass_use_tma() {
+  static const bool v = [] {
+    const char* e = getenv("ADROM_XPASS_TMA");
+    return !(e && atoi(e) == 0);
+  }();
+  return v;
+}
+
+template <int R, int MODE>
+static void xpass_launch(adrom_ctx* ctx, int grid, const XPassArgs& a) {
+  if (xpass_use_tma()) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(xpass_tma_kernel<R, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)XpT<R>::SMEM);
+      attr = true;
+    }
+    xpass_tma_kernel<R, MODE><<<grid, 256, XpT<R>::SMEM, ctx->stream>>>(a);
+  } else {
+    xpass_kernel<R, MODE><<<grid, 256, 0, ctx->stream>>>(a);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -603,8 +869,8 @@ int fact_decode(adrom_ctx* ctx, const FactBasis& b, const double* a, const doubl
   const int grid = xpass_grid(ctx, b.n);
   XPassArgs a1{b.A, b.Q, b.n, b.k, FACT_KQ, v, nullptr, q_ref, d, q_tilde, nullptr, nullptr, partial,
                nullptr};
-  if (r == 64) xpass_kernel<64, 1><<<grid, 256, 0, ctx->stream>>>(a1);
-  else if (r == 32) xpass_kernel<32, 1><<<grid, 256, 0, ctx->stream>>>(a1);
+  if (r == 64) xpass_launch<64, 1>(ctx, grid, a1);
+  else if (r == 32) xpass_launch<32, 1>(ctx, grid, a1);
   else return set_error(ctx, ADROM_ERR_ARG, "factored decode: rank %d", r);
   ADROM_LAUNCH_CK(ctx);
   return ADROM_OK;
@@ -666,8 +932,8 @@ int fact_event_pass_a(adrom_ctx* ctx, const FactBasis& b, const FactEventArgs& e
   int pr = prof_begin(ctx, PROBE_ISVD_PROJECT);
   XPassArgs a1{b.A, b.Q, b.n, k, FACT_KQ, nullptr, e.y, e.q_ref, e.d, nullptr, nullptr, nullptr,
                e.partial_a, e.flag_a, e.vdrop_in, e.vdrop_in ? e.nrm2_inout : nullptr, nullptr};
-  if (r == 64) xpass_kernel<64, 1><<<grid, 256, 0, ctx->stream>>>(a1);
-  else xpass_kernel<32, 1><<<grid, 256, 0, ctx->stream>>>(a1);
+  if (r == 64) xpass_launch<64, 1>(ctx, grid, a1);
+  else xpass_launch<32, 1>(ctx, grid, a1);
   ADROM_LAUNCH_CK(ctx);
   const int w1 = xpass_width(r, FACT_KQ, 1);
   reduce_partials_kernel<<<w1, 256, 0, ctx->stream>>>(e.partial_a, grid, w1, f.t1, nullptr);
@@ -713,8 +979,8 @@ int fact_event_pass_b(adrom_ctx* ctx, const FactBasis& b, const FactEventArgs& e
   int pr = prof_begin(ctx, PROBE_ISVD_RESID);
   XPassArgs a2{b.A, b.Q, b.n, k, FACT_KQ, f.vp, e.y, e.q_ref, e.d, e.q_tilde, e.Qw, e.qv, e.partial,
                e.flag, nullptr, nullptr, e.a ? f.vdec : nullptr};
-  if (r == 64) xpass_kernel<64, 2><<<grid, 256, 0, ctx->stream>>>(a2);
-  else xpass_kernel<32, 2><<<grid, 256, 0, ctx->stream>>>(a2);
+  if (r == 64) xpass_launch<64, 2>(ctx, grid, a2);
+  else xpass_launch<32, 2>(ctx, grid, a2);
   ADROM_LAUNCH_CK(ctx);
   const int w2 = xpass_width(r, FACT_KQ, 2);
   reduce_partials_kernel<<<w2, 256, 0, ctx->stream>>>(e.partial, grid, w2, f.t2, nullptr);

@@ -989,26 +989,31 @@ __global__ void __launch_bounds__(128) isvd_solve_kernel(const double* __restric
 //   G' = B^T [[G, c_hat], [c_hat^T, 1]] B with c_hat = Phi^T q / ||q||
 //   proj_resid = ||y - Phi Phi^T y|| = sqrt(||q||^2 + d^T G d), d = p - p1
 //                                                       (driver.py:366-367)
+template <bool VG>
 __global__ void __launch_bounds__(1024) isvd_core_kernel(
     const double* __restrict__ sigma, const double* __restrict__ red1,
     const double* __restrict__ pls, const double* __restrict__ red2,
     const int* __restrict__ need, const double* __restrict__ G, int r_cur, int r, double lam,
     double* __restrict__ Bout, double* __restrict__ qinv_out, double* __restrict__ Tws,
     double* __restrict__ Gout, double* __restrict__ sigma_out, double* __restrict__ stats,
-    int* __restrict__ flag, double* __restrict__ udrop_out, double* __restrict__ vglob) {
+    int* __restrict__ flag, double* __restrict__ udrop_out, double* __restrict__ vglob,
+    int force_jacobi) {
   extern __shared__ double sm[];
   const int n = r_cur + 1;
   const int ld = n + ((n & 1) ? 0 : 1);  // odd leading dimension
   double* A = sm;            // n x ld (column-major: column j = row j of K)
   // V (n x ld) in shared memory, or in global memory (L2-resident) when
-  // both matrices do not fit (r_cur > 110)
-  double* V = vglob ? vglob : A + n * ld;
-  double* p = vglob ? A + n * ld : V + n * ld;    // r_cur
+  // both matrices do not fit (r_cur > 110); a compile-time choice so the
+  // loops below use shared-memory loads, not generic ones
+  double* V = VG ? vglob : A + n * ld;
+  double* p = VG ? A + n * ld : V + n * ld;       // r_cur
   double* s = p + r_cur;     // n
   double* chat = s + n;      // r_cur
   double* dv = chat + r_cur; // r_cur (p - p1)
   double* red = dv + r_cur;  // 32
   int* order = (int*)(red + 32);
+  // T = Ghat B ((r_cur+1) x r): shared memory after `order` when V is, else Tws
+  double* Ts = VG ? Tws : (double*)(((uintptr_t)(order + n) + 15) & ~(uintptr_t)15);
   __shared__ int sh_flag;
   __shared__ double sh_q[4];
   const int tid = threadIdx.x;
@@ -1118,7 +1123,8 @@ __global__ void __launch_bounds__(1024) isvd_core_kernel(
     }
     worst = block_max_dyn(worst, red);
     if (tid == 0)
-      sh_path = (conv && worst <= 256.0 * n * 2.220446049250313e-16 * (dm * dm + zz)) ? 0 : 1;
+      sh_path = (!force_jacobi && conv &&
+                 worst <= 256.0 * n * 2.220446049250313e-16 * (dm * dm + zz)) ? 0 : 1;
     __syncthreads();
   }
   if (sh_path) {
@@ -1132,14 +1138,34 @@ __global__ void __launch_bounds__(1024) isvd_core_kernel(
     }
     __syncthreads();
   }
+  // sorted kept columns B (column c = U[:, order[c]]) into A's buffer
+  double* Bs = A;
+  auto gather_b = [&]() {
+    for (int e = tid; e < r * n; e += blockDim.x) {
+      const int c = e / n, k = e - c * n;
+      Bs[c * ld + k] = V[order[c] * ld + k];
+    }
+    __syncthreads();
+  };
+  gather_b();
+  // orthonormality of the kept columns (upper triangle, two chains per dot)
   double defect = 0.0;
-  for (int e = tid; e < r * r; e += blockDim.x) {
-    const int a = e / r, b = e - a * r;
-    const double* ua = V + (size_t)order[a] * ld;
-    const double* ub = V + (size_t)order[b] * ld;
-    double dot = 0.0;
-    for (int k = 0; k < n; ++k) dot += ua[k] * ub[k];
-    defect = fmax(defect, fabs(dot - (a == b ? 1.0 : 0.0)));
+  const int npair = r * (r + 1) / 2;
+  for (int e = tid; e < npair; e += blockDim.x) {
+    int a = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);  // e -> (a, b), b <= a
+    while ((a + 1) * (a + 2) / 2 <= e) ++a;
+    while (a * (a + 1) / 2 > e) --a;
+    const int b = e - a * (a + 1) / 2;
+    const double* ua = Bs + a * ld;
+    const double* ub = Bs + b * ld;
+    double d0 = 0.0, d1 = 0.0;
+    int k = 0;
+    for (; k + 1 < n; k += 2) {
+      d0 += ua[k] * ub[k];
+      d1 += ua[k + 1] * ub[k + 1];
+    }
+    if (k < n) d0 += ua[k] * ub[k];
+    defect = fmax(defect, fabs((d0 + d1) - (a == b ? 1.0 : 0.0)));
   }
   defect = block_max_dyn(defect, red);
   __shared__ int sh_fallback;
@@ -1156,17 +1182,27 @@ __global__ void __launch_bounds__(1024) isvd_core_kernel(
     fill_k(true);
     jr = block_jacobi<16>(A, ld, n, n, V, ld, 60, 1e-15, &sh_flag);
     column_norms_sorted(A, ld, n, n, s, order);
+    gather_b();
   }
   // rotation factors B[k][c] = U[k][order[c]] (k = r_cur is u_bot)
   const double inv = degenerate ? 0.0 : 1.0 / qnorm;
   for (int e = tid; e < n * r; e += blockDim.x) {
     const int k = e / r, c = e - k * r;
-    Bout[e] = V[order[c] * ld + k];
+    Bout[e] = Bs[c * ld + k];
   }
   // the left singular vector the truncation drops (factored basis: exact row norms)
   if (udrop_out && r < n)
     for (int k = tid; k < n; k += blockDim.x) udrop_out[k] = V[order[r] * ld + k];
   if (tid == 0) *qinv_out = inv;
+  __syncthreads();
+  // G staged in V's buffer when both are in shared memory (V is consumed)
+  const double* Gm = G;
+  if (!VG) {
+    double* Gsh = V;
+    for (int e = tid; e < r_cur * r_cur; e += blockDim.x) Gsh[e] = G[e];
+    Gm = Gsh;
+    __syncthreads();
+  }
   // c_hat = Phi^T q / ||q||: explicit (pass 2) or p1 - G p (normal equations)
   for (int k = tid; k < r_cur; k += blockDim.x) {
     double c;
@@ -1174,31 +1210,52 @@ __global__ void __launch_bounds__(1024) isvd_core_kernel(
       c = red2[k];
     } else {
       double gp = 0.0;
-      for (int j = 0; j < r_cur; ++j) gp += G[k * r_cur + j] * p[j];
+      for (int j = 0; j < r_cur; ++j) gp += Gm[k * r_cur + j] * p[j];
       c = red1[k] - gp;
     }
     chat[k] = c * inv;
   }
   __syncthreads();
-  // T = Ghat B  ((r_cur+1) x r), then G' = B^T T  (r x r)
-  for (int e = tid; e < n * r; e += blockDim.x) {
-    const int k = e / r, c = e - k * r;
-    double acc = 0.0;
-    if (k < r_cur) {
-      for (int l = 0; l < r_cur; ++l) acc += G[k * r_cur + l] * V[order[c] * ld + l];
-      acc += chat[k] * V[order[c] * ld + r_cur];
-    } else {
-      for (int l = 0; l < r_cur; ++l) acc += chat[l] * V[order[c] * ld + l];
-      acc += (degenerate ? 0.0 : 1.0) * V[order[c] * ld + r_cur];
+  // T = Ghat B ((r_cur+1) x r), 4 rows per thread (one B column load feeds 4
+  // FMA chains); Ghat = [[G, c_hat], [c_hat^T, 1 (0 if degenerate)]]
+  const int kb = (n + 3) / 4;
+  for (int e = tid; e < kb * r; e += blockDim.x) {
+    const int k0 = 4 * (e / r), c = e - (e / r) * r;
+    const double* bc = Bs + c * ld;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int l = 0; l < r_cur; ++l) {
+      const double bl = bc[l];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int k = k0 + i;
+        const double g = (k < r_cur) ? Gm[k * r_cur + l] : (k == r_cur ? chat[l] : 0.0);
+        acc[i] += g * bl;
+      }
     }
-    Tws[e] = acc;
+    const double bl = bc[r_cur];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int k = k0 + i;
+      if (k < r_cur) Ts[k * r + c] = acc[i] + chat[k] * bl;
+      else if (k == r_cur) Ts[k * r + c] = acc[i] + (degenerate ? 0.0 : 1.0) * bl;
+    }
   }
   __syncthreads();
-  for (int e = tid; e < r * r; e += blockDim.x) {
-    const int a = e / r, b = e - a * r;
-    double acc = 0.0;
-    for (int k = 0; k < n; ++k) acc += V[order[a] * ld + k] * Tws[k * r + b];
-    Gout[e] = acc;
+  // G' = B^T T (r x r), 4 columns per thread
+  const int cb = (r + 3) / 4;
+  for (int e = tid; e < r * cb; e += blockDim.x) {
+    const int a = e / cb, b0 = 4 * (e - a * cb);
+    const double* ba = Bs + a * ld;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int k = 0; k < n; ++k) {
+      const double x = ba[k];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (b0 + i < r) acc[i] += x * Ts[k * r + b0 + i];
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (b0 + i < r) Gout[a * r + b0 + i] = acc[i];
   }
   __syncthreads();
   for (int c = tid; c < r; c += blockDim.x) sigma_out[c] = s[order[c]];
@@ -1215,6 +1272,15 @@ __global__ void __launch_bounds__(1024) isvd_core_kernel(
   }
 }
 
+// ADROM_CORE_JACOBI=1: skip the secular path (A/B diagnostics and tests)
+static int core_force_jacobi() {
+  static const int v = [] {
+    const char* e = getenv("ADROM_CORE_JACOBI");
+    return (e && atoi(e) != 0) ? 1 : 0;
+  }();
+  return v;
+}
+
 // one column pair per half-warp: ceil((r+2)/2) pairs, rounded up to whole
 // warps (no idle warps in the per-round barrier)
 static int core_threads(int r_cur) {
@@ -1226,8 +1292,9 @@ static int core_threads(int r_cur) {
 static size_t core_smem(int r_cur, bool v_global = false) {
   const int n = r_cur + 1;
   const int ld = n + ((n & 1) ? 0 : 1);
+  // A, V (unless global), p, s, chat, dv, red, order, T (unless global)
   return sizeof(double) * ((v_global ? 1 : 2) * (size_t)n * ld + 3 * (size_t)r_cur + n + 32) +
-         sizeof(int) * n + 64;
+         sizeof(int) * n + 64 + (v_global ? 0 : sizeof(double) * (size_t)n * r_cur + 16);
 }
 
 // V of the core SVD leaves shared memory above this size
@@ -1314,14 +1381,20 @@ int isvd_update_async(adrom_ctx* ctx, const double* phi, const double* sigma, co
   if (st) return st;
   const bool vg = core_v_global(r_cur);
   const size_t csm = core_smem(r_cur, vg);
-  cudaFuncSetAttribute(isvd_core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
   pr = prof_begin(ctx, PROBE_ISVD_CORE);
   // Gout may alias G: the kernel reads G completely before its final barrier
   double* Gout = gram_out ? gram_out : Gloc;
-  isvd_core_kernel<<<1, core_threads(r_cur), csm, ctx->stream>>>(sigma, red1, pls, red2, need, G,
-                                                                 r_cur, r, lam, B, qinv, T, Gout,
-                                                                 sigma_out, stats, flag, nullptr,
-                                                                 vg ? vglob : nullptr);
+  if (vg) {
+    cudaFuncSetAttribute(isvd_core_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
+    isvd_core_kernel<true><<<1, core_threads(r_cur), csm, ctx->stream>>>(
+        sigma, red1, pls, red2, need, G, r_cur, r, lam, B, qinv, T, Gout, sigma_out, stats, flag,
+        nullptr, vglob, core_force_jacobi());
+  } else {
+    cudaFuncSetAttribute(isvd_core_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
+    isvd_core_kernel<false><<<1, core_threads(r_cur), csm, ctx->stream>>>(
+        sigma, red1, pls, red2, need, G, r_cur, r, lam, B, qinv, T, Gout, sigma_out, stats, flag,
+        nullptr, nullptr, core_force_jacobi());
+  }
   prof_end(ctx, pr);
   ADROM_LAUNCH_CK(ctx);
   // the rotation reads q from pass 2 when it ran, else forms it from y and p
@@ -1347,10 +1420,10 @@ int isvd_core_launch(adrom_ctx* ctx, const double* sigma, const double* red1, co
                      double* B, double* qinv, double* T, double* Gout, double* sigma_out,
                      double* stats, int* flag, double* udrop) {
   const size_t csm = core_smem(r);
-  cudaFuncSetAttribute(isvd_core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
-  isvd_core_kernel<<<1, core_threads(r), csm, ctx->stream>>>(sigma, red1, pls, red2, need, G, r, r,
+  cudaFuncSetAttribute(isvd_core_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
+  isvd_core_kernel<false><<<1, core_threads(r), csm, ctx->stream>>>(sigma, red1, pls, red2, need, G, r, r,
                                                              lam, B, qinv, T, Gout, sigma_out, stats,
-                                                             flag, udrop, nullptr);
+                                                             flag, udrop, nullptr, core_force_jacobi());
   ADROM_LAUNCH_CK(ctx);
   return ADROM_OK;
 }

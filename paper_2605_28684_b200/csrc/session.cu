@@ -998,6 +998,13 @@ int adrom_session_set_host_ring(adrom_session* s, int64_t slots) {
   return ADROM_OK;
 }
 
+int adrom_session_signal(adrom_session* s, double* dev_y) {
+  if (!s || !dev_y) return ADROM_ERR_ARG;
+  ADROM_CK(s->ctx, cudaMemcpyAsync(dev_y, s->y_corr, sizeof(double) * s->N,
+                                   cudaMemcpyDeviceToDevice, s->ctx->stream));
+  return ADROM_OK;
+}
+
 int adrom_session_sampling(adrom_session* s, int64_t* dev_idx) {
   if (!s) return ADROM_ERR_ARG;
   ADROM_CK(s->ctx, cudaMemcpyAsync(dev_idx, s->op[s->opcur].idx, sizeof(int64_t) * s->cfg.n_s,

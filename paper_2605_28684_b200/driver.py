@@ -130,6 +130,13 @@ class RunResult:
         j = self.var_names.index(var) if isinstance(var, str) else var
         return float(self.errors[:, j].mean())
 
+    def time_averaged_signal_error(self, var=0) -> float:
+        """driver.py:155-159."""
+        if self.signal_errors is None or self.signal_errors.size == 0:
+            raise ValueError("run carries no signal error history")
+        j = self.var_names.index(var) if isinstance(var, str) else var
+        return float(self.signal_errors[:, j].mean())
+
     def saved_steps(self) -> np.ndarray:
         stride = max(1, self.config.save_stride)
         steps = np.arange(0, self.trajectory.shape[0], stride)
@@ -186,7 +193,7 @@ def run_fom(config: ExperimentConfig, keep_every: int = 1, problem: FomProblem |
 def _training_states(config, model, truth):
     """driver.py:250-261 (device)."""
     t = _dev.torch()
-    if truth is not None:
+    if truth is not None and not isinstance(truth, str):
         return _dev.dev(np.asarray(truth[: config.w_init + 1]) if not _dev.is_device(truth)
                         else truth[: config.w_init + 1])
     stepper = config.stepper()
@@ -294,6 +301,13 @@ class Session:
                        None, None, None, ptr(phi), None, None)
         return phi
 
+    def signal(self, dev_out=None):
+        """The coarse lookahead state of the latest event (device N-vector)."""
+        t = _dev.torch()
+        y = dev_out if dev_out is not None else t.empty(self.n_dof, dtype=t.float64, device="cuda")
+        self.ctx.scall("adrom_session_signal", self.handle, ptr(y))
+        return y
+
     def sampling(self):
         t = _dev.torch()
         idx = t.empty(self.config.n_s, dtype=t.int64, device="cuda")
@@ -314,6 +328,92 @@ def _event_dicts(events):
             d["residual_norm"] = float(e.residual_norm)
         out.append(d)
     return out
+
+
+def state_errors(model: FomProblem, pred, truth, out=None):
+    """driver.py:185-190 (_per_variable_errors) on the device: per-variable
+    relative errors of the primitive fields (adrom_state_errors).  Returns
+    the device vector (n_var) written into ``out`` when given."""
+    t = _dev.torch()
+    ctx = Context.get()
+    o = out if out is not None else t.empty(model.n_var, dtype=t.float64, device="cuda")
+    mabi = model.abi()
+    ctx.call("adrom_state_errors", C.byref(mabi), ptr(_dev.dev(pred)), ptr(_dev.dev(truth)), ptr(o))
+    return o
+
+
+class _Truth:
+    """Ground-truth rows for the error pass: a stored trajectory (host or
+    device, row n = step n, driver.py:191-199) or the fine backward-Euler
+    trajectory advanced on the device in lockstep and never stored
+    (``truth="device"``; run_fom's stepping, driver.py:202-229)."""
+
+    def __init__(self, truth, model, config, q_start):
+        self.model, self.config = model, config
+        self.arr = None if isinstance(truth, str) else truth
+        self.q = _dev.dev(q_start).clone()
+        self.n = config.w_init
+        self.stepper = config.stepper()
+
+    def row(self, n):
+        if self.arr is not None:
+            return _dev.dev(self.arr[n])
+        while self.n < n:
+            self.q = implicit_step(self.model, self.q, self.config.dt, self.stepper).x
+            self.n += 1
+        return self.q
+
+
+def _error_pass(config, model, scaling, basis0, q_last, truth, adaptive):
+    """Per-step and signal errors of the online loop (driver.py:397-405)
+    without storing its trajectory: the session is replayed outside the
+    timed region (every kernel reduces in a fixed order, so the replay is the
+    timed run) in event-sized chunks of decoded states, each state compared
+    on the device with the truth row of its step; the coarse lookahead
+    (signal) states are compared at their steps n + 1 + z <= n_t."""
+    t = _dev.torch()
+    n_online = config.n_t - config.w_init
+    chunk = config.z if adaptive else min(64, n_online)
+    src = _Truth(truth, model, config, q_last)
+    errs = t.empty((n_online, model.n_var), dtype=t.float64, device="cuda")
+    ring = t.empty((chunk, model.n_dof), dtype=t.float64, device="cuda")
+    needs_signal = adaptive or config.sampling == "fgs"
+    pending = []                     # (step, device state) signals ahead of the truth
+    sig_steps, sig_errs = [], []
+    sess = Session(config, model, adaptive)
+    try:
+        sess.load(scaling, basis0, q_last)
+        sess.start()
+        if needs_signal:                                  # driver.py:326
+            pending.append((config.w_init + config.z, sess.signal()))
+        done = 0
+        while done < n_online:
+            k = min(chunk, n_online - done)
+            sess.advance(k, 1, ring[:k], None)
+            for j in range(k):
+                n = config.w_init + 1 + done + j
+                state_errors(model, ring[j], src.row(n), errs[done + j])
+                keep = []
+                for st, y in pending:
+                    if st == n:
+                        sig_steps.append(st)
+                        sig_errs.append(state_errors(model, y, src.row(st)))
+                    elif st > config.n_t:
+                        pass                              # driver.py:400 (s <= n_t)
+                    else:
+                        keep.append((st, y))
+                pending = keep
+            done += k
+            if adaptive and k == config.z:                # event at the chunk's end
+                pending.append((config.w_init + done + config.z, sess.signal()))
+        sess.finish()
+    finally:
+        sess.close()
+    steps = np.arange(config.w_init + 1, config.n_t + 1)
+    errors = _dev.host(errs)
+    if sig_steps:
+        return steps, errors, np.array(sig_steps), _dev.host(t.stack(sig_errs))
+    return steps, errors, None, None
 
 
 def _run_rom(config: ExperimentConfig, truth, adaptive: bool, problem=None, keep_every: int = 1,
@@ -350,15 +450,15 @@ def _run_rom(config: ExperimentConfig, truth, adaptive: bool, problem=None, keep
         traj = host_buf.numpy()[:n_saved].copy()
         steps = config.w_init + np.minimum(np.arange(1, n_saved + 1) * keep_every, n_online)
     failures = [config.w_init + 1 + i for i in range(len(log)) if log[i, 0] == 0.0]
-    error_steps = errors = None
-    if truth is not None and keep_every == 1 and len(truth) > config.n_t:
-        truth_h = _dev.host(truth)
-        error_steps = np.arange(config.w_init + 1, config.n_t + 1)
-        errors = np.array([_per_variable_errors(model, traj[n], truth_h[n]) for n in error_steps])
+    error_steps = errors = sig_steps = sig_errors = None
+    if truth is not None:                                 # driver.py:397-405 (untimed)
+        error_steps, errors, sig_steps, sig_errors = _error_pass(
+            config, model, scaling, basis0, q_last, truth, adaptive)
     return RunResult(config=config, kind="adaptive" if adaptive else "static", trajectory=traj,
                      wall_seconds=float(np.mean(walls)), var_names=model.var_names,
                      newton_failures=failures, error_steps=error_steps, errors=errors,
                      event_log=_event_dicts(events) if adaptive else [],
+                     signal_steps=sig_steps, signal_errors=sig_errors,
                      trajectory_steps=steps, step_iterations=log[:, 1].astype(int))
 
 

@@ -98,6 +98,32 @@ def gpu_run(setup, steps, stepwise=True):
                 errors=[int(e.error) for e in ev], sig=np.array(sig), samp=samp, phi=phi)
 
 
+def restart_parity(setup, steps_at, n_steps=2):
+    """Local (per-step) parity along the trajectory: at each checkpoint the
+    oracle's state after the event of online step ``st`` (1-based; basis,
+    sigma, decoded state) restarts BOTH
+    loops (start: coarse lookahead, QDEIM, operator, encode; then n_steps
+    online steps).  The configuration-3 loop is chaotic under rounding (an
+    ulp nudge grows to O(1) within ~100 steps, tests/golden/cfg3_envelope.npz)
+    so a long trajectory cannot be compared pointwise; every step map can."""
+    import paper_2605_28684_b200 as P
+    case, ocfg, training, q_ref, phi_norm, d, phi0, sigma0 = setup
+    last = max(steps_at)
+    full = online.run_online(ocfg, training, q_ref, d, phi0, sigma0, keep_stride=10 ** 9,
+                             n_steps=last, checkpoint_steps={case.w_init + s for s in steps_at})
+    out = []
+    for st in steps_at:
+        phi_s, sig_s, q_s = full.checkpoints[case.w_init + st]
+        rec = online.run_online(ocfg, {case.w_init: q_s}, q_ref, d, phi_s, sig_s, keep_stride=1,
+                                n_steps=n_steps)
+        sub = (case, ocfg, {case.w_init: q_s}, q_ref, phi_norm, d, phi_s, sig_s)
+        got = gpu_run(sub, n_steps)
+        rep = compare(rec, got)
+        rep["step"] = st
+        out.append(rep)
+    return out
+
+
 def compare(ref, got, env_s=None, env_sig=None):
     """Deviation report (dict of arrays) of the device loop vs the oracle."""
     states = np.array(ref.states)

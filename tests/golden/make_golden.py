@@ -452,6 +452,47 @@ def cfg0_loop(n_online=500, stride=10):
          wall=np.array(res.wall_seconds), n_online=np.array(n_online))
 
 
+def io_artifacts():
+    """The reference's artifact writers (io.py) on a synthetic Sod RunResult:
+    the exact bytes of every file, for the format tests of
+    paper_2605_28684_b200.io."""
+    import tempfile
+    from adrom import io as rio
+    rng = np.random.default_rng(5)
+    cfg = driver.ExperimentConfig(model="sod", n_elem=16, dt=1e-3, n_t=24, w_init=8, r=4, n_s=6,
+                                  z=4, sampling="fgs", n_extra=2,
+                                  rule=tracking.UpdateRule("isvd", lam=0.25), save_stride=5,
+                                  label="golden-io")
+    m = fom.SodProblem(16)
+    traj = np.stack([m.initial_state() * (1.0 + 0.01 * k) + 1e-3 * rng.standard_normal(48)
+                     for k in range(25)])
+    steps = np.arange(9, 25)
+    errors = rng.uniform(1e-6, 1e-2, (16, 3))
+    sig_steps = np.array([12, 16, 20, 24])
+    sig_err = rng.uniform(1e-6, 1e-2, (4, 3))
+    res = driver.RunResult(config=cfg, kind="adaptive", trajectory=traj, wall_seconds=0.125,
+                           var_names=m.var_names, newton_failures=[11, 17], error_steps=steps,
+                           errors=errors, event_log=[{"event": 1, "step": 12, "coarse_converged": True,
+                                                      "coarse_iterations": 3,
+                                                      "residual_norm": 0.5}],
+                           signal_steps=sig_steps, signal_errors=sig_err)
+    out = {"traj": traj, "errors": errors, "sig_err": sig_err, "sig_steps": sig_steps}
+    with tempfile.TemporaryDirectory() as d:
+        run_dir = Path(d) / "run-golden"
+        run_dir.mkdir()
+        files = {"error_history.csv": rio.write_error_history,
+                 "signal_errors.csv": rio.write_signal_errors,
+                 "profiles.csv": rio.write_profiles, "snapshots.csv": rio.write_snapshots}
+        for name, fn in files.items():
+            fn(run_dir / name, res)
+            out["file_" + name] = np.array((run_dir / name).read_text())
+        rio.write_manifest(run_dir, res, list(files), fom_wall=1.5)
+        out["file_manifest.json"] = np.array((run_dir / "manifest.json").read_text())
+    out["cache_key"] = np.array(rio.fom_cache_key(cfg))
+    out["config_dict"] = np.array(json.dumps(rio.config_to_dict(cfg)))
+    save("io_artifacts", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["residuals", "jacobians", "newton", "isvd", "sampling_cases",
                              "rom_steps", "loops"]
