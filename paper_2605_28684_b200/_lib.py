@@ -117,6 +117,8 @@ SIGNATURES = {
                                   _p, _p, _p, _p]),
     "adrom_session_sampling": (_i32, [_p, _p]),
     "adrom_session_set_host_ring": (_i32, [_p, _i64]),
+    "adrom_session_signal": (_i32, [_p, _p]),
+    "adrom_state_errors": (_i32, [_p, C.POINTER(Model), _p, _p, _p]),
 }
 
 PROBES = ["isvd_rotate", "isvd_project", "isvd_resid", "isvd_core", "fom_residual",
