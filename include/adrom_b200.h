@@ -204,6 +204,57 @@ int adrom_gram(adrom_ctx* ctx, const double* phi, int64_t n, int32_t r, double* 
 int adrom_small_svd(adrom_ctx* ctx, const double* a, int32_t m, int32_t n, double* u,
                     double* s, double* v);
 
+/* ---- tall-skinny FP64 tensor-core products (B200 extension) ------------ */
+/* No reference counterpart: numpy's `a.T @ b` / `a @ m` inside least_squares,
+ * orth, direct_update (dense.py:100-111, :175-179; tracking.py:201-213) and the
+ * large-sample DEIM pseudo-inverse (sampling.py:162-175).  DMMA (mma.sync
+ * m8n8k4 f64), deterministic split-K.
+ * adrom_ts_tn:    C (m x n, COLUMN-major: C[i + m c]) = A^T B, A row-major
+ *                 K x m (A[k lda + i]) or, if a_kmajor, A[i lda + k]; B row-major
+ *                 K x n.  m <= 128, n <= 136.
+ * adrom_ts_apply: out = A M, A row-major K x m, M row-major m x n; out row-major
+ *                 K x n (out[k ldo + c]) or, if out_kmajor, out[c ldo + k].
+ *                 m <= 128, n <= 136.  All pointers device memory. */
+int adrom_ts_tn(adrom_ctx* ctx, int64_t K, int32_t m, int32_t n, const double* A, int64_t lda,
+                int32_t a_kmajor, const double* B, int64_t ldb, double* C);
+int adrom_ts_apply(adrom_ctx* ctx, int64_t K, int32_t m, int32_t n, const double* A, int64_t lda,
+                   const double* M, double* out, int64_t ldo, int32_t out_kmajor);
+
+/* ---- offline stage and dense helpers ---------- */
+/* fit_scaling (snapshots.py:54-69): training is m snapshots of n_dof values
+ * (row-major m x n_dof, device); q_ref = training[0], phi_norm[n_var] the
+ * per-variable mean squared fluctuation with the 1e-30 floor -> 1. */
+int adrom_fit_scaling(adrom_ctx* ctx, const double* training, int32_t m, int64_t n_dof,
+                      int32_t n_var, double* q_ref, double* phi_norm);
+/* pod(preprocess(training), r) (snapshots.py:72-89 with :48-49): Householder
+ * QR + one-sided Jacobi SVD on the device, fix_column_signs (dense.py:182).
+ * phi: n_dof x r row-major, sigma: r, s_all: min(m, n_dof) singular values
+ * (optional), rank: numerical rank (s > 1e-12 s_0).  r > rank ->
+ * ADROM_ERR_DENSE (snapshots.py:86-87). */
+int adrom_pod_window(adrom_ctx* ctx, const double* training, int32_t m, int64_t n_dof,
+                     int32_t n_var, const double* q_ref, const double* phi_norm, int32_t r,
+                     double* phi, double* sigma, double* s_all, int32_t* rank);
+/* pod(snapshots, r) (snapshots.py:72-89): y is n x m row-major (one snapshot
+ * per column). */
+int adrom_pod(adrom_ctx* ctx, const double* y, int64_t n, int32_t m, int32_t r, double* phi,
+              double* sigma, double* s_all, int32_t* rank);
+/* orth (dense.py:175-179): thin-QR Q of a (n x m row-major, n >= m) with the
+ * deterministic column signs; q: n x m row-major. */
+int adrom_orth(adrom_ctx* ctx, const double* a, int64_t n, int32_t m, double* q);
+/* least_squares (dense.py:100-111): minimum-norm x (k x nb row-major) of
+ * ||a x - b|| for a (n x k row-major, n >= k) and b (n x nb row-major),
+ * singular values below 1e-12 s_max discarded (gelsd semantics). */
+int adrom_least_squares(adrom_ctx* ctx, const double* a, int64_t n, int32_t k, const double* b,
+                        int32_t nb, double* x);
+/* the LU step of newton_solve (dense.py:160-168): A x = b by LU with partial
+ * pivoting, A (n x n row-major) and b overwritten (b -> x); an exactly zero
+ * pivot -> ADROM_ERR_SINGULAR. */
+int adrom_lu_solve(adrom_ctx* ctx, double* a, int64_t n, double* b);
+/* rusanov_flux (fom.py:222-236) on n interface pairs of conserved triplets
+ * (ul, ur, out: n x 3 row-major). */
+int adrom_rusanov_flux(adrom_ctx* ctx, const double* ul, const double* ur, int64_t n,
+                       double gamma, double* out);
+
 /* ---- hyper-reduction sampling + reduced operator ----------------------- */
 /* qdeim_sample (sampling.py:107-114): first n_s pivots of the restarted
  * column-pivoted QR of phi^T (exact greedy, ties to the lowest row).

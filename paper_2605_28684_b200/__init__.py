@@ -20,10 +20,13 @@ from .fom import (
     fd_jacobian_blocks,
     implicit_step,
     reacting_mechanism,
+    rusanov_flux,
     sod_initial_state,
 )
-from .dense import SvdResult, thin_svd, max_principal_angle
-from .tracking import ReducedBasis, UpdateRule, isvd_update
+from .dense import (SvdResult, least_squares, max_principal_angle, newton_solve, orth, pivoted_qr,
+                    principal_angles, thin_svd)
+from .tracking import (ReducedBasis, SnapshotWindow, UpdateRule, direct_update, grouse_update,
+                       isvd_update, oja_update, onestep_update, wsvd_update)
 
 __version__ = "0.1.0"
 

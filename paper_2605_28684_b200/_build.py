@@ -42,6 +42,9 @@ UNITS = {
     "capi.cu": [],
     "bigsample.cu": ["--fmad=false"],  # large sampled sets (sampled residual bitwise)
     "diag.cu": ["--fmad=false"],       # error diagnostics (primitive fields as numpy)
+    "dgemm.cu": [],                    # FP64 tensor-core GEMMs of the large-sample operator
+    "hhqr.cu": [],                     # Householder QR / Q application (offline POD, orth, lstsq)
+    "offline.cu": [],                  # fit_scaling, POD, orth, least_squares
 }
 
 
@@ -85,9 +88,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             list(ex.map(lambda s: _compile(s, UNITS[s.name], verbose), todo))
     objs = [OBJ / (s.stem + ".o") for s in srcs]
     if force or todo or not LIB.exists() or LIB.stat().st_mtime < max(o.stat().st_mtime for o in objs):
-        # cuBLAS: only the plain DGEMMs of the large-sample operator (bigsample.cu)
-        cmd = [nvcc(), *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-cudart", "static",
-               "-lcublas", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
+        cmd = [nvcc(), *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-cudart", "static"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{' '.join(cmd)}\n{res.stdout}{res.stderr}")

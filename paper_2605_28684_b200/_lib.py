@@ -100,6 +100,16 @@ SIGNATURES = {
     "adrom_isvd_stream_update": (_i32, [_p, _p, _f64, C.POINTER(IsvdInfo)]),
     "adrom_isvd_stream_read": (_i32, [_p, _p, _p]),
     "adrom_small_svd": (_i32, [_p, _p, _i32, _i32, _p, _p, _p]),
+    "adrom_ts_tn": (_i32, [_p, _i64, _i32, _i32, _p, _i64, _i32, _p, _i64, _p]),
+    "adrom_ts_apply": (_i32, [_p, _i64, _i32, _i32, _p, _i64, _p, _p, _i64, _i32]),
+    "adrom_fit_scaling": (_i32, [_p, _p, _i32, _i64, _i32, _p, _p]),
+    "adrom_pod_window": (_i32, [_p, _p, _i32, _i64, _i32, _p, _p, _i32, _p, _p, _p,
+                                C.POINTER(_i32)]),
+    "adrom_pod": (_i32, [_p, _p, _i64, _i32, _i32, _p, _p, _p, C.POINTER(_i32)]),
+    "adrom_orth": (_i32, [_p, _p, _i64, _i32, _p]),
+    "adrom_least_squares": (_i32, [_p, _p, _i64, _i32, _p, _i32, _p]),
+    "adrom_rusanov_flux": (_i32, [_p, _p, _p, _i64, _f64, _p]),
+    "adrom_lu_solve": (_i32, [_p, _p, _i64, _p]),
     "adrom_qdeim": (_i32, [_p, _p, _i64, _i32, _i32, _p]),
     "adrom_fgs": (_i32, [_p, C.POINTER(Model), _p, _i32, _p, _i32, _i32, _i32, _p]),
     "adrom_deim_operator": (_i32, [_p, _p, _i64, _i32, _p, _i32, _p]),

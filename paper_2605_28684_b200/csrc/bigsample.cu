@@ -12,11 +12,12 @@
 //     prefix sums, so the closure is sorted by construction; the sampled rows
 //     are also grouped by cell (CSR) for the reduced step;
 //   * DEIM pseudo-inverse (sampling.py:162-175) by CholeskyQR2 with a
-//     certified condition bound (cuBLAS DGEMMs for the n_s x r products);
+//     certified condition bound (DMMA GEMMs of dgemm.cu for the n_s x r
+//     products);
 //   * LSPG Gauss-Newton step (projection.py:158-204): closure decode, base
 //     residual and the r finite-difference directions evaluated per sampled
 //     CELL (one residual evaluation serves all of its sampled rows), then one
-//     DGEMM forms [jac | rho] = pinv [test | res]; the r x r update runs in
+//     split-K DMMA GEMM forms [jac | rho] = pinv [test | res]; the r x r update runs in
 //     one block (sampled.cu: lspg_update_kernel).
 //
 // Compiled with --fmad=false: the sampled residuals and the perturbed closure
@@ -25,51 +26,18 @@
 #include "reacting.cuh"
 #include "rom_internal.cuh"
 #include "sampling_internal.cuh"
+#include "dgemm_internal.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
-#include <cublas_v2.h>
 
 #include <stdlib.h>
 
 namespace adrom {
 
-// ---------------------------------------------------------------------------
-// cuBLAS handle on the context stream
-// ---------------------------------------------------------------------------
-static cublasHandle_t blas(adrom_ctx* ctx) {
-  if (!ctx->blas) {
-    cublasHandle_t h = nullptr;
-    if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) return nullptr;
-    ctx->blas = h;
-  }
-  cublasHandle_t h = (cublasHandle_t)ctx->blas;
-  cublasSetStream(h, ctx->stream);
-  cublasSetPointerMode(h, CUBLAS_POINTER_MODE_HOST);
-  return h;
-}
-
-void blas_destroy(adrom_ctx* ctx) {
-  if (ctx && ctx->blas) {
-    cublasDestroy((cublasHandle_t)ctx->blas);
-    ctx->blas = nullptr;
-  }
-}
-
-// column-major C(m x n) = op(A) op(B)
-static int dgemm(adrom_ctx* ctx, bool ta, bool tb, int m, int n, int64_t k, const double* A,
-                 int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc) {
-  cublasHandle_t h = blas(ctx);
-  if (!h) return set_error(ctx, ADROM_ERR_CUDA, "cuBLAS handle creation failed");
-  const double one = 1.0, zero = 0.0;
-  const cublasStatus_t st =
-      cublasDgemm(h, ta ? CUBLAS_OP_T : CUBLAS_OP_N, tb ? CUBLAS_OP_T : CUBLAS_OP_N, m, n, (int)k,
-                  &one, A, (int)lda, B, (int)ldb, &zero, C, (int)ldc);
-  ++ctx->launches;
-  if (st != CUBLAS_STATUS_SUCCESS)
-    return set_error(ctx, ADROM_ERR_CUDA, "cublasDgemm failed (%d)", (int)st);
-  return ADROM_OK;
-}
+// split-K partial buffers: one r x (r+1) partial per K chunk (dmma_tn runs
+// one chunk per SM; more than 296 SMs would be capped here)
+constexpr int SPLITK_MAX = 296;
 
 static size_t al(size_t b) { return (b + 255) & ~(size_t)255; }
 
@@ -450,26 +418,27 @@ int deim_pinv_big(adrom_ctx* ctx, DevOp& op, int n_s, double* work, int* flag) {
   double* R1i = R1 + (size_t)r * r;        // r x r
   double* M = R1i + (size_t)r * r;         // r x r
   double* X = M + (size_t)r * r;           // r x (r+1) chol scratch
-  double* Q1 = X + (size_t)r * (r + 1);    // n_s x r, column-major (ld n_s)
+  double* Q1 = X + (size_t)r * (r + 1);    // n_s x r, row-major (like phi_s)
+  double* part = Q1 + (size_t)n_s * r;     // split-K partials
   const size_t sm = chol_smem(r);
   cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  // phi_s is row-major n_s x r = column-major r x n_s (ld r): "A_cm"
-  int st = dgemm(ctx, false, true, r, r, n_s, op.phi_s, r, op.phi_s, r, G, r);  // G = phi_s^T phi_s
+  // phi_s is row-major n_s x r
+  int st = dmma_tn(ctx, r, r, n_s, op.phi_s, r, false, op.phi_s, r, G, part, SPLITK_MAX);  // G = phi_s^T phi_s
   if (st) return st;
   chol_kernel<<<1, 512, sm, ctx->stream>>>(G, r, 0, nullptr, R1, R1i, X, flag);
   ADROM_LAUNCH_CK(ctx);
-  st = dgemm(ctx, true, false, n_s, r, r, op.phi_s, r, R1i, r, Q1, n_s);  // Q1 = phi_s R1^{-1}
+  st = dmma_apply(ctx, n_s, r, r, op.phi_s, r, R1i, Q1, r, false);  // Q1 = phi_s R1^{-1}
   if (st) return st;
-  st = dgemm(ctx, true, false, r, r, n_s, Q1, n_s, Q1, n_s, G, r);        // G2 = Q1^T Q1
+  st = dmma_tn(ctx, r, r, n_s, Q1, r, false, Q1, r, G, part, SPLITK_MAX);        // G2 = Q1^T Q1
   if (st) return st;
   chol_kernel<<<1, 512, sm, ctx->stream>>>(G, r, 1, R1, M, R1i, X, flag);
   ADROM_LAUNCH_CK(ctx);
-  // pinv^T = phi_s (Rt^T Rt)^{-1}: column-major n_s x r == pinv row-major r x n_s
-  return dgemm(ctx, true, false, n_s, r, r, op.phi_s, r, M, r, op.pinv, n_s);
+  // pinv^T = phi_s (Rt^T Rt)^{-1}, stored K-major: pinv row-major r x n_s
+  return dmma_apply(ctx, n_s, r, r, op.phi_s, r, M, op.pinv, n_s, true);
 }
 
 size_t deim_pinv_big_work_doubles(int n_s, int r) {
-  return 5 * (size_t)r * (r + 1) + (size_t)n_s * r + 64;
+  return 5 * (size_t)r * (r + 1) + (size_t)n_s * r + (size_t)SPLITK_MAX * r * r + 64;
 }
 
 // ---------------------------------------------------------------------------
@@ -649,52 +618,13 @@ __global__ void __launch_bounds__(BL_DIR_T, NBUF == 1 ? 4 : 2)
   }
 }
 
-// split-K reduction of the batched GEMM partials (fixed order: deterministic)
-__global__ void splitk_reduce_kernel(const double* __restrict__ part, int nb, int64_t sz,
-                                     double* __restrict__ C) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < sz;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int b = 0; b < nb; ++b) s += part[b * sz + e];
-    C[e] = s;
-  }
-}
-
-constexpr int SPLITK_MAX = 296;
-
-// [jac | rho] (r x n, column-major) = pinv (r x K, row-major) [test | res]^T-ish:
-// C = P'^T T'^T with P' = pinv viewed column-major K x r and T' = test viewed
-// column-major n x K.  K is split into nb chunks (one batched DGEMM, a
-// partial per chunk) so the 128 x 129 output keeps every SM busy.
+// [jac | rho] (r x n, column-major) = pinv (r x K, row-major: K-major) times
+// [test | res] (K x n, row-major): split-K DMMA GEMM (dgemm.cu), a fixed-order
+// sum of one partial per K chunk (one chunk per SM), so the 128 x 129 output
+// keeps every SM busy and the result is deterministic.
 static int gemm_jac(adrom_ctx* ctx, int r, int n, int64_t K, const double* pinv,
                     const double* test, double* C, double* part) {
-  // 74 chunks measured best for the cfg-4 shape (148 / 296 within 1-2 %)
-  static const int cap = getenv("ADROM_SPLITK") ? atoi(getenv("ADROM_SPLITK")) : 74;
-  int nb = (int)(K / 1024);
-  if (nb > cap) nb = cap;
-  if (nb > SPLITK_MAX) nb = SPLITK_MAX;
-  if (nb < 2) return dgemm(ctx, true, true, r, n, K, pinv, K, test, n, C, r);
-  cublasHandle_t h = blas(ctx);
-  if (!h) return set_error(ctx, ADROM_ERR_CUDA, "cuBLAS handle creation failed");
-  const int64_t kc = K / nb, rem = K - kc * nb;
-  const int64_t sz = (int64_t)r * n;
-  const double one = 1.0, zero = 0.0;
-  cublasStatus_t cs = cublasDgemmStridedBatched(
-      h, CUBLAS_OP_T, CUBLAS_OP_T, r, n, (int)kc, &one, pinv, (int)K, kc, test, n, kc * n, &zero,
-      part, r, sz, nb);
-  ++ctx->launches;
-  if (cs != CUBLAS_STATUS_SUCCESS)
-    return set_error(ctx, ADROM_ERR_CUDA, "cublasDgemmStridedBatched failed (%d)", (int)cs);
-  int nparts = nb;
-  if (rem > 0) {
-    const int st2 = dgemm(ctx, true, true, r, n, rem, pinv + nb * kc, K, test + nb * kc * n, n,
-                          part + (int64_t)nb * sz, r);
-    if (st2) return st2;
-    ++nparts;
-  }
-  splitk_reduce_kernel<<<(int)((sz + 255) / 256), 256, 0, ctx->stream>>>(part, nparts, sz, C);
-  ADROM_LAUNCH_CK(ctx);
-  return ADROM_OK;
+  return dmma_tn(ctx, r, n, K, pinv, K, true, test, n, C, part, SPLITK_MAX);
 }
 
 __global__ void bl_init_kernel(const double* __restrict__ a_prev, int r, double* __restrict__ st) {

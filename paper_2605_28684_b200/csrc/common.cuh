@@ -105,9 +105,6 @@ struct adrom_ctx {
   // sampling sets: FGS ranking, plan building); never handed to callers
   void* aux = nullptr;
   size_t aux_bytes = 0;
-  // cuBLAS handle (plain GEMMs of the large-sample reduced operator), lazily
-  // created on the context stream
-  void* blas = nullptr;
   // device status words: [0] error code, [1] aux int, ...
   int* dflags = nullptr;
   // pinned host staging for small results
@@ -137,8 +134,6 @@ int check_cuda(adrom_ctx* ctx, cudaError_t e, const char* where);
 void* scratch(adrom_ctx* ctx, size_t bytes, size_t offset_bytes = 0);
 int ensure_scratch(adrom_ctx* ctx, size_t bytes);
 int ensure_aux(adrom_ctx* ctx, size_t bytes);
-// cuBLAS handle bound to ctx->stream (bigsample.cu); destroyed with the context
-void blas_destroy(adrom_ctx* ctx);
 int ensure_pinned(adrom_ctx* ctx, size_t bytes);
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 // upper bound on the blocks of any reduction kernel (rows of a partials buffer)

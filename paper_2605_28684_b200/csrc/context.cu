@@ -172,7 +172,6 @@ void adrom_ctx_destroy(adrom_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   if (ctx->scratch) cudaFree(ctx->scratch);
   if (ctx->aux) cudaFree(ctx->aux);
-  adrom::blas_destroy(ctx);
   if (ctx->dflags) cudaFree(ctx->dflags);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->prof_ev) {

@@ -735,3 +735,32 @@ int fom_implicit_step(adrom_ctx* ctx, const adrom_model& m, const double* q, dou
 }
 
 }  // namespace adrom
+
+namespace adrom {
+namespace {
+// fom.py:222-236 on batches of interface states (triplets), bitwise numpy
+__global__ void rusanov_batch_kernel(const double* __restrict__ ul, const double* __restrict__ ur,
+                                     int64_t n, double gamma, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const Cons l{ul[3 * i], ul[3 * i + 1], ul[3 * i + 2]};
+    const Cons r{ur[3 * i], ur[3 * i + 1], ur[3 * i + 2]};
+    const Cons f = rusanov(l, r, gamma);
+    out[3 * i] = f.m0;
+    out[3 * i + 1] = f.m1;
+    out[3 * i + 2] = f.m2;
+  }
+}
+}  // namespace
+}  // namespace adrom
+
+extern "C" int adrom_rusanov_flux(adrom_ctx* ctx, const double* ul, const double* ur, int64_t n,
+                                  double gamma, double* out) {
+  if (!ctx || n < 0) return ADROM_ERR_ARG;
+  if (n == 0) return ADROM_OK;
+  int64_t g = (n + 255) / 256;
+  if (g > ctx->num_sms * 8) g = ctx->num_sms * 8;
+  adrom::rusanov_batch_kernel<<<(int)g, 256, 0, ctx->stream>>>(ul, ur, n, gamma, out);
+  ADROM_LAUNCH_CK(ctx);
+  return ADROM_OK;
+}

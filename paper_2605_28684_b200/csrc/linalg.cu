@@ -521,7 +521,7 @@ __global__ void __launch_bounds__(256) rot_tiled_kernel(RotArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// FP64 tensor-core rotation (R in {32, 64}): out = [phi | q_hat] B on DMMA
+// FP64 tensor-core rotation (R in {32, 64, 128}): out = [phi | q_hat] B on DMMA
 // (mma.sync m8n8k4 f64).  64-row tiles double-buffered in smem by cp.async
 // (row stride R + 4: conflict-free fragment loads; column R holds q_hat);
 // 8 warps as 4 (rows) x 2 (cols), each warp 16 rows x R/2 columns; two
@@ -530,8 +530,10 @@ __global__ void __launch_bounds__(256) rot_tiled_kernel(RotArgs a) {
 // ---------------------------------------------------------------------------
 template <int R>
 struct RotTC {
-  static constexpr int TM = 64;            // rows per tile; 2 blocks per SM
-  static constexpr int WGN = 2;            // column groups of warps
+  // R <= 64: 64-row tiles, 2 blocks per SM; R = 128: 32-row tiles (B alone is
+  // 132 KB of smem), 1 block per SM with 8 warps as 2 (rows) x 4 (cols)
+  static constexpr int TM = R <= 64 ? 64 : 32;  // rows per tile
+  static constexpr int WGN = R <= 64 ? 2 : 4;   // column groups of warps
   static constexpr int MT = 2;             // 8-row tiles per warp
   static constexpr int WR = 8 * MT;        // rows per warp
   static constexpr int NTHR = TM / WR * WGN * 32;
@@ -559,7 +561,7 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
 }
 
 template <int R>
-__global__ void __launch_bounds__(RotTC<R>::NTHR, 2) rot_tc_kernel(RotArgs a) {
+__global__ void __launch_bounds__(RotTC<R>::NTHR, R <= 64 ? 2 : 1) rot_tc_kernel(RotArgs a) {
   using C = RotTC<R>;
   extern __shared__ __align__(16) double sm[];
   double* As0 = sm;                      // 2 stages x TM x S
@@ -767,12 +769,13 @@ __global__ void __launch_bounds__(256) rot_generic_kernel(RotArgs a) {
 }
 
 bool rot_fusable(int r_in, int r_out) {
-  return r_in == r_out && (r_in == 32 || r_in == 64) && !getenv("ADROM_NO_TC_ROT");
+  return r_in == r_out && (r_in == 32 || r_in == 64 || r_in == 128) && !getenv("ADROM_NO_TC_ROT");
 }
 
-static int64_t rot_tc_grid(const adrom_ctx* ctx, int64_t n) {
-  const int64_t nt = (n + 63) / 64;
-  int64_t gg = (int64_t)ctx->num_sms * 2;
+static int64_t rot_tc_grid(const adrom_ctx* ctx, int64_t n, int r) {
+  const int tm = r <= 64 ? RotTC<64>::TM : RotTC<128>::TM;
+  const int64_t nt = (n + tm - 1) / tm;
+  int64_t gg = (int64_t)ctx->num_sms * (r <= 64 ? 2 : 1);
   if (gg > nt) gg = nt;
   return gg < 1 ? 1 : gg;
 }
@@ -782,7 +785,7 @@ size_t rot_fuse_partial_doubles(const adrom_ctx* ctx, int r) {
 }
 
 int rot_encode_finish(adrom_ctx* ctx, const RotFuse& f, int64_t n, int r, double* out) {
-  reduce_partials_kernel<<<r, 256, 0, ctx->stream>>>(f.enc_partial, (int)rot_tc_grid(ctx, n), r,
+  reduce_partials_kernel<<<r, 256, 0, ctx->stream>>>(f.enc_partial, (int)rot_tc_grid(ctx, n, r), r,
                                                      out, nullptr);
   ADROM_LAUNCH_CK(ctx);
   return ADROM_OK;
@@ -795,12 +798,15 @@ int ts_rotate(adrom_ctx* ctx, const RotArgs& a) {
     auto launch_tc = [&](auto kern, size_t sm_doubles) -> int {
       const size_t sm = sizeof(double) * sm_doubles;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      kern<<<(int)rot_tc_grid(ctx, n), RotTC<64>::NTHR, sm, ctx->stream>>>(a);
+      kern<<<(int)rot_tc_grid(ctx, n, r_in), 256, sm, ctx->stream>>>(a);
       ADROM_LAUNCH_CK(ctx);
       return ADROM_OK;
     };
+    static_assert(RotTC<32>::NTHR == 256 && RotTC<64>::NTHR == 256 && RotTC<128>::NTHR == 256,
+                  "rot_tc_kernel launches 256 threads");
     if (r_in == 32) return launch_tc(rot_tc_kernel<32>, RotTC<32>::smem_doubles);
-    return launch_tc(rot_tc_kernel<64>, RotTC<64>::smem_doubles);
+    if (r_in == 64) return launch_tc(rot_tc_kernel<64>, RotTC<64>::smem_doubles);
+    return launch_tc(rot_tc_kernel<128>, RotTC<128>::smem_doubles);
   }
   if (r_in == r_out && (r_in == 16 || r_in == 32 || r_in == 64 || r_in == 128)) {
     int64_t g = (int64_t)ctx->num_sms * 2;

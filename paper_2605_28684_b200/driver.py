@@ -22,7 +22,7 @@ from ._lib import Context, EventRecord, SessionConfig, _p, ptr
 from .errors import DenseError, RomStepError
 from .fom import (BurgersProblem, FomProblem, ReactingEulerProblem, SodProblem, TimeStepper,
                   implicit_step)
-from .snapshots import ScalingTransform, fit_scaling, pod
+from .snapshots import ScalingTransform, fit_scaling, pod_window
 from .tracking import UpdateRule
 
 __all__ = ["ExperimentConfig", "RunResult", "make_problem", "run_fom", "run_static_rom",
@@ -210,10 +210,8 @@ def offline_stage(config, model, truth=None):
     if model.n_var == 1:  # driver.py:232-247
         scaling = ScalingTransform(q_ref=training[0].clone(), phi_norm=t.ones(1, dtype=t.float64, device="cuda"))
     else:
-        scaling = fit_scaling(list(training), model.n_var)
-    d = scaling.row_scale
-    y_train = (d[None, :] * (training - scaling.q_ref[None, :])).T.contiguous()
-    basis0 = pod(y_train, config.r)
+        scaling = fit_scaling(training, model.n_var)
+    basis0 = pod_window(training, scaling, config.r)   # pod(D (q - q_ref)), driver.py:298-299
     return training, scaling, basis0
 
 
@@ -222,10 +220,10 @@ class Session:
 
     def __init__(self, config: ExperimentConfig, model: FomProblem, adaptive: bool):
         if adaptive and config.rule.kind != "isvd":
-            raise NotImplementedError(
-                f"update rule {config.rule.kind!r} is outside the B200 hot path (only isvd)")
+            raise ValueError(f"the fused session runs the isvd rule only ({config.rule.kind!r}: "
+                             "run_adaptive_rom takes the host-orchestrated path)")
         if config.cadence != "every-event":
-            raise NotImplementedError("only the every-event cadence is on the B200 path")
+            raise ValueError("the fused session runs the every-event cadence only")
         self.ctx = Context.get()
         self.config = config
         self.model = model
@@ -416,8 +414,168 @@ def _error_pass(config, model, scaling, basis0, q_last, truth, adaptive):
     return steps, errors, None, None
 
 
+def _build_sampling(config, model, basis, y_corr):
+    """driver.py:264-273."""
+    from .sampling import FeatureMap, fgs_sample, qdeim_sample, stencil_closure
+    if config.sampling == "fgs":
+        if y_corr is None:
+            raise ValueError("feature-guided sampling needs a correction state")
+        s = fgs_sample(basis, y_corr, config.n_s, FeatureMap(kind=config.feature, n_extra=config.n_extra),
+                       model)
+    else:
+        s = qdeim_sample(basis, config.n_s)
+    return stencil_closure(s, model)
+
+
+def _apply_rule(rule, basis, window, y_hat, a_minus, r):
+    """driver.py:276-288."""
+    from . import tracking as T
+    if rule.kind == "isvd":
+        return T.isvd_update(basis, y_hat, rule.lam, r)
+    if rule.kind == "wsvd":
+        return T.wsvd_update(window, r)
+    if rule.kind == "direct":
+        return T.direct_update(basis, window)
+    if rule.kind == "onestep":
+        return T.onestep_update(basis, y_hat, a_minus)
+    if rule.kind == "oja":
+        return T.oja_update(basis, y_hat, rule.eta)
+    return T.grouse_update(basis, y_hat, rule.eta)
+
+
+def _run_rom_host(config: ExperimentConfig, truth, adaptive: bool, problem=None, keep_every: int = 1,
+                  offline=None):
+    """driver.py:291-410 as a host-orchestrated loop over the library's
+    device operations: the general path for the rules other than iSVD
+    (wsvd / direct / onestep / oja / grouse) and the every-step cadence,
+    which the fused session does not run.  Every state stays on the device;
+    the trajectory rows are copied out every ``keep_every`` steps."""
+    from .fom import coarse_step
+    from .projection import build_rom_operator, decode, encode, rom_step
+    from .tracking import SnapshotWindow
+    t = _dev.torch()
+    model = problem or make_problem(config)
+    stepper = config.stepper()
+    rule = config.rule
+    training, scaling, basis0 = offline_stage(config, model, truth)
+    if offline is not None:
+        scaling, basis0 = offline
+        scaling = ScalingTransform(q_ref=_dev.dev(scaling.q_ref), phi_norm=_dev.dev(scaling.phi_norm))
+        from .tracking import ReducedBasis
+        basis0 = ReducedBasis(_dev.dev(basis0.phi), _dev.dev(basis0.sigma))
+    q_last = training[config.w_init]
+    needs_signal = adaptive or config.sampling == "fgs"
+    n_online = config.n_t - config.w_init
+    d = scaling.row_scale
+
+    def preprocess(q):
+        return d * (q - scaling.q_ref)
+
+    def one_pass():
+        basis = basis0
+        rows, steps, failures, events, signal_records, iters = [], [], [], [], [], []
+        window = None
+        if adaptive and rule.uses_window:
+            y_train = preprocess(training)             # (w_init+1) x N
+            m = min(rule.window, config.w_init)
+            window = SnapshotWindow(rule.window, initial=[y_train[j] for j in
+                                                          range(y_train.shape[0] - m, y_train.shape[0])])
+        t.cuda.synchronize()
+        t0 = time.perf_counter()
+        y_corr = prev_signal_hat = None
+        if needs_signal:
+            res = coarse_step(model, q_last, config.z, config.dt, stepper)
+            y_corr = res.x
+            signal_records.append((config.w_init + config.z, y_corr.clone()))
+            prev_signal_hat = preprocess(y_corr)
+        sampling = _build_sampling(config, model, basis, y_corr)
+        op = build_rom_operator(basis, scaling, sampling, model, config.projection)
+        state = encode(q_last, op, n=config.w_init)
+        for n in range(config.w_init, config.n_t):
+            step = rom_step(op, model, state, config.dt, tol=config.newton_tol,
+                            max_iter=config.newton_max_iter)
+            if not step.converged:
+                failures.append(n + 1)
+            iters.append(step.iterations)
+            state = step.state
+            q_tilde = decode(state, op)
+            k = n + 1 - config.w_init
+            if keep_every > 0 and (k % keep_every == 0 or k == n_online):
+                rows.append(q_tilde.clone())
+                steps.append(n + 1)
+            at_event = adaptive and (n + 1 - config.w_init) % config.z == 0
+            refresh = at_event or (adaptive and config.cadence == "every-step")
+            if not refresh:
+                continue
+            event = {"event": len(events) + 1, "step": n + 1}
+            consume = rule.history_aware and CONSUME_LOOKAHEAD
+            try:
+                if at_event and consume:
+                    res = coarse_step(model, y_corr, config.z, config.dt, stepper)
+                    y_corr = res.x
+                    signal_records.append((n + 1 + config.z, y_corr.clone()))
+                    event["coarse_converged"] = res.converged
+                    event["coarse_iterations"] = res.iterations
+                    y_hat = preprocess(y_corr)
+                    prev_signal_hat = y_hat
+                else:
+                    y_hat = prev_signal_hat
+                if at_event and window is not None:
+                    window.push(y_hat)
+                basis_new = _apply_rule(rule, basis, window, y_hat, state.a, config.r)
+                phi = _dev.dev(basis.phi)
+                from .dense import ts_apply, ts_tn
+                proj = ts_apply(phi, ts_tn(phi, y_hat[:, None])).reshape(-1)
+                event["residual_norm"] = float(t.linalg.vector_norm(y_hat - proj))
+                sampling_new = _build_sampling(config, model, basis_new, y_corr) if at_event else op.sampling
+                op = build_rom_operator(basis_new, scaling, sampling_new, model, config.projection)
+                basis = basis_new
+                state = encode(q_tilde, op, n=n + 1)
+                if at_event and not consume:
+                    res = coarse_step(model, y_corr, config.z, config.dt, stepper)
+                    y_corr = res.x
+                    signal_records.append((n + 1 + config.z, y_corr.clone()))
+                    event["coarse_converged"] = res.converged
+                    event["coarse_iterations"] = res.iterations
+                    prev_signal_hat = preprocess(y_corr)
+            except Exception as exc:  # noqa: BLE001  failed event: keep the previous operator
+                event["update_error"] = f"{type(exc).__name__}: {exc}"
+            if at_event:
+                events.append(event)
+        t.cuda.synchronize()
+        return time.perf_counter() - t0, rows, steps, failures, events, signal_records, iters
+
+    walls = []
+    for _ in range(max(1, config.timing_repeats)):
+        wall, rows, steps, failures, events, signal_records, iters = one_pass()
+        walls.append(wall)
+    traj_rows = _dev.host(t.stack(rows)) if rows else np.zeros((0, model.n_dof))
+    if keep_every == 1:
+        traj = np.concatenate([_dev.host(training), traj_rows], axis=0)
+        steps_arr = np.arange(config.n_t + 1)
+    else:
+        traj, steps_arr = traj_rows, np.array(steps)
+    error_steps = errors = sig_steps = sig_errors = None
+    if truth is not None and not isinstance(truth, str) and len(truth) > config.n_t and keep_every == 1:
+        error_steps = np.arange(config.w_init + 1, config.n_t + 1)
+        errors = np.stack([_per_variable_errors(model, traj[n], np.asarray(_dev.host(truth[n])))
+                           for n in error_steps])
+        inr = [(s_, y) for s_, y in signal_records if s_ <= config.n_t]
+        if inr:
+            sig_steps = np.array([s_ for s_, _ in inr])
+            sig_errors = np.stack([_per_variable_errors(model, _dev.host(y), np.asarray(_dev.host(truth[s_])))
+                                   for s_, y in inr])
+    return RunResult(config=config, kind="adaptive" if adaptive else "static", trajectory=traj,
+                     wall_seconds=float(np.mean(walls)), var_names=model.var_names,
+                     newton_failures=failures, error_steps=error_steps, errors=errors,
+                     event_log=events, signal_steps=sig_steps, signal_errors=sig_errors,
+                     trajectory_steps=steps_arr, step_iterations=np.array(iters, dtype=int))
+
+
 def _run_rom(config: ExperimentConfig, truth, adaptive: bool, problem=None, keep_every: int = 1,
              offline=None):
+    if adaptive and (config.rule.kind != "isvd" or config.cadence != "every-event"):
+        return _run_rom_host(config, truth, adaptive, problem, keep_every, offline)
     model = problem or make_problem(config)
     t = _dev.torch()
     training, scaling, basis0 = offline_stage(config, model, truth)
@@ -451,7 +609,11 @@ def _run_rom(config: ExperimentConfig, truth, adaptive: bool, problem=None, keep
         steps = config.w_init + np.minimum(np.arange(1, n_saved + 1) * keep_every, n_online)
     failures = [config.w_init + 1 + i for i in range(len(log)) if log[i, 0] == 0.0]
     error_steps = errors = sig_steps = sig_errors = None
-    if truth is not None:                                 # driver.py:397-405 (untimed)
+    # driver.py:397-405 (untimed).  A truth array shorter than the horizon only
+    # injects the training window (driver.py:250-252); the reference would
+    # index past its end, here the error history is simply not produced.
+    full_truth = truth is not None and (isinstance(truth, str) or len(truth) > config.n_t)
+    if full_truth:
         error_steps, errors, sig_steps, sig_errors = _error_pass(
             config, model, scaling, basis0, q_last, truth, adaptive)
     return RunResult(config=config, kind="adaptive" if adaptive else "static", trajectory=traj,

@@ -21,6 +21,7 @@ from ._lib import BURGERS, REACTING, SOD, Context, Model, NewtonInfo, ptr
 from .errors import DenseError
 
 __all__ = ["TimeStepper", "FomProblem", "BurgersProblem", "SodProblem", "ReactingEulerProblem",
+           "rusanov_flux",
            "reacting_mechanism", "NewtonResult",
            "fd_jacobian", "fd_jacobian_blocks", "implicit_step", "coarse_step",
            "sod_initial_state", "PRIM_FLOOR", "FD_EPS"]
@@ -143,6 +144,21 @@ class BurgersProblem(FomProblem):
 
     def primitive_fields(self, q):
         return {"u": q}
+
+
+def rusanov_flux(ul, ur, gamma: float):
+    """fom.py:222-236 — local Lax-Friedrichs interface flux of single
+    conserved triplets or batches (..., 3), bitwise the reference's
+    (adrom_rusanov_flux)."""
+    uld, urd = _dev.dev(ul), _dev.dev(ur)
+    if uld.shape != urd.shape or uld.shape[-1] != 3:
+        raise ValueError(f"interface states must have shape (..., 3), got {tuple(uld.shape)}")
+    shape = uld.shape
+    flat_l, flat_r = uld.reshape(-1, 3).contiguous(), urd.reshape(-1, 3).contiguous()
+    out = _dev.empty(flat_l.shape[0], 3)
+    Context.get().call("adrom_rusanov_flux", ptr(flat_l), ptr(flat_r), C.c_int64(flat_l.shape[0]),
+                       C.c_double(gamma), ptr(out))
+    return _dev.like(out.reshape(shape), ul)
 
 
 def sod_initial_state(n_elem: int, gamma: float = 1.4) -> np.ndarray:

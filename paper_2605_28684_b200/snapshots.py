@@ -1,10 +1,11 @@
 """Scaling and offline POD with the reference signatures (``adrom/snapshots.py``).
 
-Preprocess/lift are elementwise and run where the data lives; ``pod`` is the
-OFFLINE stage (outside the timed region) and uses a
-QR + small SVD (torch/cuSOLVER for the QR; the one-block Jacobi SVD of the
-CUDA library for the small triangular factor when it fits, cuSOLVER
-otherwise).
+Preprocess/lift are elementwise and run where the data lives; ``fit_scaling``
+and ``pod`` are the OFFLINE stage (outside the timed region, SURVEY §8f item
+2) and run on the library's own kernels: a fixed-order reduction for the
+scales, Householder QR of the snapshot matrix (or of its transpose when the
+window is wider than the grid) + one-sided Jacobi SVD of the triangular
+factor + Q application + fix_column_signs (csrc/hhqr.cu, csrc/offline.cu).
 """
 
 from __future__ import annotations
@@ -13,11 +14,14 @@ from dataclasses import dataclass
 
 import numpy as np
 
+import ctypes as C
+
 from . import _dev
+from ._lib import Context, ptr
 from .errors import DenseError
 from .tracking import ReducedBasis
 
-__all__ = ["ScalingTransform", "fit_scaling", "pod", "VAR_FLOOR"]
+__all__ = ["ScalingTransform", "fit_scaling", "pod", "pod_window", "VAR_FLOOR"]
 
 VAR_FLOOR = 1e-30  # snapshots.py:23
 
@@ -49,58 +53,54 @@ class ScalingTransform:
 
 
 def fit_scaling(training, n_var: int) -> ScalingTransform:
-    """snapshots.py:54-69."""
+    """snapshots.py:54-69 (adrom_fit_scaling)."""
     if len(training) < 1:
         raise ValueError("need at least one training snapshot")
     t = _dev.torch()
     first = training[0]
     dev = _dev.is_device(first)
-    tr = t.stack([_dev.dev(q) for q in training])
-    q_ref = tr[0].clone()
-    fluct = tr - q_ref
-    per_var = fluct.reshape(len(training), -1, n_var) ** 2
-    phi_norm = t.clamp_min(per_var.mean(dim=(0, 1)), VAR_FLOOR)
-    phi_norm = t.where(phi_norm <= VAR_FLOOR, t.ones_like(phi_norm), phi_norm)
+    tr = training if (_dev.is_device(training) and training.dim() == 2) else \
+        t.stack([_dev.dev(q) for q in training])
+    tr = tr.contiguous()
+    m, n = tr.shape
+    q_ref = _dev.empty(n)
+    phi_norm = _dev.empty(n_var)
+    Context.get().call("adrom_fit_scaling", ptr(tr), C.c_int32(m), C.c_int64(n), C.c_int32(n_var),
+                       ptr(q_ref), ptr(phi_norm))
     if dev:
         return ScalingTransform(q_ref=q_ref, phi_norm=phi_norm)
     return ScalingTransform(q_ref=_dev.host(q_ref), phi_norm=_dev.host(phi_norm))
 
 
-def _fix_column_signs(q):
-    """dense.py:182-189."""
-    t = _dev.torch()
-    lead = q.abs().argmax(dim=0)
-    signs = t.sign(q[lead, t.arange(q.shape[1], device=q.device)])
-    signs = t.where(signs == 0, t.ones_like(signs), signs)
-    return q * signs
-
-
 def pod(snapshots, r: int) -> ReducedBasis:
     """snapshots.py:72-89 — leading r left singular vectors, sign-fixed, with
-    the numerical-rank check (offline stage)."""
-    t = _dev.torch()
+    the numerical-rank check (adrom_pod)."""
     y = _dev.dev(snapshots)
     if y.dim() != 2:
         raise ValueError("snapshot matrix must be 2-d (one column per snapshot)")
     n, m = y.shape
     if r > min(n, m):
         raise DenseError(f"cannot extract {r} modes from a {n}x{m} matrix")
-    if not bool(t.isfinite(y).all()):
-        raise DenseError("thin_svd input contains non-finite entries")
-    if n >= m:
-        q, rr = t.linalg.qr(y)
-        if m <= 120:
-            from .dense import thin_svd
-            res = thin_svd(rr)
-            ur, s = res.u, res.s
-        else:
-            ur, s, _ = t.linalg.svd(rr)
-        u = q @ ur
-    else:
-        u, s, _ = t.linalg.svd(y, full_matrices=False)
-    rank = int((s > 1e-12 * s[0]).sum()) if float(s[0]) > 0 else 0
-    if r > rank:
-        raise DenseError(f"requested {r} modes but snapshot matrix has numerical rank {rank}")
-    phi = _fix_column_signs(u[:, :r]).contiguous()
-    sigma = s[:r].clone().contiguous()
+    phi = _dev.empty(n, r)
+    sigma = _dev.empty(r)
+    rank = C.c_int32(0)
+    Context.get().call("adrom_pod", ptr(y), C.c_int64(n), C.c_int32(m), C.c_int32(r), ptr(phi),
+                       ptr(sigma), None, C.byref(rank))
     return ReducedBasis(phi=_dev.like(phi, snapshots), sigma=_dev.like(sigma, snapshots))
+
+
+def pod_window(training, scaling: ScalingTransform, r: int) -> ReducedBasis:
+    """pod(column_stack(preprocess(q) for q in training), r) without forming
+    the N x m snapshot matrix twice (driver.py:298-299; adrom_pod_window)."""
+    tr = _dev.dev(training).contiguous()
+    m, n = tr.shape
+    nv = scaling.n_var
+    phi = _dev.empty(n, r)
+    sigma = _dev.empty(r)
+    rank = C.c_int32(0)
+    if r > min(n, m):
+        raise DenseError(f"cannot extract {r} modes from a {n}x{m} matrix")
+    Context.get().call("adrom_pod_window", ptr(tr), C.c_int32(m), C.c_int64(n), C.c_int32(nv),
+                       ptr(_dev.dev(scaling.q_ref)), ptr(_dev.dev(scaling.phi_norm)), C.c_int32(r),
+                       ptr(phi), ptr(sigma), None, C.byref(rank))
+    return ReducedBasis(phi=phi, sigma=sigma)

@@ -1,14 +1,18 @@
 """Device-resident basis tracking: ``ReducedBasis`` and the iSVD update.
 
 Mirrors ``/root/reference/pkg/src/adrom/tracking.py``: ``ReducedBasis``
-(51-64), ``UpdateRule`` (96-138), ``isvd_update`` (141-178).  The other
-five rules of the reference (wsvd/direct/onestep/oja/grouse) are outside
-the north-star path and are not provided.
+(51-64), ``SnapshotWindow`` (67-93), ``UpdateRule`` (96-138),
+``isvd_update`` (141-178) and the other five rules (181-246: wsvd, direct,
+onestep, oja, grouse).  The iSVD is the north-star path
+(its own fused kernels); the other rules are host-orchestrated chains of the
+library's dense kernels (Householder QR / orth, least squares, one-sided
+Jacobi SVD, FP64 tensor-core tall-skinny products).
 """
 
 from __future__ import annotations
 
 import ctypes as C
+from collections import deque
 from dataclasses import dataclass
 
 import numpy as np
@@ -16,9 +20,12 @@ import numpy as np
 from . import _dev
 from ._lib import Context, IsvdInfo, ptr
 
-__all__ = ["ReducedBasis", "UpdateRule", "isvd_update", "DEGENERATE_TOL", "last_isvd_info"]
+__all__ = ["ReducedBasis", "SnapshotWindow", "UpdateRule", "isvd_update", "wsvd_update",
+           "direct_update", "onestep_update", "oja_update", "grouse_update", "DEGENERATE_TOL",
+           "SKIP_TOL", "last_isvd_info"]
 
 DEGENERATE_TOL = 1e-12  # tracking.py:46
+SKIP_TOL = 1e-14        # tracking.py:48
 
 
 @dataclass(frozen=True)
@@ -41,9 +48,37 @@ class ReducedBasis:
         return float(np.linalg.norm(self.phi.T @ self.phi - np.eye(r)))
 
 
+class SnapshotWindow:
+    """tracking.py:67-93 — ring buffer of the most recent preprocessed
+    snapshots (device vectors), initialised from the last
+    ``min(capacity, available)`` offline snapshots."""
+
+    def __init__(self, capacity: int, initial=None):
+        if capacity < 1:
+            raise ValueError("window capacity must be at least 1")
+        self.capacity = int(capacity)
+        self._buf: deque = deque(maxlen=self.capacity)
+        init = list(initial) if initial is not None else []
+        for y in init[-self.capacity:]:
+            self._buf.append(_dev.dev(y).clone())
+
+    def push(self, y_hat) -> None:
+        self._buf.append(_dev.dev(y_hat).clone())
+
+    def __len__(self) -> int:
+        return len(self._buf)
+
+    @property
+    def matrix(self):
+        """N x len column matrix (device)."""
+        if not self._buf:
+            raise ValueError("snapshot window is empty")
+        return _dev.torch().stack(list(self._buf), dim=1).contiguous()
+
+
 @dataclass(frozen=True)
 class UpdateRule:
-    """tracking.py:96-138 (only ``isvd`` is implemented on the device)."""
+    """tracking.py:96-138."""
 
     kind: str
     lam: float = 1.0
@@ -116,6 +151,86 @@ def isvd_update(basis: ReducedBasis, y_hat, lam: float, r: int) -> ReducedBasis:
                       reorthogonalised=bool(info.reorthogonalised), sweeps=info.sweeps,
                       core_path=info.core_path)
     return ReducedBasis(phi=_dev.like(phi_out, basis.phi), sigma=_dev.like(sigma_out, basis.sigma))
+
+
+def wsvd_update(window: SnapshotWindow, r: int) -> ReducedBasis:
+    """tracking.py:181-186 — POD of the current window."""
+    from .snapshots import pod
+    return pod(window.matrix, r)
+
+
+def direct_update(basis: ReducedBasis, window: SnapshotWindow) -> ReducedBasis:
+    """tracking.py:189-203 — Phi' = Y (Phi^+ Y)^+, orthonormalised."""
+    from .dense import least_squares, pinv_cut, ts_apply, orth
+    from .errors import DenseError
+    t = _dev.torch()
+    y = window.matrix
+    phi = _dev.dev(basis.phi)
+    r = phi.shape[1]
+    if y.shape[1] < r:
+        raise DenseError(f"direct update needs at least {r} window columns, have {y.shape[1]}")
+    z = least_squares(phi, y)                     # r x w
+    phi_tilde = ts_apply(y, pinv_cut(z))          # N x r
+    q = orth(phi_tilde)
+    rdiag = ts_tn_diag(q, phi_tilde).abs()        # |diag(R)| of phi_tilde = Q R
+    if float(rdiag.min()) <= 1e-12 * max(float(rdiag.max()), 1e-300):
+        raise DenseError("direct update produced a rank-deficient basis")
+    return ReducedBasis(phi=_dev.like(q, basis.phi), sigma=_dev.like(_dev.dev(basis.sigma).clone(), basis.sigma))
+
+
+def ts_tn_diag(q, a):
+    """diag(Q^T A) on the tensor cores (the R diagonal of A = Q R)."""
+    from .dense import ts_tn
+    return ts_tn(q, a).diagonal()
+
+
+def onestep_update(basis: ReducedBasis, y_prev_hat, a_minus) -> ReducedBasis:
+    """tracking.py:206-216 — rank-one correction of the projection error of
+    the latest snapshot at the predicted reduced state (skipped when the
+    reduced state is numerically zero)."""
+    from .dense import orth, ts_apply
+    t = _dev.torch()
+    a = _dev.dev(a_minus)
+    denom = float(t.dot(a, a))
+    if denom < SKIP_TOL ** 2:
+        return basis
+    phi = _dev.dev(basis.phi)
+    resid = _dev.dev(y_prev_hat) - ts_apply(phi, a[:, None]).reshape(-1)
+    phi_new = orth(phi + t.outer(resid, a) / denom)
+    return ReducedBasis(phi=_dev.like(phi_new, basis.phi), sigma=_dev.like(_dev.dev(basis.sigma).clone(), basis.sigma))
+
+
+def oja_update(basis: ReducedBasis, y_prev_hat, eta: float) -> ReducedBasis:
+    """tracking.py:219-224 — Oja step + orthonormalisation."""
+    from .dense import orth, ts_tn
+    t = _dev.torch()
+    y = _dev.dev(y_prev_hat)
+    phi = _dev.dev(basis.phi)
+    yp = ts_tn(y[:, None], phi).reshape(-1)      # y^T Phi
+    phi_new = orth(phi + eta * t.outer(y, yp))
+    return ReducedBasis(phi=_dev.like(phi_new, basis.phi), sigma=_dev.like(_dev.dev(basis.sigma).clone(), basis.sigma))
+
+
+def grouse_update(basis: ReducedBasis, y_prev_hat, eta: float) -> ReducedBasis:
+    """tracking.py:227-246 — rank-one Grassmannian geodesic step (skipped
+    when the snapshot has no in-span part, no residual or zero weights)."""
+    import math
+    from .dense import least_squares, ts_apply
+    t = _dev.torch()
+    y = _dev.dev(y_prev_hat)
+    phi = _dev.dev(basis.phi)
+    w = least_squares(phi, y)
+    p = ts_apply(phi, w[:, None]).reshape(-1)
+    resid = y - p
+    pnorm = float(t.linalg.vector_norm(p))
+    rnorm = float(t.linalg.vector_norm(resid))
+    wnorm = float(t.linalg.vector_norm(w))
+    if min(pnorm, rnorm, wnorm) < SKIP_TOL:
+        return basis
+    alpha = eta * pnorm * rnorm
+    step = (math.cos(alpha) - 1.0) * p / pnorm + math.sin(alpha) * resid / rnorm
+    phi_new = phi + t.outer(step, w / wnorm)
+    return ReducedBasis(phi=_dev.like(phi_new, basis.phi), sigma=_dev.like(_dev.dev(basis.sigma).clone(), basis.sigma))
 
 
 class IsvdStream:

@@ -493,6 +493,112 @@ def io_artifacts():
     save("io_artifacts", **out)
 
 
+def dense_rules():
+    """Known answers of the dense helpers and the five non-iSVD update rules
+    (dense.py:75-200, snapshots.py:54-89, tracking.py:67-93, :181-246,
+    fom.py:222-236), from the reference's own functions on seeded inputs."""
+    from adrom import dense
+    rng = np.random.default_rng(2605)
+    out = {}
+    # least squares: tall full rank, matrix rhs, rank deficient (min norm)
+    a = rng.standard_normal((300, 7))
+    b = rng.standard_normal(300)
+    out["ls_a0"], out["ls_b0"], out["ls_x0"] = a, b, dense.least_squares(a, b)
+    bm = rng.standard_normal((300, 5))
+    out["ls_a1"], out["ls_b1"], out["ls_x1"] = a, bm, dense.least_squares(a, bm)
+    a2 = a.copy()
+    a2[:, 3] = 2.0 * a2[:, 1] - a2[:, 5]  # exactly dependent column
+    out["ls_a2"], out["ls_b2"], out["ls_x2"] = a2, b, dense.least_squares(a2, b)
+    # orth (sign-fixed thin QR)
+    a3 = rng.standard_normal((513, 9))
+    out["orth_a"], out["orth_q"] = a3, dense.orth(a3)
+    # pivoted QR pivots
+    a4 = rng.standard_normal((6, 40))
+    piv, q, r = dense.pivoted_qr(a4, 5)
+    out["pqr_a"], out["pqr_piv"] = a4, piv
+    # principal angles
+    u = np.linalg.qr(rng.standard_normal((200, 4)))[0]
+    v = np.linalg.qr(u + 1e-7 * rng.standard_normal((200, 4)))[0]
+    out["pa_u"], out["pa_v"], out["pa_theta"] = u, v, dense.principal_angles(u, v)
+    w = np.linalg.qr(rng.standard_normal((200, 3)))[0]
+    out["pa_w"], out["pa_theta2"] = w, dense.principal_angles(u, w)
+    # newton on a 2-d system
+    res_f = lambda x: np.array([x[0] ** 2 + x[1] ** 2 - 4.0, x[0] - x[1]])  # noqa: E731
+    jac_f = lambda x: np.array([[2 * x[0], 2 * x[1]], [1.0, -1.0]])  # noqa: E731
+    nr = dense.newton_solve(res_f, jac_f, np.array([1.0, 0.5]), 1e-12, 20)
+    out["newton_x"], out["newton_it"] = nr.x, np.array(nr.iterations)
+    # fit_scaling + pod: tall (Sod window), wide (Burgers), plain pod
+    m = fom.SodProblem(96)
+    st = [m.initial_state()]
+    stepper = fom.TimeStepper(dt=2e-3)
+    for _ in range(30):
+        st.append(fom.implicit_step(m, st[-1], 2e-3, stepper).x)
+    st = np.array(st)
+    sc = snapshots.fit_scaling(list(st), 3)
+    y = np.column_stack([sc.preprocess(q) for q in st])
+    bas = snapshots.pod(y, 6)
+    out["pod_train"], out["pod_qref"], out["pod_phinorm"] = st, sc.q_ref, sc.phi_norm
+    out["pod_phi"], out["pod_sigma"] = bas.phi, bas.sigma
+    yw = rng.standard_normal((40, 70)) @ np.diag(np.logspace(0, -8, 70)) @ rng.standard_normal((70, 90))
+    bw = snapshots.pod(yw, 12)
+    out["podw_y"], out["podw_phi"], out["podw_sigma"] = yw, bw.phi, bw.sigma
+    # rusanov flux on a batch
+    ul = np.abs(rng.standard_normal((50, 3))) + np.array([0.2, 0.0, 1.0])
+    ur = np.abs(rng.standard_normal((50, 3))) + np.array([0.2, 0.0, 1.0])
+    out["rus_ul"], out["rus_ur"], out["rus_f"] = ul, ur, fom.rusanov_flux(ul, ur, 1.4)
+    # the rules on one basis / window
+    n, r = 400, 5
+    phi = np.linalg.qr(rng.standard_normal((n, r)))[0]
+    sig = np.linspace(3.0, 1.0, r)
+    basis = tracking.ReducedBasis(phi, sig)
+    yy = [rng.standard_normal(n) + phi @ rng.standard_normal(r) for _ in range(8)]
+    win = tracking.SnapshotWindow(6, initial=yy[:7])
+    win.push(yy[7])
+    out["rule_phi"], out["rule_sig"], out["rule_win"] = phi, sig, win.matrix
+    out["rule_y"], out["rule_a"] = yy[7], rng.standard_normal(r)
+    out["wsvd_phi"] = tracking.wsvd_update(win, r).phi
+    out["wsvd_sig"] = tracking.wsvd_update(win, r).sigma
+    out["direct_phi"] = tracking.direct_update(basis, win).phi
+    out["onestep_phi"] = tracking.onestep_update(basis, yy[7], out["rule_a"]).phi
+    out["oja_phi"] = tracking.oja_update(basis, yy[7], 0.05).phi
+    out["grouse_phi"] = tracking.grouse_update(basis, yy[7], 0.05).phi
+    save("dense_rules", **out)
+
+
+def rule_loops():
+    """The adaptive loop with each non-iSVD rule and the every-step cadence
+    (driver.py:276-288, :346-387), real reference runs on small grids."""
+    U = tracking.UpdateRule
+    base = dict(model="burgers", n_elem=96, nu=0.01, dt=1e-3, n_t=70, r=4, n_s=6, w_init=10, z=5,
+                projection="lspg", sampling="qdeim", mode="adaptive")
+    cases = {
+        "rule_wsvd": dict(rule=U("wsvd", window=6)),
+        "rule_direct": dict(rule=U("direct", window=8)),
+        "rule_onestep": dict(rule=U("onestep")),
+        "rule_oja": dict(rule=U("oja", eta=0.05)),
+        "rule_grouse": dict(rule=U("grouse", eta=0.05)),
+        "rule_isvd_everystep": dict(rule=U("isvd", lam=0.5), cadence="every-step"),
+        "rule_oja_everystep_sod": dict(model="sod", n_elem=64, dt=5e-4, n_t=50, w_init=8, r=4, n_s=8,
+                                       sampling="fgs", n_extra=4, rule=U("oja", eta=0.02),
+                                       cadence="every-step"),
+    }
+    out = {}
+    for name, kw in cases.items():
+        cfg = driver.ExperimentConfig(**{**base, **kw})
+        truth = driver.run_fom(driver.ExperimentConfig(**{**cfg.__dict__, "mode": "fom"}))
+        res = driver.run_adaptive_rom(cfg, truth=truth.trajectory)
+        ev = [{k: (v if not isinstance(v, (np.bool_, bool)) else bool(v)) for k, v in e.items()}
+              for e in res.event_log]
+        out[name + "_cfg"] = np.array(json.dumps({k: (v.__dict__ if hasattr(v, "__dict__") else v)
+                                                  for k, v in {**base, **kw}.items()}))
+        out[name + "_truth"] = truth.trajectory
+        out[name + "_traj"] = res.trajectory
+        out[name + "_errors"] = res.errors
+        out[name + "_sig_errors"] = res.signal_errors
+        out[name + "_events"] = np.array(json.dumps(ev, default=float))
+    save("rule_loops", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["residuals", "jacobians", "newton", "isvd", "sampling_cases",
                              "rom_steps", "loops"]
