@@ -518,7 +518,7 @@ int pod_core(adrom_ctx* ctx, double* Y, int64_t N, int m, int r, double* phi, do
   double* A = Y;
   if (!tall) {  // A = Y^T (column-major m x N) = Y row-major ... transpose
     A = yt.d();
-    dim3 g((unsigned)((N + 31) / 32), (unsigned)((m + 31) / 32));
+    dim3 g((unsigned)((m + 31) / 32), (unsigned)((N + 31) / 32));  // (rows = m) x (cols = N)
     // Y column-major N x m == row-major m x N; A column-major m x N needs
     // A[j m + i] = Y[i N + j]: the transpose of the row-major m x N array
     transpose_kernel<<<g, dim3(32, 8), 0, ctx->stream>>>(Y, m, (int)N, A, m);

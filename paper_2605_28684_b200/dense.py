@@ -171,7 +171,8 @@ def pivoted_qr(a, k: int):
     if k > kk:
         raise DenseError(f"pivoted_qr: matrix has at most rank {kk}, cannot select {k} pivots")
     idx = _dev.empty(kk, dtype=t.int64)
-    Context.get().call("adrom_qdeim", ptr(ad.T.contiguous()), C.c_int64(n), C.c_int32(m),
+    at = ad.T.contiguous()
+    Context.get().call("adrom_qdeim", ptr(at), C.c_int64(n), C.c_int32(m),
                        C.c_int32(kk), ptr(idx))
     rest = t.ones(n, dtype=t.bool, device="cuda")
     rest[idx] = False

@@ -336,7 +336,8 @@ def state_errors(model: FomProblem, pred, truth, out=None):
     ctx = Context.get()
     o = out if out is not None else t.empty(model.n_var, dtype=t.float64, device="cuda")
     mabi = model.abi()
-    ctx.call("adrom_state_errors", C.byref(mabi), ptr(_dev.dev(pred)), ptr(_dev.dev(truth)), ptr(o))
+    pd, td = _dev.dev(pred), _dev.dev(truth)  # keep both device copies alive across the call
+    ctx.call("adrom_state_errors", C.byref(mabi), ptr(pd), ptr(td), ptr(o))
     return o
 
 

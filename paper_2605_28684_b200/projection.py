@@ -132,7 +132,8 @@ def encode(q, op: RomOperator, n: int = 0) -> ReducedState:
     nn, r = phi.shape
     a = _dev.empty(r)
     q_ref, d = _dev.dev(op.scaling.q_ref), _dev.dev(op.scaling.row_scale)
-    Context.get().call("adrom_encode", ptr(phi), ptr(q_ref), ptr(d), ptr(_dev.dev(q)),
+    qd = _dev.dev(q)
+    Context.get().call("adrom_encode", ptr(phi), ptr(q_ref), ptr(d), ptr(qd),
                        C.c_int64(nn), C.c_int32(r), ptr(a))
     return ReducedState(a=_dev.like(a, q), n=n)
 
@@ -143,7 +144,8 @@ def decode(state: ReducedState, op: RomOperator):
     nn, r = phi.shape
     out = _dev.empty(nn)
     q_ref, d = _dev.dev(op.scaling.q_ref), _dev.dev(op.scaling.row_scale)
-    Context.get().call("adrom_decode", ptr(phi), ptr(q_ref), ptr(d), ptr(_dev.dev(state.a)),
+    ad = _dev.dev(state.a)
+    Context.get().call("adrom_decode", ptr(phi), ptr(q_ref), ptr(d), ptr(ad),
                        C.c_int64(nn), C.c_int32(r), ptr(out))
     return _dev.like(out, state.a)
 

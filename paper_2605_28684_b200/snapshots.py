@@ -100,7 +100,8 @@ def pod_window(training, scaling: ScalingTransform, r: int) -> ReducedBasis:
     rank = C.c_int32(0)
     if r > min(n, m):
         raise DenseError(f"cannot extract {r} modes from a {n}x{m} matrix")
+    q_ref, phi_norm = _dev.dev(scaling.q_ref), _dev.dev(scaling.phi_norm)  # alive across the call
     Context.get().call("adrom_pod_window", ptr(tr), C.c_int32(m), C.c_int64(n), C.c_int32(nv),
-                       ptr(_dev.dev(scaling.q_ref)), ptr(_dev.dev(scaling.phi_norm)), C.c_int32(r),
+                       ptr(q_ref), ptr(phi_norm), C.c_int32(r),
                        ptr(phi), ptr(sigma), None, C.byref(rank))
     return ReducedBasis(phi=phi, sigma=sigma)

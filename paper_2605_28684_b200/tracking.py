@@ -252,7 +252,8 @@ class IsvdStream:
         h = C.c_void_p()
         self._ctx.call("adrom_isvd_stream_create", C.c_int64(self.n), C.c_int32(self.r), C.byref(h))
         self._h = h
-        self._ctx.scall("adrom_isvd_stream_load", self._h, ptr(phi), ptr(_dev.dev(basis.sigma)))
+        sig = _dev.dev(basis.sigma)
+        self._ctx.scall("adrom_isvd_stream_load", self._h, ptr(phi), ptr(sig))
 
     def update(self, y_hat, lam: float) -> dict:
         y = _dev.dev(y_hat)

@@ -43,10 +43,11 @@ def oracle_setup(n: int, steps: int):
     return case, ocfg, training, q_ref, phi_norm, d, phi0, sigma0
 
 
-def oracle_run(setup, steps, nudge_seed=None):
+def oracle_run(setup, steps, nudge_seed=None, pinned=None, nudge_ulps=1.0):
     case, ocfg, training, q_ref, phi_norm, d, phi0, sigma0 = setup
     return online.run_online(ocfg, training, q_ref, d, phi0, sigma0, keep_stride=1,
-                             n_steps=steps, nudge_seed=nudge_seed)
+                             n_steps=steps, nudge_seed=nudge_seed, pinned_samplings=pinned,
+                             nudge_ulps=nudge_ulps)
 
 
 def envelope(setup, steps, ref, seeds=(1, 2, 3)):
@@ -64,7 +65,7 @@ def envelope(setup, steps, ref, seeds=(1, 2, 3)):
     return env_s, env_sig
 
 
-def gpu_run(setup, steps, stepwise=True):
+def gpu_run(setup, steps, stepwise=True, keep_phi_at=()):
     """The device session from the oracle's offline results; returns the
     decoded state, iteration count, sampled rows and sigma of every step."""
     import torch
@@ -80,12 +81,15 @@ def gpu_run(setup, steps, stepwise=True):
     out = torch.empty((steps, model.n_dof), dtype=torch.float64, device="cuda")
     samp = [sess.sampling().cpu().numpy().copy()]
     sig = []
+    phis = {}
     if stepwise:
         for k in range(steps):
             sess.advance(1, 1, out[k:k + 1], None)
             _, _, _, s, _ = sess.read(1, 1)
             sig.append(s.cpu().numpy().copy())
             samp.append(sess.sampling().cpu().numpy().copy())
+            if k + 1 in keep_phi_at:
+                phis[k + 1] = sess.basis().cpu().numpy()
     else:
         sess.advance(steps, 1, out, None)
     sess.finish()
@@ -95,7 +99,8 @@ def gpu_run(setup, steps, stepwise=True):
     return dict(traj=out.cpu().numpy(), it=log[:, 1].astype(int).copy(),
                 conv=log[:, 0].copy(),
                 coarse=[int(e.coarse_iterations) for e in ev],
-                errors=[int(e.error) for e in ev], sig=np.array(sig), samp=samp, phi=phi)
+                errors=[int(e.error) for e in ev], sig=np.array(sig), samp=samp, phi=phi,
+                phis=phis)
 
 
 def restart_parity(setup, steps_at, n_steps=2):
