@@ -34,6 +34,8 @@ def main(n=1 << 16, steps=200):
         dev = np.linalg.norm(g["traj"] - np.array(rec.states), axis=1) / np.linalg.norm(np.array(rec.states), axis=1)
         print(f"restart at step {k}: its gpu {g['it']} oracle {rec.iterations} dev {dev} "
               f"samp equal {[np.array_equal(np.sort(a), np.sort(b)) for a, b in zip(g['samp'], rec.samplings)]}")
+        if k != bad[0]:
+            continue  # one case travels back (gpurun_out <= 64 MiB)
         np.savez_compressed(ROOT / "gpurun_out" / f"cfg3_badstep_{k}.npz", phi=phi_s, sigma=sig_s, q=q_s,
                             its_gpu=g["it"], its_ref=np.array(rec.iterations), traj_gpu=g["traj"],
                             traj_ref=np.array(rec.states), a_ref=np.array(rec.reduced),
