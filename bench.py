@@ -491,7 +491,6 @@ def bench_rom(args, rank, world):
     sess.advance(W)
     torch.cuda.synchronize()
     barrier(world)
-    ctx.prof_enable(True)
     l0 = ctx.launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     prof_timed = os.environ.get("ADROM_PROFILE_TIMED") == "1"  # ncu --profile-from-start off
@@ -506,16 +505,28 @@ def bench_rom(args, rank, world):
         if prof_timed:
             torch.cuda.cudart().cudaProfilerStop()
     launches = ctx.launches() - l0
+    ms = max_over_ranks(ev0.elapsed_time(ev1), world)
+    # kernel breakdown: the same number of further steps with the CUDA-event
+    # probes on (they add a record pair per probe, so the timed region above
+    # runs without them); shares are relative to this probed stretch
+    kp = min(K, case.n_t - case.w_init - W - K)
+    ctx.prof_enable(True)
+    ep0, ep1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ep0.record()
+    if kp > 0:
+        sess.advance(kp)
+    ep1.record()
+    torch.cuda.synchronize()
     probes = ctx.prof_read()
     ctx.prof_enable(False)
+    ms_probed = ep0.elapsed_time(ep1) if kp > 0 else ms
     log, events, *_ = sess.read(W + K, W + K)
     sess.close()
-    ms = max_over_ranks(ev0.elapsed_time(ev1), world)
     barrier(world)
     ms_step = ms / K
     value = world * K / (ms * 1e-3)
     per = {k: (v[0] / max(v[1], 1), v[1]) for k, v in probes.items()}
-    share = {k: round(v[0] / ms, 4) for k, v in probes.items()}
+    share = {k: round(v[0] / ms_probed, 4) for k, v in probes.items()}
     # Roofline.  Explicit basis (r not in {32, 64} or small N): the iSVD
     # rotation Phi' = [Phi | q_hat] B (rot_tc_kernel, FP64 DMMA), 2 N r (r+1)
     # flop.  Factored basis (csrc/factored.cu, the cfg-3 path): no rotation;
@@ -538,9 +549,9 @@ def bench_rom(args, rank, world):
         roof = roofline(dbytes, per["decode"][0], ncu_traffic("stream_kernel<128, 1, 1, 0>", case.name))
         roof.update({"kernel": "decode (stream_kernel<128>: q_ref + Phi a / d)",
                      "work_per_launch": {"bytes": dbytes},
-                     "share_of_step": round(probes["decode"][0] / ms, 4),
+                     "share_of_step": round(probes["decode"][0] / ms_probed, 4),
                      "dominant_kernel": {"name": "bl_dir_kernel<reacting> (FD directions, FP64 pipe)",
-                                         "share_of_step": round(probes.get("rom_step", (0, 0))[0] / ms, 4),
+                                         "share_of_step": round(probes.get("rom_step", (0, 0))[0] / ms_probed, 4),
                                          "note": "rom_step share; ncu: FP64 pipe 24 % active, "
                                                  "profiles/r1_cfg4_lspg_kernels_full.txt"}})
     elif "isvd_rotate" in per:
@@ -555,17 +566,17 @@ def bench_rom(args, rank, world):
                 "work_per_launch": {"flops": flops, "bytes": rbytes},
                 "hbm_achieved_gbs": round(rbytes / (rot_ms * 1e-3) / 1e9, 1),
                 "hbm_frac": round(rbytes / (rot_ms * 1e-3) / 1e9 / HBM_PEAK, 4),
-                "share_of_step": round(probes["isvd_rotate"][0] / ms, 4)}
+                "share_of_step": round(probes["isvd_rotate"][0] / ms_probed, 4)}
     elif "isvd_project" in per:
         kq = 16
-        k_mean = float(np.mean([(j % kq) for j in range(W, W + K)])) if case.z == 1 else 0.0
+        k_mean = float(np.mean([(j % kq) for j in range(W + K, W + K + max(kp, 1))])) if case.z == 1 else 0.0
         xbytes = 8.0 * N * (r + k_mean + 3)
         roof = roofline(xbytes, per["isvd_project"][0],
                         ncu_traffic("xpass_tma_kernel<64, 1>", case.name))
         roof.update({"kernel": "isvd_project (xpass_tma_kernel<64,1>: X^T y + exact row norms, "
                                "TMA-staged row tiles)",
                      "work_per_launch": {"bytes": xbytes, "k_mean": k_mean},
-                     "share_of_step": round(probes["isvd_project"][0] / ms, 4)})
+                     "share_of_step": round(probes["isvd_project"][0] / ms_probed, 4)})
     isvd_keys = ("isvd_project", "isvd_resid", "isvd_core", "isvd_rotate")
     n_upd = max(probes.get("isvd_project", (0, 1))[1], 1)
     isvd_ms = sum(probes.get(k, (0, 0))[0] for k in isvd_keys) / n_upd
@@ -599,7 +610,10 @@ def bench_rom(args, rank, world):
         "share_of_step": share,
         "setup_s": {"offline": round(t_off, 3), "start": round(t_start, 3)},
         "rom_iterations_mean": float(np.mean(log[:, 1])) if len(log) else None,
-        "qdeim_rounds_per_step": round(probes.get("qdeim_round", (0, 0))[1] / K, 2),
+        "qdeim_rounds_per_step": round(probes.get("qdeim_round", (0, 0))[1] / max(kp, 1), 2),
+        "probed_steps": {"steps": kp, "ms_per_step": round(ms_probed / max(kp, 1), 4),
+                         "note": "kernel breakdown from a second stretch with CUDA-event probes on; "
+                                 "the timed region runs without them"},
         "event_errors": sum(1 for e in events if e.error),
     }
     line["clocks"] = clk.summary()
