@@ -100,6 +100,35 @@ __device__ __forceinline__ double warp_colnorm2(const double* col, int k, int r,
   return (w[0] + w[2]) + (w[1] + w[3]);
 }
 
+// C (column-major, C[l * ldc + k]) = A B for A (M x K, row-major lda) and B
+// (K x N, row-major ldb), M, N <= 128: the whole block, one warp per 8 x 8
+// output tile on the FP64 tensor cores (mma.sync m8n8k4), K in steps of 4
+// with zero fill past K.  Operands in shared or global memory.
+__device__ __forceinline__ void block_dmma_gemm(const double* A, int lda, const double* B, int ldb,
+                                                int M, int N, int K, double* C, int ldc) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int tm = (M + 7) >> 3, tn = (N + 7) >> 3;
+  const int fr = lane >> 2, fk = lane & 3;
+  for (int t = warp; t < tm * tn; t += nw) {
+    const int i0 = 8 * (t / tn), j0 = 8 * (t % tn);
+    const int ar = i0 + fr, bc = j0 + fr;
+    double d0 = 0.0, d1 = 0.0;
+    for (int k0 = 0; k0 < K; k0 += 4) {
+      const int kk = k0 + fk;
+      const double a = (ar < M && kk < K) ? A[(size_t)ar * lda + kk] : 0.0;
+      const double b = (kk < K && bc < N) ? B[(size_t)kk * ldb + bc] : 0.0;
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(d0), "+d"(d1)
+                   : "d"(a), "d"(b));
+    }
+    const int orow = i0 + fr, oc = j0 + 2 * fk;
+    if (orow < M) {
+      if (oc < N) C[(size_t)oc * ldc + orow] = d0;
+      if (oc + 1 < N) C[(size_t)(oc + 1) * ldc + orow] = d1;
+    }
+  }
+}
+
 __device__ bool block_qr_certified_solve(double* jA, int ld, int r, double* rhs, double* out,
                                          double* vbuf, double* red, double cert_bound = LS_CERT) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
@@ -132,9 +161,9 @@ __device__ bool block_qr_certified_solve(double* jA, int ld, int r, double* rhs,
     for (int j = k + 1 + warp; j <= r; j += nw) {
       double* cj = (j < r) ? jA + (size_t)j * ld : rhs;
       double s = 0.0;
-      for (int i = k + lane; i < r; i += 32) s += col[i] * cj[i];
+      for (int i = k + lane; i < r; i += 32) s = fma(col[i], cj[i], s);
       s = warp_sum(s) * beta;
-      for (int i = k + lane; i < r; i += 32) cj[i] -= s * col[i];
+      for (int i = k + lane; i < r; i += 32) cj[i] = fma(-s, col[i], cj[i]);
       if (j == k + 1 && j < r) {
         __syncwarp();
         const double a1 = warp_colnorm2(cj, j, r, lane);
@@ -158,33 +187,31 @@ __device__ bool block_qr_certified_solve(double* jA, int ld, int r, double* rhs,
   rf = block_sum_dyn(rf, red);
   double inv2 = 0.0;
   bool bad = false;
-  for (int c = warp; c < r; c += nw) {
-    // lane holds b_j for j = lane + 32 t (t < 4, r <= 128)
-    double b[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) b[t] = (lane + 32 * t == c) ? 1.0 : 0.0;
-    for (int i = c; i >= 0; --i) {
-      const int ti = i >> 5, li = i & 31;
-      double bi = 0.0;
-#pragma unroll
-      for (int t = 0; t < 4; ++t)
-        if (t == ti) bi = b[t];
-      bi = __shfl_sync(0xffffffffu, bi, li);
+  // ||R^{-1}||_F: thread per column c of R^{-1} (R x = e_c, back
+  // substitution), x_i (i < c) kept in the free strictly-lower triangle of
+  // the R storage, at row c of column i (consecutive threads, consecutive
+  // addresses); x_c = 1 / R_cc in a register.  R (upper triangle + diagonal)
+  // is only read.
+  __syncthreads();
+  for (int c = tid; c < r; c += blockDim.x) {
+    const double dc = jA[(size_t)c * ld + c];
+    double xc = 0.0;
+    if (dc == 0.0) bad = true;
+    else xc = 1.0 / dc;
+    inv2 += xc * xc;
+    for (int i = c - 1; i >= 0; --i) {
+      double acc = -jA[(size_t)c * ld + i] * xc;           // j = c term
+      for (int j = i + 1; j < c; ++j) acc = fma(-jA[(size_t)j * ld + i], jA[(size_t)j * ld + c], acc);
       const double d = jA[(size_t)i * ld + i];
       double xi;
       if (d == 0.0) {
         bad = true;
         xi = 0.0;
       } else {
-        xi = bi / d;
+        xi = acc / d;
       }
-      if (lane == 0) inv2 += xi * xi;
-      const double* col = jA + (size_t)i * ld;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int j = lane + 32 * t;
-        if (j < i) b[t] -= col[j] * xi;
-      }
+      jA[(size_t)i * ld + c] = xi;  // row c > i of column i: strictly lower
+      inv2 += xi * xi;
     }
   }
   inv2 = block_sum_dyn(inv2, red);
@@ -303,25 +330,9 @@ __global__ void __launch_bounds__(512) lspg_kernel(RomStepArgs A) {
       test[e] = A.op.phi_s[e] - A.dt * (A.op.d_s[j] * df);
     }
     __syncthreads();
-    // jac = pinv @ test -> stored column-major in jA; thread per entry
-    // (consecutive threads: consecutive l, coalesced rows of test).  The sum
-    // keeps the 32-lane strided + butterfly order of a warp reduction.
-    for (int o = tid; o < r * r; o += blockDim.x) {
-      const int k = o / r, l = o - k * r;
-      const double* pk = pinv + (int64_t)k * n_s;
-      double v[32];
-#pragma unroll
-      for (int q = 0; q < 32; ++q) {
-        double t = 0.0;
-        for (int j = q; j < n_s; j += 32) t += pk[j] * test[j * r + l];
-        v[q] = t;
-      }
-#pragma unroll
-      for (int w = 16; w > 0; w >>= 1)
-#pragma unroll
-        for (int q = 0; q < w; ++q) v[q] = v[q] + v[q + w];
-      jA[l * ld + k] = v[0];
-    }
+    // jac = pinv @ test (r x n_s times n_s x r) on the FP64 tensor cores,
+    // stored column-major in jA
+    block_dmma_gemm(pinv, n_s, test, r, r, r, n_s, jA, ld);
     __syncthreads();
     // grad = jac^T rho
     double g2 = 0.0;
