@@ -218,6 +218,14 @@ __device__ __forceinline__ Cons sod_face(const Cons& l, const SodQ& ql, const Co
   return f;
 }
 constexpr int SODW_NT = 256;
+constexpr int SODW_CELLS = 30;  // output cells per warp chunk (lanes 1..30; 0 and 31 are halo)
+// Lane l of a chunk holds cell c0 - 1 + l (clamped to the grid: the clamp IS
+// the zero-gradient ghost copy of fom.py:267), so every lane evaluates its
+// primitives / physical flux once, faces come from the right neighbour by a
+// shuffle, and no lane runs a divergent halo branch (the former 32-cell form
+// recomputed the halo cells' primitives in lanes 0 and 31, tripling the
+// FP64 latency chain).  Halo cells are evaluated by both neighbouring chunks
+// (2 of 32 lanes): the same operations on the same operands, bitwise.
 template <int MODE>
 __global__ void __launch_bounds__(SODW_NT) sod_rhs_warp_kernel(
     const double* __restrict__ q, double* __restrict__ out, int64_t n, double dx, double gamma,
@@ -225,18 +233,17 @@ __global__ void __launch_bounds__(SODW_NT) sod_rhs_warp_kernel(
     int* __restrict__ flag) {
   __shared__ double red[SODW_NT / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t nchunks = (n + 31) / 32;
+  const int64_t nchunks = (n + SODW_CELLS - 1) / SODW_CELLS;
   const int64_t wstride = (int64_t)gridDim.x * (SODW_NT / 32);
   double acc = 0.0;
   bool bad = false;
   constexpr unsigned FULL = 0xffffffffu;
   for (int64_t ch = (int64_t)blockIdx.x * (SODW_NT / 32) + warp; ch < nchunks; ch += wstride) {
-    const int64_t c = ch * 32 + lane;
-    const bool valid = c < n;
-    const int64_t cc = valid ? c : n - 1;
+    const int64_t c = ch * SODW_CELLS - 1 + lane;  // this lane's cell (unclamped)
+    const int64_t cc = c < 0 ? 0 : (c > n - 1 ? n - 1 : c);
     const Cons u = load_cons(q, cc);
     const SodQ qu = sod_q(u, gamma);
-    // right neighbour (zero-gradient ghost at the end: fom.py:267)
+    // face between this lane's cell and the next lane's
     Cons ur;
     SodQ qr;
     ur.m0 = __shfl_down_sync(FULL, u.m0, 1);
@@ -246,25 +253,13 @@ __global__ void __launch_bounds__(SODW_NT) sod_rhs_warp_kernel(
     qr.f1 = __shfl_down_sync(FULL, qu.f1, 1);
     qr.f2 = __shfl_down_sync(FULL, qu.f2, 1);
     qr.a = __shfl_down_sync(FULL, qu.a, 1);
-    if (cc + 1 >= n) {
-      ur = u;
-      qr = qu;
-    } else if (lane == 31) {
-      ur = load_cons(q, cc + 1);
-      qr = sod_q(ur, gamma);
-    }
-    const Cons fr = sod_face(u, qu, ur, qr);
+    const Cons fr = sod_face(u, qu, ur, qr);  // lane 31: unused
     Cons fl;
     fl.m0 = __shfl_up_sync(FULL, fr.m0, 1);
     fl.m1 = __shfl_up_sync(FULL, fr.m1, 1);
     fl.m2 = __shfl_up_sync(FULL, fr.m2, 1);
-    if (lane == 0) {
-      const int64_t li = cc == 0 ? 0 : cc - 1;
-      const Cons ul = load_cons(q, li);
-      fl = sod_face(ul, sod_q(ul, gamma), u, qu);
-    }
-    Cons o = sod_cell_from_faces(fl, fr, dx);
-    if (valid) {
+    if (lane >= 1 && lane <= SODW_CELLS && c < n) {
+      Cons o = sod_cell_from_faces(fl, fr, dx);
       if (MODE == 1) {
         o.m0 = (u.m0 - qprev[3 * c]) - dt * o.m0;
         o.m1 = (u.m1 - qprev[3 * c + 1]) - dt * o.m1;
@@ -560,7 +555,7 @@ static int launch_residual(adrom_ctx* ctx, const adrom_model& m, const double* x
       burgers_rhs_kernel<0><<<nb, BURG_NT, 0, ctx->stream>>>(x, out, m.n_elem, burgers_params(m),
                                                             nullptr, 0.0, nullptr, nullptr);
   } else {
-    nb = grid_for(ctx, m.n_elem, SODW_NT);
+    nb = grid_for(ctx, m.n_elem, (SODW_NT / 32) * SODW_CELLS);
     if (newton)
       sod_rhs_warp_kernel<1><<<nb, SODW_NT, 0, ctx->stream>>>(x, out, m.n_elem, m.dx, m.gamma,
                                                             qprev, dt, partial, flag);

@@ -98,25 +98,56 @@ class RomOperator:
     def phi_sampled(self):
         return _dev.host(self._buf["phi_s"][: self._n_s * self._r].reshape(self._n_s, self._r))
 
+    # The device kernels gather through the stencil closure of the sampled
+    # rows (sampling.py:178-189).  A caller-supplied closure that is a strict
+    # superset of it (projection.py:73-79 takes sampling.closure verbatim)
+    # changes nothing the operator computes, only these arrays' extent, so
+    # the views are then formed from sampling.closure like the reference's.
+    def _user_closure(self):
+        clo = np.asarray(self.sampling.closure, dtype=np.int64)
+        dev_clo = _dev.host(self._buf["closure"][: self._n_c])
+        return None if np.array_equal(clo, dev_clo) else clo
+
     @property
     def closure(self):
-        return _dev.host(self._buf["closure"][: self._n_c])
+        clo = self._user_closure()
+        return clo if clo is not None else _dev.host(self._buf["closure"][: self._n_c])
 
     @property
     def q_ref_closure(self):
+        clo = self._user_closure()
+        if clo is not None:
+            return np.asarray(_dev.host(self.scaling.q_ref))[clo]
         return _dev.host(self._buf["q_ref_c"][: self._n_c])
 
     @property
     def dinv_phi_closure(self):
+        clo = self._user_closure()
+        if clo is not None:
+            d = np.asarray(_dev.host(self.scaling.row_scale))
+            return np.asarray(_dev.host(self.basis.phi))[clo, :] / d[clo][:, None]
         return _dev.host(self._buf["dinv_phi_c"][: self._n_c * self._r].reshape(self._n_c, self._r))
 
     @property
     def sample_pos(self):
+        clo = self._user_closure()
+        if clo is not None:
+            return np.searchsorted(clo, np.asarray(self.sampling.indices))
         return _dev.host(self._buf["sample_pos"][: self._n_s])
 
     def decode_closure(self, a):
-        """projection.py:86-87 (on the device closure)."""
-        qc =self._buf["q_ref_c"][: self._n_c] + \
+        """projection.py:86-87 (on the device closure, or on a caller-supplied
+        superset closure)."""
+        clo = self._user_closure()
+        if clo is not None:
+            t = _dev.torch()
+            ci = t.from_numpy(clo).cuda()
+            d = _dev.dev(self.scaling.row_scale)[ci]
+            dphi = _dev.dev(self.basis.phi)[ci] / d[:, None]
+            from .dense import ts_apply
+            qc = _dev.dev(self.scaling.q_ref)[ci] + ts_apply(dphi.contiguous(), _dev.dev(a)[:, None]).reshape(-1)
+            return _dev.like(qc, a)
+        qc = self._buf["q_ref_c"][: self._n_c] + \
             self._buf["dinv_phi_c"][: self._n_c * self._r].reshape(self._n_c, self._r) @ _dev.dev(a)
         return _dev.like(qc, a)
 

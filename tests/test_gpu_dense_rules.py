@@ -197,3 +197,32 @@ def test_rule_loops_vs_reference(golden, name):
         assert ("update_error" in a) == ("update_error" in b)
         assert a.get("coarse_iterations") == b.get("coarse_iterations")
         assert np.isclose(a["residual_norm"], b["residual_norm"], rtol=1e-6, atol=1e-11)
+
+
+def test_operator_with_superset_closure():
+    """projection.py:73-79 takes sampling.closure verbatim: a caller closure
+    larger than the stencil closure changes the operator's closure arrays
+    (shape, sample_pos) but nothing it computes."""
+    import paper_2605_28684_b200 as P
+    rng = np.random.default_rng(9)
+    n = 64
+    m = P.BurgersProblem(n, nu=0.01)
+    phi = np.linalg.qr(rng.standard_normal((n, 4)))[0]
+    basis = P.ReducedBasis(phi, np.ones(4))
+    sc = P.ScalingTransform(q_ref=m.initial_state(), phi_norm=np.ones(1))
+    s0 = P.stencil_closure(P.SamplingSet(indices=np.array([5, 20, 33, 50]),
+                                         closure=np.array([5, 20, 33, 50])), m)
+    big = P.SamplingSet(indices=s0.indices, closure=np.unique(np.concatenate([s0.closure, [0, 1, 63]])))
+    op0 = P.build_rom_operator(basis, sc, s0, m, "lspg")
+    op1 = P.build_rom_operator(basis, sc, big, m, "lspg")
+    assert np.array_equal(op1.closure, big.closure)
+    assert np.array_equal(op1.closure[op1.sample_pos], big.indices)
+    a = rng.standard_normal(4)
+    d1 = np.asarray(op1.decode_closure(a))
+    d0 = np.asarray(op0.decode_closure(a))
+    pos = np.searchsorted(op1.closure, op0.closure)
+    assert np.allclose(d1[pos], d0, rtol=1e-13, atol=1e-15)
+    st = P.ReducedState(a=a, n=0)
+    r0 = P.rom_step(op0, m, st, 1e-3)
+    r1 = P.rom_step(op1, m, st, 1e-3)
+    assert np.array_equal(np.asarray(r0.state.a), np.asarray(r1.state.a))
