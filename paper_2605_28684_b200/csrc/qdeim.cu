@@ -49,12 +49,6 @@ static long long qp_refresh_factor() {
   return t;
 }
 
-// sampled threshold selection before the radix passes (ADROM_QDEIM_RADIX=1: off)
-static bool qs_sampled_select() {
-  static const bool v = getenv("ADROM_QDEIM_RADIX") == nullptr;
-  return v;
-}
-
 // refresh-set capacity over its target, in percent (the selection stops once
 // the rows sharing the selected bound prefix fit); ADROM_QDEIM_CAPF overrides
 static long long qp_refresh_slack() {
@@ -296,103 +290,6 @@ __global__ void __launch_bounds__(1024) qs_digit_kernel(SelState* st, int shift,
       st->done = 1;
     }
   }
-}
-
-// Sampled selection (tried before the radix passes, which then no-op): a
-// deterministic stride sample of QS_SAMPLES keys, sorted in one block, gives
-// QS_NCAND thresholds whose expected counts spread over [M, cap]; one counting
-// pass measures all of them and the tightest one with M <= count <= cap is
-// taken (theta = its key, tau = the largest value below it: every row left
-// outside is bounded by tau, which is all the certification needs).  If no
-// candidate fits (heavy ties, tiny sets) the radix select runs as before.
-constexpr int QS_SAMPLES = 4096, QS_NCAND = 8;
-
-__global__ void __launch_bounds__(1024) qs_sample_kernel(const double* __restrict__ vals, int64_t n,
-                                                         long long M, long long cap,
-                                                         unsigned long long* __restrict__ cand) {
-  __shared__ unsigned long long sk[QS_SAMPLES];
-  const int tid = threadIdx.x;
-  if (n < 16 * (int64_t)QS_SAMPLES || cap < M) {
-    if (tid < 2 * QS_NCAND) cand[tid] = 0ull;  // disabled: radix path
-    return;
-  }
-  const int64_t stride = n / QS_SAMPLES;
-  for (int i = tid; i < QS_SAMPLES; i += blockDim.x) sk[i] = qp_key(vals[(int64_t)i * stride + stride / 2]);
-  __syncthreads();
-  // bitonic sort, descending
-  for (int k = 2; k <= QS_SAMPLES; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = tid; i < QS_SAMPLES; i += blockDim.x) {
-        const int l = i ^ j;
-        if (l > i) {
-          const unsigned long long a = sk[i], b = sk[l];
-          const bool desc = (i & k) == 0;
-          if (desc ? (a < b) : (a > b)) {
-            sk[i] = b;
-            sk[l] = a;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  if (tid < QS_NCAND) {
-    // expected count of keys >= sk[rank] is (rank + 1) * stride
-    const double target = (double)M + (double)(cap - M) * (tid + 1.0) / (QS_NCAND + 1.0);
-    long long rank = (long long)(target / (double)stride) - 1;
-    if (rank < 0) rank = 0;
-    if (rank > QS_SAMPLES - 1) rank = QS_SAMPLES - 1;
-    cand[tid] = sk[rank];
-    cand[QS_NCAND + tid] = 0ull;
-  }
-}
-
-__global__ void __launch_bounds__(256) qs_count_kernel(const double* __restrict__ vals, int64_t n,
-                                                       unsigned long long* __restrict__ cand) {
-  __shared__ unsigned long long th[QS_NCAND];
-  __shared__ unsigned int bc[QS_NCAND];
-  if (threadIdx.x < QS_NCAND) {
-    th[threadIdx.x] = cand[threadIdx.x];
-    bc[threadIdx.x] = 0u;
-  }
-  __syncthreads();
-  if (th[0] == 0ull) return;
-  unsigned int c[QS_NCAND];
-#pragma unroll
-  for (int q = 0; q < QS_NCAND; ++q) c[q] = 0u;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const unsigned long long k = qp_key(vals[i]);
-#pragma unroll
-    for (int q = 0; q < QS_NCAND; ++q) c[q] += (k >= th[q]) ? 1u : 0u;
-  }
-#pragma unroll
-  for (int q = 0; q < QS_NCAND; ++q) {
-    const unsigned int w = __reduce_add_sync(0xffffffffu, c[q]);
-    if ((threadIdx.x & 31) == 0 && w) atomicAdd(&bc[q], w);
-  }
-  __syncthreads();
-  if (threadIdx.x < QS_NCAND && bc[threadIdx.x])
-    atomicAdd(&cand[QS_NCAND + threadIdx.x], (unsigned long long)bc[threadIdx.x]);
-}
-
-__global__ void qs_pick_kernel(SelState* st, long long cap, const unsigned long long* __restrict__ cand) {
-  if (threadIdx.x != 0 || cand[0] == 0ull) return;
-  const long long need = st->need;
-  int best = -1;
-  unsigned long long bcount = 0ull;
-  for (int q = 0; q < QS_NCAND; ++q) {
-    const unsigned long long cnt = cand[QS_NCAND + q];
-    if (cand[q] >= 2ull && (long long)cnt >= need && (long long)cnt <= cap &&
-        (best < 0 || cnt < bcount)) {
-      best = q;
-      bcount = cnt;
-    }
-  }
-  if (best < 0) return;  // radix select decides
-  st->theta = cand[best];
-  st->tau = __longlong_as_double((long long)(cand[best] - 2ull));
-  st->done = 1;
 }
 
 // rows with key >= theta -> out[0..), one atomic per block and round
@@ -952,8 +849,7 @@ size_t qdeim_pool_workspace_bytes(int64_t n, int r, int count) {
   b += align_up(sizeof(int64_t) * (size_t)P);              // pool idx
   b += align_up(sizeof(double) * (size_t)P * r);           // Rv
   b += 2 * align_up(sizeof(double) * (size_t)P);           // pres2, pn2
-  b += 2 * align_up(sizeof(SelState)) +
-       align_up(sizeof(unsigned int) * QS_BINS + sizeof(unsigned long long) * 2 * QS_NCAND);  // selection
+  b += 2 * align_up(sizeof(SelState)) + align_up(sizeof(unsigned int) * QS_BINS);  // selection
   b += align_up(sizeof(double) * (size_t)n);               // bounds in refresh-list order
   b += align_up(sizeof(int64_t) * (size_t)n);              // refresh list
   b += align_up(sizeof(double) * (size_t)(r + FACT_KQ) * r);  // W D (factored rows)
@@ -1579,8 +1475,7 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
   SelState* sel = (SelState*)take(sizeof(SelState));
   SelState* selR = (SelState*)take(sizeof(SelState));
   int64_t* rlist = (int64_t*)take(sizeof(int64_t) * (size_t)n);
-  unsigned int* hist = (unsigned int*)take(sizeof(unsigned int) * QS_BINS +
-                                           sizeof(unsigned long long) * 2 * QS_NCAND);
+  unsigned int* hist = (unsigned int*)take(sizeof(unsigned int) * QS_BINS);
   double* blist = (double*)take(sizeof(double) * (size_t)n);  // bounds in refresh-list order
   double* Mw = (double*)take(sizeof(double) * (size_t)(r + FACT_KQ) * r);
   double* D = (double*)take(sizeof(double) * (size_t)r * r);
@@ -1640,17 +1535,6 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
                     long long cap, int extend) -> int {
     qs_init_kernel<<<1, 256, 0, ctx->stream>>>(st, M, hist);
     ADROM_LAUNCH_CK(ctx);
-    if (qs_sampled_select()) {
-      unsigned long long* cand = (unsigned long long*)(hist + QS_BINS) ;
-      qs_sample_kernel<<<1, 1024, 0, ctx->stream>>>(vals, nn, M, cap, cand);
-      ADROM_LAUNCH_CK(ctx);
-      int64_t cg = (nn + 2047) / 2048;
-      if (cg > sg) cg = sg;
-      qs_count_kernel<<<(int)(cg < 1 ? 1 : cg), 256, 0, ctx->stream>>>(vals, nn, cand);
-      ADROM_LAUNCH_CK(ctx);
-      qs_pick_kernel<<<1, 32, 0, ctx->stream>>>(st, cap, cand);
-      ADROM_LAUNCH_CK(ctx);
-    }
     int64_t hg = (nn + 2047) / 2048;
     if (hg > sg) hg = sg;
     for (int shift = 64 - QS_BITS;; shift -= QS_BITS) {
