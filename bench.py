@@ -656,7 +656,7 @@ def e2e_rom(args, case):
     import torch
     from paper_2605_28684_b200.driver import Session, offline_stage
     cfg, model = rom_experiment(case)
-    K = min(case.n_t - case.w_init, max(args.steps, E2E_MIN_STEPS))
+    K = min(case.n_t - case.w_init, max(args.steps, args.e2e_steps or E2E_MIN_STEPS))
     if case.model == "reacting":
         # configuration 4's synthetic ROM degenerates after its second event
         # (the Gauss-Newton solve stops converging and the reduced Jacobian's
@@ -954,6 +954,8 @@ def main(argv=None):
                                                          "cfg4-residual"])
     ap.add_argument("--n-elem", dest="n", type=int, default=0, help="override grid size (testing)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", dest="e2e_steps", type=int, default=0,
+                    help="online steps of the e2e run (0: the default horizon)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "ours":
