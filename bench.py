@@ -868,11 +868,12 @@ CFG4_METRIC = "reacting Euler residual Gcell/s (cfg4: 2^20 cells x 13 vars)"
 
 
 def bench_cfg4(args, rank, world):
-    """Configuration-4 residual (208 B/cell, HBM
-    bound).  Only the residual exists for this model in this revision; a
-    step = one residual evaluation over the grid.  The reference has no such
-    model, so there is no reference arm (cpu_baseline: the numpy oracle that
-    defines the model, timed on a bounded sample)."""
+    """Configuration-4 residual alone (`--config cfg4-residual`; SURVEY §8a
+    row a3, §8d: 208 B/cell): a step = one residual evaluation over the grid.
+    The full configuration-4 adaptive loop is `--config cfg4` (bench_rom).
+    The reference has no such model, so there is no reference arm
+    (cpu_baseline: the numpy oracle that defines the model, timed on a
+    bounded sample)."""
     import torch
     import paper_2605_28684_b200 as P
     from paper_2605_28684_b200 import _lib
