@@ -649,14 +649,15 @@ def e2e_rom(args, case):
     copied back to pinned host memory (the reference keeps its trajectory on
     the host, driver.py:306/344) — into a ring of E2E_RING host slots, since a
     full trajectory of 2^24-cell states does not fit in pinned memory.  The
-    horizon is max(K, 200) online steps of the reference's timed region
-    (driver.py:319-389 covers all n_t - w_init steps), so the one-time upload
-    of the offline basis (8.6 GB at cfg 3) is amortised over a realistic
-    stretch of the run instead of K = 20 steps."""
+    horizon is the reference's whole timed region (driver.py:319-389: all
+    n_t - w_init online steps; --e2e-steps overrides), so the one-time upload
+    of the offline basis (8.6 GB at cfg 3) is amortised like the reference's
+    setup is."""
     import torch
     from paper_2605_28684_b200.driver import Session, offline_stage
     cfg, model = rom_experiment(case)
-    K = min(case.n_t - case.w_init, max(args.steps, args.e2e_steps or E2E_MIN_STEPS))
+    # the reference's timed region covers every online step (driver.py:319-389)
+    K = min(case.n_t - case.w_init, max(args.steps, args.e2e_steps or (case.n_t - case.w_init)))
     if case.model == "reacting":
         # configuration 4's synthetic ROM degenerates after its second event
         # (the Gauss-Newton solve stops converging and the reduced Jacobian's

@@ -964,20 +964,11 @@ __global__ void __launch_bounds__(128) isvd_solve_kernel(const double* __restric
     __syncthreads();
     conv = sh_done != 0;
   }
+  // a basis far from orthonormal (the Neumann series did not converge):
+  // isvd_solve_direct_kernel solves G p = p1 directly; need[1] tells it to
+  if (tid == 0) need[1] = (sh_done != 1) ? 1 : 0;
+  if (sh_done != 1) return;
   if (tid == 0) {
-    if (sh_done != 1) {
-      // fallback for a far-from-orthonormal basis: Gauss-Seidel on the SPD
-      // system G p = p1 (always convergent for SPD G; rare, slow, one thread)
-      for (int j = 0; j < r; ++j) sp[j] = red1[j];
-      for (int sweep = 0; sweep < 200; ++sweep) {
-        for (int i = 0; i < r; ++i) {
-          double s = red1[i];
-          for (int k = 0; k < r; ++k)
-            if (k != i) s -= G[i * r + k] * sp[k];
-          sp[i] = s / G[i * r + i];
-        }
-      }
-    }
     double pdot = 0.0;
     for (int j = 0; j < r; ++j) pdot += sp[j] * red1[j];
     const double yy = red1[r];
@@ -986,6 +977,66 @@ __global__ void __launch_bounds__(128) isvd_solve_kernel(const double* __restric
   }
   __syncthreads();
   for (int j = tid; j < r; j += blockDim.x) p[j] = sp[j];
+}
+
+// G p = p1 by Gaussian elimination with partial pivoting on the whole block
+// (G = Phi^T Phi is SPD; pivoting only guards a drifted tracked Gram), run
+// when isvd_solve_kernel flagged need[1]; O(r^3 / 3) in shared memory
+// instead of the former one-thread Gauss-Seidel (200 serial sweeps, ~14 ms
+// at r = 64 late in a 2000-step configuration-3 run).
+__global__ void __launch_bounds__(256) isvd_solve_direct_kernel(const double* __restrict__ red1,
+                                                                const double* __restrict__ G, int r,
+                                                                double ratio, double* __restrict__ p,
+                                                                int* __restrict__ need) {
+  if (need[1] == 0) return;
+  extern __shared__ double sa[];  // r x (r + 1) augmented, row-major (ld r + 1)
+  __shared__ int piv_sh;
+  const int tid = threadIdx.x, ld = r + 1;
+  for (int e = tid; e < r * r; e += blockDim.x) sa[(e / r) * ld + (e % r)] = G[e];
+  for (int i = tid; i < r; i += blockDim.x) sa[i * ld + r] = red1[i];
+  __syncthreads();
+  for (int k = 0; k < r; ++k) {
+    if (tid == 0) {
+      int pv = k;
+      double best = fabs(sa[k * ld + k]);
+      for (int i = k + 1; i < r; ++i) {
+        const double v = fabs(sa[i * ld + k]);
+        if (v > best) {
+          best = v;
+          pv = i;
+        }
+      }
+      piv_sh = pv;
+    }
+    __syncthreads();
+    const int pv = piv_sh;
+    if (pv != k)
+      for (int j = tid; j <= r; j += blockDim.x) {
+        const double t = sa[k * ld + j];
+        sa[k * ld + j] = sa[pv * ld + j];
+        sa[pv * ld + j] = t;
+      }
+    __syncthreads();
+    const double akk = sa[k * ld + k];
+    const int m = r - k - 1;
+    for (int e = tid; e < m * (m + 1); e += blockDim.x) {
+      const int i = k + 1 + e / (m + 1), j = k + 1 + e % (m + 1);
+      sa[i * ld + j] -= (sa[i * ld + k] / akk) * sa[k * ld + j];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    for (int i = r - 1; i >= 0; --i) {
+      double s = sa[i * ld + r];
+      for (int j = i + 1; j < r; ++j) s -= sa[i * ld + j] * p[j];
+      p[i] = s / sa[i * ld + i];
+    }
+    double pdot = 0.0;
+    for (int j = 0; j < r; ++j) pdot += p[j] * red1[j];
+    const double yy = red1[r];
+    need[0] = (yy - pdot > ratio * yy) ? 0 : 1;
+    need[1] = 0;
+  }
 }
 
 // iSVD core (tracking.py:163-177) for p = lstsq coefficients (isvd_solve_kernel):
@@ -1329,6 +1380,15 @@ size_t isvd_workspace_bytes(adrom_ctx* ctx, int64_t n, int r_cur, int r) {
   return b;
 }
 
+static int isvd_solve_direct_launch(adrom_ctx* ctx, const double* red1, const double* G, int r,
+                                    double ratio, double* p, int* need) {
+  const size_t sm = sizeof(double) * (size_t)r * (r + 1);
+  cudaFuncSetAttribute(isvd_solve_direct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  isvd_solve_direct_kernel<<<1, 256, sm, ctx->stream>>>(red1, G, r, ratio, p, need);
+  ADROM_LAUNCH_CK(ctx);
+  return ADROM_OK;
+}
+
 int isvd_update_async(adrom_ctx* ctx, const double* phi, const double* sigma, const double* y,
                       int64_t n, int r_cur, int r, double lam, double* phi_out,
                       double* sigma_out, const double* gram_in, double* gram_out, void* ws,
@@ -1380,6 +1440,8 @@ int isvd_update_async(adrom_ctx* ctx, const double* phi, const double* sigma, co
   // least squares p = G^{-1} p1 (gelsd semantics for a full-rank basis)
   isvd_solve_kernel<<<1, 128, 0, ctx->stream>>>(red1, G, r_cur, reorth_ratio, pls, need);
   ADROM_LAUNCH_CK(ctx);
+  st = isvd_solve_direct_launch(ctx, red1, G, r_cur, reorth_ratio, pls, need);
+  if (st) return st;
   // pass 2 (only if ||y||^2 - p.p1 would cancel): q = y - Phi p, Phi^T q, ||q||^2
   pr = prof_begin(ctx, PROBE_ISVD_RESID);
   st = ts_residual(ctx, phi, n, r_cur, pls, y, red2, partial, flag, need, qbuf);
@@ -1416,6 +1478,8 @@ int isvd_solve_launch(adrom_ctx* ctx, const double* red1, const double* G, int r
                       int* need) {
   isvd_solve_kernel<<<1, 128, 0, ctx->stream>>>(red1, G, r, ISVD_REORTH_RATIO, p, need);
   ADROM_LAUNCH_CK(ctx);
+  int st = isvd_solve_direct_launch(ctx, red1, G, r, ISVD_REORTH_RATIO, p, need);
+  if (st) return st;
   return ADROM_OK;
 }
 

@@ -74,3 +74,24 @@ def test_core_lambda_zero_and_tiny_tail():
     _check(phi, sig, y, 0.1, r)
     phi, sig, y = _case(8192, r, np.linspace(2, 1, r), rng.standard_normal(r), 0.3, rng)
     _check(phi, sig, y, 0.0, r)
+
+
+def test_least_squares_far_from_orthonormal_basis():
+    """tracking.py:161 (gelsd) on a basis whose Gram matrix is far from the
+    identity: the Neumann series of the tracked-Gram solve diverges and the
+    block-parallel direct solve (isvd_solve_direct_kernel) takes over."""
+    from paper_2605_28684_b200 import ReducedBasis, isvd_update
+    from oracle import subspace
+    rng = np.random.default_rng(17)
+    n, r = 5000, 24
+    phi = np.linalg.qr(rng.standard_normal((n, r)))[0]
+    phi = phi @ (np.eye(r) + 0.6 * rng.standard_normal((r, r)) / np.sqrt(r))   # G = M^T M, ||G - I|| > 1
+    sig = np.linspace(3.0, 0.5, r)
+    y = phi @ rng.standard_normal(r) + 0.2 * rng.standard_normal(n)
+    got = isvd_update(ReducedBasis(phi, sig), y, 0.7, r)
+    ref_phi, ref_sig, _ = subspace.isvd_update(phi, sig, y, 0.7, r)
+    assert np.allclose(got.sigma, ref_sig, rtol=1e-9)
+    g = np.asarray(got.phi)
+    sgn = np.sign(np.sum(g * ref_phi, axis=0))
+    rel = np.linalg.norm(g * sgn - ref_phi, axis=0) / np.linalg.norm(ref_phi, axis=0)
+    assert rel.max() < 1e-8, rel.max()
