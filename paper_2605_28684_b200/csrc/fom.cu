@@ -238,10 +238,8 @@ __global__ void __launch_bounds__(SODW_NT) sod_rhs_warp_kernel(
   double acc = 0.0;
   bool bad = false;
   constexpr unsigned FULL = 0xffffffffu;
-  for (int64_t ch = (int64_t)blockIdx.x * (SODW_NT / 32) + warp; ch < nchunks; ch += wstride) {
+  auto process = [&](int64_t ch, const Cons& u) {
     const int64_t c = ch * SODW_CELLS - 1 + lane;  // this lane's cell (unclamped)
-    const int64_t cc = c < 0 ? 0 : (c > n - 1 ? n - 1 : c);
-    const Cons u = load_cons(q, cc);
     const SodQ qu = sod_q(u, gamma);
     // face between this lane's cell and the next lane's
     Cons ur;
@@ -271,7 +269,21 @@ __global__ void __launch_bounds__(SODW_NT) sod_rhs_warp_kernel(
       out[3 * c + 1] = o.m1;
       out[3 * c + 2] = o.m2;
     }
+  };
+  auto cell_of = [&](int64_t ch) {
+    const int64_t c = ch * SODW_CELLS - 1 + lane;
+    return c < 0 ? (int64_t)0 : (c > n - 1 ? n - 1 : c);
+  };
+  // two chunks per iteration: both chunks' loads are in flight before either
+  // is evaluated (memory-level parallelism for the latency-bound loads)
+  int64_t ch = (int64_t)blockIdx.x * (SODW_NT / 32) + warp;
+  for (; ch + wstride < nchunks; ch += 2 * wstride) {
+    const Cons u0 = load_cons(q, cell_of(ch));
+    const Cons u1 = load_cons(q, cell_of(ch + wstride));
+    process(ch, u0);
+    process(ch + wstride, u1);
   }
+  if (ch < nchunks) process(ch, load_cons(q, cell_of(ch)));
   if (MODE == 1) {
     const double s = block_sum<SODW_NT>(acc, red);
     if (threadIdx.x == 0) partial[blockIdx.x] = s;
