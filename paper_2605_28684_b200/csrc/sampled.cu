@@ -84,22 +84,6 @@ constexpr double LS_CERT = 1e10;
 // The SVD path with V in L2 then only runs for cond > ~1e12.
 constexpr double LS_CERT_BIG = 0.99e12;
 
-// sum of col[k..r)^2 with exactly the rounding of block_sum_dyn over a
-// thread-per-element layout (element k + t on thread t, r - k <= 128), but
-// computed by one warp: the four per-warp butterflies, then the second-level
-// butterfly (w0 + w2) + (w1 + w3)
-__device__ __forceinline__ double warp_colnorm2(const double* col, int k, int r, int lane) {
-  double w[4];
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    const int i = k + 32 * t + lane;
-    double e = 0.0;
-    if (i < r) e = 0.0 + col[i] * col[i];
-    w[t] = warp_sum(e);
-  }
-  return (w[0] + w[2]) + (w[1] + w[3]);
-}
-
 // C (column-major, C[l * ldc + k]) = A B for A (M x K, row-major lda) and B
 // (K x N, row-major ldb), M, N <= 128: the whole block, one warp per 8 x 8
 // output tile on the FP64 tensor cores (mma.sync m8n8k4), K in steps of 4
@@ -132,47 +116,78 @@ __device__ __forceinline__ void block_dmma_gemm(const double* A, int lda, const 
 __device__ bool block_qr_certified_solve(double* jA, int ld, int r, double* rhs, double* out,
                                          double* vbuf, double* red, double cert_bound = LS_CERT) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  __shared__ double sh_beta, sh_alpha, sh_nrm2;
-  // Householder QR, two barriers per column: the warp that updates column
-  // k+1 also forms its trailing norm for the next step.  v_k lives in col[k]
-  // during step k; R's diagonal is written back one step later.
-  {
-    const double a0 = warp_colnorm2(jA, 0, r, lane);
-    if (tid == 0) sh_nrm2 = a0;
-  }
+  __shared__ double sh_beta[2], sh_alpha[2];
+  // Householder QR, one barrier per column.  Warp 0 owns the critical chain:
+  // it applies reflector k to column k+1, forms that column's trailing norm
+  // and reflector k+1 (alpha, beta, v's head) for the next step; warps 1..
+  // apply reflector k to the other columns and the rhs, two columns at a
+  // time (independent reductions in flight).  v_k lives in col[k] during
+  // step k; R's diagonal is written back one step later.
+  auto reflector = [&](double* c, int j, int slot) {  // warp 0, column j
+    double a = 0.0;
+    for (int i = j + lane; i < r; i += 32) a = fma(c[i], c[i], a);
+    a = warp_sum(a);
+    if (lane == 0) {
+      const double x0 = c[j];
+      const double nrm = sqrt(a);
+      const double alpha = (x0 >= 0.0) ? -nrm : nrm;
+      // v = x - alpha e1, beta = 1 / (v^T v / 2) = 1 / (nrm^2 - x0 alpha)
+      const double vtv_half = a - x0 * alpha;
+      sh_alpha[slot] = alpha;
+      sh_beta[slot] = (vtv_half > 0.0) ? 1.0 / vtv_half : 0.0;
+      c[j] = x0 - alpha;
+    }
+  };
+  if (warp == 0) reflector(jA, 0, 0);
   __syncthreads();
   for (int k = 0; k < r; ++k) {
     double* col = jA + (size_t)k * ld;
-    if (tid == 0) {
-      if (k > 0) jA[(size_t)(k - 1) * ld + (k - 1)] = sh_alpha;
-      const double a = sh_nrm2;
-      const double x0 = col[k];
-      const double nrm = sqrt(a);
-      const double alpha = (x0 >= 0.0) ? -nrm : nrm;
-      sh_alpha = alpha;
-      // v = x - alpha e1, beta = 1 / (v^T v / 2) = 1 / (nrm^2 - x0 alpha)
-      const double vtv_half = a - x0 * alpha;
-      sh_beta = (vtv_half > 0.0) ? 1.0 / vtv_half : 0.0;
-      col[k] = x0 - alpha;
-    }
-    __syncthreads();
-    const double beta = sh_beta;
-    // apply H = I - beta v v^T to trailing columns and the rhs (warp per column)
-    for (int j = k + 1 + warp; j <= r; j += nw) {
-      double* cj = (j < r) ? jA + (size_t)j * ld : rhs;
-      double s = 0.0;
-      for (int i = k + lane; i < r; i += 32) s = fma(col[i], cj[i], s);
-      s = warp_sum(s) * beta;
-      for (int i = k + lane; i < r; i += 32) cj[i] = fma(-s, col[i], cj[i]);
-      if (j == k + 1 && j < r) {
+    const double beta = sh_beta[k & 1];
+    if (warp == 0) {
+      if (k > 0 && lane == 0) jA[(size_t)(k - 1) * ld + (k - 1)] = sh_alpha[(k - 1) & 1];
+      if (k + 1 < r) {
+        double* cj = jA + (size_t)(k + 1) * ld;
+        double s = 0.0;
+        for (int i = k + lane; i < r; i += 32) s = fma(col[i], cj[i], s);
+        s = warp_sum(s) * beta;
+        for (int i = k + lane; i < r; i += 32) cj[i] = fma(-s, col[i], cj[i]);
         __syncwarp();
-        const double a1 = warp_colnorm2(cj, j, r, lane);
-        if (lane == 0) sh_nrm2 = a1;
+        reflector(cj, k + 1, (k + 1) & 1);
+      }
+    }
+    if (warp != 0 || nw == 1) {
+      // columns k+2 .. r-1 and the rhs (index r), two per pass; at the last
+      // step (k + 1 == r) only the rhs
+      const int first = (k + 1 < r) ? k + 2 : r, last = r;  // inclusive
+      const int nwk = nw > 1 ? nw - 1 : 1, wi = nw > 1 ? warp - 1 : 0;
+      for (int j0 = first + 2 * wi; j0 <= last; j0 += 2 * nwk) {
+        const int j1 = j0 + 1;
+        double* c0 = (j0 < r) ? jA + (size_t)j0 * ld : rhs;
+        double* c1 = (j1 < r) ? jA + (size_t)j1 * ld : rhs;
+        const bool two = j1 <= last;
+        double s0 = 0.0, s1 = 0.0;
+        for (int i = k + lane; i < r; i += 32) {
+          const double v = col[i];
+          s0 = fma(v, c0[i], s0);
+          if (two) s1 = fma(v, c1[i], s1);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+          s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        }
+        s0 *= beta;
+        s1 *= beta;
+        for (int i = k + lane; i < r; i += 32) {
+          const double v = col[i];
+          c0[i] = fma(-s0, v, c0[i]);
+          if (two) c1[i] = fma(-s1, v, c1[i]);
+        }
       }
     }
     __syncthreads();
   }
-  if (tid == 0) jA[(size_t)(r - 1) * ld + (r - 1)] = sh_alpha;
+  if (tid == 0) jA[(size_t)(r - 1) * ld + (r - 1)] = sh_alpha[(r - 1) & 1];
   __syncthreads();
   (void)vbuf;
   (void)red;
