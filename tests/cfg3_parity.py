@@ -165,6 +165,7 @@ def compare(ref, got, env_s=None, env_sig=None):
     it_ref = np.array(ref.iterations)
     rep = dict(dev=dev, it_ref=it_ref, it_got=got["it"],
                coarse_ref=[e["coarse_iterations"] for e in ref.events],
+               coarse_conv_ref=[bool(e.get("coarse_converged", True)) for e in ref.events],
                coarse_got=got["coarse"], event_errors=got["errors"],
                fail_ref=list(ref.failures))
     if len(got["sig"]):
