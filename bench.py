@@ -551,7 +551,7 @@ def bench_rom(args, rank, world):
     # between re-anchors (one event per step here); the mean over the timed
     # events is used.  QDEIM is larger in total but is a sequence of rounds of small
     # kernels (qdeim_rounds_per_step below).
-    roof = None
+    roof = roof1 = None
     if case.model == "reacting" and "decode" in per:
         # configuration 4: the largest kernels are FP64-pipe bound (the FD
         # directions of the large-sample LSPG step, bl_dir_kernel, ~1.4 ms per
@@ -584,13 +584,24 @@ def bench_rom(args, rank, world):
     elif "isvd_project" in per:
         kq = 16
         k_mean = float(np.mean([(j % kq) for j in range(W + K, W + K + max(kp, 1))])) if case.z == 1 else 0.0
+        # the largest single kernel of the step (serialised launch list,
+        # profiles/r2_cfg3_timed_launches.txt) is pass 2 (q = y - X(Wp) into
+        # its Q panel, X^T q, state-transfer sums, fused decode): reads A, the
+        # k live Q columns, y, q_ref, d; writes q and q~: 8 N (r + k + 5)
+        x2bytes = 8.0 * N * (r + k_mean + 5)
+        roof = roofline(x2bytes, per["isvd_resid"][0],
+                        ncu_traffic("xpass_tma_kernel<64, 2>", case.name))
+        roof.update({"kernel": "isvd_resid (xpass_tma_kernel<64,2>: q = y - X(Wp), X^T q, "
+                               "state-transfer sums, fused decode; TMA-staged row tiles)",
+                     "work_per_launch": {"bytes": x2bytes, "k_mean": k_mean},
+                     "share_of_step": round(probes["isvd_resid"][0] / ms_probed, 4)})
+        # pass 1 (X^T y + exact row norms): 8 N (r + k + 3)
         xbytes = 8.0 * N * (r + k_mean + 3)
-        roof = roofline(xbytes, per["isvd_project"][0],
-                        ncu_traffic("xpass_tma_kernel<64, 1>", case.name))
-        roof.update({"kernel": "isvd_project (xpass_tma_kernel<64,1>: X^T y + exact row norms, "
-                               "TMA-staged row tiles)",
-                     "work_per_launch": {"bytes": xbytes, "k_mean": k_mean},
-                     "share_of_step": round(probes["isvd_project"][0] / ms_probed, 4)})
+        roof1 = roofline(xbytes, per["isvd_project"][0],
+                         ncu_traffic("xpass_tma_kernel<64, 1>", case.name))
+        roof1.update({"kernel": "isvd_project (xpass_tma_kernel<64,1>)",
+                      "work_per_launch": {"bytes": xbytes, "k_mean": k_mean},
+                      "share_of_step": round(probes["isvd_project"][0] / ms_probed, 4)})
     isvd_keys = ("isvd_project", "isvd_resid", "isvd_core", "isvd_rotate")
     n_upd = max(probes.get("isvd_project", (0, 1))[1], 1)
     isvd_ms = sum(probes.get(k, (0, 0))[0] for k in isvd_keys) / n_upd
@@ -610,6 +621,8 @@ def bench_rom(args, rank, world):
                          if 8 * N * r > 126e6 else "working set L2-resident (latency-bound)",
                    "parallelism": f"replicas{world}"},
         "roofline": roof,
+        "roofline_pass1": roof1 if "isvd_project" in per and "isvd_rotate" not in per
+                          and case.model != "reacting" else None,
         "gpu_launches": launches,
         "fom_residual_gcells": fres["gcells"],
         "fom_residual": fres,

@@ -11,11 +11,14 @@ sys.path.insert(0, str(ROOT))
 
 
 def main():
+    import os
     import torch
     import bench
     from paper_2605_28684_b200.dense import ts_tn
     from paper_2605_28684_b200.driver import Session, offline_stage
-    case = bench.rom_case("cfg3", 0)
+    from paper_2605_28684_b200 import configs
+    n_env = int(os.environ.get("ADROM_DEFECT_N", "0"))
+    case = configs.cfg3(n_env) if n_env else bench.rom_case("cfg3", 0)  # the recipe on that grid
     cfg, model = bench.rom_experiment(case)
     training, scaling, basis0 = offline_stage(cfg, model)
     q_last = training[cfg.w_init].clone()
