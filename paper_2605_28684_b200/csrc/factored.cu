@@ -604,14 +604,16 @@ __global__ void vdrop_kernel(const double* __restrict__ W, int rk, int r,
 
 // QDEIM k = 0 bounds of the new basis: ||Phi'_i||^2 <= ||Phi_i||^2 + (q_i / ||q||)^2
 // (B has orthonormal columns); nrm2_next keeps the bound for the next event
+// sb = [qinv, ||p2||]: with the refined direction q_hat_i = (q_i - Phi_i p2)
+// qinv, |q_hat_i| <= (|q_i| + ||Phi_i|| ||p2||) qinv
 __global__ void seed_bounds_kernel(const double* __restrict__ nrm2, const double* __restrict__ qv,
-                                   const double* __restrict__ qinv, int64_t n,
+                                   const double* __restrict__ sb, int64_t n,
                                    double* __restrict__ res2, double* __restrict__ bnd2,
                                    unsigned char* __restrict__ ver, double* __restrict__ nrm2_next) {
-  const double qi = *qinv;
+  const double qi = sb[0], p2n = sb[1];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const double qh = qv[i] * qi;
+    const double qh = (fabs(qv[i]) + (p2n > 0.0 ? sqrt(nrm2[i]) * p2n : 0.0)) * qi;
     const double b = (nrm2[i] + qh * qh) * (1.0 + 64.0 * 2.220446049250313e-16);
     nrm2_next[i] = b;
     res2[i] = b;
@@ -900,7 +902,7 @@ int fact_reanchor(adrom_ctx* ctx, const FactBasis& b, double* out, double* nrm2,
 }
 
 struct FactSmall {
-  double *vdec, *vp, *red1, *red2, *pls, *t1, *t2, *Bm, *Tm, *sb;
+  double *vdec, *vp, *red1, *red2, *pls, *t1, *t2, *Bm, *Tm, *sb, *p2;
   int* need;
 };
 
@@ -915,8 +917,9 @@ static FactSmall fact_small_layout(double* w, int r) {
   f.t2 = f.t1 + r + FACT_KQ + 1;      // r + KQ + 1 (reduced pass-2 sums)
   f.Bm = f.t2 + 2 * (r + FACT_KQ) + 2;  // (r + 1) x r
   f.Tm = f.Bm + (r + 1) * r;            // (r + 1) x r
-  f.sb = f.Tm + (r + 1) * r;            // [0] qinv, [2 .. r+3) dropped vector
-  f.need = (int*)(f.sb + r + 8);
+  f.sb = f.Tm + (r + 1) * r;            // [0] qinv, [1] ||p2||, [2 .. r+3) dropped vector
+  f.need = (int*)(f.sb + r + 8);        // 4 ints
+  f.p2 = f.sb + r + 12;                 // r: least-squares refinement
   return f;
 }
 
@@ -952,6 +955,21 @@ int fact_event_pass_a(adrom_ctx* ctx, const FactBasis& b, const FactEventArgs& e
 }
 
 // the rest of the event on the main stream: least squares, pass 2 with the
+// the refined direction q_hat = (q - Phi p2) qinv in factored form: with
+// Phi' = Phi B_top + q_hat b_bot = X W (B_top - qinv p2 b_bot) + q qinv b_bot,
+// B_top (and the dropped vector's top) absorb the rank-one correction
+__global__ void refine_b_kernel(double* __restrict__ B, double* __restrict__ udrop,
+                                const double* __restrict__ p2, const double* __restrict__ sb,
+                                int r, int r_out) {
+  const double qi = sb[0];
+  for (int e = threadIdx.x; e < r * r_out; e += blockDim.x) {
+    const int k = e / r_out, c = e - k * r_out;
+    B[e] -= qi * p2[k] * B[(size_t)r * r_out + c];
+  }
+  if (udrop)
+    for (int k = threadIdx.x; k < r; k += blockDim.x) udrop[k] -= qi * p2[k] * udrop[r];
+}
+
 // fused decode of the reduced state, core SVD, W', state transfer, seeds
 int fact_event_pass_b(adrom_ctx* ctx, const FactBasis& b, const FactEventArgs& e) {
   const int r = b.r, k = b.k, rk = r + k;
@@ -995,6 +1013,9 @@ int fact_event_pass_b(adrom_ctx* ctx, const FactBasis& b, const FactEventArgs& e
   }
   ADROM_CK(ctx, cudaMemcpyAsync(f.red2 + r, f.t2 + r + FACT_KQ, sizeof(double), cudaMemcpyDeviceToDevice,
                                 ctx->stream));
+  // one least-squares refinement step: q' = q - Phi p2 (isvd_refine_kernel)
+  st = isvd_refine_launch(ctx, e.G, r, f.red2, f.pls, f.p2, f.sb + 1, f.need);
+  if (st) return st;
   // core: K, its SVD, B, qinv, the tracked Gram of the new basis, sigma'
   pr = prof_begin(ctx, PROBE_ISVD_CORE);
   double* udrop = f.sb + 2;
@@ -1002,13 +1023,17 @@ int fact_event_pass_b(adrom_ctx* ctx, const FactBasis& b, const FactEventArgs& e
                         e.G_out, e.sigma_out, e.stats, e.flag, udrop);
   prof_end(ctx, pr);
   if (st) return st;
-  // W' and the state transfer for the new basis
-  wnext_kernel<<<(rk + 1) * r / 256 + 1, 256, 0, ctx->stream>>>(b.W, rk, r, f.Bm, f.sb, e.W_out);
-  ADROM_LAUNCH_CK(ctx);
+  // state transfer for the new basis: a' = B_top^T G a + b_bot^T qinv c'.a,
+  // from the refined c' = Phi^T q' (red2) and the unmodified B
   if (e.a_out) {
     encode_factored_kernel<<<1, 128, 0, ctx->stream>>>(e.G, r, e.a, f.red2, f.sb, f.Bm, e.a_out);
     ADROM_LAUNCH_CK(ctx);
   }
+  refine_b_kernel<<<1, 256, 0, ctx->stream>>>(f.Bm, e.vdrop_out ? udrop : nullptr, f.p2, f.sb, r, r);
+  ADROM_LAUNCH_CK(ctx);
+  // W' for the new basis
+  wnext_kernel<<<(rk + 1) * r / 256 + 1, 256, 0, ctx->stream>>>(b.W, rk, r, f.Bm, f.sb, e.W_out);
+  ADROM_LAUNCH_CK(ctx);
   if (e.vdrop_out) {
     vdrop_kernel<<<1, 128, 0, ctx->stream>>>(b.W, rk, r, udrop, f.sb, e.vdrop_out);
     ADROM_LAUNCH_CK(ctx);

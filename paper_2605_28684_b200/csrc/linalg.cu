@@ -435,6 +435,8 @@ struct RotArgs {
   int r_in, r_out;
   double* out;
   RotFuse fuse;  // fused epilogue work (rot_tc_kernel only)
+  const double* p2 = nullptr;  // least-squares refinement (r_in; null = none):
+                               // with q from qbuf, q_hat = (qbuf - phi p2) qinv
 };
 
 template <int R>
@@ -455,7 +457,8 @@ __global__ void __launch_bounds__(256) rot_tiled_kernel(RotArgs a) {
   const int tid = threadIdx.x;
   const bool use_q = a.qbuf && (a.need == nullptr || *a.need != 0);
   for (int e = tid; e < (R + 1) * R; e += 256) Bs[e] = a.B[e];
-  for (int e = tid; e < R; e += 256) ps[e] = use_q ? 0.0 : a.p[e];
+  for (int e = tid; e < R; e += 256) ps[e] = use_q ? (a.p2 ? a.p2[e] : 0.0) : a.p[e];
+  const bool dot = !use_q || a.p2 != nullptr;
   const double qinv = *a.qinv;
   const int rg = tid >> 4, cg = tid & 15;
   const int64_t n = a.n;
@@ -476,14 +479,10 @@ __global__ void __launch_bounds__(256) rot_tiled_kernel(RotArgs a) {
     for (int e = tid; e < C::TM; e += 256) {
       double qh = 0.0;
       if (e < rows) {
-        double qv;
-        if (use_q) {
-          qv = a.qbuf[row0 + e];
-        } else {
-          double s = 0.0;
+        double s = 0.0;
+        if (dot)
           for (int k = 0; k < R; ++k) s = fma(As[e * C::SA + k], ps[k], s);
-          qv = a.y[row0 + e] - s;
-        }
+        const double qv = (use_q ? a.qbuf[row0 + e] : a.y[row0 + e]) - s;
         qh = qv * qinv;
       }
       As[e * C::SA + R] = qh;
@@ -576,7 +575,8 @@ __global__ void __launch_bounds__(RotTC<R>::NTHR, R <= 64 ? 2 : 1) rot_tc_kernel
 #pragma unroll
   for (int j = 0; j < C::NT; ++j) enc_acc[j][0] = enc_acc[j][1] = 0.0;
   for (int e = tid; e < (R + 1) * R; e += C::NTHR) Bs[(e / R) * C::S + (e % R)] = a.B[e];
-  for (int e = tid; e < R; e += C::NTHR) ps[e] = use_q ? 0.0 : a.p[e];
+  for (int e = tid; e < R; e += C::NTHR) ps[e] = use_q ? (a.p2 ? a.p2[e] : 0.0) : a.p[e];
+  const bool dot = !use_q || a.p2 != nullptr;
   const double qinv = *a.qinv;
   const int64_t n = a.n;
   const int64_t ntiles = (n + C::TM - 1) / C::TM;
@@ -609,15 +609,13 @@ __global__ void __launch_bounds__(RotTC<R>::NTHR, R <= 64 ? 2 : 1) rot_tc_kernel
     for (int e = tid; e < 2 * C::TM; e += C::NTHR) {
       const int rr = e >> 1, half = e & 1;
       double qv = 0.0;
-      if (!use_q) {
-        double s = 0.0;
+      double s = 0.0;
+      if (dot) {
 #pragma unroll 8
         for (int k = half * (R / 2); k < (half + 1) * (R / 2); ++k) s = fma(As[rr * C::S + k], ps[k], s);
         s += __shfl_xor_sync(0xffffffffu, s, 1);
-        qv = (row0 + rr < n) ? a.y[row0 + rr] - s : 0.0;
-      } else {
-        qv = (row0 + rr < n) ? a.qbuf[row0 + rr] : 0.0;
       }
+      if (row0 + rr < n) qv = (use_q ? a.qbuf[row0 + rr] : a.y[row0 + rr]) - s;
       if (half == 0) As[rr * C::S + R] = qv * qinv;
     }
     double acc[C::MT][C::NT][2];
@@ -730,7 +728,8 @@ __global__ void __launch_bounds__(256) rot_generic_kernel(RotArgs a) {
   const int tid = threadIdx.x;
   const bool use_q = a.qbuf && (a.need == nullptr || *a.need != 0);
   for (int e = tid; e < (r_in + 1) * r_out; e += 256) Bs[e] = a.B[e];
-  for (int e = tid; e < r_in; e += 256) ps[e] = use_q ? 0.0 : a.p[e];
+  for (int e = tid; e < r_in; e += 256) ps[e] = use_q ? (a.p2 ? a.p2[e] : 0.0) : a.p[e];
+  const bool dot = !use_q || a.p2 != nullptr;
   const double qinv = *a.qinv;
   const int64_t ntiles = (a.n + T - 1) / T;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -743,14 +742,10 @@ __global__ void __launch_bounds__(256) rot_generic_kernel(RotArgs a) {
     }
     __syncthreads();
     for (int e = tid; e < rows; e += 256) {
-      double qv;
-      if (use_q) {
-        qv = a.qbuf[row0 + e];
-      } else {
-        double s = 0.0;
+      double s = 0.0;
+      if (dot)
         for (int k = 0; k < r_in; ++k) s = fma(As[e * S + k], ps[k], s);
-        qv = a.y[row0 + e] - s;
-      }
+      const double qv = (use_q ? a.qbuf[row0 + e] : a.y[row0 + e]) - s;
       As[e * S + r_in] = qv * qinv;
     }
     __syncthreads();
@@ -1370,6 +1365,7 @@ size_t isvd_workspace_bytes(adrom_ctx* ctx, int64_t n, int r_cur, int r) {
   b += align_up(sizeof(double) * isvd_partial_doubles(ctx, r_cur));  // partials (Gram's too)
   b += 2 * align_up(sizeof(double) * (r_cur + 1));     // red1, red2
   b += align_up(sizeof(double) * r_cur);               // p (least squares)
+  b += align_up(sizeof(double) * r_cur);               // p2 (refinement)
   b += align_up(sizeof(double) * (r_cur + 1) * r);     // B
   b += align_up(sizeof(double) * (r_cur + 1) * r);     // T
   b += align_up(sizeof(double) * r_cur * r_cur);       // Gram (when not supplied)
@@ -1379,6 +1375,141 @@ size_t isvd_workspace_bytes(adrom_ctx* ctx, int64_t n, int r_cur, int r) {
   b += align_up(sizeof(double) * core_vglob_doubles(r_cur));  // core V (r_cur > 110)
   return b;
 }
+
+// One step of least-squares refinement after the explicit residual pass
+// (need[0] != 0): red2 = [c = Phi^T q, ||q||^2] for q = y - Phi p.  With the
+// tracked Gram G, p2 = G^{-1} c (Neumann series; Gaussian elimination with
+// partial pivoting when it diverges), p += p2, and q' = q - Phi p2 is the
+// residual used from here on: red2 <- [c - G p2, ||q||^2 - 2 p2.c +
+// p2.G p2].  The tracked-Gram solve alone leaves q off Phi's complement by the
+// Gram's error times ||y|| / ||q||, which compounds over events (orthonormality
+// defect 7e-2 after 600 configuration-3 events at N = 2^16 against the
+// reference's 3e-3); one refinement step makes q orthogonal to the actual
+// basis (defect 2e-14 in the numpy prototype).  p2norm (optional) <- ||p2||.
+__global__ void __launch_bounds__(256) isvd_refine_kernel(const double* __restrict__ G, int r,
+                                                          double* __restrict__ red2,
+                                                          double* __restrict__ p,
+                                                          double* __restrict__ p2,
+                                                          double* __restrict__ p2norm,
+                                                          const int* __restrict__ need) {
+  extern __shared__ double sa[];  // r x (r + 1) augmented system (fallback)
+  __shared__ double c[128], x[128], t[128], nx[128];
+  __shared__ double red[32];
+  __shared__ int sh_done, piv_sh;
+  const int tid = threadIdx.x;
+  if (need && need[0] == 0) {
+    for (int j = tid; j < r; j += blockDim.x) p2[j] = 0.0;
+    if (tid == 0 && p2norm) *p2norm = 0.0;
+    return;
+  }
+  for (int j = tid; j < r; j += blockDim.x) {
+    c[j] = red2[j];
+    x[j] = red2[j];
+    t[j] = red2[j];
+  }
+  __syncthreads();
+  // Neumann series x = sum_m (-(G - I))^m c
+  bool conv = false;
+  for (int it = 0; it < 60 && !conv; ++it) {
+    for (int i = tid; i < r; i += blockDim.x) {
+      double sacc = 0.0;
+      for (int k = 0; k < r; ++k) sacc = fma(G[i * r + k] - (i == k ? 1.0 : 0.0), t[k], sacc);
+      nx[i] = -sacc;
+    }
+    __syncthreads();
+    double tn = 0.0, xn = 0.0;
+    for (int j = tid; j < r; j += blockDim.x) {
+      t[j] = nx[j];
+      x[j] += nx[j];
+      tn += nx[j] * nx[j];
+      xn += x[j] * x[j];
+    }
+    tn = block_sum_dyn(tn, red);
+    xn = block_sum_dyn(xn, red);
+    if (tid == 0) sh_done = (tn <= 1e-34 * xn) ? 1 : (!(tn <= 1e300) ? 2 : 0);
+    __syncthreads();
+    conv = sh_done != 0;
+  }
+  if (sh_done != 1) {  // Gaussian elimination with partial pivoting
+    const int ld = r + 1;
+    for (int e = tid; e < r * r; e += blockDim.x) sa[(e / r) * ld + (e % r)] = G[e];
+    for (int i = tid; i < r; i += blockDim.x) sa[i * ld + r] = c[i];
+    __syncthreads();
+    for (int k = 0; k < r; ++k) {
+      if (tid == 0) {
+        int pv = k;
+        double best = fabs(sa[k * ld + k]);
+        for (int i = k + 1; i < r; ++i)
+          if (fabs(sa[i * ld + k]) > best) {
+            best = fabs(sa[i * ld + k]);
+            pv = i;
+          }
+        piv_sh = pv;
+      }
+      __syncthreads();
+      const int pv = piv_sh;
+      if (pv != k)
+        for (int j = tid; j <= r; j += blockDim.x) {
+          const double tt = sa[k * ld + j];
+          sa[k * ld + j] = sa[pv * ld + j];
+          sa[pv * ld + j] = tt;
+        }
+      __syncthreads();
+      const double akk = sa[k * ld + k];
+      const int m = r - k - 1;
+      for (int e = tid; e < m * (m + 1); e += blockDim.x) {
+        const int i = k + 1 + e / (m + 1), j = k + 1 + e % (m + 1);
+        sa[i * ld + j] -= (sa[i * ld + k] / akk) * sa[k * ld + j];
+      }
+      __syncthreads();
+    }
+    if (tid == 0)
+      for (int i = r - 1; i >= 0; --i) {
+        double sacc = sa[i * ld + r];
+        for (int j = i + 1; j < r; ++j) sacc -= sa[i * ld + j] * x[j];
+        x[i] = sacc / sa[i * ld + i];
+      }
+    __syncthreads();
+  }
+  // G x, the new residual's coefficients and norm
+  for (int i = tid; i < r; i += blockDim.x) {
+    double sacc = 0.0;
+    for (int k = 0; k < r; ++k) sacc = fma(G[i * r + k], x[k], sacc);
+    nx[i] = sacc;
+  }
+  __syncthreads();
+  double xc = 0.0, xgx = 0.0, xx = 0.0;
+  for (int j = tid; j < r; j += blockDim.x) {
+    xc += x[j] * c[j];
+    xgx += x[j] * nx[j];
+    xx += x[j] * x[j];
+  }
+  xc = block_sum_dyn(xc, red);
+  xgx = block_sum_dyn(xgx, red);
+  xx = block_sum_dyn(xx, red);
+  for (int j = tid; j < r; j += blockDim.x) {
+    p[j] += x[j];
+    p2[j] = x[j];
+    red2[j] = c[j] - nx[j];
+  }
+  if (tid == 0) {
+    const double qq = red2[r] - 2.0 * xc + xgx;
+    red2[r] = qq > 0.0 ? qq : 0.0;
+    if (p2norm) *p2norm = sqrt(xx);
+  }
+}
+
+int isvd_refine_launch(adrom_ctx* ctx, const double* G, int r, double* red2, double* p,
+                       double* p2, double* p2norm, const int* need) {
+  if (r > 128) return set_error(ctx, ADROM_ERR_ARG, "isvd refine: rank %d > 128", r);
+  const size_t sm = sizeof(double) * (size_t)r * (r + 1);
+  cudaFuncSetAttribute(isvd_refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  isvd_refine_kernel<<<1, 256, sm, ctx->stream>>>(G, r, red2, p, p2, p2norm, need);
+  ADROM_LAUNCH_CK(ctx);
+  return ADROM_OK;
+}
+
+__global__ void set_need_kernel(int* need) { need[0] = 1; }
 
 static int isvd_solve_direct_launch(adrom_ctx* ctx, const double* red1, const double* G, int r,
                                     double ratio, double* p, int* need) {
@@ -1413,6 +1544,7 @@ int isvd_update_async(adrom_ctx* ctx, const double* phi, const double* sigma, co
   double* red1 = (double*)take(sizeof(double) * (r_cur + 1));
   double* red2 = (double*)take(sizeof(double) * (r_cur + 1));
   double* pls = (double*)take(sizeof(double) * r_cur);
+  double* p2 = (double*)take(sizeof(double) * r_cur);
   double* B = (double*)take(sizeof(double) * (r_cur + 1) * r);
   double* T = (double*)take(sizeof(double) * (r_cur + 1) * r);
   double* Gloc = (double*)take(sizeof(double) * r_cur * r_cur);
@@ -1442,10 +1574,16 @@ int isvd_update_async(adrom_ctx* ctx, const double* phi, const double* sigma, co
   ADROM_LAUNCH_CK(ctx);
   st = isvd_solve_direct_launch(ctx, red1, G, r_cur, reorth_ratio, pls, need);
   if (st) return st;
-  // pass 2 (only if ||y||^2 - p.p1 would cancel): q = y - Phi p, Phi^T q, ||q||^2
+  // pass 2 always: q = y - Phi p, Phi^T q, ||q||^2, then one least-squares
+  // refinement step (isvd_refine_kernel: q' = q - Phi p2 orthogonal to the
+  // actual basis; the rotation forms q_hat = (q - Phi p2) / ||q'||)
+  set_need_kernel<<<1, 1, 0, ctx->stream>>>(need);
+  ADROM_LAUNCH_CK(ctx);
   pr = prof_begin(ctx, PROBE_ISVD_RESID);
   st = ts_residual(ctx, phi, n, r_cur, pls, y, red2, partial, flag, need, qbuf);
   prof_end(ctx, pr);
+  if (st) return st;
+  st = isvd_refine_launch(ctx, G, r_cur, red2, pls, p2, nullptr, need);
   if (st) return st;
   const bool vg = core_v_global(r_cur);
   const size_t csm = core_smem(r_cur, vg);
@@ -1468,6 +1606,7 @@ int isvd_update_async(adrom_ctx* ctx, const double* phi, const double* sigma, co
   // the rotation reads q from pass 2 when it ran, else forms it from y and p
   RotArgs ra{phi, y, qbuf, need, pls, qinv, B, n, r_cur, r, phi_out};
   if (fuse) ra.fuse = *fuse;
+  ra.p2 = p2;
   pr = prof_begin(ctx, PROBE_ISVD_ROTATE);
   st = ts_rotate(ctx, ra);
   prof_end(ctx, pr);
@@ -1483,7 +1622,6 @@ int isvd_solve_launch(adrom_ctx* ctx, const double* red1, const double* G, int r
   return ADROM_OK;
 }
 
-__global__ void set_need_kernel(int* need) { need[0] = 1; }
 
 int isvd_core_launch(adrom_ctx* ctx, const double* sigma, const double* red1, const double* pls,
                      const double* red2, const int* need, const double* G, int r, double lam,

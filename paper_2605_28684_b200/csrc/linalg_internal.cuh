@@ -67,6 +67,9 @@ __global__ void reduce_partials_kernel(const double* __restrict__ partial, int n
 __global__ void set_need_kernel(int* need);
 int isvd_solve_launch(adrom_ctx* ctx, const double* red1, const double* G, int r, double* p,
                       int* need);
+// least-squares refinement after the explicit residual pass (linalg.cu)
+int isvd_refine_launch(adrom_ctx* ctx, const double* G, int r, double* red2, double* p,
+                       double* p2, double* p2norm, const int* need);
 int isvd_core_launch(adrom_ctx* ctx, const double* sigma, const double* red1, const double* pls,
                      const double* red2, const int* need, const double* G, int r, double lam,
                      double* B, double* qinv, double* T, double* Gout, double* sigma_out,
