@@ -1670,6 +1670,9 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
                          "rank deficiency at pivot step %d (residual column norm %.3e)",
                          chosen + hstate[2] - 1, hres[0]);
       const int knew = hstate[0];
+      if (getenv("ADROM_QDEIM_TRACE") && atoi(getenv("ADROM_QDEIM_TRACE")) >= 1)
+        fprintf(stderr, "qdeim round %d: k %d -> %d (refresh %lld rows)\n", rounds, k, knew,
+                (long long)rl_n);
       if (knew == k) {
         if (!all && mref < n) {  // stale bounds block progress: refresh more rows
           mref = (mref * 4 < n) ? mref * 4 : n;
