@@ -120,6 +120,19 @@ struct adrom_ctx {
   // a helper context (own stream) that records its probes into the parent's
   // probe table, e.g. the session's coarse-step stream
   adrom_ctx* prof_parent = nullptr;
+  // small device -> pinned-host copies that ride on the NEXT host
+  // synchronisation of this stream instead of forcing their own (the
+  // session's per-event status words): ride_add() registers one,
+  // ride_flush() enqueues them (called right before a stream synchronise and
+  // before the device words are reset); ride_done counts flushed batches
+  struct Ride {
+    const void* src;
+    void* dst;
+    size_t bytes;
+  };
+  Ride rides[4];
+  int n_rides = 0;
+  long long ride_done = 0;
 };
 
 #define ADROM_PROF_SLOTS 8192
@@ -135,6 +148,18 @@ void* scratch(adrom_ctx* ctx, size_t bytes, size_t offset_bytes = 0);
 int ensure_scratch(adrom_ctx* ctx, size_t bytes);
 int ensure_aux(adrom_ctx* ctx, size_t bytes);
 int ensure_pinned(adrom_ctx* ctx, size_t bytes);
+inline void ride_add(adrom_ctx* ctx, const void* src, void* dst, size_t bytes) {
+  if (ctx->n_rides < 4) ctx->rides[ctx->n_rides++] = adrom_ctx::Ride{src, dst, bytes};
+}
+// enqueue the registered copies on the context's stream (no synchronisation)
+inline void ride_flush(adrom_ctx* ctx) {
+  if (!ctx->n_rides) return;
+  for (int i = 0; i < ctx->n_rides; ++i)
+    cudaMemcpyAsync(ctx->rides[i].dst, ctx->rides[i].src, ctx->rides[i].bytes,
+                    cudaMemcpyDeviceToHost, ctx->stream);
+  ctx->n_rides = 0;
+  ++ctx->ride_done;
+}
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 // upper bound on the blocks of any reduction kernel (rows of a partials buffer)
 inline int partial_rows(const adrom_ctx* ctx) { return ctx->num_sms * 4; }

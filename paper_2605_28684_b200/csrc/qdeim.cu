@@ -159,17 +159,33 @@ __global__ void qs_init_kernel(SelState* st, long long M, unsigned int* hist) {
   for (int j = threadIdx.x; j < QS_BINS; j += blockDim.x) hist[j] = 0u;
 }
 
-// histogram of the next digit over the candidates vals[0..n) (contiguous:
-// the bounds of every row, or of the refresh list's rows in list order)
-__global__ void __launch_bounds__(256) qs_hist_kernel(const double* __restrict__ vals, int64_t n,
-                                                      const SelState* __restrict__ st, int shift,
-                                                      unsigned int* __restrict__ hist) {
-  if (st->done) return;
+// ---------------------------------------------------------------------------
+// The whole selection in ONE cooperative launch: up to six histogram passes
+// (two grid barriers each: histogram -> digit choice by block 0), the stream
+// compaction of the selected rows and the -1 fill of the unused output
+// slots.  The separate kernels above cost 15 dependent launches per
+// selection (7 selections per configuration-3 event), most of them early
+// exits; here a finished selection leaves the pass loop at once.
+// `hist` must be zero on entry (every digit step leaves it zeroed).
+// ---------------------------------------------------------------------------
+struct SelArgs {
+  const double* vals;   // candidates' bounds (contiguous)
+  int64_t n;
+  const int64_t* list;  // candidate slot -> row (null: identity)
+  SelState* st;
+  unsigned int* hist;
+  long long M;          // rows wanted
+  long long cap;        // output capacity
+  int extend;
+  int64_t* out;         // cap slots; unused ones -> -1
+};
+
+__device__ __forceinline__ void qs_hist_pass(const double* vals, int64_t n,
+                                             unsigned long long prefix, unsigned long long mask,
+                                             int shift, unsigned int* hist, unsigned int* sh) {
   constexpr int ITEMS = 8;
-  __shared__ unsigned int sh[QS_BINS];
   for (int b = threadIdx.x; b < QS_BINS; b += blockDim.x) sh[b] = 0u;
   __syncthreads();
-  const unsigned long long prefix = st->prefix, mask = st->mask;
   const unsigned long long dmask = (1ull << qs_bits(shift)) - 1ull;
   const int lane = threadIdx.x & 31;
   const int64_t tile = (int64_t)blockDim.x * ITEMS;
@@ -178,13 +194,12 @@ __global__ void __launch_bounds__(256) qs_hist_kernel(const double* __restrict__
 #pragma unroll
     for (int q = 0; q < ITEMS; ++q) {
       const int64_t j = t0 + (int64_t)q * blockDim.x + threadIdx.x;
-      v[q] = (j < n) ? vals[j] : -1.0;
+      v[q] = (j < n) ? __ldg(vals + j) : -1.0;
     }
 #pragma unroll
     for (int q = 0; q < ITEMS; ++q) {
       const unsigned long long k = qp_key(v[q]);
       const int dig = (k != 0ull && (k & mask) == prefix) ? (int)((k >> shift) & dmask) : -1;
-      // bounds crowd into a few bins: aggregate equal digits per warp first
       const int d0 = __shfl_sync(0xffffffffu, dig, 0);
       if (__all_sync(0xffffffffu, dig == d0)) {
         if (lane == 0 && d0 >= 0) atomicAdd(&sh[d0], 32u);
@@ -201,21 +216,21 @@ __global__ void __launch_bounds__(256) qs_hist_kernel(const double* __restrict__
   }
 }
 
-// one block of 1024 (4 bins each, from the top): pick the digit holding the
-// need-th largest remaining key
-__global__ void __launch_bounds__(1024) qs_digit_kernel(SelState* st, int shift,
-                                                        unsigned int* __restrict__ hist,
-                                                        long long pcap, int extend) {
-  if (st->done) return;
-  __shared__ long long wsum[32];
-  __shared__ int dig_sh, dlow_sh;
-  __shared__ long long excl_sh, bin_sh;
+// digit choice of one pass by ONE block of NT threads (QS_BINS / NT bins per
+// thread, from the top): pick the digit holding the need-th largest remaining
+// key; the pool may take every bin from the top down to the lowest one whose
+// cumulative count still fits the capacity (and holds the need-th key)
+template <int NT>
+__device__ __forceinline__ void qs_digit_step(volatile SelState* st, int shift, unsigned int* hist,
+                                              long long pcap, int extend, long long* wsum,
+                                              int* ish, long long* lsh) {
+  constexpr int BPT = QS_BINS / NT;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  long long hb[4];
+  long long hb[BPT];
   long long h = 0;
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    hb[e] = hist[QS_BINS - 1 - (4 * tid + e)];
+  for (int e = 0; e < BPT; ++e) {
+    hb[e] = __ldcg(hist + (QS_BINS - 1 - (BPT * tid + e)));
     h += hb[e];
   }
   long long v = h;
@@ -226,8 +241,8 @@ __global__ void __launch_bounds__(1024) qs_digit_kernel(SelState* st, int shift,
   }
   if (lane == 31) wsum[warp] = v;
   if (tid == 0) {
-    dig_sh = -1;
-    dlow_sh = QS_BINS;
+    ish[0] = -1;        // digit
+    ish[1] = QS_BINS;   // lowest bin that still fits
   }
   __syncthreads();
   long long off = 0;
@@ -235,105 +250,144 @@ __global__ void __launch_bounds__(1024) qs_digit_kernel(SelState* st, int shift,
   const long long incl = v + off;
   long long excl = incl - h;
   const long long need = st->need;
-  // the pool may take every bin from the top down to the lowest one whose
-  // cumulative count still fits the capacity (and holds the need-th key)
   if (extend) {
     const long long limit = pcap - st->above;
     long long c = excl;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
+    for (int e = 0; e < BPT; ++e) {
       c += hb[e];
-      if (hb[e] > 0 && c >= need && c <= limit) atomicMin(&dlow_sh, QS_BINS - 1 - (4 * tid + e));
+      if (hb[e] > 0 && c >= need && c <= limit) atomicMin(&ish[1], QS_BINS - 1 - (BPT * tid + e));
     }
   }
   if (excl < need && incl >= need) {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
+    for (int e = 0; e < BPT; ++e) {
       if (excl < need && excl + hb[e] >= need) {
-        dig_sh = QS_BINS - 1 - (4 * tid + e);
-        excl_sh = excl;
-        bin_sh = hb[e];
+        ish[0] = QS_BINS - 1 - (BPT * tid + e);
+        lsh[0] = excl;
+        lsh[1] = hb[e];
       }
       excl += hb[e];
     }
   }
   __syncthreads();
 #pragma unroll
-  for (int e = 0; e < 4; ++e) hist[4 * tid + e] = 0u;  // ready for the next pass
+  for (int e = 0; e < BPT; ++e) hist[BPT * tid + e] = 0u;  // ready for the next pass / selection
   if (tid == 0) {
-    if (dig_sh < 0) {  // fewer candidates than M: take every live row
+    const int dig = ish[0], dlow = ish[1];
+    if (dig < 0) {  // fewer candidates than M: take every live row
       st->theta = 1ull;
       st->tau = -1.0;
       st->done = 1;
-      return;
-    }
-    if (dlow_sh < QS_BINS) {  // bins dlow.. of this prefix fit: done
-      const unsigned long long th = st->prefix | ((unsigned long long)dlow_sh << shift);
+    } else if (dlow < QS_BINS) {  // bins dlow.. of this prefix fit: done
+      const unsigned long long th = st->prefix | ((unsigned long long)dlow << shift);
       st->theta = th < 1ull ? 1ull : th;
-      st->tau = (st->theta >= 2ull) ? __longlong_as_double((long long)(st->theta - 2ull)) : -1.0;
+      st->tau = (th >= 2ull) ? __longlong_as_double((long long)(th - 2ull)) : -1.0;
       st->done = 1;
-      return;
-    }
-    const unsigned long long d = (unsigned long long)dig_sh;
-    st->prefix |= d << shift;
-    st->mask |= ((1ull << qs_bits(shift)) - 1ull) << shift;
-    st->above += excl_sh;
-    st->need = need - excl_sh;
-    const long long with_bin = st->above + bin_sh;
-    if (with_bin <= pcap || shift == 0) {
-      // take the whole bin if it fits, else (last digit: exact ties) only above it
-      const unsigned long long lo = st->prefix;  // smallest key carrying the prefix
-      const unsigned long long th = (with_bin <= pcap) ? lo : lo + 1ull;
-      st->theta = th < 1ull ? 1ull : th;
-      // largest key outside: theta - 1 -> bound bits theta - 2
-      st->tau = (st->theta >= 2ull) ? __longlong_as_double((long long)(st->theta - 2ull)) : -1.0;
-      st->done = 1;
+    } else {
+      const unsigned long long pre = st->prefix | ((unsigned long long)dig << shift);
+      st->prefix = pre;
+      st->mask = st->mask | (((1ull << qs_bits(shift)) - 1ull) << shift);
+      const long long above = st->above + lsh[0];
+      st->above = above;
+      st->need = need - lsh[0];
+      const long long with_bin = above + lsh[1];
+      if (with_bin <= pcap || shift == 0) {
+        const unsigned long long th0 = (with_bin <= pcap) ? pre : pre + 1ull;
+        const unsigned long long th = th0 < 1ull ? 1ull : th0;
+        st->theta = th;
+        st->tau = (th >= 2ull) ? __longlong_as_double((long long)(th - 2ull)) : -1.0;
+        st->done = 1;
+      }
     }
   }
+  __syncthreads();
 }
 
-// rows with key >= theta -> out[0..), one atomic per block and round
-__global__ void __launch_bounds__(256) qs_compact_kernel(const double* __restrict__ vals, int64_t n,
-                                                         const int64_t* __restrict__ list,
-                                                         SelState* __restrict__ st,
-                                                         int64_t* __restrict__ out, long long cap) {
-  constexpr int ITEMS = 4;
-  __shared__ int wcnt[8];
-  __shared__ unsigned long long base_sh;
-  const unsigned long long theta = st->theta;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t tile = (int64_t)blockDim.x * ITEMS;
-  for (int64_t t0 = blockIdx.x * tile; t0 < n; t0 += (int64_t)gridDim.x * tile) {
-    int64_t rows[ITEMS];
-    unsigned int balls[ITEMS];
-    int mine = 0;
-#pragma unroll
-    for (int q = 0; q < ITEMS; ++q) {
-      const int64_t j = t0 + (int64_t)q * blockDim.x + threadIdx.x;
-      const bool take = j < n && qp_key(vals[j]) >= theta;
-      rows[q] = take ? (list ? list[j] : j) : -1;
-      balls[q] = __ballot_sync(0xffffffffu, take);
-      mine += __popc(balls[q]);
+__global__ void __launch_bounds__(256) qs_select_compact_kernel(SelArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ unsigned int sh[QS_BINS];
+  __shared__ long long wsum[8];
+  __shared__ int ish[2];
+  __shared__ long long lsh[2];
+  volatile SelState* st = a.st;
+  for (int pass = 0; pass < 6; ++pass) {
+    const int shift = (pass == 5) ? 0 : 52 - QS_BITS * pass;
+    unsigned long long prefix = 0ull, mask = 0ull;
+    if (pass > 0) {
+      prefix = st->prefix;
+      mask = st->mask;
     }
-    if (lane == 0) wcnt[warp] = mine;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int tot = 0;
-      for (int w = 0; w < 8; ++w) tot += wcnt[w];
-      base_sh = tot ? atomicAdd(&st->count, (unsigned long long)tot) : 0ull;
-    }
-    __syncthreads();
-    unsigned long long pos = base_sh;
-    for (int w = 0; w < warp; ++w) pos += wcnt[w];
-#pragma unroll
-    for (int q = 0; q < ITEMS; ++q) {
-      if (rows[q] >= 0) {
-        const unsigned long long slot = pos + __popc(balls[q] & ((1u << lane) - 1u));
-        if ((long long)slot < cap) out[slot] = rows[q];
+    qs_hist_pass(a.vals, a.n, prefix, mask, shift, a.hist, sh);
+    grid.sync();
+    if (blockIdx.x == 0) {
+      if (pass == 0) {
+        if (threadIdx.x == 0) {
+          st->prefix = 0ull;
+          st->mask = 0ull;
+          st->theta = 1ull;
+          st->above = 0;
+          st->need = a.M;
+          st->done = 0;
+          st->tau = -1.0;
+          st->count = 0ull;
+        }
+        __syncthreads();
       }
-      pos += __popc(balls[q]);
+      qs_digit_step<256>(st, shift, a.hist, a.cap, a.extend, wsum, ish, lsh);
+      __threadfence();
     }
-    __syncthreads();
+    grid.sync();
+    if (st->done) break;
+  }
+  // compaction: rows with key >= theta -> out[0..), one atomic per block and tile
+  {
+    constexpr int ITEMS = 4;
+    int* wcnt = reinterpret_cast<int*>(sh);
+    unsigned long long* base_sh = reinterpret_cast<unsigned long long*>(sh + 16);
+    const unsigned long long theta = st->theta;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t tile = (int64_t)blockDim.x * ITEMS;
+    for (int64_t t0 = blockIdx.x * tile; t0 < a.n; t0 += (int64_t)gridDim.x * tile) {
+      int64_t rows[ITEMS];
+      unsigned int balls[ITEMS];
+      int mine = 0;
+#pragma unroll
+      for (int q = 0; q < ITEMS; ++q) {
+        const int64_t j = t0 + (int64_t)q * blockDim.x + threadIdx.x;
+        const bool take = j < a.n && qp_key(__ldg(a.vals + j)) >= theta;
+        rows[q] = take ? (a.list ? a.list[j] : j) : -1;
+        balls[q] = __ballot_sync(0xffffffffu, take);
+        mine += __popc(balls[q]);
+      }
+      if (lane == 0) wcnt[warp] = mine;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int tot = 0;
+        for (int w = 0; w < 8; ++w) tot += wcnt[w];
+        *base_sh = tot ? atomicAdd((unsigned long long*)&a.st->count, (unsigned long long)tot) : 0ull;
+      }
+      __syncthreads();
+      unsigned long long pos = *base_sh;
+      for (int w = 0; w < warp; ++w) pos += wcnt[w];
+#pragma unroll
+      for (int q = 0; q < ITEMS; ++q) {
+        if (rows[q] >= 0) {
+          const unsigned long long slot = pos + __popc(balls[q] & ((1u << lane) - 1u));
+          if ((long long)slot < a.cap) a.out[slot] = rows[q];
+        }
+        pos += __popc(balls[q]);
+      }
+      __syncthreads();
+    }
+  }
+  grid.sync();
+  {
+    const unsigned long long cnt = st->count;
+    const long long from = (long long)cnt < a.cap ? (long long)cnt : a.cap;
+    for (int64_t i = from + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.cap;
+         i += (int64_t)gridDim.x * blockDim.x)
+      a.out[i] = -1;
   }
 }
 
@@ -467,13 +521,6 @@ __global__ void __launch_bounds__(256) qp_rows_kernel(const double* __restrict__
       }
     }
   }
-}
-
-// -1 in every pool slot (rows with fewer than T valid candidates keep -1)
-__global__ void qp_fill_kernel(int64_t* __restrict__ p, int64_t P) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
-       i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = -1;
 }
 
 // ---------------------------------------------------------------------------
@@ -1437,6 +1484,20 @@ static int qp_resvec(adrom_ctx* ctx, const double* phi, int r, const int64_t* po
   return ADROM_OK;
 }
 
+// diagnostics (ADROM_QDEIM_TRACE >= 2): rows whose bound exceeds g / 4^j
+__global__ void qp_count_above_kernel(const double* __restrict__ bnd2, int64_t n, double g,
+                                      unsigned long long* __restrict__ cnt) {
+  unsigned long long c[4] = {0, 0, 0, 0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double b = bnd2[i];
+    double t = g;
+    for (int j = 0; j < 4; ++j, t *= 0.25) c[j] += b > t;
+  }
+  for (int j = 0; j < 4; ++j)
+    if (c[j]) atomicAdd(&cnt[j], c[j]);
+}
+
 void qdeim_seed_buffers(void* ws, int64_t n, double** res2, double** bnd2, unsigned char** ver) {
   char* w = (char*)ws;
   *res2 = (double*)w;
@@ -1529,22 +1590,23 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
     QP_RV(128, false);
 #undef QP_RV
   };
-  const int sg = ctx->num_sms * 4;
-  // theta/tau of the rows holding the M largest bounds (<= cap rows taken)
-  auto select = [&](SelState* st, const double* vals, int64_t nn, long long M,
-                    long long cap, int extend) -> int {
-    qs_init_kernel<<<1, 256, 0, ctx->stream>>>(st, M, hist);
-    ADROM_LAUNCH_CK(ctx);
+  // theta/tau of the rows holding the M largest bounds (<= cap rows taken),
+  // compacted into out[0..cap) (unused slots -1): one cooperative launch
+  int sbpm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sbpm, qs_select_compact_kernel, 256, 0);
+  if (sbpm < 1) return set_error(ctx, ADROM_ERR_CUDA, "qdeim: selection kernel cannot be resident");
+  const int sgrid_max = ctx->num_sms * (sbpm < 4 ? sbpm : 4);
+  ADROM_CK(ctx, cudaMemsetAsync(hist, 0, sizeof(unsigned int) * QS_BINS, ctx->stream));
+  auto select_compact = [&](SelState* st, const double* vals, int64_t nn, const int64_t* list,
+                            long long M, long long cap, int extend, int64_t* out) -> int {
     int64_t hg = (nn + 2047) / 2048;
-    if (hg > sg) hg = sg;
-    for (int shift = 64 - QS_BITS;; shift -= QS_BITS) {
-      if (shift < 0) shift = 0;
-      qs_hist_kernel<<<(int)(hg < 1 ? 1 : hg), 256, 0, ctx->stream>>>(vals, nn, st, shift, hist);
-      ADROM_LAUNCH_CK(ctx);
-      qs_digit_kernel<<<1, 1024, 0, ctx->stream>>>(st, shift, hist, cap, extend);
-      ADROM_LAUNCH_CK(ctx);
-      if (shift == 0) break;
-    }
+    if (hg > sgrid_max) hg = sgrid_max;
+    if (hg < 1) hg = 1;
+    SelArgs sa{vals, nn, list, st, hist, M, cap, extend, out};
+    void* args[] = {&sa};
+    ADROM_CK(ctx, cudaLaunchCooperativeKernel((void*)qs_select_compact_kernel, (int)hg, 256, args, 0,
+                                              ctx->stream));
+    ++ctx->launches;
     return ADROM_OK;
   };
   const long long M = qp_pool_m();
@@ -1577,14 +1639,8 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
         // refresh the mref rows with the largest (possibly stale) bounds
         const long long capm = mref + (mref * qp_refresh_slack()) / 100;
         const long long cap = (capm < n) ? capm : n;
-        st = select(selR, bnd2, n, mref, cap, qp_extend_refresh());
+        st = select_compact(selR, bnd2, n, nullptr, mref, cap, qp_extend_refresh(), rlist);
         if (st) return st;
-        int64_t fg = (cap + 255) / 256;
-        if (fg > ctx->num_sms * 8) fg = ctx->num_sms * 8;
-        qp_fill_kernel<<<(int)fg, 256, 0, ctx->stream>>>(rlist, cap);
-        ADROM_LAUNCH_CK(ctx);
-        qs_compact_kernel<<<sg, 256, 0, ctx->stream>>>(bnd2, n, nullptr, selR, rlist, cap);
-        ADROM_LAUNCH_CK(ctx);
         if (getenv("ADROM_QDEIM_TRACE") && atoi(getenv("ADROM_QDEIM_TRACE")) >= 2) {
           // refresh work: direction tiles of 8 computed per 8-row tile vs per row
           std::vector<int64_t> hl(cap);
@@ -1645,12 +1701,8 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
         const int64_t* cl = rl_n ? rlist : nullptr;
         const double* cv = rl_n ? blist : bnd2;
         const int64_t cn = rl_n ? rl_n : n;
-        st = select(sel, cv, cn, M, (long long)P, 1);
+        st = select_compact(sel, cv, cn, cl, M, (long long)P, 1, pool_idx);
         if (st) return st;
-        qp_fill_kernel<<<(int)gg, 256, 0, ctx->stream>>>(pool_idx, P);
-        ADROM_LAUNCH_CK(ctx);
-        qs_compact_kernel<<<sg, 256, 0, ctx->stream>>>(cv, cn, cl, sel, pool_idx, (long long)P);
-        ADROM_LAUNCH_CK(ctx);
       }
       st = resvec(k);
       if (st) return st;
@@ -1664,6 +1716,7 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
                                     ctx->stream));
       ADROM_CK(ctx, cudaMemcpyAsync(hres, err_res, sizeof(double), cudaMemcpyDeviceToHost,
                                     ctx->stream));
+      ride_flush(ctx);  // the caller's pending status words share this round trip
       ADROM_CK(ctx, cudaStreamSynchronize(ctx->stream));
       if (hstate[2])
         return set_error(ctx, ADROM_ERR_SINGULAR,
@@ -1673,6 +1726,24 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
       if (getenv("ADROM_QDEIM_TRACE") && atoi(getenv("ADROM_QDEIM_TRACE")) >= 1)
         fprintf(stderr, "qdeim round %d: k %d -> %d (refresh %lld rows)\n", rounds, k, knew,
                 (long long)rl_n);
+      if (getenv("ADROM_QDEIM_TRACE") && atoi(getenv("ADROM_QDEIM_TRACE")) >= 2 && !all) {
+        unsigned long long* dc = nullptr;
+        unsigned long long hc[4];
+        double taus[2];
+        cudaMalloc(&dc, sizeof(hc));
+        cudaMemsetAsync(dc, 0, sizeof(hc), ctx->stream);
+        const double g2 = hres[0] * hres[0];
+        qp_count_above_kernel<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(bnd2, n, g2, dc);
+        cudaMemcpyAsync(hc, dc, sizeof(hc), cudaMemcpyDeviceToHost, ctx->stream);
+        cudaMemcpyAsync(&taus[0], &sel->tau, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+        cudaMemcpyAsync(&taus[1], &selR->tau, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+        cudaStreamSynchronize(ctx->stream);
+        cudaFree(dc);
+        fprintf(stderr,
+                "  stop residual^2 g=%.3e tau_pool=%.3e tau_outside=%.3e rows with bound > g, g/4, "
+                "g/16, g/64: %llu %llu %llu %llu\n",
+                g2, taus[0], taus[1], hc[0], hc[1], hc[2], hc[3]);
+      }
       if (knew == k) {
         if (!all && mref < n) {  // stale bounds block progress: refresh more rows
           mref = (mref * 4 < n) ? mref * 4 : n;

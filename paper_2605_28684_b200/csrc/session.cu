@@ -30,9 +30,14 @@ namespace {
 // on the coarse-step stream, reset there before the pass)
 constexpr int PASS_A_FLAG = 20;
 
+// pinned staging slots of the status words that ride on a later
+// synchronisation (ride_add): iSVD statistics, iSVD flags, reduced-step flag
+constexpr size_t PIN_STATS = 512, PIN_ISVD_FLAGS = 1024, PIN_FAIL_STEP = 1280;
+
 int read_flags(adrom_ctx* ctx, int* host_flags) {
   ADROM_CK(ctx, cudaMemcpyAsync(ctx->pinned, ctx->dflags, sizeof(int) * 24,
                                 cudaMemcpyDeviceToHost, ctx->stream));
+  ride_flush(ctx);
   ADROM_CK(ctx, cudaStreamSynchronize(ctx->stream));
   int tmp[24];
   memcpy(tmp, ctx->pinned, sizeof(int) * 24);
@@ -42,6 +47,7 @@ int read_flags(adrom_ctx* ctx, int* host_flags) {
 }
 
 int reset_flags(adrom_ctx* ctx) {
+  ride_flush(ctx);  // pending copies of the words read them before the reset
   ADROM_CK(ctx, cudaMemsetAsync(ctx->dflags, 0, sizeof(int) * 16, ctx->stream));
   return ADROM_OK;
 }
@@ -158,6 +164,7 @@ struct adrom_session {
   int64_t n_down = 0;
   double* step_log = nullptr;    // n_t_online x 3
   int* fail_step = nullptr;
+  bool fail_step_read = false;  // the last event brought fail_step back with its status words
   int64_t n_online = 0;          // steps done
   int64_t cap_steps = 0;
   std::vector<adrom_event_record> events;
@@ -512,27 +519,37 @@ int run_event_factored(adrom_session* s, adrom_event_record& ev, bool* decoded) 
   if (st) return st;
   *decoded = true;
   s->nrm2_exact = true;  // pass 1 made nrm2[cur] exact for the current basis
-  int flags[16];
-  ADROM_CK(ctx, cudaMemcpyAsync((char*)ctx->pinned + 512, s->isvd_stats, sizeof(double) * 8,
-                                cudaMemcpyDeviceToHost, ctx->stream));
-  st = read_flags(ctx, flags);
-  if (st) return st;
-  const double* hs = (const double*)((char*)ctx->pinned + 512);
-  if (flags[0] & 1) {
+  // the iSVD's status words ride on the sampling stage's first host
+  // synchronisation (a QDEIM round); the sampling and the operator write only
+  // spare buffers, so a failed update costs nothing but their time
+  ride_add(ctx, s->isvd_stats, (char*)ctx->pinned + PIN_STATS, sizeof(double) * 8);
+  ride_add(ctx, ctx->dflags, (char*)ctx->pinned + PIN_ISVD_FLAGS, sizeof(int) * 24);
+  const FactBasis b2{s->phi[s->acur], s->Qb, s->r, b.k + 1, s->Wd[nxt], s->N, s->A32[s->acur]};
+  const int onx = 1 - s->opcur;
+  // the reduced step's failure flag shares the operator's final read
+  ride_add(ctx, s->fail_step, (char*)ctx->pinned + PIN_FAIL_STEP, sizeof(int));
+  st = build_sampling_operator(s, nullptr, s->op[onx], s->y_corr, true, &b2, s->nrm2[nxt]);
+  if (st == ADROM_ERR_CUDA) return st;
+  if (st) {  // an error return may precede the stage's synchronisation
+    ride_flush(ctx);
+    ADROM_CK(ctx, cudaStreamSynchronize(ctx->stream));
+  }
+  s->fail_step_read = true;  // pinned + PIN_FAIL_STEP holds this step's flag
+  const double* hs = (const double*)((char*)ctx->pinned + PIN_STATS);
+  int iflags[24];
+  memcpy(iflags, (char*)ctx->pinned + PIN_ISVD_FLAGS, sizeof(iflags));
+  iflags[0] |= iflags[PASS_A_FLAG];
+  if (iflags[0] & 1) {
     ev.error = ADROM_ERR_NONFINITE;
     return ADROM_OK;
   }
-  if (flags[0] & 8) {
+  if (iflags[0] & 8) {
     ev.error = ADROM_ERR_NOCONV;
     return ADROM_OK;
   }
   ev.residual_norm = hs[2];
   if (getenv("ADROM_DEBUG_CORE"))
     fprintf(stderr, "core: sweeps %g converged %g fallback %g\n", hs[5], hs[6], hs[7]);
-  const FactBasis b2{s->phi[s->acur], s->Qb, s->r, b.k + 1, s->Wd[nxt], s->N, s->A32[s->acur]};
-  const int onx = 1 - s->opcur;
-  st = build_sampling_operator(s, nullptr, s->op[onx], s->y_corr, true, &b2, s->nrm2[nxt]);
-  if (st == ADROM_ERR_CUDA) return st;
   if (st) {
     ev.error = st;
     return ADROM_OK;
@@ -923,10 +940,15 @@ int adrom_session_advance(adrom_session* s, int64_t n_steps, int64_t save_every,
       s->events.push_back(ev);
       // a failed reduced step aborts the run like the reference (driver.py:338)
       int fs = -1;
-      ADROM_CK(ctx, cudaMemcpyAsync(ctx->pinned, s->fail_step, sizeof(int),
-                                    cudaMemcpyDeviceToHost, ctx->stream));
-      ADROM_CK(ctx, cudaStreamSynchronize(ctx->stream));
-      memcpy(&fs, ctx->pinned, sizeof(int));
+      if (s->fail_step_read) {  // came back with the event's own status words
+        memcpy(&fs, (char*)ctx->pinned + PIN_FAIL_STEP, sizeof(int));
+        s->fail_step_read = false;
+      } else {
+        ADROM_CK(ctx, cudaMemcpyAsync(ctx->pinned, s->fail_step, sizeof(int),
+                                      cudaMemcpyDeviceToHost, ctx->stream));
+        ADROM_CK(ctx, cudaStreamSynchronize(ctx->stream));
+        memcpy(&fs, ctx->pinned, sizeof(int));
+      }
       if (fs >= 0)
         return set_error(ctx, ADROM_ERR_ROMSTEP, "rank-deficient sampled Jacobian at online step %d",
                          fs + (int)s->cfg.w_init + 1);
