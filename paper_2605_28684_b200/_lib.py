@@ -132,7 +132,8 @@ SIGNATURES = {
 }
 
 PROBES = ["isvd_rotate", "isvd_project", "isvd_resid", "isvd_core", "fom_residual",
-          "fom_jacobian", "fom_solve", "qdeim_round", "rom_step", "decode", "operator", "encode"]
+          "fom_jacobian", "fom_solve", "qdeim_round", "rom_step", "decode", "operator", "encode",
+          "isvd_small", "isvd_reanchor"]
 
 _lib = None
 _lock = threading.Lock()

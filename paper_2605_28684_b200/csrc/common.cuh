@@ -178,6 +178,8 @@ enum ProbeId {
   PROBE_DECODE = 9,
   PROBE_OPERATOR = 10,
   PROBE_ENCODE = 11,
+  PROBE_ISVD_SMALL = 12,    // least squares p = G^-1 p1, refinement, W', seeds (the r x r chain)
+  PROBE_ISVD_REANCHOR = 13, // A = X W every FACT_KQ events
 };
 // record a begin / end event for probe `id` (no-op unless profiling)
 int prof_begin(adrom_ctx* ctx, int id);

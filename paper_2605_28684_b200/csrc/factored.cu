@@ -890,8 +890,10 @@ int fact_reanchor(adrom_ctx* ctx, const FactBasis& b, double* out, double* nrm2,
     const int64_t nt = (b.n + 63) / 64;
     int64_t g = (int64_t)ctx->num_sms;
     if (g > nt) g = nt;
+    const int pr = prof_begin(ctx, PROBE_ISVD_REANCHOR);
     kern<<<(int)(g < 1 ? 1 : g), 256, sm, ctx->stream>>>(b.A, b.Q, b.k, b.W, b.n, out, nrm2,
                                                          out32);
+    prof_end(ctx, pr);
     ADROM_LAUNCH_CK(ctx);
     return ADROM_OK;
   };
@@ -983,7 +985,9 @@ int fact_event_pass_b(adrom_ctx* ctx, const FactBasis& b, const FactEventArgs& e
     ADROM_CK(ctx, cudaMemcpyAsync(f.vdec, e.a, sizeof(double) * r, cudaMemcpyDeviceToDevice, ctx->stream));
   }
   // least squares p = G^{-1} p1; the explicit residual pass always runs here
+  int prs = prof_begin(ctx, PROBE_ISVD_SMALL);
   int st = isvd_solve_launch(ctx, f.red1, e.G, r, f.pls, f.need);
+  prof_end(ctx, prs);
   if (st) return st;
   set_need_kernel<<<1, 1, 0, ctx->stream>>>(f.need);
   ADROM_LAUNCH_CK(ctx);
@@ -1014,7 +1018,9 @@ int fact_event_pass_b(adrom_ctx* ctx, const FactBasis& b, const FactEventArgs& e
   ADROM_CK(ctx, cudaMemcpyAsync(f.red2 + r, f.t2 + r + FACT_KQ, sizeof(double), cudaMemcpyDeviceToDevice,
                                 ctx->stream));
   // one least-squares refinement step: q' = q - Phi p2 (isvd_refine_kernel)
+  prs = prof_begin(ctx, PROBE_ISVD_SMALL);
   st = isvd_refine_launch(ctx, e.G, r, f.red2, f.pls, f.p2, f.sb + 1, f.need);
+  prof_end(ctx, prs);
   if (st) return st;
   // core: K, its SVD, B, qinv, the tracked Gram of the new basis, sigma'
   pr = prof_begin(ctx, PROBE_ISVD_CORE);
@@ -1073,6 +1079,7 @@ struct adrom_isvd_stream {
   double *A[2] = {nullptr, nullptr}, *Q = nullptr, *W[2] = {nullptr, nullptr};
   double *sigma[2] = {nullptr, nullptr}, *G[2] = {nullptr, nullptr};
   double *partial = nullptr, *partial_a = nullptr, *small = nullptr, *stats = nullptr;
+  size_t partial_doubles = 0;  // capacity of `partial`
   std::vector<void*> allocs;
   double* alloc(size_t count) {
     void* p = nullptr;
@@ -1100,7 +1107,11 @@ int adrom_isvd_stream_create(adrom_ctx* ctx, int64_t n, int32_t r, adrom_isvd_st
     ok &= (s->G[b] = s->alloc((size_t)r * r)) != nullptr;
   }
   ok &= (s->Q = s->alloc((size_t)n * FACT_KQ)) != nullptr;
-  ok &= (s->partial = s->alloc(fact_partial_doubles(ctx, n, r))) != nullptr;
+  // (the load's Gram pass needs r x r doubles per block: a short stream's
+  // xpass partials alone are smaller than one of them)
+  s->partial_doubles = fact_partial_doubles(ctx, n, r);
+  if (s->partial_doubles < gram_partial_doubles(ctx, r)) s->partial_doubles = gram_partial_doubles(ctx, r);
+  ok &= (s->partial = s->alloc(s->partial_doubles)) != nullptr;
   ok &= (s->partial_a = s->alloc(fact_partial_doubles(ctx, n, r))) != nullptr;
   ok &= (s->small = s->alloc(fact_small_doubles(r))) != nullptr;
   ok &= (s->stats = s->alloc(16)) != nullptr;
@@ -1132,7 +1143,7 @@ int adrom_isvd_stream_load(adrom_isvd_stream* s, const double* phi, const double
   s->acur = 0;
   s->cur = 0;
   s->w_id = true;
-  return ts_gram(ctx, s->A[0], s->n, s->r, s->G[0], s->partial, fact_partial_doubles(ctx, s->n, s->r));
+  return ts_gram(ctx, s->A[0], s->n, s->r, s->G[0], s->partial, s->partial_doubles);
 }
 
 int adrom_isvd_stream_update(adrom_isvd_stream* s, const double* y_hat, double lam,

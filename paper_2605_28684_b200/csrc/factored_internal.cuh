@@ -25,6 +25,10 @@ struct FactBasis {
   int64_t n;
   // optional fp32 shadow of A (the QDEIM refresh gathers it)
   const float* A32 = nullptr;
+  // optional: the direction the last iSVD event dropped, in X coordinates
+  // (r + k entries).  The event's QDEIM seed ||Phi_i||^2 + q^_i^2 exceeds the
+  // new row norm by exactly (X_i . vdrop)^2; the bound refresh subtracts it
+  const double* vdrop = nullptr;
 };
 
 struct FactEventArgs {

@@ -897,6 +897,9 @@ int ts_gram(adrom_ctx* ctx, const double* phi, int64_t n, int r, double* gram, d
   if (r > 128) return set_error(ctx, ADROM_ERR_ARG, "gram: rank %d unsupported", r);
   int64_t g = (n + 63) / 64;
   const int64_t cap = (int64_t)(cap_doubles / ((size_t)r * r));
+  if (cap < 1)  // every block writes an r x r partial
+    return set_error(ctx, ADROM_ERR_ARG, "gram: partials buffer of %zu doubles is smaller than r^2",
+                     cap_doubles);
   int64_t lim = (int64_t)ctx->num_sms * 2;
   if (lim > cap) lim = cap;
   if (g > lim) g = lim;

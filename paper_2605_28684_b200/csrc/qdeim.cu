@@ -1438,15 +1438,24 @@ static int qp_refresh_bf(adrom_ctx* ctx, const double* phi, const double* Qx, in
                                                ver, blist);
 }
 
-// Mm ((r + FACT_KQ) x r) = W D for the directions l < k (rows >= r + kf zero)
+// Mm ((r + FACT_KQ) x r) = W D for the directions l < k (rows >= r + kf zero).
+// With the dropped direction of the iSVD event (vdrop, X coordinates) column 0
+// is vdrop and the directions follow in columns 1..k: the refresh then removes
+// the seed's slack (X_i . vdrop)^2 together with the first downdate, and a
+// row's version counts columns of this extended list.
 __global__ void qp_wd_kernel(const double* __restrict__ W, int rkf, int r,
-                             const double* __restrict__ D, int k, double* __restrict__ Mm) {
+                             const double* __restrict__ D, int k,
+                             const double* __restrict__ vdrop, double* __restrict__ Mm) {
+  const int sh = vdrop ? 1 : 0;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < (r + FACT_KQ) * r;
        e += gridDim.x * blockDim.x) {
-    const int j = e / r, l = e - j * r;
+    const int j = e / r, c = e - j * r, l = c - sh;
     double s = 0.0;
-    if (j < rkf && l < k)
-      for (int c = 0; c < r; ++c) s += W[(size_t)j * r + c] * D[(size_t)c * r + l];
+    if (j < rkf) {
+      if (l < 0) s = vdrop[j];
+      else if (l < k)
+        for (int q = 0; q < r; ++q) s += W[(size_t)j * r + q] * D[(size_t)q * r + l];
+    }
     Mm[e] = s;
   }
 }
@@ -1665,13 +1674,15 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
                   rows, v0, tile_work, row_work);
         }
         if (fact) {
+          // (k < m <= r, so the extended list of k + 1 columns fits the r of Mw)
+          const int kx = k + (fb->vdrop ? 1 : 0);
           qp_wd_kernel<<<(r + FACT_KQ) * r / 256 + 1, 256, 0, ctx->stream>>>(fb->W, r + fb->k, r, D,
-                                                                            k, Mw);
+                                                                            k, fb->vdrop, Mw);
           ADROM_LAUNCH_CK(ctx);
           st = (r == 32) ? qp_refresh_bf<32, true>(ctx, fb->A, fb->Q, fb->k, fb->n, nrmb, rlist, cap, Mw,
-                                                   k, res2, bnd2, ver, blist, fb->A32)
+                                                   kx, res2, bnd2, ver, blist, fb->A32)
                          : qp_refresh_bf<64, true>(ctx, fb->A, fb->Q, fb->k, fb->n, nrmb, rlist, cap, Mw,
-                                                   k, res2, bnd2, ver, blist, fb->A32);
+                                                   kx, res2, bnd2, ver, blist, fb->A32);
         } else if (r == 32 || r == 64 || r == 128) {
           st = (r == 32)
                    ? qp_refresh_bf<32, false>(ctx, phi, nullptr, 0, (int64_t)0, nullptr, rlist, cap, D, k, res2, bnd2, ver, blist)

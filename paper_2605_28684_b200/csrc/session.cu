@@ -524,7 +524,9 @@ int run_event_factored(adrom_session* s, adrom_event_record& ev, bool* decoded) 
   // spare buffers, so a failed update costs nothing but their time
   ride_add(ctx, s->isvd_stats, (char*)ctx->pinned + PIN_STATS, sizeof(double) * 8);
   ride_add(ctx, ctx->dflags, (char*)ctx->pinned + PIN_ISVD_FLAGS, sizeof(int) * 24);
-  const FactBasis b2{s->phi[s->acur], s->Qb, s->r, b.k + 1, s->Wd[nxt], s->N, s->A32[s->acur]};
+  const FactBasis b2{s->phi[s->acur], s->Qb,     s->r,           b.k + 1,
+                     s->Wd[nxt],       s->N,      s->A32[s->acur],
+                     getenv("ADROM_QDEIM_NO_VDROP") ? nullptr : s->vdrop[nxt]};
   const int onx = 1 - s->opcur;
   // the reduced step's failure flag shares the operator's final read
   ride_add(ctx, s->fail_step, (char*)ctx->pinned + PIN_FAIL_STEP, sizeof(int));
