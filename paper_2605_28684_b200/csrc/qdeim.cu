@@ -901,7 +901,7 @@ size_t qdeim_pool_workspace_bytes(int64_t n, int r, int count) {
   b += align_up(sizeof(int64_t) * (size_t)n);              // refresh list
   b += align_up(sizeof(double) * (size_t)(r + FACT_KQ) * r);  // W D (factored rows)
   b += align_up((size_t)n);                                // per-row downdate version
-  b += align_up(sizeof(double) * (size_t)r * r);           // D
+  b += 2 * align_up(sizeof(double) * (size_t)r * r);       // D, complement basis E
   b += align_up(sizeof(int64_t) * (size_t)r);              // local pivots
   b += align_up(sizeof(int) * 8) + align_up(sizeof(double) * 2);
   b += 3 * align_up(sizeof(double) * 4096);                // per-block bests
@@ -1121,8 +1121,18 @@ __global__ void __launch_bounds__(QpBf<R, FACT, T>::WPB * 32, 1)
                          const double* __restrict__ nrmb, const int64_t* __restrict__ list,
                          int64_t cap, const double* __restrict__ Mm, int k,
                          double* __restrict__ res2, double* __restrict__ bnd2,
-                         unsigned char* __restrict__ ver, double* __restrict__ blist) {
+                         unsigned char* __restrict__ ver, double* __restrict__ blist,
+                         int kver, const int* __restrict__ cflag) {
   using C = QpBf<R, FACT, T>;
+  // complement mode (kver >= 0): the k columns of Mm span the orthogonal
+  // complement of the confirmed directions, so a row's residual is the SUM of
+  // its squared components, res2 = sum (|S^| + delta)^2 -- no subtraction from
+  // the seed, whose slack and the accumulated under-subtractions otherwise
+  // swamp the last pivots' small residuals.  Every listed row is recomputed
+  // and stamped with version kver.  *cflag != k: the complement basis is
+  // incomplete -> bounds are left as they are.
+  const bool cmode = kver >= 0;
+  const bool cskip = cmode && cflag && *cflag != k;
   constexpr int KX = C::KX, KS = C::KS, NT = C::NT, RS = C::RS, WPB = C::WPB;
   constexpr int EPC = C::EPC, LC = C::LC, RPI = C::RPI;
   extern __shared__ __align__(16) unsigned char qbf_sm[];
@@ -1178,7 +1188,11 @@ __global__ void __launch_bounds__(QpBf<R, FACT, T>::WPB * 32, 1)
   // first tile's gather overlaps the prologue
   int64_t li_cur = load_list(tl);
   issue(li_cur, 0);
-  int v_cur = (lane < 16 && li_cur >= 0) ? (int)ver[li_cur] : k;
+  auto row_ver = [&](int64_t li) -> int {
+    if (!(lane < 16 && li >= 0) || cskip) return k;
+    return cmode ? 0 : (int)ver[li];
+  };
+  int v_cur = row_ver(li_cur);
   int64_t li_next = load_list(tl + tstride);
   // row scales of Mm (directions l < k only)
   for (int j = threadIdx.x; j < KX; j += blockDim.x) {
@@ -1215,7 +1229,7 @@ __global__ void __launch_bounds__(QpBf<R, FACT, T>::WPB * 32, 1)
   for (; tl < tiles; tl += tstride) {
     const int64_t tn = tl + tstride;
     issue(li_next, s ^ 1);  // empty rows when tn >= tiles
-    const int v_next = (lane < 16 && li_next >= 0) ? (int)ver[li_next] : k;
+    const int v_next = row_ver(li_next);
     const int64_t li_nn = load_list(tn + tstride);
     const int vmin = __reduce_min_sync(0xffffffffu, v_cur);
     asm volatile("cp.async.wait_group 1;\n" ::: "memory");
@@ -1343,7 +1357,8 @@ __global__ void __launch_bounds__(QpBf<R, FACT, T>::WPB * 32, 1)
           for (int q = 0; q < 4; ++q) {
             const int h = q >> 1, l = 8 * (d0 + u) + 2 * t + (q & 1);
             const float sv = (c[u][0][q] + c[u][1][q]) + c[u][2][q];
-            float a = fabsf(sv) - fmaf(dx[h], (q & 1) ? m2.y : m2.x, dt0[h]);
+            const float dl = fmaf(dx[h], (q & 1) ? m2.y : m2.x, dt0[h]);
+            float a = cmode ? fabsf(sv) + dl : fabsf(sv) - dl;
             a = (l >= vr[h] && l < k && a > 0.f) ? a : 0.f;
             sub[h] = fmaf(a, a, sub[h]);
           }
@@ -1358,10 +1373,12 @@ __global__ void __launch_bounds__(QpBf<R, FACT, T>::WPB * 32, 1)
         if (t == 0 && pos < cap) {
           double b = (i >= 0) ? b2o[h] : -1.0;
           if (i >= 0 && vr[h] < k && isfinite(sub[h])) {
-            const double r2 = fmax(r2o[h] - (double)sub[h] * (1.0 - 1.0 / 16384.0), 0.0);
+            // fp32 rounding of the sum: deflated when subtracted, inflated when it IS the bound
+            const double r2 = cmode ? fmin(r2o[h], (double)sub[h] * (1.0 + 1.0 / 16384.0))
+                                    : fmax(r2o[h] - (double)sub[h] * (1.0 - 1.0 / 16384.0), 0.0);
             res2[i] = r2;
-            ver[i] = (unsigned char)k;
-            b = fmin(b, r2 + 8.0 * (double)(k + 2) * QP_EPS * nrm[h]);
+            ver[i] = (unsigned char)(cmode ? kver : k);
+            b = fmin(b, r2 + 8.0 * (double)((cmode ? kver : k) + 2) * QP_EPS * nrm[h]);
             bnd2[i] = b;
           }
           blist[pos] = b;
@@ -1406,7 +1423,7 @@ template <int R, bool FACT, typename T>
 static int qp_refresh_bf_launch(adrom_ctx* ctx, const T* phi, const double* Qx, int kf, int64_t qn,
                                 const double* nrmb, const int64_t* list, int64_t cap,
                                 const double* Mm, int k, double* res2, double* bnd2,
-                                unsigned char* ver, double* blist) {
+                                unsigned char* ver, double* blist, int kver, const int* cflag) {
   using C = QpBf<R, FACT, T>;
   const size_t sm = C::smem_bytes;
   const int64_t tiles = (cap + 15) / 16;
@@ -1415,7 +1432,7 @@ static int qp_refresh_bf_launch(adrom_ctx* ctx, const T* phi, const double* Qx, 
   cudaFuncSetAttribute(qp_refresh_bf_kernel<R, FACT, T>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   qp_refresh_bf_kernel<R, FACT, T><<<(int)(g < 1 ? 1 : g), C::WPB * 32, sm, ctx->stream>>>(
-      phi, Qx, kf, qn, nrmb, list, cap, Mm, k, res2, bnd2, ver, blist);
+      phi, Qx, kf, qn, nrmb, list, cap, Mm, k, res2, bnd2, ver, blist, kver, cflag);
   ADROM_LAUNCH_CK(ctx);
   return ADROM_OK;
 }
@@ -1426,16 +1443,131 @@ template <int R, bool FACT>
 static int qp_refresh_bf(adrom_ctx* ctx, const double* phi, const double* Qx, int kf, int64_t qn,
                          const double* nrmb, const int64_t* list, int64_t cap, const double* Mm,
                          int k, double* res2, double* bnd2, unsigned char* ver, double* blist,
-                         const float* phi32 = nullptr) {
+                         const float* phi32 = nullptr, int kver = -1, const int* cflag = nullptr) {
   if (qp_refresh_fp64()) {
     const int st = qp_refresh_tc<R, FACT>(ctx, phi, Qx, kf, qn, nrmb, list, cap, Mm, k, res2, bnd2, ver);
     return st ? st : qp_list_bounds(ctx, list, cap, bnd2, blist);
   }
   if (FACT && phi32)
     return qp_refresh_bf_launch<R, FACT, float>(ctx, phi32, Qx, kf, qn, nrmb, list, cap, Mm, k, res2,
-                                                bnd2, ver, blist);
+                                                bnd2, ver, blist, kver, cflag);
   return qp_refresh_bf_launch<R, FACT, double>(ctx, phi, Qx, kf, qn, nrmb, list, cap, Mm, k, res2, bnd2,
-                                               ver, blist);
+                                               ver, blist, kver, cflag);
+}
+
+// ---------------------------------------------------------------------------
+// E (r x r row-major, columns 0 .. r-k-1): an orthonormal basis of the
+// orthogonal complement of the k confirmed directions D[:, :k] in R^r, by
+// pivoted Gram-Schmidt on the projector P = I - D D^T (one block, r <= 64).
+// Every new vector is re-orthogonalised against D and the vectors found so
+// far.  *found = the number of columns produced (r - k unless D has lost
+// orthonormality; the refresh then leaves the bounds alone).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) qp_complement_kernel(const double* __restrict__ D, int r, int k,
+                                                            double* __restrict__ E,
+                                                            int* __restrict__ found) {
+  constexpr int RM = 64, S = RM + 1;
+  extern __shared__ __align__(16) double csm[];  // QP_COMPLEMENT_SMEM bytes
+  double* P = csm;            // P[a * S + b]
+  double* Ds = P + RM * S;    // D[a * S + l], l < k
+  double* Es = Ds + RM * S;   // E[a * S + t]
+  double* cn = Es + RM * S;   // RM
+  double* e = cn + RM;        // RM
+  double* w = e + RM;         // RM
+  double* cf = w + RM;        // 2 RM
+  __shared__ int bsel;
+  __shared__ double nsel;
+  const int tid = threadIdx.x;
+  const int nE = r - k;
+  for (int x = tid; x < r * r; x += blockDim.x) {
+    const int a = x / r, l = x - a * r;
+    Ds[a * S + l] = (l < k) ? D[(size_t)a * r + l] : 0.0;
+  }
+  __syncthreads();
+  for (int x = tid; x < r * r; x += blockDim.x) {
+    const int a = x / r, b = x - a * r;
+    double s = (a == b) ? 1.0 : 0.0;
+    for (int l = 0; l < k; ++l) s = fma(-Ds[a * S + l], Ds[b * S + l], s);
+    P[a * S + b] = s;
+  }
+  __syncthreads();
+  int t = 0;
+  for (; t < nE; ++t) {
+    for (int b = tid; b < r; b += blockDim.x) {
+      double s = 0.0;
+      for (int a = 0; a < r; ++a) s = fma(P[a * S + b], P[a * S + b], s);
+      cn[b] = s;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int bb = 0;
+      for (int b = 1; b < r; ++b)
+        if (cn[b] > cn[bb]) bb = b;
+      bsel = bb;
+      nsel = cn[bb];
+    }
+    __syncthreads();
+    if (!(nsel > 1e-8)) break;  // (trace of the deflated projector is nE - t >= 1)
+    const int bb = bsel;
+    for (int a = tid; a < r; a += blockDim.x) e[a] = P[a * S + bb];
+    __syncthreads();
+    // two Gram-Schmidt passes against [D | E found so far], then normalise
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int l = tid; l < k + t; l += blockDim.x) {
+        const double* Bc = (l < k) ? Ds + l : Es + (l - k);
+        double s = 0.0;
+        for (int a = 0; a < r; ++a) s = fma(Bc[a * S], e[a], s);
+        cf[l] = s;
+      }
+      __syncthreads();
+      for (int a = tid; a < r; a += blockDim.x) {
+        double s = e[a];
+        for (int l = 0; l < k; ++l) s = fma(-Ds[a * S + l], cf[l], s);
+        for (int l = 0; l < t; ++l) s = fma(-Es[a * S + l], cf[k + l], s);
+        e[a] = s;
+      }
+      __syncthreads();
+    }
+    if (tid == 0) {
+      double s = 0.0;
+      for (int a = 0; a < r; ++a) s = fma(e[a], e[a], s);
+      nsel = s;
+    }
+    __syncthreads();
+    if (!(nsel > 1e-10)) break;
+    const double inv = 1.0 / sqrt(nsel);
+    for (int a = tid; a < r; a += blockDim.x) {
+      const double v = e[a] * inv;
+      e[a] = v;
+      Es[a * S + t] = v;
+    }
+    __syncthreads();
+    // deflate: P <- (I - e e^T) P
+    for (int b = tid; b < r; b += blockDim.x) {
+      double s = 0.0;
+      for (int a = 0; a < r; ++a) s = fma(e[a], P[a * S + b], s);
+      w[b] = s;
+    }
+    __syncthreads();
+    for (int x = tid; x < r * r; x += blockDim.x) {
+      const int a = x / r, b = x - a * r;
+      P[a * S + b] = fma(-e[a], w[b], P[a * S + b]);
+    }
+    __syncthreads();
+  }
+  for (int x = tid; x < r * r; x += blockDim.x) {
+    const int a = x / r, c = x - a * r;
+    E[(size_t)a * r + c] = (c < t) ? Es[a * S + c] : 0.0;
+  }
+  if (tid == 0) *found = t;
+}
+
+constexpr size_t QP_COMPLEMENT_SMEM = sizeof(double) * (3 * 64 * 65 + 5 * 64);
+
+// complement-mode refresh (ADROM_QDEIM_COMPLEMENT=0 turns it off)
+static bool qp_complement_on() {
+  static const bool v = !(getenv("ADROM_QDEIM_COMPLEMENT") && atoi(getenv("ADROM_QDEIM_COMPLEMENT")) == 0);
+  return v;
 }
 
 // Mm ((r + FACT_KQ) x r) = W D for the directions l < k (rows >= r + kf zero).
@@ -1549,6 +1681,7 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
   double* blist = (double*)take(sizeof(double) * (size_t)n);  // bounds in refresh-list order
   double* Mw = (double*)take(sizeof(double) * (size_t)(r + FACT_KQ) * r);
   double* D = (double*)take(sizeof(double) * (size_t)r * r);
+  double* Ec = (double*)take(sizeof(double) * (size_t)r * r);
   int64_t* piv = (int64_t*)take(sizeof(int64_t) * (size_t)r);
   int* state = (int*)take(sizeof(int) * 8);
   double* err_res = (double*)take(sizeof(double) * 2);
@@ -1673,7 +1806,32 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
           fprintf(stderr, "qdeim refresh: k=%d rows=%lld ver0=%lld tile_work=%lld row_work=%lld\n", k,
                   rows, v0, tile_work, row_work);
         }
-        if (fact) {
+        // Late rounds (at most as many directions left as confirmed): bounds
+        // from the complement basis, see qp_refresh_bf_kernel
+        const bool cmode = qp_complement_on() && !qp_refresh_fp64() && (r == 32 || r == 64) &&
+                           k >= 1 && (r - k) <= k;
+        int* cfound = state + 5;
+        if (cmode) {
+          cudaFuncSetAttribute(qp_complement_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)QP_COMPLEMENT_SMEM);
+          qp_complement_kernel<<<1, 256, QP_COMPLEMENT_SMEM, ctx->stream>>>(D, r, k, Ec, cfound);
+          ADROM_LAUNCH_CK(ctx);
+        }
+        if (fact && cmode) {
+          const int kver = k + (fb->vdrop ? 1 : 0);
+          qp_wd_kernel<<<(r + FACT_KQ) * r / 256 + 1, 256, 0, ctx->stream>>>(fb->W, r + fb->k, r, Ec,
+                                                                            r - k, nullptr, Mw);
+          ADROM_LAUNCH_CK(ctx);
+          st = (r == 32) ? qp_refresh_bf<32, true>(ctx, fb->A, fb->Q, fb->k, fb->n, nrmb, rlist, cap, Mw,
+                                                   r - k, res2, bnd2, ver, blist, fb->A32, kver, cfound)
+                         : qp_refresh_bf<64, true>(ctx, fb->A, fb->Q, fb->k, fb->n, nrmb, rlist, cap, Mw,
+                                                   r - k, res2, bnd2, ver, blist, fb->A32, kver, cfound);
+        } else if (cmode) {
+          st = (r == 32) ? qp_refresh_bf<32, false>(ctx, phi, nullptr, 0, (int64_t)0, nullptr, rlist, cap,
+                                                    Ec, r - k, res2, bnd2, ver, blist, nullptr, k, cfound)
+                         : qp_refresh_bf<64, false>(ctx, phi, nullptr, 0, (int64_t)0, nullptr, rlist, cap,
+                                                    Ec, r - k, res2, bnd2, ver, blist, nullptr, k, cfound);
+        } else if (fact) {
           // (k < m <= r, so the extended list of k + 1 columns fits the r of Mw)
           const int kx = k + (fb->vdrop ? 1 : 0);
           qp_wd_kernel<<<(r + FACT_KQ) * r / 256 + 1, 256, 0, ctx->stream>>>(fb->W, r + fb->k, r, D,
