@@ -137,13 +137,22 @@ struct SelState {
   int pad;
   double tau;
   unsigned long long count;  // compaction counter
+  // sign + exponent digit of the last selection's threshold, tagged
+  // (QS_HINT_TAG | digit): the next selection through this state starts with
+  // the mantissa digit inside that bin and falls back if the guess is wrong
+  unsigned long long hint;
 };
+constexpr unsigned long long QS_HINT_TAG = 0xC0FFEE5E1EC70000ull;
 
-// radix select in 12-bit digits: bits 63..52 (sign + exponent) first, then
-// the mantissa 12 bits at a time (passes at shifts 52, 40, 28, 16, 4, 0; the
-// last one is 4 bits wide)
-constexpr int QS_BITS = 12, QS_BINS = 1 << QS_BITS;
-__host__ __device__ inline int qs_bits(int shift) { return shift == 0 ? 4 : QS_BITS; }
+// radix select: bits 63..60 (sign + the top three exponent bits) first, then
+// 12 bits at a time (passes at shifts 60, 48, 36, 24, 12, 0).  Squared row
+// norms of a basis share the top digit, so a selection normally starts from
+// the previous one's top digit (SelState::hint) with the pass at shift 48 --
+// eight exponent and four mantissa bits, bins 4.4 % wide -- and is done after
+// that single pass when the threshold bin fits the capacity's slack.
+constexpr int QS_BITS = 12, QS_BINS = 1 << QS_BITS, QS_TOP_SHIFT = 60;
+__host__ __device__ inline int qs_bits(int shift) { return shift == QS_TOP_SHIFT ? 4 : QS_BITS; }
+__host__ __device__ inline int qs_shift(int pass) { return pass == 0 ? QS_TOP_SHIFT : 60 - QS_BITS * pass; }
 
 __global__ void qs_init_kernel(SelState* st, long long M, unsigned int* hist) {
   if (threadIdx.x == 0) {
@@ -156,7 +165,7 @@ __global__ void qs_init_kernel(SelState* st, long long M, unsigned int* hist) {
     st->tau = -1.0;
     st->count = 0ull;
   }
-  for (int j = threadIdx.x; j < QS_BINS; j += blockDim.x) hist[j] = 0u;
+  for (int j = threadIdx.x; j < QS_BINS + 32; j += blockDim.x) hist[j] = 0u;
 }
 
 // ---------------------------------------------------------------------------
@@ -180,11 +189,15 @@ struct SelArgs {
   int64_t* out;         // cap slots; unused ones -> -1
 };
 
+// HINT: `prefix` is a guessed top digit; keys above its bin are counted into
+// hist[QS_BINS] (they all belong to the selection)
+template <bool HINT>
 __device__ __forceinline__ void qs_hist_pass(const double* vals, int64_t n,
                                              unsigned long long prefix, unsigned long long mask,
                                              int shift, unsigned int* hist, unsigned int* sh) {
   constexpr int ITEMS = 8;
   for (int b = threadIdx.x; b < QS_BINS; b += blockDim.x) sh[b] = 0u;
+  unsigned int above = 0u;
   __syncthreads();
   const unsigned long long dmask = (1ull << qs_bits(shift)) - 1ull;
   const int lane = threadIdx.x & 31;
@@ -200,14 +213,21 @@ __device__ __forceinline__ void qs_hist_pass(const double* vals, int64_t n,
     for (int q = 0; q < ITEMS; ++q) {
       const unsigned long long k = qp_key(v[q]);
       const int dig = (k != 0ull && (k & mask) == prefix) ? (int)((k >> shift) & dmask) : -1;
+      if (HINT) above += (k & mask) > prefix;
+      // bounds crowd into a few bins (or miss the prefix: -1): one vote for the
+      // leader's digit, the other lanes add on their own
       const int d0 = __shfl_sync(0xffffffffu, dig, 0);
-      if (__all_sync(0xffffffffu, dig == d0)) {
-        if (lane == 0 && d0 >= 0) atomicAdd(&sh[d0], 32u);
-      } else {
-        const unsigned int peers = __match_any_sync(0xffffffffu, dig);
-        if (dig >= 0 && lane == __ffs(peers) - 1) atomicAdd(&sh[dig], (unsigned int)__popc(peers));
+      const unsigned int same = __ballot_sync(0xffffffffu, dig == d0);
+      if (lane == 0) {
+        if (d0 >= 0) atomicAdd(&sh[d0], (unsigned int)__popc(same));
+      } else if (dig >= 0 && dig != d0) {
+        atomicAdd(&sh[dig], 1u);
       }
     }
+  }
+  if (HINT) {
+    above = __reduce_add_sync(0xffffffffu, above);
+    if (lane == 0 && above) atomicAdd(&hist[QS_BINS], above);
   }
   __syncthreads();
   for (int b = threadIdx.x; b < QS_BINS; b += blockDim.x) {
@@ -223,7 +243,7 @@ __device__ __forceinline__ void qs_hist_pass(const double* vals, int64_t n,
 template <int NT>
 __device__ __forceinline__ void qs_digit_step(volatile SelState* st, int shift, unsigned int* hist,
                                               long long pcap, int extend, long long* wsum,
-                                              int* ish, long long* lsh) {
+                                              int* ish, long long* lsh, bool hint_pass = false) {
   constexpr int BPT = QS_BINS / NT;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   long long hb[BPT];
@@ -275,7 +295,9 @@ __device__ __forceinline__ void qs_digit_step(volatile SelState* st, int shift, 
   for (int e = 0; e < BPT; ++e) hist[BPT * tid + e] = 0u;  // ready for the next pass / selection
   if (tid == 0) {
     const int dig = ish[0], dlow = ish[1];
-    if (dig < 0) {  // fewer candidates than M: take every live row
+    if (dig < 0 && hint_pass) {  // the need-th key lies below the guessed bin
+      st->done = 2;
+    } else if (dig < 0) {  // fewer candidates than M: take every live row
       st->theta = 1ull;
       st->tau = -1.0;
       st->done = 1;
@@ -311,53 +333,103 @@ __global__ void __launch_bounds__(256) qs_select_compact_kernel(SelArgs a) {
   __shared__ int ish[2];
   __shared__ long long lsh[2];
   volatile SelState* st = a.st;
-  for (int pass = 0; pass < 6; ++pass) {
-    const int shift = (pass == 5) ? 0 : 52 - QS_BITS * pass;
+  auto init_state = [&]() {  // thread 0 of block 0
+    st->prefix = 0ull;
+    st->mask = 0ull;
+    st->theta = 1ull;
+    st->above = 0;
+    st->need = a.M;
+    st->done = 0;
+    st->tau = -1.0;
+    st->count = 0ull;
+  };
+  int pass = 0;
+  bool fin = false;  // (the state's own flag is stale until the first digit step)
+  // guessed top digit: one pass over the mantissa digit inside its bin
+  const unsigned long long hint = st->hint;  // (rewritten only after a grid barrier)
+  if ((hint & ~0xFFFFull) == QS_HINT_TAG) {
+    const unsigned long long topmask = 0xFull << QS_TOP_SHIFT;
+    const unsigned long long hp = (hint & 0xFull) << QS_TOP_SHIFT;
+    qs_hist_pass<true>(a.vals, a.n, hp, topmask, qs_shift(1), a.hist, sh);
+    grid.sync();
+    if (blockIdx.x == 0) {
+      __shared__ int hint_ok;
+      if (threadIdx.x == 0) {
+        const long long above = (long long)__ldcg(a.hist + QS_BINS);
+        a.hist[QS_BINS] = 0u;
+        init_state();
+        hint_ok = above < a.M;  // else the threshold lies above the guessed bin
+        if (hint_ok) {
+          st->prefix = hp;
+          st->mask = topmask;
+          st->above = above;
+          st->need = a.M - above;
+        }
+      }
+      __syncthreads();
+      if (hint_ok) {
+        qs_digit_step<256>(st, qs_shift(1), a.hist, a.cap, a.extend, wsum, ish, lsh, true);
+      } else {
+        for (int b = threadIdx.x; b < QS_BINS; b += blockDim.x) a.hist[b] = 0u;
+        if (threadIdx.x == 0) st->done = 2;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0 && st->done == 2) {  // wrong guess: the full selection from the top
+        init_state();
+        st->hint = 0ull;
+      }
+      __threadfence();
+    }
+    grid.sync();
+    pass = (st->hint == 0ull) ? 0 : 2;
+    fin = st->done != 0;
+  }
+  for (; pass < 6 && !fin; ++pass) {
+    const int shift = qs_shift(pass);
     unsigned long long prefix = 0ull, mask = 0ull;
     if (pass > 0) {
       prefix = st->prefix;
       mask = st->mask;
     }
-    qs_hist_pass(a.vals, a.n, prefix, mask, shift, a.hist, sh);
+    qs_hist_pass<false>(a.vals, a.n, prefix, mask, shift, a.hist, sh);
     grid.sync();
     if (blockIdx.x == 0) {
       if (pass == 0) {
-        if (threadIdx.x == 0) {
-          st->prefix = 0ull;
-          st->mask = 0ull;
-          st->theta = 1ull;
-          st->above = 0;
-          st->need = a.M;
-          st->done = 0;
-          st->tau = -1.0;
-          st->count = 0ull;
-        }
+        if (threadIdx.x == 0) init_state();
         __syncthreads();
       }
       qs_digit_step<256>(st, shift, a.hist, a.cap, a.extend, wsum, ish, lsh);
       __threadfence();
     }
     grid.sync();
-    if (st->done) break;
+    fin = st->done != 0;
   }
-  // compaction: rows with key >= theta -> out[0..), one atomic per block and tile
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const unsigned long long th = st->theta;
+    st->hint = (th >= 2ull) ? (QS_HINT_TAG | (th >> QS_TOP_SHIFT)) : 0ull;
+  }
+  // compaction: rows with key >= theta -> out[0..).  One atomic per block and
+  // 4096-candidate tile (the counter is a single address: few, large
+  // reservations); only the votes are kept between the count and the write.
   {
-    constexpr int ITEMS = 4;
+    constexpr int ITEMS = 16;
     int* wcnt = reinterpret_cast<int*>(sh);
     unsigned long long* base_sh = reinterpret_cast<unsigned long long*>(sh + 16);
     const unsigned long long theta = st->theta;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t tile = (int64_t)blockDim.x * ITEMS;
     for (int64_t t0 = blockIdx.x * tile; t0 < a.n; t0 += (int64_t)gridDim.x * tile) {
-      int64_t rows[ITEMS];
+      double v[ITEMS];
+#pragma unroll
+      for (int q = 0; q < ITEMS; ++q) {
+        const int64_t j = t0 + (int64_t)q * blockDim.x + threadIdx.x;
+        v[q] = (j < a.n) ? __ldg(a.vals + j) : -1.0;
+      }
       unsigned int balls[ITEMS];
       int mine = 0;
 #pragma unroll
       for (int q = 0; q < ITEMS; ++q) {
-        const int64_t j = t0 + (int64_t)q * blockDim.x + threadIdx.x;
-        const bool take = j < a.n && qp_key(__ldg(a.vals + j)) >= theta;
-        rows[q] = take ? (a.list ? a.list[j] : j) : -1;
-        balls[q] = __ballot_sync(0xffffffffu, take);
+        balls[q] = __ballot_sync(0xffffffffu, qp_key(v[q]) >= theta);
         mine += __popc(balls[q]);
       }
       if (lane == 0) wcnt[warp] = mine;
@@ -370,13 +442,16 @@ __global__ void __launch_bounds__(256) qs_select_compact_kernel(SelArgs a) {
       __syncthreads();
       unsigned long long pos = *base_sh;
       for (int w = 0; w < warp; ++w) pos += wcnt[w];
+      if (mine) {
 #pragma unroll
-      for (int q = 0; q < ITEMS; ++q) {
-        if (rows[q] >= 0) {
-          const unsigned long long slot = pos + __popc(balls[q] & ((1u << lane) - 1u));
-          if ((long long)slot < a.cap) a.out[slot] = rows[q];
+        for (int q = 0; q < ITEMS; ++q) {
+          if (balls[q] & (1u << lane)) {
+            const int64_t j = t0 + (int64_t)q * blockDim.x + threadIdx.x;
+            const unsigned long long slot = pos + __popc(balls[q] & ((1u << lane) - 1u));
+            if ((long long)slot < a.cap) a.out[slot] = a.list ? a.list[j] : j;
+          }
+          pos += __popc(balls[q]);
         }
-        pos += __popc(balls[q]);
       }
       __syncthreads();
     }
@@ -896,7 +971,7 @@ size_t qdeim_pool_workspace_bytes(int64_t n, int r, int count) {
   b += align_up(sizeof(int64_t) * (size_t)P);              // pool idx
   b += align_up(sizeof(double) * (size_t)P * r);           // Rv
   b += 2 * align_up(sizeof(double) * (size_t)P);           // pres2, pn2
-  b += 2 * align_up(sizeof(SelState)) + align_up(sizeof(unsigned int) * QS_BINS);  // selection
+  b += 2 * align_up(sizeof(SelState)) + align_up(sizeof(unsigned int) * (QS_BINS + 32));  // selection
   b += align_up(sizeof(double) * (size_t)n);               // bounds in refresh-list order
   b += align_up(sizeof(int64_t) * (size_t)n);              // refresh list
   b += align_up(sizeof(double) * (size_t)(r + FACT_KQ) * r);  // W D (factored rows)
@@ -1457,11 +1532,14 @@ static int qp_refresh_bf(adrom_ctx* ctx, const double* phi, const double* Qx, in
 
 // ---------------------------------------------------------------------------
 // E (r x r row-major, columns 0 .. r-k-1): an orthonormal basis of the
-// orthogonal complement of the k confirmed directions D[:, :k] in R^r, by
-// pivoted Gram-Schmidt on the projector P = I - D D^T (one block, r <= 64).
-// Every new vector is re-orthogonalised against D and the vectors found so
-// far.  *found = the number of columns produced (r - k unless D has lost
-// orthonormality; the refresh then leaves the bounds alone).
+// orthogonal complement of the k confirmed directions D[:, :k] in R^r: the
+// pivoted Cholesky factor of the projector P = I - D D^T (P = L L^T with
+// rank r - k makes L^T L = I), one block, r <= 64.  A step costs one argmax
+// over the running diagonal and one column of L; the diagonal of the
+// deflated projector has trace r - k - t, so its largest entry is at least
+// 1 / r until the factor is complete.  One Gram-Schmidt pass against D
+// removes the rounding of P.  *found = columns produced (r - k unless D has
+// lost orthonormality; the refresh then leaves the bounds alone).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) qp_complement_kernel(const double* __restrict__ D, int r, int k,
                                                             double* __restrict__ E,
@@ -1470,14 +1548,12 @@ __global__ void __launch_bounds__(256) qp_complement_kernel(const double* __rest
   extern __shared__ __align__(16) double csm[];  // QP_COMPLEMENT_SMEM bytes
   double* P = csm;            // P[a * S + b]
   double* Ds = P + RM * S;    // D[a * S + l], l < k
-  double* Es = Ds + RM * S;   // E[a * S + t]
-  double* cn = Es + RM * S;   // RM
-  double* e = cn + RM;        // RM
-  double* w = e + RM;         // RM
-  double* cf = w + RM;        // 2 RM
-  __shared__ int bsel;
-  __shared__ double nsel;
-  const int tid = threadIdx.x;
+  double* L = Ds + RM * S;    // L[a * S + t]
+  double* dg = L + RM * S;    // running diagonal (RM)
+  double* cf = dg + RM;       // RM x 33 coefficients D^T L (nE <= 32) -- reuses P after the factor
+  __shared__ int jsel;
+  __shared__ double dsel;
+  const int tid = threadIdx.x, lane = tid & 31;
   const int nE = r - k;
   for (int x = tid; x < r * r; x += blockDim.x) {
     const int a = x / r, l = x - a * r;
@@ -1486,78 +1562,70 @@ __global__ void __launch_bounds__(256) qp_complement_kernel(const double* __rest
   __syncthreads();
   for (int x = tid; x < r * r; x += blockDim.x) {
     const int a = x / r, b = x - a * r;
-    double s = (a == b) ? 1.0 : 0.0;
-    for (int l = 0; l < k; ++l) s = fma(-Ds[a * S + l], Ds[b * S + l], s);
-    P[a * S + b] = s;
+    double s0 = (a == b) ? 1.0 : 0.0, s1 = 0.0;
+    int l = 0;
+    for (; l + 1 < k; l += 2) {
+      s0 = fma(-Ds[a * S + l], Ds[b * S + l], s0);
+      s1 = fma(-Ds[a * S + l + 1], Ds[b * S + l + 1], s1);
+    }
+    if (l < k) s0 = fma(-Ds[a * S + l], Ds[b * S + l], s0);
+    P[a * S + b] = s0 + s1;
+    if (a == b) dg[a] = s0 + s1;
   }
   __syncthreads();
   int t = 0;
   for (; t < nE; ++t) {
-    for (int b = tid; b < r; b += blockDim.x) {
-      double s = 0.0;
-      for (int a = 0; a < r; ++a) s = fma(P[a * S + b], P[a * S + b], s);
-      cn[b] = s;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      int bb = 0;
-      for (int b = 1; b < r; ++b)
-        if (cn[b] > cn[bb]) bb = b;
-      bsel = bb;
-      nsel = cn[bb];
-    }
-    __syncthreads();
-    if (!(nsel > 1e-8)) break;  // (trace of the deflated projector is nE - t >= 1)
-    const int bb = bsel;
-    for (int a = tid; a < r; a += blockDim.x) e[a] = P[a * S + bb];
-    __syncthreads();
-    // two Gram-Schmidt passes against [D | E found so far], then normalise
-    for (int pass = 0; pass < 2; ++pass) {
-      for (int l = tid; l < k + t; l += blockDim.x) {
-        const double* Bc = (l < k) ? Ds + l : Es + (l - k);
-        double s = 0.0;
-        for (int a = 0; a < r; ++a) s = fma(Bc[a * S], e[a], s);
-        cf[l] = s;
+    if (tid < 32) {  // argmax of the running diagonal (ties to the lowest index)
+      double v = (lane < r) ? dg[lane] : -1.0;
+      int j = lane;
+      if (lane + 32 < r && dg[lane + 32] > v) {
+        v = dg[lane + 32];
+        j = lane + 32;
       }
-      __syncthreads();
-      for (int a = tid; a < r; a += blockDim.x) {
-        double s = e[a];
-        for (int l = 0; l < k; ++l) s = fma(-Ds[a * S + l], cf[l], s);
-        for (int l = 0; l < t; ++l) s = fma(-Es[a * S + l], cf[k + l], s);
-        e[a] = s;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+        const int j2 = __shfl_xor_sync(0xffffffffu, j, o);
+        if (v2 > v || (v2 == v && j2 < j)) {
+          v = v2;
+          j = j2;
+        }
       }
-      __syncthreads();
-    }
-    if (tid == 0) {
-      double s = 0.0;
-      for (int a = 0; a < r; ++a) s = fma(e[a], e[a], s);
-      nsel = s;
+      if (lane == 0) {
+        jsel = j;
+        dsel = v;
+      }
     }
     __syncthreads();
-    if (!(nsel > 1e-10)) break;
-    const double inv = 1.0 / sqrt(nsel);
-    for (int a = tid; a < r; a += blockDim.x) {
-      const double v = e[a] * inv;
-      e[a] = v;
-      Es[a * S + t] = v;
-    }
-    __syncthreads();
-    // deflate: P <- (I - e e^T) P
-    for (int b = tid; b < r; b += blockDim.x) {
-      double s = 0.0;
-      for (int a = 0; a < r; ++a) s = fma(e[a], P[a * S + b], s);
-      w[b] = s;
-    }
-    __syncthreads();
-    for (int x = tid; x < r * r; x += blockDim.x) {
-      const int a = x / r, b = x - a * r;
-      P[a * S + b] = fma(-e[a], w[b], P[a * S + b]);
+    if (!(dsel > 1e-6)) break;
+    const int j = jsel;
+    const double inv = 1.0 / sqrt(dsel);
+    if (tid < r) {
+      double v = P[tid * S + j];
+      for (int q = 0; q < t; ++q) v = fma(-L[tid * S + q], L[j * S + q], v);
+      v *= inv;
+      L[tid * S + t] = v;
+      dg[tid] = (tid == j) ? -1.0 : dg[tid] - v * v;  // a used pivot never returns
     }
     __syncthreads();
   }
+  // one Gram-Schmidt pass against D: L -= D (D^T L)
+  cf = P;  // the projector is no longer needed
+  for (int x = tid; x < k * t; x += blockDim.x) {
+    const int l = x / t, c = x - l * t;
+    double s0 = 0.0;
+    for (int a = 0; a < r; ++a) s0 = fma(Ds[a * S + l], L[a * S + c], s0);
+    cf[l * 33 + c] = s0;
+  }
+  __syncthreads();
   for (int x = tid; x < r * r; x += blockDim.x) {
     const int a = x / r, c = x - a * r;
-    E[(size_t)a * r + c] = (c < t) ? Es[a * S + c] : 0.0;
+    double v = 0.0;
+    if (c < t) {
+      v = L[a * S + c];
+      for (int l = 0; l < k; ++l) v = fma(-Ds[a * S + l], cf[l * 33 + c], v);
+    }
+    E[(size_t)a * r + c] = v;
   }
   if (tid == 0) *found = t;
 }
@@ -1677,7 +1745,7 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
   SelState* sel = (SelState*)take(sizeof(SelState));
   SelState* selR = (SelState*)take(sizeof(SelState));
   int64_t* rlist = (int64_t*)take(sizeof(int64_t) * (size_t)n);
-  unsigned int* hist = (unsigned int*)take(sizeof(unsigned int) * QS_BINS);
+  unsigned int* hist = (unsigned int*)take(sizeof(unsigned int) * (QS_BINS + 32));  // [QS_BINS]: rows above a hinted bin
   double* blist = (double*)take(sizeof(double) * (size_t)n);  // bounds in refresh-list order
   double* Mw = (double*)take(sizeof(double) * (size_t)(r + FACT_KQ) * r);
   double* D = (double*)take(sizeof(double) * (size_t)r * r);
@@ -1738,7 +1806,7 @@ int qdeim_pool_select(adrom_ctx* ctx, const double* phi, int64_t n, int r, int c
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sbpm, qs_select_compact_kernel, 256, 0);
   if (sbpm < 1) return set_error(ctx, ADROM_ERR_CUDA, "qdeim: selection kernel cannot be resident");
   const int sgrid_max = ctx->num_sms * (sbpm < 4 ? sbpm : 4);
-  ADROM_CK(ctx, cudaMemsetAsync(hist, 0, sizeof(unsigned int) * QS_BINS, ctx->stream));
+  ADROM_CK(ctx, cudaMemsetAsync(hist, 0, sizeof(unsigned int) * (QS_BINS + 32), ctx->stream));
   auto select_compact = [&](SelState* st, const double* vals, int64_t nn, const int64_t* list,
                             long long M, long long cap, int extend, int64_t* out) -> int {
     int64_t hg = (nn + 2047) / 2048;
