@@ -1546,11 +1546,10 @@ __global__ void __launch_bounds__(256) qp_complement_kernel(const double* __rest
                                                             int* __restrict__ found) {
   constexpr int RM = 64, S = RM + 1;
   extern __shared__ __align__(16) double csm[];  // QP_COMPLEMENT_SMEM bytes
-  double* P = csm;            // P[a * S + b]
-  double* Ds = P + RM * S;    // D[a * S + l], l < k
+  double* Ds = csm;           // D[a * S + l], l < k
   double* L = Ds + RM * S;    // L[a * S + t]
-  double* dg = L + RM * S;    // running diagonal (RM)
-  double* cf = dg + RM;       // RM x 33 coefficients D^T L (nE <= 32) -- reuses P after the factor
+  double* cf = L + RM * S;    // D^T L: k x 33 (r - k <= 32 columns)
+  double* dg = cf + RM * S;   // running diagonal (RM)
   __shared__ int jsel;
   __shared__ double dsel;
   const int tid = threadIdx.x, lane = tid & 31;
@@ -1560,17 +1559,16 @@ __global__ void __launch_bounds__(256) qp_complement_kernel(const double* __rest
     Ds[a * S + l] = (l < k) ? D[(size_t)a * r + l] : 0.0;
   }
   __syncthreads();
-  for (int x = tid; x < r * r; x += blockDim.x) {
-    const int a = x / r, b = x - a * r;
-    double s0 = (a == b) ? 1.0 : 0.0, s1 = 0.0;
-    int l = 0;
-    for (; l + 1 < k; l += 2) {
-      s0 = fma(-Ds[a * S + l], Ds[b * S + l], s0);
-      s1 = fma(-Ds[a * S + l + 1], Ds[b * S + l + 1], s1);
-    }
-    if (l < k) s0 = fma(-Ds[a * S + l], Ds[b * S + l], s0);
-    P[a * S + b] = s0 + s1;
-    if (a == b) dg[a] = s0 + s1;
+  // diag(P) = 1 - |row a of D|^2; the columns of P are formed when chosen
+  // (four threads per row share the sum over the directions)
+  const int row = tid >> 2, part = tid & 3;
+  {
+    double s0 = 0.0;
+    if (row < r)
+      for (int l = part; l < k; l += 4) s0 = fma(Ds[row * S + l], Ds[row * S + l], s0);
+    s0 += __shfl_xor_sync(0xffffffffu, s0, 1);
+    s0 += __shfl_xor_sync(0xffffffffu, s0, 2);
+    if (row < r && part == 0) dg[row] = 1.0 - s0;
   }
   __syncthreads();
   int t = 0;
@@ -1600,17 +1598,23 @@ __global__ void __launch_bounds__(256) qp_complement_kernel(const double* __rest
     if (!(dsel > 1e-6)) break;
     const int j = jsel;
     const double inv = 1.0 / sqrt(dsel);
-    if (tid < r) {
-      double v = P[tid * S + j];
-      for (int q = 0; q < t; ++q) v = fma(-L[tid * S + q], L[j * S + q], v);
-      v *= inv;
-      L[tid * S + t] = v;
-      dg[tid] = (tid == j) ? -1.0 : dg[tid] - v * v;  // a used pivot never returns
+    // L[:, t] = (P[:, j] - L[:, :t] L[j, :t]^T) / sqrt(d_j),  P[a][j] = delta_aj - D_a . D_j
+    double v = 0.0;
+    if (row < r) {
+      for (int l = part; l < k; l += 4) v = fma(-Ds[row * S + l], Ds[j * S + l], v);
+      for (int q = part; q < t; q += 4) v = fma(-L[row * S + q], L[j * S + q], v);
+    }
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    __syncthreads();  // every read of L[:, :t] done before column t is written
+    if (row < r && part == 0) {
+      v = (v + (row == j ? 1.0 : 0.0)) * inv;
+      L[row * S + t] = v;
+      dg[row] = (row == j) ? -1.0 : dg[row] - v * v;  // a used pivot never returns
     }
     __syncthreads();
   }
   // one Gram-Schmidt pass against D: L -= D (D^T L)
-  cf = P;  // the projector is no longer needed
   for (int x = tid; x < k * t; x += blockDim.x) {
     const int l = x / t, c = x - l * t;
     double s0 = 0.0;
