@@ -322,10 +322,17 @@ __global__ void __launch_bounds__(1024) deim_pinv_qr_kernel(DevOp op, int n_s,
   __syncthreads();
   for (int k = 0; k < r; ++k) {
     double* col = A + (size_t)k * ld;
-    double a = 0.0;
-    for (int i = k + tid; i < m; i += blockDim.x) a += col[i] * col[i];
-    a = block_sum_dyn(a, red);
+    // the column norm by one warp (m is a few hundred at most): one barrier
+    // per reflector instead of a block-wide reduction
+    if (warp == 0) {
+      double a = 0.0;
+      for (int i = k + lane; i < m; i += 32) a += col[i] * col[i];
+      a = warp_sum(a);
+      if (lane == 0) red[0] = a;
+    }
+    __syncthreads();
     if (tid == 0) {
+      const double a = red[0];
       const double x0 = col[k], nrm = sqrt(a);
       const double alpha = (x0 >= 0.0) ? -nrm : nrm;
       const double vtv_half = a - x0 * alpha;
