@@ -148,8 +148,10 @@ void* scratch(adrom_ctx* ctx, size_t bytes, size_t offset_bytes = 0);
 int ensure_scratch(adrom_ctx* ctx, size_t bytes);
 int ensure_aux(adrom_ctx* ctx, size_t bytes);
 int ensure_pinned(adrom_ctx* ctx, size_t bytes);
+inline void ride_flush(adrom_ctx* ctx);
 inline void ride_add(adrom_ctx* ctx, const void* src, void* dst, size_t bytes) {
-  if (ctx->n_rides < 4) ctx->rides[ctx->n_rides++] = adrom_ctx::Ride{src, dst, bytes};
+  if (ctx->n_rides == 4) ride_flush(ctx);  // (a full table is enqueued at once, never dropped)
+  ctx->rides[ctx->n_rides++] = adrom_ctx::Ride{src, dst, bytes};
 }
 // enqueue the registered copies on the context's stream (no synchronisation)
 inline void ride_flush(adrom_ctx* ctx) {

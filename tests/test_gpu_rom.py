@@ -86,6 +86,21 @@ def test_qdeim_pool_graded_rows(n, r, span):
     assert list(P.qdeim_sample(_basis(phi), r).indices) == want
 
 
+def test_qdeim_selection_hint_across_scales():
+    """The pool selection starts from the previous threshold's top digit
+    (SelState::hint, csrc/qdeim.cu) and must fall back to the full digit
+    sequence when the guess is wrong: the same rows scaled by 10^3 move every
+    bound (a squared norm) from below 1 to above 2, i.e. to another top digit,
+    and back.  Uniform scaling leaves the greedy pivots unchanged."""
+    P = _pkg()
+    n, r = 1 << 17, 32
+    rng = np.random.default_rng(7)
+    phi = np.linalg.qr(rng.standard_normal((n, r)))[0]
+    want, _ = hyper.greedy_pivots(phi, r)
+    for scale in (1.0, 1e3, 1.0, 1e-3, 1e3):
+        assert list(P.qdeim_sample(_basis(scale * phi), r).indices) == want, scale
+
+
 def test_qdeim_pod_basis_vs_lapack():
     # realistic smooth basis (Burgers POD, cfg-0 physics at N=4096): geqp3 pivots
     P = _pkg()
