@@ -101,6 +101,32 @@ def test_qdeim_selection_hint_across_scales():
         assert list(P.qdeim_sample(_basis(scale * phi), r).indices) == want, scale
 
 
+def test_qdeim_downdated_bounds_path():
+    """ADROM_QDEIM_COMPLEMENT=0 keeps the downdated bounds in every round
+    (the default switches to complement-basis bounds once r - k <= k); the
+    switch is read once per process, so this path runs in a child process.
+    Both must return the exact greedy pivots."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np\n"
+        "sys.path.insert(0, %r)\n"
+        "import paper_2605_28684_b200 as P\n"
+        "from oracle import hyper\n"
+        "n, r = 1 << 17, 64\n"
+        "phi = np.linalg.qr(np.random.default_rng(n + r).standard_normal((n, r)))[0]\n"
+        "want, _ = hyper.greedy_pivots(phi, r)\n"
+        "got = list(P.qdeim_sample(P.ReducedBasis(phi=phi, sigma=np.ones(r)), r).indices)\n"
+        "assert got == want, (got, want)\n"
+        "print('pivots equal')\n"
+    ) % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, ADROM_QDEIM_COMPLEMENT="0")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0 and "pivots equal" in out.stdout, out.stderr[-2000:]
+
+
 def test_qdeim_pod_basis_vs_lapack():
     # realistic smooth basis (Burgers POD, cfg-0 physics at N=4096): geqp3 pivots
     P = _pkg()
