@@ -798,6 +798,7 @@ __global__ void __launch_bounds__(256) gather_rows_tc_kernel(FactBasis b, const 
   for (int64_t t = (int64_t)blockIdx.x * 8 + warp; t < tiles; t += (int64_t)gridDim.x * 8) {
     const int64_t p = t * 8 + rq;
     const int64_t i = (p < count) ? rows[p] : -1;
+    if (!__any_sync(0xffffffffu, i >= 0)) continue;  // a tile of empty slots (row -1)
     double af[KS];
 #pragma unroll
     for (int j = 0; j < KS; ++j) {

@@ -652,6 +652,24 @@ __global__ void __launch_bounds__(256) qp_resvec_kernel(const double* __restrict
         for (int h = 0; h < 4; ++h) v[u][h] = make_double2(0.0, 0.0);
       }
     }
+    // a warp whose slots are all empty (the pool holds fewer rows than its
+    // capacity) or excluded only marks them
+    {
+      bool any = false;
+#pragma unroll
+      for (int u = 0; u < U; ++u) any |= live[u];
+      if (!__any_sync(0xffffffffu, any)) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t p = g * per_iter + u * RPW + seg;
+          if (p < P && sl == 0) {
+            pres2[p] = -1.0;
+            pn2[p] = 0.0;
+          }
+        }
+        continue;
+      }
+    }
     double nrm[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
